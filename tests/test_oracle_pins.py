@@ -1,0 +1,251 @@
+"""Pins for the CPU oracle (``-m "not gpu"``): each test checks the oracle against
+something other than itself — closed forms, finite differences, invariants, an
+independent library routine (torch float64 cross_entropy + autograd), a
+hand-derived golden example.  SURVEY.md §8(c) pins p1-p9; DESIGN.md §Pins.
+"""
+import json
+import math
+import os
+
+import numpy as np
+import pytest
+
+import oracle
+from oracle import lce
+import synth
+
+GOLD = os.path.join(os.path.dirname(__file__), "golden")
+
+
+def _rand(N, H, V, seed=0, std=1.0, n_ign=2, ignore_index=-100):
+    rng = np.random.default_rng(seed)
+    X = rng.standard_normal((N, H))
+    W = rng.standard_normal((V, H)) * std / math.sqrt(H)
+    t = rng.integers(0, V, N)
+    if n_ign:
+        t[rng.permutation(N)[:n_ign]] = ignore_index
+    return X, W, t
+
+
+# ---- golden closed form (hand-derived 2-token, 3-word example) -----------------------------
+@pytest.mark.parametrize("red", ["sum", "mean"])
+def test_golden_closed_form(red):
+    g = json.load(open(os.path.join(GOLD, "closed_form_2x3.json")))
+    out = lce(np.array(g["X"]), np.array(g["W"]), np.array(g["t"]), reduction=red)
+    c = g["cases"][red]
+    assert out["loss"] == pytest.approx(c["loss"], rel=1e-14)
+    np.testing.assert_allclose(out["dX"], c["dX"], rtol=1e-13, atol=1e-15)
+    np.testing.assert_allclose(out["dW"], c["dW"], rtol=1e-13, atol=1e-15)
+    np.testing.assert_allclose(out["lse"], g["lse"], rtol=1e-14)
+    none = lce(np.array(g["X"]), np.array(g["W"]), np.array(g["t"]), reduction="none")
+    np.testing.assert_allclose(none["loss"], g["loss_rows"], rtol=1e-14)
+
+
+# ---- p1: central finite differences ---------------------------------------------------------
+@pytest.mark.parametrize("red", ["sum", "mean", "none"])
+def test_finite_differences(red):
+    N, H, V = 16, 8, 32
+    X, W, t = _rand(N, H, V, seed=1, std=2.0)
+    scale = 0.75
+    out = lce(X, W, t, reduction=red, scale=scale)
+
+    def f(Xp, Wp):
+        o = lce(Xp, Wp, t, reduction=red, scale=1.0, need_grads=False)
+        return scale * (np.sum(o["loss"]) if red == "none" else o["loss"])
+
+    eps = 1e-6
+    rng = np.random.default_rng(7)
+    for _ in range(12):
+        i, h = rng.integers(N), rng.integers(H)
+        Xp, Xm = X.copy(), X.copy()
+        Xp[i, h] += eps
+        Xm[i, h] -= eps
+        fd = (f(Xp, W) - f(Xm, W)) / (2 * eps)
+        assert fd == pytest.approx(out["dX"][i, h], abs=1e-8)
+        v = rng.integers(V)
+        Wp, Wm = W.copy(), W.copy()
+        Wp[v, h] += eps
+        Wm[v, h] -= eps
+        fd = (f(X, Wp) - f(X, Wm)) / (2 * eps)
+        assert fd == pytest.approx(out["dW"][v, h], abs=1e-8)
+
+
+# ---- p2: W = 0 closed form ------------------------------------------------------------------
+@pytest.mark.parametrize("red", ["sum", "mean"])
+def test_w_zero_closed_form(red):
+    lnv = json.load(open(os.path.join(GOLD, "w_zero_lnV.json")))["lnV"]
+    N, H, V = 40, 16, 4096
+    X, _, t = _rand(N, H, V, seed=2, n_ign=5)
+    W = np.zeros((V, H))
+    out = lce(X, W, t, reduction=red, scale=1.5)
+    valid = t != -100
+    nv = valid.sum()
+    exp_loss = lnv["4096"] * (nv if red == "sum" else 1.0)
+    assert out["loss"] == pytest.approx(exp_loss, rel=1e-13)
+    assert np.all(out["dX"] == 0.0)
+    coef = 1.5 * (1.0 if red == "sum" else 1.0 / nv)
+    xs = X[valid].sum(axis=0)
+    dW = np.tile(coef * xs / V, (V, 1))
+    for i in np.nonzero(valid)[0]:
+        dW[t[i]] -= coef * X[i]
+    np.testing.assert_allclose(out["dW"], dW, atol=1e-13)
+
+
+# ---- p3: zero row sums via a constant column ------------------------------------------------
+def test_constant_column_probe():
+    N, H, V = 24, 7, 50
+    X, W, t = _rand(N, H, V, seed=3, std=3.0)
+    c = 0.37
+    X2 = np.concatenate([X, np.ones((N, 1))], axis=1)
+    W2 = np.concatenate([W, np.full((V, 1), c)], axis=1)
+    a = lce(X, W, t, reduction="sum")
+    b = lce(X2, W2, t, reduction="sum")
+    assert b["loss"] == pytest.approx(a["loss"], rel=1e-13)
+    np.testing.assert_allclose(b["dX"][:, :H], a["dX"], atol=1e-13)
+    assert np.max(np.abs(b["dX"][:, H])) < 1e-14 * max(1.0, np.max(np.abs(a["dX"])))
+    assert np.max(np.abs(a["dW"].sum(axis=0))) < 1e-13
+
+
+# ---- p4: identical rows and V = 1 -----------------------------------------------------------
+def test_identical_rows_and_v1():
+    N, H, V = 10, 6, 33
+    X, W, t = _rand(N, H, V, seed=4, n_ign=0)
+    Wi = np.tile(W[:1], (V, 1))
+    out = lce(X, Wi, t, reduction="mean")
+    assert out["loss"] == pytest.approx(math.log(V), rel=1e-13)
+    assert np.max(np.abs(out["dX"])) < 1e-15
+    out1 = lce(X, W[:1], np.zeros(N, dtype=np.int64), reduction="sum")
+    assert out1["loss"] == 0.0
+    assert np.all(out1["dX"] == 0.0) and np.all(out1["dW"] == 0.0)
+
+
+# ---- p5: ignore masking ---------------------------------------------------------------------
+@pytest.mark.parametrize("ignore_index", [-100, 0])
+def test_ignore_masking(ignore_index):
+    N, H, V = 30, 8, 40
+    X, W, t = _rand(N, H, V, seed=5, n_ign=6, ignore_index=ignore_index)
+    ign = t == ignore_index
+    a = lce(X, W, t, ignore_index=ignore_index, reduction="mean")
+    assert a["n_valid"] == int((~ign).sum())
+    assert np.all(a["dX"][ign] == 0.0)
+    X2 = X.copy()
+    X2[ign] = np.random.default_rng(9).standard_normal((ign.sum(), H)) * 5
+    b = lce(X2, W, t, ignore_index=ignore_index, reduction="mean")
+    assert a["loss"] == b["loss"]
+    np.testing.assert_array_equal(a["dX"][~ign], b["dX"][~ign])
+    np.testing.assert_allclose(a["dW"], b["dW"], rtol=0, atol=1e-15)
+    none = lce(X, W, t, ignore_index=ignore_index, reduction="none")
+    assert np.all(none["loss"][ign] == 0.0)
+
+
+# ---- p6: scale linearity --------------------------------------------------------------------
+def test_scale_linearity():
+    X, W, t = _rand(12, 8, 20, seed=6)
+    a = lce(X, W, t, reduction="mean", scale=1.0)
+    b = lce(X, W, t, reduction="mean", scale=2.0)
+    assert a["loss"] == b["loss"]
+    np.testing.assert_array_equal(2 * a["dX"], b["dX"])
+    np.testing.assert_array_equal(2 * a["dW"], b["dW"])
+
+
+# ---- p7: SUM vs MEAN ------------------------------------------------------------------------
+def test_sum_vs_mean():
+    X, W, t = _rand(20, 8, 30, seed=7, n_ign=3)
+    s = lce(X, W, t, reduction="sum")
+    m = lce(X, W, t, reduction="mean")
+    nv = s["n_valid"]
+    assert s["loss"] == pytest.approx(nv * m["loss"], rel=1e-13)
+    np.testing.assert_allclose(s["dX"], nv * m["dX"], rtol=1e-12, atol=1e-15)
+    np.testing.assert_allclose(s["dW"], nv * m["dW"], rtol=1e-12, atol=1e-15)
+
+
+# ---- p8: independent library routine (torch float64 cross_entropy + autograd) --------------
+@pytest.mark.parametrize("red", ["sum", "mean", "none"])
+@pytest.mark.parametrize("ignore_index", [-100, 0])
+def test_torch_crosscheck(red, ignore_index):
+    torch = pytest.importorskip("torch")
+    N, H, V = 64, 32, 300
+    X, W, t = _rand(N, H, V, seed=8, std=4.0, n_ign=7, ignore_index=ignore_index)
+    out = lce(X, W, t, ignore_index=ignore_index, reduction=red, scale=1.0)
+    Xt = torch.tensor(X, dtype=torch.float64, requires_grad=True)
+    Wt = torch.tensor(W, dtype=torch.float64, requires_grad=True)
+    L = torch.nn.functional.cross_entropy(Xt @ Wt.T, torch.tensor(t), ignore_index=ignore_index, reduction=red)
+    (L.sum() if red == "none" else L).backward()
+    np.testing.assert_allclose(np.asarray(out["loss"]), L.detach().numpy(), rtol=1e-12, atol=1e-13)
+    np.testing.assert_allclose(out["dX"], Xt.grad.numpy(), rtol=1e-10, atol=1e-14)
+    np.testing.assert_allclose(out["dW"], Wt.grad.numpy(), rtol=1e-10, atol=1e-14)
+
+
+# ---- R2 / R4 readings -----------------------------------------------------------------------
+def test_mean_all_ignored_is_zero():
+    X, W, _ = _rand(8, 4, 10, seed=9, n_ign=0)
+    t = np.full(8, -100)
+    out = lce(X, W, t, reduction="mean")
+    assert out["loss"] == 0.0 and np.all(out["dX"] == 0) and np.all(out["dW"] == 0)
+    assert out["n_valid"] == 0
+
+
+def test_bad_target_is_nan():
+    X, W, t = _rand(8, 4, 10, seed=10, n_ign=0)
+    t[3] = 10
+    out = lce(X, W, t, reduction="sum")
+    assert math.isnan(out["loss"]) and out["bad_targets"] == 1
+
+
+# ---- p9: shard combination ------------------------------------------------------------------
+@pytest.mark.parametrize("g", [2, 3, 8])
+def test_shard_combination(g):
+    N, H, V = 33, 8, 203
+    X, W, t = _rand(N, H, V, seed=11, std=3.0, n_ign=4)
+    full = lce(X, W, t, reduction="sum")
+    bounds = np.linspace(0, V, g + 1).astype(int)
+    stats = [oracle.shard_stats(X, W[a:b], t, a) for a, b in zip(bounds[:-1], bounds[1:])]
+    lse, z_t = oracle.combine_shards(stats)
+    np.testing.assert_allclose(lse, full["lse"], rtol=1e-14)
+    valid = t != -100
+    assert np.sum(np.where(valid, lse - z_t, 0.0)) == pytest.approx(full["loss"], rel=1e-13)
+
+
+# ---- row-slice helper equals the full problem ----------------------------------------------
+def test_rows_helper_matches_full():
+    X, W, t = _rand(50, 8, 64, seed=12, n_ign=5)
+    full = lce(X, W, t, reduction="mean", scale=0.5, block_rows=7)
+    valid, nv, coef = oracle.coef_for(t, -100, "mean", 0.5)
+    sl = slice(10, 23)
+    l, lse, dX, _ = oracle.rows(X[sl], W, t[sl], coef[sl])
+    np.testing.assert_allclose(dX, full["dX"][sl], rtol=1e-13, atol=1e-16)
+    np.testing.assert_allclose(lse, full["lse"][sl], rtol=1e-14)
+
+
+# ---- SPEC memory model cross-check ------------------------------------------
+def test_spec_memory_model_example():
+    full, chunked, red = oracle.lce_output_memory(8, 1024, 128256, 1024)
+    assert full / 1e9 == pytest.approx(4.2025, rel=1e-3)
+    assert chunked / 1e9 == pytest.approx(0.5253, rel=1e-3)
+    assert red == pytest.approx(0.875)
+
+
+# ---- synthetic inputs -----------------------------------------------------------------------
+def test_synth_bf16_rounding_matches_torch():
+    torch = pytest.importorskip("torch")
+    a = np.random.default_rng(0).standard_normal(100000).astype(np.float32) * 3
+    a[:4] = [1.00390625, 1.01171875, -1.00390625, 0.0]  # exact ties
+    ours = synth.f32_to_bf16_bits(a)
+    ref = torch.from_numpy(a).to(torch.bfloat16).view(torch.int16).numpy().view(np.uint16)
+    np.testing.assert_array_equal(ours, ref)
+
+
+def test_synth_recipe():
+    a = synth.make_inputs(1000, 64, 5000, seed=3, alpha=4.0, dist="zipf")
+    b = synth.make_inputs(1000, 64, 5000, seed=3, alpha=4.0, dist="zipf")
+    np.testing.assert_array_equal(a.X, b.X)
+    np.testing.assert_array_equal(a.W, b.W)
+    np.testing.assert_array_equal(a.t, b.t)
+    assert int((a.t == -100).sum()) == 50
+    v = a.t[a.t != -100]
+    assert v.min() >= 0 and v.max() < 5000
+    assert np.bincount(v).max() > 20  # Zipf is skewed
+    W = synth.bf16_bits_to_f64(a.W)
+    assert np.std(W) * math.sqrt(64) == pytest.approx(4.0, rel=0.05)
+    tiny = synth.make_config("tiny")
+    assert int((tiny.t == -100).sum()) == 13
