@@ -1,0 +1,178 @@
+/*
+ * slf_lce.h — C ABI of libslf_lce.so: the fused linear-cross-entropy (LCE) hot
+ * path on B200 (sm_100a).
+ *
+ * The operation (§3.3 "Optimized Triton Kernels"): the fused
+ * LinearCrossEntropy kernel "fuses the projection and loss calculation,
+ * computing gradients in small chunks to avoid materializing the full logits
+ * tensor", "without sacrificing accuracy" against the "torch standard method"
+ * (Fig. fig:lce caption).  With
+ *
+ *   X = hidden [N, H] bf16 row-major, W = LM-head weight [V, H] bf16 row-major,
+ *   t = targets [N] int32, Z = X W^T (never stored),
+ *   lse_i = log sum_v exp Z_iv, valid_i = (t_i != ignore_index),
+ *   l_i = valid_i ? lse_i - Z_{i,t_i} : 0,
+ *   coef_i = scale * valid_i * (1/n_valid if MEAN else 1),
+ *   G = coef (softmax(Z) - onehot(t)),
+ *
+ * the library returns loss (fp32; sum, mean or per-row), dhidden = G W and
+ * dweight = G^T X (bf16), with device memory for intermediates bounded by the
+ * caller-provided workspace (no N x V buffer exists).  Readings of the paper
+ * (ignore_index equality, MEAN with n_valid = 0 -> 0, `scale` scales gradients
+ * only, out-of-range targets are a data error) are DESIGN.md R1-R9.
+ *
+ * Conventions for every entry point
+ *  - All pointers except `loss_out` / host outputs documented as host are
+ *    DEVICE pointers to caller-owned memory (allocated e.g. by torch).  The
+ *    library never allocates device memory; its only device scratch is
+ *    `workspace`.  Device pointers must be 16-byte aligned (SLF_ERR_ALIGN).
+ *  - Calls enqueue work on `stream` (a cudaStream_t; NULL = legacy default
+ *    stream) and return without synchronising.  Argument and launch errors are
+ *    synchronous return codes; the message is in slf_last_error_string().
+ *    Data errors (a valid target outside [0, V_global)) are asynchronous: the
+ *    loss becomes NaN and slf_lce_status() reports the count.
+ *  - No global mutable state except a thread-local last-error string and a
+ *    per-device attribute cache; calls on different streams are independent
+ *    provided they use different workspaces.
+ *  - Requirements: H % 8 == 0 (16-byte TMA row strides), N >= 1, V_local >= 1,
+ *    an sm_100 device (SLF_ERR_UNSUPPORTED otherwise).
+ */
+#ifndef SLF_LCE_H_
+#define SLF_LCE_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef int slf_status;
+#define SLF_OK 0
+#define SLF_ERR_ARG 1           /* null required pointer, bad size or enum */
+#define SLF_ERR_ALIGN 2         /* a device pointer is not 16-byte aligned */
+#define SLF_ERR_WORKSPACE 3     /* workspace_bytes smaller than required   */
+#define SLF_ERR_CUDA 4          /* CUDA launch / driver error              */
+#define SLF_ERR_UNSUPPORTED 5   /* not an sm_100 device                    */
+#define SLF_ERR_UNIMPLEMENTED 6 /* requested schedule not built yet        */
+
+typedef enum { SLF_SUM = 0, SLF_MEAN = 1, SLF_NONE = 2 } slf_reduction;
+
+/* Schedules.  R: forward statistics pass over all
+ * vocabulary tiles, then recompute the logits tile by tile in backward
+ * (8·N·H·V tensor FLOPs, exact fp32 dhidden accumulation). */
+typedef enum { SLF_SCHED_AUTO = 0, SLF_SCHED_R = 1 } slf_schedule;
+
+/* Per-row statistics record ("RowStat", 16 bytes) exchanged between the
+ * forward and backward halves: lse2 = lse * log2(e); coef as above;
+ * tloc = t - vocab_start if the target lies in this vocab shard else -1;
+ * valid = 1 if t != ignore_index. */
+typedef struct {
+  float lse2;
+  float coef;
+  int32_t tloc;
+  int32_t valid;
+} slf_rowstat;
+
+/* Per-row shard statistics ("ShardStat", 16 bytes) for vocab-parallel use:
+ * m = max_v Z_iv and s = sum_v exp(Z_iv - m) over this shard's columns,
+ * zt = Z_{i,t_i} if t_i is in this shard else 0, hit = 1.0f if it is. */
+typedef struct {
+  float m;
+  float s;
+  float zt;
+  float hit;
+} slf_shardstat;
+
+/* Library version (major*10000 + minor*100 + patch). */
+int slf_lce_version(void);
+
+/* Message for the last error on this thread ("" if none).  Host string owned
+ * by the library, valid until the next call on this thread. */
+const char* slf_last_error_string(void);
+
+/* Workspace bytes the planner needs for a problem of this shape when it must
+ * stay within `budget_bytes` (0 = default budget: max(5% of N*V_local*2, 16 MiB),
+ * the BASELINE.json "extra memory <= 5% of the materialised-logits footprint"
+ * target).  Returns 0 if no plan fits the budget or the shape is invalid. */
+size_t slf_lce_workspace_bytes(int64_t N, int64_t H, int64_t V_local, int schedule, size_t budget_bytes);
+
+/* Writes a one-line description of the plan (schedule, row block, vocab chunk,
+ * launches) into the HOST buffer `out` of `cap` bytes.  Returns SLF_OK or
+ * SLF_ERR_ARG / SLF_ERR_WORKSPACE. */
+slf_status slf_lce_plan_describe(int64_t N, int64_t H, int64_t V_local, int schedule, size_t budget_bytes,
+                                 char* out, size_t cap);
+
+/* The whole hot path on one GPU (V_local = V_global, vocab_start = 0):
+ * forward statistics, loss, and both gradients.
+ *   hidden   [N, H] bf16, row-major (ld = H)               (read)
+ *   weight   [V, H] bf16, row-major (ld = H)               (read)
+ *   targets  [N] int32                                     (read)
+ *   loss_out DEVICE fp32: [1] for SUM/MEAN, [N] for NONE   (written)
+ *   dhidden  [N, H] bf16 (may be NULL to skip)             (overwritten)
+ *   dweight  [V, H] bf16 (may be NULL to skip)             (overwritten)
+ *   workspace, workspace_bytes: >= slf_lce_workspace_bytes(N,H,V,schedule,budget)
+ * Gradients are those of scale*loss (SUM/MEAN) or of scale*sum_i l_i (NONE).
+ * Rows with t_i == ignore_index get dhidden rows of exactly +0.0. */
+slf_status slf_lce_fwd_bwd(const void* hidden, const void* weight, const int32_t* targets, int64_t N, int64_t H,
+                           int64_t V, int32_t ignore_index, int reduction, float scale, float* loss_out,
+                           void* dhidden, void* dweight, void* workspace, size_t workspace_bytes, int schedule,
+                           size_t budget_bytes, void* stream);
+
+/* Forward half (schedule R split; also the vocab-shard seam).  Computes the
+ * loss and the RowStat array [N] (16 B/row, DEVICE, caller-owned) that
+ * slf_lce_bwd consumes.  `scale` enters coef only.  Single GPU form. */
+slf_status slf_lce_fwd(const void* hidden, const void* weight, const int32_t* targets, int64_t N, int64_t H,
+                       int64_t V, int32_t ignore_index, int reduction, float scale, float* loss_out,
+                       slf_rowstat* rowstat, void* workspace, size_t workspace_bytes, size_t budget_bytes,
+                       void* stream);
+
+/* Vocab-shard forward, part 1: this shard's per-row statistics.
+ *   weight_shard [V_local, H] bf16 = rows [vocab_start, vocab_start+V_local) of W
+ *   shardstat    [N] slf_shardstat (DEVICE, written)
+ * No loss is formed; gather the g shards' arrays (e.g. NCCL all-gather, rank
+ * order) and call slf_lce_stats_combine. */
+slf_status slf_lce_fwd_shard_stats(const void* hidden, const void* weight_shard, const int32_t* targets, int64_t N,
+                                   int64_t H, int64_t V_local, int64_t vocab_start, int32_t ignore_index,
+                                   slf_shardstat* shardstat, void* workspace, size_t workspace_bytes,
+                                   size_t budget_bytes, void* stream);
+
+/* Vocab-shard forward, part 2: merge g shards' statistics (`stats` is
+ * [g][N] slf_shardstat, DEVICE, shard order) into the loss and this shard's
+ * RowStat (tloc relative to vocab_start, V_local wide).  Targets are range
+ * checked against V_global.  Deterministic (fixed shard order). */
+slf_status slf_lce_stats_combine(const slf_shardstat* stats, int g, const int32_t* targets, int64_t N,
+                                 int64_t vocab_start, int64_t V_local, int64_t V_global, int32_t ignore_index,
+                                 int reduction, float scale, float* loss_out, slf_rowstat* rowstat,
+                                 void* workspace, size_t workspace_bytes, void* stream);
+
+/* Backward half: recompute the logits tile by tile, form
+ * G = grad_scale * coef * (softmax - onehot) in fp32, round to bf16, and feed
+ * it to the dweight and dhidden GEMMs.
+ *   rowstat  [N] from slf_lce_fwd / slf_lce_stats_combine (read)
+ *   dhidden  [N, H]: bf16 if dhidden_fp32 == 0, else fp32 (the shard partial
+ *            to be summed across shards)               (overwritten; may be NULL)
+ *   dweight  [V_local, H] bf16                          (overwritten; may be NULL)
+ * grad_scale multiplies coef (the autograd grad_output). */
+slf_status slf_lce_bwd(const void* hidden, const void* weight, const int32_t* targets, const slf_rowstat* rowstat,
+                       int64_t N, int64_t H, int64_t V_local, float grad_scale, void* dhidden, int dhidden_fp32,
+                       void* dweight, void* workspace, size_t workspace_bytes, size_t budget_bytes,
+                       void* stream);
+
+/* Synchronises `stream` and returns (in *bad_targets, HOST) the number of
+ * valid targets outside [0, V_global) seen by the last call that used this
+ * workspace, and (in *n_valid, HOST, may be NULL) the number of valid rows. */
+slf_status slf_lce_status(const void* workspace, void* stream, int32_t* bad_targets, int64_t* n_valid);
+
+/* Test entry point: a plain bf16 GEMM D[M,N] (fp32, row-major, ld = N) =
+ * A * B through the same tcgen05 core, with A [M,K] (a_mn = 0: K contiguous)
+ * or stored as [K,M] (a_mn = 1), B stored [N,K] (b_mn = 0) or [K,N] (b_mn = 1).
+ * Used by the GPU tests to check the core against torch.matmul. */
+slf_status slf_debug_gemm(const void* A, const void* B, float* D, int64_t M, int64_t N, int64_t K, int a_mn,
+                          int b_mn, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* SLF_LCE_H_ */

@@ -1,0 +1,9 @@
+"""B200-native fused linear-cross-entropy (SlideFormer §3.3 LCE kernel, arXiv 2603.16428).
+
+Hot path: libslf_lce.so (hand-written sm_100a CUDA: TMA + tcgen05/TMEM GEMM tiles with fused
+LCE epilogues) behind the C ABI in include/slf_lce.h; this package is the thin Python binding.
+"""
+from .lce import (  # noqa: F401
+    LCEFunction, alloc_workspace, debug_gemm, lce_bwd, lce_fwd, lce_fwd_bwd, plan_describe, shard_stats,
+    stats_combine, status, workspace_bytes,
+)

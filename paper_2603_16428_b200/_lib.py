@@ -1,0 +1,79 @@
+"""ctypes binding to libslf_lce.so (include/slf_lce.h).  Argument marshalling only.
+
+The library is REQUIRED: if it is missing or fails to load, every call raises — there is no
+CPU or PyTorch fallback on the product path.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import threading
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+SO_PATH = os.path.join(HERE, "libslf_lce.so")
+
+SLF_OK = 0
+STATUS_NAMES = {0: "SLF_OK", 1: "SLF_ERR_ARG", 2: "SLF_ERR_ALIGN", 3: "SLF_ERR_WORKSPACE", 4: "SLF_ERR_CUDA",
+                5: "SLF_ERR_UNSUPPORTED", 6: "SLF_ERR_UNIMPLEMENTED"}
+REDUCTIONS = {"sum": 0, "mean": 1, "none": 2}
+SCHEDULES = {"auto": 0, "R": 1}
+
+# Every symbol include/slf_lce.h declares.
+EXPORTS = ["slf_lce_version", "slf_last_error_string", "slf_lce_workspace_bytes", "slf_lce_plan_describe",
+           "slf_lce_fwd_bwd", "slf_lce_fwd", "slf_lce_fwd_shard_stats", "slf_lce_stats_combine", "slf_lce_bwd",
+           "slf_lce_status", "slf_debug_gemm"]
+
+_lock = threading.Lock()
+_lib = None
+
+P = ctypes.c_void_p
+I64 = ctypes.c_int64
+I32 = ctypes.c_int32
+INT = ctypes.c_int
+F32 = ctypes.c_float
+SZ = ctypes.c_size_t
+
+
+class SlfError(RuntimeError):
+    pass
+
+
+def _declare(lib):
+    sig = {
+        "slf_lce_version": (INT, []),
+        "slf_last_error_string": (ctypes.c_char_p, []),
+        "slf_lce_workspace_bytes": (SZ, [I64, I64, I64, INT, SZ]),
+        "slf_lce_plan_describe": (INT, [I64, I64, I64, INT, SZ, ctypes.c_char_p, SZ]),
+        "slf_lce_fwd_bwd": (INT, [P, P, P, I64, I64, I64, I32, INT, F32, P, P, P, P, SZ, INT, SZ, P]),
+        "slf_lce_fwd": (INT, [P, P, P, I64, I64, I64, I32, INT, F32, P, P, P, SZ, SZ, P]),
+        "slf_lce_fwd_shard_stats": (INT, [P, P, P, I64, I64, I64, I64, I32, P, P, SZ, SZ, P]),
+        "slf_lce_stats_combine": (INT, [P, INT, P, I64, I64, I64, I64, I32, INT, F32, P, P, P, SZ, P]),
+        "slf_lce_bwd": (INT, [P, P, P, P, I64, I64, I64, F32, P, INT, P, P, SZ, SZ, P]),
+        "slf_lce_status": (INT, [P, P, ctypes.POINTER(I32), ctypes.POINTER(I64)]),
+        "slf_debug_gemm": (INT, [P, P, P, I64, I64, I64, INT, INT, P]),
+    }
+    for name, (res, args) in sig.items():
+        f = getattr(lib, name)
+        f.restype = res
+        f.argtypes = args
+
+
+def lib():
+    """Load libslf_lce.so (built in-tree by paper_2603_16428_b200.build / __graft_entry__.build)."""
+    global _lib
+    if _lib is None:
+        with _lock:
+            if _lib is None:
+                if not os.path.exists(SO_PATH):
+                    raise SlfError(f"{SO_PATH} is missing: run `python -m paper_2603_16428_b200.build` "
+                                   "(there is no fallback path)")
+                l = ctypes.CDLL(SO_PATH)
+                _declare(l)
+                _lib = l
+    return _lib
+
+
+def check(status: int, what: str):
+    if status != SLF_OK:
+        msg = lib().slf_last_error_string().decode(errors="replace")
+        raise SlfError(f"{what} failed with {STATUS_NAMES.get(status, status)}: {msg}")

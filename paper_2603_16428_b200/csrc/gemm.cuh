@@ -1,0 +1,355 @@
+// gemm.cuh — persistent, warp-specialised TMA -> tcgen05 -> TMEM GEMM core for sm_100a with the
+// LCE epilogues fused into the tile.
+//
+//   D[M, N] = A[M, K] * B[K, N]   (bf16 in, fp32 accumulate in TMEM)
+//   A is K-major (stored [M][K]) or MN-major (stored [K][M]); B is K-major (stored [N][K]) or
+//   MN-major (stored [K][N]).  One CTA per SM, 128 x 256 output tile, K-step 64 (one 128-byte
+//   swizzle row), 4-stage smem ring fed by TMA, two 256-column TMEM accumulators so the epilogue
+//   of tile i overlaps the mainloop of tile i+1.
+//   warp 0: TMA producer (one lane) | warp 1: tcgen05.mma issuer (one lane) | warp 2: TMEM
+//   allocator | warps 4-7: epilogue, thread = accumulator row (TMEM lane).
+//
+// Epilogues ("fuses the projection and loss calculation, computing gradients in
+// small chunks"):
+//   EPI_STATS : per (row, 256-column vocab tile) max m and sum exp(z - m); gathers the target logit.
+//   EPI_GRAD  : G = coef * (exp(z - lse) - [v == t]) in fp32, rounded to bf16, stored to the chunk.
+//   EPI_DW    : dW tile (bf16), store or fp32 read-add-write of the previous row block's partial.
+//   EPI_DX    : dX tile: fp32 store / accumulate across vocab chunks, final bf16 conversion with
+//               ignored rows forced to +0.
+//   EPI_F32   : plain fp32 store (test entry point).
+#pragma once
+#include <cuda.h>
+#include <cstdint>
+
+#include "ptx.cuh"
+#include "../../include/slf_lce.h"
+
+namespace slf {
+
+constexpr int BM = 128;
+constexpr int BN = 256;
+constexpr int BK = 64;
+constexpr int STAGES = 4;
+constexpr int A_STAGE_BYTES = BM * BK * 2;  // 16 KiB
+constexpr int B_STAGE_BYTES = BN * BK * 2;  // 32 KiB
+constexpr int STAGE_BYTES = A_STAGE_BYTES + B_STAGE_BYTES;
+constexpr int GEMM_THREADS = 256;
+constexpr uint32_t TMEM_COLS = 512;  // 2 x 256-column fp32 accumulators
+constexpr int GEMM_SMEM_BYTES = STAGES * STAGE_BYTES + 1024 /*align slack*/ + 256 /*barriers*/;
+
+enum EpiKind { EPI_STATS = 0, EPI_GRAD = 1, EPI_DW = 2, EPI_DX = 3, EPI_F32 = 4 };
+
+// DX epilogue modes.
+enum DxMode { DX_STORE_F32 = 0, DX_ACC_F32 = 1, DX_ACC_FINAL_BF16 = 2, DX_STORE_FINAL_BF16 = 3 };
+
+struct GemmArgs {
+  int M, N, K;
+  int tiles_m, tiles_n, num_tiles, group_m;
+  // EPI_STATS
+  const int32_t* targets;  // row 0 of the GEMM
+  int64_t tcol0;           // target id that maps to GEMM column 0 (vocab_start + chunk start)
+  int32_t ignore_index;
+  float2* partials;        // [tiles_n][M]
+  float* zt;               // [M]
+  // EPI_GRAD / EPI_DX
+  const slf_rowstat* rowstat;  // row 0 of the GEMM (GRAD, DX)
+  int64_t col0;                // chunk start relative to the shard (GRAD: compare with rowstat.tloc)
+  float grad_scale;
+  // outputs
+  void* out;
+  int64_t ld_out;
+  int mode;
+  void* out2;  // DX final bf16 destination (row 0 of the GEMM)
+  int64_t ld_out2;
+};
+
+__device__ __forceinline__ void tile_coords(int tile, const GemmArgs& a, int& m_blk, int& n_blk) {
+  // Grouped raster: walk group_m row tiles down before stepping to the next column tile, so one
+  // wave of 148 tiles shares a few A row-panels and B column-panels in L2.
+  const int per_group = a.group_m * a.tiles_n;
+  const int g = tile / per_group;
+  const int first_m = g * a.group_m;
+  const int gm = min(a.group_m, a.tiles_m - first_m);
+  const int in = tile - g * per_group;
+  m_blk = first_m + in % gm;
+  n_blk = in / gm;
+}
+
+template <int EPI>
+__device__ __forceinline__ void epilogue_tile(const GemmArgs& a, uint32_t taddr, int m_blk, int n_blk, int row_in_tile) {
+  const int r = m_blk * BM + row_in_tile;
+  const bool row_ok = r < a.M;
+  const int n0 = n_blk * BN;
+  const int ncols = min(BN, a.N - n0);
+  uint32_t v[32];
+
+  if constexpr (EPI == EPI_STATS) {
+    int tl = -1;
+    if (row_ok) {
+      const int32_t t = a.targets[r];
+      const int64_t loc = (int64_t)t - a.tcol0 - n0;
+      tl = (t != a.ignore_index && loc >= 0 && loc < ncols) ? (int)loc : -1;
+    }
+    float mx = -INFINITY;
+#pragma unroll 1
+    for (int c = 0; c < BN / 32; ++c) {
+      if (c * 32 >= ncols) break;  // warp-uniform
+      tmem_ld32(taddr + c * 32, v);
+      tmem_ld_wait();
+#pragma unroll
+      for (int i = 0; i < 32; ++i)
+        if (c * 32 + i < ncols) mx = fmaxf(mx, __uint_as_float(v[i]));
+    }
+    const float mb = mx * LOG2E;
+    float s = 0.f, zt = 0.f;
+#pragma unroll 1
+    for (int c = 0; c < BN / 32; ++c) {
+      if (c * 32 >= ncols) break;
+      tmem_ld32(taddr + c * 32, v);
+      tmem_ld_wait();
+#pragma unroll
+      for (int i = 0; i < 32; ++i) {
+        const float z = __uint_as_float(v[i]);
+        const float e = ex2(fmaf(z, LOG2E, -mb));
+        s += (c * 32 + i < ncols) ? e : 0.f;
+        zt = (c * 32 + i == tl) ? z : zt;
+      }
+    }
+    if (row_ok) {
+      a.partials[(size_t)n_blk * a.M + r] = make_float2(mx, s);
+      if (tl >= 0) a.zt[r] = zt;
+    }
+  } else if constexpr (EPI == EPI_GRAD) {
+    float coef = 0.f, lse2 = 0.f;
+    int tl = -1;
+    if (row_ok) {
+      const slf_rowstat rs = a.rowstat[r];
+      coef = rs.coef * a.grad_scale;
+      lse2 = rs.lse2;
+      const int64_t loc = (int64_t)rs.tloc - a.col0 - n0;
+      tl = (rs.tloc >= 0 && loc >= 0 && loc < ncols) ? (int)loc : -1;
+    }
+    uint16_t* out = reinterpret_cast<uint16_t*>(a.out) + (size_t)r * a.ld_out + n0;
+#pragma unroll 1
+    for (int c = 0; c < BN / 32; ++c) {
+      if (c * 32 >= ncols) break;
+      tmem_ld32(taddr + c * 32, v);
+      tmem_ld_wait();
+      uint32_t p[16];
+#pragma unroll
+      for (int i = 0; i < 32; i += 2) {
+        const int j0 = c * 32 + i, j1 = j0 + 1;
+        float g0 = coef * ex2(fmaf(__uint_as_float(v[i]), LOG2E, -lse2)) - (j0 == tl ? coef : 0.f);
+        float g1 = coef * ex2(fmaf(__uint_as_float(v[i + 1]), LOG2E, -lse2)) - (j1 == tl ? coef : 0.f);
+        g0 = j0 < ncols ? g0 : 0.f;
+        g1 = j1 < ncols ? g1 : 0.f;
+        p[i / 2] = pack_bf16x2(g0, g1);
+      }
+      if (row_ok) {
+        uint4* dst = reinterpret_cast<uint4*>(out + c * 32);
+#pragma unroll
+        for (int q = 0; q < 4; ++q) dst[q] = make_uint4(p[4 * q], p[4 * q + 1], p[4 * q + 2], p[4 * q + 3]);
+      }
+    }
+  } else if constexpr (EPI == EPI_DW) {
+    uint16_t* out = reinterpret_cast<uint16_t*>(a.out) + (size_t)r * a.ld_out + n0;
+#pragma unroll 1
+    for (int c = 0; c < BN / 32; ++c) {
+      if (c * 32 >= ncols) break;
+      tmem_ld32(taddr + c * 32, v);
+      tmem_ld_wait();
+      if (row_ok) {
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const int j = c * 32 + q * 8;
+          if (j < ncols) {  // ncols % 8 == 0 (H % 8 == 0)
+            uint4* dst = reinterpret_cast<uint4*>(out + j);
+            float f[8];
+#pragma unroll
+            for (int e = 0; e < 8; ++e) f[e] = __uint_as_float(v[q * 8 + e]);
+            if (a.mode == 1) {
+              const uint4 old = *dst;
+              f[0] += bf16lo_to_f32(old.x); f[1] += bf16hi_to_f32(old.x);
+              f[2] += bf16lo_to_f32(old.y); f[3] += bf16hi_to_f32(old.y);
+              f[4] += bf16lo_to_f32(old.z); f[5] += bf16hi_to_f32(old.z);
+              f[6] += bf16lo_to_f32(old.w); f[7] += bf16hi_to_f32(old.w);
+            }
+            *dst = make_uint4(pack_bf16x2(f[0], f[1]), pack_bf16x2(f[2], f[3]), pack_bf16x2(f[4], f[5]),
+                              pack_bf16x2(f[6], f[7]));
+          }
+        }
+      }
+    }
+  } else if constexpr (EPI == EPI_DX) {
+    const bool valid = row_ok && a.rowstat[r].valid != 0;
+    float* acc = reinterpret_cast<float*>(a.out) + (size_t)r * a.ld_out + n0;
+    uint16_t* fin = reinterpret_cast<uint16_t*>(a.out2) + (size_t)r * a.ld_out2 + n0;
+#pragma unroll 1
+    for (int c = 0; c < BN / 32; ++c) {
+      if (c * 32 >= ncols) break;
+      tmem_ld32(taddr + c * 32, v);
+      tmem_ld_wait();
+      if (row_ok) {
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const int j = c * 32 + q * 8;
+          if (j < ncols) {
+            float f[8];
+#pragma unroll
+            for (int e = 0; e < 8; ++e) f[e] = valid ? __uint_as_float(v[q * 8 + e]) : 0.f;
+            float4* d4 = reinterpret_cast<float4*>(acc + j);
+            if (a.mode == DX_ACC_F32 || a.mode == DX_ACC_FINAL_BF16) {
+              const float4 o0 = d4[0], o1 = d4[1];
+              f[0] += o0.x; f[1] += o0.y; f[2] += o0.z; f[3] += o0.w;
+              f[4] += o1.x; f[5] += o1.y; f[6] += o1.z; f[7] += o1.w;
+            }
+            if (a.mode == DX_STORE_F32 || a.mode == DX_ACC_F32) {
+              d4[0] = make_float4(f[0], f[1], f[2], f[3]);
+              d4[1] = make_float4(f[4], f[5], f[6], f[7]);
+            } else {
+              uint4 o = make_uint4(pack_bf16x2(f[0], f[1]), pack_bf16x2(f[2], f[3]), pack_bf16x2(f[4], f[5]),
+                                   pack_bf16x2(f[6], f[7]));
+              if (!valid) o = make_uint4(0u, 0u, 0u, 0u);  // +0.0 exactly for ignored rows
+              *reinterpret_cast<uint4*>(fin + j) = o;
+            }
+          }
+        }
+      }
+    }
+  } else {  // EPI_F32
+    float* out = reinterpret_cast<float*>(a.out) + (size_t)r * a.ld_out + n0;
+#pragma unroll 1
+    for (int c = 0; c < BN / 32; ++c) {
+      if (c * 32 >= ncols) break;
+      tmem_ld32(taddr + c * 32, v);
+      tmem_ld_wait();
+      if (row_ok) {
+#pragma unroll
+        for (int i = 0; i < 32; ++i)
+          if (c * 32 + i < ncols) out[c * 32 + i] = __uint_as_float(v[i]);
+      }
+    }
+  }
+}
+
+template <int EPI, bool A_MN, bool B_MN>
+__global__ void __launch_bounds__(GEMM_THREADS, 1)
+    lce_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                    const GemmArgs args) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sA = smem;
+  uint8_t* sB = smem + STAGES * A_STAGE_BYTES;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE_BYTES);
+  uint64_t* empty = full + STAGES;
+  uint64_t* tfull = empty + STAGES;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+
+  const uint32_t warp = warp_idx_sync();
+  const uint32_t lane = threadIdx.x & 31;
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch_desc(&tmA);
+    tma_prefetch_desc(&tmB);
+#pragma unroll
+    for (int i = 0; i < STAGES; ++i) {
+      mbar_init(&full[i], 1);
+      mbar_init(&empty[i], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&tfull[i], 1);
+      mbar_init(&tempty[i], 4);  // one arrive per epilogue warp
+    }
+    fence_barrier_init();
+  }
+  if (warp == 2) tmem_alloc<TMEM_COLS>(tmem_slot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+  const int num_kb = (args.K + BK - 1) / BK;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      // ===== TMA producer =====
+      const uint64_t pol = policy_evict_normal();
+      uint32_t stage = 0, phase = 0;
+      for (int tile = blockIdx.x; tile < args.num_tiles; tile += gridDim.x) {
+        int m_blk, n_blk;
+        tile_coords(tile, args, m_blk, n_blk);
+        for (int kb = 0; kb < num_kb; ++kb) {
+          mbar_wait(&empty[stage], phase ^ 1);
+          mbar_arrive_expect_tx(&full[stage], STAGE_BYTES);
+          uint8_t* a_dst = sA + stage * A_STAGE_BYTES;
+          uint8_t* b_dst = sB + stage * B_STAGE_BYTES;
+          if constexpr (!A_MN) {
+            tma_load_2d(&tmA, &full[stage], a_dst, kb * BK, m_blk * BM, pol);
+          } else {
+#pragma unroll
+            for (int j = 0; j < BM / 64; ++j)
+              tma_load_2d(&tmA, &full[stage], a_dst + j * 8192, m_blk * BM + j * 64, kb * BK, pol);
+          }
+          if constexpr (!B_MN) {
+            tma_load_2d(&tmB, &full[stage], b_dst, kb * BK, n_blk * BN, pol);
+          } else {
+#pragma unroll
+            for (int j = 0; j < BN / 64; ++j)
+              tma_load_2d(&tmB, &full[stage], b_dst + j * 8192, n_blk * BN + j * 64, kb * BK, pol);
+          }
+          if (++stage == STAGES) { stage = 0; phase ^= 1; }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      // ===== tcgen05.mma issuer =====
+      constexpr uint32_t idesc = make_idesc_bf16(BM, BN, A_MN, B_MN);
+      uint32_t stage = 0, phase = 0, local = 0;
+      for (int tile = blockIdx.x; tile < args.num_tiles; tile += gridDim.x, ++local) {
+        const uint32_t acc = local & 1, acc_phase = (local >> 1) & 1;
+        mbar_wait(&tempty[acc], acc_phase ^ 1);
+        tc_fence_after();
+        const uint32_t d_tmem = tmem_base + acc * BN;
+        for (int kb = 0; kb < num_kb; ++kb) {
+          mbar_wait(&full[stage], phase);
+          tc_fence_after();
+          const uint32_t a_base = smem_u32(sA + stage * A_STAGE_BYTES);
+          const uint32_t b_base = smem_u32(sB + stage * B_STAGE_BYTES);
+#pragma unroll
+          for (int k = 0; k < BK / 16; ++k) {
+            const uint64_t ad = A_MN ? make_sdesc(a_base + k * 2048, 8192, 1024) : make_sdesc(a_base + k * 32, 16, 1024);
+            const uint64_t bd = B_MN ? make_sdesc(b_base + k * 2048, 8192, 1024) : make_sdesc(b_base + k * 32, 16, 1024);
+            mma_bf16(d_tmem, ad, bd, idesc, (kb | k) != 0);
+          }
+          mma_commit(&empty[stage]);  // frees the smem slot once these MMAs have read it
+          if (++stage == STAGES) { stage = 0; phase ^= 1; }
+        }
+        mma_commit(&tfull[acc]);  // accumulator ready for the epilogue
+      }
+    }
+  } else if (warp >= 4) {
+    // ===== epilogue: thread = TMEM lane = output row =====
+    const uint32_t ew = warp - 4;
+    uint32_t local = 0;
+    for (int tile = blockIdx.x; tile < args.num_tiles; tile += gridDim.x, ++local) {
+      int m_blk, n_blk;
+      tile_coords(tile, args, m_blk, n_blk);
+      const uint32_t acc = local & 1, acc_phase = (local >> 1) & 1;
+      mbar_wait(&tfull[acc], acc_phase);
+      tc_fence_after();
+      const uint32_t taddr = tmem_base + ((ew * 32) << 16) + acc * BN;
+      epilogue_tile<EPI>(args, taddr, m_blk, n_blk, ew * 32 + lane);
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&tempty[acc]);
+    }
+  }
+  __syncthreads();
+  if (warp == 2) {
+    tc_fence_after();
+    tmem_dealloc<TMEM_COLS>(tmem_base);
+  }
+}
+
+}  // namespace slf

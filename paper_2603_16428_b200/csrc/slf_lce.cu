@@ -1,0 +1,505 @@
+// slf_lce.cu — host side of libslf_lce.so: argument checks, the schedule planner, TMA descriptor
+// construction and the launch sequence of the fused LCE hot path (include/slf_lce.h,
+// DESIGN.md §Boundary, §Schedules).  Device code lives in gemm.cuh and aux_kernels.cuh.
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <cudaTypedefs.h>
+
+#include <algorithm>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+
+#include "../../include/slf_lce.h"
+#include "aux_kernels.cuh"
+#include "gemm.cuh"
+
+using namespace slf;
+
+namespace {
+
+thread_local std::string g_err;
+
+slf_status fail(slf_status s, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  g_err = buf;
+  return s;
+}
+
+#define SLF_CUDA(x)                                                                                        \
+  do {                                                                                                     \
+    cudaError_t e_ = (x);                                                                                  \
+    if (e_ != cudaSuccess) return fail(SLF_ERR_CUDA, "%s: %s (%s:%d)", #x, cudaGetErrorString(e_), __FILE__, __LINE__); \
+  } while (0)
+#define SLF_TRY(x)                   \
+  do {                               \
+    slf_status s_ = (x);             \
+    if (s_ != SLF_OK) return s_;     \
+  } while (0)
+
+constexpr int kMaxDev = 64;
+
+struct DevInfo {
+  int sms = 0;
+  int major = 0;
+  int minor = 0;
+  bool gemm_attr_set[32] = {};
+};
+
+std::mutex g_mu;
+DevInfo g_dev[kMaxDev];
+
+slf_status device_info(DevInfo** out) {
+  int dev = 0;
+  SLF_CUDA(cudaGetDevice(&dev));
+  if (dev < 0 || dev >= kMaxDev) return fail(SLF_ERR_UNSUPPORTED, "device ordinal %d out of range", dev);
+  std::lock_guard<std::mutex> lk(g_mu);
+  DevInfo& d = g_dev[dev];
+  if (d.sms == 0) {
+    SLF_CUDA(cudaDeviceGetAttribute(&d.sms, cudaDevAttrMultiProcessorCount, dev));
+    SLF_CUDA(cudaDeviceGetAttribute(&d.major, cudaDevAttrComputeCapabilityMajor, dev));
+    SLF_CUDA(cudaDeviceGetAttribute(&d.minor, cudaDevAttrComputeCapabilityMinor, dev));
+  }
+  if (d.major != 10 || d.minor != 0)
+    return fail(SLF_ERR_UNSUPPORTED, "libslf_lce is built for sm_100a; device is sm_%d%d", d.major, d.minor);
+  *out = &d;
+  return SLF_OK;
+}
+
+PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  });
+  return fn;
+}
+
+// 2-D bf16 tensor map, dims {inner (contiguous), outer}, 128-byte swizzle, zero fill out of bounds.
+slf_status make_tmap(CUtensorMap* m, const void* base, uint64_t inner, uint64_t outer, uint64_t row_stride_bytes,
+                     uint32_t box_inner, uint32_t box_outer) {
+  auto fn = encode_fn();
+  if (!fn) return fail(SLF_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+  cuuint64_t dims[2] = {inner, outer};
+  cuuint64_t strides[1] = {row_stride_bytes};
+  cuuint32_t box[2] = {box_inner, box_outer};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box, estr,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS)
+    return fail(SLF_ERR_CUDA, "cuTensorMapEncodeTiled failed (%d): dims %llu x %llu stride %llu box %u x %u", (int)r,
+                (unsigned long long)inner, (unsigned long long)outer, (unsigned long long)row_stride_bytes, box_inner,
+                box_outer);
+  return SLF_OK;
+}
+// Operand views.  K-major: stored [rows][K] -> box {64, rows_per_tile}.  MN-major: stored [K][MN]
+// -> box {64, 64}, several boxes per stage.
+slf_status tmap_kmajor(CUtensorMap* m, const void* base, int64_t K, int64_t rows, int64_t ld, uint32_t box_rows) {
+  return make_tmap(m, base, (uint64_t)K, (uint64_t)rows, (uint64_t)ld * 2, 64, box_rows);
+}
+slf_status tmap_mnmajor(CUtensorMap* m, const void* base, int64_t MN, int64_t K, int64_t ld) {
+  return make_tmap(m, base, (uint64_t)MN, (uint64_t)K, (uint64_t)ld * 2, 64, 64);
+}
+
+template <int EPI, bool A_MN, bool B_MN>
+slf_status launch_gemm(DevInfo* dev, const CUtensorMap& ta, const CUtensorMap& tb, GemmArgs a, cudaStream_t s) {
+  constexpr int kId = EPI * 4 + (A_MN ? 2 : 0) + (B_MN ? 1 : 0);
+  auto kfn = lce_gemm_kernel<EPI, A_MN, B_MN>;
+  {
+    std::lock_guard<std::mutex> lk(g_mu);
+    if (!dev->gemm_attr_set[kId]) {
+      SLF_CUDA(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, GEMM_SMEM_BYTES));
+      dev->gemm_attr_set[kId] = true;
+    }
+  }
+  if (a.M <= 0 || a.N <= 0 || a.K <= 0) return SLF_OK;
+  a.tiles_m = (a.M + BM - 1) / BM;
+  a.tiles_n = (a.N + BN - 1) / BN;
+  a.num_tiles = a.tiles_m * a.tiles_n;
+  a.group_m = std::min(a.tiles_m, 16);
+  const int grid = std::min(a.num_tiles, dev->sms);
+  kfn<<<grid, GEMM_THREADS, GEMM_SMEM_BYTES, s>>>(ta, tb, a);
+  SLF_CUDA(cudaGetLastError());
+  return SLF_OK;
+}
+
+// ---- planner (schedule R) ----------------------------------------------------------------------
+inline size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
+
+struct Plan {
+  int64_t R = 0, Cv = 0, nR = 0, nC = 0;
+  size_t off_rowstat = 0, off_shard = 0, off_zt = 0, off_union = 0, off_dxacc = 0;
+  size_t fwd_bytes = 0, bwd_bytes = 0, total = 0;
+};
+
+size_t default_budget(int64_t N, int64_t V) {
+  const size_t five = (size_t)(0.05 * (double)N * (double)V * 2.0);
+  return std::max(five, (size_t)16 << 20);
+}
+
+bool plan_r(int64_t N, int64_t H, int64_t V, size_t budget, Plan* out) {
+  if (N < 1 || H < 8 || V < 1) return false;
+  if (budget == 0) budget = default_budget(N, V);
+  Plan p;
+  p.off_rowstat = WS_HEADER_BYTES;
+  p.off_shard = align_up(p.off_rowstat + (size_t)N * 16, 1024);
+  p.off_zt = align_up(p.off_shard + (size_t)N * 16, 1024);
+  p.off_union = align_up(p.off_zt + (size_t)N * 4, 1024);
+  const int64_t tiles_v = (V + BN - 1) / BN;
+  p.fwd_bytes = (size_t)tiles_v * N * 8;
+  if (p.off_union + p.fwd_bytes > budget) return false;
+  const int64_t Vr = align_up((size_t)V, BN);
+  double best = 1e300;
+  bool found = false;
+  for (int64_t nR = 1; nR <= 64; ++nR) {
+    const int64_t R = (int64_t)align_up((size_t)((N + nR - 1) / nR), BM);
+    if (nR > 1 && (nR - 1) * R >= N) continue;  // empty trailing block
+    const size_t dx = align_up((size_t)R * H * 4, 1024);
+    if (p.off_union + dx >= budget) continue;
+    const size_t avail = budget - p.off_union - dx;
+    int64_t Cv = (int64_t)(avail / ((size_t)R * 2)) / BN * BN;
+    Cv = std::min(Cv, Vr);
+    if (Cv < std::min<int64_t>(Vr, 1024)) continue;
+    const int64_t nC = (V + Cv - 1) / Cv;
+    const int64_t nRr = (N + R - 1) / R;
+    // Cost model in bytes of extra HBM traffic: dW bf16 RMW per extra row block, dX fp32 RMW per
+    // extra vocab chunk, and ~5 us of launch/tail per GEMM launch expressed as bytes at 6.5 TB/s.
+    const double cost = (double)(nRr - 1) * V * H * 4 + (double)nRr * (nC - 1) * R * H * 8 +
+                        (double)nRr * nC * 3 * 5e-6 * 6.5e12;
+    if (cost < best) {
+      best = cost;
+      p.R = R;
+      p.Cv = Cv;
+      p.nR = nRr;
+      p.nC = nC;
+      found = true;
+    }
+  }
+  if (!found) return false;
+  const size_t g_bytes = align_up((size_t)p.R * p.Cv * 2, 1024);
+  p.off_dxacc = p.off_union + g_bytes;
+  p.bwd_bytes = g_bytes + (size_t)p.R * H * 4;
+  p.total = p.off_union + std::max(p.fwd_bytes, p.bwd_bytes);
+  if (p.total > budget) return false;
+  *out = p;
+  return true;
+}
+
+bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
+
+slf_status check_common(const void* hidden, const void* weight, const int32_t* targets, int64_t N, int64_t H,
+                        int64_t V, const void* ws) {
+  if (!hidden || !weight || !targets || !ws) return fail(SLF_ERR_ARG, "null required pointer");
+  if (N < 1 || H < 8 || V < 1) return fail(SLF_ERR_ARG, "bad sizes N=%lld H=%lld V=%lld", (long long)N, (long long)H, (long long)V);
+  if (H % 8) return fail(SLF_ERR_ARG, "H must be a multiple of 8 (got %lld)", (long long)H);
+  if (N > (1ll << 31) - 1 || V > (1ll << 31) - 1 || H > (1 << 20)) return fail(SLF_ERR_ARG, "sizes exceed int32 tile indexing");
+  if (!aligned16(hidden) || !aligned16(weight) || !aligned16(targets) || !aligned16(ws))
+    return fail(SLF_ERR_ALIGN, "device pointers must be 16-byte aligned");
+  return SLF_OK;
+}
+
+// ---- phases ------------------------------------------------------------------------------------
+struct Ctx {
+  DevInfo* dev;
+  cudaStream_t s;
+  uint8_t* ws;
+  Plan plan;
+};
+
+WsHeader* hdr_of(uint8_t* ws) { return reinterpret_cast<WsHeader*>(ws); }
+double* block_sums_of(uint8_t* ws) { return reinterpret_cast<double*>(ws + 256); }
+
+// Forward statistics of one shard: EPI_STATS GEMM over all (row tile, vocab tile), then the
+// per-row merge into ShardStat.
+slf_status phase_stats(Ctx& c, const void* X, const void* W, const int32_t* t, int64_t N, int64_t H, int64_t V_l,
+                       int64_t vocab_start, int32_t ignore_index, slf_shardstat* out) {
+  CUtensorMap ta, tb;
+  SLF_TRY(tmap_kmajor(&ta, X, H, N, H, BM));
+  SLF_TRY(tmap_kmajor(&tb, W, H, V_l, H, BN));
+  GemmArgs a{};
+  a.M = (int)N;
+  a.N = (int)V_l;
+  a.K = (int)H;
+  a.targets = t;
+  a.tcol0 = vocab_start;
+  a.ignore_index = ignore_index;
+  a.partials = reinterpret_cast<float2*>(c.ws + c.plan.off_union);
+  a.zt = reinterpret_cast<float*>(c.ws + c.plan.off_zt);
+  SLF_TRY((launch_gemm<EPI_STATS, false, false>(c.dev, ta, tb, a, c.s)));
+  const int tiles_v = (int)((V_l + BN - 1) / BN);
+  local_combine_kernel<<<(unsigned)((N + 255) / 256), 256, 0, c.s>>>(a.partials, tiles_v, a.zt, t, N, vocab_start,
+                                                                     V_l, ignore_index, out);
+  SLF_CUDA(cudaGetLastError());
+  return SLF_OK;
+}
+
+slf_status phase_combine(Ctx& c, const slf_shardstat* st, int g, const int32_t* t, int64_t N, int64_t vocab_start,
+                         int64_t V_l, int64_t V_global, int32_t ignore_index, int reduction, float scale,
+                         float* loss_out, slf_rowstat* rowstat) {
+  const unsigned blocks = (unsigned)((N + 255) / 256);
+  if (blocks > (unsigned)MAX_LOSS_BLOCKS * 4) return fail(SLF_ERR_ARG, "N too large for the loss reduction");
+  prep_targets_kernel<<<1, 1024, 0, c.s>>>(t, N, ignore_index, V_global, hdr_of(c.ws));
+  SLF_CUDA(cudaGetLastError());
+  final_combine_kernel<<<blocks, 256, 0, c.s>>>(st, g, t, N, vocab_start, V_l, V_global, ignore_index, reduction,
+                                                scale, loss_out, rowstat, hdr_of(c.ws), block_sums_of(c.ws));
+  SLF_CUDA(cudaGetLastError());
+  return SLF_OK;
+}
+
+// Backward (schedule R): for each row block r, for each vocab chunk c: recompute the logits tile
+// by tile and form G (EPI_GRAD) -> dW_c (+)= G^T X_r (EPI_DW) -> dX_r (+)= G W_c (EPI_DX).
+slf_status phase_backward(Ctx& c, const void* X, const void* W, const slf_rowstat* rowstat, int64_t N, int64_t H,
+                          int64_t V_l, float grad_scale, void* dX, int dX_fp32, void* dW) {
+  if (!dX && !dW) return SLF_OK;
+  const Plan& p = c.plan;
+  uint8_t* G = c.ws + p.off_union;
+  float* dxacc = reinterpret_cast<float*>(c.ws + p.off_dxacc);
+  const int64_t ldG = p.Cv;
+  for (int64_t rb = 0; rb < p.nR; ++rb) {
+    const int64_t r0 = rb * p.R;
+    const int64_t rows = std::min(p.R, N - r0);
+    if (rows <= 0) break;
+    const uint8_t* Xr = reinterpret_cast<const uint8_t*>(X) + (size_t)r0 * H * 2;
+    for (int64_t cb = 0; cb < p.nC; ++cb) {
+      const int64_t c0 = cb * p.Cv;
+      const int64_t wc = std::min(p.Cv, V_l - c0);
+      const uint8_t* Wc = reinterpret_cast<const uint8_t*>(W) + (size_t)c0 * H * 2;
+      {  // G[rows, wc] = coef * (softmax - onehot), recomputed
+        CUtensorMap ta, tb;
+        SLF_TRY(tmap_kmajor(&ta, Xr, H, rows, H, BM));
+        SLF_TRY(tmap_kmajor(&tb, Wc, H, wc, H, BN));
+        GemmArgs a{};
+        a.M = (int)rows;
+        a.N = (int)wc;
+        a.K = (int)H;
+        a.rowstat = rowstat + r0;
+        a.col0 = c0;
+        a.grad_scale = grad_scale;
+        a.out = G;
+        a.ld_out = ldG;
+        SLF_TRY((launch_gemm<EPI_GRAD, false, false>(c.dev, ta, tb, a, c.s)));
+      }
+      if (dW) {  // dW[c0:c0+wc] (+)= G^T X_r : A = G^T (MN-major), B = X_r (MN-major)
+        CUtensorMap ta, tb;
+        SLF_TRY(tmap_mnmajor(&ta, G, wc, rows, ldG));
+        SLF_TRY(tmap_mnmajor(&tb, Xr, H, rows, H));
+        GemmArgs a{};
+        a.M = (int)wc;
+        a.N = (int)H;
+        a.K = (int)rows;
+        a.out = reinterpret_cast<uint8_t*>(dW) + (size_t)c0 * H * 2;
+        a.ld_out = H;
+        a.mode = rb > 0 ? 1 : 0;
+        SLF_TRY((launch_gemm<EPI_DW, true, true>(c.dev, ta, tb, a, c.s)));
+      }
+      if (dX) {  // dX_r (+)= G W_c : A = G (K-major), B = W_c (MN-major)
+        CUtensorMap ta, tb;
+        SLF_TRY(tmap_kmajor(&ta, G, wc, rows, ldG, BM));
+        SLF_TRY(tmap_mnmajor(&tb, Wc, H, wc, H));
+        GemmArgs a{};
+        a.M = (int)rows;
+        a.N = (int)H;
+        a.K = (int)wc;
+        a.rowstat = rowstat + r0;
+        if (dX_fp32) {
+          a.out = reinterpret_cast<float*>(dX) + (size_t)r0 * H;
+          a.ld_out = H;
+          a.mode = cb == 0 ? DX_STORE_F32 : DX_ACC_F32;
+        } else {
+          a.out = dxacc;
+          a.ld_out = H;
+          a.out2 = reinterpret_cast<uint8_t*>(dX) + (size_t)r0 * H * 2;
+          a.ld_out2 = H;
+          if (p.nC == 1)
+            a.mode = DX_STORE_FINAL_BF16;
+          else if (cb == 0)
+            a.mode = DX_STORE_F32;
+          else if (cb == p.nC - 1)
+            a.mode = DX_ACC_FINAL_BF16;
+          else
+            a.mode = DX_ACC_F32;
+        }
+        SLF_TRY((launch_gemm<EPI_DX, false, true>(c.dev, ta, tb, a, c.s)));
+      }
+    }
+  }
+  return SLF_OK;
+}
+
+slf_status setup(Ctx& c, int64_t N, int64_t H, int64_t V_l, size_t budget, void* ws, size_t ws_bytes, void* stream) {
+  SLF_TRY(device_info(&c.dev));
+  if (!plan_r(N, H, V_l, budget, &c.plan))
+    return fail(SLF_ERR_WORKSPACE, "no schedule-R plan fits the budget (N=%lld H=%lld V=%lld budget=%zu)",
+                (long long)N, (long long)H, (long long)V_l, budget ? budget : default_budget(N, V_l));
+  if (ws_bytes < c.plan.total)
+    return fail(SLF_ERR_WORKSPACE, "workspace %zu bytes < required %zu", ws_bytes, c.plan.total);
+  c.s = reinterpret_cast<cudaStream_t>(stream);
+  c.ws = reinterpret_cast<uint8_t*>(ws);
+  return SLF_OK;
+}
+
+}  // namespace
+
+// ---- C ABI ---------------------------------------------------------------------------------------
+extern "C" {
+
+int slf_lce_version(void) { return 100; }
+
+const char* slf_last_error_string(void) { return g_err.c_str(); }
+
+size_t slf_lce_workspace_bytes(int64_t N, int64_t H, int64_t V_local, int schedule, size_t budget_bytes) {
+  if (schedule != SLF_SCHED_AUTO && schedule != SLF_SCHED_R) return 0;
+  Plan p;
+  if (!plan_r(N, H, V_local, budget_bytes, &p)) return 0;
+  return p.total;
+}
+
+slf_status slf_lce_plan_describe(int64_t N, int64_t H, int64_t V_local, int schedule, size_t budget_bytes, char* out,
+                                 size_t cap) {
+  if (!out || cap == 0) return fail(SLF_ERR_ARG, "null output buffer");
+  if (schedule != SLF_SCHED_AUTO && schedule != SLF_SCHED_R) return fail(SLF_ERR_UNIMPLEMENTED, "schedule %d", schedule);
+  Plan p;
+  if (!plan_r(N, H, V_local, budget_bytes, &p)) return fail(SLF_ERR_WORKSPACE, "no plan fits");
+  const int64_t launches = 4 + p.nR * p.nC * 3;
+  snprintf(out, cap,
+           "schedule=R row_block=%lld n_row_blocks=%lld vocab_chunk=%lld n_vocab_chunks=%lld workspace=%zu "
+           "fwd_partials=%zu bwd=%zu launches=%lld",
+           (long long)p.R, (long long)p.nR, (long long)p.Cv, (long long)p.nC, p.total, p.fwd_bytes, p.bwd_bytes,
+           (long long)launches);
+  return SLF_OK;
+}
+
+slf_status slf_lce_fwd_bwd(const void* hidden, const void* weight, const int32_t* targets, int64_t N, int64_t H,
+                           int64_t V, int32_t ignore_index, int reduction, float scale, float* loss_out,
+                           void* dhidden, void* dweight, void* workspace, size_t workspace_bytes, int schedule,
+                           size_t budget_bytes, void* stream) {
+  SLF_TRY(check_common(hidden, weight, targets, N, H, V, workspace));
+  if (!loss_out) return fail(SLF_ERR_ARG, "null loss_out");
+  if (reduction < SLF_SUM || reduction > SLF_NONE) return fail(SLF_ERR_ARG, "bad reduction %d", reduction);
+  if (schedule != SLF_SCHED_AUTO && schedule != SLF_SCHED_R) return fail(SLF_ERR_UNIMPLEMENTED, "schedule %d", schedule);
+  if ((dhidden && !aligned16(dhidden)) || (dweight && !aligned16(dweight)))
+    return fail(SLF_ERR_ALIGN, "gradient pointers must be 16-byte aligned");
+  Ctx c;
+  SLF_TRY(setup(c, N, H, V, budget_bytes, workspace, workspace_bytes, stream));
+  slf_shardstat* st = reinterpret_cast<slf_shardstat*>(c.ws + c.plan.off_shard);
+  slf_rowstat* rs = reinterpret_cast<slf_rowstat*>(c.ws + c.plan.off_rowstat);
+  SLF_TRY(phase_stats(c, hidden, weight, targets, N, H, V, 0, ignore_index, st));
+  SLF_TRY(phase_combine(c, st, 1, targets, N, 0, V, V, ignore_index, reduction, scale, loss_out, rs));
+  SLF_TRY(phase_backward(c, hidden, weight, rs, N, H, V, 1.0f, dhidden, 0, dweight));
+  return SLF_OK;
+}
+
+slf_status slf_lce_fwd(const void* hidden, const void* weight, const int32_t* targets, int64_t N, int64_t H,
+                       int64_t V, int32_t ignore_index, int reduction, float scale, float* loss_out,
+                       slf_rowstat* rowstat, void* workspace, size_t workspace_bytes, size_t budget_bytes,
+                       void* stream) {
+  SLF_TRY(check_common(hidden, weight, targets, N, H, V, workspace));
+  if (!loss_out || !rowstat) return fail(SLF_ERR_ARG, "null loss_out/rowstat");
+  if (reduction < SLF_SUM || reduction > SLF_NONE) return fail(SLF_ERR_ARG, "bad reduction %d", reduction);
+  if (!aligned16(rowstat)) return fail(SLF_ERR_ALIGN, "rowstat must be 16-byte aligned");
+  Ctx c;
+  SLF_TRY(setup(c, N, H, V, budget_bytes, workspace, workspace_bytes, stream));
+  slf_shardstat* st = reinterpret_cast<slf_shardstat*>(c.ws + c.plan.off_shard);
+  SLF_TRY(phase_stats(c, hidden, weight, targets, N, H, V, 0, ignore_index, st));
+  SLF_TRY(phase_combine(c, st, 1, targets, N, 0, V, V, ignore_index, reduction, scale, loss_out, rowstat));
+  return SLF_OK;
+}
+
+slf_status slf_lce_fwd_shard_stats(const void* hidden, const void* weight_shard, const int32_t* targets, int64_t N,
+                                   int64_t H, int64_t V_local, int64_t vocab_start, int32_t ignore_index,
+                                   slf_shardstat* shardstat, void* workspace, size_t workspace_bytes,
+                                   size_t budget_bytes, void* stream) {
+  SLF_TRY(check_common(hidden, weight_shard, targets, N, H, V_local, workspace));
+  if (!shardstat) return fail(SLF_ERR_ARG, "null shardstat");
+  if (!aligned16(shardstat)) return fail(SLF_ERR_ALIGN, "shardstat must be 16-byte aligned");
+  if (vocab_start < 0) return fail(SLF_ERR_ARG, "vocab_start < 0");
+  Ctx c;
+  SLF_TRY(setup(c, N, H, V_local, budget_bytes, workspace, workspace_bytes, stream));
+  SLF_TRY(phase_stats(c, hidden, weight_shard, targets, N, H, V_local, vocab_start, ignore_index, shardstat));
+  return SLF_OK;
+}
+
+slf_status slf_lce_stats_combine(const slf_shardstat* stats, int g, const int32_t* targets, int64_t N,
+                                 int64_t vocab_start, int64_t V_local, int64_t V_global, int32_t ignore_index,
+                                 int reduction, float scale, float* loss_out, slf_rowstat* rowstat,
+                                 void* workspace, size_t workspace_bytes, void* stream) {
+  if (!stats || !targets || !loss_out || !rowstat || !workspace) return fail(SLF_ERR_ARG, "null required pointer");
+  if (g < 1 || N < 1 || V_local < 1 || V_global < 1 || vocab_start < 0 || vocab_start + V_local > V_global)
+    return fail(SLF_ERR_ARG, "bad shard geometry");
+  if (reduction < SLF_SUM || reduction > SLF_NONE) return fail(SLF_ERR_ARG, "bad reduction %d", reduction);
+  if (!aligned16(stats) || !aligned16(targets) || !aligned16(rowstat) || !aligned16(workspace))
+    return fail(SLF_ERR_ALIGN, "device pointers must be 16-byte aligned");
+  if (workspace_bytes < WS_HEADER_BYTES) return fail(SLF_ERR_WORKSPACE, "workspace smaller than its header");
+  Ctx c;
+  SLF_TRY(device_info(&c.dev));
+  c.s = reinterpret_cast<cudaStream_t>(stream);
+  c.ws = reinterpret_cast<uint8_t*>(workspace);
+  SLF_TRY(phase_combine(c, stats, g, targets, N, vocab_start, V_local, V_global, ignore_index, reduction, scale,
+                        loss_out, rowstat));
+  return SLF_OK;
+}
+
+slf_status slf_lce_bwd(const void* hidden, const void* weight, const int32_t* targets, const slf_rowstat* rowstat,
+                       int64_t N, int64_t H, int64_t V_local, float grad_scale, void* dhidden, int dhidden_fp32,
+                       void* dweight, void* workspace, size_t workspace_bytes, size_t budget_bytes, void* stream) {
+  SLF_TRY(check_common(hidden, weight, targets, N, H, V_local, workspace));
+  if (!rowstat) return fail(SLF_ERR_ARG, "null rowstat");
+  if (!aligned16(rowstat) || (dhidden && !aligned16(dhidden)) || (dweight && !aligned16(dweight)))
+    return fail(SLF_ERR_ALIGN, "device pointers must be 16-byte aligned");
+  Ctx c;
+  SLF_TRY(setup(c, N, H, V_local, budget_bytes, workspace, workspace_bytes, stream));
+  SLF_TRY(phase_backward(c, hidden, weight, rowstat, N, H, V_local, grad_scale, dhidden, dhidden_fp32, dweight));
+  return SLF_OK;
+}
+
+slf_status slf_lce_status(const void* workspace, void* stream, int32_t* bad_targets, int64_t* n_valid) {
+  if (!workspace || !bad_targets) return fail(SLF_ERR_ARG, "null pointer");
+  SLF_CUDA(cudaStreamSynchronize(reinterpret_cast<cudaStream_t>(stream)));
+  WsHeader h;
+  SLF_CUDA(cudaMemcpy(&h, workspace, sizeof(h), cudaMemcpyDeviceToHost));
+  *bad_targets = h.bad;
+  if (n_valid) *n_valid = (int64_t)h.n_valid;
+  return SLF_OK;
+}
+
+slf_status slf_debug_gemm(const void* A, const void* B, float* D, int64_t M, int64_t N, int64_t K, int a_mn,
+                          int b_mn, void* stream) {
+  if (!A || !B || !D) return fail(SLF_ERR_ARG, "null pointer");
+  if (M < 8 || N < 8 || K < 8 || M % 8 || N % 8 || K % 8) return fail(SLF_ERR_ARG, "M, N, K must be multiples of 8");
+  if (!aligned16(A) || !aligned16(B) || !aligned16(D)) return fail(SLF_ERR_ALIGN, "pointers must be 16-byte aligned");
+  DevInfo* dev;
+  SLF_TRY(device_info(&dev));
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  CUtensorMap ta, tb;
+  if (a_mn)
+    SLF_TRY(tmap_mnmajor(&ta, A, M, K, M));
+  else
+    SLF_TRY(tmap_kmajor(&ta, A, K, M, K, BM));
+  if (b_mn)
+    SLF_TRY(tmap_mnmajor(&tb, B, N, K, N));
+  else
+    SLF_TRY(tmap_kmajor(&tb, B, K, N, K, BN));
+  GemmArgs a{};
+  a.M = (int)M;
+  a.N = (int)N;
+  a.K = (int)K;
+  a.out = D;
+  a.ld_out = N;
+  if (!a_mn && !b_mn) return launch_gemm<EPI_F32, false, false>(dev, ta, tb, a, s);
+  if (!a_mn && b_mn) return launch_gemm<EPI_F32, false, true>(dev, ta, tb, a, s);
+  if (a_mn && !b_mn) return launch_gemm<EPI_F32, true, false>(dev, ta, tb, a, s);
+  return launch_gemm<EPI_F32, true, true>(dev, ta, tb, a, s);
+}
+
+}  // extern "C"

@@ -1,0 +1,195 @@
+"""Python API of the fused linear-cross-entropy hot path (thin layer over libslf_lce.so).
+
+Every step of the path runs in the library's CUDA kernels; this module only checks dtypes,
+allocates outputs / workspace with torch and passes pointers and the current stream.
+Semantics: include/slf_lce.h and DESIGN.md (§3.3 fused LinearCrossEntropy).
+"""
+from __future__ import annotations
+
+import ctypes
+
+import torch
+
+from ._lib import REDUCTIONS, SCHEDULES, check, lib
+
+ROWSTAT_BYTES = 16
+SHARDSTAT_BYTES = 16
+
+
+def _stream_ptr(device) -> int:
+    return torch.cuda.current_stream(device).cuda_stream
+
+
+def _ptr(t):
+    return None if t is None else t.data_ptr()
+
+
+def _prep(hidden: torch.Tensor, weight: torch.Tensor, targets: torch.Tensor):
+    if not (hidden.is_cuda and weight.is_cuda and targets.is_cuda):
+        raise ValueError("hidden, weight and targets must be CUDA tensors (no CPU path)")
+    if hidden.dtype != torch.bfloat16 or weight.dtype != torch.bfloat16:
+        raise TypeError("hidden and weight must be bfloat16")
+    if hidden.dim() != 2 or weight.dim() != 2 or hidden.shape[1] != weight.shape[1]:
+        raise ValueError(f"shape mismatch: hidden {tuple(hidden.shape)} weight {tuple(weight.shape)}")
+    hidden = hidden.contiguous()
+    weight = weight.contiguous()
+    targets = targets.reshape(-1)
+    if targets.dtype != torch.int32:
+        targets = targets.to(torch.int32)
+    targets = targets.contiguous()
+    if targets.numel() != hidden.shape[0]:
+        raise ValueError("targets must have N entries")
+    return hidden, weight, targets
+
+
+def workspace_bytes(N: int, H: int, V: int, schedule: str = "auto", budget_bytes: int = 0) -> int:
+    return int(lib().slf_lce_workspace_bytes(N, H, V, SCHEDULES[schedule], budget_bytes))
+
+
+def plan_describe(N: int, H: int, V: int, schedule: str = "auto", budget_bytes: int = 0) -> str:
+    buf = ctypes.create_string_buffer(512)
+    check(lib().slf_lce_plan_describe(N, H, V, SCHEDULES[schedule], budget_bytes, buf, 512), "slf_lce_plan_describe")
+    return buf.value.decode()
+
+
+def alloc_workspace(N: int, H: int, V: int, device, schedule: str = "auto", budget_bytes: int = 0) -> torch.Tensor:
+    nb = workspace_bytes(N, H, V, schedule, budget_bytes)
+    if nb == 0:
+        raise RuntimeError(f"no LCE plan fits the budget for N={N} H={H} V={V} budget={budget_bytes}")
+    return torch.empty(nb, dtype=torch.uint8, device=device)
+
+
+def lce_fwd_bwd(hidden, weight, targets, ignore_index: int = -100, reduction: str = "mean", scale: float = 1.0,
+                need_dhidden: bool = True, need_dweight: bool = True, budget_bytes: int = 0, workspace=None,
+                out=None, schedule: str = "auto"):
+    """Fused LCE forward + backward.  Returns (loss fp32, dhidden bf16 | None, dweight bf16 | None).
+
+    ``out`` may be a (loss, dhidden, dweight) triple of preallocated tensors to write into.
+    """
+    hidden, weight, targets = _prep(hidden, weight, targets)
+    N, H = hidden.shape
+    V = weight.shape[0]
+    dev = hidden.device
+    red = REDUCTIONS[reduction]
+    if out is not None:
+        loss, dX, dW = out
+    else:
+        loss = torch.empty(N if reduction == "none" else 1, dtype=torch.float32, device=dev)
+        dX = torch.empty_like(hidden) if need_dhidden else None
+        dW = torch.empty_like(weight) if need_dweight else None
+    if workspace is None:
+        workspace = alloc_workspace(N, H, V, dev, schedule, budget_bytes)
+    check(lib().slf_lce_fwd_bwd(hidden.data_ptr(), weight.data_ptr(), targets.data_ptr(), N, H, V, ignore_index, red,
+                                float(scale), loss.data_ptr(), _ptr(dX), _ptr(dW), workspace.data_ptr(),
+                                workspace.numel(), SCHEDULES[schedule], budget_bytes, _stream_ptr(dev)),
+          "slf_lce_fwd_bwd")
+    return (loss if reduction == "none" else loss[0]), dX, dW
+
+
+def lce_fwd(hidden, weight, targets, ignore_index: int = -100, reduction: str = "mean", scale: float = 1.0,
+            budget_bytes: int = 0, workspace=None):
+    """Forward half (schedule R split).  Returns (loss, rowstat [N, 16 bytes as uint8])."""
+    hidden, weight, targets = _prep(hidden, weight, targets)
+    N, H = hidden.shape
+    V = weight.shape[0]
+    dev = hidden.device
+    loss = torch.empty(N if reduction == "none" else 1, dtype=torch.float32, device=dev)
+    rowstat = torch.empty(N, ROWSTAT_BYTES, dtype=torch.uint8, device=dev)
+    if workspace is None:
+        workspace = alloc_workspace(N, H, V, dev, budget_bytes=budget_bytes)
+    check(lib().slf_lce_fwd(hidden.data_ptr(), weight.data_ptr(), targets.data_ptr(), N, H, V, ignore_index,
+                            REDUCTIONS[reduction], float(scale), loss.data_ptr(), rowstat.data_ptr(),
+                            workspace.data_ptr(), workspace.numel(), budget_bytes, _stream_ptr(dev)), "slf_lce_fwd")
+    return (loss if reduction == "none" else loss[0]), rowstat
+
+
+def lce_bwd(hidden, weight, targets, rowstat, grad_scale: float = 1.0, need_dhidden: bool = True,
+            need_dweight: bool = True, dhidden_fp32: bool = False, budget_bytes: int = 0, workspace=None):
+    """Backward half: recompute logits per tile, G -> dhidden, dweight.  grad_scale = upstream grad."""
+    hidden, weight, targets = _prep(hidden, weight, targets)
+    N, H = hidden.shape
+    V = weight.shape[0]
+    dev = hidden.device
+    dX = None
+    if need_dhidden:
+        dX = torch.empty(N, H, dtype=torch.float32 if dhidden_fp32 else torch.bfloat16, device=dev)
+    dW = torch.empty_like(weight) if need_dweight else None
+    if workspace is None:
+        workspace = alloc_workspace(N, H, V, dev, budget_bytes=budget_bytes)
+    check(lib().slf_lce_bwd(hidden.data_ptr(), weight.data_ptr(), targets.data_ptr(), rowstat.data_ptr(), N, H, V,
+                            float(grad_scale), _ptr(dX), int(dhidden_fp32), _ptr(dW), workspace.data_ptr(),
+                            workspace.numel(), budget_bytes, _stream_ptr(dev)), "slf_lce_bwd")
+    return dX, dW
+
+
+def shard_stats(hidden, weight_shard, targets, vocab_start: int, ignore_index: int = -100, budget_bytes: int = 0,
+                workspace=None):
+    """This vocab shard's per-row (m, s, z_t, hit) as a float32 [N, 4] tensor."""
+    hidden, weight_shard, targets = _prep(hidden, weight_shard, targets)
+    N, H = hidden.shape
+    V_l = weight_shard.shape[0]
+    dev = hidden.device
+    st = torch.empty(N, 4, dtype=torch.float32, device=dev)
+    if workspace is None:
+        workspace = alloc_workspace(N, H, V_l, dev, budget_bytes=budget_bytes)
+    check(lib().slf_lce_fwd_shard_stats(hidden.data_ptr(), weight_shard.data_ptr(), targets.data_ptr(), N, H, V_l,
+                                        vocab_start, ignore_index, st.data_ptr(), workspace.data_ptr(),
+                                        workspace.numel(), budget_bytes, _stream_ptr(dev)), "slf_lce_fwd_shard_stats")
+    return st
+
+
+def stats_combine(stats, targets, vocab_start: int, V_local: int, V_global: int, ignore_index: int = -100,
+                  reduction: str = "mean", scale: float = 1.0, workspace=None):
+    """Merge [g, N, 4] shard statistics (shard order) into (loss, this shard's rowstat)."""
+    if stats.dtype != torch.float32 or stats.dim() != 3 or stats.shape[2] != 4:
+        raise ValueError("stats must be float32 [g, N, 4]")
+    stats = stats.contiguous()
+    g, N, _ = stats.shape
+    targets = targets.reshape(-1).to(torch.int32).contiguous()
+    dev = stats.device
+    loss = torch.empty(N if reduction == "none" else 1, dtype=torch.float32, device=dev)
+    rowstat = torch.empty(N, ROWSTAT_BYTES, dtype=torch.uint8, device=dev)
+    if workspace is None:
+        workspace = torch.empty(64 * 1024, dtype=torch.uint8, device=dev)
+    check(lib().slf_lce_stats_combine(stats.data_ptr(), g, targets.data_ptr(), N, vocab_start, V_local, V_global,
+                                      ignore_index, REDUCTIONS[reduction], float(scale), loss.data_ptr(),
+                                      rowstat.data_ptr(), workspace.data_ptr(), workspace.numel(), _stream_ptr(dev)),
+          "slf_lce_stats_combine")
+    return (loss if reduction == "none" else loss[0]), rowstat
+
+
+def status(workspace, device=None):
+    """(bad_targets, n_valid) of the last call that used this workspace (synchronises the stream)."""
+    bad = ctypes.c_int32(0)
+    nv = ctypes.c_int64(0)
+    check(lib().slf_lce_status(workspace.data_ptr(), _stream_ptr(device or workspace.device), ctypes.byref(bad),
+                               ctypes.byref(nv)), "slf_lce_status")
+    return bad.value, nv.value
+
+
+def debug_gemm(A, B, a_mn: bool, b_mn: bool, M: int, N: int, K: int):
+    """D[M, N] fp32 = A * B through the tcgen05 core (see slf_debug_gemm)."""
+    D = torch.empty(M, N, dtype=torch.float32, device=A.device)
+    check(lib().slf_debug_gemm(A.data_ptr(), B.data_ptr(), D.data_ptr(), M, N, K, int(a_mn), int(b_mn),
+                               _stream_ptr(A.device)), "slf_debug_gemm")
+    return D
+
+
+class LCEFunction(torch.autograd.Function):
+    """autograd wrapper on the schedule-R split: forward keeps only the 16-byte RowStat per token."""
+
+    @staticmethod
+    def forward(ctx, hidden, weight, targets, ignore_index=-100, reduction="mean"):
+        loss, rowstat = lce_fwd(hidden, weight, targets, ignore_index, reduction, 1.0)
+        ctx.save_for_backward(hidden, weight, targets, rowstat)
+        ctx.reduction = reduction
+        return loss
+
+    @staticmethod
+    def backward(ctx, grad_out):
+        hidden, weight, targets, rowstat = ctx.saved_tensors
+        if ctx.reduction == "none":
+            raise NotImplementedError("reduction='none' backward needs a per-row grad; use lce_bwd")
+        g = float(grad_out.item())
+        dX, dW = lce_bwd(hidden, weight, targets, rowstat, g, ctx.needs_input_grad[0], ctx.needs_input_grad[1])
+        return dX, dW, None, None, None

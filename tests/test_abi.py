@@ -1,0 +1,75 @@
+"""CPU tests of the C ABI: the library loads, exports every symbol include/slf_lce.h declares,
+and the host-only planner entry points honour the memory budget (no CUDA calls here)."""
+import os
+import re
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+@pytest.fixture(scope="module")
+def L():
+    from paper_2603_16428_b200 import build
+    build.build()
+    from paper_2603_16428_b200 import _lib
+    return _lib.lib()
+
+
+def header_functions():
+    src = open(os.path.join(ROOT, "include", "slf_lce.h")).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    return sorted(set(re.findall(r"\b(slf_[a-z_0-9]+)\s*\(", src)))
+
+
+def test_header_symbols_exported(L):
+    from paper_2603_16428_b200 import _lib
+    names = header_functions()
+    assert set(names) == set(_lib.EXPORTS), names
+    for n in names:
+        assert hasattr(L, n), n
+    assert L.slf_lce_version() >= 100
+
+
+def test_so_is_sm100a():
+    import subprocess
+    so = os.path.join(ROOT, "paper_2603_16428_b200", "libslf_lce.so")
+    out = subprocess.run(["cuobjdump", "-lelf", so], capture_output=True, text=True).stdout
+    assert "sm_100a" in out
+    sass = subprocess.run(["cuobjdump", "-sass", so], capture_output=True, text=True).stdout
+    assert "UTCHMMA" in sass and "UTMALDG" in sass and "LDTM" in sass  # tcgen05.mma, TMA, tcgen05.ld
+
+
+@pytest.mark.parametrize("cfg", ["tiny", "llama8b", "qwen7b", "llama70b", "mistral123b"])
+def test_planner_budget(L, cfg):
+    import synth
+    c = synth.CONFIGS[cfg]
+    N, H, V = c["N"], c["H"], c["V"]
+    from paper_2603_16428_b200 import lce
+    ws = lce.workspace_bytes(N, H, V)
+    budget = max(int(0.05 * N * V * 2), 16 << 20)
+    desc = None
+    if ws:
+        assert ws <= budget
+        desc = lce.plan_describe(N, H, V)
+        assert "schedule=R" in desc
+    if cfg in ("tiny", "llama8b", "qwen7b"):
+        assert ws > 0, desc
+    if cfg == "llama8b":
+        assert ws <= 0.05 * N * V * 2  # BASELINE.json: extra memory <= 5% of the N*V*2 logits
+
+
+def test_planner_infeasible_and_errors(L):
+    from paper_2603_16428_b200 import lce, _lib
+    assert lce.workspace_bytes(16384, 4096, 128256, budget_bytes=1 << 20) == 0
+    assert lce.workspace_bytes(0, 4096, 128256) == 0
+    with pytest.raises(_lib.SlfError):
+        lce.plan_describe(16384, 4096, 128256, budget_bytes=1 << 20)
+
+
+def test_sharded_planner(L):
+    from paper_2603_16428_b200 import lce
+    for g in (2, 4, 8):
+        V_l = (128256 + g - 1) // g
+        ws = lce.workspace_bytes(16384, 4096, V_l, budget_bytes=int(0.05 * 16384 * 128256 * 2))
+        assert ws > 0

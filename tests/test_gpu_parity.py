@@ -1,0 +1,240 @@
+"""GPU parity tests (``-m gpu``): the CUDA path through the C ABI against the fp64 oracle on the
+same seeded inputs.  Tolerances (BASELINE.json north_star): loss relative 1e-3, dX and dW
+max|err| <= 2e-2 * max|ref|; integer masking bit-exact.
+"""
+import math
+
+import numpy as np
+import pytest
+
+import oracle
+import synth
+from gpu_util import (GRAD_TOL, assert_loss_close, bf16_to_np64, oracle_inputs, rel_max_err, to_dev)
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def slf():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_2603_16428_b200 as m
+    return m
+
+
+def run_gpu(slf, inp, reduction="mean", scale=1.0, budget=0, ignore_index=-100):
+    X, W, t = to_dev(inp, torch)
+    loss, dX, dW = slf.lce_fwd_bwd(X, W, t, ignore_index=ignore_index, reduction=reduction, scale=scale,
+                                   budget_bytes=budget)
+    torch.cuda.synchronize()
+    return loss, dX, dW
+
+
+def check_against_oracle(slf, inp, reduction="mean", scale=1.0, budget=0, ignore_index=-100):
+    loss, dX, dW = run_gpu(slf, inp, reduction, scale, budget, ignore_index)
+    Xo, Wo, to = oracle_inputs(inp)
+    ref = oracle.lce(Xo, Wo, to, ignore_index=ignore_index, reduction=reduction, scale=scale)
+    assert_loss_close(loss.detach().cpu().numpy(), ref["loss"], reduction)
+    gx = bf16_to_np64(dX)
+    gw = bf16_to_np64(dW)
+    ex, ew = rel_max_err(gx, ref["dX"]), rel_max_err(gw, ref["dW"])
+    assert ex <= GRAD_TOL, f"dX rel max err {ex}"
+    assert ew <= GRAD_TOL, f"dW rel max err {ew}"
+    ign = inp.t == ignore_index
+    if ign.any():  # ignored rows are exactly +0.0 (bf16 bits 0x0000)
+        bits = dX.view(torch.int16).cpu().numpy()[ign]
+        assert np.all(bits == 0)
+    return ex, ew
+
+
+# ---- the GEMM core alone -------------------------------------------------------------------------
+@pytest.mark.parametrize("a_mn", [False, True])
+@pytest.mark.parametrize("b_mn", [False, True])
+@pytest.mark.parametrize("shape", [(128, 256, 64), (384, 512, 320), (200, 264, 136), (1024, 768, 2048)])
+def test_gemm_core(slf, a_mn, b_mn, shape):
+    M, N, K = shape
+    g = torch.Generator(device="cpu").manual_seed(M * 7 + N * 3 + K)
+    A = torch.randn(M, K, generator=g).to(torch.bfloat16)
+    B = torch.randn(K, N, generator=g).to(torch.bfloat16)
+    ref = (A.double() @ B.double()).numpy()
+    Ad = (A.t().contiguous() if a_mn else A).cuda()           # a_mn: stored [K, M]
+    Bd = (B.contiguous() if b_mn else B.t().contiguous()).cuda()  # b_mn: stored [K, N]; else [N, K]
+    D = slf.debug_gemm(Ad, Bd, a_mn, b_mn, M, N, K)
+    torch.cuda.synchronize()
+    err = rel_max_err(D.cpu().numpy(), ref)
+    assert err < 1e-5, err
+
+
+# ---- full path vs oracle -------------------------------------------------------------------------
+@pytest.mark.parametrize("reduction", ["mean", "sum", "none"])
+@pytest.mark.parametrize("alpha,dist", [(1.0, "uniform"), (4.0, "zipf"), (4.0, "uniform")])
+def test_tiny_parity(slf, reduction, alpha, dist):
+    inp = synth.make_config("tiny", seed=11, alpha=alpha, dist=dist)
+    check_against_oracle(slf, inp, reduction=reduction, scale=1.0 if reduction != "sum" else 0.25)
+
+
+def test_multichunk_ragged_parity(slf):
+    """Several row blocks and vocab chunks, ragged tails in every GEMM dimension."""
+    inp = synth.make_inputs(1000, 200, 5000, seed=5, alpha=4.0, dist="zipf")
+    budget = 3 << 19  # 1.5 MiB forces nR > 1 and nC > 1
+    desc = slf.plan_describe(1000, 200, 5000, budget_bytes=budget)
+    kv = dict(x.split("=") for x in desc.split())
+    assert int(kv["n_row_blocks"]) > 1 and int(kv["n_vocab_chunks"]) > 1, desc
+    check_against_oracle(slf, inp, reduction="mean", budget=budget)
+    check_against_oracle(slf, inp, reduction="none", budget=budget)
+
+
+@pytest.mark.parametrize("N,H,V", [(1, 8, 1), (1, 64, 300), (130, 136, 257), (257, 512, 4096)])
+def test_small_edges(slf, N, H, V):
+    inp = synth.make_inputs(N, H, V, seed=N + V, alpha=2.0, ignore_frac=0.0 if N < 10 else 0.05)
+    check_against_oracle(slf, inp, reduction="mean")
+
+
+def test_ignore_index_zero(slf):
+    inp = synth.make_inputs(300, 128, 1000, seed=3, ignore_index=0, alpha=2.0)
+    check_against_oracle(slf, inp, reduction="mean", ignore_index=0)
+
+
+@pytest.mark.slow
+def test_llama_head_reduced_n(slf):
+    """Full Llama-3.1-8B head (H=4096, V=128256) at N=512: every element against the oracle."""
+    inp = synth.make_config("llama8b", seed=21, alpha=4.0, dist="zipf", N=512)
+    ex, ew = check_against_oracle(slf, inp, reduction="mean")
+    print(f"llama8b N=512: dX err {ex:.2e} dW err {ew:.2e}")
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("cfg", ["qwen7b", "mistral123b"])
+def test_other_heads_reduced_n(slf, cfg):
+    inp = synth.make_config(cfg, seed=22, alpha=1.0, dist="uniform", N=256)
+    check_against_oracle(slf, inp, reduction="sum", scale=1.0 / 256)
+
+
+# ---- invariants ----------------------------------------------------------------------------------
+def test_w_zero_closed_form(slf):
+    inp = synth.make_config("tiny", seed=4)
+    X, W, t = to_dev(inp, torch)
+    W.zero_()
+    loss, dX, dW = slf.lce_fwd_bwd(X, W, t, reduction="mean")
+    torch.cuda.synchronize()
+    assert float(loss) == pytest.approx(math.log(4096), rel=1e-6)
+    assert torch.all(dX == 0)
+    valid = inp.t != -100
+    Xo = synth.bf16_bits_to_f64(inp.X)
+    coef = 1.0 / valid.sum()
+    ref = np.tile(coef * Xo[valid].sum(0) / 4096, (4096, 1))
+    for i in np.nonzero(valid)[0]:
+        ref[inp.t[i]] -= coef * Xo[i]
+    assert rel_max_err(bf16_to_np64(dW), ref) < GRAD_TOL
+
+
+def test_scale_linearity_and_determinism(slf):
+    inp = synth.make_inputs(700, 256, 3000, seed=9, alpha=3.0)
+    a = run_gpu(slf, inp, "mean", 1.0)
+    b = run_gpu(slf, inp, "mean", 2.0)
+    c = run_gpu(slf, inp, "mean", 1.0)
+    assert float(a[0]) == float(b[0]) == float(c[0])
+    assert torch.equal(a[1].float() * 2, b[1].float()) and torch.equal(a[2].float() * 2, b[2].float())
+    assert torch.equal(a[1], c[1]) and torch.equal(a[2], c[2])
+
+
+def test_ignored_rows_do_not_leak(slf):
+    inp = synth.make_inputs(400, 128, 2000, seed=10, alpha=2.0)
+    a = run_gpu(slf, inp, "sum")
+    ign = inp.t == -100
+    inp2 = synth.LCEInputs(**{**inp.__dict__})
+    X2 = inp.X.copy()
+    X2[ign] = synth.f32_to_bf16_bits(np.random.default_rng(0).standard_normal((ign.sum(), 128)).astype(np.float32) * 7)
+    inp2.X = X2
+    b = run_gpu(slf, inp2, "sum")
+    assert float(a[0]) == float(b[0])
+    assert torch.equal(a[1][torch.from_numpy(~ign).cuda()], b[1][torch.from_numpy(~ign).cuda()])
+    assert torch.equal(a[2].float().abs(), b[2].float().abs())
+
+
+def test_status_counts(slf):
+    inp = synth.make_config("tiny", seed=1)
+    X, W, t = to_dev(inp, torch)
+    ws = slf.alloc_workspace(256, 512, 4096, X.device)
+    loss, _, _ = slf.lce_fwd_bwd(X, W, t, workspace=ws)
+    bad, nv = slf.status(ws)
+    assert bad == 0 and nv == 243
+    t[5] = 4096
+    loss, _, _ = slf.lce_fwd_bwd(X, W, t, workspace=ws)
+    bad, nv = slf.status(ws)
+    assert bad == 1 and math.isnan(float(loss))
+
+
+def test_all_ignored_mean(slf):
+    inp = synth.make_config("tiny", seed=2)
+    inp.t[:] = -100
+    loss, dX, dW = run_gpu(slf, inp, "mean")
+    assert float(loss) == 0.0 and torch.all(dX == 0) and torch.all(dW == 0)
+
+
+# ---- split API, autograd, shard emulation --------------------------------------------------------
+def test_split_matches_fused(slf):
+    inp = synth.make_inputs(600, 256, 3000, seed=12, alpha=3.0)
+    X, W, t = to_dev(inp, torch)
+    loss_a, dX_a, dW_a = slf.lce_fwd_bwd(X, W, t, reduction="mean")
+    loss_b, rs = slf.lce_fwd(X, W, t, reduction="mean")
+    dX_b, dW_b = slf.lce_bwd(X, W, t, rs, 1.0)
+    torch.cuda.synchronize()
+    assert float(loss_a) == float(loss_b)
+    assert torch.equal(dX_a, dX_b) and torch.equal(dW_a, dW_b)
+    Xr = X.clone().requires_grad_(True)
+    Wr = W.clone().requires_grad_(True)
+    L = slf.LCEFunction.apply(Xr, Wr, t, -100, "mean")
+    (3.0 * L).backward()
+    assert torch.equal(Xr.grad.float(), dX_a.float() * 3) or rel_max_err(bf16_to_np64(Xr.grad), 3 * bf16_to_np64(dX_a)) < 1e-2
+
+
+@pytest.mark.parametrize("g", [2, 3])
+def test_vocab_shard_emulation(slf, g):
+    """g vocab shards on one GPU through the split API (the multi-GPU seam): per-shard statistics,
+    combine in shard order, per-shard backward with fp32 dX partials summed as an all-reduce would."""
+    inp = synth.make_inputs(500, 256, 4100, seed=13, alpha=4.0, dist="zipf")
+    X, W, t = to_dev(inp, torch)
+    V = 4100
+    bounds = [V * k // g for k in range(g + 1)]
+    stats = torch.stack([slf.shard_stats(X, W[a:b].contiguous(), t, a) for a, b in zip(bounds[:-1], bounds[1:])])
+    dX = torch.zeros(500, 256, dtype=torch.float32, device="cuda")
+    dWs = []
+    losses = []
+    for k, (a, b) in enumerate(zip(bounds[:-1], bounds[1:])):
+        loss, rs = slf.stats_combine(stats, t, a, b - a, V, reduction="mean")
+        losses.append(float(loss))
+        dXk, dWk = slf.lce_bwd(X, W[a:b].contiguous(), t, rs, 1.0, dhidden_fp32=True)
+        dX += dXk
+        dWs.append(dWk)
+    torch.cuda.synchronize()
+    assert len(set(losses)) == 1
+    Xo, Wo, to = oracle_inputs(inp)
+    ref = oracle.lce(Xo, Wo, to, reduction="mean")
+    assert_loss_close(losses[0], ref["loss"], "mean")
+    assert rel_max_err(dX.cpu().numpy(), ref["dX"]) <= GRAD_TOL
+    assert rel_max_err(bf16_to_np64(torch.cat(dWs)), ref["dW"]) <= GRAD_TOL
+    ign = inp.t == -100
+    assert np.all(dX.cpu().numpy()[ign] == 0)
+
+
+# ---- full Llama-3.1-8B size, in the launch configuration bench.py times ---------------------------
+@pytest.mark.slow
+def test_llama_full_size_sampled(slf):
+    inp = synth.make_config("llama8b", seed=0, alpha=1.0, dist="uniform")
+    X, W, t = to_dev(inp, torch)
+    loss_rows, dX, dW = slf.lce_fwd_bwd(X, W, t, reduction="none", scale=1.0)
+    loss_m, dX_m, dW_m = slf.lce_fwd_bwd(X, W, t, reduction="mean")
+    torch.cuda.synchronize()
+    rng = np.random.default_rng(5)
+    rows = np.sort(rng.choice(inp.N, 48, replace=False))
+    rows = np.concatenate([rows, np.nonzero(inp.t == -100)[0][:4]])
+    Xo = synth.bf16_bits_to_f64(inp.X[rows])
+    Wo = synth.bf16_bits_to_f64(inp.W)
+    valid, nv, coef = oracle.coef_for(inp.t, -100, "mean", 1.0)
+    l, lse, dXo, _ = oracle.rows(Xo, Wo, inp.t[rows].astype(np.int64), coef[rows])
+    assert_loss_close(loss_rows.cpu().numpy()[rows], l, "none")
+    assert rel_max_err(bf16_to_np64(dX_m)[rows], dXo) <= GRAD_TOL
+    assert float(loss_m) == pytest.approx(float(loss_rows[torch.from_numpy(valid).cuda()].double().sum()) / nv, rel=1e-5)
+    assert torch.isfinite(dW_m.float()).all()
