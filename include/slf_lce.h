@@ -171,6 +171,31 @@ slf_status slf_lce_status(const void* workspace, void* stream, int32_t* bad_targ
 slf_status slf_debug_gemm(const void* A, const void* B, float* D, int64_t M, int64_t N, int64_t K, int a_mn,
                           int b_mn, void* stream);
 
+/* Vocab-shard backward, last step: dhidden bf16 [N, H] = RNE(dhidden_fp32 [N, H]) after the
+ * caller has summed the shards' fp32 partials (e.g. NCCL all-reduce); rows whose RowStat says
+ * ignored are written as +0.0.  All DEVICE pointers, 16-byte aligned. */
+slf_status slf_lce_dx_finalize(const float* dhidden_fp32, const slf_rowstat* rowstat, void* dhidden, int64_t N,
+                               int64_t H, void* stream);
+
+/* ---- instrumentation (bench.py / profiling only; not needed for correctness) ----
+ * slf_profile_begin: from now on, every kernel the library launches FROM THIS THREAD is bracketed
+ * by a pair of CUDA events recorded on its stream.  slf_profile_end: synchronises those events and
+ * writes per-kind totals into HOST arrays of SLF_PROF_KINDS entries: device milliseconds, launches,
+ * algorithmic FLOPs (2*M*N*K of each GEMM launch) and algorithmic bytes (aux kernels: bytes they
+ * must read + write).  Kinds: */
+#define SLF_PROF_KINDS 10
+#define SLF_PROF_GEMM_STATS 0 /* forward logits tile GEMM + stats epilogue          */
+#define SLF_PROF_GEMM_GRAD 1  /* backward recompute GEMM + dlogit (G) epilogue      */
+#define SLF_PROF_GEMM_DW 2    /* dW = G^T X                                         */
+#define SLF_PROF_GEMM_DX 3    /* dX = G W                                           */
+#define SLF_PROF_GEMM_DEBUG 4 /* slf_debug_gemm                                     */
+#define SLF_PROF_PREP 5       /* target scan                                        */
+#define SLF_PROF_LOCAL_COMBINE 6
+#define SLF_PROF_FINAL_COMBINE 7
+#define SLF_PROF_DX_FINALIZE 8
+slf_status slf_profile_begin(void);
+slf_status slf_profile_end(double* ms, int64_t* launches, double* flops, double* bytes);
+
 #ifdef __cplusplus
 }
 #endif

@@ -4,6 +4,6 @@ Hot path: libslf_lce.so (hand-written sm_100a CUDA: TMA + tcgen05/TMEM GEMM tile
 LCE epilogues) behind the C ABI in include/slf_lce.h; this package is the thin Python binding.
 """
 from .lce import (  # noqa: F401
-    LCEFunction, alloc_workspace, debug_gemm, lce_bwd, lce_fwd, lce_fwd_bwd, plan_describe, shard_stats,
+    LCEFunction, Profile, alloc_workspace, debug_gemm, dx_finalize, lce_bwd, lce_fwd, lce_fwd_bwd, plan_describe, shard_stats,
     stats_combine, status, workspace_bytes,
 )

@@ -21,7 +21,9 @@ SCHEDULES = {"auto": 0, "R": 1}
 # Every symbol include/slf_lce.h declares.
 EXPORTS = ["slf_lce_version", "slf_last_error_string", "slf_lce_workspace_bytes", "slf_lce_plan_describe",
            "slf_lce_fwd_bwd", "slf_lce_fwd", "slf_lce_fwd_shard_stats", "slf_lce_stats_combine", "slf_lce_bwd",
-           "slf_lce_status", "slf_debug_gemm"]
+           "slf_lce_status", "slf_debug_gemm", "slf_lce_dx_finalize", "slf_profile_begin", "slf_profile_end"]
+PROF_KINDS = ["gemm_stats", "gemm_grad", "gemm_dw", "gemm_dx", "gemm_debug", "prep", "local_combine", "final_combine",
+              "dx_finalize", "unused"]
 
 _lock = threading.Lock()
 _lib = None
@@ -51,6 +53,9 @@ def _declare(lib):
         "slf_lce_bwd": (INT, [P, P, P, P, I64, I64, I64, F32, P, INT, P, P, SZ, SZ, P]),
         "slf_lce_status": (INT, [P, P, ctypes.POINTER(I32), ctypes.POINTER(I64)]),
         "slf_debug_gemm": (INT, [P, P, P, I64, I64, I64, INT, INT, P]),
+        "slf_lce_dx_finalize": (INT, [P, P, P, I64, I64, P]),
+        "slf_profile_begin": (INT, []),
+        "slf_profile_end": (INT, [P, P, P, P]),
     }
     for name, (res, args) in sig.items():
         f = getattr(lib, name)

@@ -153,4 +153,19 @@ __global__ void __launch_bounds__(256) final_combine_kernel(const slf_shardstat*
   }
 }
 
+// dhidden bf16 = RNE(fp32 sum of shard partials); ignored rows -> +0.0.  8 elements per thread.
+__global__ void __launch_bounds__(256) dx_finalize_kernel(const float* __restrict__ in,
+                                                         const slf_rowstat* __restrict__ rs, uint16_t* __restrict__ out,
+                                                         int64_t N, int64_t H) {
+  const int64_t groups = N * H / 8;
+  for (int64_t gi = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; gi < groups; gi += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t row = gi * 8 / H;
+    const float4 a = reinterpret_cast<const float4*>(in)[2 * gi];
+    const float4 b = reinterpret_cast<const float4*>(in)[2 * gi + 1];
+    uint4 o = make_uint4(pack_bf16x2(a.x, a.y), pack_bf16x2(a.z, a.w), pack_bf16x2(b.x, b.y), pack_bf16x2(b.z, b.w));
+    if (!rs[row].valid) o = make_uint4(0u, 0u, 0u, 0u);
+    reinterpret_cast<uint4*>(out)[gi] = o;
+  }
+}
+
 }  // namespace slf

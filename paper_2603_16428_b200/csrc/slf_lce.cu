@@ -11,6 +11,7 @@
 #include <cstring>
 #include <mutex>
 #include <string>
+#include <vector>
 
 #include "../../include/slf_lce.h"
 #include "aux_kernels.cuh"
@@ -44,6 +45,45 @@ slf_status fail(slf_status s, const char* fmt, ...) {
   } while (0)
 
 constexpr int kMaxDev = 64;
+
+// ---- instrumentation (slf_profile_begin/end) ---------------------------------------------------
+struct ProfRec {
+  int kind;
+  cudaEvent_t a, b;
+  double flops, bytes;
+};
+struct ProfState {
+  bool on = false;
+  std::vector<ProfRec> recs;
+  std::vector<cudaEvent_t> pool;
+};
+thread_local ProfState g_prof;
+
+cudaEvent_t prof_event() {
+  if (!g_prof.pool.empty()) {
+    cudaEvent_t e = g_prof.pool.back();
+    g_prof.pool.pop_back();
+    return e;
+  }
+  cudaEvent_t e = nullptr;
+  cudaEventCreate(&e);
+  return e;
+}
+// RAII bracket around one launch; no-op unless profiling is on.
+struct ProfScope {
+  int idx = -1;
+  cudaStream_t s;
+  ProfScope(int kind, cudaStream_t s_, double flops, double bytes) : s(s_) {
+    if (!g_prof.on) return;
+    ProfRec r{kind, prof_event(), prof_event(), flops, bytes};
+    cudaEventRecord(r.a, s);
+    g_prof.recs.push_back(r);
+    idx = (int)g_prof.recs.size() - 1;
+  }
+  ~ProfScope() {
+    if (idx >= 0) cudaEventRecord(g_prof.recs[idx].b, s);
+  }
+};
 
 struct DevInfo {
   int sms = 0;
@@ -114,6 +154,11 @@ slf_status tmap_mnmajor(CUtensorMap* m, const void* base, int64_t MN, int64_t K,
 
 template <int EPI, bool A_MN, bool B_MN>
 slf_status launch_gemm(DevInfo* dev, const CUtensorMap& ta, const CUtensorMap& tb, GemmArgs a, cudaStream_t s) {
+  constexpr int kKind = EPI == EPI_STATS ? SLF_PROF_GEMM_STATS
+                        : EPI == EPI_GRAD ? SLF_PROF_GEMM_GRAD
+                        : EPI == EPI_DW   ? SLF_PROF_GEMM_DW
+                        : EPI == EPI_DX   ? SLF_PROF_GEMM_DX
+                                          : SLF_PROF_GEMM_DEBUG;
   constexpr int kId = EPI * 4 + (A_MN ? 2 : 0) + (B_MN ? 1 : 0);
   auto kfn = lce_gemm_kernel<EPI, A_MN, B_MN>;
   {
@@ -129,6 +174,7 @@ slf_status launch_gemm(DevInfo* dev, const CUtensorMap& ta, const CUtensorMap& t
   a.num_tiles = a.tiles_m * a.tiles_n;
   a.group_m = std::min(a.tiles_m, 16);
   const int grid = std::min(a.num_tiles, dev->sms);
+  ProfScope ps(kKind, s, 2.0 * a.M * a.N * (double)a.K, 0.0);
   kfn<<<grid, GEMM_THREADS, GEMM_SMEM_BYTES, s>>>(ta, tb, a);
   SLF_CUDA(cudaGetLastError());
   return SLF_OK;
@@ -238,6 +284,7 @@ slf_status phase_stats(Ctx& c, const void* X, const void* W, const int32_t* t, i
   a.zt = reinterpret_cast<float*>(c.ws + c.plan.off_zt);
   SLF_TRY((launch_gemm<EPI_STATS, false, false>(c.dev, ta, tb, a, c.s)));
   const int tiles_v = (int)((V_l + BN - 1) / BN);
+  ProfScope ps(SLF_PROF_LOCAL_COMBINE, c.s, 0.0, (double)N * (tiles_v * 8.0 + 4 + 4 + 16));
   local_combine_kernel<<<(unsigned)((N + 255) / 256), 256, 0, c.s>>>(a.partials, tiles_v, a.zt, t, N, vocab_start,
                                                                      V_l, ignore_index, out);
   SLF_CUDA(cudaGetLastError());
@@ -249,8 +296,12 @@ slf_status phase_combine(Ctx& c, const slf_shardstat* st, int g, const int32_t* 
                          float* loss_out, slf_rowstat* rowstat) {
   const unsigned blocks = (unsigned)((N + 255) / 256);
   if (blocks > (unsigned)MAX_LOSS_BLOCKS * 4) return fail(SLF_ERR_ARG, "N too large for the loss reduction");
-  prep_targets_kernel<<<1, 1024, 0, c.s>>>(t, N, ignore_index, V_global, hdr_of(c.ws));
+  {
+    ProfScope ps(SLF_PROF_PREP, c.s, 0.0, (double)N * 4);
+    prep_targets_kernel<<<1, 1024, 0, c.s>>>(t, N, ignore_index, V_global, hdr_of(c.ws));
+  }
   SLF_CUDA(cudaGetLastError());
+  ProfScope ps(SLF_PROF_FINAL_COMBINE, c.s, 0.0, (double)N * (g * 16.0 + 4 + 16 + 4));
   final_combine_kernel<<<blocks, 256, 0, c.s>>>(st, g, t, N, vocab_start, V_l, V_global, ignore_index, reduction,
                                                 scale, loss_out, rowstat, hdr_of(c.ws), block_sums_of(c.ws));
   SLF_CUDA(cudaGetLastError());
@@ -470,6 +521,53 @@ slf_status slf_lce_status(const void* workspace, void* stream, int32_t* bad_targ
   SLF_CUDA(cudaMemcpy(&h, workspace, sizeof(h), cudaMemcpyDeviceToHost));
   *bad_targets = h.bad;
   if (n_valid) *n_valid = (int64_t)h.n_valid;
+  return SLF_OK;
+}
+
+slf_status slf_lce_dx_finalize(const float* dhidden_fp32, const slf_rowstat* rowstat, void* dhidden, int64_t N,
+                               int64_t H, void* stream) {
+  if (!dhidden_fp32 || !rowstat || !dhidden) return fail(SLF_ERR_ARG, "null pointer");
+  if (N < 1 || H < 8 || H % 8) return fail(SLF_ERR_ARG, "bad sizes");
+  if (!aligned16(dhidden_fp32) || !aligned16(rowstat) || !aligned16(dhidden))
+    return fail(SLF_ERR_ALIGN, "pointers must be 16-byte aligned");
+  DevInfo* dev;
+  SLF_TRY(device_info(&dev));
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  const int64_t groups = N * H / 8;
+  const int blocks = (int)std::min<int64_t>((groups + 255) / 256, (int64_t)dev->sms * 8);
+  ProfScope ps(SLF_PROF_DX_FINALIZE, s, 0.0, (double)N * H * 6 + N * 16.0);
+  dx_finalize_kernel<<<blocks, 256, 0, s>>>(dhidden_fp32, rowstat, reinterpret_cast<uint16_t*>(dhidden), N, H);
+  SLF_CUDA(cudaGetLastError());
+  return SLF_OK;
+}
+
+slf_status slf_profile_begin(void) {
+  for (auto& r : g_prof.recs) {
+    g_prof.pool.push_back(r.a);
+    g_prof.pool.push_back(r.b);
+  }
+  g_prof.recs.clear();
+  g_prof.on = true;
+  return SLF_OK;
+}
+
+slf_status slf_profile_end(double* ms, int64_t* launches, double* flops, double* bytes) {
+  g_prof.on = false;
+  for (int k = 0; k < SLF_PROF_KINDS; ++k) {
+    if (ms) ms[k] = 0;
+    if (launches) launches[k] = 0;
+    if (flops) flops[k] = 0;
+    if (bytes) bytes[k] = 0;
+  }
+  for (auto& r : g_prof.recs) {
+    SLF_CUDA(cudaEventSynchronize(r.b));
+    float t = 0.f;
+    SLF_CUDA(cudaEventElapsedTime(&t, r.a, r.b));
+    if (ms) ms[r.kind] += t;
+    if (launches) launches[r.kind] += 1;
+    if (flops) flops[r.kind] += r.flops;
+    if (bytes) bytes[r.kind] += r.bytes;
+  }
   return SLF_OK;
 }
 

@@ -167,6 +167,36 @@ def status(workspace, device=None):
     return bad.value, nv.value
 
 
+def dx_finalize(dx32, rowstat, out=None):
+    """bf16 dhidden from the fp32 sum of shard partials (ignored rows -> +0.0)."""
+    N, H = dx32.shape
+    if out is None:
+        out = torch.empty(N, H, dtype=torch.bfloat16, device=dx32.device)
+    check(lib().slf_lce_dx_finalize(dx32.data_ptr(), rowstat.data_ptr(), out.data_ptr(), N, H,
+                                    _stream_ptr(dx32.device)), "slf_lce_dx_finalize")
+    return out
+
+
+class Profile:
+    """Context manager over slf_profile_begin/end: per-kernel-kind device ms, launches, FLOPs, bytes."""
+
+    def __enter__(self):
+        check(lib().slf_profile_begin(), "slf_profile_begin")
+        return self
+
+    def __exit__(self, *exc):
+        from ._lib import PROF_KINDS
+        n = len(PROF_KINDS)
+        ms = (ctypes.c_double * n)()
+        la = (ctypes.c_int64 * n)()
+        fl = (ctypes.c_double * n)()
+        by = (ctypes.c_double * n)()
+        check(lib().slf_profile_end(ms, la, fl, by), "slf_profile_end")
+        self.kinds = {k: dict(ms=ms[i], launches=la[i], flops=fl[i], bytes=by[i])
+                      for i, k in enumerate(PROF_KINDS) if la[i]}
+        return False
+
+
 def debug_gemm(A, B, a_mn: bool, b_mn: bool, M: int, N: int, K: int):
     """D[M, N] fp32 = A * B through the tcgen05 core (see slf_debug_gemm)."""
     D = torch.empty(M, N, dtype=torch.float32, device=A.device)
