@@ -104,16 +104,22 @@ def lce_fwd(hidden, weight, targets, ignore_index: int = -100, reduction: str = 
 
 
 def lce_bwd(hidden, weight, targets, rowstat, grad_scale: float = 1.0, need_dhidden: bool = True,
-            need_dweight: bool = True, dhidden_fp32: bool = False, budget_bytes: int = 0, workspace=None):
-    """Backward half: recompute logits per tile, G -> dhidden, dweight.  grad_scale = upstream grad."""
+            need_dweight: bool = True, dhidden_fp32: bool = False, budget_bytes: int = 0, workspace=None,
+            out=None):
+    """Backward half: recompute logits per tile, G -> dhidden, dweight.  grad_scale = upstream grad.
+
+    ``out`` may be a preallocated (dhidden, dweight) pair (either may be None to skip it)."""
     hidden, weight, targets = _prep(hidden, weight, targets)
     N, H = hidden.shape
     V = weight.shape[0]
     dev = hidden.device
-    dX = None
-    if need_dhidden:
-        dX = torch.empty(N, H, dtype=torch.float32 if dhidden_fp32 else torch.bfloat16, device=dev)
-    dW = torch.empty_like(weight) if need_dweight else None
+    if out is not None:
+        dX, dW = out
+    else:
+        dX = None
+        if need_dhidden:
+            dX = torch.empty(N, H, dtype=torch.float32 if dhidden_fp32 else torch.bfloat16, device=dev)
+        dW = torch.empty_like(weight) if need_dweight else None
     if workspace is None:
         workspace = alloc_workspace(N, H, V, dev, budget_bytes=budget_bytes)
     check(lib().slf_lce_bwd(hidden.data_ptr(), weight.data_ptr(), targets.data_ptr(), rowstat.data_ptr(), N, H, V,
