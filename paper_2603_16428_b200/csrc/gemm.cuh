@@ -26,16 +26,25 @@
 
 namespace slf {
 
-constexpr int BM = 128;
-constexpr int BN = 256;
-constexpr int BK = 64;
-constexpr int STAGES = 4;
-constexpr int A_STAGE_BYTES = BM * BK * 2;  // 16 KiB
-constexpr int B_STAGE_BYTES = BN * BK * 2;  // 32 KiB
-constexpr int STAGE_BYTES = A_STAGE_BYTES + B_STAGE_BYTES;
+constexpr int BM = 128;  // accumulator rows per CTA (TMEM lanes)
+constexpr int BN = 256;  // accumulator columns (one tcgen05.mma N)
+constexpr int BK = 64;   // one 128-byte swizzle row of bf16
 constexpr int GEMM_THREADS = 256;
 constexpr uint32_t TMEM_COLS = 512;  // 2 x 256-column fp32 accumulators
-constexpr int GEMM_SMEM_BYTES = STAGES * STAGE_BYTES + 1024 /*align slack*/ + 256 /*barriers*/;
+
+// CG = 1: one CTA computes a 128 x 256 tile (cta_group::1).  CG = 2: a CTA pair (cluster of 2)
+// computes a 256 x 256 tile with cta_group::2 — each CTA stages its own 128 rows of A and half
+// (128 rows) of B, the leader issues the MMA, both CTAs hold 128 accumulator rows in TMEM.
+template <int CG>
+struct Cfg {
+  static constexpr int TILE_M = BM * CG;
+  static constexpr int B_ROWS = BN / CG;  // rows of B (N extent) staged per CTA
+  static constexpr int A_BYTES = BM * BK * 2;
+  static constexpr int B_BYTES = B_ROWS * BK * 2;
+  static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+  static constexpr int STAGES = CG == 2 ? 6 : 4;
+  static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 /*align slack*/ + 256 /*barriers*/;
+};
 
 enum EpiKind { EPI_STATS = 0, EPI_GRAD = 1, EPI_DW = 2, EPI_DX = 3, EPI_F32 = 4 };
 
@@ -76,8 +85,8 @@ __device__ __forceinline__ void tile_coords(int tile, const GemmArgs& a, int& m_
 }
 
 template <int EPI>
-__device__ __forceinline__ void epilogue_tile(const GemmArgs& a, uint32_t taddr, int m_blk, int n_blk, int row_in_tile) {
-  const int r = m_blk * BM + row_in_tile;
+__device__ __forceinline__ void epilogue_tile(const GemmArgs& a, uint32_t taddr, int row0, int n_blk, int row_in_tile) {
+  const int r = row0 + row_in_tile;
   const bool row_ok = r < a.M;
   const int n0 = n_blk * BN;
   const int ncols = min(BN, a.N - n0);
@@ -232,81 +241,113 @@ __device__ __forceinline__ void epilogue_tile(const GemmArgs& a, uint32_t taddr,
   }
 }
 
-template <int EPI, bool A_MN, bool B_MN>
+template <int EPI, bool A_MN, bool B_MN, int CG>
 __global__ void __launch_bounds__(GEMM_THREADS, 1)
     lce_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                     const GemmArgs args) {
+  using C = Cfg<CG>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sA = smem;
-  uint8_t* sB = smem + STAGES * A_STAGE_BYTES;
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE_BYTES);
-  uint64_t* empty = full + STAGES;
-  uint64_t* tfull = empty + STAGES;
+  uint8_t* sB = smem + C::STAGES * C::A_BYTES;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + C::STAGES * C::STAGE_BYTES);
+  uint64_t* empty = full + C::STAGES;
+  uint64_t* tfull = empty + C::STAGES;
   uint64_t* tempty = tfull + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
 
   const uint32_t warp = warp_idx_sync();
   const uint32_t lane = threadIdx.x & 31;
+  const uint32_t rank = CG == 2 ? cluster_ctarank() : 0;  // 0 = pair leader
+  const int first_tile = blockIdx.x / CG;
+  const int tile_stride = gridDim.x / CG;
 
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&tmA);
     tma_prefetch_desc(&tmB);
 #pragma unroll
-    for (int i = 0; i < STAGES; ++i) {
+    for (int i = 0; i < C::STAGES; ++i) {
       mbar_init(&full[i], 1);
       mbar_init(&empty[i], 1);
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(&tfull[i], 1);
-      mbar_init(&tempty[i], 4);  // one arrive per epilogue warp
+      mbar_init(&tempty[i], 4 * CG);  // one arrive per epilogue warp of every CTA of the pair
     }
     fence_barrier_init();
   }
-  if (warp == 2) tmem_alloc<TMEM_COLS>(tmem_slot);
+  if (warp == 2) {
+    if constexpr (CG == 2)
+      tmem_alloc_pair<TMEM_COLS>(tmem_slot);
+    else
+      tmem_alloc<TMEM_COLS>(tmem_slot);
+  }
   tc_fence_before();
-  __syncthreads();
+  if constexpr (CG == 2)
+    cluster_sync();
+  else
+    __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
   const int num_kb = (args.K + BK - 1) / BK;
 
   if (warp == 0) {
     if (lane == 0) {
-      // ===== TMA producer =====
+      // ===== TMA producer (both CTAs of a pair load their own halves) =====
       const uint64_t pol = policy_evict_normal();
       uint32_t stage = 0, phase = 0;
-      for (int tile = blockIdx.x; tile < args.num_tiles; tile += gridDim.x) {
+      for (int tile = first_tile; tile < args.num_tiles; tile += tile_stride) {
         int m_blk, n_blk;
         tile_coords(tile, args, m_blk, n_blk);
+        const int a_row = m_blk * C::TILE_M + (int)rank * BM;
+        const int b_row = n_blk * BN + (int)rank * C::B_ROWS;
         for (int kb = 0; kb < num_kb; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1);
-          mbar_arrive_expect_tx(&full[stage], STAGE_BYTES);
-          uint8_t* a_dst = sA + stage * A_STAGE_BYTES;
-          uint8_t* b_dst = sB + stage * B_STAGE_BYTES;
-          if constexpr (!A_MN) {
-            tma_load_2d(&tmA, &full[stage], a_dst, kb * BK, m_blk * BM, pol);
-          } else {
+          uint8_t* a_dst = sA + stage * C::A_BYTES;
+          uint8_t* b_dst = sB + stage * C::B_BYTES;
+          if constexpr (CG == 1) {
+            mbar_arrive_expect_tx(&full[stage], C::STAGE_BYTES);
+            if constexpr (!A_MN) {
+              tma_load_2d(&tmA, &full[stage], a_dst, kb * BK, a_row, pol);
+            } else {
 #pragma unroll
-            for (int j = 0; j < BM / 64; ++j)
-              tma_load_2d(&tmA, &full[stage], a_dst + j * 8192, m_blk * BM + j * 64, kb * BK, pol);
-          }
-          if constexpr (!B_MN) {
-            tma_load_2d(&tmB, &full[stage], b_dst, kb * BK, n_blk * BN, pol);
-          } else {
+              for (int j = 0; j < BM / 64; ++j) tma_load_2d(&tmA, &full[stage], a_dst + j * 8192, a_row + j * 64, kb * BK, pol);
+            }
+            if constexpr (!B_MN) {
+              tma_load_2d(&tmB, &full[stage], b_dst, kb * BK, b_row, pol);
+            } else {
 #pragma unroll
-            for (int j = 0; j < BN / 64; ++j)
-              tma_load_2d(&tmB, &full[stage], b_dst + j * 8192, n_blk * BN + j * 64, kb * BK, pol);
+              for (int j = 0; j < C::B_ROWS / 64; ++j)
+                tma_load_2d(&tmB, &full[stage], b_dst + j * 8192, b_row + j * 64, kb * BK, pol);
+            }
+          } else {
+            // Both CTAs' bytes complete on the leader's full barrier; only the leader arrives.
+            if (rank == 0) mbar_arrive_expect_tx(&full[stage], C::STAGE_BYTES * 2);
+            const uint32_t fb = mapa_shared(smem_u32(&full[stage]), 0);
+            if constexpr (!A_MN) {
+              tma_load_2d_pair(&tmA, fb, a_dst, kb * BK, a_row, pol);
+            } else {
+#pragma unroll
+              for (int j = 0; j < BM / 64; ++j) tma_load_2d_pair(&tmA, fb, a_dst + j * 8192, a_row + j * 64, kb * BK, pol);
+            }
+            if constexpr (!B_MN) {
+              tma_load_2d_pair(&tmB, fb, b_dst, kb * BK, b_row, pol);
+            } else {
+#pragma unroll
+              for (int j = 0; j < C::B_ROWS / 64; ++j)
+                tma_load_2d_pair(&tmB, fb, b_dst + j * 8192, b_row + j * 64, kb * BK, pol);
+            }
           }
-          if (++stage == STAGES) { stage = 0; phase ^= 1; }
+          if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
         }
       }
     }
   } else if (warp == 1) {
-    if (lane == 0) {
-      // ===== tcgen05.mma issuer =====
-      constexpr uint32_t idesc = make_idesc_bf16(BM, BN, A_MN, B_MN);
+    if (lane == 0 && rank == 0) {
+      // ===== tcgen05.mma issuer (pair leader only) =====
+      constexpr uint32_t idesc = make_idesc_bf16(C::TILE_M, BN, A_MN, B_MN);
       uint32_t stage = 0, phase = 0, local = 0;
-      for (int tile = blockIdx.x; tile < args.num_tiles; tile += gridDim.x, ++local) {
+      for (int tile = first_tile; tile < args.num_tiles; tile += tile_stride, ++local) {
         const uint32_t acc = local & 1, acc_phase = (local >> 1) & 1;
         mbar_wait(&tempty[acc], acc_phase ^ 1);
         tc_fence_after();
@@ -314,41 +355,61 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
         for (int kb = 0; kb < num_kb; ++kb) {
           mbar_wait(&full[stage], phase);
           tc_fence_after();
-          const uint32_t a_base = smem_u32(sA + stage * A_STAGE_BYTES);
-          const uint32_t b_base = smem_u32(sB + stage * B_STAGE_BYTES);
+          const uint32_t a_base = smem_u32(sA + stage * C::A_BYTES);
+          const uint32_t b_base = smem_u32(sB + stage * C::B_BYTES);
 #pragma unroll
           for (int k = 0; k < BK / 16; ++k) {
             const uint64_t ad = A_MN ? make_sdesc(a_base + k * 2048, 8192, 1024) : make_sdesc(a_base + k * 32, 16, 1024);
             const uint64_t bd = B_MN ? make_sdesc(b_base + k * 2048, 8192, 1024) : make_sdesc(b_base + k * 32, 16, 1024);
-            mma_bf16(d_tmem, ad, bd, idesc, (kb | k) != 0);
+            if constexpr (CG == 2)
+              mma_bf16_pair(d_tmem, ad, bd, idesc, (kb | k) != 0);
+            else
+              mma_bf16(d_tmem, ad, bd, idesc, (kb | k) != 0);
           }
-          mma_commit(&empty[stage]);  // frees the smem slot once these MMAs have read it
-          if (++stage == STAGES) { stage = 0; phase ^= 1; }
+          // frees the smem slot (in both CTAs) once these MMAs have read it
+          if constexpr (CG == 2)
+            mma_commit_pair(&empty[stage], 0x3);
+          else
+            mma_commit(&empty[stage]);
+          if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
         }
-        mma_commit(&tfull[acc]);  // accumulator ready for the epilogue
+        // accumulator ready for the epilogue warps (of both CTAs)
+        if constexpr (CG == 2)
+          mma_commit_pair(&tfull[acc], 0x3);
+        else
+          mma_commit(&tfull[acc]);
       }
     }
   } else if (warp >= 4) {
     // ===== epilogue: thread = TMEM lane = output row =====
     const uint32_t ew = warp - 4;
     uint32_t local = 0;
-    for (int tile = blockIdx.x; tile < args.num_tiles; tile += gridDim.x, ++local) {
+    for (int tile = first_tile; tile < args.num_tiles; tile += tile_stride, ++local) {
       int m_blk, n_blk;
       tile_coords(tile, args, m_blk, n_blk);
       const uint32_t acc = local & 1, acc_phase = (local >> 1) & 1;
       mbar_wait(&tfull[acc], acc_phase);
       tc_fence_after();
       const uint32_t taddr = tmem_base + ((ew * 32) << 16) + acc * BN;
-      epilogue_tile<EPI>(args, taddr, m_blk, n_blk, ew * 32 + lane);
+      epilogue_tile<EPI>(args, taddr, m_blk * C::TILE_M + (int)rank * BM, n_blk, ew * 32 + lane);
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(&tempty[acc]);
+      if (lane == 0) {
+        if constexpr (CG == 2)
+          mbar_arrive_cluster(mapa_shared(smem_u32(&tempty[acc]), 0));
+        else
+          mbar_arrive(&tempty[acc]);
+      }
     }
   }
   __syncthreads();
+  if constexpr (CG == 2) cluster_sync();
   if (warp == 2) {
     tc_fence_after();
-    tmem_dealloc<TMEM_COLS>(tmem_base);
+    if constexpr (CG == 2)
+      tmem_dealloc_pair<TMEM_COLS>(tmem_base);
+    else
+      tmem_dealloc<TMEM_COLS>(tmem_base);
   }
 }
 

@@ -8,6 +8,7 @@
 #include <algorithm>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <string>
@@ -89,7 +90,7 @@ struct DevInfo {
   int sms = 0;
   int major = 0;
   int minor = 0;
-  bool gemm_attr_set[32] = {};
+  bool gemm_attr_set[64] = {};
 };
 
 std::mutex g_mu;
@@ -152,32 +153,60 @@ slf_status tmap_mnmajor(CUtensorMap* m, const void* base, int64_t MN, int64_t K,
   return make_tmap(m, base, (uint64_t)MN, (uint64_t)K, (uint64_t)ld * 2, 64, 64);
 }
 
-template <int EPI, bool A_MN, bool B_MN>
-slf_status launch_gemm(DevInfo* dev, const CUtensorMap& ta, const CUtensorMap& tb, GemmArgs a, cudaStream_t s) {
+// CTA-group selection: 2 (CTA pairs, 256 x 256 tiles; default) or 1 (128 x 256), env SLF_CTA_GROUP.
+int cta_group() {
+  static int cg = [] {
+    const char* e = getenv("SLF_CTA_GROUP");
+    return (e && atoi(e) == 1) ? 1 : 2;
+  }();
+  return cg;
+}
+uint32_t b_box_rows() { return (uint32_t)(BN / cta_group()); }
+
+template <int EPI, bool A_MN, bool B_MN, int CG>
+slf_status launch_gemm_cg(DevInfo* dev, const CUtensorMap& ta, const CUtensorMap& tb, GemmArgs a, cudaStream_t s) {
+  using C = Cfg<CG>;
   constexpr int kKind = EPI == EPI_STATS ? SLF_PROF_GEMM_STATS
                         : EPI == EPI_GRAD ? SLF_PROF_GEMM_GRAD
                         : EPI == EPI_DW   ? SLF_PROF_GEMM_DW
                         : EPI == EPI_DX   ? SLF_PROF_GEMM_DX
                                           : SLF_PROF_GEMM_DEBUG;
-  constexpr int kId = EPI * 4 + (A_MN ? 2 : 0) + (B_MN ? 1 : 0);
-  auto kfn = lce_gemm_kernel<EPI, A_MN, B_MN>;
+  constexpr int kId = (EPI * 4 + (A_MN ? 2 : 0) + (B_MN ? 1 : 0)) * 2 + (CG - 1);
+  auto kfn = lce_gemm_kernel<EPI, A_MN, B_MN, CG>;
   {
     std::lock_guard<std::mutex> lk(g_mu);
     if (!dev->gemm_attr_set[kId]) {
-      SLF_CUDA(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, GEMM_SMEM_BYTES));
+      SLF_CUDA(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM_BYTES));
       dev->gemm_attr_set[kId] = true;
     }
   }
   if (a.M <= 0 || a.N <= 0 || a.K <= 0) return SLF_OK;
-  a.tiles_m = (a.M + BM - 1) / BM;
+  a.tiles_m = (a.M + C::TILE_M - 1) / C::TILE_M;
   a.tiles_n = (a.N + BN - 1) / BN;
   a.num_tiles = a.tiles_m * a.tiles_n;
-  a.group_m = std::min(a.tiles_m, 16);
-  const int grid = std::min(a.num_tiles, dev->sms);
+  a.group_m = std::min(a.tiles_m, 16 / CG);
+  const int units = std::min(a.num_tiles, dev->sms / CG);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)(units * CG));
+  cfg.blockDim = dim3(GEMM_THREADS);
+  cfg.dynamicSmemBytes = C::SMEM_BYTES;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = CG;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
   ProfScope ps(kKind, s, 2.0 * a.M * a.N * (double)a.K, 0.0);
-  kfn<<<grid, GEMM_THREADS, GEMM_SMEM_BYTES, s>>>(ta, tb, a);
-  SLF_CUDA(cudaGetLastError());
+  SLF_CUDA(cudaLaunchKernelEx(&cfg, kfn, ta, tb, a));
   return SLF_OK;
+}
+
+template <int EPI, bool A_MN, bool B_MN>
+slf_status launch_gemm(DevInfo* dev, const CUtensorMap& ta, const CUtensorMap& tb, GemmArgs a, cudaStream_t s) {
+  if (cta_group() == 2) return launch_gemm_cg<EPI, A_MN, B_MN, 2>(dev, ta, tb, a, s);
+  return launch_gemm_cg<EPI, A_MN, B_MN, 1>(dev, ta, tb, a, s);
 }
 
 // ---- planner (schedule R) ----------------------------------------------------------------------
@@ -272,7 +301,7 @@ slf_status phase_stats(Ctx& c, const void* X, const void* W, const int32_t* t, i
                        int64_t vocab_start, int32_t ignore_index, slf_shardstat* out) {
   CUtensorMap ta, tb;
   SLF_TRY(tmap_kmajor(&ta, X, H, N, H, BM));
-  SLF_TRY(tmap_kmajor(&tb, W, H, V_l, H, BN));
+  SLF_TRY(tmap_kmajor(&tb, W, H, V_l, H, b_box_rows()));
   GemmArgs a{};
   a.M = (int)N;
   a.N = (int)V_l;
@@ -329,7 +358,7 @@ slf_status phase_backward(Ctx& c, const void* X, const void* W, const slf_rowsta
       {  // G[rows, wc] = coef * (softmax - onehot), recomputed
         CUtensorMap ta, tb;
         SLF_TRY(tmap_kmajor(&ta, Xr, H, rows, H, BM));
-        SLF_TRY(tmap_kmajor(&tb, Wc, H, wc, H, BN));
+        SLF_TRY(tmap_kmajor(&tb, Wc, H, wc, H, b_box_rows()));
         GemmArgs a{};
         a.M = (int)rows;
         a.N = (int)wc;
@@ -587,7 +616,7 @@ slf_status slf_debug_gemm(const void* A, const void* B, float* D, int64_t M, int
   if (b_mn)
     SLF_TRY(tmap_mnmajor(&tb, B, N, K, N));
   else
-    SLF_TRY(tmap_kmajor(&tb, B, K, N, K, BN));
+    SLF_TRY(tmap_kmajor(&tb, B, K, N, K, b_box_rows()));
   GemmArgs a{};
   a.M = (int)M;
   a.N = (int)N;
