@@ -166,6 +166,7 @@ def main():
     ap.add_argument("--alpha", type=float, default=1.0)
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--budget", type=int, default=0, help="workspace budget bytes (0 = 5%% of N*V*2)")
+    ap.add_argument("--schedule", default="auto", choices=["auto", "R", "S"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     args = ap.parse_args()
@@ -210,7 +211,8 @@ def main():
 
     def step(Xs=X, ts=t):
         if g == 1:
-            slf.lce_fwd_bwd(Xs, W, ts, out=(loss, dX, dW), workspace=ws, budget_bytes=args.budget)
+            slf.lce_fwd_bwd(Xs, W, ts, out=(loss, dX, dW), workspace=ws, budget_bytes=args.budget,
+                            schedule=args.schedule)
             return loss
         st = slf.shard_stats(Xs, W, ts, v0, workspace=ws, budget_bytes=args.budget)
         dist.all_gather_into_tensor(stats_all.view(g * N, 4), st)
@@ -323,7 +325,8 @@ def main():
                    "V_per_gpu": V_l, "parallelism": f"vocab-sharded x{g}" if g > 1 else "single GPU",
                    "targets": args.dist, "logit_std": args.alpha, "ignore_frac": 0.05,
                    "l2": "inputs larger than L2 (W alone is %.2f GB vs 126 MB L2); no flush" % (V_l * H * 2 / 1e9),
-                   "plan": slf.plan_describe(N, H, V_l, budget_bytes=args.budget)},
+                   "plan": slf.plan_describe(N, H, V_l, budget_bytes=args.budget,
+                                             schedule=args.schedule if g == 1 else "R")},
         "tflops": tflops, "frac_of_peak_burst": tflops / peaks["burst"],
         "frac_of_peak_sustained": tflops / peaks["sustained"],
         "roofline": {"bound": "tensor", "kernel": dom_name, "achieved": achieved, "peak": peaks["sustained"],

@@ -58,10 +58,15 @@ typedef int slf_status;
 
 typedef enum { SLF_SUM = 0, SLF_MEAN = 1, SLF_NONE = 2 } slf_reduction;
 
-/* Schedules.  R: forward statistics pass over all
- * vocabulary tiles, then recompute the logits tile by tile in backward
- * (8·N·H·V tensor FLOPs, exact fp32 dhidden accumulation). */
-typedef enum { SLF_SCHED_AUTO = 0, SLF_SCHED_R = 1 } slf_schedule;
+/* Schedules.  R: forward statistics pass over all vocabulary
+ * tiles, then recompute the logits tile by tile in backward (8·N·H·V tensor
+ * FLOPs; the only schedule of the split / shard entry points).  S (fused call
+ * only): per row chunk, one forward pass whose epilogue stashes
+ * p~ = bf16(exp(z - m_tile)), then dX and dW straight from the stash, the
+ * one-hot term applied exactly (6·N·H·V).  AUTO: S when its plan fits the
+ * budget, else R; slf_lce_workspace_bytes(AUTO) is enough for every entry
+ * point. */
+typedef enum { SLF_SCHED_AUTO = 0, SLF_SCHED_R = 1, SLF_SCHED_S = 2 } slf_schedule;
 
 /* Per-row statistics record ("RowStat", 16 bytes) exchanged between the
  * forward and backward halves: lse2 = lse * log2(e); coef as above;
@@ -183,7 +188,7 @@ slf_status slf_lce_dx_finalize(const float* dhidden_fp32, const slf_rowstat* row
  * writes per-kind totals into HOST arrays of SLF_PROF_KINDS entries: device milliseconds, launches,
  * algorithmic FLOPs (2*M*N*K of each GEMM launch) and algorithmic bytes (aux kernels: bytes they
  * must read + write).  Kinds: */
-#define SLF_PROF_KINDS 10
+#define SLF_PROF_KINDS 16
 #define SLF_PROF_GEMM_STATS 0 /* forward logits tile GEMM + stats epilogue          */
 #define SLF_PROF_GEMM_GRAD 1  /* backward recompute GEMM + dlogit (G) epilogue      */
 #define SLF_PROF_GEMM_DW 2    /* dW = G^T X                                         */
@@ -193,6 +198,11 @@ slf_status slf_lce_dx_finalize(const float* dhidden_fp32, const slf_rowstat* row
 #define SLF_PROF_LOCAL_COMBINE 6
 #define SLF_PROF_FINAL_COMBINE 7
 #define SLF_PROF_DX_FINALIZE 8
+#define SLF_PROF_GEMM_GROUP 9         /* one launch holding the dW and dX GEMMs of a chunk */
+#define SLF_PROF_COMBINE_TRANSFORM 10 /* schedule S: lse, loss, stash -> G_P in place     */
+#define SLF_PROF_CSR 11               /* schedule S: target CSR (stable counting sort)    */
+#define SLF_PROF_ONEHOT 12            /* schedule S: dW[v] -= coef * sum x_i               */
+#define SLF_PROF_LOSS_REDUCE 13       /* schedule S: deterministic loss sum               */
 slf_status slf_profile_begin(void);
 slf_status slf_profile_end(double* ms, int64_t* launches, double* flops, double* bytes);
 

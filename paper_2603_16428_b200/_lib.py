@@ -16,14 +16,14 @@ SLF_OK = 0
 STATUS_NAMES = {0: "SLF_OK", 1: "SLF_ERR_ARG", 2: "SLF_ERR_ALIGN", 3: "SLF_ERR_WORKSPACE", 4: "SLF_ERR_CUDA",
                 5: "SLF_ERR_UNSUPPORTED", 6: "SLF_ERR_UNIMPLEMENTED"}
 REDUCTIONS = {"sum": 0, "mean": 1, "none": 2}
-SCHEDULES = {"auto": 0, "R": 1}
+SCHEDULES = {"auto": 0, "R": 1, "S": 2}
 
 # Every symbol include/slf_lce.h declares.
 EXPORTS = ["slf_lce_version", "slf_last_error_string", "slf_lce_workspace_bytes", "slf_lce_plan_describe",
            "slf_lce_fwd_bwd", "slf_lce_fwd", "slf_lce_fwd_shard_stats", "slf_lce_stats_combine", "slf_lce_bwd",
            "slf_lce_status", "slf_debug_gemm", "slf_lce_dx_finalize", "slf_profile_begin", "slf_profile_end"]
 PROF_KINDS = ["gemm_stats", "gemm_grad", "gemm_dw", "gemm_dx", "gemm_debug", "prep", "local_combine", "final_combine",
-              "dx_finalize", "unused"]
+              "dx_finalize", "gemm_group", "combine_transform", "csr", "onehot", "loss_reduce", "k14", "k15"]
 
 _lock = threading.Lock()
 _lib = None

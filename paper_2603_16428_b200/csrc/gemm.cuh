@@ -46,24 +46,27 @@ struct Cfg {
   static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 /*align slack*/ + 256 /*barriers*/;
 };
 
-enum EpiKind { EPI_STATS = 0, EPI_GRAD = 1, EPI_DW = 2, EPI_DX = 3, EPI_F32 = 4 };
+enum EpiKind { EPI_STATS = 0, EPI_GRAD = 1, EPI_DW = 2, EPI_DX = 3, EPI_F32 = 4, EPI_STASH = 5, EPI_DXS = 6 };
 
-// DX epilogue modes.
+// DX epilogue modes (schedule R).
 enum DxMode { DX_STORE_F32 = 0, DX_ACC_F32 = 1, DX_ACC_FINAL_BF16 = 2, DX_STORE_FINAL_BF16 = 3 };
 
 struct GemmArgs {
   int M, N, K;
   int tiles_m, tiles_n, num_tiles, group_m;
-  // EPI_STATS
+  // EPI_STATS / EPI_STASH
   const int32_t* targets;  // row 0 of the GEMM
   int64_t tcol0;           // target id that maps to GEMM column 0 (vocab_start + chunk start)
   int32_t ignore_index;
   float2* partials;        // [tiles_n][M]
   float* zt;               // [M]
-  // EPI_GRAD / EPI_DX
-  const slf_rowstat* rowstat;  // row 0 of the GEMM (GRAD, DX)
+  // EPI_GRAD / EPI_DX / EPI_DXS
+  const slf_rowstat* rowstat;  // row 0 of the GEMM
   int64_t col0;                // chunk start relative to the shard (GRAD: compare with rowstat.tloc)
   float grad_scale;
+  int rows_buf;                // GRAD: rows [M, rows_buf) of the G buffer are written as zeros
+  const uint16_t* wrow;        // DXS: the shard's W (one-hot gather W[tloc]); row stride ld_w
+  int64_t ld_w;
   // outputs
   void* out;
   int64_t ld_out;
@@ -74,7 +77,7 @@ struct GemmArgs {
 
 __device__ __forceinline__ void tile_coords(int tile, const GemmArgs& a, int& m_blk, int& n_blk) {
   // Grouped raster: walk group_m row tiles down before stepping to the next column tile, so one
-  // wave of 148 tiles shares a few A row-panels and B column-panels in L2.
+  // wave of tiles shares a few A row-panels and B column-panels in L2.
   const int per_group = a.group_m * a.tiles_n;
   const int g = tile / per_group;
   const int first_m = g * a.group_m;
@@ -128,6 +131,105 @@ __device__ __forceinline__ void epilogue_tile(const GemmArgs& a, uint32_t taddr,
       a.partials[(size_t)n_blk * a.M + r] = make_float2(mx, s);
       if (tl >= 0) a.zt[r] = zt;
     }
+  } else if constexpr (EPI == EPI_STASH) {
+    // Schedule S forward: (m, s) per (row, tile) as EPI_STATS, plus the bf16 stash
+    // p~ = exp(z - m_tile) of the whole tile (no recompute later).
+    int tl = -1;
+    if (row_ok) {
+      const int32_t t = a.targets[r];
+      const int64_t loc = (int64_t)t - a.tcol0 - n0;
+      tl = (t != a.ignore_index && loc >= 0 && loc < ncols) ? (int)loc : -1;
+    }
+    float mx = -INFINITY;
+#pragma unroll 1
+    for (int c = 0; c < BN / 32; ++c) {
+      if (c * 32 >= ncols) break;
+      tmem_ld32(taddr + c * 32, v);
+      tmem_ld_wait();
+#pragma unroll
+      for (int i = 0; i < 32; ++i)
+        if (c * 32 + i < ncols) mx = fmaxf(mx, __uint_as_float(v[i]));
+    }
+    const float mb = mx * LOG2E;
+    float s = 0.f, zt = 0.f;
+    uint16_t* out = reinterpret_cast<uint16_t*>(a.out) + (size_t)r * a.ld_out + n0;
+#pragma unroll 1
+    for (int c = 0; c < BN / 32; ++c) {
+      if (c * 32 >= ncols) break;
+      tmem_ld32(taddr + c * 32, v);
+      tmem_ld_wait();
+      uint32_t p[16];
+#pragma unroll
+      for (int i = 0; i < 32; i += 2) {
+        const float z0 = __uint_as_float(v[i]), z1 = __uint_as_float(v[i + 1]);
+        float e0 = ex2(fmaf(z0, LOG2E, -mb)), e1 = ex2(fmaf(z1, LOG2E, -mb));
+        e0 = (c * 32 + i < ncols) ? e0 : 0.f;
+        e1 = (c * 32 + i + 1 < ncols) ? e1 : 0.f;
+        s += e0 + e1;
+        zt = (c * 32 + i == tl) ? z0 : zt;
+        zt = (c * 32 + i + 1 == tl) ? z1 : zt;
+        p[i / 2] = pack_bf16x2(e0, e1);
+      }
+      if (row_ok) {
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+          if (c * 32 + q * 8 < ncols)
+            *reinterpret_cast<uint4*>(out + c * 32 + q * 8) = make_uint4(p[4 * q], p[4 * q + 1], p[4 * q + 2], p[4 * q + 3]);
+      }
+    }
+    if (row_ok) {
+      a.partials[(size_t)n_blk * a.M + r] = make_float2(mx, s);
+      if (tl >= 0) a.zt[r] = zt;
+    }
+  } else if constexpr (EPI == EPI_DXS) {
+    // Schedule S dX: acc = G_P W (softmax term); subtract the one-hot term coef * W[t] exactly in
+    // fp32 (only for targets inside this shard); ignored rows are +0.0.
+    float coef = 0.f;
+    int tl = -1;
+    bool valid = false;
+    if (row_ok) {
+      const slf_rowstat rs = a.rowstat[r];
+      coef = rs.coef * a.grad_scale;
+      tl = rs.tloc;
+      valid = rs.valid != 0;
+    }
+    const uint16_t* wt = a.wrow + (size_t)(tl >= 0 ? tl : 0) * a.ld_w + n0;
+#pragma unroll 1
+    for (int c = 0; c < BN / 32; ++c) {
+      if (c * 32 >= ncols) break;
+      tmem_ld32(taddr + c * 32, v);
+      tmem_ld_wait();
+      if (row_ok) {
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const int j = c * 32 + q * 8;
+          if (j < ncols) {
+            float f[8];
+#pragma unroll
+            for (int e = 0; e < 8; ++e) f[e] = __uint_as_float(v[q * 8 + e]);
+            if (tl >= 0) {
+              const uint4 w = *reinterpret_cast<const uint4*>(wt + j);
+              f[0] -= coef * bf16lo_to_f32(w.x); f[1] -= coef * bf16hi_to_f32(w.x);
+              f[2] -= coef * bf16lo_to_f32(w.y); f[3] -= coef * bf16hi_to_f32(w.y);
+              f[4] -= coef * bf16lo_to_f32(w.z); f[5] -= coef * bf16hi_to_f32(w.z);
+              f[6] -= coef * bf16lo_to_f32(w.w); f[7] -= coef * bf16hi_to_f32(w.w);
+            }
+            if (!valid)
+#pragma unroll
+              for (int e = 0; e < 8; ++e) f[e] = 0.f;
+            if (a.mode == 0) {
+              uint16_t* o = reinterpret_cast<uint16_t*>(a.out) + (size_t)r * a.ld_out + n0 + j;
+              *reinterpret_cast<uint4*>(o) = make_uint4(pack_bf16x2(f[0], f[1]), pack_bf16x2(f[2], f[3]),
+                                                        pack_bf16x2(f[4], f[5]), pack_bf16x2(f[6], f[7]));
+            } else {
+              float4* o = reinterpret_cast<float4*>(reinterpret_cast<float*>(a.out) + (size_t)r * a.ld_out + n0 + j);
+              o[0] = make_float4(f[0], f[1], f[2], f[3]);
+              o[1] = make_float4(f[4], f[5], f[6], f[7]);
+            }
+          }
+        }
+      }
+    }
   } else if constexpr (EPI == EPI_GRAD) {
     float coef = 0.f, lse2 = 0.f;
     int tl = -1;
@@ -154,10 +256,11 @@ __device__ __forceinline__ void epilogue_tile(const GemmArgs& a, uint32_t taddr,
         g1 = j1 < ncols ? g1 : 0.f;
         p[i / 2] = pack_bf16x2(g0, g1);
       }
-      if (row_ok) {
+      if (r < a.rows_buf) {  // rows past M (inside the buffer) are written as zeros
         uint4* dst = reinterpret_cast<uint4*>(out + c * 32);
 #pragma unroll
-        for (int q = 0; q < 4; ++q) dst[q] = make_uint4(p[4 * q], p[4 * q + 1], p[4 * q + 2], p[4 * q + 3]);
+        for (int q = 0; q < 4; ++q)
+          dst[q] = row_ok ? make_uint4(p[4 * q], p[4 * q + 1], p[4 * q + 2], p[4 * q + 3]) : make_uint4(0u, 0u, 0u, 0u);
       }
     }
   } else if constexpr (EPI == EPI_DW) {
@@ -241,10 +344,67 @@ __device__ __forceinline__ void epilogue_tile(const GemmArgs& a, uint32_t taddr,
   }
 }
 
-template <int EPI, bool A_MN, bool B_MN, int CG>
+// Runtime epilogue dispatch (one problem of a group decides per tile).
+__device__ __forceinline__ void epilogue_dispatch(int epi, const GemmArgs& a, uint32_t taddr, int row0, int n_blk,
+                                                  int row_in_tile) {
+  switch (epi) {
+    case EPI_STATS: epilogue_tile<EPI_STATS>(a, taddr, row0, n_blk, row_in_tile); break;
+    case EPI_GRAD: epilogue_tile<EPI_GRAD>(a, taddr, row0, n_blk, row_in_tile); break;
+    case EPI_DW: epilogue_tile<EPI_DW>(a, taddr, row0, n_blk, row_in_tile); break;
+    case EPI_DX: epilogue_tile<EPI_DX>(a, taddr, row0, n_blk, row_in_tile); break;
+    case EPI_STASH: epilogue_tile<EPI_STASH>(a, taddr, row0, n_blk, row_in_tile); break;
+    case EPI_DXS: epilogue_tile<EPI_DXS>(a, taddr, row0, n_blk, row_in_tile); break;
+    default: epilogue_tile<EPI_F32>(a, taddr, row0, n_blk, row_in_tile); break;
+  }
+}
+
+// ---- grouped persistent kernel ---------------------------------------------------------------
+// Up to MAXP independent GEMM problems share one launch (e.g. the dW and dX GEMMs of one chunk):
+// problem p owns global tiles [tile_begin[p], tile_begin[p+1]).  Each unit (CTA or CTA pair) walks
+// either a host-built list (sched: balanced by K-blocks, longest first) or tiles u, u+units, ...
+constexpr int MAXP = 2;
+
+struct Prob {
+  GemmArgs a;
+  int epi, a_mn, b_mn, tile_begin;
+};
+
+struct GroupArgs {
+  Prob p[MAXP];
+  int nprob;
+  int num_tiles;
+  const int* sched;  // [units][sched_stride] tile ids, -1 terminated (nullptr: round robin)
+  int sched_stride;
+};
+
+struct TMaps {
+  CUtensorMap m[2 * MAXP];  // A, B of each problem
+};
+
+struct TileIter {
+  const GroupArgs& g;
+  int unit, units, i;
+  __device__ TileIter(const GroupArgs& g_, int unit_, int units_) : g(g_), unit(unit_), units(units_), i(0) {}
+  __device__ __forceinline__ int next() {
+    int t;
+    if (g.sched) {
+      t = i < g.sched_stride ? __ldg(g.sched + (size_t)unit * g.sched_stride + i) : -1;
+    } else {
+      t = unit + i * units;
+      if (t >= g.num_tiles) t = -1;
+    }
+    ++i;
+    return t;
+  }
+};
+
+__device__ __forceinline__ int prob_of(const GroupArgs& g, int tile) {
+  return (g.nprob > 1 && tile >= g.p[1].tile_begin) ? 1 : 0;
+}
+
+template <int CG>
 __global__ void __launch_bounds__(GEMM_THREADS, 1)
-    lce_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-                    const GemmArgs args) {
+    lce_group_kernel(const __grid_constant__ TMaps tm, const __grid_constant__ GroupArgs g) {
   using C = Cfg<CG>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -259,12 +419,11 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
   const uint32_t warp = warp_idx_sync();
   const uint32_t lane = threadIdx.x & 31;
   const uint32_t rank = CG == 2 ? cluster_ctarank() : 0;  // 0 = pair leader
-  const int first_tile = blockIdx.x / CG;
-  const int tile_stride = gridDim.x / CG;
+  const int unit = blockIdx.x / CG;
+  const int units = gridDim.x / CG;
 
   if (warp == 0 && lane == 0) {
-    tma_prefetch_desc(&tmA);
-    tma_prefetch_desc(&tmB);
+    for (int i = 0; i < 2 * g.nprob; ++i) tma_prefetch_desc(&tm.m[i]);
 #pragma unroll
     for (int i = 0; i < C::STAGES; ++i) {
       mbar_init(&full[i], 1);
@@ -289,53 +448,59 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
-  const int num_kb = (args.K + BK - 1) / BK;
 
   if (warp == 0) {
     if (lane == 0) {
       // ===== TMA producer (both CTAs of a pair load their own halves) =====
       const uint64_t pol = policy_evict_normal();
       uint32_t stage = 0, phase = 0;
-      for (int tile = first_tile; tile < args.num_tiles; tile += tile_stride) {
+      TileIter it(g, unit, units);
+      for (int tile = it.next(); tile >= 0; tile = it.next()) {
+        const int pi = prob_of(g, tile);
+        const Prob& P = g.p[pi];
+        const CUtensorMap* tA = &tm.m[2 * pi];
+        const CUtensorMap* tB = &tm.m[2 * pi + 1];
         int m_blk, n_blk;
-        tile_coords(tile, args, m_blk, n_blk);
+        tile_coords(tile - P.tile_begin, P.a, m_blk, n_blk);
         const int a_row = m_blk * C::TILE_M + (int)rank * BM;
         const int b_row = n_blk * BN + (int)rank * C::B_ROWS;
+        const int num_kb = (P.a.K + BK - 1) / BK;
+        const bool a_mn = P.a_mn, b_mn = P.b_mn;
         for (int kb = 0; kb < num_kb; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1);
           uint8_t* a_dst = sA + stage * C::A_BYTES;
           uint8_t* b_dst = sB + stage * C::B_BYTES;
           if constexpr (CG == 1) {
             mbar_arrive_expect_tx(&full[stage], C::STAGE_BYTES);
-            if constexpr (!A_MN) {
-              tma_load_2d(&tmA, &full[stage], a_dst, kb * BK, a_row, pol);
+            if (!a_mn) {
+              tma_load_2d(tA, &full[stage], a_dst, kb * BK, a_row, pol);
             } else {
 #pragma unroll
-              for (int j = 0; j < BM / 64; ++j) tma_load_2d(&tmA, &full[stage], a_dst + j * 8192, a_row + j * 64, kb * BK, pol);
+              for (int j = 0; j < BM / 64; ++j) tma_load_2d(tA, &full[stage], a_dst + j * 8192, a_row + j * 64, kb * BK, pol);
             }
-            if constexpr (!B_MN) {
-              tma_load_2d(&tmB, &full[stage], b_dst, kb * BK, b_row, pol);
+            if (!b_mn) {
+              tma_load_2d(tB, &full[stage], b_dst, kb * BK, b_row, pol);
             } else {
 #pragma unroll
               for (int j = 0; j < C::B_ROWS / 64; ++j)
-                tma_load_2d(&tmB, &full[stage], b_dst + j * 8192, b_row + j * 64, kb * BK, pol);
+                tma_load_2d(tB, &full[stage], b_dst + j * 8192, b_row + j * 64, kb * BK, pol);
             }
           } else {
             // Both CTAs' bytes complete on the leader's full barrier; only the leader arrives.
             if (rank == 0) mbar_arrive_expect_tx(&full[stage], C::STAGE_BYTES * 2);
             const uint32_t fb = mapa_shared(smem_u32(&full[stage]), 0);
-            if constexpr (!A_MN) {
-              tma_load_2d_pair(&tmA, fb, a_dst, kb * BK, a_row, pol);
+            if (!a_mn) {
+              tma_load_2d_pair(tA, fb, a_dst, kb * BK, a_row, pol);
             } else {
 #pragma unroll
-              for (int j = 0; j < BM / 64; ++j) tma_load_2d_pair(&tmA, fb, a_dst + j * 8192, a_row + j * 64, kb * BK, pol);
+              for (int j = 0; j < BM / 64; ++j) tma_load_2d_pair(tA, fb, a_dst + j * 8192, a_row + j * 64, kb * BK, pol);
             }
-            if constexpr (!B_MN) {
-              tma_load_2d_pair(&tmB, fb, b_dst, kb * BK, b_row, pol);
+            if (!b_mn) {
+              tma_load_2d_pair(tB, fb, b_dst, kb * BK, b_row, pol);
             } else {
 #pragma unroll
               for (int j = 0; j < C::B_ROWS / 64; ++j)
-                tma_load_2d_pair(&tmB, fb, b_dst + j * 8192, b_row + j * 64, kb * BK, pol);
+                tma_load_2d_pair(tB, fb, b_dst + j * 8192, b_row + j * 64, kb * BK, pol);
             }
           }
           if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
@@ -345,9 +510,13 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
   } else if (warp == 1) {
     if (lane == 0 && rank == 0) {
       // ===== tcgen05.mma issuer (pair leader only) =====
-      constexpr uint32_t idesc = make_idesc_bf16(C::TILE_M, BN, A_MN, B_MN);
       uint32_t stage = 0, phase = 0, local = 0;
-      for (int tile = first_tile; tile < args.num_tiles; tile += tile_stride, ++local) {
+      TileIter it(g, unit, units);
+      for (int tile = it.next(); tile >= 0; tile = it.next(), ++local) {
+        const Prob& P = g.p[prob_of(g, tile)];
+        const bool a_mn = P.a_mn, b_mn = P.b_mn;
+        const uint32_t idesc = make_idesc_bf16(C::TILE_M, BN, a_mn, b_mn);
+        const int num_kb = (P.a.K + BK - 1) / BK;
         const uint32_t acc = local & 1, acc_phase = (local >> 1) & 1;
         mbar_wait(&tempty[acc], acc_phase ^ 1);
         tc_fence_after();
@@ -359,8 +528,8 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
           const uint32_t b_base = smem_u32(sB + stage * C::B_BYTES);
 #pragma unroll
           for (int k = 0; k < BK / 16; ++k) {
-            const uint64_t ad = A_MN ? make_sdesc(a_base + k * 2048, 8192, 1024) : make_sdesc(a_base + k * 32, 16, 1024);
-            const uint64_t bd = B_MN ? make_sdesc(b_base + k * 2048, 8192, 1024) : make_sdesc(b_base + k * 32, 16, 1024);
+            const uint64_t ad = a_mn ? make_sdesc(a_base + k * 2048, 8192, 1024) : make_sdesc(a_base + k * 32, 16, 1024);
+            const uint64_t bd = b_mn ? make_sdesc(b_base + k * 2048, 8192, 1024) : make_sdesc(b_base + k * 32, 16, 1024);
             if constexpr (CG == 2)
               mma_bf16_pair(d_tmem, ad, bd, idesc, (kb | k) != 0);
             else
@@ -384,14 +553,16 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     // ===== epilogue: thread = TMEM lane = output row =====
     const uint32_t ew = warp - 4;
     uint32_t local = 0;
-    for (int tile = first_tile; tile < args.num_tiles; tile += tile_stride, ++local) {
+    TileIter it(g, unit, units);
+    for (int tile = it.next(); tile >= 0; tile = it.next(), ++local) {
+      const Prob& P = g.p[prob_of(g, tile)];
       int m_blk, n_blk;
-      tile_coords(tile, args, m_blk, n_blk);
+      tile_coords(tile - P.tile_begin, P.a, m_blk, n_blk);
       const uint32_t acc = local & 1, acc_phase = (local >> 1) & 1;
       mbar_wait(&tfull[acc], acc_phase);
       tc_fence_after();
       const uint32_t taddr = tmem_base + ((ew * 32) << 16) + acc * BN;
-      epilogue_tile<EPI>(args, taddr, m_blk * C::TILE_M + (int)rank * BM, n_blk, ew * 32 + lane);
+      epilogue_dispatch(P.epi, P.a, taddr, m_blk * C::TILE_M + (int)rank * BM, n_blk, ew * 32 + lane);
       tc_fence_before();
       __syncwarp();
       if (lane == 0) {

@@ -1,0 +1,218 @@
+// s_kernels.cuh — HBM-bound kernels of schedule S (no recompute).
+//   combine_transform : per row of a chunk: merge the (m_t, s_t) tile statistics into lse, the row
+//                       loss and RowStat, then rescale the bf16 stash p~ = exp(z - m_t) in place
+//                       into G_P = coef * exp(z - lse)  (softmax term only; the one-hot term is
+//                       applied exactly elsewhere: dX epilogue and onehot_kernel).
+//   csr_*             : stable counting sort of the valid in-shard tokens by target id (the
+//                       "target CSR"): counts, exclusive scan + hit list, rank by brute force over
+//                       earlier tokens (deterministic, no atomics on positions), scatter.
+//   onehot_kernel     : dW[v] -= coef * sum_{i in CSR[v]} x_i, summed in fp32 in token order.
+//   loss_reduce       : deterministic sum of the per-row losses.
+#pragma once
+#include <cstdint>
+
+#include "../../include/slf_lce.h"
+#include "aux_kernels.cuh"
+#include "ptx.cuh"
+
+namespace slf {
+
+__device__ __forceinline__ float coef_of(int reduction, float scale, unsigned long long n_valid) {
+  return (reduction == SLF_MEAN) ? (n_valid ? scale / (float)n_valid : 0.f) : scale;
+}
+
+// One block (256 threads) per row of the chunk.  Fixed-order reductions (deterministic).
+__global__ void __launch_bounds__(256) combine_transform_kernel(
+    const float2* __restrict__ partials, int tiles, int rows, const float* __restrict__ zt,
+    const int32_t* __restrict__ t, int64_t V, int64_t ld_stash, int32_t ignore_index, int reduction, float scale,
+    float grad_scale, const WsHeader* __restrict__ hdr, float* __restrict__ loss_rows,
+    slf_rowstat* __restrict__ rowstat, uint16_t* __restrict__ stash) {
+  extern __shared__ float r_t[];  // [tiles]
+  __shared__ float red[256];
+  const int i = blockIdx.x;
+  const int tid = threadIdx.x;
+  float m = -INFINITY;
+  for (int k = tid; k < tiles; k += 256) m = fmaxf(m, partials[(size_t)k * rows + i].x);
+  red[tid] = m;
+  __syncthreads();
+  for (int o = 128; o > 0; o >>= 1) {
+    if (tid < o) red[tid] = fmaxf(red[tid], red[tid + o]);
+    __syncthreads();
+  }
+  const float M = red[0];
+  __syncthreads();
+  float s = 0.f;
+  for (int k = tid; k < tiles; k += 256) {
+    const float2 p = partials[(size_t)k * rows + i];
+    s += p.y * ex2((p.x - M) * LOG2E);
+  }
+  red[tid] = s;
+  __syncthreads();
+  for (int o = 128; o > 0; o >>= 1) {
+    if (tid < o) red[tid] += red[tid + o];
+    __syncthreads();
+  }
+  const float lse = M + logf(red[0]);
+  const int32_t tt = t[i];
+  const bool valid = tt != ignore_index;
+  const bool bad = valid && (tt < 0 || (int64_t)tt >= V);
+  const float coef = (valid && !bad) ? coef_of(reduction, scale, hdr->n_valid) : 0.f;
+  if (tid == 0) {
+    float l = valid ? (lse - zt[i]) : 0.f;
+    if (bad) l = __int_as_float(0x7fc00000);
+    loss_rows[i] = l;
+    rowstat[i] = slf_rowstat{lse * LOG2E, coef, (valid && !bad) ? tt : -1, valid ? 1 : 0};
+  }
+  const float cg = coef * grad_scale;
+  const float lse2 = lse * LOG2E;
+  for (int k = tid; k < tiles; k += 256) r_t[k] = cg * ex2(partials[(size_t)k * rows + i].x * LOG2E - lse2);
+  __syncthreads();
+  // G_P = p~ * r_t, in place, 8 bf16 per 16-byte access.
+  uint4* row = reinterpret_cast<uint4*>(stash + (size_t)i * ld_stash);
+  const int64_t groups = (V + 7) / 8;
+  for (int64_t q = tid; q < groups; q += 256) {
+    const float r = r_t[(q * 8) / 256];
+    uint4 w = row[q];
+    w.x = pack_bf16x2(bf16lo_to_f32(w.x) * r, bf16hi_to_f32(w.x) * r);
+    w.y = pack_bf16x2(bf16lo_to_f32(w.y) * r, bf16hi_to_f32(w.y) * r);
+    w.z = pack_bf16x2(bf16lo_to_f32(w.z) * r, bf16hi_to_f32(w.z) * r);
+    w.w = pack_bf16x2(bf16lo_to_f32(w.w) * r, bf16hi_to_f32(w.w) * r);
+    row[q] = w;
+  }
+}
+
+// ---- target CSR ------------------------------------------------------------------------------
+__device__ __forceinline__ bool in_shard(int32_t tt, int32_t ignore_index, int64_t vocab_start, int64_t V_l) {
+  const int64_t loc = (int64_t)tt - vocab_start;
+  return tt != ignore_index && loc >= 0 && loc < V_l;
+}
+
+__global__ void csr_zero_kernel(int32_t* __restrict__ cnt, int64_t n) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    cnt[i] = 0;
+}
+
+__global__ void csr_count_kernel(const int32_t* __restrict__ t, int64_t N, int32_t ignore_index, int64_t vocab_start,
+                                 int64_t V_l, int32_t* __restrict__ cnt) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < N && in_shard(t[i], ignore_index, vocab_start, V_l)) atomicAdd(&cnt[t[i] - vocab_start], 1);
+}
+
+// Single block: off = exclusive_scan(cnt) over V_l entries (off[V_l] = total); hit list of rows with
+// cnt > 0 in increasing row order; n_hits stored in off[V_l + 1].
+__global__ void __launch_bounds__(1024) csr_scan_kernel(const int32_t* __restrict__ cnt, int64_t V_l,
+                                                       int32_t* __restrict__ off, int32_t* __restrict__ hits) {
+  __shared__ int32_t sc[1024], sh[1024];
+  const int tid = threadIdx.x;
+  const int64_t per = (V_l + 1023) / 1024;
+  const int64_t b = tid * per, e = min(V_l, b + per);
+  int32_t s = 0, h = 0;
+  for (int64_t v = b; v < e; ++v) {
+    s += cnt[v];
+    h += cnt[v] > 0;
+  }
+  sc[tid] = s;
+  sh[tid] = h;
+  __syncthreads();
+  for (int o = 1; o < 1024; o <<= 1) {  // inclusive Hillis-Steele scan (fixed order, integer)
+    const int32_t a = tid >= o ? sc[tid - o] : 0, c = tid >= o ? sh[tid - o] : 0;
+    __syncthreads();
+    sc[tid] += a;
+    sh[tid] += c;
+    __syncthreads();
+  }
+  int32_t run = tid ? sc[tid - 1] : 0, hr = tid ? sh[tid - 1] : 0;
+  for (int64_t v = b; v < e; ++v) {
+    off[v] = run;
+    run += cnt[v];
+    if (cnt[v] > 0) hits[hr++] = (int32_t)v;
+  }
+  if (tid == 1023) {
+    off[V_l] = sc[1023];
+    off[V_l + 1] = sh[1023];
+  }
+}
+
+// rank_i = #{j < i : t_j == t_i, both in shard}; idx[off[t_i] + rank_i] = i.  Brute force over
+// earlier tokens through shared-memory tiles (only for targets that occur more than once).
+__global__ void __launch_bounds__(256) csr_scatter_kernel(const int32_t* __restrict__ t, int64_t N,
+                                                         int32_t ignore_index, int64_t vocab_start, int64_t V_l,
+                                                         const int32_t* __restrict__ cnt,
+                                                         const int32_t* __restrict__ off, int32_t* __restrict__ idx) {
+  __shared__ int32_t tile[2048];
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  int32_t key = -1;
+  bool need = false;
+  if (i < N && in_shard(t[i], ignore_index, vocab_start, V_l)) {
+    key = t[i];
+    need = cnt[key - vocab_start] > 1;
+  }
+  const int any_need = __syncthreads_or(need);
+  int32_t rank = 0;
+  if (any_need) {
+    const int64_t end = (int64_t)blockIdx.x * blockDim.x + blockDim.x;  // tokens before this block's last
+    for (int64_t j0 = 0; j0 < end && j0 < N; j0 += 2048) {
+      for (int k = threadIdx.x; k < 2048; k += blockDim.x) tile[k] = (j0 + k < N) ? t[j0 + k] : ignore_index;
+      __syncthreads();
+      if (need) {
+        const int64_t rem = i - j0;
+        const int lim = rem < 2048 ? (int)rem : 2048;
+        for (int k = 0; k < lim; ++k) rank += (tile[k] == key);
+      }
+      __syncthreads();
+    }
+  }
+  if (key >= 0) idx[off[key - vocab_start] + rank] = (int32_t)i;  // key >= 0 <=> valid and in shard
+}
+
+// dW[v] = bf16( f32(dW[v]) - coef * sum_{i in CSR[v]} x_i ), sums in fp32 in token order.
+// grid.x over hit rows (bounded by min(N, V_l); n_hits in off[V_l + 1]), grid.y over 1024-column slabs.
+__global__ void __launch_bounds__(128) onehot_kernel(const uint16_t* __restrict__ X, int64_t H,
+                                                    const int32_t* __restrict__ off, const int32_t* __restrict__ idx,
+                                                    const int32_t* __restrict__ hits, int64_t V_l, int reduction,
+                                                    float scale, float grad_scale, const WsHeader* __restrict__ hdr,
+                                                    uint16_t* __restrict__ dW) {
+  const int64_t k = blockIdx.x;
+  if (k >= off[V_l + 1]) return;
+  const int32_t v = hits[k];
+  const int64_t col = ((int64_t)blockIdx.y * 128 + threadIdx.x) * 8;
+  if (col >= H) return;
+  float acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  for (int32_t p = off[v]; p < off[v + 1]; ++p) {
+    const uint4 x = *reinterpret_cast<const uint4*>(X + (size_t)idx[p] * H + col);
+    acc[0] += bf16lo_to_f32(x.x); acc[1] += bf16hi_to_f32(x.x);
+    acc[2] += bf16lo_to_f32(x.y); acc[3] += bf16hi_to_f32(x.y);
+    acc[4] += bf16lo_to_f32(x.z); acc[5] += bf16hi_to_f32(x.z);
+    acc[6] += bf16lo_to_f32(x.w); acc[7] += bf16hi_to_f32(x.w);
+  }
+  const float c = coef_of(reduction, scale, hdr->n_valid) * grad_scale;
+  uint4* d = reinterpret_cast<uint4*>(dW + (size_t)v * H + col);
+  const uint4 o = *d;
+  *d = make_uint4(pack_bf16x2(bf16lo_to_f32(o.x) - c * acc[0], bf16hi_to_f32(o.x) - c * acc[1]),
+                  pack_bf16x2(bf16lo_to_f32(o.y) - c * acc[2], bf16hi_to_f32(o.y) - c * acc[3]),
+                  pack_bf16x2(bf16lo_to_f32(o.z) - c * acc[4], bf16hi_to_f32(o.z) - c * acc[5]),
+                  pack_bf16x2(bf16lo_to_f32(o.w) - c * acc[6], bf16hi_to_f32(o.w) - c * acc[7]));
+}
+
+// Single block: deterministic sum (fixed strided subsets + fixed tree, fp64) of the row losses.
+__global__ void __launch_bounds__(1024) loss_reduce_kernel(const float* __restrict__ loss_rows, int64_t N,
+                                                          int reduction, const WsHeader* __restrict__ hdr,
+                                                          float* __restrict__ loss_out) {
+  __shared__ double sh[1024];
+  double a = 0.0;
+  for (int64_t i = threadIdx.x; i < N; i += 1024) a += (double)loss_rows[i];
+  sh[threadIdx.x] = a;
+  __syncthreads();
+  for (int o = 512; o > 0; o >>= 1) {
+    if ((int)threadIdx.x < o) sh[threadIdx.x] += sh[threadIdx.x + o];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    double tot = sh[0];
+    const unsigned long long nv = hdr->n_valid;
+    if (reduction == SLF_MEAN) tot = nv ? tot / (double)nv : 0.0;
+    loss_out[0] = hdr->bad > 0 ? __int_as_float(0x7fc00000) : (float)tot;
+  }
+}
+
+}  // namespace slf

@@ -17,6 +17,7 @@
 #include "../../include/slf_lce.h"
 #include "aux_kernels.cuh"
 #include "gemm.cuh"
+#include "s_kernels.cuh"
 
 using namespace slf;
 
@@ -163,29 +164,97 @@ int cta_group() {
 }
 uint32_t b_box_rows() { return (uint32_t)(BN / cta_group()); }
 
-template <int EPI, bool A_MN, bool B_MN, int CG>
-slf_status launch_gemm_cg(DevInfo* dev, const CUtensorMap& ta, const CUtensorMap& tb, GemmArgs a, cudaStream_t s) {
-  using C = Cfg<CG>;
-  constexpr int kKind = EPI == EPI_STATS ? SLF_PROF_GEMM_STATS
-                        : EPI == EPI_GRAD ? SLF_PROF_GEMM_GRAD
-                        : EPI == EPI_DW   ? SLF_PROF_GEMM_DW
-                        : EPI == EPI_DX   ? SLF_PROF_GEMM_DX
-                                          : SLF_PROF_GEMM_DEBUG;
-  constexpr int kId = (EPI * 4 + (A_MN ? 2 : 0) + (B_MN ? 1 : 0)) * 2 + (CG - 1);
-  auto kfn = lce_gemm_kernel<EPI, A_MN, B_MN, CG>;
-  {
-    std::lock_guard<std::mutex> lk(g_mu);
-    if (!dev->gemm_attr_set[kId]) {
-      SLF_CUDA(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM_BYTES));
-      dev->gemm_attr_set[kId] = true;
-    }
+// One GEMM problem of a launch: operand tensor maps, extents and epilogue arguments.
+struct ProbSpec {
+  CUtensorMap ta, tb;
+  GemmArgs a{};
+  int epi = EPI_F32;
+  bool a_mn = false, b_mn = false;
+};
+
+int prof_kind_of(int epi) {
+  switch (epi) {
+    case EPI_STATS:
+    case EPI_STASH: return SLF_PROF_GEMM_STATS;
+    case EPI_GRAD: return SLF_PROF_GEMM_GRAD;
+    case EPI_DW: return SLF_PROF_GEMM_DW;
+    case EPI_DX:
+    case EPI_DXS: return SLF_PROF_GEMM_DX;
+    default: return SLF_PROF_GEMM_DEBUG;
   }
-  if (a.M <= 0 || a.N <= 0 || a.K <= 0) return SLF_OK;
-  a.tiles_m = (a.M + C::TILE_M - 1) / C::TILE_M;
+}
+
+void finish_geometry(GemmArgs& a, int cg) {
+  const int tile_m = BM * cg;
+  a.tiles_m = (a.M + tile_m - 1) / tile_m;
   a.tiles_n = (a.N + BN - 1) / BN;
   a.num_tiles = a.tiles_m * a.tiles_n;
-  a.group_m = std::min(a.tiles_m, 16 / CG);
-  const int units = std::min(a.num_tiles, dev->sms / CG);
+  a.group_m = std::max(1, std::min(a.tiles_m, 16 / cg));
+}
+
+// Longest-processing-time-first assignment of the tiles of a group to `units` persistent units:
+// tiles sorted by K-blocks (descending, stable by id), each given to the least-loaded unit.
+// Returns a [units][stride] table of tile ids, -1 padded.
+std::vector<int> lpt_table(const ProbSpec* ps, int n, int units, int* stride) {
+  std::vector<std::pair<int, int>> tiles;  // (kblocks, id)
+  int id = 0;
+  for (int p = 0; p < n; ++p) {
+    const int kb = (ps[p].a.K + BK - 1) / BK;
+    for (int t = 0; t < ps[p].a.num_tiles; ++t) tiles.push_back({kb, id++});
+  }
+  std::stable_sort(tiles.begin(), tiles.end(), [](auto& x, auto& y) { return x.first > y.first; });
+  std::vector<std::vector<int>> lists(units);
+  std::vector<long long> load(units, 0);
+  for (auto& t : tiles) {
+    int best = 0;
+    for (int u = 1; u < units; ++u)
+      if (load[u] < load[best]) best = u;
+    lists[best].push_back(t.second);
+    load[best] += t.first + 4;  // + a small per-tile epilogue/pipeline cost
+  }
+  size_t mx = 1;
+  for (auto& l : lists) mx = std::max(mx, l.size() + 1);
+  *stride = (int)mx;
+  std::vector<int> tab((size_t)units * mx, -1);
+  for (int u = 0; u < units; ++u)
+    for (size_t i = 0; i < lists[u].size(); ++i) tab[(size_t)u * mx + i] = lists[u][i];
+  return tab;
+}
+
+template <int CG>
+slf_status launch_group_cg(DevInfo* dev, ProbSpec* ps, int n, cudaStream_t s, const int* sched, int sched_stride,
+                           int prof_kind) {
+  using C = Cfg<CG>;
+  auto kfn = lce_group_kernel<CG>;
+  {
+    std::lock_guard<std::mutex> lk(g_mu);
+    if (!dev->gemm_attr_set[CG]) {
+      SLF_CUDA(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM_BYTES));
+      dev->gemm_attr_set[CG] = true;
+    }
+  }
+  TMaps tm;
+  GroupArgs g{};
+  int total = 0;
+  double flops = 0;
+  int np = 0;
+  for (int p = 0; p < n; ++p) {
+    GemmArgs a = ps[p].a;
+    if (a.M <= 0 || a.N <= 0 || a.K <= 0) continue;
+    finish_geometry(a, CG);
+    tm.m[2 * np] = ps[p].ta;
+    tm.m[2 * np + 1] = ps[p].tb;
+    g.p[np] = Prob{a, ps[p].epi, ps[p].a_mn ? 1 : 0, ps[p].b_mn ? 1 : 0, total};
+    total += a.num_tiles;
+    flops += 2.0 * a.M * a.N * (double)a.K;
+    ++np;
+  }
+  if (np == 0) return SLF_OK;
+  g.nprob = np;
+  g.num_tiles = total;
+  g.sched = sched;
+  g.sched_stride = sched_stride;
+  const int units = sched ? dev->sms / CG : std::min(total, dev->sms / CG);
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((unsigned)(units * CG));
   cfg.blockDim = dim3(GEMM_THREADS);
@@ -198,25 +267,44 @@ slf_status launch_gemm_cg(DevInfo* dev, const CUtensorMap& ta, const CUtensorMap
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  ProfScope ps(kKind, s, 2.0 * a.M * a.N * (double)a.K, 0.0);
-  SLF_CUDA(cudaLaunchKernelEx(&cfg, kfn, ta, tb, a));
+  ProfScope pscope(prof_kind >= 0 ? prof_kind : prof_kind_of(g.p[0].epi), s, flops, 0.0);
+  SLF_CUDA(cudaLaunchKernelEx(&cfg, kfn, tm, g));
   return SLF_OK;
+}
+
+slf_status launch_group(DevInfo* dev, ProbSpec* ps, int n, cudaStream_t s, const int* sched = nullptr,
+                        int sched_stride = 0, int prof_kind = -1) {
+  if (cta_group() == 2) return launch_group_cg<2>(dev, ps, n, s, sched, sched_stride, prof_kind);
+  return launch_group_cg<1>(dev, ps, n, s, sched, sched_stride, prof_kind);
 }
 
 template <int EPI, bool A_MN, bool B_MN>
 slf_status launch_gemm(DevInfo* dev, const CUtensorMap& ta, const CUtensorMap& tb, GemmArgs a, cudaStream_t s) {
-  if (cta_group() == 2) return launch_gemm_cg<EPI, A_MN, B_MN, 2>(dev, ta, tb, a, s);
-  return launch_gemm_cg<EPI, A_MN, B_MN, 1>(dev, ta, tb, a, s);
+  ProbSpec p;
+  p.ta = ta;
+  p.tb = tb;
+  p.a = a;
+  p.epi = EPI;
+  p.a_mn = A_MN;
+  p.b_mn = B_MN;
+  return launch_group(dev, &p, 1, s);
 }
 
 // ---- planner (schedule R) ----------------------------------------------------------------------
 inline size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
 
 struct Plan {
+  int sched = SLF_SCHED_R;
+  // schedule R: row block R x vocab chunk Cv
   int64_t R = 0, Cv = 0, nR = 0, nC = 0;
-  size_t off_rowstat = 0, off_shard = 0, off_zt = 0, off_union = 0, off_dxacc = 0;
+  // schedule S: row chunk C (whole vocabulary stashed per chunk)
+  int64_t C = 0, nCh = 0, ld_stash = 0;
+  size_t off_sched = 0, off_rowstat = 0, off_shard = 0, off_zt = 0, off_union = 0, off_dxacc = 0;
+  size_t off_loss = 0, off_cnt = 0, off_off = 0, off_hits = 0, off_idx = 0, off_part = 0, off_stash = 0;
   size_t fwd_bytes = 0, bwd_bytes = 0, total = 0;
 };
+
+constexpr size_t SCHED_ARENA_BYTES = 256 * 1024;
 
 size_t default_budget(int64_t N, int64_t V) {
   const size_t five = (size_t)(0.05 * (double)N * (double)V * 2.0);
@@ -227,7 +315,9 @@ bool plan_r(int64_t N, int64_t H, int64_t V, size_t budget, Plan* out) {
   if (N < 1 || H < 8 || V < 1) return false;
   if (budget == 0) budget = default_budget(N, V);
   Plan p;
-  p.off_rowstat = WS_HEADER_BYTES;
+  p.sched = SLF_SCHED_R;
+  p.off_sched = WS_HEADER_BYTES;
+  p.off_rowstat = p.off_sched + SCHED_ARENA_BYTES;
   p.off_shard = align_up(p.off_rowstat + (size_t)N * 16, 1024);
   p.off_zt = align_up(p.off_shard + (size_t)N * 16, 1024);
   p.off_union = align_up(p.off_zt + (size_t)N * 4, 1024);
@@ -238,7 +328,7 @@ bool plan_r(int64_t N, int64_t H, int64_t V, size_t budget, Plan* out) {
   double best = 1e300;
   bool found = false;
   for (int64_t nR = 1; nR <= 64; ++nR) {
-    const int64_t R = (int64_t)align_up((size_t)((N + nR - 1) / nR), BM);
+    const int64_t R = (int64_t)align_up((size_t)((N + nR - 1) / nR), 256);
     if (nR > 1 && (nR - 1) * R >= N) continue;  // empty trailing block
     const size_t dx = align_up((size_t)R * H * 4, 1024);
     if (p.off_union + dx >= budget) continue;
@@ -251,7 +341,7 @@ bool plan_r(int64_t N, int64_t H, int64_t V, size_t budget, Plan* out) {
     // Cost model in bytes of extra HBM traffic: dW bf16 RMW per extra row block, dX fp32 RMW per
     // extra vocab chunk, and ~5 us of launch/tail per GEMM launch expressed as bytes at 6.5 TB/s.
     const double cost = (double)(nRr - 1) * V * H * 4 + (double)nRr * (nC - 1) * R * H * 8 +
-                        (double)nRr * nC * 3 * 5e-6 * 6.5e12;
+                        (double)nRr * nC * 2 * 5e-6 * 6.5e12;
     if (cost < best) {
       best = cost;
       p.R = R;
@@ -267,6 +357,43 @@ bool plan_r(int64_t N, int64_t H, int64_t V, size_t budget, Plan* out) {
   p.bwd_bytes = g_bytes + (size_t)p.R * H * 4;
   p.total = p.off_union + std::max(p.fwd_bytes, p.bwd_bytes);
   if (p.total > budget) return false;
+  *out = p;
+  return true;
+}
+
+// Schedule S layout: header | sched arena | RowStat [N] | z_t [N] | row losses [N] | CSR counts
+// [V+2] | CSR offsets [V+2] | hit rows [min(N,V)] | CSR token idx [N] | tile partials [tiles][C] |
+// stash [C][ld_stash] bf16.  C = the largest multiple of 256 rows that fits the budget.
+bool plan_s(int64_t N, int64_t H, int64_t V, size_t budget, Plan* out) {
+  if (N < 1 || H < 8 || V < 1) return false;
+  if (budget == 0) budget = default_budget(N, V);
+  Plan p;
+  p.sched = SLF_SCHED_S;
+  p.off_sched = WS_HEADER_BYTES;
+  p.off_rowstat = p.off_sched + SCHED_ARENA_BYTES;
+  p.off_zt = align_up(p.off_rowstat + (size_t)N * 16, 1024);
+  p.off_loss = align_up(p.off_zt + (size_t)N * 4, 1024);
+  p.off_cnt = align_up(p.off_loss + (size_t)N * 4, 1024);
+  p.off_off = align_up(p.off_cnt + (size_t)(V + 2) * 4, 1024);
+  p.off_hits = align_up(p.off_off + (size_t)(V + 2) * 4, 1024);
+  p.off_idx = align_up(p.off_hits + (size_t)std::min(N, V) * 4, 1024);
+  p.off_part = align_up(p.off_idx + (size_t)N * 4, 1024);
+  const int64_t tiles_v = (V + BN - 1) / BN;
+  p.ld_stash = (int64_t)align_up((size_t)V, 8);
+  const int64_t Nmax = (int64_t)align_up((size_t)N, 256);
+  int64_t best = 0;
+  for (int64_t C = 256; C <= Nmax; C += 256) {
+    const size_t part = align_up((size_t)tiles_v * C * 8, 1024);
+    const size_t tot = p.off_part + part + (size_t)C * p.ld_stash * 2;
+    if (tot <= budget) best = C;
+    else break;
+  }
+  if (best == 0) return false;
+  p.C = best;
+  p.nCh = (N + best - 1) / best;
+  p.off_stash = p.off_part + align_up((size_t)tiles_v * best * 8, 1024);
+  p.total = p.off_stash + (size_t)best * p.ld_stash * 2;
+  p.fwd_bytes = p.total - p.off_part;
   *out = p;
   return true;
 }
@@ -295,6 +422,28 @@ struct Ctx {
 WsHeader* hdr_of(uint8_t* ws) { return reinterpret_cast<WsHeader*>(ws); }
 double* block_sums_of(uint8_t* ws) { return reinterpret_cast<double*>(ws + 256); }
 
+// Per-call arena of LPT tile tables (uploaded once per call into the workspace).
+struct SchedArena {
+  std::vector<int> host;
+  std::vector<std::pair<size_t, int>> tables;  // (offset in ints, stride)
+  int add(const ProbSpec* ps, int n, int units) {
+    int stride = 0;
+    std::vector<int> t = lpt_table(ps, n, units, &stride);
+    tables.push_back({host.size(), stride});
+    host.insert(host.end(), t.begin(), t.end());
+    return (int)tables.size() - 1;
+  }
+  slf_status upload(Ctx& c) {
+    if (host.empty()) return SLF_OK;
+    if (host.size() * 4 > SCHED_ARENA_BYTES) return fail(SLF_ERR_WORKSPACE, "tile schedule arena overflow");
+    SLF_CUDA(cudaMemcpyAsync(c.ws + c.plan.off_sched, host.data(), host.size() * 4, cudaMemcpyHostToDevice, c.s));
+    return SLF_OK;
+  }
+  const int* dev(Ctx& c, int k) const {
+    return reinterpret_cast<const int*>(c.ws + c.plan.off_sched) + tables[k].first;
+  }
+};
+
 // Forward statistics of one shard: EPI_STATS GEMM over all (row tile, vocab tile), then the
 // per-row merge into ShardStat.
 slf_status phase_stats(Ctx& c, const void* X, const void* W, const int32_t* t, int64_t N, int64_t H, int64_t V_l,
@@ -320,16 +469,19 @@ slf_status phase_stats(Ctx& c, const void* X, const void* W, const int32_t* t, i
   return SLF_OK;
 }
 
+slf_status launch_prep(Ctx& c, const int32_t* t, int64_t N, int32_t ignore_index, int64_t V_global) {
+  ProfScope ps(SLF_PROF_PREP, c.s, 0.0, (double)N * 4);
+  prep_targets_kernel<<<1, 1024, 0, c.s>>>(t, N, ignore_index, V_global, hdr_of(c.ws));
+  SLF_CUDA(cudaGetLastError());
+  return SLF_OK;
+}
+
 slf_status phase_combine(Ctx& c, const slf_shardstat* st, int g, const int32_t* t, int64_t N, int64_t vocab_start,
                          int64_t V_l, int64_t V_global, int32_t ignore_index, int reduction, float scale,
                          float* loss_out, slf_rowstat* rowstat) {
   const unsigned blocks = (unsigned)((N + 255) / 256);
   if (blocks > (unsigned)MAX_LOSS_BLOCKS * 4) return fail(SLF_ERR_ARG, "N too large for the loss reduction");
-  {
-    ProfScope ps(SLF_PROF_PREP, c.s, 0.0, (double)N * 4);
-    prep_targets_kernel<<<1, 1024, 0, c.s>>>(t, N, ignore_index, V_global, hdr_of(c.ws));
-  }
-  SLF_CUDA(cudaGetLastError());
+  SLF_TRY(launch_prep(c, t, N, ignore_index, V_global));
   ProfScope ps(SLF_PROF_FINAL_COMBINE, c.s, 0.0, (double)N * (g * 16.0 + 4 + 16 + 4));
   final_combine_kernel<<<blocks, 256, 0, c.s>>>(st, g, t, N, vocab_start, V_l, V_global, ignore_index, reduction,
                                                 scale, loss_out, rowstat, hdr_of(c.ws), block_sums_of(c.ws));
@@ -338,7 +490,8 @@ slf_status phase_combine(Ctx& c, const slf_shardstat* st, int g, const int32_t* 
 }
 
 // Backward (schedule R): for each row block r, for each vocab chunk c: recompute the logits tile
-// by tile and form G (EPI_GRAD) -> dW_c (+)= G^T X_r (EPI_DW) -> dX_r (+)= G W_c (EPI_DX).
+// by tile and form G (EPI_GRAD), then ONE grouped launch of dW_c (+)= G^T X_r (EPI_DW) and
+// dX_r (+)= G W_c (EPI_DX) with an LPT tile table (no wave quantisation between the two).
 slf_status phase_backward(Ctx& c, const void* X, const void* W, const slf_rowstat* rowstat, int64_t N, int64_t H,
                           int64_t V_l, float grad_scale, void* dX, int dX_fp32, void* dW) {
   if (!dX && !dW) return SLF_OK;
@@ -346,6 +499,78 @@ slf_status phase_backward(Ctx& c, const void* X, const void* W, const slf_rowsta
   uint8_t* G = c.ws + p.off_union;
   float* dxacc = reinterpret_cast<float*>(c.ws + p.off_dxacc);
   const int64_t ldG = p.Cv;
+  const int cg = cta_group();
+  const int units = c.dev->sms / cg;
+
+  auto build = [&](int64_t rb, int64_t cb, ProbSpec* ps, int* n) -> slf_status {
+    const int64_t r0 = rb * p.R, rows = std::min(p.R, N - r0);
+    const int64_t c0 = cb * p.Cv, wc = std::min(p.Cv, V_l - c0);
+    const uint8_t* Xr = reinterpret_cast<const uint8_t*>(X) + (size_t)r0 * H * 2;
+    const uint8_t* Wc = reinterpret_cast<const uint8_t*>(W) + (size_t)c0 * H * 2;
+    *n = 0;
+    if (dW) {  // dW[c0:c0+wc] (+)= G^T X_r : A = G^T (MN-major), B = X_r (MN-major)
+      ProbSpec& q = ps[(*n)++];
+      SLF_TRY(tmap_mnmajor(&q.ta, G, wc, rows, ldG));
+      SLF_TRY(tmap_mnmajor(&q.tb, Xr, H, rows, H));
+      q.epi = EPI_DW;
+      q.a_mn = q.b_mn = true;
+      q.a = GemmArgs{};
+      q.a.M = (int)wc;
+      q.a.N = (int)H;
+      q.a.K = (int)rows;
+      q.a.out = reinterpret_cast<uint8_t*>(dW) + (size_t)c0 * H * 2;
+      q.a.ld_out = H;
+      q.a.mode = rb > 0 ? 1 : 0;
+      finish_geometry(q.a, cg);
+    }
+    if (dX) {  // dX_r (+)= G W_c : A = G (K-major), B = W_c (MN-major)
+      ProbSpec& q = ps[(*n)++];
+      SLF_TRY(tmap_kmajor(&q.ta, G, wc, rows, ldG, BM));
+      SLF_TRY(tmap_mnmajor(&q.tb, Wc, H, wc, H));
+      q.epi = EPI_DX;
+      q.a_mn = false;
+      q.b_mn = true;
+      GemmArgs a{};
+      a.M = (int)rows;
+      a.N = (int)H;
+      a.K = (int)wc;
+      a.rowstat = rowstat + r0;
+      if (dX_fp32) {
+        a.out = reinterpret_cast<float*>(dX) + (size_t)r0 * H;
+        a.ld_out = H;
+        a.mode = cb == 0 ? DX_STORE_F32 : DX_ACC_F32;
+      } else {
+        a.out = dxacc;
+        a.ld_out = H;
+        a.out2 = reinterpret_cast<uint8_t*>(dX) + (size_t)r0 * H * 2;
+        a.ld_out2 = H;
+        a.mode = p.nC == 1 ? DX_STORE_FINAL_BF16
+                 : cb == 0 ? DX_STORE_F32
+                 : cb == p.nC - 1 ? DX_ACC_FINAL_BF16
+                                  : DX_ACC_F32;
+      }
+      finish_geometry(a, cg);
+      q.a = a;
+    }
+    return SLF_OK;
+  };
+
+  // LPT tables for the (at most 4) distinct (rows, wc) shapes, uploaded once.
+  SchedArena arena;
+  std::vector<std::pair<std::pair<int64_t, int64_t>, int>> keys;
+  for (int64_t rb = 0; rb < p.nR; ++rb)
+    for (int64_t cb = 0; cb < p.nC; ++cb) {
+      const auto key = std::make_pair(std::min(p.R, N - rb * p.R), std::min(p.Cv, V_l - cb * p.Cv));
+      bool have = false;
+      for (auto& k : keys) have |= k.first == key;
+      if (have) continue;
+      ProbSpec ps[2];
+      int n = 0;
+      SLF_TRY(build(rb, cb, ps, &n));
+      keys.push_back({key, arena.add(ps, n, units)});
+    }
+  SLF_TRY(arena.upload(c));
+
   for (int64_t rb = 0; rb < p.nR; ++rb) {
     const int64_t r0 = rb * p.R;
     const int64_t rows = std::min(p.R, N - r0);
@@ -368,60 +593,174 @@ slf_status phase_backward(Ctx& c, const void* X, const void* W, const slf_rowsta
         a.grad_scale = grad_scale;
         a.out = G;
         a.ld_out = ldG;
+        a.rows_buf = (int)p.R;
         SLF_TRY((launch_gemm<EPI_GRAD, false, false>(c.dev, ta, tb, a, c.s)));
       }
-      if (dW) {  // dW[c0:c0+wc] (+)= G^T X_r : A = G^T (MN-major), B = X_r (MN-major)
-        CUtensorMap ta, tb;
-        SLF_TRY(tmap_mnmajor(&ta, G, wc, rows, ldG));
-        SLF_TRY(tmap_mnmajor(&tb, Xr, H, rows, H));
-        GemmArgs a{};
-        a.M = (int)wc;
-        a.N = (int)H;
-        a.K = (int)rows;
-        a.out = reinterpret_cast<uint8_t*>(dW) + (size_t)c0 * H * 2;
-        a.ld_out = H;
-        a.mode = rb > 0 ? 1 : 0;
-        SLF_TRY((launch_gemm<EPI_DW, true, true>(c.dev, ta, tb, a, c.s)));
-      }
-      if (dX) {  // dX_r (+)= G W_c : A = G (K-major), B = W_c (MN-major)
-        CUtensorMap ta, tb;
-        SLF_TRY(tmap_kmajor(&ta, G, wc, rows, ldG, BM));
-        SLF_TRY(tmap_mnmajor(&tb, Wc, H, wc, H));
-        GemmArgs a{};
-        a.M = (int)rows;
-        a.N = (int)H;
-        a.K = (int)wc;
-        a.rowstat = rowstat + r0;
-        if (dX_fp32) {
-          a.out = reinterpret_cast<float*>(dX) + (size_t)r0 * H;
-          a.ld_out = H;
-          a.mode = cb == 0 ? DX_STORE_F32 : DX_ACC_F32;
-        } else {
-          a.out = dxacc;
-          a.ld_out = H;
-          a.out2 = reinterpret_cast<uint8_t*>(dX) + (size_t)r0 * H * 2;
-          a.ld_out2 = H;
-          if (p.nC == 1)
-            a.mode = DX_STORE_FINAL_BF16;
-          else if (cb == 0)
-            a.mode = DX_STORE_F32;
-          else if (cb == p.nC - 1)
-            a.mode = DX_ACC_FINAL_BF16;
-          else
-            a.mode = DX_ACC_F32;
-        }
-        SLF_TRY((launch_gemm<EPI_DX, false, true>(c.dev, ta, tb, a, c.s)));
-      }
+      ProbSpec ps[2];
+      int n = 0;
+      SLF_TRY(build(rb, cb, ps, &n));
+      int k = 0;
+      const auto key = std::make_pair(rows, wc);
+      for (auto& kk : keys)
+        if (kk.first == key) k = kk.second;
+      SLF_TRY(launch_group(c.dev, ps, n, c.s, arena.dev(c, k), arena.tables[k].second,
+                           n == 2 ? SLF_PROF_GEMM_GROUP : -1));
     }
   }
   return SLF_OK;
 }
 
-slf_status setup(Ctx& c, int64_t N, int64_t H, int64_t V_l, size_t budget, void* ws, size_t ws_bytes, void* stream) {
+// Schedule S (single GPU): per row chunk, ONE forward GEMM whose epilogue keeps the tile
+// statistics and stashes p~ = bf16(exp(z - m_tile)); combine + in-place transform to the softmax
+// term G_P; ONE grouped launch of dX_chunk = G_P W (- coef W[t], exact, epilogue) and
+// dW (+)= G_P^T X_chunk; finally dW[v] -= coef sum_{t_i = v} x_i from the target CSR.  No logits
+// are recomputed: 6 N H V tensor FLOPs.
+slf_status phase_s(Ctx& c, const void* X, const void* W, const int32_t* t, int64_t N, int64_t H, int64_t V,
+                   int32_t ignore_index, int reduction, float scale, float* loss_out, void* dX, void* dW) {
+  const Plan& p = c.plan;
+  const int cg = cta_group();
+  const int units = c.dev->sms / cg;
+  slf_rowstat* rs = reinterpret_cast<slf_rowstat*>(c.ws + p.off_rowstat);
+  float* zt = reinterpret_cast<float*>(c.ws + p.off_zt);
+  float* loss_rows = reduction == SLF_NONE ? loss_out : reinterpret_cast<float*>(c.ws + p.off_loss);
+  int32_t* cnt = reinterpret_cast<int32_t*>(c.ws + p.off_cnt);
+  int32_t* off = reinterpret_cast<int32_t*>(c.ws + p.off_off);
+  int32_t* hits = reinterpret_cast<int32_t*>(c.ws + p.off_hits);
+  int32_t* idx = reinterpret_cast<int32_t*>(c.ws + p.off_idx);
+  float2* part = reinterpret_cast<float2*>(c.ws + p.off_part);
+  uint16_t* stash = reinterpret_cast<uint16_t*>(c.ws + p.off_stash);
+  const int tiles_v = (int)((V + BN - 1) / BN);
+
+  SLF_TRY(launch_prep(c, t, N, ignore_index, V));
+  if (dW) {
+    ProfScope ps(SLF_PROF_CSR, c.s, 0.0, (double)V * 12 + (double)N * 12);
+    csr_zero_kernel<<<std::min<int64_t>((V + 2 + 255) / 256, 1024), 256, 0, c.s>>>(cnt, V + 2);
+    csr_count_kernel<<<(unsigned)((N + 255) / 256), 256, 0, c.s>>>(t, N, ignore_index, 0, V, cnt);
+    csr_scan_kernel<<<1, 1024, 0, c.s>>>(cnt, V, off, hits);
+    csr_scatter_kernel<<<(unsigned)((N + 255) / 256), 256, 0, c.s>>>(t, N, ignore_index, 0, V, cnt, off, idx);
+    SLF_CUDA(cudaGetLastError());
+  }
+
+  auto build_bwd = [&](int64_t ch, ProbSpec* ps, int* n) -> slf_status {
+    const int64_t r0 = ch * p.C, rows = std::min(p.C, N - r0);
+    const uint8_t* Xr = reinterpret_cast<const uint8_t*>(X) + (size_t)r0 * H * 2;
+    *n = 0;
+    if (dX) {  // dX_chunk = G_P W : A = G_P (K-major over V), B = W (MN-major)
+      ProbSpec& q = ps[(*n)++];
+      SLF_TRY(tmap_kmajor(&q.ta, stash, V, rows, p.ld_stash, BM));
+      SLF_TRY(tmap_mnmajor(&q.tb, W, H, V, H));
+      q.epi = EPI_DXS;
+      q.a_mn = false;
+      q.b_mn = true;
+      q.a = GemmArgs{};
+      q.a.M = (int)rows;
+      q.a.N = (int)H;
+      q.a.K = (int)V;
+      q.a.rowstat = rs + r0;
+      q.a.grad_scale = 1.0f;
+      q.a.wrow = reinterpret_cast<const uint16_t*>(W);
+      q.a.ld_w = H;
+      q.a.out = reinterpret_cast<uint8_t*>(dX) + (size_t)r0 * H * 2;
+      q.a.ld_out = H;
+      q.a.mode = 0;
+      finish_geometry(q.a, cg);
+    }
+    if (dW) {  // dW (+)= G_P^T X_chunk : A = G_P^T (MN-major), B = X_chunk (MN-major)
+      ProbSpec& q = ps[(*n)++];
+      SLF_TRY(tmap_mnmajor(&q.ta, stash, V, rows, p.ld_stash));
+      SLF_TRY(tmap_mnmajor(&q.tb, Xr, H, rows, H));
+      q.epi = EPI_DW;
+      q.a_mn = q.b_mn = true;
+      q.a = GemmArgs{};
+      q.a.M = (int)V;
+      q.a.N = (int)H;
+      q.a.K = (int)rows;
+      q.a.out = dW;
+      q.a.ld_out = H;
+      q.a.mode = ch > 0 ? 1 : 0;
+      finish_geometry(q.a, cg);
+    }
+    return SLF_OK;
+  };
+
+  SchedArena arena;
+  int k_full = -1, k_last = -1;
+  if (dX || dW) {
+    ProbSpec ps[2];
+    int n = 0;
+    SLF_TRY(build_bwd(0, ps, &n));
+    k_full = arena.add(ps, n, units);
+    if (N % p.C) {
+      SLF_TRY(build_bwd(p.nCh - 1, ps, &n));
+      k_last = arena.add(ps, n, units);
+    }
+    SLF_TRY(arena.upload(c));
+  }
+
+  for (int64_t ch = 0; ch < p.nCh; ++ch) {
+    const int64_t r0 = ch * p.C, rows = std::min(p.C, N - r0);
+    {  // forward: statistics + p~ stash
+      CUtensorMap ta, tb;
+      SLF_TRY(tmap_kmajor(&ta, reinterpret_cast<const uint8_t*>(X) + (size_t)r0 * H * 2, H, rows, H, BM));
+      SLF_TRY(tmap_kmajor(&tb, W, H, V, H, b_box_rows()));
+      GemmArgs a{};
+      a.M = (int)rows;
+      a.N = (int)V;
+      a.K = (int)H;
+      a.targets = t + r0;
+      a.tcol0 = 0;
+      a.ignore_index = ignore_index;
+      a.partials = part;
+      a.zt = zt + r0;
+      a.out = stash;
+      a.ld_out = p.ld_stash;
+      SLF_TRY((launch_gemm<EPI_STASH, false, false>(c.dev, ta, tb, a, c.s)));
+    }
+    {
+      ProfScope ps(SLF_PROF_COMBINE_TRANSFORM, c.s, 0.0, (double)rows * (tiles_v * 8.0 + V * 4.0 + 24));
+      combine_transform_kernel<<<(unsigned)rows, 256, tiles_v * sizeof(float), c.s>>>(
+          part, tiles_v, (int)rows, zt + r0, t + r0, V, p.ld_stash, ignore_index, reduction, scale, 1.0f,
+          hdr_of(c.ws), loss_rows + r0, rs + r0, stash);
+      SLF_CUDA(cudaGetLastError());
+    }
+    if (dX || dW) {
+      ProbSpec ps[2];
+      int n = 0;
+      SLF_TRY(build_bwd(ch, ps, &n));
+      const int k = (rows == p.C || k_last < 0) ? k_full : k_last;
+      SLF_TRY(launch_group(c.dev, ps, n, c.s, arena.dev(c, k), arena.tables[k].second,
+                           n == 2 ? SLF_PROF_GEMM_GROUP : -1));
+    }
+  }
+  if (dW) {
+    ProfScope ps(SLF_PROF_ONEHOT, c.s, 0.0, (double)N * H * 2 * 2);
+    dim3 grid((unsigned)std::min<int64_t>(N, V), (unsigned)((H + 1023) / 1024));
+    onehot_kernel<<<grid, 128, 0, c.s>>>(reinterpret_cast<const uint16_t*>(X), H, off, idx, hits, V, reduction, scale,
+                                         1.0f, hdr_of(c.ws), reinterpret_cast<uint16_t*>(dW));
+    SLF_CUDA(cudaGetLastError());
+  }
+  if (reduction != SLF_NONE) {
+    ProfScope ps(SLF_PROF_LOSS_REDUCE, c.s, 0.0, (double)N * 4);
+    loss_reduce_kernel<<<1, 1024, 0, c.s>>>(loss_rows, N, reduction, hdr_of(c.ws), loss_out);
+    SLF_CUDA(cudaGetLastError());
+  }
+  return SLF_OK;
+}
+
+// Plan selection: SLF_SCHED_S for the fused single-GPU call when it fits (no recompute),
+// otherwise schedule R; the split / shard entry points always use R.
+bool plan_any(int64_t N, int64_t H, int64_t V, int schedule, size_t budget, bool allow_s, Plan* out) {
+  if ((schedule == SLF_SCHED_S || schedule == SLF_SCHED_AUTO) && allow_s && plan_s(N, H, V, budget, out)) return true;
+  if (schedule == SLF_SCHED_S) return false;
+  return plan_r(N, H, V, budget, out);
+}
+
+slf_status setup(Ctx& c, int64_t N, int64_t H, int64_t V_l, size_t budget, void* ws, size_t ws_bytes, void* stream,
+                 int schedule = SLF_SCHED_R, bool allow_s = false) {
   SLF_TRY(device_info(&c.dev));
-  if (!plan_r(N, H, V_l, budget, &c.plan))
-    return fail(SLF_ERR_WORKSPACE, "no schedule-R plan fits the budget (N=%lld H=%lld V=%lld budget=%zu)",
-                (long long)N, (long long)H, (long long)V_l, budget ? budget : default_budget(N, V_l));
+  if (!plan_any(N, H, V_l, schedule, budget, allow_s, &c.plan))
+    return fail(SLF_ERR_WORKSPACE, "no plan fits the budget (N=%lld H=%lld V=%lld budget=%zu schedule=%d)",
+                (long long)N, (long long)H, (long long)V_l, budget ? budget : default_budget(N, V_l), schedule);
   if (ws_bytes < c.plan.total)
     return fail(SLF_ERR_WORKSPACE, "workspace %zu bytes < required %zu", ws_bytes, c.plan.total);
   c.s = reinterpret_cast<cudaStream_t>(stream);
@@ -439,24 +778,34 @@ int slf_lce_version(void) { return 100; }
 const char* slf_last_error_string(void) { return g_err.c_str(); }
 
 size_t slf_lce_workspace_bytes(int64_t N, int64_t H, int64_t V_local, int schedule, size_t budget_bytes) {
-  if (schedule != SLF_SCHED_AUTO && schedule != SLF_SCHED_R) return 0;
-  Plan p;
-  if (!plan_r(N, H, V_local, budget_bytes, &p)) return 0;
-  return p.total;
+  Plan r, s;
+  const bool has_r = plan_r(N, H, V_local, budget_bytes, &r);
+  const bool has_s = plan_s(N, H, V_local, budget_bytes, &s);
+  switch (schedule) {
+    case SLF_SCHED_R: return has_r ? r.total : 0;
+    case SLF_SCHED_S: return has_s ? s.total : 0;
+    case SLF_SCHED_AUTO: return std::max(has_r ? r.total : 0, has_s ? s.total : 0);
+    default: return 0;
+  }
 }
 
 slf_status slf_lce_plan_describe(int64_t N, int64_t H, int64_t V_local, int schedule, size_t budget_bytes, char* out,
                                  size_t cap) {
   if (!out || cap == 0) return fail(SLF_ERR_ARG, "null output buffer");
-  if (schedule != SLF_SCHED_AUTO && schedule != SLF_SCHED_R) return fail(SLF_ERR_UNIMPLEMENTED, "schedule %d", schedule);
+  if (schedule < SLF_SCHED_AUTO || schedule > SLF_SCHED_S) return fail(SLF_ERR_ARG, "schedule %d", schedule);
   Plan p;
-  if (!plan_r(N, H, V_local, budget_bytes, &p)) return fail(SLF_ERR_WORKSPACE, "no plan fits");
-  const int64_t launches = 4 + p.nR * p.nC * 3;
-  snprintf(out, cap,
-           "schedule=R row_block=%lld n_row_blocks=%lld vocab_chunk=%lld n_vocab_chunks=%lld workspace=%zu "
-           "fwd_partials=%zu bwd=%zu launches=%lld",
-           (long long)p.R, (long long)p.nR, (long long)p.Cv, (long long)p.nC, p.total, p.fwd_bytes, p.bwd_bytes,
-           (long long)launches);
+  if (!plan_any(N, H, V_local, schedule, budget_bytes, true, &p)) return fail(SLF_ERR_WORKSPACE, "no plan fits");
+  if (p.sched == SLF_SCHED_S) {
+    snprintf(out, cap,
+             "schedule=S row_chunk=%lld n_chunks=%lld stash_bytes=%zu workspace=%zu launches=%lld",
+             (long long)p.C, (long long)p.nCh, (size_t)p.C * p.ld_stash * 2, p.total, (long long)(8 + p.nCh * 3));
+  } else {
+    snprintf(out, cap,
+             "schedule=R row_block=%lld n_row_blocks=%lld vocab_chunk=%lld n_vocab_chunks=%lld workspace=%zu "
+             "fwd_partials=%zu bwd=%zu launches=%lld",
+             (long long)p.R, (long long)p.nR, (long long)p.Cv, (long long)p.nC, p.total, p.fwd_bytes, p.bwd_bytes,
+             (long long)(4 + p.nR * p.nC * 2));
+  }
   return SLF_OK;
 }
 
@@ -467,11 +816,14 @@ slf_status slf_lce_fwd_bwd(const void* hidden, const void* weight, const int32_t
   SLF_TRY(check_common(hidden, weight, targets, N, H, V, workspace));
   if (!loss_out) return fail(SLF_ERR_ARG, "null loss_out");
   if (reduction < SLF_SUM || reduction > SLF_NONE) return fail(SLF_ERR_ARG, "bad reduction %d", reduction);
-  if (schedule != SLF_SCHED_AUTO && schedule != SLF_SCHED_R) return fail(SLF_ERR_UNIMPLEMENTED, "schedule %d", schedule);
+  if (schedule < SLF_SCHED_AUTO || schedule > SLF_SCHED_S) return fail(SLF_ERR_ARG, "schedule %d", schedule);
   if ((dhidden && !aligned16(dhidden)) || (dweight && !aligned16(dweight)))
     return fail(SLF_ERR_ALIGN, "gradient pointers must be 16-byte aligned");
+  if (!aligned16(loss_out)) return fail(SLF_ERR_ALIGN, "loss_out must be 16-byte aligned");
   Ctx c;
-  SLF_TRY(setup(c, N, H, V, budget_bytes, workspace, workspace_bytes, stream));
+  SLF_TRY(setup(c, N, H, V, budget_bytes, workspace, workspace_bytes, stream, schedule, true));
+  if (c.plan.sched == SLF_SCHED_S)
+    return phase_s(c, hidden, weight, targets, N, H, V, ignore_index, reduction, scale, loss_out, dhidden, dweight);
   slf_shardstat* st = reinterpret_cast<slf_shardstat*>(c.ws + c.plan.off_shard);
   slf_rowstat* rs = reinterpret_cast<slf_rowstat*>(c.ws + c.plan.off_rowstat);
   SLF_TRY(phase_stats(c, hidden, weight, targets, N, H, V, 0, ignore_index, st));

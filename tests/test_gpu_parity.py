@@ -23,16 +23,19 @@ def slf():
     return m
 
 
-def run_gpu(slf, inp, reduction="mean", scale=1.0, budget=0, ignore_index=-100):
+SCHEDS = ["R", "S"]
+
+
+def run_gpu(slf, inp, reduction="mean", scale=1.0, budget=0, ignore_index=-100, schedule="auto"):
     X, W, t = to_dev(inp, torch)
     loss, dX, dW = slf.lce_fwd_bwd(X, W, t, ignore_index=ignore_index, reduction=reduction, scale=scale,
-                                   budget_bytes=budget)
+                                   budget_bytes=budget, schedule=schedule)
     torch.cuda.synchronize()
     return loss, dX, dW
 
 
-def check_against_oracle(slf, inp, reduction="mean", scale=1.0, budget=0, ignore_index=-100):
-    loss, dX, dW = run_gpu(slf, inp, reduction, scale, budget, ignore_index)
+def check_against_oracle(slf, inp, reduction="mean", scale=1.0, budget=0, ignore_index=-100, schedule="auto"):
+    loss, dX, dW = run_gpu(slf, inp, reduction, scale, budget, ignore_index, schedule)
     Xo, Wo, to = oracle_inputs(inp)
     ref = oracle.lce(Xo, Wo, to, ignore_index=ignore_index, reduction=reduction, scale=scale)
     assert_loss_close(loss.detach().cpu().numpy(), ref["loss"], reduction)
@@ -67,48 +70,64 @@ def test_gemm_core(slf, a_mn, b_mn, shape):
 
 
 # ---- full path vs oracle -------------------------------------------------------------------------
+@pytest.mark.parametrize("sched", SCHEDS)
 @pytest.mark.parametrize("reduction", ["mean", "sum", "none"])
 @pytest.mark.parametrize("alpha,dist", [(1.0, "uniform"), (4.0, "zipf"), (4.0, "uniform")])
-def test_tiny_parity(slf, reduction, alpha, dist):
+def test_tiny_parity(slf, reduction, alpha, dist, sched):
     inp = synth.make_config("tiny", seed=11, alpha=alpha, dist=dist)
-    check_against_oracle(slf, inp, reduction=reduction, scale=1.0 if reduction != "sum" else 0.25)
+    check_against_oracle(slf, inp, reduction=reduction, scale=1.0 if reduction != "sum" else 0.25, schedule=sched)
 
 
-def test_multichunk_ragged_parity(slf):
-    """Several row blocks and vocab chunks, ragged tails in every GEMM dimension."""
+def test_multichunk_ragged_parity_r(slf):
+    """Schedule R: several row blocks and vocab chunks, ragged tails in every GEMM dimension."""
     inp = synth.make_inputs(1000, 200, 5000, seed=5, alpha=4.0, dist="zipf")
     budget = 1 << 20  # 1 MiB forces nR > 1 and nC > 1
-    desc = slf.plan_describe(1000, 200, 5000, budget_bytes=budget)
+    desc = slf.plan_describe(1000, 200, 5000, budget_bytes=budget, schedule="R")
     kv = dict(x.split("=") for x in desc.split())
     assert int(kv["n_row_blocks"]) > 1 and int(kv["n_vocab_chunks"]) > 1, desc
-    check_against_oracle(slf, inp, reduction="mean", budget=budget)
-    check_against_oracle(slf, inp, reduction="none", budget=budget)
+    check_against_oracle(slf, inp, reduction="mean", budget=budget, schedule="R")
+    check_against_oracle(slf, inp, reduction="none", budget=budget, schedule="R")
 
 
+@pytest.mark.parametrize("reduction", ["mean", "none"])
+def test_multichunk_ragged_parity_s(slf, reduction):
+    """Schedule S: several row chunks (ragged last chunk), Zipf targets (hot dW rows), V tail."""
+    inp = synth.make_inputs(1000, 200, 5000, seed=6, alpha=4.0, dist="zipf")
+    budget = 4 << 20
+    desc = slf.plan_describe(1000, 200, 5000, budget_bytes=budget, schedule="S")
+    kv = dict(x.split("=") for x in desc.split())
+    assert int(kv["n_chunks"]) > 2, desc
+    check_against_oracle(slf, inp, reduction=reduction, budget=budget, schedule="S")
+
+
+@pytest.mark.parametrize("sched", SCHEDS)
 @pytest.mark.parametrize("N,H,V", [(1, 8, 1), (1, 64, 300), (130, 136, 257), (257, 512, 4096)])
-def test_small_edges(slf, N, H, V):
+def test_small_edges(slf, N, H, V, sched):
     inp = synth.make_inputs(N, H, V, seed=N + V, alpha=2.0, ignore_frac=0.0 if N < 10 else 0.05)
-    check_against_oracle(slf, inp, reduction="mean")
+    check_against_oracle(slf, inp, reduction="mean", schedule=sched)
 
 
-def test_ignore_index_zero(slf):
+@pytest.mark.parametrize("sched", SCHEDS)
+def test_ignore_index_zero(slf, sched):
     inp = synth.make_inputs(300, 128, 1000, seed=3, ignore_index=0, alpha=2.0)
-    check_against_oracle(slf, inp, reduction="mean", ignore_index=0)
+    check_against_oracle(slf, inp, reduction="mean", ignore_index=0, schedule=sched)
 
 
 @pytest.mark.slow
-def test_llama_head_reduced_n(slf):
-    """Full Llama-3.1-8B head (H=4096, V=128256) at N=512: every element against the oracle."""
-    inp = synth.make_config("llama8b", seed=21, alpha=4.0, dist="zipf", N=512)
-    ex, ew = check_against_oracle(slf, inp, reduction="mean")
-    print(f"llama8b N=512: dX err {ex:.2e} dW err {ew:.2e}")
+@pytest.mark.parametrize("sched", SCHEDS)
+def test_llama_head_reduced_n(slf, sched):
+    """Full Llama-3.1-8B head (H=4096, V=128256) at N=1024: every element against the oracle."""
+    inp = synth.make_config("llama8b", seed=21, alpha=4.0, dist="zipf", N=1024)
+    ex, ew = check_against_oracle(slf, inp, reduction="mean", schedule=sched, budget=64 << 20)
+    print(f"llama8b N=1024 {sched}: dX err {ex:.2e} dW err {ew:.2e}")
 
 
 @pytest.mark.slow
+@pytest.mark.parametrize("sched", SCHEDS)
 @pytest.mark.parametrize("cfg", ["qwen7b", "mistral123b"])
-def test_other_heads_reduced_n(slf, cfg):
-    inp = synth.make_config(cfg, seed=22, alpha=1.0, dist="uniform", N=256)
-    check_against_oracle(slf, inp, reduction="sum", scale=1.0 / 256)
+def test_other_heads_reduced_n(slf, cfg, sched):
+    inp = synth.make_config(cfg, seed=22, alpha=1.0, dist="uniform", N=512)
+    check_against_oracle(slf, inp, reduction="sum", scale=1.0 / 256, schedule=sched, budget=64 << 20)
 
 
 # ---- invariants ----------------------------------------------------------------------------------
@@ -129,47 +148,51 @@ def test_w_zero_closed_form(slf):
     assert rel_max_err(bf16_to_np64(dW), ref) < GRAD_TOL
 
 
-def test_scale_linearity_and_determinism(slf):
-    inp = synth.make_inputs(700, 256, 3000, seed=9, alpha=3.0)
-    a = run_gpu(slf, inp, "mean", 1.0)
-    b = run_gpu(slf, inp, "mean", 2.0)
-    c = run_gpu(slf, inp, "mean", 1.0)
+@pytest.mark.parametrize("sched", SCHEDS)
+def test_scale_linearity_and_determinism(slf, sched):
+    inp = synth.make_inputs(700, 256, 3000, seed=9, alpha=3.0, dist="zipf")
+    a = run_gpu(slf, inp, "mean", 1.0, budget=2 << 20, schedule=sched)
+    b = run_gpu(slf, inp, "mean", 2.0, budget=2 << 20, schedule=sched)
+    c = run_gpu(slf, inp, "mean", 1.0, budget=2 << 20, schedule=sched)
     assert float(a[0]) == float(b[0]) == float(c[0])
     assert torch.equal(a[1].float() * 2, b[1].float()) and torch.equal(a[2].float() * 2, b[2].float())
     assert torch.equal(a[1], c[1]) and torch.equal(a[2], c[2])
 
 
-def test_ignored_rows_do_not_leak(slf):
+@pytest.mark.parametrize("sched", SCHEDS)
+def test_ignored_rows_do_not_leak(slf, sched):
     inp = synth.make_inputs(400, 128, 2000, seed=10, alpha=2.0)
-    a = run_gpu(slf, inp, "sum")
+    a = run_gpu(slf, inp, "sum", schedule=sched)
     ign = inp.t == -100
     inp2 = synth.LCEInputs(**{**inp.__dict__})
     X2 = inp.X.copy()
     X2[ign] = synth.f32_to_bf16_bits(np.random.default_rng(0).standard_normal((ign.sum(), 128)).astype(np.float32) * 7)
     inp2.X = X2
-    b = run_gpu(slf, inp2, "sum")
+    b = run_gpu(slf, inp2, "sum", schedule=sched)
     assert float(a[0]) == float(b[0])
     assert torch.equal(a[1][torch.from_numpy(~ign).cuda()], b[1][torch.from_numpy(~ign).cuda()])
     assert torch.equal(a[2].float().abs(), b[2].float().abs())
 
 
-def test_status_counts(slf):
+@pytest.mark.parametrize("sched", ["auto", "R"])
+def test_status_counts(slf, sched):
     inp = synth.make_config("tiny", seed=1)
     X, W, t = to_dev(inp, torch)
     ws = slf.alloc_workspace(256, 512, 4096, X.device)
-    loss, _, _ = slf.lce_fwd_bwd(X, W, t, workspace=ws)
+    loss, _, _ = slf.lce_fwd_bwd(X, W, t, workspace=ws, schedule=sched)
     bad, nv = slf.status(ws)
     assert bad == 0 and nv == 243
     t[5] = 4096
-    loss, _, _ = slf.lce_fwd_bwd(X, W, t, workspace=ws)
+    loss, _, _ = slf.lce_fwd_bwd(X, W, t, workspace=ws, schedule=sched)
     bad, nv = slf.status(ws)
     assert bad == 1 and math.isnan(float(loss))
 
 
-def test_all_ignored_mean(slf):
+@pytest.mark.parametrize("sched", SCHEDS)
+def test_all_ignored_mean(slf, sched):
     inp = synth.make_config("tiny", seed=2)
     inp.t[:] = -100
-    loss, dX, dW = run_gpu(slf, inp, "mean")
+    loss, dX, dW = run_gpu(slf, inp, "mean", schedule=sched)
     assert float(loss) == 0.0 and torch.all(dX == 0) and torch.all(dW == 0)
 
 
@@ -177,7 +200,11 @@ def test_all_ignored_mean(slf):
 def test_split_matches_fused(slf):
     inp = synth.make_inputs(600, 256, 3000, seed=12, alpha=3.0)
     X, W, t = to_dev(inp, torch)
-    loss_a, dX_a, dW_a = slf.lce_fwd_bwd(X, W, t, reduction="mean")
+    loss_a, dX_a, dW_a = slf.lce_fwd_bwd(X, W, t, reduction="mean", schedule="R")
+    loss_s, dX_s, dW_s = slf.lce_fwd_bwd(X, W, t, reduction="mean", schedule="S")
+    assert abs(float(loss_s) - float(loss_a)) <= 1e-5 * abs(float(loss_a))
+    assert rel_max_err(bf16_to_np64(dX_s), bf16_to_np64(dX_a)) < 1e-2
+    assert rel_max_err(bf16_to_np64(dW_s), bf16_to_np64(dW_a)) < 1e-2
     loss_b, rs = slf.lce_fwd(X, W, t, reduction="mean")
     dX_b, dW_b = slf.lce_bwd(X, W, t, rs, 1.0)
     torch.cuda.synchronize()
@@ -226,6 +253,9 @@ def test_llama_full_size_sampled(slf):
     X, W, t = to_dev(inp, torch)
     loss_rows, dX, dW = slf.lce_fwd_bwd(X, W, t, reduction="none", scale=1.0)
     loss_m, dX_m, dW_m = slf.lce_fwd_bwd(X, W, t, reduction="mean")
+    loss_r, dX_r, dW_r = slf.lce_fwd_bwd(X, W, t, reduction="mean", schedule="R")
+    assert float(loss_r) == pytest.approx(float(loss_m), rel=1e-5)
+    assert rel_max_err(bf16_to_np64(dW_m), bf16_to_np64(dW_r)) < 1e-2
     torch.cuda.synchronize()
     rng = np.random.default_rng(5)
     rows = np.sort(rng.choice(inp.N, 48, replace=False))
