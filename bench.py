@@ -205,22 +205,17 @@ def main():
     dW = torch.empty(V_l, H, dtype=torch.bfloat16, device=dev)
     extra = ws.numel()
     if g > 1:
-        stats_all = torch.empty(g, N, 4, dtype=torch.float32, device=dev)
-        dx32 = torch.empty(N, H, dtype=torch.float32, device=dev)
-        extra += stats_all.numel() * 4 + dx32.numel() * 4
+        from paper_2603_16428_b200.sharded import VocabShardedLCE
+        sharded = VocabShardedLCE(V, budget_bytes=args.budget)
+        assert (sharded.v0, sharded.v1) == (v0, v1)
+        extra += g * N * 16 + N * H * 4  # gathered statistics + fp32 dX partial
 
     def step(Xs=X, ts=t):
         if g == 1:
             slf.lce_fwd_bwd(Xs, W, ts, out=(loss, dX, dW), workspace=ws, budget_bytes=args.budget,
                             schedule=args.schedule)
             return loss
-        st = slf.shard_stats(Xs, W, ts, v0, workspace=ws, budget_bytes=args.budget)
-        dist.all_gather_into_tensor(stats_all.view(g * N, 4), st)
-        l, rs = slf.stats_combine(stats_all, ts, v0, V_l, V, workspace=ws)
-        d32, _ = slf.lce_bwd(Xs, W, ts, rs, 1.0, dhidden_fp32=True, workspace=ws, budget_bytes=args.budget,
-                             out=(dx32, dW))
-        dist.all_reduce(d32)
-        slf.dx_finalize(d32, rs, out=dX)
+        l, _, _ = sharded.forward_backward(Xs, W, ts, workspace=ws, dW_out=dW, dX_out=dX)
         return l
 
     def barrier():

@@ -13,7 +13,8 @@
 // small chunks"):
 //   EPI_STATS : per (row, 256-column vocab tile) max m and sum exp(z - m); gathers the target logit.
 //   EPI_GRAD  : G = coef * (exp(z - lse) - [v == t]) in fp32, rounded to bf16, stored to the chunk.
-//   EPI_DW    : dW tile (bf16), store or fp32 read-add-write of the previous row block's partial.
+//   EPI_DW    : dW tile (bf16), store or fp32 read-add-write of the previous partial, through
+//               TMA-staged 64-column chunks (epilogue_dw_tma).
 //   EPI_DX    : dX tile: fp32 store / accumulate across vocab chunks, final bf16 conversion with
 //               ignored rows forced to +0.
 //   EPI_F32   : plain fp32 store (test entry point).
@@ -43,7 +44,8 @@ struct Cfg {
   static constexpr int B_BYTES = B_ROWS * BK * 2;
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
   static constexpr int STAGES = CG == 2 ? 6 : 4;
-  static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 /*align slack*/ + 256 /*barriers*/;
+  static constexpr int STAGING_BYTES = 2 * BM * 64 * 2;  // 2 x [128 rows x 64 bf16] epilogue TMA buffers
+  static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + STAGING_BYTES + 1024 /*align slack*/ + 256 /*barriers*/;
 };
 
 enum EpiKind { EPI_STATS = 0, EPI_GRAD = 1, EPI_DW = 2, EPI_DX = 3, EPI_F32 = 4, EPI_STASH = 5, EPI_DXS = 6 };
@@ -263,35 +265,6 @@ __device__ __forceinline__ void epilogue_tile(const GemmArgs& a, uint32_t taddr,
           dst[q] = row_ok ? make_uint4(p[4 * q], p[4 * q + 1], p[4 * q + 2], p[4 * q + 3]) : make_uint4(0u, 0u, 0u, 0u);
       }
     }
-  } else if constexpr (EPI == EPI_DW) {
-    uint16_t* out = reinterpret_cast<uint16_t*>(a.out) + (size_t)r * a.ld_out + n0;
-#pragma unroll 1
-    for (int c = 0; c < BN / 32; ++c) {
-      if (c * 32 >= ncols) break;
-      tmem_ld32(taddr + c * 32, v);
-      tmem_ld_wait();
-      if (row_ok) {
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          const int j = c * 32 + q * 8;
-          if (j < ncols) {  // ncols % 8 == 0 (H % 8 == 0)
-            uint4* dst = reinterpret_cast<uint4*>(out + j);
-            float f[8];
-#pragma unroll
-            for (int e = 0; e < 8; ++e) f[e] = __uint_as_float(v[q * 8 + e]);
-            if (a.mode == 1) {
-              const uint4 old = *dst;
-              f[0] += bf16lo_to_f32(old.x); f[1] += bf16hi_to_f32(old.x);
-              f[2] += bf16lo_to_f32(old.y); f[3] += bf16hi_to_f32(old.y);
-              f[4] += bf16lo_to_f32(old.z); f[5] += bf16hi_to_f32(old.z);
-              f[6] += bf16lo_to_f32(old.w); f[7] += bf16hi_to_f32(old.w);
-            }
-            *dst = make_uint4(pack_bf16x2(f[0], f[1]), pack_bf16x2(f[2], f[3]), pack_bf16x2(f[4], f[5]),
-                              pack_bf16x2(f[6], f[7]));
-          }
-        }
-      }
-    }
   } else if constexpr (EPI == EPI_DX) {
     const bool valid = row_ok && a.rowstat[r].valid != 0;
     float* acc = reinterpret_cast<float*>(a.out) + (size_t)r * a.ld_out + n0;
@@ -344,13 +317,82 @@ __device__ __forceinline__ void epilogue_tile(const GemmArgs& a, uint32_t taddr,
   }
 }
 
+// dW tile epilogue through TMA (store, or read-add-write of the previous bf16 partial when
+// mode == 1).  The 128 x 256 tile is processed in four 64-column chunks staged in two swizzled
+// 16 KB smem buffers: TMA loads the old chunk (coalesced), each thread adds its row's fp32
+// accumulator from TMEM and writes bf16 back to smem, TMA stores the chunk.  Thread-per-row global
+// accesses would touch 32 cache lines per warp instruction; this keeps the short-K dW GEMMs of
+// schedule S tensor-bound instead of epilogue-bound.
+__device__ __forceinline__ void epilogue_dw_tma(const GemmArgs& a, const CUtensorMap* tmC, uint32_t taddr, int row0,
+                                                int n_blk, int rl, uint8_t* stg, uint64_t* sbar, uint32_t& sphase,
+                                                bool lead) {
+  constexpr uint32_t CHUNK_BYTES = BM * 64 * 2;
+  const int n0 = n_blk * BN;
+  const int nch = min(BN, a.N - n0 + 63) / 64;  // 64-column chunks with at least one valid column
+  const bool rmw = a.mode == 1;
+  const uint32_t sbase = smem_u32(stg);
+  // The previous tile's stores must have finished reading both buffers.
+  if (lead) bulk_wait_read<0>();
+  named_bar_sync(1, 128);
+  if (rmw && lead) {
+    for (int k = 0; k < 2 && k < nch; ++k) {
+      mbar_arrive_expect_tx(&sbar[k], CHUNK_BYTES);
+      tma_load_2d(tmC, &sbar[k], stg + k * CHUNK_BYTES, n0 + k * 64, row0, policy_evict_normal());
+    }
+  }
+  uint32_t v0[32], v1[32];
+  for (int k = 0; k < nch; ++k) {
+    const int b = k & 1;
+    tmem_ld32(taddr + k * 64, v0);
+    tmem_ld32(taddr + k * 64 + 32, v1);
+    tmem_ld_wait();
+    if (rmw) {
+      mbar_wait(&sbar[b], (sphase >> b) & 1);
+      sphase ^= 1u << b;
+    }
+    const uint32_t rowaddr = sbase + b * CHUNK_BYTES + rl * 128;
+#pragma unroll
+    for (int gi = 0; gi < 8; ++gi) {
+      const uint32_t addr = rowaddr + ((gi ^ (rl & 7)) << 4);  // 128B swizzle: granule gi of row rl
+      const uint32_t* src = gi < 4 ? &v0[gi * 8] : &v1[(gi - 4) * 8];
+      float f[8];
+#pragma unroll
+      for (int e = 0; e < 8; ++e) f[e] = __uint_as_float(src[e]);
+      if (rmw) {
+        const uint4 o = lds128(addr);
+        f[0] += bf16lo_to_f32(o.x); f[1] += bf16hi_to_f32(o.x);
+        f[2] += bf16lo_to_f32(o.y); f[3] += bf16hi_to_f32(o.y);
+        f[4] += bf16lo_to_f32(o.z); f[5] += bf16hi_to_f32(o.z);
+        f[6] += bf16lo_to_f32(o.w); f[7] += bf16hi_to_f32(o.w);
+      }
+      sts128(addr, make_uint4(pack_bf16x2(f[0], f[1]), pack_bf16x2(f[2], f[3]), pack_bf16x2(f[4], f[5]),
+                              pack_bf16x2(f[6], f[7])));
+    }
+    fence_proxy_async_smem();
+    named_bar_sync(1, 128);
+    if (lead) {
+      tma_store_2d(tmC, stg + b * CHUNK_BYTES, n0 + k * 64, row0);
+      bulk_commit();
+    }
+    if (k + 1 < nch) {
+      // Buffer (k+1)&1 is free once the store issued for chunk k-1 has been read out.
+      if (lead) bulk_wait_read<1>();
+      if (rmw && lead && k + 2 < nch) {
+        bulk_wait_read<0>();  // buffer b (chunk k) is reused for chunk k+2
+        mbar_arrive_expect_tx(&sbar[b], CHUNK_BYTES);
+        tma_load_2d(tmC, &sbar[b], stg + b * CHUNK_BYTES, n0 + (k + 2) * 64, row0, policy_evict_normal());
+      }
+      named_bar_sync(1, 128);
+    }
+  }
+}
+
 // Runtime epilogue dispatch (one problem of a group decides per tile).
 __device__ __forceinline__ void epilogue_dispatch(int epi, const GemmArgs& a, uint32_t taddr, int row0, int n_blk,
                                                   int row_in_tile) {
   switch (epi) {
     case EPI_STATS: epilogue_tile<EPI_STATS>(a, taddr, row0, n_blk, row_in_tile); break;
     case EPI_GRAD: epilogue_tile<EPI_GRAD>(a, taddr, row0, n_blk, row_in_tile); break;
-    case EPI_DW: epilogue_tile<EPI_DW>(a, taddr, row0, n_blk, row_in_tile); break;
     case EPI_DX: epilogue_tile<EPI_DX>(a, taddr, row0, n_blk, row_in_tile); break;
     case EPI_STASH: epilogue_tile<EPI_STASH>(a, taddr, row0, n_blk, row_in_tile); break;
     case EPI_DXS: epilogue_tile<EPI_DXS>(a, taddr, row0, n_blk, row_in_tile); break;
@@ -378,7 +420,7 @@ struct GroupArgs {
 };
 
 struct TMaps {
-  CUtensorMap m[2 * MAXP];  // A, B of each problem
+  CUtensorMap m[3 * MAXP];  // A, B, and the output C (EPI_DW: dW, TMA-staged epilogue) of each problem
 };
 
 struct TileIter {
@@ -410,11 +452,13 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sA = smem;
   uint8_t* sB = smem + C::STAGES * C::A_BYTES;
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + C::STAGES * C::STAGE_BYTES);
+  uint8_t* stg = smem + C::STAGES * C::STAGE_BYTES;  // 2 x 16 KB epilogue staging (1024-aligned)
+  uint64_t* full = reinterpret_cast<uint64_t*>(stg + C::STAGING_BYTES);
   uint64_t* empty = full + C::STAGES;
   uint64_t* tfull = empty + C::STAGES;
   uint64_t* tempty = tfull + 2;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  uint64_t* sbar = tempty + 2;  // staging-load barriers (2)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(sbar + 2);
 
   const uint32_t warp = warp_idx_sync();
   const uint32_t lane = threadIdx.x & 31;
@@ -423,7 +467,8 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
   const int units = gridDim.x / CG;
 
   if (warp == 0 && lane == 0) {
-    for (int i = 0; i < 2 * g.nprob; ++i) tma_prefetch_desc(&tm.m[i]);
+    for (int i = 0; i < 3 * g.nprob; ++i)
+      if (i % 3 < 2 || g.p[i / 3].epi == EPI_DW) tma_prefetch_desc(&tm.m[i]);
 #pragma unroll
     for (int i = 0; i < C::STAGES; ++i) {
       mbar_init(&full[i], 1);
@@ -432,6 +477,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     for (int i = 0; i < 2; ++i) {
       mbar_init(&tfull[i], 1);
       mbar_init(&tempty[i], 4 * CG);  // one arrive per epilogue warp of every CTA of the pair
+      mbar_init(&sbar[i], 1);
     }
     fence_barrier_init();
   }
@@ -458,8 +504,8 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
       for (int tile = it.next(); tile >= 0; tile = it.next()) {
         const int pi = prob_of(g, tile);
         const Prob& P = g.p[pi];
-        const CUtensorMap* tA = &tm.m[2 * pi];
-        const CUtensorMap* tB = &tm.m[2 * pi + 1];
+        const CUtensorMap* tA = &tm.m[3 * pi];
+        const CUtensorMap* tB = &tm.m[3 * pi + 1];
         int m_blk, n_blk;
         tile_coords(tile - P.tile_begin, P.a, m_blk, n_blk);
         const int a_row = m_blk * C::TILE_M + (int)rank * BM;
@@ -553,16 +599,22 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     // ===== epilogue: thread = TMEM lane = output row =====
     const uint32_t ew = warp - 4;
     uint32_t local = 0;
+    uint32_t sphase = 0;  // parity bits of the two staging barriers
     TileIter it(g, unit, units);
     for (int tile = it.next(); tile >= 0; tile = it.next(), ++local) {
-      const Prob& P = g.p[prob_of(g, tile)];
+      const int pi = prob_of(g, tile);
+      const Prob& P = g.p[pi];
       int m_blk, n_blk;
       tile_coords(tile - P.tile_begin, P.a, m_blk, n_blk);
       const uint32_t acc = local & 1, acc_phase = (local >> 1) & 1;
       mbar_wait(&tfull[acc], acc_phase);
       tc_fence_after();
       const uint32_t taddr = tmem_base + ((ew * 32) << 16) + acc * BN;
-      epilogue_dispatch(P.epi, P.a, taddr, m_blk * C::TILE_M + (int)rank * BM, n_blk, ew * 32 + lane);
+      if (P.epi == EPI_DW)
+        epilogue_dw_tma(P.a, &tm.m[3 * pi + 2], taddr, m_blk * C::TILE_M + (int)rank * BM, n_blk, ew * 32 + lane,
+                        stg, sbar, sphase, ew == 0 && lane == 0);
+      else
+        epilogue_dispatch(P.epi, P.a, taddr, m_blk * C::TILE_M + (int)rank * BM, n_blk, ew * 32 + lane);
       tc_fence_before();
       __syncwarp();
       if (lane == 0) {
@@ -573,6 +625,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
       }
     }
   }
+  if (warp == 4 && lane == 0) bulk_wait<0>();  // epilogue TMA stores complete before exit
   __syncthreads();
   if constexpr (CG == 2) cluster_sync();
   if (warp == 2) {

@@ -166,7 +166,7 @@ uint32_t b_box_rows() { return (uint32_t)(BN / cta_group()); }
 
 // One GEMM problem of a launch: operand tensor maps, extents and epilogue arguments.
 struct ProbSpec {
-  CUtensorMap ta, tb;
+  CUtensorMap ta, tb, tc;  // tc: output map (EPI_DW only)
   GemmArgs a{};
   int epi = EPI_F32;
   bool a_mn = false, b_mn = false;
@@ -242,8 +242,9 @@ slf_status launch_group_cg(DevInfo* dev, ProbSpec* ps, int n, cudaStream_t s, co
     GemmArgs a = ps[p].a;
     if (a.M <= 0 || a.N <= 0 || a.K <= 0) continue;
     finish_geometry(a, CG);
-    tm.m[2 * np] = ps[p].ta;
-    tm.m[2 * np + 1] = ps[p].tb;
+    tm.m[3 * np] = ps[p].ta;
+    tm.m[3 * np + 1] = ps[p].tb;
+    tm.m[3 * np + 2] = ps[p].tc;
     g.p[np] = Prob{a, ps[p].epi, ps[p].a_mn ? 1 : 0, ps[p].b_mn ? 1 : 0, total};
     total += a.num_tiles;
     flops += 2.0 * a.M * a.N * (double)a.K;
@@ -521,6 +522,7 @@ slf_status phase_backward(Ctx& c, const void* X, const void* W, const slf_rowsta
       q.a.out = reinterpret_cast<uint8_t*>(dW) + (size_t)c0 * H * 2;
       q.a.ld_out = H;
       q.a.mode = rb > 0 ? 1 : 0;
+      SLF_TRY(tmap_kmajor(&q.tc, q.a.out, H, wc, H, BM));
       finish_geometry(q.a, cg);
     }
     if (dX) {  // dX_r (+)= G W_c : A = G (K-major), B = W_c (MN-major)
@@ -678,6 +680,7 @@ slf_status phase_s(Ctx& c, const void* X, const void* W, const int32_t* t, int64
       q.a.out = dW;
       q.a.ld_out = H;
       q.a.mode = ch > 0 ? 1 : 0;
+      SLF_TRY(tmap_kmajor(&q.tc, dW, H, V, H, BM));
       finish_geometry(q.a, cg);
     }
     return SLF_OK;

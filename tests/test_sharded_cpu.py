@@ -1,0 +1,126 @@
+"""World-size-2/3 CPU tests (gloo) of the vocab-sharded orchestration (paper_2603_16428_b200.sharded).
+
+The CUDA kernels cannot run here, so the per-shard compute ops are replaced by float64 stand-ins
+built on the oracle's plain definitions; what is under test is the host-side logic of the N>1
+path: shard bounds, the rank-ordered all-gather of per-token statistics, the shard-order combine,
+the fp32 all-reduce of dX partials and the locality of dW.  The result must equal the single-process
+oracle on the full vocabulary.
+"""
+import os
+import socket
+import types
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+import oracle
+from paper_2603_16428_b200.sharded import VocabShardedLCE, shard_bounds
+
+
+def _fake_ops():
+    def shard_stats(X, W_l, t, v0, ignore_index=-100, workspace=None, budget_bytes=0):
+        m, s, zt = oracle.shard_stats(X.numpy(), W_l.numpy(), t.numpy(), v0, ignore_index)
+        V_l = W_l.shape[0]
+        tt = t.numpy()
+        hit = (tt != ignore_index) & (tt - v0 >= 0) & (tt - v0 < V_l)
+        return torch.from_numpy(np.stack([m, s, zt, hit.astype(np.float64)], axis=1))
+
+    def stats_combine(allst, t, v0, V_l, V, ignore_index=-100, reduction="mean", scale=1.0, workspace=None):
+        a = allst.numpy()
+        lse, z = oracle.combine_shards([(a[k, :, 0], a[k, :, 1], a[k, :, 2]) for k in range(a.shape[0])])
+        tt = t.numpy()
+        valid, nv, coef = oracle.coef_for(tt, ignore_index, reduction, scale)
+        l = np.where(valid, lse - z, 0.0)
+        loss = l.sum() if reduction == "sum" else (l.sum() / nv if nv else 0.0)
+        tloc = np.where(valid & (tt - v0 >= 0) & (tt - v0 < V_l), tt - v0, -1)
+        return torch.tensor(loss), types.SimpleNamespace(lse=lse, coef=coef, tloc=tloc, valid=valid)
+
+    def lce_bwd(X, W_l, t, rs, grad_scale, dhidden_fp32=True, workspace=None, budget_bytes=0, out=None):
+        Z = X.numpy() @ W_l.numpy().T
+        P = np.exp(Z - rs.lse[:, None])
+        rows = np.nonzero(rs.tloc >= 0)[0]
+        P[rows, rs.tloc[rows]] -= 1.0
+        G = grad_scale * rs.coef[:, None] * P
+        dx32, dW = out
+        dx32.copy_(torch.from_numpy(G @ W_l.numpy()))
+        dW.copy_(torch.from_numpy(G.T @ X.numpy()))
+        return dx32, dW
+
+    def dx_finalize(dx32, rs, out=None):
+        r = dx32.clone()
+        r[torch.from_numpy(~rs.valid)] = 0.0
+        return r
+
+    return types.SimpleNamespace(shard_stats=shard_stats, stats_combine=stats_combine, lce_bwd=lce_bwd,
+                                 dx_finalize=dx_finalize)
+
+
+def _worker(rank, world, port, N, H, V, red, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        rng = np.random.default_rng(0)
+        X = rng.standard_normal((N, H))
+        W = rng.standard_normal((V, H)) * 3 / np.sqrt(H)
+        t = rng.integers(0, V, N)
+        t[rng.permutation(N)[:5]] = -100
+        lce = VocabShardedLCE(V, ops=_fake_ops())
+        v0, v1 = lce.v0, lce.v1
+        loss, dX, dW = lce.forward_backward(torch.from_numpy(X), torch.from_numpy(W[v0:v1].copy()),
+                                            torch.from_numpy(t), reduction=red, scale=0.5)
+        q.put((rank, float(loss), dX.numpy(), dW.numpy(), v0, v1))
+    finally:
+        dist.destroy_process_group()
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+@pytest.mark.parametrize("world,red", [(2, "mean"), (3, "sum")])
+def test_vocab_sharded_orchestration(world, red):
+    N, H, V = 40, 16, 203
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, N, H, V, red, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=120) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    rng = np.random.default_rng(0)
+    X = rng.standard_normal((N, H))
+    W = rng.standard_normal((V, H)) * 3 / np.sqrt(H)
+    t = rng.integers(0, V, N)
+    t[rng.permutation(N)[:5]] = -100
+    ref = oracle.lce(X, W, t, reduction=red, scale=0.5)
+    res.sort(key=lambda r: r[0])
+    covered = []
+    for rank, loss, dX, dW, v0, v1 in res:
+        assert loss == pytest.approx(ref["loss"], rel=1e-12)
+        np.testing.assert_allclose(dX, ref["dX"], rtol=1e-10, atol=1e-14)
+        np.testing.assert_allclose(dW, ref["dW"][v0:v1], rtol=1e-10, atol=1e-14)
+        covered.append((v0, v1))
+    assert covered[0][0] == 0 and covered[-1][1] == V
+    assert all(a[1] == b[0] for a, b in zip(covered[:-1], covered[1:]))
+
+
+def test_shard_bounds():
+    for V in (128256, 203, 8):
+        for g in (1, 2, 3, 8):
+            b = [shard_bounds(V, g, r) for r in range(g)]
+            assert b[0][0] == 0 and b[-1][1] == V
+            assert all(x[1] == y[0] for x, y in zip(b[:-1], b[1:]))
+            sizes = [y - x for x, y in b]
+            assert max(sizes) - min(sizes) <= 1
+    with pytest.raises(ValueError):
+        shard_bounds(10, 2, 2)
