@@ -323,9 +323,10 @@ __device__ __forceinline__ void epilogue_tile(const GemmArgs& a, uint32_t taddr,
 // accumulator from TMEM and writes bf16 back to smem, TMA stores the chunk.  Thread-per-row global
 // accesses would touch 32 cache lines per warp instruction; this keeps the short-K dW GEMMs of
 // schedule S tensor-bound instead of epilogue-bound.
+template <typename ReleaseTmem>
 __device__ __forceinline__ void epilogue_dw_tma(const GemmArgs& a, const CUtensorMap* tmC, uint32_t taddr, int row0,
                                                 int n_blk, int rl, uint8_t* stg, uint64_t* sbar, uint32_t& sphase,
-                                                bool lead) {
+                                                bool lead, ReleaseTmem release_tmem) {
   constexpr uint32_t CHUNK_BYTES = BM * 64 * 2;
   const int n0 = n_blk * BN;
   const int nch = min(BN, a.N - n0 + 63) / 64;  // 64-column chunks with at least one valid column
@@ -346,6 +347,7 @@ __device__ __forceinline__ void epilogue_dw_tma(const GemmArgs& a, const CUtenso
     tmem_ld32(taddr + k * 64, v0);
     tmem_ld32(taddr + k * 64 + 32, v1);
     tmem_ld_wait();
+    if (k == nch - 1) release_tmem();  // the accumulator is in registers: let the next MMA start
     if (rmw) {
       mbar_wait(&sbar[b], (sphase >> b) & 1);
       sphase ^= 1u << b;
@@ -427,17 +429,18 @@ struct TileIter {
   const GroupArgs& g;
   int unit, units, i;
   __device__ TileIter(const GroupArgs& g_, int unit_, int units_) : g(g_), unit(unit_), units(units_), i(0) {}
-  __device__ __forceinline__ int next() {
+  __device__ __forceinline__ int at(int k) const {
     int t;
     if (g.sched) {
-      t = i < g.sched_stride ? __ldg(g.sched + (size_t)unit * g.sched_stride + i) : -1;
+      t = k < g.sched_stride ? __ldg(g.sched + (size_t)unit * g.sched_stride + k) : -1;
     } else {
-      t = unit + i * units;
+      t = unit + k * units;
       if (t >= g.num_tiles) t = -1;
     }
-    ++i;
     return t;
   }
+  __device__ __forceinline__ int next() { return at(i++); }
+  __device__ __forceinline__ int peek() const { return at(i); }
 };
 
 __device__ __forceinline__ int prob_of(const GroupArgs& g, int tile) {
@@ -610,18 +613,34 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
       mbar_wait(&tfull[acc], acc_phase);
       tc_fence_after();
       const uint32_t taddr = tmem_base + ((ew * 32) << 16) + acc * BN;
-      if (P.epi == EPI_DW)
+      auto release = [&]() {
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) {
+          if constexpr (CG == 2)
+            mbar_arrive_cluster(mapa_shared(smem_u32(&tempty[acc]), 0));
+          else
+            mbar_arrive(&tempty[acc]);
+        }
+      };
+      if (P.epi == EPI_DW) {
+        // Warm L2 with the old dW rows of this unit's next tile while this one is processed.
+        const int nt = it.peek();
+        if (ew == 0 && lane == 0 && nt >= 0) {
+          const int npi = prob_of(g, nt);
+          const Prob& Q = g.p[npi];
+          if (Q.epi == EPI_DW && Q.a.mode == 1) {
+            int qm, qn;
+            tile_coords(nt - Q.tile_begin, Q.a, qm, qn);
+            for (int k = 0; k < BN / 64 && qn * BN + k * 64 < Q.a.N; ++k)
+              tma_prefetch_l2_2d(&tm.m[3 * npi + 2], qn * BN + k * 64, qm * C::TILE_M + (int)rank * BM);
+          }
+        }
         epilogue_dw_tma(P.a, &tm.m[3 * pi + 2], taddr, m_blk * C::TILE_M + (int)rank * BM, n_blk, ew * 32 + lane,
-                        stg, sbar, sphase, ew == 0 && lane == 0);
-      else
+                        stg, sbar, sphase, ew == 0 && lane == 0, release);
+      } else {
         epilogue_dispatch(P.epi, P.a, taddr, m_blk * C::TILE_M + (int)rank * BM, n_blk, ew * 32 + lane);
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) {
-        if constexpr (CG == 2)
-          mbar_arrive_cluster(mapa_shared(smem_u32(&tempty[acc]), 0));
-        else
-          mbar_arrive(&tempty[acc]);
+        release();
       }
     }
   }
