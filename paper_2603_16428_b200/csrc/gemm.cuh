@@ -43,8 +43,8 @@ struct Cfg {
   static constexpr int A_BYTES = BM * BK * 2;
   static constexpr int B_BYTES = B_ROWS * BK * 2;
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
-  static constexpr int STAGES = CG == 2 ? 6 : 4;
-  static constexpr int STAGING_BYTES = 2 * BM * 64 * 2;  // 2 x [128 rows x 64 bf16] epilogue TMA buffers
+  static constexpr int STAGES = CG == 2 ? 5 : 3;
+  static constexpr int STAGING_BYTES = 4 * BM * 64 * 2;  // 4 x [128 rows x 64 bf16] epilogue TMA buffers
   static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + STAGING_BYTES + 1024 /*align slack*/ + 256 /*barriers*/;
 };
 
@@ -318,41 +318,42 @@ __device__ __forceinline__ void epilogue_tile(const GemmArgs& a, uint32_t taddr,
 }
 
 // dW tile epilogue through TMA (store, or read-add-write of the previous bf16 partial when
-// mode == 1).  The 128 x 256 tile is processed in four 64-column chunks staged in two swizzled
-// 16 KB smem buffers: TMA loads the old chunk (coalesced), each thread adds its row's fp32
-// accumulator from TMEM and writes bf16 back to smem, TMA stores the chunk.  Thread-per-row global
-// accesses would touch 32 cache lines per warp instruction; this keeps the short-K dW GEMMs of
-// schedule S tensor-bound instead of epilogue-bound.
-template <typename ReleaseTmem>
+// mode == 1).  The 128 x 256 tile is split into four 64-column chunks, one swizzled 16 KB smem
+// buffer each.  The old chunks are requested by TMA (coalesced) BEFORE the accumulator is waited
+// for, so their latency hides behind this tile's MMAs; each thread then adds its row's fp32
+// accumulator from TMEM, writes bf16 back to smem, and four TMA stores write the tile out.
+// Thread-per-row global accesses would touch 32 cache lines per warp instruction; this keeps the
+// short-K dW GEMMs of schedule S tensor-bound instead of epilogue-bound.
+template <typename WaitAcc, typename ReleaseTmem>
 __device__ __forceinline__ void epilogue_dw_tma(const GemmArgs& a, const CUtensorMap* tmC, uint32_t taddr, int row0,
                                                 int n_blk, int rl, uint8_t* stg, uint64_t* sbar, uint32_t& sphase,
-                                                bool lead, ReleaseTmem release_tmem) {
+                                                bool lead, WaitAcc wait_acc, ReleaseTmem release_tmem) {
   constexpr uint32_t CHUNK_BYTES = BM * 64 * 2;
   const int n0 = n_blk * BN;
   const int nch = min(BN, a.N - n0 + 63) / 64;  // 64-column chunks with at least one valid column
   const bool rmw = a.mode == 1;
   const uint32_t sbase = smem_u32(stg);
-  // The previous tile's stores must have finished reading both buffers.
+  // The previous tile's stores must have finished reading the buffers.
   if (lead) bulk_wait_read<0>();
   named_bar_sync(1, 128);
   if (rmw && lead) {
-    for (int k = 0; k < 2 && k < nch; ++k) {
+    for (int k = 0; k < nch; ++k) {
       mbar_arrive_expect_tx(&sbar[k], CHUNK_BYTES);
       tma_load_2d(tmC, &sbar[k], stg + k * CHUNK_BYTES, n0 + k * 64, row0, policy_evict_normal());
     }
   }
+  wait_acc();
   uint32_t v0[32], v1[32];
   for (int k = 0; k < nch; ++k) {
-    const int b = k & 1;
     tmem_ld32(taddr + k * 64, v0);
     tmem_ld32(taddr + k * 64 + 32, v1);
     tmem_ld_wait();
     if (k == nch - 1) release_tmem();  // the accumulator is in registers: let the next MMA start
     if (rmw) {
-      mbar_wait(&sbar[b], (sphase >> b) & 1);
-      sphase ^= 1u << b;
+      mbar_wait(&sbar[k], (sphase >> k) & 1);
+      sphase ^= 1u << k;
     }
-    const uint32_t rowaddr = sbase + b * CHUNK_BYTES + rl * 128;
+    const uint32_t rowaddr = sbase + k * CHUNK_BYTES + rl * 128;
 #pragma unroll
     for (int gi = 0; gi < 8; ++gi) {
       const uint32_t addr = rowaddr + ((gi ^ (rl & 7)) << 4);  // 128B swizzle: granule gi of row rl
@@ -370,22 +371,12 @@ __device__ __forceinline__ void epilogue_dw_tma(const GemmArgs& a, const CUtenso
       sts128(addr, make_uint4(pack_bf16x2(f[0], f[1]), pack_bf16x2(f[2], f[3]), pack_bf16x2(f[4], f[5]),
                               pack_bf16x2(f[6], f[7])));
     }
-    fence_proxy_async_smem();
-    named_bar_sync(1, 128);
-    if (lead) {
-      tma_store_2d(tmC, stg + b * CHUNK_BYTES, n0 + k * 64, row0);
-      bulk_commit();
-    }
-    if (k + 1 < nch) {
-      // Buffer (k+1)&1 is free once the store issued for chunk k-1 has been read out.
-      if (lead) bulk_wait_read<1>();
-      if (rmw && lead && k + 2 < nch) {
-        bulk_wait_read<0>();  // buffer b (chunk k) is reused for chunk k+2
-        mbar_arrive_expect_tx(&sbar[b], CHUNK_BYTES);
-        tma_load_2d(tmC, &sbar[b], stg + b * CHUNK_BYTES, n0 + (k + 2) * 64, row0, policy_evict_normal());
-      }
-      named_bar_sync(1, 128);
-    }
+  }
+  fence_proxy_async_smem();
+  named_bar_sync(1, 128);
+  if (lead) {
+    for (int k = 0; k < nch; ++k) tma_store_2d(tmC, stg + k * CHUNK_BYTES, n0 + k * 64, row0);
+    bulk_commit();
   }
 }
 
@@ -460,8 +451,8 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
   uint64_t* empty = full + C::STAGES;
   uint64_t* tfull = empty + C::STAGES;
   uint64_t* tempty = tfull + 2;
-  uint64_t* sbar = tempty + 2;  // staging-load barriers (2)
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(sbar + 2);
+  uint64_t* sbar = tempty + 2;  // staging-load barriers (4)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(sbar + 4);
 
   const uint32_t warp = warp_idx_sync();
   const uint32_t lane = threadIdx.x & 31;
@@ -480,8 +471,8 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     for (int i = 0; i < 2; ++i) {
       mbar_init(&tfull[i], 1);
       mbar_init(&tempty[i], 4 * CG);  // one arrive per epilogue warp of every CTA of the pair
-      mbar_init(&sbar[i], 1);
     }
+    for (int i = 0; i < 4; ++i) mbar_init(&sbar[i], 1);
     fence_barrier_init();
   }
   if (warp == 2) {
@@ -610,8 +601,10 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
       int m_blk, n_blk;
       tile_coords(tile - P.tile_begin, P.a, m_blk, n_blk);
       const uint32_t acc = local & 1, acc_phase = (local >> 1) & 1;
-      mbar_wait(&tfull[acc], acc_phase);
-      tc_fence_after();
+      auto wait_acc = [&]() {
+        mbar_wait(&tfull[acc], acc_phase);
+        tc_fence_after();
+      };
       const uint32_t taddr = tmem_base + ((ew * 32) << 16) + acc * BN;
       auto release = [&]() {
         tc_fence_before();
@@ -637,8 +630,9 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
           }
         }
         epilogue_dw_tma(P.a, &tm.m[3 * pi + 2], taddr, m_blk * C::TILE_M + (int)rank * BM, n_blk, ew * 32 + lane,
-                        stg, sbar, sphase, ew == 0 && lane == 0, release);
+                        stg, sbar, sphase, ew == 0 && lane == 0, wait_acc, release);
       } else {
+        wait_acc();
         epilogue_dispatch(P.epi, P.a, taddr, m_blk * C::TILE_M + (int)rank * BM, n_blk, ew * 32 + lane);
         release();
       }
