@@ -327,7 +327,8 @@ __device__ __forceinline__ void epilogue_tile(const GemmArgs& a, uint32_t taddr,
 template <typename WaitAcc, typename ReleaseTmem>
 __device__ __forceinline__ void epilogue_dw_tma(const GemmArgs& a, const CUtensorMap* tmC, uint32_t taddr, int row0,
                                                 int n_blk, int rl, uint8_t* stg, uint64_t* sbar, uint32_t& sphase,
-                                                bool lead, WaitAcc wait_acc, ReleaseTmem release_tmem) {
+                                                bool lead, WaitAcc wait_acc, ReleaseTmem release_tmem,
+                                                int dbg = 0) {
   constexpr uint32_t CHUNK_BYTES = BM * 64 * 2;
   const int n0 = n_blk * BN;
   const int nch = min(BN, a.N - n0 + 63) / 64;  // 64-column chunks with at least one valid column
@@ -336,13 +337,14 @@ __device__ __forceinline__ void epilogue_dw_tma(const GemmArgs& a, const CUtenso
   // The previous tile's stores must have finished reading the buffers.
   if (lead) bulk_wait_read<0>();
   named_bar_sync(1, 128);
+  if (dbg & 2) wait_acc();
   if (rmw && lead) {
     for (int k = 0; k < nch; ++k) {
       mbar_arrive_expect_tx(&sbar[k], CHUNK_BYTES);
       tma_load_2d(tmC, &sbar[k], stg + k * CHUNK_BYTES, n0 + k * 64, row0, policy_evict_normal());
     }
   }
-  wait_acc();
+  if (!(dbg & 2)) wait_acc();
   uint32_t v0[32], v1[32];
   for (int k = 0; k < nch; ++k) {
     tmem_ld32(taddr + k * 64, v0);
@@ -408,6 +410,7 @@ struct GroupArgs {
   Prob p[MAXP];
   int nprob;
   int num_tiles;
+  int dbg;  // timing-experiment knobs (0 in production): 1 = no L2 prefetch, 2 = late old-dW loads
   const int* sched;  // [units][sched_stride] tile ids, -1 terminated (nullptr: round robin)
   int sched_stride;
 };
@@ -488,6 +491,10 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  // PDL: let the next launch's CTAs start their prologue as soon as SMs free up, and wait for the
+  // previous grid (whose outputs we read, and whose inputs we may overwrite) before any global access.
+  griddep_launch_dependents();
+  griddep_wait();
 
   if (warp == 0) {
     if (lane == 0) {
@@ -619,7 +626,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
       if (P.epi == EPI_DW) {
         // Warm L2 with the old dW rows of this unit's next tile while this one is processed.
         const int nt = it.peek();
-        if (ew == 0 && lane == 0 && nt >= 0) {
+        if (ew == 0 && lane == 0 && nt >= 0 && !(g.dbg & 1)) {
           const int npi = prob_of(g, nt);
           const Prob& Q = g.p[npi];
           if (Q.epi == EPI_DW && Q.a.mode == 1) {
@@ -630,7 +637,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
           }
         }
         epilogue_dw_tma(P.a, &tm.m[3 * pi + 2], taddr, m_blk * C::TILE_M + (int)rank * BM, n_blk, ew * 32 + lane,
-                        stg, sbar, sphase, ew == 0 && lane == 0, wait_acc, release);
+                        stg, sbar, sphase, ew == 0 && lane == 0, wait_acc, release, g.dbg);
       } else {
         wait_acc();
         epilogue_dispatch(P.epi, P.a, taddr, m_blk * C::TILE_M + (int)rank * BM, n_blk, ew * 32 + lane);

@@ -255,19 +255,26 @@ slf_status launch_group_cg(DevInfo* dev, ProbSpec* ps, int n, cudaStream_t s, co
   g.num_tiles = total;
   g.sched = sched;
   g.sched_stride = sched_stride;
+  static const int dbg = getenv("SLF_DEBUG_EPI") ? atoi(getenv("SLF_DEBUG_EPI")) : 0;  // timing experiments only
+  g.dbg = dbg;
   const int units = sched ? dev->sms / CG : std::min(total, dev->sms / CG);
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((unsigned)(units * CG));
   cfg.blockDim = dim3(GEMM_THREADS);
   cfg.dynamicSmemBytes = C::SMEM_BYTES;
   cfg.stream = s;
-  cudaLaunchAttribute attr[1];
+  cudaLaunchAttribute attr[2];
   attr[0].id = cudaLaunchAttributeClusterDimension;
   attr[0].val.clusterDim.x = CG;
   attr[0].val.clusterDim.y = 1;
   attr[0].val.clusterDim.z = 1;
+  // Programmatic dependent launch: this grid's CTAs may start (prologue: barrier init, TMEM
+  // alloc, descriptor prefetch) while the previous kernel drains; griddepcontrol.wait in the
+  // kernel holds every global-memory access until the previous grid has completed.
+  attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[1].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = 2;
   ProfScope pscope(prof_kind >= 0 ? prof_kind : prof_kind_of(g.p[0].epi), s, flops, 0.0);
   SLF_CUDA(cudaLaunchKernelEx(&cfg, kfn, tm, g));
   return SLF_OK;
@@ -680,6 +687,8 @@ slf_status phase_s(Ctx& c, const void* X, const void* W, const int32_t* t, int64
       q.a.out = dW;
       q.a.ld_out = H;
       q.a.mode = ch > 0 ? 1 : 0;
+      static const bool no_rmw = getenv("SLF_DEBUG_DW_NO_RMW") != nullptr;  // timing experiments only (wrong dW)
+      if (no_rmw) q.a.mode = 0;
       SLF_TRY(tmap_kmajor(&q.tc, dW, H, V, H, BM));
       finish_geometry(q.a, cg);
     }
