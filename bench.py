@@ -210,7 +210,7 @@ def main():
     extra = ws.numel()
     if g > 1:
         from paper_2603_16428_b200.sharded import VocabShardedLCE
-        sharded = VocabShardedLCE(V, budget_bytes=args.budget)
+        sharded = VocabShardedLCE(V, budget_bytes=args.budget, schedule="R" if args.schedule == "R" else "S")
         assert (sharded.v0, sharded.v1) == (v0, v1)
         extra += g * N * 16 + N * H * 4  # gathered statistics + fp32 dX partial
 
@@ -334,7 +334,7 @@ def main():
                    "targets": args.dist, "logit_std": args.alpha, "ignore_frac": 0.05,
                    "l2": "inputs larger than L2 (W alone is %.2f GB vs 126 MB L2); no flush" % (V_l * H * 2 / 1e9),
                    "plan": slf.plan_describe(N, H, V_l, budget_bytes=args.budget,
-                                             schedule=args.schedule if g == 1 else "R")},
+                                             schedule=args.schedule)},
         "tflops": tflops, "frac_of_peak_burst": tflops / peaks["burst"],
         "frac_of_peak_sustained": tflops / peaks["sustained"],
         "roofline": {"bound": "tensor", "kernel": dom_name, "achieved": achieved, "peak": peaks["sustained"],

@@ -164,6 +164,44 @@ slf_status slf_lce_bwd(const void* hidden, const void* weight, const int32_t* ta
                        void* dweight, void* workspace, size_t workspace_bytes, size_t budget_bytes,
                        void* stream);
 
+/* ---- schedule S split for vocab shards ----
+ * Each rank owns W rows [vocab_start, vocab_start + V_local).  Per step:
+ *   slf_lce_s_begin                                  targets scan + this shard's target CSR
+ *   for chunk c in [0, n_chunks):   (rows [c*chunk_rows, min(N, (c+1)*chunk_rows)))
+ *     slf_lce_s_chunk_stats(c) -> shardstat_chunk [rows_c]      stash GEMM + local row merge
+ *     caller: gather the g shards' shardstat_chunk in rank order -> stats [g][rows_c]
+ *     slf_lce_s_chunk_bwd(c, stats, g) -> dhidden rows of the chunk (fp32 partial: sum it across
+ *         shards, then slf_lce_dx_finalize those rows with the chunk's RowStat), dW (+)=
+ *   slf_lce_s_end                                    one-hot dW correction, loss
+ * The same workspace must be used for all calls of a step; chunk_rows / n_chunks come from
+ * slf_lce_s_plan for the same (N, H, V_local, budget).  Rowstats of the step are kept in the
+ * workspace; slf_lce_s_rowstat returns a device pointer to them (for slf_lce_dx_finalize). */
+slf_status slf_lce_s_plan(int64_t N, int64_t H, int64_t V_local, size_t budget_bytes, int64_t* chunk_rows,
+                          int64_t* n_chunks);
+slf_status slf_lce_s_begin(const int32_t* targets, int64_t N, int64_t H, int64_t V_local, int64_t vocab_start,
+                           int64_t V_global, int32_t ignore_index, int need_dweight, void* workspace,
+                           size_t workspace_bytes, size_t budget_bytes, void* stream);
+slf_status slf_lce_s_chunk_stats(const void* hidden, const void* weight_shard, const int32_t* targets, int64_t N,
+                                 int64_t H, int64_t V_local, int64_t vocab_start, int64_t V_global,
+                                 int32_t ignore_index, int64_t chunk, slf_shardstat* shardstat_chunk, void* workspace,
+                                 size_t workspace_bytes, size_t budget_bytes, void* stream);
+/* dhidden_chunk: row 0 of the chunk's rows ([rows_c, H]; fp32 if dhidden_fp32 else bf16; may be
+ * NULL); dweight: [V_local, H] bf16 (may be NULL; must be the same buffer for every chunk);
+ * loss_rows: DEVICE fp32 [N] for SUM/MEAN may be NULL (kept in the workspace), for NONE the
+ * caller's per-row loss buffer. */
+slf_status slf_lce_s_chunk_bwd(const void* hidden, const void* weight_shard, const int32_t* targets, int64_t N,
+                               int64_t H, int64_t V_local, int64_t vocab_start, int64_t V_global,
+                               int32_t ignore_index, int reduction, float scale, int64_t chunk,
+                               const slf_shardstat* stats, int g, float* loss_rows, void* dhidden_chunk,
+                               int dhidden_fp32, void* dweight, void* workspace, size_t workspace_bytes,
+                               size_t budget_bytes, void* stream);
+slf_status slf_lce_s_end(const void* hidden, int64_t N, int64_t H, int64_t V_local, int reduction, float scale,
+                         float* loss_out, void* dweight, void* workspace, size_t workspace_bytes, size_t budget_bytes,
+                         void* stream);
+/* DEVICE pointer (in *out) to the step's RowStat array [N] inside `workspace` (schedule S). */
+slf_status slf_lce_s_rowstat(int64_t N, int64_t H, int64_t V_local, size_t budget_bytes, void* workspace,
+                             const slf_rowstat** out);
+
 /* Synchronises `stream` and returns (in *bad_targets, HOST) the number of
  * valid targets outside [0, V_global) seen by the last call that used this
  * workspace, and (in *n_valid, HOST, may be NULL) the number of valid rows. */

@@ -21,7 +21,9 @@ SCHEDULES = {"auto": 0, "R": 1, "S": 2}
 # Every symbol include/slf_lce.h declares.
 EXPORTS = ["slf_lce_version", "slf_last_error_string", "slf_lce_workspace_bytes", "slf_lce_plan_describe",
            "slf_lce_fwd_bwd", "slf_lce_fwd", "slf_lce_fwd_shard_stats", "slf_lce_stats_combine", "slf_lce_bwd",
-           "slf_lce_status", "slf_debug_gemm", "slf_lce_dx_finalize", "slf_profile_begin", "slf_profile_end"]
+           "slf_lce_status", "slf_debug_gemm", "slf_lce_dx_finalize", "slf_profile_begin", "slf_profile_end",
+           "slf_lce_s_plan", "slf_lce_s_begin", "slf_lce_s_chunk_stats", "slf_lce_s_chunk_bwd", "slf_lce_s_end",
+           "slf_lce_s_rowstat"]
 PROF_KINDS = ["gemm_stats", "gemm_grad", "gemm_dw", "gemm_dx", "gemm_debug", "prep", "local_combine", "final_combine",
               "dx_finalize", "gemm_group", "combine_transform", "csr", "onehot", "loss_reduce", "k14", "k15"]
 
@@ -56,6 +58,13 @@ def _declare(lib):
         "slf_lce_dx_finalize": (INT, [P, P, P, I64, I64, P]),
         "slf_profile_begin": (INT, []),
         "slf_profile_end": (INT, [P, P, P, P]),
+        "slf_lce_s_plan": (INT, [I64, I64, I64, SZ, ctypes.POINTER(I64), ctypes.POINTER(I64)]),
+        "slf_lce_s_begin": (INT, [P, I64, I64, I64, I64, I64, I32, INT, P, SZ, SZ, P]),
+        "slf_lce_s_chunk_stats": (INT, [P, P, P, I64, I64, I64, I64, I64, I32, I64, P, P, SZ, SZ, P]),
+        "slf_lce_s_chunk_bwd": (INT, [P, P, P, I64, I64, I64, I64, I64, I32, INT, F32, I64, P, INT, P, P, INT, P, P,
+                                      SZ, SZ, P]),
+        "slf_lce_s_end": (INT, [P, I64, I64, I64, INT, F32, P, P, P, SZ, SZ, P]),
+        "slf_lce_s_rowstat": (INT, [I64, I64, I64, SZ, P, ctypes.POINTER(P)]),
     }
     for name, (res, args) in sig.items():
         f = getattr(lib, name)

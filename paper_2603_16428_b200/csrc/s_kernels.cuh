@@ -21,55 +21,48 @@ __device__ __forceinline__ float coef_of(int reduction, float scale, unsigned lo
   return (reduction == SLF_MEAN) ? (n_valid ? scale / (float)n_valid : 0.f) : scale;
 }
 
-// One block (256 threads) per row of the chunk.  Fixed-order reductions (deterministic).
+// One block (256 threads) per row of the chunk.  The row's global statistics come from the g
+// shards' ShardStats (fixed shard order; g = 1 on one GPU), the per-tile rescale factors from this
+// shard's own tile partials.  Deterministic.
 __global__ void __launch_bounds__(256) combine_transform_kernel(
-    const float2* __restrict__ partials, int tiles, int rows, const float* __restrict__ zt,
-    const int32_t* __restrict__ t, int64_t V, int64_t ld_stash, int32_t ignore_index, int reduction, float scale,
-    float grad_scale, const WsHeader* __restrict__ hdr, float* __restrict__ loss_rows,
-    slf_rowstat* __restrict__ rowstat, uint16_t* __restrict__ stash) {
+    const slf_shardstat* __restrict__ st, int g, const float2* __restrict__ partials, int tiles, int rows,
+    const int32_t* __restrict__ t, int64_t vocab_start, int64_t V_l, int64_t V_global, int64_t ld_stash,
+    int32_t ignore_index, int reduction, float scale, float grad_scale, const WsHeader* __restrict__ hdr,
+    float* __restrict__ loss_rows, slf_rowstat* __restrict__ rowstat, uint16_t* __restrict__ stash) {
   extern __shared__ float r_t[];  // [tiles]
-  __shared__ float red[256];
+  __shared__ float sM, sLse;
   const int i = blockIdx.x;
   const int tid = threadIdx.x;
-  float m = -INFINITY;
-  for (int k = tid; k < tiles; k += 256) m = fmaxf(m, partials[(size_t)k * rows + i].x);
-  red[tid] = m;
-  __syncthreads();
-  for (int o = 128; o > 0; o >>= 1) {
-    if (tid < o) red[tid] = fmaxf(red[tid], red[tid + o]);
-    __syncthreads();
-  }
-  const float M = red[0];
-  __syncthreads();
-  float s = 0.f;
-  for (int k = tid; k < tiles; k += 256) {
-    const float2 p = partials[(size_t)k * rows + i];
-    s += p.y * ex2((p.x - M) * LOG2E);
-  }
-  red[tid] = s;
-  __syncthreads();
-  for (int o = 128; o > 0; o >>= 1) {
-    if (tid < o) red[tid] += red[tid + o];
-    __syncthreads();
-  }
-  const float lse = M + logf(red[0]);
-  const int32_t tt = t[i];
-  const bool valid = tt != ignore_index;
-  const bool bad = valid && (tt < 0 || (int64_t)tt >= V);
-  const float coef = (valid && !bad) ? coef_of(reduction, scale, hdr->n_valid) : 0.f;
   if (tid == 0) {
-    float l = valid ? (lse - zt[i]) : 0.f;
+    float M = -INFINITY;
+    for (int k = 0; k < g; ++k) M = fmaxf(M, st[(size_t)k * rows + i].m);
+    float S = 0.f, z = 0.f;
+    for (int k = 0; k < g; ++k) {
+      const slf_shardstat q = st[(size_t)k * rows + i];
+      S += q.s * ex2((q.m - M) * LOG2E);
+      z += q.zt;  // exactly one shard has the target (the others store 0)
+    }
+    const float lse = M + logf(S);
+    const int32_t tt = t[i];
+    const bool valid = tt != ignore_index;
+    const bool bad = valid && (tt < 0 || (int64_t)tt >= V_global);
+    const float coef = (valid && !bad) ? coef_of(reduction, scale, hdr->n_valid) : 0.f;
+    float l = valid ? (lse - z) : 0.f;
     if (bad) l = __int_as_float(0x7fc00000);
     loss_rows[i] = l;
-    rowstat[i] = slf_rowstat{lse * LOG2E, coef, (valid && !bad) ? tt : -1, valid ? 1 : 0};
+    const int64_t loc = (int64_t)tt - vocab_start;
+    const int32_t tloc = (valid && !bad && loc >= 0 && loc < V_l) ? (int32_t)loc : -1;
+    rowstat[i] = slf_rowstat{lse * LOG2E, coef, tloc, valid ? 1 : 0};
+    sM = coef * grad_scale;
+    sLse = lse * LOG2E;
   }
-  const float cg = coef * grad_scale;
-  const float lse2 = lse * LOG2E;
+  __syncthreads();
+  const float cg = sM, lse2 = sLse;
   for (int k = tid; k < tiles; k += 256) r_t[k] = cg * ex2(partials[(size_t)k * rows + i].x * LOG2E - lse2);
   __syncthreads();
   // G_P = p~ * r_t, in place, 8 bf16 per 16-byte access.
   uint4* row = reinterpret_cast<uint4*>(stash + (size_t)i * ld_stash);
-  const int64_t groups = (V + 7) / 8;
+  const int64_t groups = (V_l + 7) / 8;
   for (int64_t q = tid; q < groups; q += 256) {
     const float r = r_t[(q * 8) / 256];
     uint4 w = row[q];

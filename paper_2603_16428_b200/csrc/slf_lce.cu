@@ -385,7 +385,8 @@ bool plan_s(int64_t N, int64_t H, int64_t V, size_t budget, Plan* out) {
   p.off_off = align_up(p.off_cnt + (size_t)(V + 2) * 4, 1024);
   p.off_hits = align_up(p.off_off + (size_t)(V + 2) * 4, 1024);
   p.off_idx = align_up(p.off_hits + (size_t)std::min(N, V) * 4, 1024);
-  p.off_part = align_up(p.off_idx + (size_t)N * 4, 1024);
+  p.off_shard = align_up(p.off_idx + (size_t)N * 4, 1024);  // per-chunk ShardStat (g = 1 path)
+  p.off_part = align_up(p.off_shard + (size_t)N * 16, 1024);
   const int64_t tiles_v = (V + BN - 1) / BN;
   p.ld_stash = (int64_t)align_up((size_t)V, 8);
   const int64_t Nmax = (int64_t)align_up((size_t)N, 256);
@@ -619,144 +620,206 @@ slf_status phase_backward(Ctx& c, const void* X, const void* W, const slf_rowsta
   return SLF_OK;
 }
 
-// Schedule S (single GPU): per row chunk, ONE forward GEMM whose epilogue keeps the tile
-// statistics and stashes p~ = bf16(exp(z - m_tile)); combine + in-place transform to the softmax
-// term G_P; ONE grouped launch of dX_chunk = G_P W (- coef W[t], exact, epilogue) and
-// dW (+)= G_P^T X_chunk; finally dW[v] -= coef sum_{t_i = v} x_i from the target CSR.  No logits
-// are recomputed: 6 N H V tensor FLOPs.
+// ---- schedule S ---------------------------------------------------------------------------------
+// Per row chunk, ONE forward GEMM whose epilogue keeps the tile statistics and stashes
+// p~ = bf16(exp(z - m_tile)); the g shards' row statistics are merged and the stash is rescaled in
+// place into the softmax term G_P; ONE grouped launch of dX_chunk = G_P W (- coef W[t], exact, in
+// the epilogue) and dW (+)= G_P^T X_chunk; finally dW[v] -= coef sum_{t_i = v} x_i from the target
+// CSR.  No logits are recomputed: 6 N H V tensor FLOPs.  The pieces below are used by the fused
+// single-GPU call (g = 1) and by the vocab-shard split API (the caller gathers the per-chunk
+// statistics and all-reduces the per-chunk fp32 dX partials).
+struct SArgs {
+  const void* X;
+  const void* W;  // this shard's rows [vocab_start, vocab_start + V_l)
+  const int32_t* t;
+  int64_t N, H, V_l, vs, Vg;
+  int32_t ign;
+};
+
+slf_status s_begin(Ctx& c, const SArgs& a, bool need_dw) {
+  const Plan& p = c.plan;
+  SLF_TRY(launch_prep(c, a.t, a.N, a.ign, a.Vg));
+  if (need_dw) {
+    int32_t* cnt = reinterpret_cast<int32_t*>(c.ws + p.off_cnt);
+    int32_t* off = reinterpret_cast<int32_t*>(c.ws + p.off_off);
+    int32_t* hits = reinterpret_cast<int32_t*>(c.ws + p.off_hits);
+    int32_t* idx = reinterpret_cast<int32_t*>(c.ws + p.off_idx);
+    ProfScope ps(SLF_PROF_CSR, c.s, 0.0, (double)a.V_l * 12 + (double)a.N * 12);
+    csr_zero_kernel<<<(unsigned)std::min<int64_t>((a.V_l + 2 + 255) / 256, 1024), 256, 0, c.s>>>(cnt, a.V_l + 2);
+    csr_count_kernel<<<(unsigned)((a.N + 255) / 256), 256, 0, c.s>>>(a.t, a.N, a.ign, a.vs, a.V_l, cnt);
+    csr_scan_kernel<<<1, 1024, 0, c.s>>>(cnt, a.V_l, off, hits);
+    csr_scatter_kernel<<<(unsigned)((a.N + 255) / 256), 256, 0, c.s>>>(a.t, a.N, a.ign, a.vs, a.V_l, cnt, off, idx);
+    SLF_CUDA(cudaGetLastError());
+  }
+  return SLF_OK;
+}
+
+// Stash GEMM of chunk `ch` and this shard's per-row statistics of the chunk (out[rows]).
+slf_status s_chunk_stats(Ctx& c, const SArgs& a, int64_t ch, slf_shardstat* out) {
+  const Plan& p = c.plan;
+  const int64_t r0 = ch * p.C, rows = std::min(p.C, a.N - r0);
+  float* zt = reinterpret_cast<float*>(c.ws + p.off_zt);
+  float2* part = reinterpret_cast<float2*>(c.ws + p.off_part);
+  CUtensorMap ta, tb;
+  SLF_TRY(tmap_kmajor(&ta, reinterpret_cast<const uint8_t*>(a.X) + (size_t)r0 * a.H * 2, a.H, rows, a.H, BM));
+  SLF_TRY(tmap_kmajor(&tb, a.W, a.H, a.V_l, a.H, b_box_rows()));
+  GemmArgs g{};
+  g.M = (int)rows;
+  g.N = (int)a.V_l;
+  g.K = (int)a.H;
+  g.targets = a.t + r0;
+  g.tcol0 = a.vs;
+  g.ignore_index = a.ign;
+  g.partials = part;
+  g.zt = zt + r0;
+  g.out = c.ws + p.off_stash;
+  g.ld_out = p.ld_stash;
+  SLF_TRY((launch_gemm<EPI_STASH, false, false>(c.dev, ta, tb, g, c.s)));
+  const int tiles_v = (int)((a.V_l + BN - 1) / BN);
+  ProfScope ps(SLF_PROF_LOCAL_COMBINE, c.s, 0.0, (double)rows * (tiles_v * 8.0 + 24));
+  local_combine_kernel<<<(unsigned)((rows + 255) / 256), 256, 0, c.s>>>(part, tiles_v, zt + r0, a.t + r0, rows,
+                                                                        a.vs, a.V_l, a.ign, out);
+  SLF_CUDA(cudaGetLastError());
+  return SLF_OK;
+}
+
+slf_status s_build_bwd(Ctx& c, const SArgs& a, int64_t ch, void* dXc, int dx_fp32, void* dW, ProbSpec* ps, int* n) {
+  const Plan& p = c.plan;
+  const int cg = cta_group();
+  const int64_t r0 = ch * p.C, rows = std::min(p.C, a.N - r0);
+  const uint8_t* Xr = reinterpret_cast<const uint8_t*>(a.X) + (size_t)r0 * a.H * 2;
+  uint8_t* stash = c.ws + p.off_stash;
+  slf_rowstat* rs = reinterpret_cast<slf_rowstat*>(c.ws + p.off_rowstat);
+  *n = 0;
+  if (dXc) {  // dX_chunk = G_P W : A = G_P (K-major over V_l), B = W (MN-major)
+    ProbSpec& q = ps[(*n)++];
+    SLF_TRY(tmap_kmajor(&q.ta, stash, a.V_l, rows, p.ld_stash, BM));
+    SLF_TRY(tmap_mnmajor(&q.tb, a.W, a.H, a.V_l, a.H));
+    q.epi = EPI_DXS;
+    q.a_mn = false;
+    q.b_mn = true;
+    q.a = GemmArgs{};
+    q.a.M = (int)rows;
+    q.a.N = (int)a.H;
+    q.a.K = (int)a.V_l;
+    q.a.rowstat = rs + r0;
+    q.a.grad_scale = 1.0f;
+    q.a.wrow = reinterpret_cast<const uint16_t*>(a.W);
+    q.a.ld_w = a.H;
+    q.a.out = dXc;
+    q.a.ld_out = a.H;
+    q.a.mode = dx_fp32 ? 1 : 0;
+    finish_geometry(q.a, cg);
+  }
+  if (dW) {  // dW (+)= G_P^T X_chunk : A = G_P^T (MN-major), B = X_chunk (MN-major)
+    ProbSpec& q = ps[(*n)++];
+    SLF_TRY(tmap_mnmajor(&q.ta, stash, a.V_l, rows, p.ld_stash));
+    SLF_TRY(tmap_mnmajor(&q.tb, Xr, a.H, rows, a.H));
+    q.epi = EPI_DW;
+    q.a_mn = q.b_mn = true;
+    q.a = GemmArgs{};
+    q.a.M = (int)a.V_l;
+    q.a.N = (int)a.H;
+    q.a.K = (int)rows;
+    q.a.out = dW;
+    q.a.ld_out = a.H;
+    q.a.mode = ch > 0 ? 1 : 0;
+    static const bool no_rmw = getenv("SLF_DEBUG_DW_NO_RMW") != nullptr;  // timing experiments only (wrong dW)
+    if (no_rmw) q.a.mode = 0;
+    SLF_TRY(tmap_kmajor(&q.tc, dW, a.H, a.V_l, a.H, BM));
+    finish_geometry(q.a, cg);
+  }
+  return SLF_OK;
+}
+
+// Merge the g shards' statistics of chunk `ch` (st[g][rows], shard order), transform the stash in
+// place, and run the grouped dX/dW launch.  dXc = row 0 of the chunk's dhidden rows (bf16, or fp32
+// when dx_fp32: this shard's partial, to be summed across shards).  `sched` (optional) is a
+// prebuilt LPT table for this chunk shape; otherwise one is built and uploaded.
+slf_status s_chunk_bwd(Ctx& c, const SArgs& a, int64_t ch, const slf_shardstat* st, int g, int reduction, float scale,
+                       float* loss_rows_all, void* dXc, int dx_fp32, void* dW, const int* sched = nullptr,
+                       int sched_stride = 0) {
+  const Plan& p = c.plan;
+  const int64_t r0 = ch * p.C, rows = std::min(p.C, a.N - r0);
+  const int tiles_v = (int)((a.V_l + BN - 1) / BN);
+  {
+    ProfScope ps(SLF_PROF_COMBINE_TRANSFORM, c.s, 0.0, (double)rows * (tiles_v * 8.0 + a.V_l * 4.0 + 16.0 * g + 24));
+    combine_transform_kernel<<<(unsigned)rows, 256, tiles_v * sizeof(float), c.s>>>(
+        st, g, reinterpret_cast<const float2*>(c.ws + p.off_part), tiles_v, (int)rows, a.t + r0, a.vs, a.V_l, a.Vg,
+        p.ld_stash, a.ign, reduction, scale, 1.0f, hdr_of(c.ws), loss_rows_all + r0,
+        reinterpret_cast<slf_rowstat*>(c.ws + p.off_rowstat) + r0, reinterpret_cast<uint16_t*>(c.ws + p.off_stash));
+    SLF_CUDA(cudaGetLastError());
+  }
+  if (!dXc && !dW) return SLF_OK;
+  ProbSpec ps[2];
+  int n = 0;
+  SLF_TRY(s_build_bwd(c, a, ch, dXc, dx_fp32, dW, ps, &n));
+  SchedArena arena;
+  if (!sched) {
+    const int k = arena.add(ps, n, c.dev->sms / cta_group());
+    SLF_TRY(arena.upload(c));
+    sched = arena.dev(c, k);
+    sched_stride = arena.tables[k].second;
+  }
+  return launch_group(c.dev, ps, n, c.s, sched, sched_stride, n == 2 ? SLF_PROF_GEMM_GROUP : -1);
+}
+
+slf_status s_end(Ctx& c, const SArgs& a, int reduction, float scale, float* loss_out, void* dW) {
+  const Plan& p = c.plan;
+  if (dW) {
+    ProfScope ps(SLF_PROF_ONEHOT, c.s, 0.0, (double)a.N * a.H * 2 * 2);
+    dim3 grid((unsigned)std::min<int64_t>(a.N, a.V_l), (unsigned)((a.H + 1023) / 1024));
+    onehot_kernel<<<grid, 128, 0, c.s>>>(reinterpret_cast<const uint16_t*>(a.X), a.H,
+                                         reinterpret_cast<const int32_t*>(c.ws + p.off_off),
+                                         reinterpret_cast<const int32_t*>(c.ws + p.off_idx),
+                                         reinterpret_cast<const int32_t*>(c.ws + p.off_hits), a.V_l, reduction, scale,
+                                         1.0f, hdr_of(c.ws), reinterpret_cast<uint16_t*>(dW));
+    SLF_CUDA(cudaGetLastError());
+  }
+  if (reduction != SLF_NONE) {
+    ProfScope ps(SLF_PROF_LOSS_REDUCE, c.s, 0.0, (double)a.N * 4);
+    loss_reduce_kernel<<<1, 1024, 0, c.s>>>(reinterpret_cast<const float*>(c.ws + p.off_loss), a.N, reduction,
+                                            hdr_of(c.ws), loss_out);
+    SLF_CUDA(cudaGetLastError());
+  }
+  return SLF_OK;
+}
+
+float* s_loss_rows(Ctx& c, int reduction, float* loss_out) {
+  return reduction == SLF_NONE ? loss_out : reinterpret_cast<float*>(c.ws + c.plan.off_loss);
+}
+
+// The fused single-GPU call under schedule S (g = 1: a chunk's statistics are its own).
 slf_status phase_s(Ctx& c, const void* X, const void* W, const int32_t* t, int64_t N, int64_t H, int64_t V,
                    int32_t ignore_index, int reduction, float scale, float* loss_out, void* dX, void* dW) {
   const Plan& p = c.plan;
-  const int cg = cta_group();
-  const int units = c.dev->sms / cg;
-  slf_rowstat* rs = reinterpret_cast<slf_rowstat*>(c.ws + p.off_rowstat);
-  float* zt = reinterpret_cast<float*>(c.ws + p.off_zt);
-  float* loss_rows = reduction == SLF_NONE ? loss_out : reinterpret_cast<float*>(c.ws + p.off_loss);
-  int32_t* cnt = reinterpret_cast<int32_t*>(c.ws + p.off_cnt);
-  int32_t* off = reinterpret_cast<int32_t*>(c.ws + p.off_off);
-  int32_t* hits = reinterpret_cast<int32_t*>(c.ws + p.off_hits);
-  int32_t* idx = reinterpret_cast<int32_t*>(c.ws + p.off_idx);
-  float2* part = reinterpret_cast<float2*>(c.ws + p.off_part);
-  uint16_t* stash = reinterpret_cast<uint16_t*>(c.ws + p.off_stash);
-  const int tiles_v = (int)((V + BN - 1) / BN);
-
-  SLF_TRY(launch_prep(c, t, N, ignore_index, V));
-  if (dW) {
-    ProfScope ps(SLF_PROF_CSR, c.s, 0.0, (double)V * 12 + (double)N * 12);
-    csr_zero_kernel<<<std::min<int64_t>((V + 2 + 255) / 256, 1024), 256, 0, c.s>>>(cnt, V + 2);
-    csr_count_kernel<<<(unsigned)((N + 255) / 256), 256, 0, c.s>>>(t, N, ignore_index, 0, V, cnt);
-    csr_scan_kernel<<<1, 1024, 0, c.s>>>(cnt, V, off, hits);
-    csr_scatter_kernel<<<(unsigned)((N + 255) / 256), 256, 0, c.s>>>(t, N, ignore_index, 0, V, cnt, off, idx);
-    SLF_CUDA(cudaGetLastError());
-  }
-
-  auto build_bwd = [&](int64_t ch, ProbSpec* ps, int* n) -> slf_status {
-    const int64_t r0 = ch * p.C, rows = std::min(p.C, N - r0);
-    const uint8_t* Xr = reinterpret_cast<const uint8_t*>(X) + (size_t)r0 * H * 2;
-    *n = 0;
-    if (dX) {  // dX_chunk = G_P W : A = G_P (K-major over V), B = W (MN-major)
-      ProbSpec& q = ps[(*n)++];
-      SLF_TRY(tmap_kmajor(&q.ta, stash, V, rows, p.ld_stash, BM));
-      SLF_TRY(tmap_mnmajor(&q.tb, W, H, V, H));
-      q.epi = EPI_DXS;
-      q.a_mn = false;
-      q.b_mn = true;
-      q.a = GemmArgs{};
-      q.a.M = (int)rows;
-      q.a.N = (int)H;
-      q.a.K = (int)V;
-      q.a.rowstat = rs + r0;
-      q.a.grad_scale = 1.0f;
-      q.a.wrow = reinterpret_cast<const uint16_t*>(W);
-      q.a.ld_w = H;
-      q.a.out = reinterpret_cast<uint8_t*>(dX) + (size_t)r0 * H * 2;
-      q.a.ld_out = H;
-      q.a.mode = 0;
-      finish_geometry(q.a, cg);
-    }
-    if (dW) {  // dW (+)= G_P^T X_chunk : A = G_P^T (MN-major), B = X_chunk (MN-major)
-      ProbSpec& q = ps[(*n)++];
-      SLF_TRY(tmap_mnmajor(&q.ta, stash, V, rows, p.ld_stash));
-      SLF_TRY(tmap_mnmajor(&q.tb, Xr, H, rows, H));
-      q.epi = EPI_DW;
-      q.a_mn = q.b_mn = true;
-      q.a = GemmArgs{};
-      q.a.M = (int)V;
-      q.a.N = (int)H;
-      q.a.K = (int)rows;
-      q.a.out = dW;
-      q.a.ld_out = H;
-      q.a.mode = ch > 0 ? 1 : 0;
-      static const bool no_rmw = getenv("SLF_DEBUG_DW_NO_RMW") != nullptr;  // timing experiments only (wrong dW)
-      if (no_rmw) q.a.mode = 0;
-      SLF_TRY(tmap_kmajor(&q.tc, dW, H, V, H, BM));
-      finish_geometry(q.a, cg);
-    }
-    return SLF_OK;
-  };
-
+  const SArgs a{X, W, t, N, H, V, 0, V, ignore_index};
+  SLF_TRY(s_begin(c, a, dW != nullptr));
+  // LPT tables for the full and the ragged last chunk, uploaded once.
   SchedArena arena;
   int k_full = -1, k_last = -1;
   if (dX || dW) {
     ProbSpec ps[2];
     int n = 0;
-    SLF_TRY(build_bwd(0, ps, &n));
-    k_full = arena.add(ps, n, units);
+    SLF_TRY(s_build_bwd(c, a, 0, dX, 0, dW, ps, &n));
+    k_full = arena.add(ps, n, c.dev->sms / cta_group());
     if (N % p.C) {
-      SLF_TRY(build_bwd(p.nCh - 1, ps, &n));
-      k_last = arena.add(ps, n, units);
+      SLF_TRY(s_build_bwd(c, a, p.nCh - 1, dX, 0, dW, ps, &n));
+      k_last = arena.add(ps, n, c.dev->sms / cta_group());
     }
     SLF_TRY(arena.upload(c));
   }
-
+  slf_shardstat* st = reinterpret_cast<slf_shardstat*>(c.ws + p.off_shard);
+  float* loss_rows = s_loss_rows(c, reduction, loss_out);
   for (int64_t ch = 0; ch < p.nCh; ++ch) {
     const int64_t r0 = ch * p.C, rows = std::min(p.C, N - r0);
-    {  // forward: statistics + p~ stash
-      CUtensorMap ta, tb;
-      SLF_TRY(tmap_kmajor(&ta, reinterpret_cast<const uint8_t*>(X) + (size_t)r0 * H * 2, H, rows, H, BM));
-      SLF_TRY(tmap_kmajor(&tb, W, H, V, H, b_box_rows()));
-      GemmArgs a{};
-      a.M = (int)rows;
-      a.N = (int)V;
-      a.K = (int)H;
-      a.targets = t + r0;
-      a.tcol0 = 0;
-      a.ignore_index = ignore_index;
-      a.partials = part;
-      a.zt = zt + r0;
-      a.out = stash;
-      a.ld_out = p.ld_stash;
-      SLF_TRY((launch_gemm<EPI_STASH, false, false>(c.dev, ta, tb, a, c.s)));
-    }
-    {
-      ProfScope ps(SLF_PROF_COMBINE_TRANSFORM, c.s, 0.0, (double)rows * (tiles_v * 8.0 + V * 4.0 + 24));
-      combine_transform_kernel<<<(unsigned)rows, 256, tiles_v * sizeof(float), c.s>>>(
-          part, tiles_v, (int)rows, zt + r0, t + r0, V, p.ld_stash, ignore_index, reduction, scale, 1.0f,
-          hdr_of(c.ws), loss_rows + r0, rs + r0, stash);
-      SLF_CUDA(cudaGetLastError());
-    }
-    if (dX || dW) {
-      ProbSpec ps[2];
-      int n = 0;
-      SLF_TRY(build_bwd(ch, ps, &n));
-      const int k = (rows == p.C || k_last < 0) ? k_full : k_last;
-      SLF_TRY(launch_group(c.dev, ps, n, c.s, arena.dev(c, k), arena.tables[k].second,
-                           n == 2 ? SLF_PROF_GEMM_GROUP : -1));
-    }
+    SLF_TRY(s_chunk_stats(c, a, ch, st));
+    const int k = (rows == p.C || k_last < 0) ? k_full : k_last;
+    SLF_TRY(s_chunk_bwd(c, a, ch, st, 1, reduction, scale, loss_rows,
+                        dX ? reinterpret_cast<uint8_t*>(dX) + (size_t)r0 * H * 2 : nullptr, 0, dW,
+                        k >= 0 ? arena.dev(c, k) : nullptr, k >= 0 ? arena.tables[k].second : 0));
   }
-  if (dW) {
-    ProfScope ps(SLF_PROF_ONEHOT, c.s, 0.0, (double)N * H * 2 * 2);
-    dim3 grid((unsigned)std::min<int64_t>(N, V), (unsigned)((H + 1023) / 1024));
-    onehot_kernel<<<grid, 128, 0, c.s>>>(reinterpret_cast<const uint16_t*>(X), H, off, idx, hits, V, reduction, scale,
-                                         1.0f, hdr_of(c.ws), reinterpret_cast<uint16_t*>(dW));
-    SLF_CUDA(cudaGetLastError());
-  }
-  if (reduction != SLF_NONE) {
-    ProfScope ps(SLF_PROF_LOSS_REDUCE, c.s, 0.0, (double)N * 4);
-    loss_reduce_kernel<<<1, 1024, 0, c.s>>>(loss_rows, N, reduction, hdr_of(c.ws), loss_out);
-    SLF_CUDA(cudaGetLastError());
-  }
-  return SLF_OK;
+  return s_end(c, a, reduction, scale, loss_out, dW);
 }
 
 // Plan selection: SLF_SCHED_S for the fused single-GPU call when it fits (no recompute),
@@ -904,6 +967,89 @@ slf_status slf_lce_bwd(const void* hidden, const void* weight, const int32_t* ta
   Ctx c;
   SLF_TRY(setup(c, N, H, V_local, budget_bytes, workspace, workspace_bytes, stream));
   SLF_TRY(phase_backward(c, hidden, weight, rowstat, N, H, V_local, grad_scale, dhidden, dhidden_fp32, dweight));
+  return SLF_OK;
+}
+
+// ---- schedule S split (vocab shards) ----------------------------------------------------------------
+static slf_status setup_s(Ctx& c, int64_t N, int64_t H, int64_t V_l, size_t budget, void* ws, size_t ws_bytes,
+                          void* stream) {
+  return setup(c, N, H, V_l, budget, ws, ws_bytes, stream, SLF_SCHED_S, true);
+}
+
+slf_status slf_lce_s_plan(int64_t N, int64_t H, int64_t V_local, size_t budget_bytes, int64_t* chunk_rows,
+                          int64_t* n_chunks) {
+  if (!chunk_rows || !n_chunks) return fail(SLF_ERR_ARG, "null output");
+  Plan p;
+  if (!plan_s(N, H, V_local, budget_bytes, &p)) return fail(SLF_ERR_WORKSPACE, "no schedule-S plan fits the budget");
+  *chunk_rows = p.C;
+  *n_chunks = p.nCh;
+  return SLF_OK;
+}
+
+slf_status slf_lce_s_begin(const int32_t* targets, int64_t N, int64_t H, int64_t V_local, int64_t vocab_start,
+                           int64_t V_global, int32_t ignore_index, int need_dweight, void* workspace,
+                           size_t workspace_bytes, size_t budget_bytes, void* stream) {
+  if (!targets || !workspace) return fail(SLF_ERR_ARG, "null required pointer");
+  if (!aligned16(targets) || !aligned16(workspace)) return fail(SLF_ERR_ALIGN, "pointers must be 16-byte aligned");
+  if (vocab_start < 0 || vocab_start + V_local > V_global) return fail(SLF_ERR_ARG, "bad shard geometry");
+  Ctx c;
+  SLF_TRY(setup_s(c, N, H, V_local, budget_bytes, workspace, workspace_bytes, stream));
+  const SArgs a{nullptr, nullptr, targets, N, H, V_local, vocab_start, V_global, ignore_index};
+  return s_begin(c, a, need_dweight != 0);
+}
+
+slf_status slf_lce_s_chunk_stats(const void* hidden, const void* weight_shard, const int32_t* targets, int64_t N,
+                                 int64_t H, int64_t V_local, int64_t vocab_start, int64_t V_global,
+                                 int32_t ignore_index, int64_t chunk, slf_shardstat* shardstat_chunk, void* workspace,
+                                 size_t workspace_bytes, size_t budget_bytes, void* stream) {
+  SLF_TRY(check_common(hidden, weight_shard, targets, N, H, V_local, workspace));
+  if (!shardstat_chunk || !aligned16(shardstat_chunk)) return fail(SLF_ERR_ARG, "bad shardstat_chunk");
+  if (vocab_start < 0 || vocab_start + V_local > V_global) return fail(SLF_ERR_ARG, "bad shard geometry");
+  Ctx c;
+  SLF_TRY(setup_s(c, N, H, V_local, budget_bytes, workspace, workspace_bytes, stream));
+  if (chunk < 0 || chunk >= c.plan.nCh) return fail(SLF_ERR_ARG, "chunk %lld out of range", (long long)chunk);
+  const SArgs a{hidden, weight_shard, targets, N, H, V_local, vocab_start, V_global, ignore_index};
+  return s_chunk_stats(c, a, chunk, shardstat_chunk);
+}
+
+slf_status slf_lce_s_chunk_bwd(const void* hidden, const void* weight_shard, const int32_t* targets, int64_t N,
+                               int64_t H, int64_t V_local, int64_t vocab_start, int64_t V_global,
+                               int32_t ignore_index, int reduction, float scale, int64_t chunk,
+                               const slf_shardstat* stats, int g, float* loss_rows, void* dhidden_chunk,
+                               int dhidden_fp32, void* dweight, void* workspace, size_t workspace_bytes,
+                               size_t budget_bytes, void* stream) {
+  SLF_TRY(check_common(hidden, weight_shard, targets, N, H, V_local, workspace));
+  if (!stats || g < 1 || !aligned16(stats)) return fail(SLF_ERR_ARG, "bad stats");
+  if (reduction < SLF_SUM || reduction > SLF_NONE) return fail(SLF_ERR_ARG, "bad reduction %d", reduction);
+  if (reduction == SLF_NONE && !loss_rows) return fail(SLF_ERR_ARG, "reduction NONE needs loss_rows");
+  if ((dhidden_chunk && !aligned16(dhidden_chunk)) || (dweight && !aligned16(dweight)))
+    return fail(SLF_ERR_ALIGN, "gradient pointers must be 16-byte aligned");
+  Ctx c;
+  SLF_TRY(setup_s(c, N, H, V_local, budget_bytes, workspace, workspace_bytes, stream));
+  if (chunk < 0 || chunk >= c.plan.nCh) return fail(SLF_ERR_ARG, "chunk %lld out of range", (long long)chunk);
+  const SArgs a{hidden, weight_shard, targets, N, H, V_local, vocab_start, V_global, ignore_index};
+  float* lr = reduction == SLF_NONE ? loss_rows : reinterpret_cast<float*>(c.ws + c.plan.off_loss);
+  return s_chunk_bwd(c, a, chunk, stats, g, reduction, scale, lr, dhidden_chunk, dhidden_fp32, dweight);
+}
+
+slf_status slf_lce_s_end(const void* hidden, int64_t N, int64_t H, int64_t V_local, int reduction, float scale,
+                         float* loss_out, void* dweight, void* workspace, size_t workspace_bytes, size_t budget_bytes,
+                         void* stream) {
+  if (!hidden || !workspace) return fail(SLF_ERR_ARG, "null required pointer");
+  if (reduction != SLF_NONE && !loss_out) return fail(SLF_ERR_ARG, "null loss_out");
+  if (reduction < SLF_SUM || reduction > SLF_NONE) return fail(SLF_ERR_ARG, "bad reduction %d", reduction);
+  Ctx c;
+  SLF_TRY(setup_s(c, N, H, V_local, budget_bytes, workspace, workspace_bytes, stream));
+  const SArgs a{hidden, nullptr, nullptr, N, H, V_local, 0, V_local, 0};
+  return s_end(c, a, reduction, scale, loss_out, dweight);
+}
+
+slf_status slf_lce_s_rowstat(int64_t N, int64_t H, int64_t V_local, size_t budget_bytes, void* workspace,
+                             const slf_rowstat** out) {
+  if (!workspace || !out) return fail(SLF_ERR_ARG, "null pointer");
+  Plan p;
+  if (!plan_s(N, H, V_local, budget_bytes, &p)) return fail(SLF_ERR_WORKSPACE, "no schedule-S plan fits the budget");
+  *out = reinterpret_cast<const slf_rowstat*>(reinterpret_cast<uint8_t*>(workspace) + p.off_rowstat);
   return SLF_OK;
 }
 

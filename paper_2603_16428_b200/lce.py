@@ -183,6 +183,79 @@ def dx_finalize(dx32, rowstat, out=None):
     return out
 
 
+# ---- schedule S split for vocab shards (include/slf_lce.h) ---------------------------------------
+def s_plan(N: int, H: int, V_local: int, budget_bytes: int = 0):
+    """(chunk_rows, n_chunks) of the schedule-S plan."""
+    c, n = ctypes.c_int64(0), ctypes.c_int64(0)
+    check(lib().slf_lce_s_plan(N, H, V_local, budget_bytes, ctypes.byref(c), ctypes.byref(n)), "slf_lce_s_plan")
+    return c.value, n.value
+
+
+class SShard:
+    """One step of schedule S on this rank's vocab shard, driven chunk by chunk (the caller does the
+    collectives between the calls; see paper_2603_16428_b200.sharded)."""
+
+    def __init__(self, hidden, weight_shard, targets, vocab_start: int, V_global: int, ignore_index: int = -100,
+                 reduction: str = "mean", scale: float = 1.0, budget_bytes: int = 0, workspace=None):
+        self.X, self.W, self.t = _prep(hidden, weight_shard, targets)
+        self.N, self.H = self.X.shape
+        self.V_l = self.W.shape[0]
+        self.vs, self.V = vocab_start, V_global
+        self.ign, self.red, self.scale = ignore_index, REDUCTIONS[reduction], float(scale)
+        self.budget = budget_bytes
+        self.C, self.n_chunks = s_plan(self.N, self.H, self.V_l, budget_bytes)
+        dev = self.X.device
+        self.ws = workspace if workspace is not None else alloc_workspace(self.N, self.H, self.V_l, dev, "S",
+                                                                           budget_bytes)
+        self.stream = _stream_ptr(dev)
+
+    def rows(self, ch: int):
+        r0 = ch * self.C
+        return r0, min(self.C, self.N - r0)
+
+    def begin(self, need_dweight: bool = True):
+        check(lib().slf_lce_s_begin(self.t.data_ptr(), self.N, self.H, self.V_l, self.vs, self.V, self.ign,
+                                    int(need_dweight), self.ws.data_ptr(), self.ws.numel(), self.budget, self.stream),
+              "slf_lce_s_begin")
+
+    def chunk_stats(self, ch: int, out=None):
+        r0, rows = self.rows(ch)
+        st = out if out is not None else torch.empty(rows, 4, dtype=torch.float32, device=self.X.device)
+        check(lib().slf_lce_s_chunk_stats(self.X.data_ptr(), self.W.data_ptr(), self.t.data_ptr(), self.N, self.H,
+                                          self.V_l, self.vs, self.V, self.ign, ch, st.data_ptr(), self.ws.data_ptr(),
+                                          self.ws.numel(), self.budget, self.stream), "slf_lce_s_chunk_stats")
+        return st
+
+    def chunk_bwd(self, ch: int, stats, dX_chunk=None, dhidden_fp32: bool = True, dW=None, loss_rows=None):
+        """stats: float32 [g, rows, 4] (rank order)."""
+        g = stats.shape[0]
+        check(lib().slf_lce_s_chunk_bwd(self.X.data_ptr(), self.W.data_ptr(), self.t.data_ptr(), self.N, self.H,
+                                        self.V_l, self.vs, self.V, self.ign, self.red, self.scale, ch,
+                                        stats.data_ptr(), g, _ptr(loss_rows), _ptr(dX_chunk), int(dhidden_fp32),
+                                        _ptr(dW), self.ws.data_ptr(), self.ws.numel(), self.budget, self.stream),
+              "slf_lce_s_chunk_bwd")
+
+    def end(self, loss_out=None, dW=None):
+        check(lib().slf_lce_s_end(self.X.data_ptr(), self.N, self.H, self.V_l, self.red, self.scale, _ptr(loss_out),
+                                  _ptr(dW), self.ws.data_ptr(), self.ws.numel(), self.budget, self.stream),
+              "slf_lce_s_end")
+
+    def rowstat(self):
+        """Device address of the step's RowStat array [N] (inside the workspace)."""
+        p = ctypes.c_void_p(0)
+        check(lib().slf_lce_s_rowstat(self.N, self.H, self.V_l, self.budget, self.ws.data_ptr(), ctypes.byref(p)),
+              "slf_lce_s_rowstat")
+        return p.value
+
+
+def dx_finalize_ptr(dx32, rowstat_ptr: int, out):
+    """dx_finalize with a raw RowStat device address (rows already offset by the caller)."""
+    N, H = dx32.shape
+    check(lib().slf_lce_dx_finalize(dx32.data_ptr(), rowstat_ptr, out.data_ptr(), N, H, _stream_ptr(dx32.device)),
+          "slf_lce_dx_finalize")
+    return out
+
+
 class Profile:
     """Context manager over slf_profile_begin/end: per-kernel-kind device ms, launches, FLOPs, bytes."""
 

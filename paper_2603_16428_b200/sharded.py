@@ -1,17 +1,24 @@
 """Vocab-sharded LCE across GPUs of one box (BASELINE.json north_star).
 
-Rank k of a process group of size g owns LM-head rows [V*k//g, V*(k+1)//g).  One step:
+Rank k of a process group of size g owns LM-head rows [V*k//g, V*(k+1)//g).  Every compute step
+is a libslf_lce.so kernel; this module only orders the calls and the collectives.
 
-    st_k   = shard_stats(X, W_k, t, v0_k)              per-row (m, s, z_t, hit) of the local vocab
-    ST     = all_gather(st_k)  (rank order)            16 B/token per rank over NCCL / NVLink
-    loss, rs_k = stats_combine(ST, t, v0_k, V_k, V)    deterministic shard-order merge
-    dX_k, dW_k = lce_bwd(X, W_k, t, rs_k, fp32 dX)     recompute per tile; dW stays local
-    dX     = all_reduce(sum_k dX_k)                    fp32 N*H*4 over NCCL
-    dX_bf16 = dx_finalize(dX, rs_k)
+Schedule S (default; no recompute), per row chunk c of the S plan:
 
-Every compute step is a libslf_lce.so kernel; this module only orders the calls and the two
-collectives.  The ops are injectable so the orchestration can be tested with world_size 2 on CPU
-(gloo) against the oracle (tests/test_sharded_cpu.py).
+    st_k   = s_chunk_stats(c)                   stash GEMM + this shard's per-row (m, s, z_t, hit)
+    ST     = all_gather(st_k)  (rank order)     16 B/token per rank
+    s_chunk_bwd(c, ST)                          merge, in-place G_P transform, dX_c partial (fp32) + dW_k (+)=
+    all_reduce(dX_c)  (async, overlaps the next chunk's stash GEMM), then dx_finalize(rows of c)
+  and s_begin / s_end around the chunks (target CSR; one-hot dW correction and loss).
+
+Schedule R (the north-star literal, recompute in backward):
+
+    st_k = shard_stats ; ST = all_gather(st_k) ; loss, rs_k = stats_combine(ST)
+    dX_k, dW_k = lce_bwd(rs_k, fp32 dX) ; all_reduce(dX_k) ; dx_finalize
+
+The ops are injectable so the R orchestration can be tested with world_size 2/3 on CPU (gloo)
+against the oracle (tests/test_sharded_cpu.py); the S orchestration is tested on one GPU by
+emulating the shards (tests/test_gpu_parity.py::test_vocab_shard_emulation_s).
 """
 from __future__ import annotations
 
@@ -34,7 +41,7 @@ def cuda_ops():
 class VocabShardedLCE:
     """Fused LCE with the LM head split by vocabulary rows across the ranks of `group`."""
 
-    def __init__(self, V_global: int, group=None, ops=None, budget_bytes: int = 0):
+    def __init__(self, V_global: int, group=None, ops=None, budget_bytes: int = 0, schedule: str = "S"):
         import torch.distributed as dist
         self.dist = dist
         self.group = group
@@ -44,6 +51,9 @@ class VocabShardedLCE:
         self.v0, self.v1 = shard_bounds(V_global, self.g, self.rank)
         self.ops = ops or cuda_ops()
         self.budget = budget_bytes
+        if schedule not in ("S", "R"):
+            raise ValueError("schedule must be 'S' or 'R'")
+        self.schedule = schedule if ops is None else "R"  # injected (CPU) ops implement the R seam only
         self._bufs = {}
 
     def _buf(self, key, shape, dtype, device):
@@ -57,11 +67,17 @@ class VocabShardedLCE:
     def forward_backward(self, X, W_local, t, ignore_index: int = -100, reduction: str = "mean",
                          scale: float = 1.0, workspace=None, dW_out=None, dX_out=None):
         """Returns (loss, dX bf16 [N, H] (replicated), dW_local [V_k, H])."""
-        import torch
-        N, H = X.shape
         V_l = self.v1 - self.v0
         if W_local.shape[0] != V_l:
             raise ValueError(f"rank {self.rank} expects {V_l} vocab rows, got {W_local.shape[0]}")
+        if self.schedule == "S":
+            return self._fwd_bwd_s(X, W_local, t, ignore_index, reduction, scale, workspace, dW_out, dX_out)
+        return self._fwd_bwd_r(X, W_local, t, ignore_index, reduction, scale, workspace, dW_out, dX_out)
+
+    def _fwd_bwd_r(self, X, W_local, t, ignore_index, reduction, scale, workspace, dW_out, dX_out):
+        import torch
+        N, H = X.shape
+        V_l = self.v1 - self.v0
         st = self.ops.shard_stats(X, W_local, t, self.v0, ignore_index=ignore_index, workspace=workspace,
                                   budget_bytes=self.budget)
         allst = self._buf("stats", (self.g, N, 4), st.dtype, st.device)
@@ -76,3 +92,43 @@ class VocabShardedLCE:
         self.dist.all_reduce(dx32, group=self.group)
         dX = self.ops.dx_finalize(dx32, rs, out=dX_out)
         return loss, dX, dW
+
+    def _fwd_bwd_s(self, X, W_local, t, ignore_index, reduction, scale, workspace, dW_out, dX_out):
+        import torch
+        from . import lce
+        N, H = X.shape
+        sh = lce.SShard(X, W_local, t, self.v0, self.V, ignore_index, reduction, scale, self.budget, workspace)
+        dev = X.device
+        C, nch = sh.C, sh.n_chunks
+        dW = dW_out if dW_out is not None else torch.empty_like(W_local)
+        dX = dX_out if dX_out is not None else torch.empty(N, H, dtype=torch.bfloat16, device=dev)
+        loss = torch.empty(N if reduction == "none" else 1, dtype=torch.float32, device=dev)
+        st_loc = self._buf("s_st", (C, 4), torch.float32, dev)
+        st_all = self._buf("s_stall", (self.g * C, 4), torch.float32, dev)
+        dxb = [self._buf(f"s_dx{i}", (C, H), torch.float32, dev) for i in range(2)]
+        rs_base = sh.rowstat()
+        sh.begin(need_dweight=True)
+        pending = [None, None]  # (work handle, r0, rows) of the all-reduce in flight per buffer
+
+        def finalize(slot):
+            h, r0, rows = pending[slot]
+            h.wait()
+            lce.dx_finalize_ptr(dxb[slot][:rows], rs_base + r0 * 16, dX[r0:r0 + rows])
+            pending[slot] = None
+
+        for ch in range(nch):
+            r0, rows = sh.rows(ch)
+            slot = ch % 2
+            st = sh.chunk_stats(ch, out=st_loc[:rows])
+            gathered = st_all[:self.g * rows]
+            self.dist.all_gather_into_tensor(gathered, st, group=self.group)
+            if pending[slot] is not None:
+                finalize(slot)
+            sh.chunk_bwd(ch, gathered.view(self.g, rows, 4), dX_chunk=dxb[slot][:rows], dhidden_fp32=True, dW=dW,
+                         loss_rows=loss if reduction == "none" else None)
+            pending[slot] = (self.dist.all_reduce(dxb[slot][:rows], group=self.group, async_op=True), r0, rows)
+        for slot in (0, 1):
+            if pending[slot] is not None:
+                finalize(slot)
+        sh.end(loss_out=loss if reduction != "none" else None, dW=dW)
+        return (loss if reduction == "none" else loss[0]), dX, dW

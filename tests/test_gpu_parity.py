@@ -268,3 +268,45 @@ def test_llama_full_size_sampled(slf):
     assert rel_max_err(bf16_to_np64(dX_m)[rows], dXo) <= GRAD_TOL
     assert float(loss_m) == pytest.approx(float(loss_rows[torch.from_numpy(valid).cuda()].double().sum()) / nv, rel=1e-5)
     assert torch.isfinite(dW_m.float()).all()
+
+
+@pytest.mark.parametrize("g,N,budget", [(2, 500, 1 << 21), (3, 700, 3 << 19)])
+def test_vocab_shard_emulation_s(slf, g, N, budget):
+    """Schedule S split for vocab shards, g shards emulated on one GPU: per chunk, every shard's
+    statistics are stacked in rank order (the all-gather), each shard's fp32 dX partial is summed
+    (the all-reduce) and finalised; dW stays per shard; the one-hot correction runs per shard."""
+    from paper_2603_16428_b200 import lce as L
+    V, H = 4100, 256
+    inp = synth.make_inputs(N, H, V, seed=14, alpha=4.0, dist="zipf")
+    X, W, t = to_dev(inp, torch)
+    bounds = [V * k // g for k in range(g + 1)]
+    shards = [L.SShard(X, W[a:b].contiguous(), t, a, V, reduction="mean", budget_bytes=budget)
+              for a, b in zip(bounds[:-1], bounds[1:])]
+    C, nch = shards[0].C, shards[0].n_chunks
+    assert nch > 1 and all(s.C == C and s.n_chunks == nch for s in shards), (C, nch)
+    dWs = [torch.empty(b - a, H, dtype=torch.bfloat16, device="cuda") for a, b in zip(bounds[:-1], bounds[1:])]
+    dX = torch.empty(N, H, dtype=torch.bfloat16, device="cuda")
+    for s in shards:
+        s.begin()
+    for ch in range(nch):
+        r0, rows = shards[0].rows(ch)
+        st = torch.stack([s.chunk_stats(ch) for s in shards])
+        acc = torch.zeros(rows, H, dtype=torch.float32, device="cuda")
+        for s, dWk in zip(shards, dWs):
+            part = torch.empty(rows, H, dtype=torch.float32, device="cuda")
+            s.chunk_bwd(ch, st, dX_chunk=part, dhidden_fp32=True, dW=dWk)
+            acc += part
+        L.dx_finalize_ptr(acc, shards[0].rowstat() + r0 * 16, dX[r0:r0 + rows])
+    losses = []
+    for s, dWk in zip(shards, dWs):
+        lo = torch.empty(1, dtype=torch.float32, device="cuda")
+        s.end(loss_out=lo, dW=dWk)
+        losses.append(float(lo))
+    torch.cuda.synchronize()
+    assert len(set(losses)) == 1
+    Xo, Wo, to = oracle_inputs(inp)
+    ref = oracle.lce(Xo, Wo, to, reduction="mean")
+    assert_loss_close(losses[0], ref["loss"], "mean")
+    assert rel_max_err(bf16_to_np64(dX), ref["dX"]) <= GRAD_TOL
+    assert rel_max_err(bf16_to_np64(torch.cat(dWs)), ref["dW"]) <= GRAD_TOL
+    assert np.all(dX.view(torch.int16).cpu().numpy()[inp.t == -100] == 0)

@@ -36,6 +36,8 @@ KEYS = [
 def kind_of(name: str) -> str:
     if "lce_gemm_kernel<" in name:
         return KIND.get(name.split("<")[1].split(",")[0].strip(), "gemm?")
+    if "lce_group_kernel<" in name:
+        return "gemm (group kernel)"
     return name.split("(")[0].replace("void ", "").strip()
 
 
@@ -51,7 +53,12 @@ def main():
     ap.add_argument("--tag", required=True)
     ap.add_argument("--config", default="llama8b")
     ap.add_argument("--note", default="")
+    ap.add_argument("--rep-kinds", default="", help="comma list naming the captured GEMM launches in order")
+    ap.add_argument("--launch-cycle", default="",
+                    help="comma list naming consecutive lce_group_kernel launches of the launch list cyclically")
     a = ap.parse_args()
+    rep_kinds = [k for k in a.rep_kinds.split(",") if k]
+    cycle = [k for k in a.launch_cycle.split(",") if k]
     out = [f"# ncu summary {a.tag} ({a.config})", "", a.note, ""]
     traffic = {}
     if a.rep:
@@ -61,8 +68,8 @@ def main():
         idx = {h: i for i, h in enumerate(hdr)}
         out += ["## `ncu --set full` capture (one launch per kernel kind; serialised, cold-ish cache)", "",
                 "| kernel | " + " | ".join(k[1] for k in KEYS) + " |", "|---" * (len(KEYS) + 1) + "|"]
-        for d in data:
-            k = kind_of(d[idx["Kernel Name"]])
+        for di, d in enumerate(data):
+            k = rep_kinds[di] if di < len(rep_kinds) else kind_of(d[idx["Kernel Name"]])
             cells = []
             for m, _ in KEYS:
                 if m in idx:
@@ -79,10 +86,14 @@ def main():
         rows = [r for r in csv.reader(open(a.launches)) if len(r) > 5]
         hdr = rows[0]
         agg = collections.defaultdict(lambda: [0, 0.0])
+        gi = 0
         for r in rows[1:]:
             if r[hdr.index("Metric Name")] != "gpu__time_duration.sum":
                 continue
             k = kind_of(r[hdr.index("Kernel Name")])
+            if cycle and "lce_group_kernel" in r[hdr.index("Kernel Name")]:
+                k = cycle[gi % len(cycle)]
+                gi += 1
             agg[k][0] += 1
             agg[k][1] += float(r[hdr.index("Metric Value")].replace(",", "")) / 1e6
         tot = sum(v[1] for v in agg.values())
