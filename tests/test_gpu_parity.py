@@ -310,3 +310,25 @@ def test_vocab_shard_emulation_s(slf, g, N, budget):
     assert rel_max_err(bf16_to_np64(dX), ref["dX"]) <= GRAD_TOL
     assert rel_max_err(bf16_to_np64(torch.cat(dWs)), ref["dW"]) <= GRAD_TOL
     assert np.all(dX.view(torch.int16).cpu().numpy()[inp.t == -100] == 0)
+
+
+@pytest.mark.parametrize("sched", SCHEDS)
+def test_vocab_sharded_module_world1(slf, sched):
+    """VocabShardedLCE end to end with real NCCL collectives (world size 1 on this GPU)."""
+    import os
+    import torch.distributed as dist
+    from paper_2603_16428_b200.sharded import VocabShardedLCE
+    if not dist.is_initialized():
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        os.environ.setdefault("MASTER_PORT", "29533")
+        dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
+    inp = synth.make_inputs(900, 256, 5000, seed=15, alpha=4.0, dist="zipf")
+    X, W, t = to_dev(inp, torch)
+    m = VocabShardedLCE(5000, budget_bytes=3 << 20, schedule=sched)
+    loss, dX, dW = m.forward_backward(X, W, t, reduction="mean")
+    torch.cuda.synchronize()
+    Xo, Wo, to = oracle_inputs(inp)
+    ref = oracle.lce(Xo, Wo, to, reduction="mean")
+    assert_loss_close(float(loss), ref["loss"], "mean")
+    assert rel_max_err(bf16_to_np64(dX), ref["dX"]) <= GRAD_TOL
+    assert rel_max_err(bf16_to_np64(dW), ref["dW"]) <= GRAD_TOL

@@ -1,0 +1,3 @@
+mkdir -p gpurun_out
+export PYTHONUNBUFFERED=1
+timeout 900 python -m pytest tests/test_gpu_parity.py -q -m "gpu" 2>&1 | tail -8
