@@ -63,14 +63,24 @@ __global__ void __launch_bounds__(256) combine_transform_kernel(
   // G_P = p~ * r_t, in place, 8 bf16 per 16-byte access.
   uint4* row = reinterpret_cast<uint4*>(stash + (size_t)i * ld_stash);
   const int64_t groups = (V_l + 7) / 8;
-  for (int64_t q = tid; q < groups; q += 256) {
-    const float r = r_t[(q * 8) / 256];
-    uint4 w = row[q];
-    w.x = pack_bf16x2(bf16lo_to_f32(w.x) * r, bf16hi_to_f32(w.x) * r);
-    w.y = pack_bf16x2(bf16lo_to_f32(w.y) * r, bf16hi_to_f32(w.y) * r);
-    w.z = pack_bf16x2(bf16lo_to_f32(w.z) * r, bf16hi_to_f32(w.z) * r);
-    w.w = pack_bf16x2(bf16lo_to_f32(w.w) * r, bf16hi_to_f32(w.w) * r);
-    row[q] = w;
+  constexpr int U = 4;  // 4 independent 16-byte loads in flight per thread
+  for (int64_t q0 = tid; q0 < groups; q0 += 256 * U) {
+    uint4 w[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+      if (q0 + u * 256 < groups) w[u] = row[q0 + u * 256];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int64_t q = q0 + u * 256;
+      if (q < groups) {
+        const float r = r_t[(q * 8) / 256];
+        w[u].x = pack_bf16x2(bf16lo_to_f32(w[u].x) * r, bf16hi_to_f32(w[u].x) * r);
+        w[u].y = pack_bf16x2(bf16lo_to_f32(w[u].y) * r, bf16hi_to_f32(w[u].y) * r);
+        w[u].z = pack_bf16x2(bf16lo_to_f32(w[u].z) * r, bf16hi_to_f32(w[u].z) * r);
+        w[u].w = pack_bf16x2(bf16lo_to_f32(w[u].w) * r, bf16hi_to_f32(w[u].w) * r);
+        row[q] = w[u];
+      }
+    }
   }
 }
 

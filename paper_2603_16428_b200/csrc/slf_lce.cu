@@ -200,7 +200,12 @@ std::vector<int> lpt_table(const ProbSpec* ps, int n, int units, int* stride) {
   int id = 0;
   for (int p = 0; p < n; ++p) {
     const int kb = (ps[p].a.K + BK - 1) / BK;
-    for (int t = 0; t < ps[p].a.num_tiles; ++t) tiles.push_back({kb, id++});
+    // Cost in K-blocks plus a per-tile epilogue/pipeline overhead; a dW read-modify-write tile
+    // pays extra for streaming the old partial (SLF_LPT_OVH / SLF_LPT_RMW tune the model).
+    static const int ovh = getenv("SLF_LPT_OVH") ? atoi(getenv("SLF_LPT_OVH")) : 4;
+    static const int rmw = getenv("SLF_LPT_RMW") ? atoi(getenv("SLF_LPT_RMW")) : 0;
+    const int cost = kb + ovh + ((ps[p].epi == EPI_DW && ps[p].a.mode == 1) ? rmw : 0);
+    for (int t = 0; t < ps[p].a.num_tiles; ++t) tiles.push_back({cost, id++});
   }
   std::stable_sort(tiles.begin(), tiles.end(), [](auto& x, auto& y) { return x.first > y.first; });
   std::vector<std::vector<int>> lists(units);
@@ -210,7 +215,7 @@ std::vector<int> lpt_table(const ProbSpec* ps, int n, int units, int* stride) {
     for (int u = 1; u < units; ++u)
       if (load[u] < load[best]) best = u;
     lists[best].push_back(t.second);
-    load[best] += t.first + 4;  // + a small per-tile epilogue/pipeline cost
+    load[best] += t.first;
   }
   size_t mx = 1;
   for (auto& l : lists) mx = std::max(mx, l.size() + 1);
@@ -801,7 +806,9 @@ slf_status phase_s(Ctx& c, const void* X, const void* W, const int32_t* t, int64
   if (dX || dW) {
     ProbSpec ps[2];
     int n = 0;
-    SLF_TRY(s_build_bwd(c, a, 0, dX, 0, dW, ps, &n));
+    // A full chunk past the first (dW read-modify-write) represents the common case.
+    const int64_t rep = (p.nCh > 2 || (p.nCh == 2 && N % p.C == 0)) ? 1 : 0;
+    SLF_TRY(s_build_bwd(c, a, rep, dX, 0, dW, ps, &n));
     k_full = arena.add(ps, n, c.dev->sms / cta_group());
     if (N % p.C) {
       SLF_TRY(s_build_bwd(c, a, p.nCh - 1, dX, 0, dW, ps, &n));
