@@ -21,29 +21,84 @@ __device__ __forceinline__ float coef_of(int reduction, float scale, unsigned lo
   return (reduction == SLF_MEAN) ? (n_valid ? scale / (float)n_valid : 0.f) : scale;
 }
 
+// Block-wide fixed-order (m, s) merge of one row's tile partials [tile][rows] (256 threads).
+__device__ __forceinline__ float2 merge_row_tiles(const float2* __restrict__ partials, int tiles, int rows, int i,
+                                                  float* red) {
+  const int tid = threadIdx.x;
+  float m = -INFINITY;
+  for (int k = tid; k < tiles; k += 256) m = fmaxf(m, partials[(size_t)k * rows + i].x);
+  red[tid] = m;
+  __syncthreads();
+  for (int o = 128; o > 0; o >>= 1) {
+    if (tid < o) red[tid] = fmaxf(red[tid], red[tid + o]);
+    __syncthreads();
+  }
+  const float M = red[0];
+  __syncthreads();
+  float s = 0.f;
+  for (int k = tid; k < tiles; k += 256) {
+    const float2 p = partials[(size_t)k * rows + i];
+    s += p.y * ex2((p.x - M) * LOG2E);
+  }
+  red[tid] = s;
+  __syncthreads();
+  for (int o = 128; o > 0; o >>= 1) {
+    if (tid < o) red[tid] += red[tid + o];
+    __syncthreads();
+  }
+  const float S = red[0];
+  __syncthreads();
+  return make_float2(M, S);
+}
+
+// This shard's per-row ShardStat {m, s, z_t, hit} of a chunk: one block per row.
+__global__ void __launch_bounds__(256) shard_rows_kernel(const float2* __restrict__ partials, int tiles, int rows,
+                                                        const float* __restrict__ zt, const int32_t* __restrict__ t,
+                                                        int64_t vocab_start, int64_t V_l, int32_t ignore_index,
+                                                        slf_shardstat* __restrict__ out) {
+  __shared__ float red[256];
+  const int i = blockIdx.x;
+  const float2 ms = merge_row_tiles(partials, tiles, rows, i, red);
+  if (threadIdx.x == 0) {
+    const int32_t tt = t[i];
+    const int64_t loc = (int64_t)tt - vocab_start;
+    const bool hit = tt != ignore_index && loc >= 0 && loc < V_l;
+    out[i] = slf_shardstat{ms.x, ms.y, hit ? zt[i] : 0.f, hit ? 1.f : 0.f};
+  }
+}
+
 // One block (256 threads) per row of the chunk.  The row's global statistics come from the g
 // shards' ShardStats (fixed shard order; g = 1 on one GPU), the per-tile rescale factors from this
 // shard's own tile partials.  Deterministic.
 __global__ void __launch_bounds__(256) combine_transform_kernel(
     const slf_shardstat* __restrict__ st, int g, const float2* __restrict__ partials, int tiles, int rows,
-    const int32_t* __restrict__ t, int64_t vocab_start, int64_t V_l, int64_t V_global, int64_t ld_stash,
-    int32_t ignore_index, int reduction, float scale, float grad_scale, const WsHeader* __restrict__ hdr,
-    float* __restrict__ loss_rows, slf_rowstat* __restrict__ rowstat, uint16_t* __restrict__ stash) {
+    const float* __restrict__ zt, const int32_t* __restrict__ t, int64_t vocab_start, int64_t V_l, int64_t V_global,
+    int64_t ld_stash, int32_t ignore_index, int reduction, float scale, float grad_scale,
+    const WsHeader* __restrict__ hdr, float* __restrict__ loss_rows, slf_rowstat* __restrict__ rowstat,
+    uint16_t* __restrict__ stash) {
   extern __shared__ float r_t[];  // [tiles]
-  __shared__ float sM, sLse;
+  __shared__ float sM, sLse, red[256];
   const int i = blockIdx.x;
   const int tid = threadIdx.x;
+  float2 local = make_float2(0.f, 0.f);
+  if (st == nullptr) local = merge_row_tiles(partials, tiles, rows, i, red);  // one GPU: own tiles only
   if (tid == 0) {
-    float M = -INFINITY;
-    for (int k = 0; k < g; ++k) M = fmaxf(M, st[(size_t)k * rows + i].m);
-    float S = 0.f, z = 0.f;
-    for (int k = 0; k < g; ++k) {
-      const slf_shardstat q = st[(size_t)k * rows + i];
-      S += q.s * ex2((q.m - M) * LOG2E);
-      z += q.zt;  // exactly one shard has the target (the others store 0)
+    float M = -INFINITY, S = 0.f, z = 0.f;
+    const int32_t tt = t[i];
+    if (st == nullptr) {
+      M = local.x;
+      S = local.y;
+      const int64_t loc0 = (int64_t)tt - vocab_start;
+      if (tt != ignore_index && loc0 >= 0 && loc0 < V_l) z = zt[i];
+    } else {
+      for (int k = 0; k < g; ++k) M = fmaxf(M, st[(size_t)k * rows + i].m);
+      for (int k = 0; k < g; ++k) {
+        const slf_shardstat q = st[(size_t)k * rows + i];
+        S += q.s * ex2((q.m - M) * LOG2E);
+        z += q.zt;  // exactly one shard has the target (the others store 0)
+      }
     }
     const float lse = M + logf(S);
-    const int32_t tt = t[i];
     const bool valid = tt != ignore_index;
     const bool bad = valid && (tt < 0 || (int64_t)tt >= V_global);
     const float coef = (valid && !bad) ? coef_of(reduction, scale, hdr->n_valid) : 0.f;

@@ -680,11 +680,13 @@ slf_status s_chunk_stats(Ctx& c, const SArgs& a, int64_t ch, slf_shardstat* out)
   g.out = c.ws + p.off_stash;
   g.ld_out = p.ld_stash;
   SLF_TRY((launch_gemm<EPI_STASH, false, false>(c.dev, ta, tb, g, c.s)));
-  const int tiles_v = (int)((a.V_l + BN - 1) / BN);
-  ProfScope ps(SLF_PROF_LOCAL_COMBINE, c.s, 0.0, (double)rows * (tiles_v * 8.0 + 24));
-  local_combine_kernel<<<(unsigned)((rows + 255) / 256), 256, 0, c.s>>>(part, tiles_v, zt + r0, a.t + r0, rows,
-                                                                        a.vs, a.V_l, a.ign, out);
-  SLF_CUDA(cudaGetLastError());
+  if (out) {  // shard statistics for the all-gather (vocab shards); one GPU merges in combine_transform
+    const int tiles_v = (int)((a.V_l + BN - 1) / BN);
+    ProfScope ps(SLF_PROF_LOCAL_COMBINE, c.s, 0.0, (double)rows * (tiles_v * 8.0 + 24));
+    shard_rows_kernel<<<(unsigned)rows, 256, 0, c.s>>>(part, tiles_v, (int)rows, zt + r0, a.t + r0, a.vs, a.V_l, a.ign,
+                                                       out);
+    SLF_CUDA(cudaGetLastError());
+  }
   return SLF_OK;
 }
 
@@ -750,7 +752,8 @@ slf_status s_chunk_bwd(Ctx& c, const SArgs& a, int64_t ch, const slf_shardstat* 
   {
     ProfScope ps(SLF_PROF_COMBINE_TRANSFORM, c.s, 0.0, (double)rows * (tiles_v * 8.0 + a.V_l * 4.0 + 16.0 * g + 24));
     combine_transform_kernel<<<(unsigned)rows, 256, tiles_v * sizeof(float), c.s>>>(
-        st, g, reinterpret_cast<const float2*>(c.ws + p.off_part), tiles_v, (int)rows, a.t + r0, a.vs, a.V_l, a.Vg,
+        st, g, reinterpret_cast<const float2*>(c.ws + p.off_part), tiles_v, (int)rows,
+        reinterpret_cast<const float*>(c.ws + p.off_zt) + r0, a.t + r0, a.vs, a.V_l, a.Vg,
         p.ld_stash, a.ign, reduction, scale, 1.0f, hdr_of(c.ws), loss_rows_all + r0,
         reinterpret_cast<slf_rowstat*>(c.ws + p.off_rowstat) + r0, reinterpret_cast<uint16_t*>(c.ws + p.off_stash));
     SLF_CUDA(cudaGetLastError());
@@ -816,13 +819,12 @@ slf_status phase_s(Ctx& c, const void* X, const void* W, const int32_t* t, int64
     }
     SLF_TRY(arena.upload(c));
   }
-  slf_shardstat* st = reinterpret_cast<slf_shardstat*>(c.ws + p.off_shard);
   float* loss_rows = s_loss_rows(c, reduction, loss_out);
   for (int64_t ch = 0; ch < p.nCh; ++ch) {
     const int64_t r0 = ch * p.C, rows = std::min(p.C, N - r0);
-    SLF_TRY(s_chunk_stats(c, a, ch, st));
+    SLF_TRY(s_chunk_stats(c, a, ch, nullptr));
     const int k = (rows == p.C || k_last < 0) ? k_full : k_last;
-    SLF_TRY(s_chunk_bwd(c, a, ch, st, 1, reduction, scale, loss_rows,
+    SLF_TRY(s_chunk_bwd(c, a, ch, nullptr, 1, reduction, scale, loss_rows,
                         dX ? reinterpret_cast<uint8_t*>(dX) + (size_t)r0 * H * 2 : nullptr, 0, dW,
                         k >= 0 ? arena.dev(c, k) : nullptr, k >= 0 ? arena.tables[k].second : 0));
   }
