@@ -202,6 +202,18 @@ slf_status slf_lce_s_end(const void* hidden, int64_t N, int64_t H, int64_t V_loc
 slf_status slf_lce_s_rowstat(int64_t N, int64_t H, int64_t V_local, size_t budget_bytes, void* workspace,
                              const slf_rowstat** out);
 
+/* ---- the final RMSNorm that feeds the LM head ----
+ * y = bf16(x * rstd * g), rstd = 1/sqrt(mean_h x^2 + eps) (fp32, [N]); backward with the LCE's
+ * dhidden as dy: dx = rstd * (g*dy - xhat * mean_h(xhat*g*dy)), xhat = x*rstd, and
+ * dg = sum_rows dy*xhat (fp32 [H], fixed-order, deterministic).  x, y, dy, dx: [N, H] bf16;
+ * g: [H] bf16; dy and dx may be the same buffer.  H % 8 == 0, H <= 16384.  The backward needs a
+ * workspace of slf_rmsnorm_workspace_bytes(N, H) bytes. */
+size_t slf_rmsnorm_workspace_bytes(int64_t N, int64_t H);
+slf_status slf_rmsnorm_fwd(const void* x, const void* g, int64_t N, int64_t H, float eps, void* y, float* rstd,
+                           void* stream);
+slf_status slf_rmsnorm_bwd(const void* x, const void* g, const float* rstd, const void* dy, int64_t N, int64_t H,
+                           void* dx, float* dg, void* workspace, size_t workspace_bytes, void* stream);
+
 /* Synchronises `stream` and returns (in *bad_targets, HOST) the number of
  * valid targets outside [0, V_global) seen by the last call that used this
  * workspace, and (in *n_valid, HOST, may be NULL) the number of valid rows. */
@@ -241,6 +253,7 @@ slf_status slf_lce_dx_finalize(const float* dhidden_fp32, const slf_rowstat* row
 #define SLF_PROF_CSR 11               /* schedule S: target CSR (stable counting sort)    */
 #define SLF_PROF_ONEHOT 12            /* schedule S: dW[v] -= coef * sum x_i               */
 #define SLF_PROF_LOSS_REDUCE 13       /* schedule S: deterministic loss sum               */
+#define SLF_PROF_RMSNORM 14           /* final RMSNorm forward / backward (NEXT-1)        */
 slf_status slf_profile_begin(void);
 slf_status slf_profile_end(double* ms, int64_t* launches, double* flops, double* bytes);
 

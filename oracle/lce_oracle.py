@@ -155,3 +155,37 @@ def lce_output_memory(b: int, s: int, V: int, chunk_rows: int = 1024, elem_bytes
     full = b * s * V * elem_bytes * 2
     chunked = 2 * chunk_rows * V * elem_bytes
     return full, chunked, 1.0 - chunked / full
+
+
+# ---- the final RMSNorm feeding the LM head (PAPER.md l.273 lists RMSNorm among
+# the Triton kernels next to the fused LCE).  Plain definitions in float64.
+def rmsnorm(x, g, eps: float = 1e-5):
+    """y = x / sqrt(mean_h x^2 + eps) * g.  Returns (y, rstd)."""
+    x = np.asarray(x, dtype=np.float64)
+    rstd = 1.0 / np.sqrt((x * x).mean(axis=1) + eps)
+    return x * rstd[:, None] * np.asarray(g, dtype=np.float64)[None, :], rstd
+
+
+def rmsnorm_vjp(x, g, dy, eps: float = 1e-5):
+    """Vector-Jacobian product of rmsnorm at x for the cotangent dy: (dx, dg).
+
+    With xhat = x * rstd:  dx = rstd * (g*dy - xhat * mean_h(xhat * g * dy)),  dg = sum_rows dy * xhat.
+    """
+    x = np.asarray(x, dtype=np.float64)
+    g = np.asarray(g, dtype=np.float64)
+    dy = np.asarray(dy, dtype=np.float64)
+    _, rstd = rmsnorm(x, g, eps)
+    xhat = x * rstd[:, None]
+    gdy = g[None, :] * dy
+    c = (xhat * gdy).mean(axis=1)
+    dx = rstd[:, None] * (gdy - xhat * c[:, None])
+    dg = (dy * xhat).sum(axis=0)
+    return dx, dg
+
+
+def rmsnorm_lce(x, g, W, t, eps: float = 1e-5, **kw):
+    """rmsnorm then lce: (loss, dx, dg, dW)."""
+    y, _ = rmsnorm(x, g, eps)
+    out = lce(y, W, t, **kw)
+    dx, dg = rmsnorm_vjp(x, g, out["dX"], eps)
+    return out["loss"], dx, dg, out["dW"]

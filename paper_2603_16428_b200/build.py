@@ -9,7 +9,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 SO = os.path.join(HERE, "libslf_lce.so")
 SRC = os.path.join(HERE, "csrc", "slf_lce.cu")
-DEPS = [os.path.join(HERE, "csrc", f) for f in ("slf_lce.cu", "gemm.cuh", "aux_kernels.cuh", "s_kernels.cuh", "ptx.cuh")] + [
+DEPS = [os.path.join(HERE, "csrc", f) for f in ("slf_lce.cu", "gemm.cuh", "aux_kernels.cuh", "s_kernels.cuh", "rmsnorm.cuh", "ptx.cuh")] + [
     os.path.join(ROOT, "include", "slf_lce.h")]
 
 NVCC_FLAGS = [

@@ -18,6 +18,7 @@
 #include "aux_kernels.cuh"
 #include "gemm.cuh"
 #include "s_kernels.cuh"
+#include "rmsnorm.cuh"
 
 using namespace slf;
 
@@ -1059,6 +1060,64 @@ slf_status slf_lce_s_rowstat(int64_t N, int64_t H, int64_t V_local, size_t budge
   Plan p;
   if (!plan_s(N, H, V_local, budget_bytes, &p)) return fail(SLF_ERR_WORKSPACE, "no schedule-S plan fits the budget");
   *out = reinterpret_cast<const slf_rowstat*>(reinterpret_cast<uint8_t*>(workspace) + p.off_rowstat);
+  return SLF_OK;
+}
+
+// ---- final RMSNorm (NEXT-1) ---------------------------------------------------------------------------
+static int rms_rows_per_block(DevInfo* dev, int64_t N) {
+  const int64_t blocks = std::max<int64_t>(1, 2 * (int64_t)dev->sms);
+  return (int)std::max<int64_t>(1, (N + blocks - 1) / blocks);
+}
+
+size_t slf_rmsnorm_workspace_bytes(int64_t N, int64_t H) {
+  if (N < 1 || H < 8) return 0;
+  const int64_t blocks = 2 * 148 + 64;  // upper bound on the grid for any B200 SM count
+  (void)N;
+  return (size_t)blocks * H * 4;
+}
+
+slf_status slf_rmsnorm_fwd(const void* x, const void* g, int64_t N, int64_t H, float eps, void* y, float* rstd,
+                           void* stream) {
+  if (!x || !g || !y || !rstd) return fail(SLF_ERR_ARG, "null pointer");
+  if (N < 1 || H < 8 || H % 8 || H > 16384) return fail(SLF_ERR_ARG, "bad sizes (H %% 8 == 0, H <= 16384)");
+  if (!aligned16(x) || !aligned16(g) || !aligned16(y) || !aligned16(rstd))
+    return fail(SLF_ERR_ALIGN, "pointers must be 16-byte aligned");
+  DevInfo* dev;
+  SLF_TRY(device_info(&dev));
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  ProfScope ps(SLF_PROF_RMSNORM, s, 0.0, (double)N * H * 4 + N * 4.0);
+  rmsnorm_fwd_kernel<<<(unsigned)N, RMS_THREADS, 0, s>>>(reinterpret_cast<const uint16_t*>(x),
+                                                         reinterpret_cast<const uint16_t*>(g), H, eps,
+                                                         reinterpret_cast<uint16_t*>(y), rstd);
+  SLF_CUDA(cudaGetLastError());
+  return SLF_OK;
+}
+
+slf_status slf_rmsnorm_bwd(const void* x, const void* g, const float* rstd, const void* dy, int64_t N, int64_t H,
+                           void* dx, float* dg, void* workspace, size_t workspace_bytes, void* stream) {
+  if (!x || !g || !rstd || !dy || !dx || !dg || !workspace) return fail(SLF_ERR_ARG, "null pointer");
+  if (N < 1 || H < 8 || H % 8 || H > 16384) return fail(SLF_ERR_ARG, "bad sizes (H %% 8 == 0, H <= 16384)");
+  if (!aligned16(x) || !aligned16(g) || !aligned16(rstd) || !aligned16(dy) || !aligned16(dx) || !aligned16(workspace))
+    return fail(SLF_ERR_ALIGN, "pointers must be 16-byte aligned");
+  DevInfo* dev;
+  SLF_TRY(device_info(&dev));
+  const int rpb = rms_rows_per_block(dev, N);
+  const int blocks = (int)((N + rpb - 1) / rpb);
+  if (workspace_bytes < (size_t)blocks * H * 4) return fail(SLF_ERR_WORKSPACE, "rmsnorm workspace too small");
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  float* part = reinterpret_cast<float*>(workspace);
+  {
+    ProfScope ps(SLF_PROF_RMSNORM, s, 0.0, (double)N * H * 8 + (double)blocks * H * 4);
+    const size_t smem = (size_t)H * 4;
+    if (smem > 48 * 1024)
+      SLF_CUDA(cudaFuncSetAttribute(rmsnorm_bwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    rmsnorm_bwd_kernel<<<(unsigned)blocks, RMS_THREADS, smem, s>>>(
+        reinterpret_cast<const uint16_t*>(x), reinterpret_cast<const uint16_t*>(g), rstd,
+        reinterpret_cast<const uint16_t*>(dy), N, H, rpb, reinterpret_cast<uint16_t*>(dx), part);
+    SLF_CUDA(cudaGetLastError());
+    rmsnorm_dg_reduce_kernel<<<(unsigned)((H + 255) / 256), 256, 0, s>>>(part, blocks, H, dg);
+    SLF_CUDA(cudaGetLastError());
+  }
   return SLF_OK;
 }
 

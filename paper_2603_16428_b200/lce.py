@@ -248,6 +248,45 @@ class SShard:
         return p.value
 
 
+def rmsnorm_fwd(x, g, eps: float = 1e-5):
+    """Final RMSNorm: (y bf16 [N, H], rstd fp32 [N])."""
+    if x.dtype != torch.bfloat16 or g.dtype != torch.bfloat16 or not x.is_cuda:
+        raise TypeError("x and g must be bf16 CUDA tensors")
+    x = x.contiguous()
+    N, H = x.shape
+    y = torch.empty_like(x)
+    rstd = torch.empty(N, dtype=torch.float32, device=x.device)
+    check(lib().slf_rmsnorm_fwd(x.data_ptr(), g.contiguous().data_ptr(), N, H, float(eps), y.data_ptr(),
+                                rstd.data_ptr(), _stream_ptr(x.device)), "slf_rmsnorm_fwd")
+    return y, rstd
+
+
+def rmsnorm_bwd(x, g, rstd, dy, dx=None):
+    """RMSNorm VJP: (dx bf16 [N, H], dg fp32 [H]).  dx may be dy (in place)."""
+    x = x.contiguous()
+    N, H = x.shape
+    dx = dx if dx is not None else torch.empty_like(x)
+    dg = torch.empty(H, dtype=torch.float32, device=x.device)
+    ws = torch.empty(int(lib().slf_rmsnorm_workspace_bytes(N, H)), dtype=torch.uint8, device=x.device)
+    check(lib().slf_rmsnorm_bwd(x.data_ptr(), g.contiguous().data_ptr(), rstd.data_ptr(), dy.data_ptr(), N, H,
+                                dx.data_ptr(), dg.data_ptr(), ws.data_ptr(), ws.numel(), _stream_ptr(x.device)),
+          "slf_rmsnorm_bwd")
+    return dx, dg
+
+
+def rmsnorm_lce_fwd_bwd(x, g, weight, targets, eps: float = 1e-5, ignore_index: int = -100,
+                        reduction: str = "mean", scale: float = 1.0, budget_bytes: int = 0, workspace=None,
+                        schedule: str = "auto"):
+    """Final RMSNorm + fused LCE, forward and backward: (loss, dx (pre-norm), dg fp32, dW).
+
+    y = RMSNorm(x; g) feeds the LM head; the LCE's dhidden is fed through the RMSNorm VJP in place."""
+    y, rstd = rmsnorm_fwd(x, g, eps)
+    loss, dy, dW = lce_fwd_bwd(y, weight, targets, ignore_index, reduction, scale, budget_bytes=budget_bytes,
+                               workspace=workspace, schedule=schedule)
+    dx, dg = rmsnorm_bwd(x, g, rstd, dy, dx=dy)
+    return loss, dx, dg, dW
+
+
 def dx_finalize_ptr(dx32, rowstat_ptr: int, out):
     """dx_finalize with a raw RowStat device address (rows already offset by the caller)."""
     N, H = dx32.shape

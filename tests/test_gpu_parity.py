@@ -332,3 +332,23 @@ def test_vocab_sharded_module_world1(slf, sched):
     assert_loss_close(float(loss), ref["loss"], "mean")
     assert rel_max_err(bf16_to_np64(dX), ref["dX"]) <= GRAD_TOL
     assert rel_max_err(bf16_to_np64(dW), ref["dW"]) <= GRAD_TOL
+
+
+# ---- final RMSNorm + LCE ---------------------------------------------------
+@pytest.mark.parametrize("sched", SCHEDS)
+@pytest.mark.parametrize("N,H,V", [(300, 256, 3000), (1000, 520, 4100)])
+def test_rmsnorm_lce_parity(slf, sched, N, H, V):
+    inp = synth.make_inputs(N, H, V, seed=16, alpha=3.0, dist="zipf")
+    x, W, t = to_dev(inp, torch)
+    rng = np.random.default_rng(5)
+    g_np = synth.f32_to_bf16_bits((1 + 0.2 * rng.standard_normal(H)).astype(np.float32))
+    g = torch.from_numpy(g_np.view(np.int16)).view(torch.bfloat16).cuda()
+    loss, dx, dg, dW = slf.rmsnorm_lce_fwd_bwd(x, g, W, t, eps=1e-5, reduction="mean", schedule=sched)
+    torch.cuda.synchronize()
+    xo, Wo, to = oracle_inputs(inp)
+    ref_loss, ref_dx, ref_dg, ref_dW = oracle.rmsnorm_lce(xo, synth.bf16_bits_to_f64(g_np), Wo, to, eps=1e-5,
+                                                          reduction="mean")
+    assert_loss_close(float(loss), ref_loss, "mean")
+    assert rel_max_err(bf16_to_np64(dx), ref_dx) <= GRAD_TOL
+    assert rel_max_err(dg.cpu().numpy(), ref_dg) <= GRAD_TOL
+    assert rel_max_err(bf16_to_np64(dW), ref_dW) <= GRAD_TOL

@@ -249,3 +249,64 @@ def test_synth_recipe():
     assert np.std(W) * math.sqrt(64) == pytest.approx(4.0, rel=0.05)
     tiny = synth.make_config("tiny")
     assert int((tiny.t == -100).sum()) == 13
+
+
+# ---- RMSNorm (NEXT-1) pins -------------------------------------------------------------------
+def test_rmsnorm_closed_form_and_invariance():
+    x = np.array([[3.0, 4.0]])
+    g = np.array([1.0, 2.0])
+    y, rstd = oracle.rmsnorm(x, g, eps=0.0)
+    # mean(x^2) = 12.5 -> rms = sqrt(12.5)
+    np.testing.assert_allclose(y, [[3 / math.sqrt(12.5), 8 / math.sqrt(12.5)]], rtol=1e-15)
+    xs = np.random.default_rng(0).standard_normal((5, 16))
+    ya, _ = oracle.rmsnorm(xs, np.ones(16), 0.0)
+    yb, _ = oracle.rmsnorm(7.0 * xs, np.ones(16), 0.0)
+    np.testing.assert_allclose(ya, yb, rtol=1e-13)  # scale invariance (eps = 0)
+    np.testing.assert_allclose((ya * ya).mean(axis=1), 1.0, rtol=1e-13)  # unit RMS with g = 1
+
+
+def test_rmsnorm_lce_finite_differences():
+    rng = np.random.default_rng(3)
+    N, H, V = 6, 8, 20
+    x = rng.standard_normal((N, H))
+    g = 1 + 0.3 * rng.standard_normal(H)
+    W = rng.standard_normal((V, H))
+    t = rng.integers(0, V, N)
+    t[2] = -100
+    loss, dx, dg, dW = oracle.rmsnorm_lce(x, g, W, t, eps=1e-5, reduction="mean")
+
+    def f(xp, gp):
+        return oracle.rmsnorm_lce(xp, gp, W, t, eps=1e-5, reduction="mean", need_grads=True)[0]
+
+    eps = 1e-6
+    for (i, h) in [(0, 0), (3, 5), (5, 7)]:
+        xp, xm = x.copy(), x.copy()
+        xp[i, h] += eps
+        xm[i, h] -= eps
+        assert (f(xp, g) - f(xm, g)) / (2 * eps) == pytest.approx(dx[i, h], abs=1e-8)
+    for h in (0, 4):
+        gp, gm = g.copy(), g.copy()
+        gp[h] += eps
+        gm[h] -= eps
+        assert (f(x, gp) - f(x, gm)) / (2 * eps) == pytest.approx(dg[h], abs=1e-8)
+
+
+def test_rmsnorm_torch_crosscheck():
+    torch = pytest.importorskip("torch")
+    rng = np.random.default_rng(4)
+    N, H, V = 16, 32, 50
+    x = rng.standard_normal((N, H))
+    g = 1 + 0.2 * rng.standard_normal(H)
+    W = rng.standard_normal((V, H)) / math.sqrt(H)
+    t = rng.integers(0, V, N)
+    loss, dx, dg, dW = oracle.rmsnorm_lce(x, g, W, t, eps=1e-5, reduction="sum")
+    xt = torch.tensor(x, requires_grad=True)
+    gt = torch.tensor(g, requires_grad=True)
+    Wt = torch.tensor(W, requires_grad=True)
+    y = torch.nn.functional.rms_norm(xt, (H,), gt, eps=1e-5)
+    L = torch.nn.functional.cross_entropy(y @ Wt.T, torch.tensor(t), reduction="sum")
+    L.backward()
+    assert loss == pytest.approx(float(L), rel=1e-12)
+    np.testing.assert_allclose(dx, xt.grad.numpy(), rtol=1e-9, atol=1e-12)
+    np.testing.assert_allclose(dg, gt.grad.numpy(), rtol=1e-9, atol=1e-12)
+    np.testing.assert_allclose(dW, Wt.grad.numpy(), rtol=1e-9, atol=1e-12)
