@@ -202,6 +202,12 @@ slf_status slf_lce_s_end(const void* hidden, int64_t N, int64_t H, int64_t V_loc
 slf_status slf_lce_s_rowstat(int64_t N, int64_t H, int64_t V_local, size_t budget_bytes, void* workspace,
                              const slf_rowstat** out);
 
+/* Debug: copy the per-tile clock64 trace recorded for the launch selected by the environment
+ * variable SLF_DEBUG_TRACE=k (the k-th GEMM launch of the process) into HOST `host` (n values,
+ * 8 per tile: MMA tile start / after TMEM-free wait / issued, epilogue start / accumulator ready /
+ * TMEM released / end, problem index).  Synchronises the device. */
+slf_status slf_debug_trace_read(uint64_t* host, int64_t n);
+
 /* ---- the final RMSNorm that feeds the LM head ----
  * y = bf16(x * rstd * g), rstd = 1/sqrt(mean_h x^2 + eps) (fp32, [N]); backward with the LCE's
  * dhidden as dy: dx = rstd * (g*dy - xhat * mean_h(xhat*g*dy)), xhat = x*rstd, and

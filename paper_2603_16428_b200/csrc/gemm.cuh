@@ -401,6 +401,17 @@ __device__ __forceinline__ void epilogue_dispatch(int epi, const GemmArgs& a, ui
 // either a host-built list (sched: balanced by K-blocks, longest first) or tiles u, u+units, ...
 constexpr int MAXP = 2;
 
+// Debug trace (slf_debug_trace_read): per-tile clock64 stamps of unit 0's leader CTA for one
+// selected launch.  Slots per tile: 0 MMA before tempty wait, 1 after it, 2 MMA tile issued,
+// 3 epilogue start, 4 accumulator ready, 5 TMEM released, 6 epilogue end, 7 problem index.
+constexpr int TRACE_TILES = 1024;
+__device__ unsigned long long g_trace[TRACE_TILES * 8];
+__device__ __forceinline__ unsigned long long clk() {
+  unsigned long long c;
+  asm volatile("mov.u64 %0, %%clock64;" : "=l"(c));
+  return c;
+}
+
 struct Prob {
   GemmArgs a;
   int epi, a_mn, b_mn, tile_begin;
@@ -410,7 +421,8 @@ struct GroupArgs {
   Prob p[MAXP];
   int nprob;
   int num_tiles;
-  int dbg;  // timing-experiment knobs (0 in production): 1 = no L2 prefetch, 2 = late old-dW loads
+  int dbg;  // timing-experiment knobs (0 in production): 1 = no L2 prefetch, 2 = late old-dW loads,
+            // 4 = record the per-tile trace of unit 0
   const int* sched;  // [units][sched_stride] tile ids, -1 terminated (nullptr: round robin)
   int sched_stride;
 };
@@ -565,8 +577,11 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
         const uint32_t idesc = make_idesc_bf16(C::TILE_M, BN, a_mn, b_mn);
         const int num_kb = (P.a.K + BK - 1) / BK;
         const uint32_t acc = local & 1, acc_phase = (local >> 1) & 1;
+        const bool tr = (g.dbg & 4) && blockIdx.x == 0 && local < TRACE_TILES;
+        if (tr) g_trace[local * 8 + 0] = clk();
         mbar_wait(&tempty[acc], acc_phase ^ 1);
         tc_fence_after();
+        if (tr) g_trace[local * 8 + 1] = clk();
         const uint32_t d_tmem = tmem_base + acc * BN;
         for (int kb = 0; kb < num_kb; ++kb) {
           mbar_wait(&full[stage], phase);
@@ -594,6 +609,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
           mma_commit_pair(&tfull[acc], 0x3);
         else
           mma_commit(&tfull[acc]);
+        if (tr) g_trace[local * 8 + 2] = clk();
       }
     }
   } else if (warp >= 4) {
@@ -608,14 +624,21 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
       int m_blk, n_blk;
       tile_coords(tile - P.tile_begin, P.a, m_blk, n_blk);
       const uint32_t acc = local & 1, acc_phase = (local >> 1) & 1;
+      const bool tr = (g.dbg & 4) && blockIdx.x == 0 && local < TRACE_TILES && ew == 0 && lane == 0;
+      if (tr) {
+        g_trace[local * 8 + 3] = clk();
+        g_trace[local * 8 + 7] = pi;
+      }
       auto wait_acc = [&]() {
         mbar_wait(&tfull[acc], acc_phase);
         tc_fence_after();
+        if (tr) g_trace[local * 8 + 4] = clk();
       };
       const uint32_t taddr = tmem_base + ((ew * 32) << 16) + acc * BN;
       auto release = [&]() {
         tc_fence_before();
         __syncwarp();
+        if (tr) g_trace[local * 8 + 5] = clk();
         if (lane == 0) {
           if constexpr (CG == 2)
             mbar_arrive_cluster(mapa_shared(smem_u32(&tempty[acc]), 0));
@@ -643,6 +666,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
         epilogue_dispatch(P.epi, P.a, taddr, m_blk * C::TILE_M + (int)rank * BM, n_blk, ew * 32 + lane);
         release();
       }
+      if (tr) g_trace[local * 8 + 6] = clk();
     }
   }
   if (warp == 4 && lane == 0) bulk_wait<0>();  // epilogue TMA stores complete before exit

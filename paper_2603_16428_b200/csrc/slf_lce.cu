@@ -262,7 +262,12 @@ slf_status launch_group_cg(DevInfo* dev, ProbSpec* ps, int n, cudaStream_t s, co
   g.sched = sched;
   g.sched_stride = sched_stride;
   static const int dbg = getenv("SLF_DEBUG_EPI") ? atoi(getenv("SLF_DEBUG_EPI")) : 0;  // timing experiments only
-  g.dbg = dbg;
+  g.dbg = dbg & ~4;
+  {  // SLF_DEBUG_TRACE=k: record the per-tile trace of the k-th group launch of this process
+    static const int trace_at = getenv("SLF_DEBUG_TRACE") ? atoi(getenv("SLF_DEBUG_TRACE")) : -1;
+    static int launch_no = 0;
+    if (launch_no++ == trace_at) g.dbg |= 4;
+  }
   const int units = sched ? dev->sms / CG : std::min(total, dev->sms / CG);
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((unsigned)(units * CG));
@@ -1060,6 +1065,15 @@ slf_status slf_lce_s_rowstat(int64_t N, int64_t H, int64_t V_local, size_t budge
   Plan p;
   if (!plan_s(N, H, V_local, budget_bytes, &p)) return fail(SLF_ERR_WORKSPACE, "no schedule-S plan fits the budget");
   *out = reinterpret_cast<const slf_rowstat*>(reinterpret_cast<uint8_t*>(workspace) + p.off_rowstat);
+  return SLF_OK;
+}
+
+// ---- debug trace (SLF_DEBUG_TRACE) ------------------------------------------------------------------
+slf_status slf_debug_trace_read(uint64_t* host, int64_t n) {
+  if (!host || n < 0) return fail(SLF_ERR_ARG, "bad arguments");
+  n = std::min<int64_t>(n, (int64_t)TRACE_TILES * 8);
+  SLF_CUDA(cudaDeviceSynchronize());
+  SLF_CUDA(cudaMemcpyFromSymbol(host, g_trace, (size_t)n * 8));
   return SLF_OK;
 }
 
