@@ -208,6 +208,10 @@ slf_status slf_lce_s_rowstat(int64_t N, int64_t H, int64_t V_local, size_t budge
  * TMEM released / end, problem index).  Synchronises the device. */
 slf_status slf_debug_trace_read(uint64_t* host, int64_t n);
 
+/* Debug: number of clusters of `cluster` CTAs of the GEMM kernel that can be co-resident (HOST
+ * *out), from cudaOccupancyMaxActiveClusters with the kernel's shared-memory footprint. */
+slf_status slf_debug_max_active_clusters(int cluster, int* out);
+
 /* ---- the final RMSNorm that feeds the LM head ----
  * y = bf16(x * rstd * g), rstd = 1/sqrt(mean_h x^2 + eps) (fp32, [N]); backward with the LCE's
  * dhidden as dy: dx = rstd * (g*dy - xhat * mean_h(xhat*g*dy)), xhat = x*rstd, and

@@ -1068,6 +1068,29 @@ slf_status slf_lce_s_rowstat(int64_t N, int64_t H, int64_t V_local, size_t budge
   return SLF_OK;
 }
 
+// Debug: how many clusters of `cluster` CTAs of the GEMM kernel (its smem footprint) fit at once.
+slf_status slf_debug_max_active_clusters(int cluster, int* out) {
+  if (!out || cluster < 1 || cluster > 16) return fail(SLF_ERR_ARG, "bad arguments");
+  DevInfo* dev;
+  SLF_TRY(device_info(&dev));
+  auto kfn = lce_group_kernel<2>;
+  SLF_CUDA(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg<2>::SMEM_BYTES));
+  if (cluster > 8) SLF_CUDA(cudaFuncSetAttribute(kfn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)(dev->sms / cluster * cluster));
+  cfg.blockDim = dim3(GEMM_THREADS);
+  cfg.dynamicSmemBytes = Cfg<2>::SMEM_BYTES;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = cluster;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  SLF_CUDA(cudaOccupancyMaxActiveClusters(out, kfn, &cfg));
+  return SLF_OK;
+}
+
 // ---- debug trace (SLF_DEBUG_TRACE) ------------------------------------------------------------------
 slf_status slf_debug_trace_read(uint64_t* host, int64_t n) {
   if (!host || n < 0) return fail(SLF_ERR_ARG, "bad arguments");
