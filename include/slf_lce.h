@@ -124,6 +124,15 @@ slf_status slf_lce_fwd_bwd(const void* hidden, const void* weight, const int32_t
                            void* dhidden, void* dweight, void* workspace, size_t workspace_bytes, int schedule,
                            size_t budget_bytes, void* stream);
 
+/* slf_lce_fwd_bwd with flags (gradient accumulation across micro-batches):
+ *   SLF_FLAG_ACCUMULATE_DW: dweight += dL/dW (bf16 read-add-write in fp32) instead of =.
+ * flags = 0 is exactly slf_lce_fwd_bwd. */
+#define SLF_FLAG_ACCUMULATE_DW 1u
+slf_status slf_lce_fwd_bwd_ex(const void* hidden, const void* weight, const int32_t* targets, int64_t N, int64_t H,
+                              int64_t V, int32_t ignore_index, int reduction, float scale, float* loss_out,
+                              void* dhidden, void* dweight, void* workspace, size_t workspace_bytes, int schedule,
+                              size_t budget_bytes, uint32_t flags, void* stream);
+
 /* Forward half (schedule R split; also the vocab-shard seam).  Computes the
  * loss and the RowStat array [N] (16 B/row, DEVICE, caller-owned) that
  * slf_lce_bwd consumes.  `scale` enters coef only.  Single GPU form. */
@@ -207,6 +216,10 @@ slf_status slf_lce_s_rowstat(int64_t N, int64_t H, int64_t V_local, size_t budge
  * 8 per tile: MMA tile start / after TMEM-free wait / issued, epilogue start / accumulator ready /
  * TMEM released / end, problem index).  Synchronises the device. */
 slf_status slf_debug_trace_read(uint64_t* host, int64_t n);
+
+/* p[i] = bf16(p[i] * s) for a DEVICE bf16 array of n elements (n % 8 == 0, 16-byte aligned):
+ * applies an autograd grad_output to gradients formed during the forward (LCEFunctionFused). */
+slf_status slf_scale_bf16(void* p, int64_t n, float s, void* stream);
 
 /* Debug: number of clusters of `cluster` CTAs of the GEMM kernel that can be co-resident (HOST
  * *out), from cudaOccupancyMaxActiveClusters with the kernel's shared-memory footprint. */

@@ -4,6 +4,6 @@ Hot path: libslf_lce.so (hand-written sm_100a CUDA: TMA + tcgen05/TMEM GEMM tile
 LCE epilogues) behind the C ABI in include/slf_lce.h; this package is the thin Python binding.
 """
 from .lce import (  # noqa: F401
-    LCEFunction, Profile, alloc_workspace, debug_gemm, dx_finalize, lce_bwd, lce_fwd, lce_fwd_bwd, plan_describe, shard_stats,
+    LCEFunction, LCEFunctionFused, Profile, scale_, alloc_workspace, debug_gemm, dx_finalize, lce_bwd, lce_fwd, lce_fwd_bwd, plan_describe, shard_stats,
     stats_combine, status, workspace_bytes, rmsnorm_fwd, rmsnorm_bwd, rmsnorm_lce_fwd_bwd, SShard, s_plan,
 )

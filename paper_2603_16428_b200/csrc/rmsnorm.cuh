@@ -117,4 +117,14 @@ __global__ void __launch_bounds__(256) rmsnorm_dg_reduce_kernel(const float* __r
   dg[j] = s;
 }
 
+// p[i] = bf16(p[i] * s), 8 elements per thread-iteration.
+__global__ void __launch_bounds__(256) scale_bf16_kernel(uint4* __restrict__ p, int64_t groups, float s) {
+  for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < groups; q += (int64_t)gridDim.x * blockDim.x) {
+    float f[8];
+    unpack8(p[q], f);
+    p[q] = make_uint4(pack_bf16x2(f[0] * s, f[1] * s), pack_bf16x2(f[2] * s, f[3] * s), pack_bf16x2(f[4] * s, f[5] * s),
+                      pack_bf16x2(f[6] * s, f[7] * s));
+  }
+}
+
 }  // namespace slf

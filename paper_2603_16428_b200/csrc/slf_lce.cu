@@ -437,6 +437,7 @@ struct Ctx {
   cudaStream_t s;
   uint8_t* ws;
   Plan plan;
+  bool acc_dw = false;  // SLF_FLAG_ACCUMULATE_DW: dW += instead of dW =
 };
 
 WsHeader* hdr_of(uint8_t* ws) { return reinterpret_cast<WsHeader*>(ws); }
@@ -540,7 +541,7 @@ slf_status phase_backward(Ctx& c, const void* X, const void* W, const slf_rowsta
       q.a.K = (int)rows;
       q.a.out = reinterpret_cast<uint8_t*>(dW) + (size_t)c0 * H * 2;
       q.a.ld_out = H;
-      q.a.mode = rb > 0 ? 1 : 0;
+      q.a.mode = (rb > 0 || c.acc_dw) ? 1 : 0;
       SLF_TRY(tmap_kmajor(&q.tc, q.a.out, H, wc, H, BM));
       finish_geometry(q.a, cg);
     }
@@ -736,7 +737,7 @@ slf_status s_build_bwd(Ctx& c, const SArgs& a, int64_t ch, void* dXc, int dx_fp3
     q.a.K = (int)rows;
     q.a.out = dW;
     q.a.ld_out = a.H;
-    q.a.mode = ch > 0 ? 1 : 0;
+    q.a.mode = (ch > 0 || c.acc_dw) ? 1 : 0;
     static const bool no_rmw = getenv("SLF_DEBUG_DW_NO_RMW") != nullptr;  // timing experiments only (wrong dW)
     if (no_rmw) q.a.mode = 0;
     SLF_TRY(tmap_kmajor(&q.tc, dW, a.H, a.V_l, a.H, BM));
@@ -903,7 +904,16 @@ slf_status slf_lce_fwd_bwd(const void* hidden, const void* weight, const int32_t
                            int64_t V, int32_t ignore_index, int reduction, float scale, float* loss_out,
                            void* dhidden, void* dweight, void* workspace, size_t workspace_bytes, int schedule,
                            size_t budget_bytes, void* stream) {
+  return slf_lce_fwd_bwd_ex(hidden, weight, targets, N, H, V, ignore_index, reduction, scale, loss_out, dhidden,
+                            dweight, workspace, workspace_bytes, schedule, budget_bytes, 0u, stream);
+}
+
+slf_status slf_lce_fwd_bwd_ex(const void* hidden, const void* weight, const int32_t* targets, int64_t N, int64_t H,
+                              int64_t V, int32_t ignore_index, int reduction, float scale, float* loss_out,
+                              void* dhidden, void* dweight, void* workspace, size_t workspace_bytes, int schedule,
+                              size_t budget_bytes, uint32_t flags, void* stream) {
   SLF_TRY(check_common(hidden, weight, targets, N, H, V, workspace));
+  if (flags & ~(uint32_t)SLF_FLAG_ACCUMULATE_DW) return fail(SLF_ERR_ARG, "unknown flags 0x%x", flags);
   if (!loss_out) return fail(SLF_ERR_ARG, "null loss_out");
   if (reduction < SLF_SUM || reduction > SLF_NONE) return fail(SLF_ERR_ARG, "bad reduction %d", reduction);
   if (schedule < SLF_SCHED_AUTO || schedule > SLF_SCHED_S) return fail(SLF_ERR_ARG, "schedule %d", schedule);
@@ -912,6 +922,7 @@ slf_status slf_lce_fwd_bwd(const void* hidden, const void* weight, const int32_t
   if (!aligned16(loss_out)) return fail(SLF_ERR_ALIGN, "loss_out must be 16-byte aligned");
   Ctx c;
   SLF_TRY(setup(c, N, H, V, budget_bytes, workspace, workspace_bytes, stream, schedule, true));
+  c.acc_dw = (flags & SLF_FLAG_ACCUMULATE_DW) != 0;
   if (c.plan.sched == SLF_SCHED_S)
     return phase_s(c, hidden, weight, targets, N, H, V, ignore_index, reduction, scale, loss_out, dhidden, dweight);
   slf_shardstat* st = reinterpret_cast<slf_shardstat*>(c.ws + c.plan.off_shard);
@@ -1088,6 +1099,21 @@ slf_status slf_debug_max_active_clusters(int cluster, int* out) {
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   SLF_CUDA(cudaOccupancyMaxActiveClusters(out, kfn, &cfg));
+  return SLF_OK;
+}
+
+// ---- bf16 in-place scaling (autograd: apply grad_output to gradients formed in the forward) ----------
+slf_status slf_scale_bf16(void* p, int64_t n, float s, void* stream) {
+  if (!p || n < 0 || (n % 8)) return fail(SLF_ERR_ARG, "p must be non-null and n a multiple of 8");
+  if (!aligned16(p)) return fail(SLF_ERR_ALIGN, "pointer must be 16-byte aligned");
+  DevInfo* dev;
+  SLF_TRY(device_info(&dev));
+  if (n == 0) return SLF_OK;
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  const int64_t groups = n / 8;
+  const int blocks = (int)std::min<int64_t>((groups + 255) / 256, (int64_t)dev->sms * 8);
+  scale_bf16_kernel<<<blocks, 256, 0, st>>>(reinterpret_cast<uint4*>(p), groups, s);
+  SLF_CUDA(cudaGetLastError());
   return SLF_OK;
 }
 

@@ -61,10 +61,12 @@ def alloc_workspace(N: int, H: int, V: int, device, schedule: str = "auto", budg
 
 def lce_fwd_bwd(hidden, weight, targets, ignore_index: int = -100, reduction: str = "mean", scale: float = 1.0,
                 need_dhidden: bool = True, need_dweight: bool = True, budget_bytes: int = 0, workspace=None,
-                out=None, schedule: str = "auto"):
+                out=None, schedule: str = "auto", accumulate_dw: bool = False):
     """Fused LCE forward + backward.  Returns (loss fp32, dhidden bf16 | None, dweight bf16 | None).
 
-    ``out`` may be a (loss, dhidden, dweight) triple of preallocated tensors to write into.
+    ``out`` may be a (loss, dhidden, dweight) triple of preallocated tensors to write into;
+    ``accumulate_dw`` adds dL/dW into the given dweight (gradient accumulation) instead of
+    overwriting it.
     """
     hidden, weight, targets = _prep(hidden, weight, targets)
     N, H = hidden.shape
@@ -79,10 +81,12 @@ def lce_fwd_bwd(hidden, weight, targets, ignore_index: int = -100, reduction: st
         dW = torch.empty_like(weight) if need_dweight else None
     if workspace is None:
         workspace = alloc_workspace(N, H, V, dev, schedule, budget_bytes)
-    check(lib().slf_lce_fwd_bwd(hidden.data_ptr(), weight.data_ptr(), targets.data_ptr(), N, H, V, ignore_index, red,
-                                float(scale), loss.data_ptr(), _ptr(dX), _ptr(dW), workspace.data_ptr(),
-                                workspace.numel(), SCHEDULES[schedule], budget_bytes, _stream_ptr(dev)),
-          "slf_lce_fwd_bwd")
+    if accumulate_dw and (out is None or dW is None):
+        raise ValueError("accumulate_dw needs the dweight buffer to accumulate into (out=(loss, dX, dW))")
+    check(lib().slf_lce_fwd_bwd_ex(hidden.data_ptr(), weight.data_ptr(), targets.data_ptr(), N, H, V, ignore_index,
+                                   red, float(scale), loss.data_ptr(), _ptr(dX), _ptr(dW), workspace.data_ptr(),
+                                   workspace.numel(), SCHEDULES[schedule], budget_bytes, int(bool(accumulate_dw)),
+                                   _stream_ptr(dev)), "slf_lce_fwd_bwd_ex")
     return (loss if reduction == "none" else loss[0]), dX, dW
 
 
@@ -321,6 +325,35 @@ def debug_gemm(A, B, a_mn: bool, b_mn: bool, M: int, N: int, K: int):
     check(lib().slf_debug_gemm(A.data_ptr(), B.data_ptr(), D.data_ptr(), M, N, K, int(a_mn), int(b_mn),
                                _stream_ptr(A.device)), "slf_debug_gemm")
     return D
+
+
+def scale_(t, s: float):
+    """In-place t *= s for a contiguous bf16 CUDA tensor (library kernel)."""
+    if s == 1.0 or t is None:
+        return t
+    check(lib().slf_scale_bf16(t.data_ptr(), t.numel(), float(s), _stream_ptr(t.device)), "slf_scale_bf16")
+    return t
+
+
+class LCEFunctionFused(torch.autograd.Function):
+    """autograd wrapper on the fused call (schedule S when it fits): the gradients are formed during
+    the forward (no recompute) and scaled by grad_output in backward (a no-op for grad_output == 1)."""
+
+    @staticmethod
+    def forward(ctx, hidden, weight, targets, ignore_index=-100, reduction="mean"):
+        if reduction == "none":
+            raise NotImplementedError("reduction='none' needs a per-row grad; use LCEFunction")
+        loss, dX, dW = lce_fwd_bwd(hidden, weight, targets, ignore_index, reduction, 1.0,
+                                   need_dhidden=ctx.needs_input_grad[0], need_dweight=ctx.needs_input_grad[1])
+        ctx.grads = (dX, dW)
+        return loss
+
+    @staticmethod
+    def backward(ctx, grad_out):
+        dX, dW = ctx.grads
+        ctx.grads = None
+        g = float(grad_out.item())
+        return scale_(dX, g), scale_(dW, g), None, None, None
 
 
 class LCEFunction(torch.autograd.Function):

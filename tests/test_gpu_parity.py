@@ -352,3 +352,38 @@ def test_rmsnorm_lce_parity(slf, sched, N, H, V):
     assert rel_max_err(bf16_to_np64(dx), ref_dx) <= GRAD_TOL
     assert rel_max_err(dg.cpu().numpy(), ref_dg) <= GRAD_TOL
     assert rel_max_err(bf16_to_np64(dW), ref_dW) <= GRAD_TOL
+
+
+# ---- gradient accumulation and the fused autograd function ----------------
+@pytest.mark.parametrize("sched", SCHEDS)
+def test_accumulate_dw(slf, sched):
+    """Two micro-batches with accumulate_dw equal the sum of the two separate dW (bf16 tolerance)."""
+    a = synth.make_inputs(600, 256, 3000, seed=17, alpha=3.0)
+    b = synth.make_inputs(600, 256, 3000, seed=18, alpha=3.0)
+    Xa, W, ta = to_dev(a, torch)
+    Xb, _, tb = to_dev(b, torch)
+    _, _, dWa = slf.lce_fwd_bwd(Xa, W, ta, reduction="sum", schedule=sched, budget_bytes=2 << 20)
+    _, _, dWb = slf.lce_fwd_bwd(Xb, W, tb, reduction="sum", schedule=sched, budget_bytes=2 << 20)
+    acc = dWa.clone()
+    loss = torch.empty(1, dtype=torch.float32, device="cuda")
+    dX = torch.empty_like(Xb)
+    slf.lce_fwd_bwd(Xb, W, tb, reduction="sum", schedule=sched, budget_bytes=2 << 20, out=(loss, dX, acc),
+                    accumulate_dw=True)
+    torch.cuda.synchronize()
+    ref = bf16_to_np64(dWa) + bf16_to_np64(dWb)
+    assert rel_max_err(bf16_to_np64(acc), ref) < 1e-2
+
+
+def test_fused_autograd_function(slf):
+    inp = synth.make_inputs(500, 256, 3000, seed=19, alpha=3.0)
+    X, W, t = to_dev(inp, torch)
+    Xr = X.clone().requires_grad_(True)
+    Wr = W.clone().requires_grad_(True)
+    L = slf.LCEFunctionFused.apply(Xr, Wr, t, -100, "mean")
+    (0.5 * L).backward()
+    torch.cuda.synchronize()
+    Xo, Wo, to = oracle_inputs(inp)
+    ref = oracle.lce(Xo, Wo, to, reduction="mean", scale=0.5)
+    assert_loss_close(float(L), ref["loss"], "mean")
+    assert rel_max_err(bf16_to_np64(Xr.grad), ref["dX"]) <= GRAD_TOL
+    assert rel_max_err(bf16_to_np64(Wr.grad), ref["dW"]) <= GRAD_TOL
