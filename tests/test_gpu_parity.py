@@ -332,6 +332,8 @@ def test_vocab_sharded_module_world1(slf, sched):
     assert_loss_close(float(loss), ref["loss"], "mean")
     assert rel_max_err(bf16_to_np64(dX), ref["dX"]) <= GRAD_TOL
     assert rel_max_err(bf16_to_np64(dW), ref["dW"]) <= GRAD_TOL
+    if sched == SCHEDS[-1]:
+        dist.destroy_process_group()
 
 
 # ---- final RMSNorm + LCE ---------------------------------------------------
@@ -384,6 +386,6 @@ def test_fused_autograd_function(slf):
     torch.cuda.synchronize()
     Xo, Wo, to = oracle_inputs(inp)
     ref = oracle.lce(Xo, Wo, to, reduction="mean", scale=0.5)
-    assert_loss_close(float(L), ref["loss"], "mean")
+    assert_loss_close(float(L.detach()), ref["loss"], "mean")
     assert rel_max_err(bf16_to_np64(Xr.grad), ref["dX"]) <= GRAD_TOL
     assert rel_max_err(bf16_to_np64(Wr.grad), ref["dW"]) <= GRAD_TOL
