@@ -190,7 +190,8 @@ void finish_geometry(GemmArgs& a, int cg) {
   a.tiles_m = (a.M + tile_m - 1) / tile_m;
   a.tiles_n = (a.N + BN - 1) / BN;
   a.num_tiles = a.tiles_m * a.tiles_n;
-  a.group_m = std::max(1, std::min(a.tiles_m, 16 / cg));
+  static const int gm = getenv("SLF_GROUP_M") ? atoi(getenv("SLF_GROUP_M")) : 16 / cg;  // raster experiments
+  a.group_m = std::max(1, std::min(a.tiles_m, gm));
 }
 
 // Longest-processing-time-first assignment of the tiles of a group to `units` persistent units:
@@ -218,6 +219,12 @@ std::vector<int> lpt_table(const ProbSpec* ps, int n, int units, int* stride) {
     lists[best].push_back(t.second);
     load[best] += t.first;
   }
+  // Order within a unit (experiment knob SLF_LPT_ORDER=mid): move the unit's longest tile (assigned
+  // first) to the middle of its list so long-K and short-K tiles overlap in time across units.
+  static const bool mid = getenv("SLF_LPT_ORDER") && std::string(getenv("SLF_LPT_ORDER")) == "mid";
+  if (mid)
+    for (auto& l : lists)
+      if (l.size() > 2) std::rotate(l.begin(), l.begin() + 1, l.begin() + 1 + l.size() / 2);
   size_t mx = 1;
   for (auto& l : lists) mx = std::max(mx, l.size() + 1);
   *stride = (int)mx;

@@ -389,3 +389,54 @@ def test_fused_autograd_function(slf):
     assert_loss_close(float(L.detach()), ref["loss"], "mean")
     assert rel_max_err(bf16_to_np64(Xr.grad), ref["dX"]) <= GRAD_TOL
     assert rel_max_err(bf16_to_np64(Wr.grad), ref["dW"]) <= GRAD_TOL
+
+
+# ---- every BASELINE config at full size, in bench.py's launch configuration (sampled rows) --------
+@pytest.mark.slow
+@pytest.mark.parametrize("cfg", ["llama8b", "qwen7b", "llama70b", "mistral123b"])
+def test_full_size_sampled_rows_all_configs(slf, cfg):
+    """Per-row loss and dX on 32 sampled rows (incl. ignored ones) at the config's full N, H, V with
+    the default schedule and budget; run-to-run bit-identical outputs (determinism, p10)."""
+    inp = synth.make_config(cfg, seed=1, alpha=1.0, dist="uniform")
+    X, W, t = to_dev(inp, torch)
+    loss_rows, dX, dW = slf.lce_fwd_bwd(X, W, t, reduction="none", scale=1.0)
+    l2, dX2, dW2 = slf.lce_fwd_bwd(X, W, t, reduction="none", scale=1.0)
+    torch.cuda.synchronize()
+    assert torch.equal(loss_rows, l2) and torch.equal(dX, dX2) and torch.equal(dW, dW2)
+    del l2, dX2, dW2
+    rng = np.random.default_rng(3)
+    rows = np.sort(np.concatenate([rng.choice(inp.N, 28, replace=False), np.nonzero(inp.t == -100)[0][:4]]))
+    Xo = synth.bf16_bits_to_f64(inp.X[rows])
+    Wo = synth.bf16_bits_to_f64(inp.W)
+    valid, nv, coef = oracle.coef_for(inp.t, -100, "none", 1.0)
+    l, lse, dXo, _ = oracle.rows(Xo, Wo, inp.t[rows].astype(np.int64), coef[rows])
+    assert_loss_close(loss_rows.cpu().numpy()[rows], l, "none")
+    assert rel_max_err(bf16_to_np64(dX)[rows], dXo) <= GRAD_TOL
+    assert np.all(dX[torch.from_numpy(inp.t == -100).cuda()].view(torch.int16).cpu().numpy() == 0)
+
+
+@pytest.mark.slow
+def test_llama_full_size_dw_rows(slf):
+    """dW rows at the full Llama-3.1-8B size: the oracle forms lse for all 16384 rows (materialised
+    logits, fp64) and checks 12 vocabulary rows of dW, including the most-hit target rows."""
+    inp = synth.make_config("llama8b", seed=2, alpha=4.0, dist="zipf")
+    X, W, t = to_dev(inp, torch)
+    loss, dX, dW = slf.lce_fwd_bwd(X, W, t, reduction="mean")
+    torch.cuda.synchronize()
+    Xo = synth.bf16_bits_to_f64(inp.X)
+    Wo = synth.bf16_bits_to_f64(inp.W)
+    valid, nv, coef = oracle.coef_for(inp.t, -100, "mean", 1.0)
+    hot = np.argsort(-np.bincount(inp.t[valid], minlength=inp.V))[:6]
+    vrows = np.unique(np.concatenate([hot, np.random.default_rng(4).choice(inp.V, 6, replace=False)]))
+    lse = np.empty(inp.N)
+    zt = np.empty(inp.N)
+    for s in range(0, inp.N, 1024):  # row blocks of the materialised logits (plain definition, c1-c2)
+        Z = Xo[s:s + 1024] @ Wo.T
+        m = Z.max(axis=1)
+        lse[s:s + 1024] = m + np.log(np.exp(Z - m[:, None]).sum(axis=1))
+    P = np.exp(Xo @ Wo[vrows].T - lse[:, None])                 # softmax columns of the sampled rows
+    onehot = (inp.t[:, None] == vrows[None, :]).astype(np.float64)
+    G = coef[:, None] * (P - onehot)                             # c3, columns vrows
+    ref = G.T @ Xo                                               # dW rows vrows
+    got = bf16_to_np64(dW[torch.from_numpy(vrows).cuda()])
+    assert rel_max_err(got, ref) <= GRAD_TOL
