@@ -172,7 +172,7 @@ __device__ __forceinline__ void epilogue_tile(const GemmArgs& a, uint32_t taddr,
         zt = (c * 32 + i + 1 == tl) ? z1 : zt;
         p[i / 2] = pack_bf16x2(e0, e1);
       }
-      if (row_ok) {
+      if (row_ok && !(a.mode & 32)) {  // mode bit 32: skip the stash stores (timing experiment only)
 #pragma unroll
         for (int q = 0; q < 4; ++q)
           if (c * 32 + q * 8 < ncols)

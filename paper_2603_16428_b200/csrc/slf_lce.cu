@@ -693,6 +693,8 @@ slf_status s_chunk_stats(Ctx& c, const SArgs& a, int64_t ch, slf_shardstat* out)
   g.zt = zt + r0;
   g.out = c.ws + p.off_stash;
   g.ld_out = p.ld_stash;
+  static const int dbg = getenv("SLF_DEBUG_EPI") ? atoi(getenv("SLF_DEBUG_EPI")) : 0;
+  g.mode = dbg & 32;  // timing experiment only: skip the stash stores
   SLF_TRY((launch_gemm<EPI_STASH, false, false>(c.dev, ta, tb, g, c.s)));
   if (out) {  // shard statistics for the all-gather (vocab shards); one GPU merges in combine_transform
     const int tiles_v = (int)((a.V_l + BN - 1) / BN);
