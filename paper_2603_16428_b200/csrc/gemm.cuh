@@ -73,6 +73,7 @@ struct GemmArgs {
   void* out;
   int64_t ld_out;
   int mode;
+  int tma_out;  // EPI_STASH: write the stash through the output tensor map (TMA-staged stores)
   void* out2;  // DX final bf16 destination (row 0 of the GEMM)
   int64_t ld_out2;
 };
@@ -382,6 +383,81 @@ __device__ __forceinline__ void epilogue_dw_tma(const GemmArgs& a, const CUtenso
   }
 }
 
+// Schedule S forward epilogue with TMA-staged stash stores: per (row, 256-column tile) the max m_t
+// and sum exp(z - m_t) (as EPI_STATS), the target-logit gather, and the bf16 stash
+// p~ = exp(z - m_t) written through four swizzled 16 KB smem chunks and TMA stores (coalesced),
+// instead of thread-per-row 16-byte stores that touch 32 cache lines per warp instruction.
+template <typename WaitAcc, typename ReleaseTmem>
+__device__ __forceinline__ void epilogue_stash_tma(const GemmArgs& a, const CUtensorMap* tmC, uint32_t taddr,
+                                                   int row0, int n_blk, int rl, uint8_t* stg, bool lead,
+                                                   WaitAcc wait_acc, ReleaseTmem release_tmem) {
+  constexpr uint32_t CHUNK_BYTES = BM * 64 * 2;
+  const int r = row0 + rl;
+  const bool row_ok = r < a.M;
+  const int n0 = n_blk * BN;
+  const int ncols = min(BN, a.N - n0);
+  const uint32_t sbase = smem_u32(stg);
+  int tl = -1;
+  if (row_ok) {
+    const int32_t t = a.targets[r];
+    const int64_t loc = (int64_t)t - a.tcol0 - n0;
+    tl = (t != a.ignore_index && loc >= 0 && loc < ncols) ? (int)loc : -1;
+  }
+  if (lead) bulk_wait_read<0>();  // the previous tile's stores have read the staging buffers
+  named_bar_sync(1, 128);
+  wait_acc();
+  uint32_t v[32];
+  float mx = -INFINITY;
+#pragma unroll 1
+  for (int c = 0; c < BN / 32; ++c) {
+    if (c * 32 >= ncols) break;
+    tmem_ld32(taddr + c * 32, v);
+    tmem_ld_wait();
+#pragma unroll
+    for (int i = 0; i < 32; ++i)
+      if (c * 32 + i < ncols) mx = fmaxf(mx, __uint_as_float(v[i]));
+  }
+  const float mb = mx * LOG2E;
+  float s = 0.f, zt = 0.f;
+#pragma unroll 1
+  for (int c = 0; c < BN / 32; ++c) {
+    if (c * 32 >= ncols) break;
+    tmem_ld32(taddr + c * 32, v);
+    tmem_ld_wait();
+    uint32_t p[16];
+#pragma unroll
+    for (int i = 0; i < 32; i += 2) {
+      const float z0 = __uint_as_float(v[i]), z1 = __uint_as_float(v[i + 1]);
+      float e0 = ex2(fmaf(z0, LOG2E, -mb)), e1 = ex2(fmaf(z1, LOG2E, -mb));
+      e0 = (c * 32 + i < ncols) ? e0 : 0.f;
+      e1 = (c * 32 + i + 1 < ncols) ? e1 : 0.f;
+      s += e0 + e1;
+      zt = (c * 32 + i == tl) ? z0 : zt;
+      zt = (c * 32 + i + 1 == tl) ? z1 : zt;
+      p[i / 2] = pack_bf16x2(e0, e1);
+    }
+    const uint32_t rowaddr = sbase + (c >> 1) * CHUNK_BYTES + rl * 128;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int gi = (c & 1) * 4 + q;
+      sts128(rowaddr + ((gi ^ (rl & 7)) << 4), make_uint4(p[4 * q], p[4 * q + 1], p[4 * q + 2], p[4 * q + 3]));
+    }
+  }
+  release_tmem();
+  if (row_ok) {
+    a.partials[(size_t)n_blk * a.M + r] = make_float2(mx, s);
+    if (tl >= 0) a.zt[r] = zt;
+  }
+  fence_proxy_async_smem();
+  named_bar_sync(1, 128);
+  if (lead) {
+    const int nch = (ncols + 63) / 64;
+    if (!(a.mode & 32))  // mode bit 32: skip the stash stores (timing experiment only)
+      for (int k = 0; k < nch; ++k) tma_store_2d(tmC, stg + k * CHUNK_BYTES, n0 + k * 64, row0);
+    bulk_commit();
+  }
+}
+
 // Runtime epilogue dispatch (one problem of a group decides per tile).
 __device__ __forceinline__ void epilogue_dispatch(int epi, const GemmArgs& a, uint32_t taddr, int row0, int n_blk,
                                                   int row_in_tile) {
@@ -477,7 +553,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
 
   if (warp == 0 && lane == 0) {
     for (int i = 0; i < 3 * g.nprob; ++i)
-      if (i % 3 < 2 || g.p[i / 3].epi == EPI_DW) tma_prefetch_desc(&tm.m[i]);
+      if (i % 3 < 2 || g.p[i / 3].epi == EPI_DW || g.p[i / 3].a.tma_out) tma_prefetch_desc(&tm.m[i]);
 #pragma unroll
     for (int i = 0; i < C::STAGES; ++i) {
       mbar_init(&full[i], 1);
@@ -661,6 +737,9 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
         }
         epilogue_dw_tma(P.a, &tm.m[3 * pi + 2], taddr, m_blk * C::TILE_M + (int)rank * BM, n_blk, ew * 32 + lane,
                         stg, sbar, sphase, ew == 0 && lane == 0, wait_acc, release, g.dbg);
+      } else if (P.epi == EPI_STASH && P.a.tma_out) {  // a stash tensor map is provided
+        epilogue_stash_tma(P.a, &tm.m[3 * pi + 2], taddr, m_blk * C::TILE_M + (int)rank * BM, n_blk, ew * 32 + lane,
+                           stg, ew == 0 && lane == 0, wait_acc, release);
       } else {
         wait_acc();
         epilogue_dispatch(P.epi, P.a, taddr, m_blk * C::TILE_M + (int)rank * BM, n_blk, ew * 32 + lane);

@@ -77,6 +77,8 @@ __global__ void __launch_bounds__(256) combine_transform_kernel(
     const WsHeader* __restrict__ hdr, float* __restrict__ loss_rows, slf_rowstat* __restrict__ rowstat,
     uint16_t* __restrict__ stash) {
   extern __shared__ float r_t[];  // [tiles]
+  griddep_launch_dependents();
+  griddep_wait();  // PDL: everything below reads the previous kernel's outputs
   __shared__ float sM, sLse, red[256];
   const int i = blockIdx.x;
   const int tid = threadIdx.x;

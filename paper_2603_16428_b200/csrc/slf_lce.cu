@@ -694,8 +694,15 @@ slf_status s_chunk_stats(Ctx& c, const SArgs& a, int64_t ch, slf_shardstat* out)
   g.out = c.ws + p.off_stash;
   g.ld_out = p.ld_stash;
   static const int dbg = getenv("SLF_DEBUG_EPI") ? atoi(getenv("SLF_DEBUG_EPI")) : 0;
-  g.mode = dbg & 32;  // timing experiment only: skip the stash stores
-  SLF_TRY((launch_gemm<EPI_STASH, false, false>(c.dev, ta, tb, g, c.s)));
+  g.mode = dbg & 32;            // timing experiment only: skip the stash stores
+  g.tma_out = !(dbg & 64);      // stash written through TMA-staged stores (64: thread-per-row stores)
+  ProbSpec ps;
+  ps.ta = ta;
+  ps.tb = tb;
+  SLF_TRY(tmap_kmajor(&ps.tc, c.ws + p.off_stash, a.V_l, rows, p.ld_stash, BM));
+  ps.a = g;
+  ps.epi = EPI_STASH;
+  SLF_TRY(launch_group(c.dev, &ps, 1, c.s));
   if (out) {  // shard statistics for the all-gather (vocab shards); one GPU merges in combine_transform
     const int tiles_v = (int)((a.V_l + BN - 1) / BN);
     ProfScope ps(SLF_PROF_LOCAL_COMBINE, c.s, 0.0, (double)rows * (tiles_v * 8.0 + 24));
@@ -767,12 +774,22 @@ slf_status s_chunk_bwd(Ctx& c, const SArgs& a, int64_t ch, const slf_shardstat* 
   const int tiles_v = (int)((a.V_l + BN - 1) / BN);
   {
     ProfScope ps(SLF_PROF_COMBINE_TRANSFORM, c.s, 0.0, (double)rows * (tiles_v * 8.0 + a.V_l * 4.0 + 16.0 * g + 24));
-    combine_transform_kernel<<<(unsigned)rows, 256, tiles_v * sizeof(float), c.s>>>(
-        st, g, reinterpret_cast<const float2*>(c.ws + p.off_part), tiles_v, (int)rows,
-        reinterpret_cast<const float*>(c.ws + p.off_zt) + r0, a.t + r0, a.vs, a.V_l, a.Vg,
-        p.ld_stash, a.ign, reduction, scale, 1.0f, hdr_of(c.ws), loss_rows_all + r0,
-        reinterpret_cast<slf_rowstat*>(c.ws + p.off_rowstat) + r0, reinterpret_cast<uint16_t*>(c.ws + p.off_stash));
-    SLF_CUDA(cudaGetLastError());
+    // Programmatic dependent launch: blocks start while the stash GEMM drains and wait in-kernel.
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)rows);
+    cfg.blockDim = dim3(256);
+    cfg.dynamicSmemBytes = tiles_v * sizeof(float);
+    cfg.stream = c.s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    SLF_CUDA(cudaLaunchKernelEx(
+        &cfg, combine_transform_kernel, st, g, reinterpret_cast<const float2*>(c.ws + p.off_part), tiles_v, (int)rows,
+        reinterpret_cast<const float*>(c.ws + p.off_zt) + r0, a.t + r0, a.vs, a.V_l, a.Vg, p.ld_stash, a.ign,
+        reduction, scale, 1.0f, (const WsHeader*)hdr_of(c.ws), loss_rows_all + r0,
+        reinterpret_cast<slf_rowstat*>(c.ws + p.off_rowstat) + r0, reinterpret_cast<uint16_t*>(c.ws + p.off_stash)));
   }
   if (!dXc && !dW) return SLF_OK;
   ProbSpec ps[2];
