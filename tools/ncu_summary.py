@@ -21,6 +21,7 @@ KEYS = [
     ("sm__cycles_elapsed.avg.per_second", "SM clock"),
     ("TPC.TriageCompute.sm__pipe_tensor_cycles_active_realtime.avg.pct_of_peak_sustained_elapsed",
      "tensor pipe active % (elapsed)"),
+    ("sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_elapsed", "tensor pipe active % (sm__pipe)"),
     ("sm__mem_tensor_cycles_active.avg.pct_of_peak_sustained_elapsed", "tensor smem-read active %"),
     ("sm__throughput.avg.pct_of_peak_sustained_elapsed", "SM throughput %"),
     ("lts__throughput.avg.pct_of_peak_sustained_elapsed", "L2 throughput %"),
@@ -54,6 +55,8 @@ def main():
     ap.add_argument("--config", default="llama8b")
     ap.add_argument("--note", default="")
     ap.add_argument("--rep-kinds", default="", help="comma list naming the captured GEMM launches in order")
+    ap.add_argument("--split-ms", type=float, default=0.0,
+                    help="label lce_group_kernel launches >= this many ms as gemm_group, shorter as gemm_stats")
     ap.add_argument("--launch-cycle", default="",
                     help="comma list naming consecutive lce_group_kernel launches of the launch list cyclically")
     a = ap.parse_args()
@@ -94,6 +97,9 @@ def main():
             if cycle and "lce_group_kernel" in r[hdr.index("Kernel Name")]:
                 k = cycle[gi % len(cycle)]
                 gi += 1
+            if a.split_ms and "lce_group_kernel" in r[hdr.index("Kernel Name")]:
+                ms = float(r[hdr.index("Metric Value")].replace(",", "")) / 1e6
+                k = "gemm_group" if ms >= a.split_ms else "gemm_stats"
             agg[k][0] += 1
             agg[k][1] += float(r[hdr.index("Metric Value")].replace(",", "")) / 1e6
         tot = sum(v[1] for v in agg.values())
