@@ -390,7 +390,7 @@ __device__ __forceinline__ void epilogue_dw_tma(const GemmArgs& a, const CUtenso
 template <typename WaitAcc, typename ReleaseTmem>
 __device__ __forceinline__ void epilogue_stash_tma(const GemmArgs& a, const CUtensorMap* tmC, uint32_t taddr,
                                                    int row0, int n_blk, int rl, uint8_t* stg, bool lead,
-                                                   WaitAcc wait_acc, ReleaseTmem release_tmem) {
+                                                   WaitAcc wait_acc, ReleaseTmem release_tmem, int c_off = 0) {
   constexpr uint32_t CHUNK_BYTES = BM * 64 * 2;
   const int r = row0 + rl;
   const bool row_ok = r < a.M;
@@ -453,7 +453,7 @@ __device__ __forceinline__ void epilogue_stash_tma(const GemmArgs& a, const CUte
   if (lead) {
     const int nch = (ncols + 63) / 64;
     if (!(a.mode & 32))  // mode bit 32: skip the stash stores (timing experiment only)
-      for (int k = 0; k < nch; ++k) tma_store_2d(tmC, stg + k * CHUNK_BYTES, n0 + k * 64, row0);
+      for (int k = 0; k < nch; ++k) tma_store_2d(tmC, stg + k * CHUNK_BYTES, n0 + k * 64, row0 - c_off);
     bulk_commit();
   }
 }
@@ -488,9 +488,16 @@ __device__ __forceinline__ unsigned long long clk() {
   return c;
 }
 
+// A problem's A operand (and the TMA-staged output C) may live in two row segments of different
+// tensors (schedule S's stash extended into the caller's free dhidden rows): rows (the tensor's
+// outer dimension) >= a_split come from map A2 at row - a_split, output rows >= c_split go to C2.
+constexpr int MAPS_PER_PROB = 5;  // A, B, C, A2, C2
+constexpr int NO_SPLIT = 0x7fffffff;
+
 struct Prob {
   GemmArgs a;
   int epi, a_mn, b_mn, tile_begin;
+  int a_split, c_split;
 };
 
 struct GroupArgs {
@@ -504,7 +511,7 @@ struct GroupArgs {
 };
 
 struct TMaps {
-  CUtensorMap m[3 * MAXP];  // A, B, and the output C (EPI_DW: dW, TMA-staged epilogue) of each problem
+  CUtensorMap m[MAPS_PER_PROB * MAXP];  // A, B, C (TMA-staged output), A2, C2 of each problem
 };
 
 struct TileIter {
@@ -552,8 +559,14 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
   const int units = gridDim.x / CG;
 
   if (warp == 0 && lane == 0) {
-    for (int i = 0; i < 3 * g.nprob; ++i)
-      if (i % 3 < 2 || g.p[i / 3].epi == EPI_DW || g.p[i / 3].a.tma_out) tma_prefetch_desc(&tm.m[i]);
+    for (int pi = 0; pi < g.nprob; ++pi) {
+      const Prob& P = g.p[pi];
+      tma_prefetch_desc(&tm.m[MAPS_PER_PROB * pi]);
+      tma_prefetch_desc(&tm.m[MAPS_PER_PROB * pi + 1]);
+      if (P.epi == EPI_DW || P.a.tma_out) tma_prefetch_desc(&tm.m[MAPS_PER_PROB * pi + 2]);
+      if (P.a_split != NO_SPLIT) tma_prefetch_desc(&tm.m[MAPS_PER_PROB * pi + 3]);
+      if (P.c_split != NO_SPLIT) tma_prefetch_desc(&tm.m[MAPS_PER_PROB * pi + 4]);
+    }
 #pragma unroll
     for (int i = 0; i < C::STAGES; ++i) {
       mbar_init(&full[i], 1);
@@ -593,8 +606,9 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
       for (int tile = it.next(); tile >= 0; tile = it.next()) {
         const int pi = prob_of(g, tile);
         const Prob& P = g.p[pi];
-        const CUtensorMap* tA = &tm.m[3 * pi];
-        const CUtensorMap* tB = &tm.m[3 * pi + 1];
+        const CUtensorMap* tA = &tm.m[MAPS_PER_PROB * pi];
+        const CUtensorMap* tB = &tm.m[MAPS_PER_PROB * pi + 1];
+        const CUtensorMap* tA2 = &tm.m[MAPS_PER_PROB * pi + 3];
         int m_blk, n_blk;
         tile_coords(tile - P.tile_begin, P.a, m_blk, n_blk);
         const int a_row = m_blk * C::TILE_M + (int)rank * BM;
@@ -605,13 +619,23 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
           mbar_wait(&empty[stage], phase ^ 1);
           uint8_t* a_dst = sA + stage * C::A_BYTES;
           uint8_t* b_dst = sB + stage * C::B_BYTES;
+          // A's outer (row) coordinate: M for K-major A, K for MN-major A; rows >= a_split come
+          // from the second segment's map.
+          const CUtensorMap* tAk = tA;
+          int a_r = a_row, a_k = kb * BK;
+          if (!a_mn) {
+            if (a_r >= P.a_split) { tAk = tA2; a_r -= P.a_split; }
+          } else if (a_k >= P.a_split) {
+            tAk = tA2;
+            a_k -= P.a_split;
+          }
           if constexpr (CG == 1) {
             mbar_arrive_expect_tx(&full[stage], C::STAGE_BYTES);
             if (!a_mn) {
-              tma_load_2d(tA, &full[stage], a_dst, kb * BK, a_row, pol);
+              tma_load_2d(tAk, &full[stage], a_dst, a_k, a_r, pol);
             } else {
 #pragma unroll
-              for (int j = 0; j < BM / 64; ++j) tma_load_2d(tA, &full[stage], a_dst + j * 8192, a_row + j * 64, kb * BK, pol);
+              for (int j = 0; j < BM / 64; ++j) tma_load_2d(tAk, &full[stage], a_dst + j * 8192, a_r + j * 64, a_k, pol);
             }
             if (!b_mn) {
               tma_load_2d(tB, &full[stage], b_dst, kb * BK, b_row, pol);
@@ -625,10 +649,10 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
             if (rank == 0) mbar_arrive_expect_tx(&full[stage], C::STAGE_BYTES * 2);
             const uint32_t fb = mapa_shared(smem_u32(&full[stage]), 0);
             if (!a_mn) {
-              tma_load_2d_pair(tA, fb, a_dst, kb * BK, a_row, pol);
+              tma_load_2d_pair(tAk, fb, a_dst, a_k, a_r, pol);
             } else {
 #pragma unroll
-              for (int j = 0; j < BM / 64; ++j) tma_load_2d_pair(tA, fb, a_dst + j * 8192, a_row + j * 64, kb * BK, pol);
+              for (int j = 0; j < BM / 64; ++j) tma_load_2d_pair(tAk, fb, a_dst + j * 8192, a_r + j * 64, a_k, pol);
             }
             if (!b_mn) {
               tma_load_2d_pair(tB, fb, b_dst, kb * BK, b_row, pol);
@@ -732,14 +756,16 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
             int qm, qn;
             tile_coords(nt - Q.tile_begin, Q.a, qm, qn);
             for (int k = 0; k < BN / 64 && qn * BN + k * 64 < Q.a.N; ++k)
-              tma_prefetch_l2_2d(&tm.m[3 * npi + 2], qn * BN + k * 64, qm * C::TILE_M + (int)rank * BM);
+              tma_prefetch_l2_2d(&tm.m[MAPS_PER_PROB * npi + 2], qn * BN + k * 64, qm * C::TILE_M + (int)rank * BM);
           }
         }
-        epilogue_dw_tma(P.a, &tm.m[3 * pi + 2], taddr, m_blk * C::TILE_M + (int)rank * BM, n_blk, ew * 32 + lane,
+        epilogue_dw_tma(P.a, &tm.m[MAPS_PER_PROB * pi + 2], taddr, m_blk * C::TILE_M + (int)rank * BM, n_blk, ew * 32 + lane,
                         stg, sbar, sphase, ew == 0 && lane == 0, wait_acc, release, g.dbg);
       } else if (P.epi == EPI_STASH && P.a.tma_out) {  // a stash tensor map is provided
-        epilogue_stash_tma(P.a, &tm.m[3 * pi + 2], taddr, m_blk * C::TILE_M + (int)rank * BM, n_blk, ew * 32 + lane,
-                           stg, ew == 0 && lane == 0, wait_acc, release);
+        const int row0 = m_blk * C::TILE_M + (int)rank * BM;  // output rows >= c_split go to map C2
+        const bool seg2 = row0 >= P.c_split;
+        epilogue_stash_tma(P.a, &tm.m[MAPS_PER_PROB * pi + (seg2 ? 4 : 2)], taddr, row0, n_blk, ew * 32 + lane,
+                           stg, ew == 0 && lane == 0, wait_acc, release, seg2 ? P.c_split : 0);
       } else {
         wait_acc();
         epilogue_dispatch(P.epi, P.a, taddr, m_blk * C::TILE_M + (int)rank * BM, n_blk, ew * 32 + lane);

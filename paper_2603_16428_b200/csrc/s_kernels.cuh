@@ -75,7 +75,8 @@ __global__ void __launch_bounds__(256) combine_transform_kernel(
     const float* __restrict__ zt, const int32_t* __restrict__ t, int64_t vocab_start, int64_t V_l, int64_t V_global,
     int64_t ld_stash, int32_t ignore_index, int reduction, float scale, float grad_scale,
     const WsHeader* __restrict__ hdr, float* __restrict__ loss_rows, slf_rowstat* __restrict__ rowstat,
-    uint16_t* __restrict__ stash) {
+    uint16_t* __restrict__ stash, uint16_t* __restrict__ stash2, int split) {
+  // rows [0, split) of the chunk's stash are in `stash`, rows [split, rows) in `stash2` (same stride)
   extern __shared__ float r_t[];  // [tiles]
   griddep_launch_dependents();
   griddep_wait();  // PDL: everything below reads the previous kernel's outputs
@@ -118,7 +119,7 @@ __global__ void __launch_bounds__(256) combine_transform_kernel(
   for (int k = tid; k < tiles; k += 256) r_t[k] = cg * ex2(partials[(size_t)k * rows + i].x * LOG2E - lse2);
   __syncthreads();
   // G_P = p~ * r_t, in place, 8 bf16 per 16-byte access.
-  uint4* row = reinterpret_cast<uint4*>(stash + (size_t)i * ld_stash);
+  uint4* row = reinterpret_cast<uint4*>(i < split ? stash + (size_t)i * ld_stash : stash2 + (size_t)(i - split) * ld_stash);
   const int64_t groups = (V_l + 7) / 8;
   constexpr int U = 4;  // 4 independent 16-byte loads in flight per thread
   for (int64_t q0 = tid; q0 < groups; q0 += 256 * U) {

@@ -167,10 +167,12 @@ uint32_t b_box_rows() { return (uint32_t)(BN / cta_group()); }
 
 // One GEMM problem of a launch: operand tensor maps, extents and epilogue arguments.
 struct ProbSpec {
-  CUtensorMap ta, tb, tc;  // tc: output map (EPI_DW only)
+  CUtensorMap ta, tb, tc;  // tc: TMA-staged output map (EPI_DW, EPI_STASH)
+  CUtensorMap ta2, tc2;    // second row segment of A / of the output (see Prob::a_split / c_split)
   GemmArgs a{};
   int epi = EPI_F32;
   bool a_mn = false, b_mn = false;
+  int a_split = NO_SPLIT, c_split = NO_SPLIT;
 };
 
 int prof_kind_of(int epi) {
@@ -255,10 +257,12 @@ slf_status launch_group_cg(DevInfo* dev, ProbSpec* ps, int n, cudaStream_t s, co
     GemmArgs a = ps[p].a;
     if (a.M <= 0 || a.N <= 0 || a.K <= 0) continue;
     finish_geometry(a, CG);
-    tm.m[3 * np] = ps[p].ta;
-    tm.m[3 * np + 1] = ps[p].tb;
-    tm.m[3 * np + 2] = ps[p].tc;
-    g.p[np] = Prob{a, ps[p].epi, ps[p].a_mn ? 1 : 0, ps[p].b_mn ? 1 : 0, total};
+    tm.m[MAPS_PER_PROB * np] = ps[p].ta;
+    tm.m[MAPS_PER_PROB * np + 1] = ps[p].tb;
+    tm.m[MAPS_PER_PROB * np + 2] = ps[p].tc;
+    tm.m[MAPS_PER_PROB * np + 3] = ps[p].ta2;
+    tm.m[MAPS_PER_PROB * np + 4] = ps[p].tc2;
+    g.p[np] = Prob{a, ps[p].epi, ps[p].a_mn ? 1 : 0, ps[p].b_mn ? 1 : 0, total, ps[p].a_split, ps[p].c_split};
     total += a.num_tiles;
     flops += 2.0 * a.M * a.N * (double)a.K;
     ++np;
@@ -330,7 +334,7 @@ struct Plan {
   size_t fwd_bytes = 0, bwd_bytes = 0, total = 0;
 };
 
-constexpr size_t SCHED_ARENA_BYTES = 256 * 1024;
+constexpr size_t SCHED_ARENA_BYTES = 1024 * 1024;
 
 size_t default_budget(int64_t N, int64_t V) {
   const size_t five = (size_t)(0.05 * (double)N * (double)V * 2.0);
@@ -388,7 +392,7 @@ bool plan_r(int64_t N, int64_t H, int64_t V, size_t budget, Plan* out) {
 }
 
 // Schedule S layout: header | sched arena | RowStat [N] | z_t [N] | row losses [N] | CSR counts
-// [V+2] | CSR offsets [V+2] | hit rows [min(N,V)] | CSR token idx [N] | tile partials [tiles][C] |
+// [V+2] | CSR offsets [V+2] | hit rows [min(N,V)] | CSR token idx [N] | tile partials [tiles][2C] |
 // stash [C][ld_stash] bf16.  C = the largest multiple of 256 rows that fits the budget.
 bool plan_s(int64_t N, int64_t H, int64_t V, size_t budget, Plan* out) {
   if (N < 1 || H < 8 || V < 1) return false;
@@ -410,7 +414,7 @@ bool plan_s(int64_t N, int64_t H, int64_t V, size_t budget, Plan* out) {
   const int64_t Nmax = (int64_t)align_up((size_t)N, 256);
   int64_t best = 0;
   for (int64_t C = 256; C <= Nmax; C += 256) {
-    const size_t part = align_up((size_t)tiles_v * C * 8, 1024);
+    const size_t part = align_up((size_t)tiles_v * 2 * C * 8, 1024);  // 2C: room for extended chunks
     const size_t tot = p.off_part + part + (size_t)C * p.ld_stash * 2;
     if (tot <= budget) best = C;
     else break;
@@ -418,7 +422,7 @@ bool plan_s(int64_t N, int64_t H, int64_t V, size_t budget, Plan* out) {
   if (best == 0) return false;
   p.C = best;
   p.nCh = (N + best - 1) / best;
-  p.off_stash = p.off_part + align_up((size_t)tiles_v * best * 8, 1024);
+  p.off_stash = p.off_part + align_up((size_t)tiles_v * 2 * best * 8, 1024);
   p.total = p.off_stash + (size_t)best * p.ld_stash * 2;
   p.fwd_bytes = p.total - p.off_part;
   *out = p;
@@ -674,14 +678,28 @@ slf_status s_begin(Ctx& c, const SArgs& a, bool need_dw) {
 }
 
 // Stash GEMM of chunk `ch` and this shard's per-row statistics of the chunk (out[rows]).
-slf_status s_chunk_stats(Ctx& c, const SArgs& a, int64_t ch, slf_shardstat* out) {
+// One row chunk of schedule S: rows [r0, r0 + rows).  The first min(rows, C) stash rows live in the
+// workspace; on the fused single-GPU call the chunk may be extended by `ext` rows whose stash
+// lives in the caller's dhidden buffer beyond this chunk's rows (rows not written yet).
+struct SChunk {
+  int64_t index, r0, rows, ext;
+  uint8_t* ext_base;  // stash rows [rows - ext, rows): row stride ld_stash, or nullptr
+};
+
+SChunk s_plain_chunk(const Plan& p, int64_t N, int64_t ch) {
+  const int64_t r0 = ch * p.C;
+  return SChunk{ch, r0, std::min(p.C, N - r0), 0, nullptr};
+}
+
+// Stash GEMM of a chunk and this shard's per-row statistics of the chunk (out[rows]).
+slf_status s_chunk_stats(Ctx& c, const SArgs& a, const SChunk& k, slf_shardstat* out) {
   const Plan& p = c.plan;
-  const int64_t r0 = ch * p.C, rows = std::min(p.C, a.N - r0);
+  const int64_t r0 = k.r0, rows = k.rows, main_rows = rows - k.ext;
   float* zt = reinterpret_cast<float*>(c.ws + p.off_zt);
   float2* part = reinterpret_cast<float2*>(c.ws + p.off_part);
-  CUtensorMap ta, tb;
-  SLF_TRY(tmap_kmajor(&ta, reinterpret_cast<const uint8_t*>(a.X) + (size_t)r0 * a.H * 2, a.H, rows, a.H, BM));
-  SLF_TRY(tmap_kmajor(&tb, a.W, a.H, a.V_l, a.H, b_box_rows()));
+  ProbSpec ps;
+  SLF_TRY(tmap_kmajor(&ps.ta, reinterpret_cast<const uint8_t*>(a.X) + (size_t)r0 * a.H * 2, a.H, rows, a.H, BM));
+  SLF_TRY(tmap_kmajor(&ps.tb, a.W, a.H, a.V_l, a.H, b_box_rows()));
   GemmArgs g{};
   g.M = (int)rows;
   g.N = (int)a.V_l;
@@ -694,18 +712,19 @@ slf_status s_chunk_stats(Ctx& c, const SArgs& a, int64_t ch, slf_shardstat* out)
   g.out = c.ws + p.off_stash;
   g.ld_out = p.ld_stash;
   static const int dbg = getenv("SLF_DEBUG_EPI") ? atoi(getenv("SLF_DEBUG_EPI")) : 0;
-  g.mode = dbg & 32;            // timing experiment only: skip the stash stores
-  g.tma_out = !(dbg & 64);      // stash written through TMA-staged stores (64: thread-per-row stores)
-  ProbSpec ps;
-  ps.ta = ta;
-  ps.tb = tb;
-  SLF_TRY(tmap_kmajor(&ps.tc, c.ws + p.off_stash, a.V_l, rows, p.ld_stash, BM));
+  g.mode = dbg & 32;  // timing experiment only: skip the stash stores
+  g.tma_out = 1;      // the stash is written through TMA-staged stores
+  SLF_TRY(tmap_kmajor(&ps.tc, c.ws + p.off_stash, a.V_l, main_rows, p.ld_stash, BM));
+  if (k.ext) {
+    SLF_TRY(tmap_kmajor(&ps.tc2, k.ext_base, a.V_l, k.ext, p.ld_stash, BM));
+    ps.c_split = (int)main_rows;
+  }
   ps.a = g;
   ps.epi = EPI_STASH;
   SLF_TRY(launch_group(c.dev, &ps, 1, c.s));
   if (out) {  // shard statistics for the all-gather (vocab shards); one GPU merges in combine_transform
     const int tiles_v = (int)((a.V_l + BN - 1) / BN);
-    ProfScope ps(SLF_PROF_LOCAL_COMBINE, c.s, 0.0, (double)rows * (tiles_v * 8.0 + 24));
+    ProfScope pr(SLF_PROF_LOCAL_COMBINE, c.s, 0.0, (double)rows * (tiles_v * 8.0 + 24));
     shard_rows_kernel<<<(unsigned)rows, 256, 0, c.s>>>(part, tiles_v, (int)rows, zt + r0, a.t + r0, a.vs, a.V_l, a.ign,
                                                        out);
     SLF_CUDA(cudaGetLastError());
@@ -713,22 +732,27 @@ slf_status s_chunk_stats(Ctx& c, const SArgs& a, int64_t ch, slf_shardstat* out)
   return SLF_OK;
 }
 
-slf_status s_build_bwd(Ctx& c, const SArgs& a, int64_t ch, void* dXc, int dx_fp32, void* dW, ProbSpec* ps, int* n) {
+slf_status s_build_bwd(Ctx& c, const SArgs& a, const SChunk& k, void* dXc, int dx_fp32, void* dW, ProbSpec* ps,
+                       int* n) {
   const Plan& p = c.plan;
   const int cg = cta_group();
-  const int64_t r0 = ch * p.C, rows = std::min(p.C, a.N - r0);
+  const int64_t r0 = k.r0, rows = k.rows, main_rows = rows - k.ext;
   const uint8_t* Xr = reinterpret_cast<const uint8_t*>(a.X) + (size_t)r0 * a.H * 2;
   uint8_t* stash = c.ws + p.off_stash;
   slf_rowstat* rs = reinterpret_cast<slf_rowstat*>(c.ws + p.off_rowstat);
   *n = 0;
-  if (dXc) {  // dX_chunk = G_P W : A = G_P (K-major over V_l), B = W (MN-major)
+  if (dXc) {  // dX_chunk = G_P W : A = G_P (K-major over V_l, rows split ws | ext), B = W (MN-major)
     ProbSpec& q = ps[(*n)++];
-    SLF_TRY(tmap_kmajor(&q.ta, stash, a.V_l, rows, p.ld_stash, BM));
+    q = ProbSpec{};
+    SLF_TRY(tmap_kmajor(&q.ta, stash, a.V_l, main_rows, p.ld_stash, BM));
+    if (k.ext) {
+      SLF_TRY(tmap_kmajor(&q.ta2, k.ext_base, a.V_l, k.ext, p.ld_stash, BM));
+      q.a_split = (int)main_rows;
+    }
     SLF_TRY(tmap_mnmajor(&q.tb, a.W, a.H, a.V_l, a.H));
     q.epi = EPI_DXS;
     q.a_mn = false;
     q.b_mn = true;
-    q.a = GemmArgs{};
     q.a.M = (int)rows;
     q.a.N = (int)a.H;
     q.a.K = (int)a.V_l;
@@ -741,19 +765,23 @@ slf_status s_build_bwd(Ctx& c, const SArgs& a, int64_t ch, void* dXc, int dx_fp3
     q.a.mode = dx_fp32 ? 1 : 0;
     finish_geometry(q.a, cg);
   }
-  if (dW) {  // dW (+)= G_P^T X_chunk : A = G_P^T (MN-major), B = X_chunk (MN-major)
+  if (dW) {  // dW (+)= G_P^T X_chunk : A = G_P^T (MN-major; K = rows split ws | ext), B = X_chunk (MN-major)
     ProbSpec& q = ps[(*n)++];
-    SLF_TRY(tmap_mnmajor(&q.ta, stash, a.V_l, rows, p.ld_stash));
+    q = ProbSpec{};
+    SLF_TRY(tmap_mnmajor(&q.ta, stash, a.V_l, main_rows, p.ld_stash));
+    if (k.ext) {
+      SLF_TRY(tmap_mnmajor(&q.ta2, k.ext_base, a.V_l, k.ext, p.ld_stash));
+      q.a_split = (int)main_rows;
+    }
     SLF_TRY(tmap_mnmajor(&q.tb, Xr, a.H, rows, a.H));
     q.epi = EPI_DW;
     q.a_mn = q.b_mn = true;
-    q.a = GemmArgs{};
     q.a.M = (int)a.V_l;
     q.a.N = (int)a.H;
     q.a.K = (int)rows;
     q.a.out = dW;
     q.a.ld_out = a.H;
-    q.a.mode = (ch > 0 || c.acc_dw) ? 1 : 0;
+    q.a.mode = (k.index > 0 || c.acc_dw) ? 1 : 0;
     static const bool no_rmw = getenv("SLF_DEBUG_DW_NO_RMW") != nullptr;  // timing experiments only (wrong dW)
     if (no_rmw) q.a.mode = 0;
     SLF_TRY(tmap_kmajor(&q.tc, dW, a.H, a.V_l, a.H, BM));
@@ -762,15 +790,15 @@ slf_status s_build_bwd(Ctx& c, const SArgs& a, int64_t ch, void* dXc, int dx_fp3
   return SLF_OK;
 }
 
-// Merge the g shards' statistics of chunk `ch` (st[g][rows], shard order), transform the stash in
-// place, and run the grouped dX/dW launch.  dXc = row 0 of the chunk's dhidden rows (bf16, or fp32
-// when dx_fp32: this shard's partial, to be summed across shards).  `sched` (optional) is a
-// prebuilt LPT table for this chunk shape; otherwise one is built and uploaded.
-slf_status s_chunk_bwd(Ctx& c, const SArgs& a, int64_t ch, const slf_shardstat* st, int g, int reduction, float scale,
-                       float* loss_rows_all, void* dXc, int dx_fp32, void* dW, const int* sched = nullptr,
+// Merge the g shards' statistics of the chunk (st[g][rows], shard order; nullptr on one GPU: the
+// chunk's own tile partials), transform the stash in place, and run the grouped dX/dW launch.
+// dXc = row 0 of the chunk's dhidden rows (bf16, or fp32 when dx_fp32: this shard's partial, to be
+// summed across shards).  `sched` (optional) is a prebuilt LPT table for this chunk shape.
+slf_status s_chunk_bwd(Ctx& c, const SArgs& a, const SChunk& k, const slf_shardstat* st, int g, int reduction,
+                       float scale, float* loss_rows_all, void* dXc, int dx_fp32, void* dW, const int* sched = nullptr,
                        int sched_stride = 0) {
   const Plan& p = c.plan;
-  const int64_t r0 = ch * p.C, rows = std::min(p.C, a.N - r0);
+  const int64_t r0 = k.r0, rows = k.rows;
   const int tiles_v = (int)((a.V_l + BN - 1) / BN);
   {
     ProfScope ps(SLF_PROF_COMBINE_TRANSFORM, c.s, 0.0, (double)rows * (tiles_v * 8.0 + a.V_l * 4.0 + 16.0 * g + 24));
@@ -789,18 +817,19 @@ slf_status s_chunk_bwd(Ctx& c, const SArgs& a, int64_t ch, const slf_shardstat* 
         &cfg, combine_transform_kernel, st, g, reinterpret_cast<const float2*>(c.ws + p.off_part), tiles_v, (int)rows,
         reinterpret_cast<const float*>(c.ws + p.off_zt) + r0, a.t + r0, a.vs, a.V_l, a.Vg, p.ld_stash, a.ign,
         reduction, scale, 1.0f, (const WsHeader*)hdr_of(c.ws), loss_rows_all + r0,
-        reinterpret_cast<slf_rowstat*>(c.ws + p.off_rowstat) + r0, reinterpret_cast<uint16_t*>(c.ws + p.off_stash)));
+        reinterpret_cast<slf_rowstat*>(c.ws + p.off_rowstat) + r0, reinterpret_cast<uint16_t*>(c.ws + p.off_stash),
+        reinterpret_cast<uint16_t*>(k.ext_base), (int)(rows - k.ext)));
   }
   if (!dXc && !dW) return SLF_OK;
   ProbSpec ps[2];
   int n = 0;
-  SLF_TRY(s_build_bwd(c, a, ch, dXc, dx_fp32, dW, ps, &n));
+  SLF_TRY(s_build_bwd(c, a, k, dXc, dx_fp32, dW, ps, &n));
   SchedArena arena;
   if (!sched) {
-    const int k = arena.add(ps, n, c.dev->sms / cta_group());
+    const int t = arena.add(ps, n, c.dev->sms / cta_group());
     SLF_TRY(arena.upload(c));
-    sched = arena.dev(c, k);
-    sched_stride = arena.tables[k].second;
+    sched = arena.dev(c, t);
+    sched_stride = arena.tables[t].second;
   }
   return launch_group(c.dev, ps, n, c.s, sched, sched_stride, n == 2 ? SLF_PROF_GEMM_GROUP : -1);
 }
@@ -830,36 +859,63 @@ float* s_loss_rows(Ctx& c, int reduction, float* loss_out) {
   return reduction == SLF_NONE ? loss_out : reinterpret_cast<float*>(c.ws + c.plan.off_loss);
 }
 
-// The fused single-GPU call under schedule S (g = 1: a chunk's statistics are its own).
+// The fused single-GPU call under schedule S (g = 1: a chunk's statistics are its own).  When dX
+// is requested, each chunk grows by `ext` rows whose stash lives in dhidden's not-yet-written rows
+// beyond the chunk (no extra memory): fewer chunks, fewer dW read-modify-write passes and longer
+// dW K.  SLF_S_NO_EXT=1 disables the extension.
 slf_status phase_s(Ctx& c, const void* X, const void* W, const int32_t* t, int64_t N, int64_t H, int64_t V,
                    int32_t ignore_index, int reduction, float scale, float* loss_out, void* dX, void* dW) {
   const Plan& p = c.plan;
   const SArgs a{X, W, t, N, H, V, 0, V, ignore_index};
   SLF_TRY(s_begin(c, a, dW != nullptr));
-  // LPT tables for the full and the ragged last chunk, uploaded once.
+  static const bool no_ext = getenv("SLF_S_NO_EXT") != nullptr;
+  std::vector<SChunk> chunks;
+  for (int64_t r0 = 0, ci = 0; r0 < N; ++ci) {
+    SChunk k{ci, r0, std::min(p.C, N - r0), 0, nullptr};
+    if (dX && !no_ext && k.rows == p.C) {
+      // ext rows E with E*ld_stash <= (N - r0 - C - E)*H, a multiple of 128, at most C (partials room)
+      const int64_t free_rows = N - r0 - p.C;
+      int64_t e = free_rows > 0 ? (free_rows * H) / (p.ld_stash + H) : 0;
+      e = std::min<int64_t>(e, p.C) / 128 * 128;
+      if (e > 0) {
+        k.ext = e;
+        k.rows = p.C + e;
+        k.ext_base = reinterpret_cast<uint8_t*>(dX) + (size_t)(r0 + k.rows) * H * 2;
+      }
+    }
+    chunks.push_back(k);
+    r0 += k.rows;
+  }
+  // LPT tables per distinct chunk shape (rows, ext, first/RMW), uploaded once.
   SchedArena arena;
-  int k_full = -1, k_last = -1;
+  std::vector<std::pair<std::pair<int64_t, int64_t>, int>> keys;
+  std::vector<int> tab(chunks.size(), -1);
   if (dX || dW) {
-    ProbSpec ps[2];
-    int n = 0;
-    // A full chunk past the first (dW read-modify-write) represents the common case.
-    const int64_t rep = (p.nCh > 2 || (p.nCh == 2 && N % p.C == 0)) ? 1 : 0;
-    SLF_TRY(s_build_bwd(c, a, rep, dX, 0, dW, ps, &n));
-    k_full = arena.add(ps, n, c.dev->sms / cta_group());
-    if (N % p.C) {
-      SLF_TRY(s_build_bwd(c, a, p.nCh - 1, dX, 0, dW, ps, &n));
-      k_last = arena.add(ps, n, c.dev->sms / cta_group());
+    for (size_t i = 0; i < chunks.size(); ++i) {
+      const auto key = std::make_pair(chunks[i].rows, chunks[i].ext);
+      int found = -1;
+      for (auto& kk : keys)
+        if (kk.first == key) found = kk.second;
+      if (found < 0) {
+        ProbSpec ps[2];
+        int n = 0;
+        SChunk rep = chunks[i];
+        rep.index = std::max<int64_t>(rep.index, 1);  // model the common read-modify-write case
+        SLF_TRY(s_build_bwd(c, a, rep, dX ? (uint8_t*)dX + (size_t)rep.r0 * H * 2 : nullptr, 0, dW, ps, &n));
+        found = arena.add(ps, n, c.dev->sms / cta_group());
+        keys.push_back({key, found});
+      }
+      tab[i] = found;
     }
     SLF_TRY(arena.upload(c));
   }
   float* loss_rows = s_loss_rows(c, reduction, loss_out);
-  for (int64_t ch = 0; ch < p.nCh; ++ch) {
-    const int64_t r0 = ch * p.C, rows = std::min(p.C, N - r0);
-    SLF_TRY(s_chunk_stats(c, a, ch, nullptr));
-    const int k = (rows == p.C || k_last < 0) ? k_full : k_last;
-    SLF_TRY(s_chunk_bwd(c, a, ch, nullptr, 1, reduction, scale, loss_rows,
-                        dX ? reinterpret_cast<uint8_t*>(dX) + (size_t)r0 * H * 2 : nullptr, 0, dW,
-                        k >= 0 ? arena.dev(c, k) : nullptr, k >= 0 ? arena.tables[k].second : 0));
+  for (size_t i = 0; i < chunks.size(); ++i) {
+    const SChunk& k = chunks[i];
+    SLF_TRY(s_chunk_stats(c, a, k, nullptr));
+    SLF_TRY(s_chunk_bwd(c, a, k, nullptr, 1, reduction, scale, loss_rows,
+                        dX ? reinterpret_cast<uint8_t*>(dX) + (size_t)k.r0 * H * 2 : nullptr, 0, dW,
+                        tab[i] >= 0 ? arena.dev(c, tab[i]) : nullptr, tab[i] >= 0 ? arena.tables[tab[i]].second : 0));
   }
   return s_end(c, a, reduction, scale, loss_out, dW);
 }
@@ -1061,7 +1117,7 @@ slf_status slf_lce_s_chunk_stats(const void* hidden, const void* weight_shard, c
   SLF_TRY(setup_s(c, N, H, V_local, budget_bytes, workspace, workspace_bytes, stream));
   if (chunk < 0 || chunk >= c.plan.nCh) return fail(SLF_ERR_ARG, "chunk %lld out of range", (long long)chunk);
   const SArgs a{hidden, weight_shard, targets, N, H, V_local, vocab_start, V_global, ignore_index};
-  return s_chunk_stats(c, a, chunk, shardstat_chunk);
+  return s_chunk_stats(c, a, s_plain_chunk(c.plan, N, chunk), shardstat_chunk);
 }
 
 slf_status slf_lce_s_chunk_bwd(const void* hidden, const void* weight_shard, const int32_t* targets, int64_t N,
@@ -1081,7 +1137,8 @@ slf_status slf_lce_s_chunk_bwd(const void* hidden, const void* weight_shard, con
   if (chunk < 0 || chunk >= c.plan.nCh) return fail(SLF_ERR_ARG, "chunk %lld out of range", (long long)chunk);
   const SArgs a{hidden, weight_shard, targets, N, H, V_local, vocab_start, V_global, ignore_index};
   float* lr = reduction == SLF_NONE ? loss_rows : reinterpret_cast<float*>(c.ws + c.plan.off_loss);
-  return s_chunk_bwd(c, a, chunk, stats, g, reduction, scale, lr, dhidden_chunk, dhidden_fp32, dweight);
+  return s_chunk_bwd(c, a, s_plain_chunk(c.plan, N, chunk), stats, g, reduction, scale, lr, dhidden_chunk,
+                     dhidden_fp32, dweight);
 }
 
 slf_status slf_lce_s_end(const void* hidden, int64_t N, int64_t H, int64_t V_local, int reduction, float scale,

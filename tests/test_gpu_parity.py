@@ -100,6 +100,23 @@ def test_multichunk_ragged_parity_s(slf, reduction):
     check_against_oracle(slf, inp, reduction=reduction, budget=budget, schedule="S")
 
 
+@pytest.mark.gpu
+@pytest.mark.parametrize("reduction", ["mean", "none"])
+def test_extended_chunks_parity_s(slf, reduction):
+    """Schedule S with chunks extended into dhidden's unwritten rows: H/V large enough
+    that ext rows fit (C = 256, chunks of 512 and 384 rows), ragged tail, Zipf targets; also dX only."""
+    inp = synth.make_inputs(2000, 512, 1536, seed=16, alpha=4.0, dist="zipf")
+    budget = 3 << 19
+    desc = slf.plan_describe(2000, 512, 1536, budget_bytes=budget, schedule="S")
+    assert "row_chunk=256" in desc, desc
+    check_against_oracle(slf, inp, reduction=reduction, budget=budget, schedule="S")
+    X, W, t = to_dev(inp, torch)
+    _, dX1, _ = slf.lce_fwd_bwd(X, W, t, reduction=reduction, budget_bytes=budget, schedule="S",
+                                need_dweight=False)
+    _, dX2, _ = slf.lce_fwd_bwd(X, W, t, reduction=reduction, budget_bytes=budget, schedule="S")
+    assert torch.equal(dX1, dX2)
+
+
 @pytest.mark.parametrize("sched", SCHEDS)
 @pytest.mark.parametrize("N,H,V", [(1, 8, 1), (1, 64, 300), (130, 136, 257), (257, 512, 4096)])
 def test_small_edges(slf, N, H, V, sched):
