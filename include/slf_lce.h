@@ -31,9 +31,12 @@
  *    synchronous return codes; the message is in slf_last_error_string().
  *    Data errors (a valid target outside [0, V_global)) are asynchronous: the
  *    loss becomes NaN and slf_lce_status() reports the count.
- *  - No global mutable state except a thread-local last-error string and a
- *    per-device attribute cache; calls on different streams are independent
- *    provided they use different workspaces.
+ *  - No global mutable state except a thread-local last-error string, a
+ *    per-device attribute cache and a per-device 8 MB pinned HOST ring that
+ *    stages the per-call tile tables (allocated on first use, never freed);
+ *    calls on different streams are independent provided they use different
+ *    workspaces.  The calls are not CUDA-graph-capture safe (they copy tile
+ *    tables from that host ring).
  *  - Requirements: H % 8 == 0 (16-byte TMA row strides), N >= 1, V_local >= 1,
  *    an sm_100 device (SLF_ERR_UNSUPPORTED otherwise).
  */
@@ -214,7 +217,9 @@ slf_status slf_lce_s_rowstat(int64_t N, int64_t H, int64_t V_local, size_t budge
 /* Debug: copy the per-tile clock64 trace recorded for the launch selected by the environment
  * variable SLF_DEBUG_TRACE=k (the k-th GEMM launch of the process) into HOST `host` (n values,
  * 8 per tile: MMA tile start / after TMEM-free wait / issued, epilogue start / accumulator ready /
- * TMEM released / end, problem index).  Synchronises the device. */
+ * TMEM released / end, problem index), followed by 256 x 8 per-unit counters of that launch
+ * (MMA cycles waiting on full stages / on a free accumulator, first / last clock, K-blocks,
+ * producer cycles waiting on empty stages, tiles).  Synchronises the device. */
 slf_status slf_debug_trace_read(uint64_t* host, int64_t n);
 
 /* p[i] = bf16(p[i] * s) for a DEVICE bf16 array of n elements (n % 8 == 0, 16-byte aligned):

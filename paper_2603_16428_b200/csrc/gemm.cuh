@@ -43,8 +43,12 @@ struct Cfg {
   static constexpr int A_BYTES = BM * BK * 2;
   static constexpr int B_BYTES = B_ROWS * BK * 2;
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
-  static constexpr int STAGES = CG == 2 ? 5 : 3;
-  static constexpr int STAGING_BYTES = 4 * BM * 64 * 2;  // 4 x [128 rows x 64 bf16] epilogue TMA buffers
+#ifndef SLF_EXP_STAGES  // timing experiments only (tools/): other ring depths / staging sizes
+#define SLF_EXP_STAGES 5
+#define SLF_EXP_STAGING_CHUNKS 4
+#endif
+  static constexpr int STAGES = CG == 2 ? SLF_EXP_STAGES : 3;
+  static constexpr int STAGING_BYTES = SLF_EXP_STAGING_CHUNKS * BM * 64 * 2;  // [128 rows x 64 bf16] TMA buffers
   static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + STAGING_BYTES + 1024 /*align slack*/ + 256 /*barriers*/;
 };
 
@@ -342,7 +346,8 @@ __device__ __forceinline__ void epilogue_dw_tma(const GemmArgs& a, const CUtenso
   if (rmw && lead) {
     for (int k = 0; k < nch; ++k) {
       mbar_arrive_expect_tx(&sbar[k], CHUNK_BYTES);
-      tma_load_2d(tmC, &sbar[k], stg + k * CHUNK_BYTES, n0 + k * 64, row0, policy_evict_normal());
+      tma_load_2d(tmC, &sbar[k], stg + k * CHUNK_BYTES, n0 + k * 64, row0,
+                  (dbg & 16) ? policy_evict_first() : policy_evict_normal());
     }
   }
   if (!(dbg & 2)) wait_acc();
@@ -378,7 +383,12 @@ __device__ __forceinline__ void epilogue_dw_tma(const GemmArgs& a, const CUtenso
   fence_proxy_async_smem();
   named_bar_sync(1, 128);
   if (lead) {
-    for (int k = 0; k < nch; ++k) tma_store_2d(tmC, stg + k * CHUNK_BYTES, n0 + k * 64, row0);
+    if (dbg & 16) {
+      const uint64_t pol = policy_evict_first();
+      for (int k = 0; k < nch; ++k) tma_store_2d_hint(tmC, stg + k * CHUNK_BYTES, n0 + k * 64, row0, pol);
+    } else {
+      for (int k = 0; k < nch; ++k) tma_store_2d(tmC, stg + k * CHUNK_BYTES, n0 + k * 64, row0);
+    }
     bulk_commit();
   }
 }
@@ -480,8 +490,17 @@ constexpr int MAXP = 2;
 // Debug trace (slf_debug_trace_read): per-tile clock64 stamps of unit 0's leader CTA for one
 // selected launch.  Slots per tile: 0 MMA before tempty wait, 1 after it, 2 MMA tile issued,
 // 3 epilogue start, 4 accumulator ready, 5 TMEM released, 6 epilogue end, 7 problem index.
+// After the tile slots, per unit (leader CTA), when tracing: 0 MMA cycles waiting on full stages,
+// 1 MMA cycles waiting on a free accumulator, 2 first MMA-loop clock, 3 last, 4 K-blocks issued,
+// 5 producer cycles waiting on empty stages, 6 tiles, 7 globaltimer ns from first to last clock.
 constexpr int TRACE_TILES = 1024;
-__device__ unsigned long long g_trace[TRACE_TILES * 8];
+constexpr int TRACE_UNITS = 256;
+__device__ unsigned long long g_trace[TRACE_TILES * 8 + TRACE_UNITS * 8];
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
 __device__ __forceinline__ unsigned long long clk() {
   unsigned long long c;
   asm volatile("mov.u64 %0, %%clock64;" : "=l"(c));
@@ -505,7 +524,7 @@ struct GroupArgs {
   int nprob;
   int num_tiles;
   int dbg;  // timing-experiment knobs (0 in production): 1 = no L2 prefetch, 2 = late old-dW loads,
-            // 4 = record the per-tile trace of unit 0
+            // 4 = record the per-tile trace of unit 0, 8 = L2 prefetch of the next tile's MN-major A
   const int* sched;  // [units][sched_stride] tile ids, -1 terminated (nullptr: round robin)
   int sched_stride;
 };
@@ -602,6 +621,8 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
       // ===== TMA producer (both CTAs of a pair load their own halves) =====
       const uint64_t pol = policy_evict_normal();
       uint32_t stage = 0, phase = 0;
+      unsigned long long u_ew = 0;
+      const bool tu = (g.dbg & 4) && unit < TRACE_UNITS && rank == 0;
       TileIter it(g, unit, units);
       for (int tile = it.next(); tile >= 0; tile = it.next()) {
         const int pi = prob_of(g, tile);
@@ -615,8 +636,29 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
         const int b_row = n_blk * BN + (int)rank * C::B_ROWS;
         const int num_kb = (P.a.K + BK - 1) / BK;
         const bool a_mn = P.a_mn, b_mn = P.b_mn;
+        if (g.dbg & 8) {  // experiment: pull the next tile's MN-major A operand (all of K) into L2
+          const int nt = it.peek();
+          if (nt >= 0) {
+            const int npi = prob_of(g, nt);
+            const Prob& Q = g.p[npi];
+            if (Q.a_mn) {
+              int nm, nn;
+              tile_coords(nt - Q.tile_begin, Q.a, nm, nn);
+              const int nrow = nm * C::TILE_M + (int)rank * BM;
+              const int nkb = (Q.a.K + BK - 1) / BK;
+              for (int kb = 0; kb < nkb; ++kb) {
+                const CUtensorMap* m = &tm.m[MAPS_PER_PROB * npi];
+                int k = kb * BK;
+                if (k >= Q.a_split) { m = &tm.m[MAPS_PER_PROB * npi + 3]; k -= Q.a_split; }
+                for (int j = 0; j < BM / 64; ++j) tma_prefetch_l2_2d(m, nrow + j * 64, k);
+              }
+            }
+          }
+        }
         for (int kb = 0; kb < num_kb; ++kb) {
+          unsigned long long c0 = tu ? clk() : 0;
           mbar_wait(&empty[stage], phase ^ 1);
+          if (tu) u_ew += clk() - c0;
           uint8_t* a_dst = sA + stage * C::A_BYTES;
           uint8_t* b_dst = sB + stage * C::B_BYTES;
           // A's outer (row) coordinate: M for K-major A, K for MN-major A; rows >= a_split come
@@ -665,11 +707,13 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
           if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
         }
       }
+      if (tu) g_trace[TRACE_TILES * 8 + unit * 8 + 5] = u_ew;
     }
   } else if (warp == 1) {
     if (lane == 0 && rank == 0) {
       // ===== tcgen05.mma issuer (pair leader only) =====
       uint32_t stage = 0, phase = 0, local = 0;
+      unsigned long long u_fw = 0, u_tw = 0, u_kb = 0, u_first = 0, u_gt0 = 0;
       TileIter it(g, unit, units);
       for (int tile = it.next(); tile >= 0; tile = it.next(), ++local) {
         const Prob& P = g.p[prob_of(g, tile)];
@@ -678,14 +722,29 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
         const int num_kb = (P.a.K + BK - 1) / BK;
         const uint32_t acc = local & 1, acc_phase = (local >> 1) & 1;
         const bool tr = (g.dbg & 4) && blockIdx.x == 0 && local < TRACE_TILES;
+        const bool tu = (g.dbg & 4) && unit < TRACE_UNITS;
+        unsigned long long c0 = 0;
+        if (tu) {
+          c0 = clk();
+          if (local == 0) {
+            u_first = c0;
+            u_gt0 = gtimer();
+          }
+        }
         if (tr) g_trace[local * 8 + 0] = clk();
         mbar_wait(&tempty[acc], acc_phase ^ 1);
         tc_fence_after();
+        if (tu) u_tw += clk() - c0;
         if (tr) g_trace[local * 8 + 1] = clk();
         const uint32_t d_tmem = tmem_base + acc * BN;
         for (int kb = 0; kb < num_kb; ++kb) {
+          if (tu) c0 = clk();
           mbar_wait(&full[stage], phase);
           tc_fence_after();
+          if (tu) {
+            u_fw += clk() - c0;
+            ++u_kb;
+          }
           const uint32_t a_base = smem_u32(sA + stage * C::A_BYTES);
           const uint32_t b_base = smem_u32(sB + stage * C::B_BYTES);
 #pragma unroll
@@ -710,6 +769,16 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
         else
           mma_commit(&tfull[acc]);
         if (tr) g_trace[local * 8 + 2] = clk();
+      }
+      if ((g.dbg & 4) && unit < TRACE_UNITS) {
+        unsigned long long* u = g_trace + TRACE_TILES * 8 + unit * 8;
+        u[0] = u_fw;
+        u[1] = u_tw;
+        u[2] = u_first;
+        u[3] = clk();
+        u[4] = u_kb;
+        u[6] = local;
+        u[7] = gtimer() - u_gt0;
       }
     }
   } else if (warp >= 4) {

@@ -88,11 +88,24 @@ struct ProfScope {
   }
 };
 
+// Pinned host staging ring for the per-call tile tables: an H2D cudaMemcpyAsync from pageable
+// memory may synchronise with the stream (the GPU would idle while the host enqueues the next
+// call); from pinned memory it is asynchronous.  A slot is reused only after the event recorded
+// behind its copy has completed (in practice never waited on: 8 calls in flight).
+constexpr int RING_SLOTS = 8;
+struct PinnedRing {
+  uint8_t* buf = nullptr;
+  cudaEvent_t ev[RING_SLOTS] = {};
+  bool used[RING_SLOTS] = {};
+  int next = 0;
+};
+
 struct DevInfo {
   int sms = 0;
   int major = 0;
   int minor = 0;
   bool gemm_attr_set[64] = {};
+  PinnedRing ring;
 };
 
 std::mutex g_mu;
@@ -329,12 +342,21 @@ struct Plan {
   int64_t R = 0, Cv = 0, nR = 0, nC = 0;
   // schedule S: row chunk C (whole vocabulary stashed per chunk)
   int64_t C = 0, nCh = 0, ld_stash = 0;
+  size_t sched_bytes = 0;
   size_t off_sched = 0, off_rowstat = 0, off_shard = 0, off_zt = 0, off_union = 0, off_dxacc = 0;
   size_t off_loss = 0, off_cnt = 0, off_off = 0, off_hits = 0, off_idx = 0, off_part = 0, off_stash = 0;
   size_t fwd_bytes = 0, bwd_bytes = 0, total = 0;
 };
 
-constexpr size_t SCHED_ARENA_BYTES = 1024 * 1024;
+// LPT tile-table arena: up to 8 tables of a group launch, each <= 2 x (tiles + units) ints, with
+// tiles <= (ceil(N/128) + ceil(V/128)) * ceil(H/256); clamped to [64 KB, 1 MB] (a call needing more
+// uploads one table per launch instead, phase_s).
+constexpr size_t SCHED_ARENA_MAX = 1024 * 1024;
+size_t sched_arena_bytes(int64_t N, int64_t H, int64_t V) {
+  const double tiles = (double)((N + 127) / 128 + (V + 127) / 128) * (double)((H + 255) / 256);
+  const double b = 8.0 * (2.0 * tiles + 2.0 * 148) * 4.0;
+  return align_up((size_t)std::min<double>((double)SCHED_ARENA_MAX, std::max<double>(64.0 * 1024, b)), 1024);
+}
 
 size_t default_budget(int64_t N, int64_t V) {
   const size_t five = (size_t)(0.05 * (double)N * (double)V * 2.0);
@@ -347,7 +369,8 @@ bool plan_r(int64_t N, int64_t H, int64_t V, size_t budget, Plan* out) {
   Plan p;
   p.sched = SLF_SCHED_R;
   p.off_sched = WS_HEADER_BYTES;
-  p.off_rowstat = p.off_sched + SCHED_ARENA_BYTES;
+  p.sched_bytes = sched_arena_bytes(N, H, V);
+  p.off_rowstat = p.off_sched + p.sched_bytes;
   p.off_shard = align_up(p.off_rowstat + (size_t)N * 16, 1024);
   p.off_zt = align_up(p.off_shard + (size_t)N * 16, 1024);
   p.off_union = align_up(p.off_zt + (size_t)N * 4, 1024);
@@ -400,7 +423,8 @@ bool plan_s(int64_t N, int64_t H, int64_t V, size_t budget, Plan* out) {
   Plan p;
   p.sched = SLF_SCHED_S;
   p.off_sched = WS_HEADER_BYTES;
-  p.off_rowstat = p.off_sched + SCHED_ARENA_BYTES;
+  p.sched_bytes = sched_arena_bytes(N, H, V);
+  p.off_rowstat = p.off_sched + p.sched_bytes;
   p.off_zt = align_up(p.off_rowstat + (size_t)N * 16, 1024);
   p.off_loss = align_up(p.off_zt + (size_t)N * 4, 1024);
   p.off_cnt = align_up(p.off_loss + (size_t)N * 4, 1024);
@@ -465,10 +489,26 @@ struct SchedArena {
     host.insert(host.end(), t.begin(), t.end());
     return (int)tables.size() - 1;
   }
+  bool fits(const Ctx& c) const { return host.size() * 4 <= c.plan.sched_bytes; }
   slf_status upload(Ctx& c) {
     if (host.empty()) return SLF_OK;
-    if (host.size() * 4 > SCHED_ARENA_BYTES) return fail(SLF_ERR_WORKSPACE, "tile schedule arena overflow");
-    SLF_CUDA(cudaMemcpyAsync(c.ws + c.plan.off_sched, host.data(), host.size() * 4, cudaMemcpyHostToDevice, c.s));
+    if (!fits(c)) return fail(SLF_ERR_WORKSPACE, "tile schedule arena overflow");
+    const size_t bytes = host.size() * 4;
+    std::lock_guard<std::mutex> lk(g_mu);
+    PinnedRing& r = c.dev->ring;
+    if (!r.buf) {
+      SLF_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&r.buf), (size_t)RING_SLOTS * SCHED_ARENA_MAX,
+                             cudaHostAllocDefault));
+      for (int i = 0; i < RING_SLOTS; ++i) SLF_CUDA(cudaEventCreateWithFlags(&r.ev[i], cudaEventDisableTiming));
+    }
+    const int k = r.next;
+    r.next = (r.next + 1) % RING_SLOTS;
+    if (r.used[k]) SLF_CUDA(cudaEventSynchronize(r.ev[k]));
+    uint8_t* slot = r.buf + (size_t)k * SCHED_ARENA_MAX;
+    memcpy(slot, host.data(), bytes);
+    SLF_CUDA(cudaMemcpyAsync(c.ws + c.plan.off_sched, slot, bytes, cudaMemcpyHostToDevice, c.s));
+    SLF_CUDA(cudaEventRecord(r.ev[k], c.s));
+    r.used[k] = true;
     return SLF_OK;
   }
   const int* dev(Ctx& c, int k) const {
@@ -869,6 +909,7 @@ slf_status phase_s(Ctx& c, const void* X, const void* W, const int32_t* t, int64
   const SArgs a{X, W, t, N, H, V, 0, V, ignore_index};
   SLF_TRY(s_begin(c, a, dW != nullptr));
   static const bool no_ext = getenv("SLF_S_NO_EXT") != nullptr;
+  static const int64_t ext_gran = getenv("SLF_S_EXT_GRAN") ? atoi(getenv("SLF_S_EXT_GRAN")) : 128;
   std::vector<SChunk> chunks;
   for (int64_t r0 = 0, ci = 0; r0 < N; ++ci) {
     SChunk k{ci, r0, std::min(p.C, N - r0), 0, nullptr};
@@ -876,7 +917,7 @@ slf_status phase_s(Ctx& c, const void* X, const void* W, const int32_t* t, int64
       // ext rows E with E*ld_stash <= (N - r0 - C - E)*H, a multiple of 128, at most C (partials room)
       const int64_t free_rows = N - r0 - p.C;
       int64_t e = free_rows > 0 ? (free_rows * H) / (p.ld_stash + H) : 0;
-      e = std::min<int64_t>(e, p.C) / 128 * 128;
+      e = std::min<int64_t>(e, p.C) / ext_gran * ext_gran;
       if (e > 0) {
         k.ext = e;
         k.rows = p.C + e;
@@ -907,7 +948,10 @@ slf_status phase_s(Ctx& c, const void* X, const void* W, const int32_t* t, int64
       }
       tab[i] = found;
     }
-    SLF_TRY(arena.upload(c));
+    if (arena.fits(c))
+      SLF_TRY(arena.upload(c));
+    else
+      std::fill(tab.begin(), tab.end(), -1);  // too many shapes: each launch uploads its own table
   }
   float* loss_rows = s_loss_rows(c, reduction, loss_out);
   for (size_t i = 0; i < chunks.size(); ++i) {
@@ -1203,7 +1247,7 @@ slf_status slf_scale_bf16(void* p, int64_t n, float s, void* stream) {
 // ---- debug trace (SLF_DEBUG_TRACE) ------------------------------------------------------------------
 slf_status slf_debug_trace_read(uint64_t* host, int64_t n) {
   if (!host || n < 0) return fail(SLF_ERR_ARG, "bad arguments");
-  n = std::min<int64_t>(n, (int64_t)TRACE_TILES * 8);
+  n = std::min<int64_t>(n, (int64_t)(TRACE_TILES + TRACE_UNITS) * 8);
   SLF_CUDA(cudaDeviceSynchronize());
   SLF_CUDA(cudaMemcpyFromSymbol(host, g_trace, (size_t)n * 8));
   return SLF_OK;

@@ -20,6 +20,7 @@ def main():
     ap.add_argument("--schedule", default="S")
     ap.add_argument("--chunk", type=int, default=2)
     ap.add_argument("--config", default="llama8b")
+    ap.add_argument("--stats", action="store_true", help="trace the stash GEMM instead of the group")
     a = ap.parse_args()
     sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
     import synth
@@ -32,8 +33,19 @@ def main():
     desc = slf.plan_describe(N, H, V, schedule=a.schedule)
     kv = dict(x.split("=") for x in desc.split())
     assert kv["schedule"] == "S", "trace layout assumes schedule S (stash GEMM, group) per chunk"
-    launches_per_call = 2 * int(kv["n_chunks"])
-    target = launches_per_call + 2 * a.chunk + 1
+    # chunk list of the fused call (extended chunks: slf_lce.cu phase_s; SLF_S_NO_EXT disables)
+    C, ld = int(kv["row_chunk"]), (V + 7) // 8 * 8
+    nch, r0, chunk_rows = 0, 0, []
+    while r0 < N:
+        rows = min(C, N - r0)
+        if rows == C and not os.environ.get("SLF_S_NO_EXT"):
+            e = min(max(0, (N - r0 - C) * H // (ld + H)), C) // 128 * 128
+            rows += e
+        r0 += rows
+        nch += 1
+        chunk_rows.append(rows)
+    launches_per_call = 2 * nch
+    target = launches_per_call + 2 * a.chunk + (0 if a.stats else 1)
     os.environ["SLF_DEBUG_TRACE"] = str(target)  # read once, at the first launch
     inp = synth.make_inputs(N, H, V, seed=0)
     X = torch.from_numpy(inp.X.view(np.int16)).view(torch.bfloat16).cuda()
@@ -56,8 +68,12 @@ def main():
     epi_wait = tr[:, 4] - tr[:, 3]
     epi_to_release = tr[:, 5] - tr[:, 4]
     epi_total = tr[:, 6] - tr[:, 4]
+    rows = chunk_rows[a.chunk]
+    kblocks = {0: (H if a.stats else V) / 64, 1: rows / 64}
+    print(f"chunk rows {rows}; K-blocks per tile: {kblocks}")
     for p in sorted(set(tr[:, 7].tolist())):
         m = tr[:, 7] == p
+        print(f"problem {p}: MMA issue per K-block {np.median(mma_issue[m]) / kblocks[p]:.0f} cyc (ideal 512)")
         print(f"problem {p}: {m.sum()} tiles | MMA issue (tile) median {np.median(mma_issue[m]):.0f} cyc, "
               f"MMA wait for free TMEM median {np.median(mma_wait[m]):.0f} (total {mma_wait[m].sum()}) | "
               f"epilogue wait for acc median {np.median(epi_wait[m]):.0f}, acc->release median "
