@@ -346,7 +346,7 @@ __device__ __forceinline__ void epilogue_dw_tma(const GemmArgs& a, const CUtenso
   if (rmw && lead) {
     for (int k = 0; k < nch; ++k) {
       mbar_arrive_expect_tx(&sbar[k], CHUNK_BYTES);
-      tma_load_2d(tmC, &sbar[k], stg + k * CHUNK_BYTES, n0 + k * 64, row0,
+      tma_load_2d(tmC, &sbar[k], stg + k * CHUNK_BYTES, n0 + k * 64, (dbg & 32) ? (row0 & 1023) : row0,
                   (dbg & 16) ? policy_evict_first() : policy_evict_normal());
     }
   }
@@ -524,7 +524,8 @@ struct GroupArgs {
   int nprob;
   int num_tiles;
   int dbg;  // timing-experiment knobs (0 in production): 1 = no L2 prefetch, 2 = late old-dW loads,
-            // 4 = record the per-tile trace of unit 0, 8 = L2 prefetch of the next tile's MN-major A
+            // 4 = record the per-tile trace of unit 0, 8 = L2 prefetch of the next tile's MN-major A,
+            // 16 = evict-first dW RMW traffic, 32 = old-dW loads from the first 1024 rows (wrong dW)
   const int* sched;  // [units][sched_stride] tile ids, -1 terminated (nullptr: round robin)
   int sched_stride;
 };
@@ -828,8 +829,8 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
               tma_prefetch_l2_2d(&tm.m[MAPS_PER_PROB * npi + 2], qn * BN + k * 64, qm * C::TILE_M + (int)rank * BM);
           }
         }
-        epilogue_dw_tma(P.a, &tm.m[MAPS_PER_PROB * pi + 2], taddr, m_blk * C::TILE_M + (int)rank * BM, n_blk, ew * 32 + lane,
-                        stg, sbar, sphase, ew == 0 && lane == 0, wait_acc, release, g.dbg);
+        epilogue_dw_tma(P.a, &tm.m[MAPS_PER_PROB * pi + 2], taddr, m_blk * C::TILE_M + (int)rank * BM, n_blk,
+                        ew * 32 + lane, stg, sbar, sphase, ew == 0 && lane == 0, wait_acc, release, g.dbg);
       } else if (P.epi == EPI_STASH && P.a.tma_out) {  // a stash tensor map is provided
         const int row0 = m_blk * C::TILE_M + (int)rank * BM;  // output rows >= c_split go to map C2
         const bool seg2 = row0 >= P.c_split;

@@ -752,7 +752,7 @@ slf_status s_chunk_stats(Ctx& c, const SArgs& a, const SChunk& k, slf_shardstat*
   g.out = c.ws + p.off_stash;
   g.ld_out = p.ld_stash;
   static const int dbg = getenv("SLF_DEBUG_EPI") ? atoi(getenv("SLF_DEBUG_EPI")) : 0;
-  g.mode = dbg & 32;  // timing experiment only: skip the stash stores
+  g.mode = (dbg & 64) ? 32 : 0;  // timing experiment only (SLF_DEBUG_EPI=64): skip the stash stores
   g.tma_out = 1;      // the stash is written through TMA-staged stores
   SLF_TRY(tmap_kmajor(&ps.tc, c.ws + p.off_stash, a.V_l, main_rows, p.ld_stash, BM));
   if (k.ext) {
