@@ -167,6 +167,8 @@ def main():
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--budget", type=int, default=0, help="workspace budget bytes (0 = 5%% of N*V*2)")
     ap.add_argument("--schedule", default="auto", choices=["auto", "R", "S"])
+    ap.add_argument("--parallel", default="vocab", choices=["vocab", "dp"],
+                    help="N>1: vocab-sharded W (north star) or token-sharded data parallel (full W per GPU)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     args = ap.parse_args()
@@ -193,22 +195,29 @@ def main():
     c = synth.CONFIGS[args.config]
     N, H, V = c["N"], c["H"], c["V"]
     inp = synth.make_inputs(N, H, V, seed=args.seed, alpha=args.alpha, dist=args.dist)
-    v0, v1 = V * rank // g, V * (rank + 1) // g
+    dp = g > 1 and args.parallel == "dp"
+    v0, v1 = (0, V) if dp else (V * rank // g, V * (rank + 1) // g)
+    n0, n1 = (N * rank // g, N * (rank + 1) // g) if dp else (0, N)
     V_l = v1 - v0
-    X = torch.from_numpy(inp.X.view(np.int16)).view(torch.bfloat16).to(dev)
+    N_l = n1 - n0
+    X = torch.from_numpy(inp.X[n0:n1].view(np.int16)).view(torch.bfloat16).to(dev)
     W = torch.from_numpy(inp.W[v0:v1].view(np.int16)).view(torch.bfloat16).to(dev)
-    t = torch.from_numpy(inp.t).to(dev)
+    t = torch.from_numpy(inp.t[n0:n1]).to(dev)
+    n_valid_global = int((inp.t != -100).sum())  # known when the batch is built (DP mean denominator)
 
-    if g > 1 and args.budget == 0:
+    if g > 1 and args.budget == 0 and not dp:
         # Sharded runs: 5% of the GLOBAL N*V*2 logits per GPU (SURVEY q7 "lenient" reading; both
         # ratios are reported in "memory").
         args.budget = int(0.05 * N * V * 2)
-    ws = slf.alloc_workspace(N, H, V_l, dev, budget_bytes=args.budget)
+    ws = slf.alloc_workspace(N_l, H, V_l, dev, budget_bytes=args.budget)
     loss = torch.empty(1, dtype=torch.float32, device=dev)
-    dX = torch.empty(N, H, dtype=torch.bfloat16, device=dev)
+    dX = torch.empty(N_l, H, dtype=torch.bfloat16, device=dev)
     dW = torch.empty(V_l, H, dtype=torch.bfloat16, device=dev)
     extra = ws.numel()
-    if g > 1:
+    if dp:
+        from paper_2603_16428_b200.sharded import TokenShardedLCE
+        dpm = TokenShardedLCE(budget_bytes=args.budget, schedule=args.schedule)
+    elif g > 1:
         from paper_2603_16428_b200.sharded import VocabShardedLCE
         sharded = VocabShardedLCE(V, budget_bytes=args.budget, schedule="R" if args.schedule == "R" else "S")
         assert (sharded.v0, sharded.v1) == (v0, v1)
@@ -219,6 +228,10 @@ def main():
             slf.lce_fwd_bwd(Xs, W, ts, out=(loss, dX, dW), workspace=ws, budget_bytes=args.budget,
                             schedule=args.schedule)
             return loss
+        if dp:
+            l, _, _ = dpm.forward_backward(Xs, W, ts, n_valid_global=n_valid_global, workspace=ws,
+                                           out=(loss, dX, dW))
+            return l
         l, _, _ = sharded.forward_backward(Xs, W, ts, workspace=ws, dW_out=dW, dX_out=dX)
         return l
 
@@ -266,8 +279,8 @@ def main():
     # inputs (hidden states, targets), the fused call, and a D2H read of the loss.
     e2e = None
     if not args.no_e2e:
-        Xh = torch.from_numpy(inp.X.view(np.int16)).view(torch.bfloat16).pin_memory()
-        th = torch.from_numpy(inp.t).pin_memory()
+        Xh = torch.from_numpy(inp.X[n0:n1].view(np.int16)).view(torch.bfloat16).pin_memory()
+        th = torch.from_numpy(inp.t[n0:n1]).pin_memory()
         lh = torch.empty(1, dtype=torch.float32).pin_memory()
         Xd = torch.empty_like(X)
         td = torch.empty_like(t)
@@ -330,10 +343,12 @@ def main():
         "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
         "scaling": "strong" if g > 1 else "weak", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
         "config": {"workload": f"{args.config} LM head N={N} H={H} V={V}", "N": N, "H": H, "V": V,
-                   "V_per_gpu": V_l, "parallelism": f"vocab-sharded x{g}" if g > 1 else "single GPU",
+                   "V_per_gpu": V_l, "N_per_gpu": N_l,
+                   "parallelism": (f"token-sharded data parallel x{g}" if dp else f"vocab-sharded x{g}")
+                   if g > 1 else "single GPU",
                    "targets": args.dist, "logit_std": args.alpha, "ignore_frac": 0.05,
                    "l2": "inputs larger than L2 (W alone is %.2f GB vs 126 MB L2); no flush" % (V_l * H * 2 / 1e9),
-                   "plan": slf.plan_describe(N, H, V_l, budget_bytes=args.budget,
+                   "plan": slf.plan_describe(N_l, H, V_l, budget_bytes=args.budget,
                                              schedule=args.schedule)},
         "tflops": tflops, "frac_of_peak_burst": tflops / peaks["burst"],
         "frac_of_peak_sustained": tflops / peaks["sustained"],
@@ -343,8 +358,8 @@ def main():
                      "frac_of_burst": achieved / peaks["burst"]},
         "kernels": kernels,
         "gpu_launches": launches,
-        "memory": {"extra_device_bytes": int(extra), "logits_bytes_per_gpu": N * V_l * 2,
-                   "frac_of_logits_per_gpu": extra / (N * V_l * 2), "frac_of_global_logits": extra / (N * V * 2)},
+        "memory": {"extra_device_bytes": int(extra), "logits_bytes_per_gpu": N_l * V_l * 2,
+                   "frac_of_logits_per_gpu": extra / (N_l * V_l * 2), "frac_of_global_logits": extra / (N * V * 2)},
         "clocks": clocks.summary(),
         "e2e": e2e,
     }

@@ -353,6 +353,33 @@ def test_vocab_sharded_module_world1(slf, sched):
         dist.destroy_process_group()
 
 
+@pytest.mark.gpu
+@pytest.mark.parametrize("red", ["mean", "sum"])
+def test_token_sharded_module_world1(slf, red):
+    """TokenShardedLCE (data-parallel mode) with real NCCL at world size 1:
+    the fused call under SUM with the global-mean scale, loss and dW all-reduces."""
+    import os
+    import torch.distributed as dist
+    from paper_2603_16428_b200.sharded import TokenShardedLCE
+    if not dist.is_initialized():
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        os.environ["MASTER_PORT"] = "29541"
+        dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
+    try:
+        inp = synth.make_inputs(700, 256, 3000, seed=21, alpha=4.0, dist="zipf")
+        X, W, t = to_dev(inp, torch)
+        m = TokenShardedLCE(budget_bytes=3 << 20)
+        loss, dX, dW = m.forward_backward(X, W, t, reduction=red, scale=0.5)
+        torch.cuda.synchronize()
+        Xo, Wo, to = oracle_inputs(inp)
+        ref = oracle.lce(Xo, Wo, to, reduction=red, scale=0.5)
+        assert_loss_close(float(loss), ref["loss"], red)
+        assert rel_max_err(bf16_to_np64(dX), ref["dX"]) <= GRAD_TOL
+        assert rel_max_err(bf16_to_np64(dW), ref["dW"]) <= GRAD_TOL
+    finally:
+        dist.destroy_process_group()
+
+
 # ---- final RMSNorm + LCE (SURVEY §8(f) NEXT-1) ---------------------------------------------------
 @pytest.mark.parametrize("sched", SCHEDS)
 @pytest.mark.parametrize("N,H,V", [(300, 256, 3000), (1000, 520, 4100)])
