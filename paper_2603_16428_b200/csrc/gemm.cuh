@@ -31,24 +31,24 @@ constexpr int BM = 128;  // accumulator rows per CTA (TMEM lanes)
 constexpr int BN = 256;  // accumulator columns (one tcgen05.mma N)
 constexpr int BK = 64;   // one 128-byte swizzle row of bf16
 constexpr int GEMM_THREADS = 256;
+
 constexpr uint32_t TMEM_COLS = 512;  // 2 x 256-column fp32 accumulators
 
 // CG = 1: one CTA computes a 128 x 256 tile (cta_group::1).  CG = 2: a CTA pair (cluster of 2)
 // computes a 256 x 256 tile with cta_group::2 — each CTA stages its own 128 rows of A and half
 // (128 rows) of B, the leader issues the MMA, both CTAs hold 128 accumulator rows in TMEM.
-template <int CG>
+// NB = number of 16 KB epilogue staging buffers.  CTA pairs: NB = 2 leaves room for a 6-stage
+// operand ring (faster mainloop; the stash and dX launches), NB = 4 for 5 stages (the dW
+// read-modify-write epilogue keeps all four old-value chunks in flight).  Both fit 227 KB.
+template <int CG, int NB>
 struct Cfg {
   static constexpr int TILE_M = BM * CG;
   static constexpr int B_ROWS = BN / CG;  // rows of B (N extent) staged per CTA
   static constexpr int A_BYTES = BM * BK * 2;
   static constexpr int B_BYTES = B_ROWS * BK * 2;
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
-#ifndef SLF_EXP_STAGES  // timing experiments only (tools/): other ring depths / staging sizes
-#define SLF_EXP_STAGES 5
-#define SLF_EXP_STAGING_CHUNKS 4
-#endif
-  static constexpr int STAGES = CG == 2 ? SLF_EXP_STAGES : 3;
-  static constexpr int STAGING_BYTES = SLF_EXP_STAGING_CHUNKS * BM * 64 * 2;  // [128 rows x 64 bf16] TMA buffers
+  static constexpr int STAGES = CG == 2 ? (NB <= 2 ? 6 : 5) : 3;
+  static constexpr int STAGING_BYTES = NB * BM * 64 * 2;  // [128 rows x 64 bf16] TMA buffers
   static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + STAGING_BYTES + 1024 /*align slack*/ + 256 /*barriers*/;
 };
 
@@ -329,67 +329,72 @@ __device__ __forceinline__ void epilogue_tile(const GemmArgs& a, uint32_t taddr,
 // accumulator from TMEM, writes bf16 back to smem, and four TMA stores write the tile out.
 // Thread-per-row global accesses would touch 32 cache lines per warp instruction; this keeps the
 // short-K dW GEMMs of schedule S tensor-bound instead of epilogue-bound.
-template <typename WaitAcc, typename ReleaseTmem>
+template <int NB, typename WaitAcc, typename ReleaseTmem>
 __device__ __forceinline__ void epilogue_dw_tma(const GemmArgs& a, const CUtensorMap* tmC, uint32_t taddr, int row0,
                                                 int n_blk, int rl, uint8_t* stg, uint64_t* sbar, uint32_t& sphase,
                                                 bool lead, WaitAcc wait_acc, ReleaseTmem release_tmem,
                                                 int dbg = 0) {
   constexpr uint32_t CHUNK_BYTES = BM * 64 * 2;
+  // chunks are processed NB at a time through the NB staging buffers
   const int n0 = n_blk * BN;
   const int nch = min(BN, a.N - n0 + 63) / 64;  // 64-column chunks with at least one valid column
   const bool rmw = a.mode == 1;
   const uint32_t sbase = smem_u32(stg);
-  // The previous tile's stores must have finished reading the buffers.
-  if (lead) bulk_wait_read<0>();
-  named_bar_sync(1, 128);
-  if (dbg & 2) wait_acc();
-  if (rmw && lead) {
-    for (int k = 0; k < nch; ++k) {
-      mbar_arrive_expect_tx(&sbar[k], CHUNK_BYTES);
-      tma_load_2d(tmC, &sbar[k], stg + k * CHUNK_BYTES, n0 + k * 64, (dbg & 32) ? (row0 & 1023) : row0,
-                  (dbg & 16) ? policy_evict_first() : policy_evict_normal());
-    }
-  }
-  if (!(dbg & 2)) wait_acc();
   uint32_t v0[32], v1[32];
-  for (int k = 0; k < nch; ++k) {
-    tmem_ld32(taddr + k * 64, v0);
-    tmem_ld32(taddr + k * 64 + 32, v1);
-    tmem_ld_wait();
-    if (k == nch - 1) release_tmem();  // the accumulator is in registers: let the next MMA start
-    if (rmw) {
-      mbar_wait(&sbar[k], (sphase >> k) & 1);
-      sphase ^= 1u << k;
-    }
-    const uint32_t rowaddr = sbase + k * CHUNK_BYTES + rl * 128;
-#pragma unroll
-    for (int gi = 0; gi < 8; ++gi) {
-      const uint32_t addr = rowaddr + ((gi ^ (rl & 7)) << 4);  // 128B swizzle: granule gi of row rl
-      const uint32_t* src = gi < 4 ? &v0[gi * 8] : &v1[(gi - 4) * 8];
-      float f[8];
-#pragma unroll
-      for (int e = 0; e < 8; ++e) f[e] = __uint_as_float(src[e]);
-      if (rmw) {
-        const uint4 o = lds128(addr);
-        f[0] += bf16lo_to_f32(o.x); f[1] += bf16hi_to_f32(o.x);
-        f[2] += bf16lo_to_f32(o.y); f[3] += bf16hi_to_f32(o.y);
-        f[4] += bf16lo_to_f32(o.z); f[5] += bf16hi_to_f32(o.z);
-        f[6] += bf16lo_to_f32(o.w); f[7] += bf16hi_to_f32(o.w);
+  for (int g0 = 0; g0 < nch; g0 += NB) {
+    const int gn = min(NB, nch - g0);
+    // The previous stores (of the last tile, or of the previous group) must have read the buffers.
+    if (lead) bulk_wait_read<0>();
+    named_bar_sync(1, 128);
+    if (g0 == 0 && (dbg & 2)) wait_acc();
+    if (rmw && lead) {
+      for (int j = 0; j < gn; ++j) {
+        mbar_arrive_expect_tx(&sbar[j], CHUNK_BYTES);
+        tma_load_2d(tmC, &sbar[j], stg + j * CHUNK_BYTES, n0 + (g0 + j) * 64, (dbg & 32) ? (row0 & 1023) : row0,
+                    (dbg & 16) ? policy_evict_first() : policy_evict_normal());
       }
-      sts128(addr, make_uint4(pack_bf16x2(f[0], f[1]), pack_bf16x2(f[2], f[3]), pack_bf16x2(f[4], f[5]),
-                              pack_bf16x2(f[6], f[7])));
     }
-  }
-  fence_proxy_async_smem();
-  named_bar_sync(1, 128);
-  if (lead) {
-    if (dbg & 16) {
-      const uint64_t pol = policy_evict_first();
-      for (int k = 0; k < nch; ++k) tma_store_2d_hint(tmC, stg + k * CHUNK_BYTES, n0 + k * 64, row0, pol);
-    } else {
-      for (int k = 0; k < nch; ++k) tma_store_2d(tmC, stg + k * CHUNK_BYTES, n0 + k * 64, row0);
+    if (g0 == 0 && !(dbg & 2)) wait_acc();
+    for (int j = 0; j < gn; ++j) {
+      const int k = g0 + j;
+      tmem_ld32(taddr + k * 64, v0);
+      tmem_ld32(taddr + k * 64 + 32, v1);
+      tmem_ld_wait();
+      if (k == nch - 1) release_tmem();  // the accumulator is in registers: let the next MMA start
+      if (rmw) {
+        mbar_wait(&sbar[j], (sphase >> j) & 1);
+        sphase ^= 1u << j;
+      }
+      const uint32_t rowaddr = sbase + j * CHUNK_BYTES + rl * 128;
+#pragma unroll
+      for (int gi = 0; gi < 8; ++gi) {
+        const uint32_t addr = rowaddr + ((gi ^ (rl & 7)) << 4);  // 128B swizzle: granule gi of row rl
+        const uint32_t* src = gi < 4 ? &v0[gi * 8] : &v1[(gi - 4) * 8];
+        float f[8];
+#pragma unroll
+        for (int e = 0; e < 8; ++e) f[e] = __uint_as_float(src[e]);
+        if (rmw) {
+          const uint4 o = lds128(addr);
+          f[0] += bf16lo_to_f32(o.x); f[1] += bf16hi_to_f32(o.x);
+          f[2] += bf16lo_to_f32(o.y); f[3] += bf16hi_to_f32(o.y);
+          f[4] += bf16lo_to_f32(o.z); f[5] += bf16hi_to_f32(o.z);
+          f[6] += bf16lo_to_f32(o.w); f[7] += bf16hi_to_f32(o.w);
+        }
+        sts128(addr, make_uint4(pack_bf16x2(f[0], f[1]), pack_bf16x2(f[2], f[3]), pack_bf16x2(f[4], f[5]),
+                                pack_bf16x2(f[6], f[7])));
+      }
     }
-    bulk_commit();
+    fence_proxy_async_smem();
+    named_bar_sync(1, 128);
+    if (lead) {
+      if (dbg & 16) {
+        const uint64_t pol = policy_evict_first();
+        for (int j = 0; j < gn; ++j) tma_store_2d_hint(tmC, stg + j * CHUNK_BYTES, n0 + (g0 + j) * 64, row0, pol);
+      } else {
+        for (int j = 0; j < gn; ++j) tma_store_2d(tmC, stg + j * CHUNK_BYTES, n0 + (g0 + j) * 64, row0);
+      }
+      bulk_commit();
+    }
   }
 }
 
@@ -397,7 +402,7 @@ __device__ __forceinline__ void epilogue_dw_tma(const GemmArgs& a, const CUtenso
 // and sum exp(z - m_t) (as EPI_STATS), the target-logit gather, and the bf16 stash
 // p~ = exp(z - m_t) written through four swizzled 16 KB smem chunks and TMA stores (coalesced),
 // instead of thread-per-row 16-byte stores that touch 32 cache lines per warp instruction.
-template <typename WaitAcc, typename ReleaseTmem>
+template <int NB, typename WaitAcc, typename ReleaseTmem>
 __device__ __forceinline__ void epilogue_stash_tma(const GemmArgs& a, const CUtensorMap* tmC, uint32_t taddr,
                                                    int row0, int n_blk, int rl, uint8_t* stg, bool lead,
                                                    WaitAcc wait_acc, ReleaseTmem release_tmem, int c_off = 0) {
@@ -429,9 +434,22 @@ __device__ __forceinline__ void epilogue_stash_tma(const GemmArgs& a, const CUte
   }
   const float mb = mx * LOG2E;
   float s = 0.f, zt = 0.f;
+  // 64-column chunks are staged NB at a time
 #pragma unroll 1
   for (int c = 0; c < BN / 32; ++c) {
     if (c * 32 >= ncols) break;
+    if (c > 0 && (c % (2 * NB)) == 0) {  // staging full: store this group, wait until it is read
+      fence_proxy_async_smem();
+      named_bar_sync(1, 128);
+      if (lead) {
+        if (!(a.mode & 32))
+          for (int k = c / 2 - NB; k < c / 2; ++k)
+            tma_store_2d(tmC, stg + (k % NB) * CHUNK_BYTES, n0 + k * 64, row0 - c_off);
+        bulk_commit();
+        bulk_wait_read<0>();
+      }
+      named_bar_sync(1, 128);
+    }
     tmem_ld32(taddr + c * 32, v);
     tmem_ld_wait();
     uint32_t p[16];
@@ -446,7 +464,7 @@ __device__ __forceinline__ void epilogue_stash_tma(const GemmArgs& a, const CUte
       zt = (c * 32 + i + 1 == tl) ? z1 : zt;
       p[i / 2] = pack_bf16x2(e0, e1);
     }
-    const uint32_t rowaddr = sbase + (c >> 1) * CHUNK_BYTES + rl * 128;
+    const uint32_t rowaddr = sbase + ((c >> 1) % NB) * CHUNK_BYTES + rl * 128;
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
       const int gi = (c & 1) * 4 + q;
@@ -463,7 +481,8 @@ __device__ __forceinline__ void epilogue_stash_tma(const GemmArgs& a, const CUte
   if (lead) {
     const int nch = (ncols + 63) / 64;
     if (!(a.mode & 32))  // mode bit 32: skip the stash stores (timing experiment only)
-      for (int k = 0; k < nch; ++k) tma_store_2d(tmC, stg + k * CHUNK_BYTES, n0 + k * 64, row0 - c_off);
+      for (int k = (nch - 1) / NB * NB; k < nch; ++k)
+        tma_store_2d(tmC, stg + (k % NB) * CHUNK_BYTES, n0 + k * 64, row0 - c_off);
     bulk_commit();
   }
 }
@@ -556,15 +575,15 @@ __device__ __forceinline__ int prob_of(const GroupArgs& g, int tile) {
   return (g.nprob > 1 && tile >= g.p[1].tile_begin) ? 1 : 0;
 }
 
-template <int CG>
+template <int CG, int NB>
 __global__ void __launch_bounds__(GEMM_THREADS, 1)
     lce_group_kernel(const __grid_constant__ TMaps tm, const __grid_constant__ GroupArgs g) {
-  using C = Cfg<CG>;
+  using C = Cfg<CG, NB>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sA = smem;
   uint8_t* sB = smem + C::STAGES * C::A_BYTES;
-  uint8_t* stg = smem + C::STAGES * C::STAGE_BYTES;  // 2 x 16 KB epilogue staging (1024-aligned)
+  uint8_t* stg = smem + C::STAGES * C::STAGE_BYTES;  // NB x 16 KB epilogue staging (1024-aligned)
   uint64_t* full = reinterpret_cast<uint64_t*>(stg + C::STAGING_BYTES);
   uint64_t* empty = full + C::STAGES;
   uint64_t* tfull = empty + C::STAGES;
@@ -829,12 +848,12 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
               tma_prefetch_l2_2d(&tm.m[MAPS_PER_PROB * npi + 2], qn * BN + k * 64, qm * C::TILE_M + (int)rank * BM);
           }
         }
-        epilogue_dw_tma(P.a, &tm.m[MAPS_PER_PROB * pi + 2], taddr, m_blk * C::TILE_M + (int)rank * BM, n_blk,
+        epilogue_dw_tma<NB>(P.a, &tm.m[MAPS_PER_PROB * pi + 2], taddr, m_blk * C::TILE_M + (int)rank * BM, n_blk,
                         ew * 32 + lane, stg, sbar, sphase, ew == 0 && lane == 0, wait_acc, release, g.dbg);
       } else if (P.epi == EPI_STASH && P.a.tma_out) {  // a stash tensor map is provided
         const int row0 = m_blk * C::TILE_M + (int)rank * BM;  // output rows >= c_split go to map C2
         const bool seg2 = row0 >= P.c_split;
-        epilogue_stash_tma(P.a, &tm.m[MAPS_PER_PROB * pi + (seg2 ? 4 : 2)], taddr, row0, n_blk, ew * 32 + lane,
+        epilogue_stash_tma<NB>(P.a, &tm.m[MAPS_PER_PROB * pi + (seg2 ? 4 : 2)], taddr, row0, n_blk, ew * 32 + lane,
                            stg, ew == 0 && lane == 0, wait_acc, release, seg2 ? P.c_split : 0);
       } else {
         wait_acc();

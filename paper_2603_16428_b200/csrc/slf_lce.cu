@@ -249,16 +249,16 @@ std::vector<int> lpt_table(const ProbSpec* ps, int n, int units, int* stride) {
   return tab;
 }
 
-template <int CG>
-slf_status launch_group_cg(DevInfo* dev, ProbSpec* ps, int n, cudaStream_t s, const int* sched, int sched_stride,
-                           int prof_kind) {
-  using C = Cfg<CG>;
-  auto kfn = lce_group_kernel<CG>;
+template <int CG, int NB>
+slf_status launch_group_cfg(DevInfo* dev, ProbSpec* ps, int n, cudaStream_t s, const int* sched, int sched_stride,
+                            int prof_kind) {
+  using C = Cfg<CG, NB>;
+  auto kfn = lce_group_kernel<CG, NB>;
   {
     std::lock_guard<std::mutex> lk(g_mu);
-    if (!dev->gemm_attr_set[CG]) {
+    if (!dev->gemm_attr_set[CG * 8 + NB]) {
       SLF_CUDA(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM_BYTES));
-      dev->gemm_attr_set[CG] = true;
+      dev->gemm_attr_set[CG * 8 + NB] = true;
     }
   }
   TMaps tm;
@@ -315,10 +315,20 @@ slf_status launch_group_cg(DevInfo* dev, ProbSpec* ps, int n, cudaStream_t s, co
   return SLF_OK;
 }
 
+// Launch configuration: a launch with a dW read-modify-write problem keeps four epilogue staging
+// buffers (5-stage ring); every other launch takes the 6-stage ring (SLF_STAGING=2|4 forces one,
+// timing experiments only).
 slf_status launch_group(DevInfo* dev, ProbSpec* ps, int n, cudaStream_t s, const int* sched = nullptr,
                         int sched_stride = 0, int prof_kind = -1) {
-  if (cta_group() == 2) return launch_group_cg<2>(dev, ps, n, s, sched, sched_stride, prof_kind);
-  return launch_group_cg<1>(dev, ps, n, s, sched, sched_stride, prof_kind);
+  bool dw = false;
+  for (int p = 0; p < n; ++p) dw = dw || ps[p].epi == EPI_DW;
+  static const int force = getenv("SLF_STAGING") ? atoi(getenv("SLF_STAGING")) : 0;
+  const bool four = force ? force == 4 : dw;
+  if (cta_group() == 2)
+    return four ? launch_group_cfg<2, 4>(dev, ps, n, s, sched, sched_stride, prof_kind)
+                : launch_group_cfg<2, 2>(dev, ps, n, s, sched, sched_stride, prof_kind);
+  return four ? launch_group_cfg<1, 4>(dev, ps, n, s, sched, sched_stride, prof_kind)
+              : launch_group_cfg<1, 2>(dev, ps, n, s, sched, sched_stride, prof_kind);
 }
 
 template <int EPI, bool A_MN, bool B_MN>
@@ -1211,13 +1221,13 @@ slf_status slf_debug_max_active_clusters(int cluster, int* out) {
   if (!out || cluster < 1 || cluster > 16) return fail(SLF_ERR_ARG, "bad arguments");
   DevInfo* dev;
   SLF_TRY(device_info(&dev));
-  auto kfn = lce_group_kernel<2>;
-  SLF_CUDA(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg<2>::SMEM_BYTES));
+  auto kfn = lce_group_kernel<2, 4>;
+  SLF_CUDA(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg<2, 4>::SMEM_BYTES));
   if (cluster > 8) SLF_CUDA(cudaFuncSetAttribute(kfn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((unsigned)(dev->sms / cluster * cluster));
   cfg.blockDim = dim3(GEMM_THREADS);
-  cfg.dynamicSmemBytes = Cfg<2>::SMEM_BYTES;
+  cfg.dynamicSmemBytes = Cfg<2, 4>::SMEM_BYTES;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeClusterDimension;
   attr[0].val.clusterDim.x = cluster;

@@ -12,6 +12,10 @@ import torch
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import synth  # noqa: E402
 import paper_2603_16428_b200 as slf  # noqa: E402
+import paper_2603_16428_b200._lib as _L  # noqa: E402
+
+if os.environ.get("SLF_SO"):  # experiment builds (tools/exp)
+    _L.SO_PATH = os.environ["SLF_SO"]
 
 
 def main():
