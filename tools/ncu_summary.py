@@ -38,6 +38,11 @@ def kind_of(name: str) -> str:
     if "lce_gemm_kernel<" in name:
         return KIND.get(name.split("<")[1].split(",")[0].strip(), "gemm?")
     if "lce_group_kernel<" in name:
+        # <CG, NB>: NB = 4 staging buffers only for launches with a dW read-modify-write (the
+        # schedule-S dW+dX group); NB = 2 for the stash / statistics GEMMs (slf_lce.cu launch_group)
+        args = [x.strip() for x in name.split("<")[1].split(">")[0].split(",")]
+        if len(args) >= 2:
+            return "gemm_group" if args[1] == "4" else "gemm_stats"
         return "gemm (group kernel)"
     return name.split("(")[0].replace("void ", "").strip()
 
