@@ -919,12 +919,13 @@ slf_status phase_s(Ctx& c, const void* X, const void* W, const int32_t* t, int64
   const SArgs a{X, W, t, N, H, V, 0, V, ignore_index};
   SLF_TRY(s_begin(c, a, dW != nullptr));
   static const bool no_ext = getenv("SLF_S_NO_EXT") != nullptr;
-  static const int64_t ext_gran = getenv("SLF_S_EXT_GRAN") ? atoi(getenv("SLF_S_EXT_GRAN")) : 128;
+  static const int64_t ext_gran = getenv("SLF_S_EXT_GRAN") ? atoi(getenv("SLF_S_EXT_GRAN")) : 256;
   std::vector<SChunk> chunks;
   for (int64_t r0 = 0, ci = 0; r0 < N; ++ci) {
     SChunk k{ci, r0, std::min(p.C, N - r0), 0, nullptr};
     if (dX && !no_ext && k.rows == p.C) {
-      // ext rows E with E*ld_stash <= (N - r0 - C - E)*H, a multiple of 128, at most C (partials room)
+      // ext rows E with E*ld_stash <= (N - r0 - C - E)*H, a multiple of 256 (no half-empty CTA-pair
+      // row tiles; measured 2 % faster than 128 despite one more chunk), at most C (partials room)
       const int64_t free_rows = N - r0 - p.C;
       int64_t e = free_rows > 0 ? (free_rows * H) / (p.ld_stash + H) : 0;
       e = std::min<int64_t>(e, p.C) / ext_gran * ext_gran;

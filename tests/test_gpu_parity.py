@@ -104,7 +104,7 @@ def test_multichunk_ragged_parity_s(slf, reduction):
 @pytest.mark.parametrize("reduction", ["mean", "none"])
 def test_extended_chunks_parity_s(slf, reduction):
     """Schedule S with chunks extended into dhidden's unwritten rows: H/V large enough
-    that ext rows fit (C = 256, chunks of 512 and 384 rows), ragged tail, Zipf targets; also dX only."""
+    that ext rows fit (C = 256, chunks of 512 and 256 rows), ragged tail, Zipf targets; also dX only."""
     inp = synth.make_inputs(2000, 512, 1536, seed=16, alpha=4.0, dist="zipf")
     budget = 3 << 19
     desc = slf.plan_describe(2000, 512, 1536, budget_bytes=budget, schedule="S")

@@ -39,7 +39,7 @@ def main():
     while r0 < N:
         rows = min(C, N - r0)
         if rows == C and not os.environ.get("SLF_S_NO_EXT"):
-            e = min(max(0, (N - r0 - C) * H // (ld + H)), C) // 128 * 128
+            e = min(max(0, (N - r0 - C) * H // (ld + H)), C) // 256 * 256
             rows += e
         r0 += rows
         nch += 1

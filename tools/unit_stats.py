@@ -17,7 +17,7 @@ def chunk_list(N, H, V, C):
     while r0 < N:
         rows = min(C, N - r0)
         if rows == C and not os.environ.get("SLF_S_NO_EXT"):
-            rows += min(max(0, (N - r0 - C) * H // (ld + H)), C) // 128 * 128
+            rows += min(max(0, (N - r0 - C) * H // (ld + H)), C) // 256 * 256
         out.append(rows)
         r0 += rows
     return out
