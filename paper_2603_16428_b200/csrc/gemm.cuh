@@ -387,7 +387,9 @@ __device__ __forceinline__ void epilogue_dw_tma(const GemmArgs& a, const CUtenso
     fence_proxy_async_smem();
     named_bar_sync(1, 128);
     if (lead) {
-      if (dbg & 16) {
+      if (a.mode == 2) {  // accumulate in L2: bf16 reduce-add of this tile's partial
+        for (int j = 0; j < gn; ++j) tma_reduce_add_2d(tmC, stg + j * CHUNK_BYTES, n0 + (g0 + j) * 64, row0);
+      } else if (dbg & 16) {
         const uint64_t pol = policy_evict_first();
         for (int j = 0; j < gn; ++j) tma_store_2d_hint(tmC, stg + j * CHUNK_BYTES, n0 + (g0 + j) * 64, row0, pol);
       } else {

@@ -315,13 +315,24 @@ slf_status launch_group_cfg(DevInfo* dev, ProbSpec* ps, int n, cudaStream_t s, c
   return SLF_OK;
 }
 
+// How a dW partial is accumulated into the previous one.  2 (default): the epilogue rounds its
+// fp32 partial to bf16 and a TMA reduce-add store has the L2 add it to dW (cp.reduce.async.bulk
+// .tensor .add, bf16) — nothing is loaded through the SM, so the short-K dW tiles stay fed and
+// the launch keeps the 6-stage ring.  1: the epilogue loads the old bf16 tile by TMA, adds in fp32
+// and stores (one rounding instead of two; measured max error identical, but
+// ~2.5 ms per Llama-8B step slower).  SLF_DW_ACC=1 selects it.
+int dw_acc_mode() {
+  static const int m = getenv("SLF_DW_ACC") ? atoi(getenv("SLF_DW_ACC")) : 2;
+  return m == 1 ? 1 : 2;
+}
+
 // Launch configuration: a launch with a dW read-modify-write problem keeps four epilogue staging
 // buffers (5-stage ring); every other launch takes the 6-stage ring (SLF_STAGING=2|4 forces one,
 // timing experiments only).
 slf_status launch_group(DevInfo* dev, ProbSpec* ps, int n, cudaStream_t s, const int* sched = nullptr,
                         int sched_stride = 0, int prof_kind = -1) {
   bool dw = false;
-  for (int p = 0; p < n; ++p) dw = dw || ps[p].epi == EPI_DW;
+  for (int p = 0; p < n; ++p) dw = dw || (ps[p].epi == EPI_DW && ps[p].a.mode == 1);
   static const int force = getenv("SLF_STAGING") ? atoi(getenv("SLF_STAGING")) : 0;
   const bool four = force ? force == 4 : dw;
   if (cta_group() == 2)
@@ -602,7 +613,7 @@ slf_status phase_backward(Ctx& c, const void* X, const void* W, const slf_rowsta
       q.a.K = (int)rows;
       q.a.out = reinterpret_cast<uint8_t*>(dW) + (size_t)c0 * H * 2;
       q.a.ld_out = H;
-      q.a.mode = (rb > 0 || c.acc_dw) ? 1 : 0;
+      q.a.mode = (rb > 0 || c.acc_dw) ? dw_acc_mode() : 0;
       SLF_TRY(tmap_kmajor(&q.tc, q.a.out, H, wc, H, BM));
       finish_geometry(q.a, cg);
     }
@@ -831,7 +842,7 @@ slf_status s_build_bwd(Ctx& c, const SArgs& a, const SChunk& k, void* dXc, int d
     q.a.K = (int)rows;
     q.a.out = dW;
     q.a.ld_out = a.H;
-    q.a.mode = (k.index > 0 || c.acc_dw) ? 1 : 0;
+    q.a.mode = (k.index > 0 || c.acc_dw) ? dw_acc_mode() : 0;
     static const bool no_rmw = getenv("SLF_DEBUG_DW_NO_RMW") != nullptr;  // timing experiments only (wrong dW)
     if (no_rmw) q.a.mode = 0;
     SLF_TRY(tmap_kmajor(&q.tc, dW, a.H, a.V_l, a.H, BM));

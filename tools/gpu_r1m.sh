@@ -1,3 +1,4 @@
 mkdir -p gpurun_out
 export PYTHONUNBUFFERED=1
-timeout 900 python -m pytest tests/test_gpu_parity.py -q -m "gpu and not slow" -x 2>&1 | grep -v "^\s*$" | tail -2
+timeout 1500 python -m pytest tests/test_gpu_parity.py -q -m "gpu" -x 2>&1 | grep -v "^\s*$" | tail -4
+timeout 600 python tools/dw_acc_error.py
