@@ -77,20 +77,53 @@ __global__ void __launch_bounds__(256) combine_transform_kernel(
     const WsHeader* __restrict__ hdr, float* __restrict__ loss_rows, slf_rowstat* __restrict__ rowstat,
     uint16_t* __restrict__ stash, uint16_t* __restrict__ stash2, int split) {
   // rows [0, split) of the chunk's stash are in `stash`, rows [split, rows) in `stash2` (same stride)
-  extern __shared__ float r_t[];  // [tiles]
+  extern __shared__ float r_t[];  // [tiles]: first the tile maxima m_t, then the factors r_t
   griddep_launch_dependents();
   griddep_wait();  // PDL: everything below reads the previous kernel's outputs
-  __shared__ float sM, sLse, red[256];
+  __shared__ float sM, sLse, wm[8], ws[8];
   const int i = blockIdx.x;
   const int tid = threadIdx.x;
-  float2 local = make_float2(0.f, 0.f);
-  if (st == nullptr) local = merge_row_tiles(partials, tiles, rows, i, red);  // one GPU: own tiles only
+  uint4* row = reinterpret_cast<uint4*>(i < split ? stash + (size_t)i * ld_stash : stash2 + (size_t)(i - split) * ld_stash);
+  const int64_t groups = (V_l + 7) / 8;
+  constexpr int U = 8;  // 8 independent 16-byte loads in flight per thread (4: 1.94 ms, 16: no gain)
+  // The first batch of the row is requested before the statistics are merged (latency overlap).
+  uint4 w[U];
+#pragma unroll
+  for (int u = 0; u < U; ++u)
+    if (tid + u * 256 < groups) w[u] = row[tid + u * 256];
+  // One pass over this shard's tile partials: keep m_t in smem, merge (m, s) online per thread,
+  // then a fixed-order warp-shuffle tree and a fixed-order pass over the 8 warps (deterministic).
+  float m = -INFINITY, sum = 0.f;
+  for (int k = tid; k < tiles; k += 256) {
+    const float2 p = partials[(size_t)k * rows + i];
+    r_t[k] = p.x;
+    if (st == nullptr) {
+      const float nm = fmaxf(m, p.x);
+      sum = sum * ex2((m - nm) * LOG2E) + p.y * ex2((p.x - nm) * LOG2E);
+      m = nm;
+    }
+  }
+  if (st == nullptr) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const float om = __shfl_down_sync(0xffffffffu, m, o), os = __shfl_down_sync(0xffffffffu, sum, o);
+      const float nm = fmaxf(m, om);
+      sum = (m == -INFINITY ? 0.f : sum * ex2((m - nm) * LOG2E)) + (om == -INFINITY ? 0.f : os * ex2((om - nm) * LOG2E));
+      m = nm;
+    }
+    if ((tid & 31) == 0) {
+      wm[tid >> 5] = m;
+      ws[tid >> 5] = sum;
+    }
+  }
+  __syncthreads();
   if (tid == 0) {
     float M = -INFINITY, S = 0.f, z = 0.f;
     const int32_t tt = t[i];
-    if (st == nullptr) {
-      M = local.x;
-      S = local.y;
+    if (st == nullptr) {  // one GPU: this shard's own tiles
+      for (int k = 0; k < 8; ++k) M = fmaxf(M, wm[k]);
+      for (int k = 0; k < 8; ++k)
+        if (wm[k] != -INFINITY) S += ws[k] * ex2((wm[k] - M) * LOG2E);
       const int64_t loc0 = (int64_t)tt - vocab_start;
       if (tt != ignore_index && loc0 >= 0 && loc0 < V_l) z = zt[i];
     } else {
@@ -116,29 +149,28 @@ __global__ void __launch_bounds__(256) combine_transform_kernel(
   }
   __syncthreads();
   const float cg = sM, lse2 = sLse;
-  for (int k = tid; k < tiles; k += 256) r_t[k] = cg * ex2(partials[(size_t)k * rows + i].x * LOG2E - lse2);
+  for (int k = tid; k < tiles; k += 256) r_t[k] = cg * ex2(r_t[k] * LOG2E - lse2);
   __syncthreads();
   // G_P = p~ * r_t, in place, 8 bf16 per 16-byte access.
-  uint4* row = reinterpret_cast<uint4*>(i < split ? stash + (size_t)i * ld_stash : stash2 + (size_t)(i - split) * ld_stash);
-  const int64_t groups = (V_l + 7) / 8;
-  constexpr int U = 4;  // 4 independent 16-byte loads in flight per thread
-  for (int64_t q0 = tid; q0 < groups; q0 += 256 * U) {
-    uint4 w[U];
-#pragma unroll
-    for (int u = 0; u < U; ++u)
-      if (q0 + u * 256 < groups) w[u] = row[q0 + u * 256];
+  for (int64_t q0 = tid;;) {
 #pragma unroll
     for (int u = 0; u < U; ++u) {
       const int64_t q = q0 + u * 256;
       if (q < groups) {
         const float r = r_t[(q * 8) / 256];
-        w[u].x = pack_bf16x2(bf16lo_to_f32(w[u].x) * r, bf16hi_to_f32(w[u].x) * r);
-        w[u].y = pack_bf16x2(bf16lo_to_f32(w[u].y) * r, bf16hi_to_f32(w[u].y) * r);
-        w[u].z = pack_bf16x2(bf16lo_to_f32(w[u].z) * r, bf16hi_to_f32(w[u].z) * r);
-        w[u].w = pack_bf16x2(bf16lo_to_f32(w[u].w) * r, bf16hi_to_f32(w[u].w) * r);
-        row[q] = w[u];
+        uint4 x = w[u];
+        x.x = pack_bf16x2(bf16lo_to_f32(x.x) * r, bf16hi_to_f32(x.x) * r);
+        x.y = pack_bf16x2(bf16lo_to_f32(x.y) * r, bf16hi_to_f32(x.y) * r);
+        x.z = pack_bf16x2(bf16lo_to_f32(x.z) * r, bf16hi_to_f32(x.z) * r);
+        x.w = pack_bf16x2(bf16lo_to_f32(x.w) * r, bf16hi_to_f32(x.w) * r);
+        row[q] = x;
       }
     }
+    q0 += 256 * U;
+    if (q0 >= groups) break;
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+      if (q0 + u * 256 < groups) w[u] = row[q0 + u * 256];
   }
 }
 

@@ -1,4 +1,6 @@
 mkdir -p gpurun_out
 export PYTHONUNBUFFERED=1
-timeout 1500 python -m pytest tests/test_gpu_parity.py -q -m "gpu" -x 2>&1 | grep -v "^\s*$" | tail -4
-timeout 600 python tools/dw_acc_error.py
+timeout 1500 python -m pytest tests/test_gpu_parity.py -q -m "gpu and not slow" -x -k "parity_s or extended" 2>&1 | grep -v "^\s*$" | tail -1
+for i in 1 2 3; do
+timeout 300 python tools/diag_s.py --iters 10 2>&1 | sed -n 2,2p
+done
