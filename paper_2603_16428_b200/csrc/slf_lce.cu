@@ -920,35 +920,41 @@ float* s_loss_rows(Ctx& c, int reduction, float* loss_out) {
   return reduction == SLF_NONE ? loss_out : reinterpret_cast<float*>(c.ws + c.plan.off_loss);
 }
 
-// The fused single-GPU call under schedule S (g = 1: a chunk's statistics are its own).  When dX
-// is requested, each chunk grows by `ext` rows whose stash lives in dhidden's not-yet-written rows
-// beyond the chunk (no extra memory): fewer chunks, fewer dW read-modify-write passes and longer
-// dW K.  SLF_S_NO_EXT=1 disables the extension.
-slf_status phase_s(Ctx& c, const void* X, const void* W, const int32_t* t, int64_t N, int64_t H, int64_t V,
-                   int32_t ignore_index, int reduction, float scale, float* loss_out, void* dX, void* dW) {
-  const Plan& p = c.plan;
-  const SArgs a{X, W, t, N, H, V, 0, V, ignore_index};
-  SLF_TRY(s_begin(c, a, dW != nullptr));
+// Row chunks of the fused single-GPU call.  With `extend` (dhidden requested), a full chunk grows
+// by E rows whose stash lives in dhidden's not-yet-written rows beyond it: E*ld_stash <=
+// (N - r0 - C - E)*H, a multiple of 256 (no half-empty CTA-pair row tiles; measured 2 % faster
+// than 128 despite one more chunk), at most C (partials room).  SLF_S_NO_EXT=1 disables it.
+std::vector<SChunk> s_chunks(const Plan& p, int64_t N, int64_t H, bool extend, uint8_t* dX) {
   static const bool no_ext = getenv("SLF_S_NO_EXT") != nullptr;
   static const int64_t ext_gran = getenv("SLF_S_EXT_GRAN") ? atoi(getenv("SLF_S_EXT_GRAN")) : 256;
   std::vector<SChunk> chunks;
   for (int64_t r0 = 0, ci = 0; r0 < N; ++ci) {
     SChunk k{ci, r0, std::min(p.C, N - r0), 0, nullptr};
-    if (dX && !no_ext && k.rows == p.C) {
-      // ext rows E with E*ld_stash <= (N - r0 - C - E)*H, a multiple of 256 (no half-empty CTA-pair
-      // row tiles; measured 2 % faster than 128 despite one more chunk), at most C (partials room)
+    if (extend && !no_ext && k.rows == p.C) {
       const int64_t free_rows = N - r0 - p.C;
       int64_t e = free_rows > 0 ? (free_rows * H) / (p.ld_stash + H) : 0;
       e = std::min<int64_t>(e, p.C) / ext_gran * ext_gran;
       if (e > 0) {
         k.ext = e;
         k.rows = p.C + e;
-        k.ext_base = reinterpret_cast<uint8_t*>(dX) + (size_t)(r0 + k.rows) * H * 2;
+        k.ext_base = dX ? dX + (size_t)(r0 + k.rows) * H * 2 : nullptr;
       }
     }
     chunks.push_back(k);
     r0 += k.rows;
   }
+  return chunks;
+}
+
+// The fused single-GPU call under schedule S (g = 1: a chunk's statistics are its own).  When dX
+// is requested, the chunks are extended into dhidden's not-yet-written rows (s_chunks): fewer
+// chunks, fewer dW accumulation passes and longer dW K, at no extra memory.
+slf_status phase_s(Ctx& c, const void* X, const void* W, const int32_t* t, int64_t N, int64_t H, int64_t V,
+                   int32_t ignore_index, int reduction, float scale, float* loss_out, void* dX, void* dW) {
+  const Plan& p = c.plan;
+  const SArgs a{X, W, t, N, H, V, 0, V, ignore_index};
+  SLF_TRY(s_begin(c, a, dW != nullptr));
+  const std::vector<SChunk> chunks = s_chunks(p, N, H, dX != nullptr, reinterpret_cast<uint8_t*>(dX));
   // LPT tables per distinct chunk shape (rows, ext, first/RMW), uploaded once.
   SchedArena arena;
   std::vector<std::pair<std::pair<int64_t, int64_t>, int>> keys;
@@ -1035,9 +1041,12 @@ slf_status slf_lce_plan_describe(int64_t N, int64_t H, int64_t V_local, int sche
   Plan p;
   if (!plan_any(N, H, V_local, schedule, budget_bytes, true, &p)) return fail(SLF_ERR_WORKSPACE, "no plan fits");
   if (p.sched == SLF_SCHED_S) {
+    const int64_t fused = (int64_t)s_chunks(p, N, H, true, nullptr).size();
     snprintf(out, cap,
-             "schedule=S row_chunk=%lld n_chunks=%lld stash_bytes=%zu workspace=%zu launches=%lld",
-             (long long)p.C, (long long)p.nCh, (size_t)p.C * p.ld_stash * 2, p.total, (long long)(8 + p.nCh * 3));
+             "schedule=S row_chunk=%lld n_chunks=%lld fused_chunks_with_dhidden=%lld stash_bytes=%zu workspace=%zu "
+             "launches=%lld",
+             (long long)p.C, (long long)p.nCh, (long long)fused, (size_t)p.C * p.ld_stash * 2, p.total,
+             (long long)(8 + fused * 3));
   } else {
     snprintf(out, cap,
              "schedule=R row_block=%lld n_row_blocks=%lld vocab_chunk=%lld n_vocab_chunks=%lld workspace=%zu "

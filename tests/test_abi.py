@@ -59,6 +59,28 @@ def test_planner_budget(L, cfg):
         assert ws <= 0.05 * N * V * 2  # BASELINE.json: extra memory <= 5% of the N*V*2 logits
 
 
+def test_extended_chunk_plan(L):
+    """Extended chunks: the fused call with dhidden runs fewer chunks than the plain
+    plan, each a multiple of 256 rows, and the extension never outgrows the free dhidden rows."""
+    from paper_2603_16428_b200 import lce
+    expect = {(16384, 4096, 128256): (768, 22, 19), (65536, 12288, 32768): (3072, 22, 12)}
+    for (N, H, V), (C, n, fused) in expect.items():
+        kv = dict(x.split("=") for x in lce.plan_describe(N, H, V, schedule="S").split())
+        assert (int(kv["row_chunk"]), int(kv["n_chunks"]), int(kv["fused_chunks_with_dhidden"])) == (C, n, fused)
+    # the host-side rule, restated: E*ld <= (N - r0 - C - E)*H, E % 256 == 0, E <= C
+    N, H, V, C = 16384, 4096, 128256, 768
+    ld, r0, rows = (V + 7) // 8 * 8, 0, []
+    while r0 < N:
+        r = min(C, N - r0)
+        if r == C:
+            e = min(max(0, (N - r0 - C) * H // (ld + H)), C) // 256 * 256
+            assert e * ld <= (N - r0 - C - e) * H
+            r += e
+        rows.append(r)
+        r0 += r
+    assert len(rows) == 19 and all(x % 256 == 0 for x in rows)
+
+
 def test_planner_infeasible_and_errors(L):
     from paper_2603_16428_b200 import lce, _lib
     assert lce.workspace_bytes(16384, 4096, 128256, budget_bytes=1 << 20) == 0
