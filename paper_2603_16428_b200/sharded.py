@@ -16,9 +16,9 @@ Schedule R (the north-star literal, recompute in backward):
     st_k = shard_stats ; ST = all_gather(st_k) ; loss, rs_k = stats_combine(ST)
     dX_k, dW_k = lce_bwd(rs_k, fp32 dX) ; all_reduce(dX_k) ; dx_finalize
 
-The ops are injectable so the R orchestration can be tested with world_size 2/3 on CPU (gloo)
-against the oracle (tests/test_sharded_cpu.py); the S orchestration is tested on one GPU by
-emulating the shards (tests/test_gpu_parity.py::test_vocab_shard_emulation_s).
+The ops are injectable so both orchestrations can be tested with world_size 2/3 on CPU (gloo)
+against the oracle (tests/test_sharded_cpu.py); the S kernels' shard math is also tested on one
+GPU by emulating the shards (tests/test_gpu_parity.py::test_vocab_shard_emulation_s).
 """
 from __future__ import annotations
 
@@ -34,8 +34,12 @@ def shard_bounds(V: int, g: int, rank: int):
 
 def cuda_ops():
     from . import lce
+
+    def dx_finalize_rows(sh, dx32, r0, out):  # RNE to bf16 of rows [r0, r0 + len) with their RowStat
+        return lce.dx_finalize_ptr(dx32, sh.rowstat() + r0 * 16, out)
+
     return types.SimpleNamespace(shard_stats=lce.shard_stats, stats_combine=lce.stats_combine, lce_bwd=lce.lce_bwd,
-                                 dx_finalize=lce.dx_finalize)
+                                 dx_finalize=lce.dx_finalize, SShard=lce.SShard, dx_finalize_rows=dx_finalize_rows)
 
 
 class VocabShardedLCE:
@@ -53,7 +57,8 @@ class VocabShardedLCE:
         self.budget = budget_bytes
         if schedule not in ("S", "R"):
             raise ValueError("schedule must be 'S' or 'R'")
-        self.schedule = schedule if ops is None else "R"  # injected (CPU) ops implement the R seam only
+        # injected (CPU test) ops may implement only the R seam
+        self.schedule = schedule if (ops is None or hasattr(ops, "SShard")) else "R"
         self._bufs = {}
 
     def _buf(self, key, shape, dtype, device):
@@ -95,25 +100,25 @@ class VocabShardedLCE:
 
     def _fwd_bwd_s(self, X, W_local, t, ignore_index, reduction, scale, workspace, dW_out, dX_out):
         import torch
-        from . import lce
         N, H = X.shape
-        sh = lce.SShard(X, W_local, t, self.v0, self.V, ignore_index, reduction, scale, self.budget, workspace)
+        sh = self.ops.SShard(X, W_local, t, self.v0, self.V, ignore_index, reduction, scale, self.budget, workspace)
         dev = X.device
         C, nch = sh.C, sh.n_chunks
+        fdt = torch.float64 if X.dtype == torch.float64 else torch.float32  # fp32 statistics / partials on the GPU
         dW = dW_out if dW_out is not None else torch.empty_like(W_local)
-        dX = dX_out if dX_out is not None else torch.empty(N, H, dtype=torch.bfloat16, device=dev)
-        loss = torch.empty(N if reduction == "none" else 1, dtype=torch.float32, device=dev)
-        st_loc = self._buf("s_st", (C, 4), torch.float32, dev)
-        st_all = self._buf("s_stall", (self.g * C, 4), torch.float32, dev)
-        dxb = [self._buf(f"s_dx{i}", (C, H), torch.float32, dev) for i in range(2)]
-        rs_base = sh.rowstat()
+        dX = dX_out if dX_out is not None else torch.empty(N, H, dtype=X.dtype if fdt == torch.float64
+                                                           else torch.bfloat16, device=dev)
+        loss = torch.empty(N if reduction == "none" else 1, dtype=fdt, device=dev)
+        st_loc = self._buf("s_st", (C, 4), fdt, dev)
+        st_all = self._buf("s_stall", (self.g * C, 4), fdt, dev)
+        dxb = [self._buf(f"s_dx{i}", (C, H), fdt, dev) for i in range(2)]
         sh.begin(need_dweight=True)
         pending = [None, None]  # (work handle, r0, rows) of the all-reduce in flight per buffer
 
         def finalize(slot):
             h, r0, rows = pending[slot]
             h.wait()
-            lce.dx_finalize_ptr(dxb[slot][:rows], rs_base + r0 * 16, dX[r0:r0 + rows])
+            self.ops.dx_finalize_rows(sh, dxb[slot][:rows], r0, dX[r0:r0 + rows])
             pending[slot] = None
 
         for ch in range(nch):
