@@ -209,7 +209,15 @@ def main():
         # Sharded runs: 5% of the GLOBAL N*V*2 logits per GPU (SURVEY q7 "lenient" reading; both
         # ratios are reported in "memory").
         args.budget = int(0.05 * N * V * 2)
-    ws = slf.alloc_workspace(N_l, H, V_l, dev, budget_bytes=args.budget)
+    ws_budget = args.budget
+    if g > 1 and not dp:
+        from paper_2603_16428_b200.sharded import VocabShardedLCE
+        sharded = VocabShardedLCE(V, budget_bytes=args.budget, schedule="R" if args.schedule == "R" else "S")
+        assert (sharded.v0, sharded.v1) == (v0, v1)
+        if sharded.schedule == "S":  # the workspace shares the budget with the module's dX buffers
+            ws_budget = sharded.s_workspace_budget(N, H)
+    ws = slf.alloc_workspace(N_l, H, V_l, dev, schedule="S" if (g > 1 and not dp and sharded.schedule == "S")
+                             else args.schedule, budget_bytes=ws_budget)
     loss = torch.empty(1, dtype=torch.float32, device=dev)
     dX = torch.empty(N_l, H, dtype=torch.bfloat16, device=dev)
     dW = torch.empty(V_l, H, dtype=torch.bfloat16, device=dev)
@@ -218,10 +226,11 @@ def main():
         from paper_2603_16428_b200.sharded import TokenShardedLCE
         dpm = TokenShardedLCE(budget_bytes=args.budget, schedule=args.schedule)
     elif g > 1:
-        from paper_2603_16428_b200.sharded import VocabShardedLCE
-        sharded = VocabShardedLCE(V, budget_bytes=args.budget, schedule="R" if args.schedule == "R" else "S")
-        assert (sharded.v0, sharded.v1) == (v0, v1)
-        extra += g * N * 16 + N * H * 4  # gathered statistics + fp32 dX partial
+        if sharded.schedule == "S":
+            C_s, _ = slf.s_plan(N, H, V_l, ws_budget)
+            extra += 2 * C_s * H * 4 + (g + 1) * C_s * 16  # double-buffered fp32 dX partials + statistics
+        else:
+            extra += g * N * 16 + N * H * 4  # gathered statistics + fp32 dX partial
 
     def step(Xs=X, ts=t):
         if g == 1:
@@ -348,7 +357,7 @@ def main():
                    if g > 1 else "single GPU",
                    "targets": args.dist, "logit_std": args.alpha, "ignore_frac": 0.05,
                    "l2": "inputs larger than L2 (W alone is %.2f GB vs 126 MB L2); no flush" % (V_l * H * 2 / 1e9),
-                   "plan": slf.plan_describe(N_l, H, V_l, budget_bytes=args.budget,
+                   "plan": slf.plan_describe(N_l, H, V_l, budget_bytes=ws_budget,
                                              schedule=args.schedule)},
         "tflops": tflops, "frac_of_peak_burst": tflops / peaks["burst"],
         "frac_of_peak_sustained": tflops / peaks["sustained"],

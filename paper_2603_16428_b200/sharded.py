@@ -39,7 +39,8 @@ def cuda_ops():
         return lce.dx_finalize_ptr(dx32, sh.rowstat() + r0 * 16, out)
 
     return types.SimpleNamespace(shard_stats=lce.shard_stats, stats_combine=lce.stats_combine, lce_bwd=lce.lce_bwd,
-                                 dx_finalize=lce.dx_finalize, SShard=lce.SShard, dx_finalize_rows=dx_finalize_rows)
+                                 dx_finalize=lce.dx_finalize, SShard=lce.SShard, dx_finalize_rows=dx_finalize_rows,
+                                 s_plan=lce.s_plan)
 
 
 class VocabShardedLCE:
@@ -60,6 +61,33 @@ class VocabShardedLCE:
         # injected (CPU test) ops may implement only the R seam
         self.schedule = schedule if (ops is None or hasattr(ops, "SShard")) else "R"
         self._bufs = {}
+
+    def s_workspace_budget(self, N: int, H: int) -> int:
+        """Schedule S: the planner budget for this rank's workspace such that the workspace plus this
+        module's per-chunk buffers (two fp32 dX partials [C, H], the gathered statistics g*C*16 B and
+        the local ones C*16 B) stay within `budget_bytes` (0: 5 % of the global N*V*2 logits, the
+        lenient reading of SURVEY q7).  So the memory claim covers everything the step allocates."""
+        from . import lce
+        total = self.budget or int(0.05 * N * self.V * 2)
+        V_l = self.v1 - self.v0
+        def need(b):
+            ws = lce.workspace_bytes(N, H, V_l, "S", b)
+            if ws == 0:
+                return None
+            C, _n = lce.s_plan(N, H, V_l, b)
+            return ws + 2 * C * H * 4 + (self.g + 1) * C * 16
+
+        lo, hi = 0, total  # largest planner budget whose total need fits (bisection; need grows with b)
+        for _ in range(40):
+            mid = (lo + hi + 1) // 2
+            nb = need(mid)
+            if nb is not None and nb <= total:
+                lo = mid
+            else:
+                hi = mid - 1
+        if need(lo) is None:
+            raise RuntimeError(f"no schedule-S plan fits {total} bytes with its dX buffers")
+        return lo
 
     def _buf(self, key, shape, dtype, device):
         import torch
@@ -101,7 +129,8 @@ class VocabShardedLCE:
     def _fwd_bwd_s(self, X, W_local, t, ignore_index, reduction, scale, workspace, dW_out, dX_out):
         import torch
         N, H = X.shape
-        sh = self.ops.SShard(X, W_local, t, self.v0, self.V, ignore_index, reduction, scale, self.budget, workspace)
+        budget = self.s_workspace_budget(N, H) if hasattr(self.ops, "s_plan") else self.budget
+        sh = self.ops.SShard(X, W_local, t, self.v0, self.V, ignore_index, reduction, scale, budget, workspace)
         dev = X.device
         C, nch = sh.C, sh.n_chunks
         fdt = torch.float64 if X.dtype == torch.float64 else torch.float32  # fp32 statistics / partials on the GPU
