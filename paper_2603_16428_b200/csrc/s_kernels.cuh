@@ -192,48 +192,71 @@ __global__ void csr_count_kernel(const int32_t* __restrict__ t, int64_t N, int32
 }
 
 // Single block: off = exclusive_scan(cnt) over V_l entries (off[V_l] = total); hit list of rows with
-// cnt > 0 in increasing row order; n_hits stored in off[V_l + 1].
+// cnt > 0 in increasing row order; n_hits stored in off[V_l + 1].  Coalesced: 1024 consecutive
+// entries per pass, warp-shuffle scans plus a running carry (integer, exact).
 __global__ void __launch_bounds__(1024) csr_scan_kernel(const int32_t* __restrict__ cnt, int64_t V_l,
                                                        int32_t* __restrict__ off, int32_t* __restrict__ hits) {
-  __shared__ int32_t sc[1024], sh[1024];
-  const int tid = threadIdx.x;
-  const int64_t per = (V_l + 1023) / 1024;
-  const int64_t b = tid * per, e = min(V_l, b + per);
-  int32_t s = 0, h = 0;
-  for (int64_t v = b; v < e; ++v) {
-    s += cnt[v];
-    h += cnt[v] > 0;
-  }
-  sc[tid] = s;
-  sh[tid] = h;
-  __syncthreads();
-  for (int o = 1; o < 1024; o <<= 1) {  // inclusive Hillis-Steele scan (fixed order, integer)
-    const int32_t a = tid >= o ? sc[tid - o] : 0, c = tid >= o ? sh[tid - o] : 0;
+  __shared__ int32_t wsum[32], whit[32];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  int32_t carry_s = 0, carry_h = 0;  // identical in every thread
+  for (int64_t base = 0; base < V_l; base += 1024) {
+    const int64_t v = base + tid;
+    const int32_t c = v < V_l ? cnt[v] : 0, h = c > 0 ? 1 : 0;
+    int32_t si = c, hi = h;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int32_t a = __shfl_up_sync(0xffffffffu, si, o), b2 = __shfl_up_sync(0xffffffffu, hi, o);
+      if (lane >= o) {
+        si += a;
+        hi += b2;
+      }
+    }
+    if (lane == 31) {
+      wsum[warp] = si;
+      whit[warp] = hi;
+    }
     __syncthreads();
-    sc[tid] += a;
-    sh[tid] += c;
+    if (warp == 0) {
+      int32_t ws = wsum[lane], wh = whit[lane];
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int32_t a = __shfl_up_sync(0xffffffffu, ws, o), b2 = __shfl_up_sync(0xffffffffu, wh, o);
+        if (lane >= o) {
+          ws += a;
+          wh += b2;
+        }
+      }
+      wsum[lane] = ws;  // inclusive over warps
+      whit[lane] = wh;
+    }
     __syncthreads();
+    const int32_t ps = carry_s + (warp ? wsum[warp - 1] : 0) + si - c;
+    const int32_t ph = carry_h + (warp ? whit[warp - 1] : 0) + hi - h;
+    if (v < V_l) {
+      off[v] = ps;
+      if (h) hits[ph] = (int32_t)v;
+    }
+    carry_s += wsum[31];
+    carry_h += whit[31];
+    __syncthreads();  // wsum / whit are rewritten by the next pass
   }
-  int32_t run = tid ? sc[tid - 1] : 0, hr = tid ? sh[tid - 1] : 0;
-  for (int64_t v = b; v < e; ++v) {
-    off[v] = run;
-    run += cnt[v];
-    if (cnt[v] > 0) hits[hr++] = (int32_t)v;
-  }
-  if (tid == 1023) {
-    off[V_l] = sc[1023];
-    off[V_l + 1] = sh[1023];
+  if (tid == 0) {
+    off[V_l] = carry_s;
+    off[V_l + 1] = carry_h;
   }
 }
 
 // rank_i = #{j < i : t_j == t_i, both in shard}; idx[off[t_i] + rank_i] = i.  Brute force over
-// earlier tokens through shared-memory tiles (only for targets that occur more than once).
+// earlier tokens through shared-memory tiles (only for targets that occur more than once); four
+// lanes per token each count a quarter of every tile, summed with shuffles (integer, exact).
+constexpr int CSR_TOK_PER_BLOCK = 64;
 __global__ void __launch_bounds__(256) csr_scatter_kernel(const int32_t* __restrict__ t, int64_t N,
                                                          int32_t ignore_index, int64_t vocab_start, int64_t V_l,
                                                          const int32_t* __restrict__ cnt,
                                                          const int32_t* __restrict__ off, int32_t* __restrict__ idx) {
   __shared__ int32_t tile[2048];
-  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int part = threadIdx.x & 3;
+  const int64_t i = (int64_t)blockIdx.x * CSR_TOK_PER_BLOCK + (threadIdx.x >> 2);
   int32_t key = -1;
   bool need = false;
   if (i < N && in_shard(t[i], ignore_index, vocab_start, V_l)) {
@@ -243,19 +266,21 @@ __global__ void __launch_bounds__(256) csr_scatter_kernel(const int32_t* __restr
   const int any_need = __syncthreads_or(need);
   int32_t rank = 0;
   if (any_need) {
-    const int64_t end = (int64_t)blockIdx.x * blockDim.x + blockDim.x;  // tokens before this block's last
+    const int64_t end = (int64_t)blockIdx.x * CSR_TOK_PER_BLOCK + CSR_TOK_PER_BLOCK;  // tokens before the last
     for (int64_t j0 = 0; j0 < end && j0 < N; j0 += 2048) {
       for (int k = threadIdx.x; k < 2048; k += blockDim.x) tile[k] = (j0 + k < N) ? t[j0 + k] : ignore_index;
       __syncthreads();
       if (need) {
         const int64_t rem = i - j0;
         const int lim = rem < 2048 ? (int)rem : 2048;
-        for (int k = 0; k < lim; ++k) rank += (tile[k] == key);
+        for (int k = part; k < lim; k += 4) rank += (tile[k] == key);
       }
       __syncthreads();
     }
   }
-  if (key >= 0) idx[off[key - vocab_start] + rank] = (int32_t)i;  // key >= 0 <=> valid and in shard
+  rank += __shfl_xor_sync(0xffffffffu, rank, 1);
+  rank += __shfl_xor_sync(0xffffffffu, rank, 2);
+  if (key >= 0 && part == 0) idx[off[key - vocab_start] + rank] = (int32_t)i;  // valid and in shard
 }
 
 // dW[v] = bf16( f32(dW[v]) - coef * sum_{i in CSR[v]} x_i ), sums in fp32 in token order.

@@ -732,7 +732,8 @@ slf_status s_begin(Ctx& c, const SArgs& a, bool need_dw) {
     csr_zero_kernel<<<(unsigned)std::min<int64_t>((a.V_l + 2 + 255) / 256, 1024), 256, 0, c.s>>>(cnt, a.V_l + 2);
     csr_count_kernel<<<(unsigned)((a.N + 255) / 256), 256, 0, c.s>>>(a.t, a.N, a.ign, a.vs, a.V_l, cnt);
     csr_scan_kernel<<<1, 1024, 0, c.s>>>(cnt, a.V_l, off, hits);
-    csr_scatter_kernel<<<(unsigned)((a.N + 255) / 256), 256, 0, c.s>>>(a.t, a.N, a.ign, a.vs, a.V_l, cnt, off, idx);
+    csr_scatter_kernel<<<(unsigned)((a.N + CSR_TOK_PER_BLOCK - 1) / CSR_TOK_PER_BLOCK), 256, 0, c.s>>>(
+        a.t, a.N, a.ign, a.vs, a.V_l, cnt, off, idx);
     SLF_CUDA(cudaGetLastError());
   }
   return SLF_OK;

@@ -1,3 +1,6 @@
 mkdir -p gpurun_out
 export PYTHONUNBUFFERED=1
 timeout 1500 python -m pytest tests/test_gpu_parity.py -q -m "gpu and not slow" -x 2>&1 | grep -v "^\s*$" | tail -2
+for i in 1 2; do
+timeout 300 python tools/diag_s.py --iters 10 2>&1 | sed -n 2,2p
+done
