@@ -387,7 +387,9 @@ __device__ __forceinline__ void epilogue_dw_tma(const GemmArgs& a, const CUtenso
     fence_proxy_async_smem();
     named_bar_sync(1, 128);
     if (lead) {
-      if (a.mode == 2) {  // accumulate in L2: bf16 reduce-add of this tile's partial
+      if (dbg & 256) {
+        // timing experiment only: no dW store at all (wrong dW)
+      } else if (a.mode == 2) {  // accumulate in L2: bf16 reduce-add of this tile's partial
         for (int j = 0; j < gn; ++j) tma_reduce_add_2d(tmC, stg + j * CHUNK_BYTES, n0 + (g0 + j) * 64, row0);
       } else if (dbg & 16) {
         const uint64_t pol = policy_evict_first();
@@ -546,7 +548,8 @@ struct GroupArgs {
   int num_tiles;
   int dbg;  // timing-experiment knobs (0 in production): 1 = no L2 prefetch, 2 = late old-dW loads,
             // 4 = record the per-tile trace of unit 0, 8 = L2 prefetch of the next tile's MN-major A,
-            // 16 = evict-first dW RMW traffic, 32 = old-dW loads from the first 1024 rows (wrong dW)
+            // 16 = evict-first dW RMW traffic, 32 = old-dW loads from the first 1024 rows (wrong dW),
+            // 256 = no dW stores (wrong dW)
   const int* sched;  // [units][sched_stride] tile ids, -1 terminated (nullptr: round robin)
   int sched_stride;
 };
