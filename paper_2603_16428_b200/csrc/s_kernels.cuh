@@ -192,17 +192,31 @@ __global__ void csr_count_kernel(const int32_t* __restrict__ t, int64_t N, int32
 }
 
 // Single block: off = exclusive_scan(cnt) over V_l entries (off[V_l] = total); hit list of rows with
-// cnt > 0 in increasing row order; n_hits stored in off[V_l + 1].  Coalesced: 1024 consecutive
-// entries per pass, warp-shuffle scans plus a running carry (integer, exact).
+// cnt > 0 in increasing row order; n_hits stored in off[V_l + 1].  Each pass covers 8192
+// consecutive entries: eight per thread (coalesced loads, all in flight at once), a serial scan of
+// the thread's eight, warp-shuffle scans of the thread totals and a running carry (integer, exact).
 __global__ void __launch_bounds__(1024) csr_scan_kernel(const int32_t* __restrict__ cnt, int64_t V_l,
                                                        int32_t* __restrict__ off, int32_t* __restrict__ hits) {
+  constexpr int PER = 8, SPAN = 1024 * PER;
+  __shared__ int32_t stage[SPAN];
   __shared__ int32_t wsum[32], whit[32];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   int32_t carry_s = 0, carry_h = 0;  // identical in every thread
-  for (int64_t base = 0; base < V_l; base += 1024) {
-    const int64_t v = base + tid;
-    const int32_t c = v < V_l ? cnt[v] : 0, h = c > 0 ? 1 : 0;
-    int32_t si = c, hi = h;
+  for (int64_t base = 0; base < V_l; base += SPAN) {
+#pragma unroll
+    for (int k = 0; k < PER; ++k) {  // coalesced: entry base + k*1024 + tid
+      const int64_t v = base + k * 1024 + tid;
+      stage[k * 1024 + tid] = v < V_l ? cnt[v] : 0;
+    }
+    __syncthreads();
+    int32_t c[PER], s = 0, h = 0;
+#pragma unroll
+    for (int k = 0; k < PER; ++k) {  // this thread's eight consecutive entries
+      c[k] = stage[tid * PER + k];
+      s += c[k];
+      h += c[k] > 0;
+    }
+    int32_t si = s, hi = h;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
       const int32_t a = __shfl_up_sync(0xffffffffu, si, o), b2 = __shfl_up_sync(0xffffffffu, hi, o);
@@ -230,15 +244,20 @@ __global__ void __launch_bounds__(1024) csr_scan_kernel(const int32_t* __restric
       whit[lane] = wh;
     }
     __syncthreads();
-    const int32_t ps = carry_s + (warp ? wsum[warp - 1] : 0) + si - c;
-    const int32_t ph = carry_h + (warp ? whit[warp - 1] : 0) + hi - h;
-    if (v < V_l) {
-      off[v] = ps;
-      if (h) hits[ph] = (int32_t)v;
+    int32_t ps = carry_s + (warp ? wsum[warp - 1] : 0) + si - s;
+    int32_t ph = carry_h + (warp ? whit[warp - 1] : 0) + hi - h;
+#pragma unroll
+    for (int k = 0; k < PER; ++k) {
+      const int64_t v = base + (int64_t)tid * PER + k;
+      if (v < V_l) {
+        off[v] = ps;
+        if (c[k] > 0) hits[ph++] = (int32_t)v;
+      }
+      ps += c[k];
     }
     carry_s += wsum[31];
     carry_h += whit[31];
-    __syncthreads();  // wsum / whit are rewritten by the next pass
+    __syncthreads();  // stage / wsum / whit are rewritten by the next pass
   }
   if (tid == 0) {
     off[V_l] = carry_s;
