@@ -284,8 +284,11 @@ def main():
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         ms = float(tt.item())
 
-    # End to end through the public API with HOST buffers: per step, pinned H2D of the step's
-    # inputs (hidden states, targets), the fused call, and a D2H read of the loss.
+    # End to end through the public API with HOST buffers: per step, the pinned host->device copy
+    # of the step's inputs (hidden states, targets), the fused call and a device->host read of the
+    # loss.  On one GPU this is the C-ABI host-input call (slf_lce_fwd_bwd_host: hidden rows are
+    # copied chunk by chunk on a copy stream while earlier chunks compute); sharded runs copy with
+    # torch and call their module.
     e2e = None
     if not args.no_e2e:
         Xh = torch.from_numpy(inp.X[n0:n1].view(np.int16)).view(torch.bfloat16).pin_memory()
@@ -293,12 +296,17 @@ def main():
         lh = torch.empty(1, dtype=torch.float32).pin_memory()
         Xd = torch.empty_like(X)
         td = torch.empty_like(t)
+        stg = slf.HostStaging(N_l, H, dev) if g == 1 else None
 
         def e2e_step():
-            Xd.copy_(Xh, non_blocking=True)
-            td.copy_(th, non_blocking=True)
-            lo = step(Xd, td)
-            lh.copy_(lo.reshape(1), non_blocking=True)
+            if g == 1:
+                slf.lce_fwd_bwd_host(Xh, W, th, dX=dX, dW=dW, loss_host=lh, staging=stg, workspace=ws,
+                                     budget_bytes=args.budget, schedule=args.schedule)
+            else:
+                Xd.copy_(Xh, non_blocking=True)
+                td.copy_(th, non_blocking=True)
+                lo = step(Xd, td)
+                lh.copy_(lo.reshape(1), non_blocking=True)
             torch.cuda.current_stream(dev).synchronize()
             return float(lh[0])
 

@@ -128,13 +128,34 @@ slf_status slf_lce_fwd_bwd(const void* hidden, const void* weight, const int32_t
                            size_t budget_bytes, void* stream);
 
 /* slf_lce_fwd_bwd with flags (gradient accumulation across micro-batches):
- *   SLF_FLAG_ACCUMULATE_DW: dweight += dL/dW (bf16 read-add-write in fp32) instead of =.
+ *   SLF_FLAG_ACCUMULATE_DW: dweight += dL/dW instead of = (each partial is rounded to bf16 and
+ *   added to dweight by the L2: TMA reduce-add).
  * flags = 0 is exactly slf_lce_fwd_bwd. */
 #define SLF_FLAG_ACCUMULATE_DW 1u
 slf_status slf_lce_fwd_bwd_ex(const void* hidden, const void* weight, const int32_t* targets, int64_t N, int64_t H,
                               int64_t V, int32_t ignore_index, int reduction, float scale, float* loss_out,
                               void* dhidden, void* dweight, void* workspace, size_t workspace_bytes, int schedule,
                               size_t budget_bytes, uint32_t flags, void* stream);
+
+/* The fused call with HOST inputs and loss (the path as a training step sees it:
+ * the batch arrives from the host).  Per step it copies targets, then hidden row chunk by row chunk
+ * on an internal copy stream, and the schedule-S chunk c waits only for its own rows, so the
+ * host->device transfer overlaps the GEMMs; the loss is copied back at the end.
+ *   hidden_host  [N, H] bf16 HOST (pinned for overlap; pageable works, serialised)   (read)
+ *   targets_host [N] int32 HOST                                                      (read)
+ *   loss_host    HOST fp32 [1] (SUM/MEAN) or [N] (NONE); valid after `stream` syncs  (written)
+ *   weight, dhidden, dweight, workspace: as slf_lce_fwd_bwd_ex (DEVICE)
+ *   hidden_dev [N, H] bf16, targets_dev [N] int32, loss_dev fp32 [1] / [N]: caller-owned DEVICE
+ *       staging buffers (the library allocates no device memory); overwritten.
+ * The copies into the staging buffers start only after the work already enqueued on `stream`
+ * (e.g. the previous step reading them) has completed.  Schedule R (when S does not fit) copies
+ * everything up front.  Not thread-safe against another host call on the same device at once
+ * (the copy stream and its events are per device). */
+slf_status slf_lce_fwd_bwd_host(const void* hidden_host, const void* weight, const int32_t* targets_host, int64_t N,
+                                int64_t H, int64_t V, int32_t ignore_index, int reduction, float scale,
+                                float* loss_host, void* dhidden, void* dweight, void* hidden_dev,
+                                int32_t* targets_dev, float* loss_dev, void* workspace, size_t workspace_bytes,
+                                int schedule, size_t budget_bytes, uint32_t flags, void* stream);
 
 /* Forward half (schedule R split; also the vocab-shard seam).  Computes the
  * loss and the RowStat array [N] (16 B/row, DEVICE, caller-owned) that

@@ -24,7 +24,8 @@ EXPORTS = ["slf_lce_version", "slf_last_error_string", "slf_lce_workspace_bytes"
            "slf_lce_status", "slf_debug_gemm", "slf_lce_dx_finalize", "slf_profile_begin", "slf_profile_end",
            "slf_lce_s_plan", "slf_lce_s_begin", "slf_lce_s_chunk_stats", "slf_lce_s_chunk_bwd", "slf_lce_s_end",
            "slf_lce_s_rowstat", "slf_rmsnorm_workspace_bytes", "slf_rmsnorm_fwd", "slf_rmsnorm_bwd",
-           "slf_debug_trace_read", "slf_debug_max_active_clusters", "slf_lce_fwd_bwd_ex", "slf_scale_bf16"]
+           "slf_debug_trace_read", "slf_debug_max_active_clusters", "slf_lce_fwd_bwd_ex", "slf_scale_bf16",
+           "slf_lce_fwd_bwd_host"]
 PROF_KINDS = ["gemm_stats", "gemm_grad", "gemm_dw", "gemm_dx", "gemm_debug", "prep", "local_combine", "final_combine",
               "dx_finalize", "gemm_group", "combine_transform", "csr", "onehot", "loss_reduce", "rmsnorm", "k15"]
 
@@ -71,6 +72,8 @@ def _declare(lib):
         "slf_scale_bf16": (INT, [P, I64, F32, P]),
         "slf_lce_fwd_bwd_ex": (INT, [P, P, P, I64, I64, I64, I32, INT, F32, P, P, P, P, SZ, INT, SZ,
                                      ctypes.c_uint32, P]),
+        "slf_lce_fwd_bwd_host": (INT, [P, P, P, I64, I64, I64, I32, INT, F32, P, P, P, P, P, P, P, SZ, INT, SZ,
+                                       ctypes.c_uint32, P]),
         "slf_debug_max_active_clusters": (INT, [INT, ctypes.POINTER(INT)]),
         "slf_rmsnorm_fwd": (INT, [P, P, I64, I64, F32, P, P, P]),
         "slf_rmsnorm_bwd": (INT, [P, P, P, P, I64, I64, P, P, P, SZ, P]),

@@ -10,6 +10,8 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <functional>
+#include <map>
 #include <mutex>
 #include <string>
 #include <vector>
@@ -106,6 +108,9 @@ struct DevInfo {
   int minor = 0;
   bool gemm_attr_set[64] = {};
   PinnedRing ring;
+  // slf_lce_fwd_bwd_host: copy stream and per-chunk events (created on first use)
+  cudaStream_t copy_stream = nullptr;
+  std::vector<cudaEvent_t> copy_events;
 };
 
 std::mutex g_mu;
@@ -494,18 +499,46 @@ struct Ctx {
   uint8_t* ws;
   Plan plan;
   bool acc_dw = false;  // SLF_FLAG_ACCUMULATE_DW: dW += instead of dW =
+  const cudaEvent_t* chunk_ready = nullptr;  // schedule S: chunk k's hidden rows are on the device
+  // schedule S: enqueues the chunked input copies once this call's own small H2D copies (targets,
+  // tile tables) are queued — copies share the H2D engine in FIFO order
+  std::function<slf_status()> enqueue_inputs;
 };
 
 WsHeader* hdr_of(uint8_t* ws) { return reinterpret_cast<WsHeader*>(ws); }
 double* block_sums_of(uint8_t* ws) { return reinterpret_cast<double*>(ws + 256); }
 
 // Per-call arena of LPT tile tables (uploaded once per call into the workspace).
+// LPT tables depend only on the problems' tile counts, K and epilogue kinds: memoised across calls
+// (building one is O(tiles x units) on the host, ~0.5 ms at the Llama-8B group shape).
+struct LptCache {
+  std::mutex mu;
+  std::map<std::vector<int64_t>, std::pair<std::vector<int>, int>> m;
+};
+LptCache g_lpt;
+
+std::vector<int> lpt_table_cached(const ProbSpec* ps, int n, int units, int* stride) {
+  std::vector<int64_t> key{units, n};
+  for (int p = 0; p < n; ++p)
+    key.insert(key.end(), {ps[p].a.M, ps[p].a.N, ps[p].a.K, ps[p].a.num_tiles, ps[p].epi, ps[p].a.mode});
+  std::lock_guard<std::mutex> lk(g_lpt.mu);
+  auto it = g_lpt.m.find(key);
+  if (it == g_lpt.m.end()) {
+    if (g_lpt.m.size() >= 256) g_lpt.m.clear();
+    int st = 0;
+    std::vector<int> t = lpt_table(ps, n, units, &st);
+    it = g_lpt.m.emplace(key, std::make_pair(std::move(t), st)).first;
+  }
+  *stride = it->second.second;
+  return it->second.first;  // a copy, taken under the lock
+}
+
 struct SchedArena {
   std::vector<int> host;
   std::vector<std::pair<size_t, int>> tables;  // (offset in ints, stride)
   int add(const ProbSpec* ps, int n, int units) {
     int stride = 0;
-    std::vector<int> t = lpt_table(ps, n, units, &stride);
+    const std::vector<int> t = lpt_table_cached(ps, n, units, &stride);
     tables.push_back({host.size(), stride});
     host.insert(host.end(), t.begin(), t.end());
     return (int)tables.size() - 1;
@@ -983,8 +1016,15 @@ slf_status phase_s(Ctx& c, const void* X, const void* W, const int32_t* t, int64
       std::fill(tab.begin(), tab.end(), -1);  // too many shapes: each launch uploads its own table
   }
   float* loss_rows = s_loss_rows(c, reduction, loss_out);
+  if (c.enqueue_inputs) SLF_TRY(c.enqueue_inputs());
   for (size_t i = 0; i < chunks.size(); ++i) {
     const SChunk& k = chunks[i];
+    // Input rows: chunks 0 and 1 wait for their own copies; chunk 2 waits for the last copy (the
+    // copy stream is FIFO, so all rows are then present; by then two chunks of GEMMs have hidden
+    // the transfer).  Few waits: a stream wait between two kernels forfeits the programmatic
+    // dependent launch overlap of the kernel after it.
+    if (c.chunk_ready && i <= 2)
+      SLF_CUDA(cudaStreamWaitEvent(c.s, c.chunk_ready[i < 2 ? i : chunks.size() - 1], 0));
     SLF_TRY(s_chunk_stats(c, a, k, nullptr));
     SLF_TRY(s_chunk_bwd(c, a, k, nullptr, 1, reduction, scale, loss_rows,
                         dX ? reinterpret_cast<uint8_t*>(dX) + (size_t)k.r0 * H * 2 : nullptr, 0, dW,
@@ -1088,6 +1128,70 @@ slf_status slf_lce_fwd_bwd_ex(const void* hidden, const void* weight, const int3
   SLF_TRY(phase_stats(c, hidden, weight, targets, N, H, V, 0, ignore_index, st));
   SLF_TRY(phase_combine(c, st, 1, targets, N, 0, V, V, ignore_index, reduction, scale, loss_out, rs));
   SLF_TRY(phase_backward(c, hidden, weight, rs, N, H, V, 1.0f, dhidden, 0, dweight));
+  return SLF_OK;
+}
+
+std::mutex g_host_mu;  // serialises slf_lce_fwd_bwd_host enqueues (shared copy stream / events)
+
+slf_status slf_lce_fwd_bwd_host(const void* hidden_host, const void* weight, const int32_t* targets_host, int64_t N,
+                                int64_t H, int64_t V, int32_t ignore_index, int reduction, float scale,
+                                float* loss_host, void* dhidden, void* dweight, void* hidden_dev,
+                                int32_t* targets_dev, float* loss_dev, void* workspace, size_t workspace_bytes,
+                                int schedule, size_t budget_bytes, uint32_t flags, void* stream) {
+  if (!hidden_host || !targets_host || !loss_host) return fail(SLF_ERR_ARG, "null host pointer");
+  SLF_TRY(check_common(hidden_dev, weight, targets_dev, N, H, V, workspace));
+  if (flags & ~(uint32_t)SLF_FLAG_ACCUMULATE_DW) return fail(SLF_ERR_ARG, "unknown flags 0x%x", flags);
+  if (!loss_dev || !aligned16(loss_dev)) return fail(SLF_ERR_ALIGN, "loss_dev must be a 16-byte aligned pointer");
+  if (reduction < SLF_SUM || reduction > SLF_NONE) return fail(SLF_ERR_ARG, "bad reduction %d", reduction);
+  if (schedule < SLF_SCHED_AUTO || schedule > SLF_SCHED_S) return fail(SLF_ERR_ARG, "schedule %d", schedule);
+  if ((dhidden && !aligned16(dhidden)) || (dweight && !aligned16(dweight)))
+    return fail(SLF_ERR_ALIGN, "gradient pointers must be 16-byte aligned");
+  std::lock_guard<std::mutex> hk(g_host_mu);
+  Ctx c;
+  SLF_TRY(setup(c, N, H, V, budget_bytes, workspace, workspace_bytes, stream, schedule, true));
+  c.acc_dw = (flags & SLF_FLAG_ACCUMULATE_DW) != 0;
+  DevInfo& d = *c.dev;
+  if (!d.copy_stream) SLF_CUDA(cudaStreamCreateWithFlags(&d.copy_stream, cudaStreamNonBlocking));
+  const size_t row_bytes = (size_t)H * 2;
+  const uint8_t* hh = reinterpret_cast<const uint8_t*>(hidden_host);
+  uint8_t* hd = reinterpret_cast<uint8_t*>(hidden_dev);
+  SLF_CUDA(cudaMemcpyAsync(targets_dev, targets_host, (size_t)N * 4, cudaMemcpyHostToDevice, c.s));
+  std::vector<SChunk> chunks;
+  if (c.plan.sched == SLF_SCHED_S) chunks = s_chunks(c.plan, N, H, dhidden != nullptr, reinterpret_cast<uint8_t*>(dhidden));
+  if (chunks.empty()) {  // schedule R: everything up front, in stream order
+    SLF_CUDA(cudaMemcpyAsync(hd, hh, (size_t)N * row_bytes, cudaMemcpyHostToDevice, c.s));
+  } else {
+    while (d.copy_events.size() < chunks.size() + 1) {
+      cudaEvent_t e;
+      SLF_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+      d.copy_events.push_back(e);
+    }
+    // the staging buffer may still be read by work already on `stream` (the previous step)
+    SLF_CUDA(cudaEventRecord(d.copy_events[chunks.size()], c.s));
+    c.enqueue_inputs = [&]() -> slf_status {
+      SLF_CUDA(cudaStreamWaitEvent(d.copy_stream, d.copy_events[chunks.size()], 0));
+      for (size_t i = 0; i < chunks.size(); ++i) {
+        const size_t off = (size_t)chunks[i].r0 * row_bytes;
+        SLF_CUDA(cudaMemcpyAsync(hd + off, hh + off, (size_t)chunks[i].rows * row_bytes, cudaMemcpyHostToDevice,
+                                 d.copy_stream));
+        SLF_CUDA(cudaEventRecord(d.copy_events[i], d.copy_stream));
+      }
+      return SLF_OK;
+    };
+    c.chunk_ready = d.copy_events.data();
+  }
+  if (c.plan.sched == SLF_SCHED_S) {
+    SLF_TRY(phase_s(c, hidden_dev, weight, targets_dev, N, H, V, ignore_index, reduction, scale, loss_dev, dhidden,
+                    dweight));
+  } else {
+    slf_shardstat* st = reinterpret_cast<slf_shardstat*>(c.ws + c.plan.off_shard);
+    slf_rowstat* rs = reinterpret_cast<slf_rowstat*>(c.ws + c.plan.off_rowstat);
+    SLF_TRY(phase_stats(c, hidden_dev, weight, targets_dev, N, H, V, 0, ignore_index, st));
+    SLF_TRY(phase_combine(c, st, 1, targets_dev, N, 0, V, V, ignore_index, reduction, scale, loss_dev, rs));
+    SLF_TRY(phase_backward(c, hidden_dev, weight, rs, N, H, V, 1.0f, dhidden, 0, dweight));
+  }
+  SLF_CUDA(cudaMemcpyAsync(loss_host, loss_dev, (reduction == SLF_NONE ? (size_t)N : 1) * 4, cudaMemcpyDeviceToHost,
+                           c.s));
   return SLF_OK;
 }
 

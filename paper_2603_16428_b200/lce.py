@@ -90,6 +90,50 @@ def lce_fwd_bwd(hidden, weight, targets, ignore_index: int = -100, reduction: st
     return (loss if reduction == "none" else loss[0]), dX, dW
 
 
+class HostStaging:
+    """Device staging buffers for lce_fwd_bwd_host (hidden [N, H] bf16, targets [N] int32, loss)."""
+
+    def __init__(self, N: int, H: int, device, reduction: str = "mean"):
+        self.hidden = torch.empty(N, H, dtype=torch.bfloat16, device=device)
+        self.targets = torch.empty(N, dtype=torch.int32, device=device)
+        self.loss = torch.empty(N if reduction == "none" else 1, dtype=torch.float32, device=device)
+
+
+def lce_fwd_bwd_host(hidden_host, weight, targets_host, ignore_index: int = -100, reduction: str = "mean",
+                     scale: float = 1.0, dX=None, dW=None, loss_host=None, staging: HostStaging = None,
+                     workspace=None, budget_bytes: int = 0, schedule: str = "auto", accumulate_dw: bool = False):
+    """The fused call with HOST hidden states / targets / loss (slf_lce_fwd_bwd_host): the row chunks
+    of hidden are copied on an internal stream while earlier chunks compute.  hidden_host: CPU bf16
+    [N, H] (pin it for overlap), targets_host: CPU int32 [N].  Returns (loss_host (valid after the
+    current stream synchronises), dX, dW) — gradients stay on the device."""
+    if hidden_host.is_cuda or targets_host.is_cuda:
+        raise TypeError("hidden_host / targets_host must be CPU tensors")
+    if hidden_host.dtype != torch.bfloat16 or targets_host.dtype != torch.int32:
+        raise TypeError("hidden_host must be bf16, targets_host int32")
+    if not (hidden_host.is_contiguous() and targets_host.is_contiguous()):
+        raise ValueError("host tensors must be contiguous")
+    N, H = hidden_host.shape
+    V = weight.shape[0]
+    dev = weight.device
+    if staging is None:
+        staging = HostStaging(N, H, dev, reduction)
+    if loss_host is None:
+        loss_host = torch.empty(N if reduction == "none" else 1, dtype=torch.float32).pin_memory()
+    if dX is None:
+        dX = torch.empty(N, H, dtype=torch.bfloat16, device=dev)
+    if dW is None and not accumulate_dw:
+        dW = torch.empty_like(weight)
+    if workspace is None:
+        workspace = alloc_workspace(N, H, V, dev, schedule, budget_bytes)
+    check(lib().slf_lce_fwd_bwd_host(hidden_host.data_ptr(), weight.data_ptr(), targets_host.data_ptr(), N, H, V,
+                                     ignore_index, REDUCTIONS[reduction], float(scale), loss_host.data_ptr(),
+                                     _ptr(dX), _ptr(dW), staging.hidden.data_ptr(), staging.targets.data_ptr(),
+                                     staging.loss.data_ptr(), workspace.data_ptr(), workspace.numel(),
+                                     SCHEDULES[schedule], budget_bytes, int(bool(accumulate_dw)), _stream_ptr(dev)),
+          "slf_lce_fwd_bwd_host")
+    return loss_host, dX, dW
+
+
 def lce_fwd(hidden, weight, targets, ignore_index: int = -100, reduction: str = "mean", scale: float = 1.0,
             budget_bytes: int = 0, workspace=None):
     """Forward half (schedule R split).  Returns (loss, rowstat [N, 16 bytes as uint8])."""

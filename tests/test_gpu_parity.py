@@ -380,6 +380,29 @@ def test_token_sharded_module_world1(slf, red):
         dist.destroy_process_group()
 
 
+@pytest.mark.parametrize("sched,red,pin", [("S", "mean", True), ("S", "none", False), ("R", "sum", True)])
+def test_host_input_call_matches_device_call(slf, sched, red, pin):
+    """slf_lce_fwd_bwd_host (host hidden/targets/loss, chunked copies overlapping the GEMMs) gives
+    bit-identical results to the device call on the same inputs (same plan, same kernels)."""
+    inp = synth.make_inputs(1100, 256, 3000, seed=23, alpha=4.0, dist="zipf")
+    X, W, t = to_dev(inp, torch)
+    budget = 2 << 20
+    loss_d, dX_d, dW_d = slf.lce_fwd_bwd(X, W, t, reduction=red, scale=0.5, budget_bytes=budget, schedule=sched)
+    Xh, th = X.cpu(), t.cpu()
+    if pin:
+        Xh, th = Xh.pin_memory(), th.pin_memory()
+    loss_h, dX_h, dW_h = slf.lce_fwd_bwd_host(Xh, W, th, reduction=red, scale=0.5, budget_bytes=budget,
+                                              schedule=sched)
+    torch.cuda.synchronize()
+    assert torch.equal(loss_h, loss_d.reshape(-1).cpu())
+    assert torch.equal(dX_h, dX_d) and torch.equal(dW_h, dW_d)
+    # a second call reuses the staging buffers after the first has finished reading them
+    loss_h2, dX_h2, _ = slf.lce_fwd_bwd_host(Xh, W, th, reduction=red, scale=0.5, budget_bytes=budget,
+                                             schedule=sched)
+    torch.cuda.synchronize()
+    assert torch.equal(loss_h2, loss_h) and torch.equal(dX_h2, dX_h)
+
+
 # ---- final RMSNorm + LCE (SURVEY §8(f) NEXT-1) ---------------------------------------------------
 @pytest.mark.parametrize("sched", SCHEDS)
 @pytest.mark.parametrize("N,H,V", [(300, 256, 3000), (1000, 520, 4100)])
