@@ -167,6 +167,8 @@ def main():
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--budget", type=int, default=0, help="workspace budget bytes (0 = 5%% of N*V*2)")
     ap.add_argument("--schedule", default="auto", choices=["auto", "R", "S"])
+    ap.add_argument("--module", action="store_true",
+                    help="run the multi-GPU module path (NCCL process group) even at world size 1 (testing)")
     ap.add_argument("--parallel", default="vocab", choices=["vocab", "dp"],
                     help="N>1: vocab-sharded W (north star) or token-sharded data parallel (full W per GPU)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -178,6 +180,12 @@ def main():
         run_reference(args)
         return
 
+    # The JSON line is the only thing this process writes to stdout: libraries that print to the C
+    # stdout (e.g. NCCL's version banner) are sent to stderr for the rest of the run.
+    json_out = os.fdopen(os.dup(1), "w")
+    sys.stdout.flush()
+    os.dup2(2, 1)
+
     import torch
     import torch.distributed as dist
 
@@ -188,14 +196,17 @@ def main():
     local = int(os.environ.get("LOCAL_RANK", "0"))
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
-    if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+    multi = world > 1 or args.module  # the multi-GPU code path (also at world size 1 with --module)
+    if multi:
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        os.environ.setdefault("MASTER_PORT", "29547")
+        dist.init_process_group("nccl", device_id=dev, rank=rank, world_size=world)
     g = world
 
     c = synth.CONFIGS[args.config]
     N, H, V = c["N"], c["H"], c["V"]
     inp = synth.make_inputs(N, H, V, seed=args.seed, alpha=args.alpha, dist=args.dist)
-    dp = g > 1 and args.parallel == "dp"
+    dp = multi and args.parallel == "dp"
     v0, v1 = (0, V) if dp else (V * rank // g, V * (rank + 1) // g)
     n0, n1 = (N * rank // g, N * (rank + 1) // g) if dp else (0, N)
     V_l = v1 - v0
@@ -205,18 +216,18 @@ def main():
     t = torch.from_numpy(inp.t[n0:n1]).to(dev)
     n_valid_global = int((inp.t != -100).sum())  # known when the batch is built (DP mean denominator)
 
-    if g > 1 and args.budget == 0 and not dp:
+    if multi and args.budget == 0 and not dp:
         # Sharded runs: 5% of the GLOBAL N*V*2 logits per GPU (SURVEY q7 "lenient" reading; both
         # ratios are reported in "memory").
         args.budget = int(0.05 * N * V * 2)
     ws_budget = args.budget
-    if g > 1 and not dp:
+    if multi and not dp:
         from paper_2603_16428_b200.sharded import VocabShardedLCE
         sharded = VocabShardedLCE(V, budget_bytes=args.budget, schedule="R" if args.schedule == "R" else "S")
         assert (sharded.v0, sharded.v1) == (v0, v1)
         if sharded.schedule == "S":  # the workspace shares the budget with the module's dX buffers
             ws_budget = sharded.s_workspace_budget(N, H)
-    ws = slf.alloc_workspace(N_l, H, V_l, dev, schedule="S" if (g > 1 and not dp and sharded.schedule == "S")
+    ws = slf.alloc_workspace(N_l, H, V_l, dev, schedule="S" if (multi and not dp and sharded.schedule == "S")
                              else args.schedule, budget_bytes=ws_budget)
     loss = torch.empty(1, dtype=torch.float32, device=dev)
     dX = torch.empty(N_l, H, dtype=torch.bfloat16, device=dev)
@@ -225,7 +236,7 @@ def main():
     if dp:
         from paper_2603_16428_b200.sharded import TokenShardedLCE
         dpm = TokenShardedLCE(budget_bytes=args.budget, schedule=args.schedule)
-    elif g > 1:
+    elif multi:
         if sharded.schedule == "S":
             C_s, _ = slf.s_plan(N, H, V_l, ws_budget)
             extra += 2 * C_s * H * 4 + (g + 1) * C_s * 16  # double-buffered fp32 dX partials + statistics
@@ -233,7 +244,7 @@ def main():
             extra += g * N * 16 + N * H * 4  # gathered statistics + fp32 dX partial
 
     def step(Xs=X, ts=t):
-        if g == 1:
+        if not multi:
             slf.lce_fwd_bwd(Xs, W, ts, out=(loss, dX, dW), workspace=ws, budget_bytes=args.budget,
                             schedule=args.schedule)
             return loss
@@ -245,7 +256,7 @@ def main():
         return l
 
     def barrier():
-        if g > 1:
+        if multi:
             dist.barrier(device_ids=[local])
 
     for _ in range(args.warmup):
@@ -279,7 +290,7 @@ def main():
             step()
         torch.cuda.synchronize()
     barrier()
-    if g > 1:
+    if multi:
         tt = torch.tensor([ms], dtype=torch.float64, device=dev)
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         ms = float(tt.item())
@@ -296,10 +307,10 @@ def main():
         lh = torch.empty(1, dtype=torch.float32).pin_memory()
         Xd = torch.empty_like(X)
         td = torch.empty_like(t)
-        stg = slf.HostStaging(N_l, H, dev) if g == 1 else None
+        stg = slf.HostStaging(N_l, H, dev) if not multi else None
 
         def e2e_step():
-            if g == 1:
+            if not multi:
                 slf.lce_fwd_bwd_host(Xh, W, th, dX=dX, dW=dW, loss_host=lh, staging=stg, workspace=ws,
                                      budget_bytes=args.budget, schedule=args.schedule)
             else:
@@ -322,7 +333,7 @@ def main():
         f1.record(stream)
         torch.cuda.synchronize()
         ems = f0.elapsed_time(f1) / args.steps
-        if g > 1:
+        if multi:
             tt = torch.tensor([ems], dtype=torch.float64, device=dev)
             dist.all_reduce(tt, op=dist.ReduceOp.MAX)
             ems = float(tt.item())
@@ -330,7 +341,7 @@ def main():
                "h2d_bytes_per_step": int(X.numel() * 2 + t.numel() * 4), "d2h_bytes_per_step": 4}
 
     if rank != 0:
-        if g > 1:
+        if multi:
             dist.destroy_process_group()
         return
 
@@ -358,11 +369,11 @@ def main():
     out = {
         "metric": METRIC, "value": N / (ms / 1e3), "unit": UNIT, "n_gpus": g, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
-        "scaling": "strong" if g > 1 else "weak", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
+        "scaling": "strong" if multi else "weak", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
         "config": {"workload": f"{args.config} LM head N={N} H={H} V={V}", "N": N, "H": H, "V": V,
                    "V_per_gpu": V_l, "N_per_gpu": N_l,
                    "parallelism": (f"token-sharded data parallel x{g}" if dp else f"vocab-sharded x{g}")
-                   if g > 1 else "single GPU",
+                   if multi else "single GPU",
                    "targets": args.dist, "logit_std": args.alpha, "ignore_frac": 0.05,
                    "l2": "inputs larger than L2 (W alone is %.2f GB vs 126 MB L2); no flush" % (V_l * H * 2 / 1e9),
                    "plan": slf.plan_describe(N_l, H, V_l, budget_bytes=ws_budget,
@@ -382,8 +393,8 @@ def main():
     }
     if g == 1 and not args.no_cpu_baseline:
         out["cpu_baseline"] = cpu_baseline(inp, args.config)
-    print(json.dumps(out), flush=True)
-    if g > 1:
+    print(json.dumps(out), file=json_out, flush=True)
+    if multi:
         dist.destroy_process_group()
 
 
