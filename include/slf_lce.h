@@ -121,7 +121,10 @@ slf_status slf_lce_plan_describe(int64_t N, int64_t H, int64_t V_local, int sche
  *   dweight  [V, H] bf16 (may be NULL to skip)             (overwritten)
  *   workspace, workspace_bytes: >= slf_lce_workspace_bytes(N,H,V,schedule,budget)
  * Gradients are those of scale*loss (SUM/MEAN) or of scale*sum_i l_i (NONE).
- * Rows with t_i == ignore_index get dhidden rows of exactly +0.0. */
+ * Rows with t_i == ignore_index get dhidden rows of exactly +0.0.
+ * Under schedule S the rows of dhidden that are not written yet also serve as stash scratch
+ * (extended row chunks): dhidden must not alias hidden, weight or the workspace,
+ * and its contents before the call are irrelevant. */
 slf_status slf_lce_fwd_bwd(const void* hidden, const void* weight, const int32_t* targets, int64_t N, int64_t H,
                            int64_t V, int32_t ignore_index, int reduction, float scale, float* loss_out,
                            void* dhidden, void* dweight, void* workspace, size_t workspace_bytes, int schedule,
