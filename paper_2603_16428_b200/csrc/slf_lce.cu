@@ -1106,11 +1106,31 @@ slf_status slf_lce_fwd_bwd(const void* hidden, const void* weight, const int32_t
                             dweight, workspace, workspace_bytes, schedule, budget_bytes, 0u, stream);
 }
 
+bool overlaps(const void* a, size_t na, const void* b, size_t nb) {
+  if (!a || !b) return false;
+  const uintptr_t x = reinterpret_cast<uintptr_t>(a), y = reinterpret_cast<uintptr_t>(b);
+  return x < y + nb && y < x + na;
+}
+
+// Outputs must not alias the inputs or the workspace (dhidden's unwritten rows are stash scratch).
+slf_status check_outputs(const void* hidden, const void* weight, int64_t N, int64_t H, int64_t V, const void* dhidden,
+                         const void* dweight, const void* workspace, size_t workspace_bytes) {
+  const size_t xb = (size_t)N * H * 2, wb = (size_t)V * H * 2;
+  if (overlaps(dhidden, xb, hidden, xb) || overlaps(dhidden, xb, weight, wb) ||
+      overlaps(dhidden, xb, workspace, workspace_bytes) || overlaps(dhidden, xb, dweight, wb))
+    return fail(SLF_ERR_ARG, "dhidden overlaps hidden, weight, dweight or the workspace");
+  if (overlaps(dweight, wb, hidden, xb) || overlaps(dweight, wb, weight, wb) ||
+      overlaps(dweight, wb, workspace, workspace_bytes))
+    return fail(SLF_ERR_ARG, "dweight overlaps hidden, weight or the workspace");
+  return SLF_OK;
+}
+
 slf_status slf_lce_fwd_bwd_ex(const void* hidden, const void* weight, const int32_t* targets, int64_t N, int64_t H,
                               int64_t V, int32_t ignore_index, int reduction, float scale, float* loss_out,
                               void* dhidden, void* dweight, void* workspace, size_t workspace_bytes, int schedule,
                               size_t budget_bytes, uint32_t flags, void* stream) {
   SLF_TRY(check_common(hidden, weight, targets, N, H, V, workspace));
+  SLF_TRY(check_outputs(hidden, weight, N, H, V, dhidden, dweight, workspace, workspace_bytes));
   if (flags & ~(uint32_t)SLF_FLAG_ACCUMULATE_DW) return fail(SLF_ERR_ARG, "unknown flags 0x%x", flags);
   if (!loss_out) return fail(SLF_ERR_ARG, "null loss_out");
   if (reduction < SLF_SUM || reduction > SLF_NONE) return fail(SLF_ERR_ARG, "bad reduction %d", reduction);
@@ -1140,6 +1160,7 @@ slf_status slf_lce_fwd_bwd_host(const void* hidden_host, const void* weight, con
                                 int schedule, size_t budget_bytes, uint32_t flags, void* stream) {
   if (!hidden_host || !targets_host || !loss_host) return fail(SLF_ERR_ARG, "null host pointer");
   SLF_TRY(check_common(hidden_dev, weight, targets_dev, N, H, V, workspace));
+  SLF_TRY(check_outputs(hidden_dev, weight, N, H, V, dhidden, dweight, workspace, workspace_bytes));
   if (flags & ~(uint32_t)SLF_FLAG_ACCUMULATE_DW) return fail(SLF_ERR_ARG, "unknown flags 0x%x", flags);
   if (!loss_dev || !aligned16(loss_dev)) return fail(SLF_ERR_ALIGN, "loss_dev must be a 16-byte aligned pointer");
   if (reduction < SLF_SUM || reduction > SLF_NONE) return fail(SLF_ERR_ARG, "bad reduction %d", reduction);

@@ -95,3 +95,19 @@ def test_sharded_planner(L):
         V_l = (128256 + g - 1) // g
         ws = lce.workspace_bytes(16384, 4096, V_l, budget_bytes=int(0.05 * 16384 * 128256 * 2))
         assert ws > 0
+
+
+def test_output_aliasing_rejected(L):
+    """dhidden / dweight overlapping the inputs or the workspace is an argument error, reported before
+    any device work (host-side check; fake 16-byte aligned addresses are never dereferenced)."""
+    from paper_2603_16428_b200 import _lib
+    lib = _lib.lib()
+    N, H, V = 512, 64, 1000
+    X, W, T, WS = 1 << 32, 2 << 32, 3 << 32, 4 << 32
+    ws_bytes = 1 << 24
+    loss = 5 << 32
+    base = (X, W, T, N, H, V, -100, 1, 1.0, loss)
+    for dX, dW in ((X + 1024, 6 << 32), (7 << 32, W), (WS + 4096, 6 << 32), (7 << 32, WS), (7 << 32, X)):
+        st = lib.slf_lce_fwd_bwd_ex(*base, dX, dW, WS, ws_bytes, 0, 0, 0, None)
+        assert _lib.STATUS_NAMES.get(st) == "SLF_ERR_ARG", (dX, dW, st)
+        assert b"overlaps" in lib.slf_last_error_string()
