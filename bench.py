@@ -167,6 +167,8 @@ def main():
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--budget", type=int, default=0, help="workspace budget bytes (0 = 5%% of N*V*2)")
     ap.add_argument("--schedule", default="auto", choices=["auto", "R", "S"])
+    ap.add_argument("--emulate-shards", type=int, default=0,
+                    help="with --module at world size 1: time rank 0's vocab shard of G GPUs (no exchange)")
     ap.add_argument("--module", action="store_true",
                     help="run the multi-GPU module path (NCCL process group) even at world size 1 (testing)")
     ap.add_argument("--parallel", default="vocab", choices=["vocab", "dp"],
@@ -207,7 +209,8 @@ def main():
     N, H, V = c["N"], c["H"], c["V"]
     inp = synth.make_inputs(N, H, V, seed=args.seed, alpha=args.alpha, dist=args.dist)
     dp = multi and args.parallel == "dp"
-    v0, v1 = (0, V) if dp else (V * rank // g, V * (rank + 1) // g)
+    G = args.emulate_shards if (args.emulate_shards and world == 1 and args.module and not dp) else g
+    v0, v1 = (0, V) if dp else (V * rank // G, V * (rank + 1) // G)
     n0, n1 = (N * rank // g, N * (rank + 1) // g) if dp else (0, N)
     V_l = v1 - v0
     N_l = n1 - n0
@@ -223,7 +226,8 @@ def main():
     ws_budget = args.budget
     if multi and not dp:
         from paper_2603_16428_b200.sharded import VocabShardedLCE
-        sharded = VocabShardedLCE(V, budget_bytes=args.budget, schedule="R" if args.schedule == "R" else "S")
+        sharded = VocabShardedLCE(V, budget_bytes=args.budget, schedule="R" if args.schedule == "R" else "S",
+                                  emulate_shard=(G, 0) if G != g else None)
         assert (sharded.v0, sharded.v1) == (v0, v1)
         if sharded.schedule == "S":  # the workspace shares the budget with the module's dX buffers
             ws_budget = sharded.s_workspace_budget(N, H)

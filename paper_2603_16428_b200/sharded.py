@@ -46,14 +46,23 @@ def cuda_ops():
 class VocabShardedLCE:
     """Fused LCE with the LM head split by vocabulary rows across the ranks of `group`."""
 
-    def __init__(self, V_global: int, group=None, ops=None, budget_bytes: int = 0, schedule: str = "S"):
+    def __init__(self, V_global: int, group=None, ops=None, budget_bytes: int = 0, schedule: str = "S",
+                 emulate_shard=None):
+        """emulate_shard=(G, r): timing only — compute shard r of G vocab shards while the collectives
+        run over the actual group (world size 1: a single rank's per-GPU work at G GPUs, without the
+        exchange; the loss and dhidden are then those of the shard alone)."""
         import torch.distributed as dist
         self.dist = dist
         self.group = group
         self.g = dist.get_world_size(group)
         self.rank = dist.get_rank(group)
         self.V = V_global
-        self.v0, self.v1 = shard_bounds(V_global, self.g, self.rank)
+        if emulate_shard is not None:
+            self.v0, self.v1 = shard_bounds(V_global, *emulate_shard)
+            self.g_budget = emulate_shard[0]
+        else:
+            self.v0, self.v1 = shard_bounds(V_global, self.g, self.rank)
+            self.g_budget = self.g
         self.ops = ops or cuda_ops()
         self.budget = budget_bytes
         if schedule not in ("S", "R"):
@@ -75,7 +84,7 @@ class VocabShardedLCE:
             if ws == 0:
                 return None
             C, _n = lce.s_plan(N, H, V_l, b)
-            return ws + 2 * C * H * 4 + (self.g + 1) * C * 16
+            return ws + 2 * C * H * 4 + (self.g_budget + 1) * C * 16
 
         lo, hi = 0, total  # largest planner budget whose total need fits (bisection; need grows with b)
         for _ in range(40):
