@@ -111,3 +111,20 @@ def test_output_aliasing_rejected(L):
         st = lib.slf_lce_fwd_bwd_ex(*base, dX, dW, WS, ws_bytes, 0, 0, 0, None)
         assert _lib.STATUS_NAMES.get(st) == "SLF_ERR_ARG", (dX, dW, st)
         assert b"overlaps" in lib.slf_last_error_string()
+
+
+def test_sharded_s_budget_covers_module_buffers(L):
+    """VocabShardedLCE (schedule S): workspace + double-buffered fp32 dX partials + gathered
+    statistics stay within 5 % of the global logits at every shard count (host-side planner only)."""
+    from paper_2603_16428_b200 import lce
+    from paper_2603_16428_b200.sharded import VocabShardedLCE, shard_bounds
+    N, H, V = 16384, 4096, 128256
+    for g in (2, 4, 8):
+        m = VocabShardedLCE.__new__(VocabShardedLCE)  # no process group needed for the planner
+        m.g = m.g_budget = g
+        m.V, m.budget = V, 0
+        m.v0, m.v1 = shard_bounds(V, g, 0)
+        b = m.s_workspace_budget(N, H)
+        C, _ = lce.s_plan(N, H, m.v1 - m.v0, b)
+        total = lce.workspace_bytes(N, H, m.v1 - m.v0, "S", b) + 2 * C * H * 4 + (g + 1) * C * 16
+        assert C >= 256 and total <= 0.05 * N * V * 2, (g, C, total)
