@@ -895,7 +895,8 @@ slf_status s_chunk_bwd(Ctx& c, const SArgs& a, const SChunk& k, const slf_shards
   const Plan& p = c.plan;
   const int64_t r0 = k.r0, rows = k.rows;
   const int tiles_v = (int)((a.V_l + BN - 1) / BN);
-  {
+  static const bool skip_ct = getenv("SLF_DEBUG_EPI") && (atoi(getenv("SLF_DEBUG_EPI")) & 512);  // timing only
+  if (!skip_ct) {
     ProfScope ps(SLF_PROF_COMBINE_TRANSFORM, c.s, 0.0, (double)rows * (tiles_v * 8.0 + a.V_l * 4.0 + 16.0 * g + 24));
     // Programmatic dependent launch: blocks start while the stash GEMM drains and wait in-kernel.
     cudaLaunchConfig_t cfg = {};
