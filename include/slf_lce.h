@@ -58,6 +58,7 @@ typedef int slf_status;
 #define SLF_ERR_CUDA 4          /* CUDA launch / driver error              */
 #define SLF_ERR_UNSUPPORTED 5   /* not an sm_100 device                    */
 #define SLF_ERR_UNIMPLEMENTED 6 /* requested schedule not built yet        */
+#define SLF_ERR_COMM 7          /* collective transport (NCCL / callback)  */
 
 typedef enum { SLF_SUM = 0, SLF_MEAN = 1, SLF_NONE = 2 } slf_reduction;
 
@@ -237,6 +238,70 @@ slf_status slf_lce_s_end(const void* hidden, int64_t N, int64_t H, int64_t V_loc
 /* DEVICE pointer (in *out) to the step's RowStat array [N] inside `workspace` (schedule S). */
 slf_status slf_lce_s_rowstat(int64_t N, int64_t H, int64_t V_local, size_t budget_bytes, void* workspace,
                              const slf_rowstat** out);
+
+/* ---- vocab-sharded LCE in one call, collectives inside the library (SURVEY §8(b) "Comm", §8(e)) ----
+ * BASELINE.json north_star: "the LM head is vocab-sharded (V/g rows per GPU): NCCL over NVLink
+ * all-reduces the per-token (max, sum-exp, target-logit) triples in forward and dhidden in backward,
+ * and dW stays local to its shard" — PAPER.md l.273's fused LCE split across the g GPUs of one box.
+ *
+ * A communicator (slf_comm) binds one process = one GPU = one rank.  Transports:
+ *   slf_comm_init:           NCCL (loaded at run time: the libnccl.so.2 already in the process,
+ *                            e.g. PyTorch's, else the system one; SLF_ERR_COMM if none).  Bootstrap:
+ *                            rank 0 calls slf_comm_get_unique_id (128 HOST bytes) and the caller
+ *                            ships them to every rank (e.g. torch.distributed broadcast).
+ *   slf_comm_init_callbacks: caller-provided collectives (tests: gloo through host copies).  The
+ *                            callbacks are invoked on the calling thread with the library's stream;
+ *                            they must leave the result visible to later work on that stream
+ *                            (e.g. synchronise it, copy, copy back) and return 0 on success.
+ * The communicator keeps one internal CUDA stream and four events (NCCL transport); it must be
+ * destroyed with slf_comm_destroy on the device it was created on.  Not thread-safe: one call at a
+ * time per communicator. */
+typedef struct slf_comm_s* slf_comm;
+/* recv[r * bytes_per_rank ...] = rank r's send[0 .. bytes_per_rank), r = 0..world-1 (DEVICE). */
+typedef int (*slf_allgather_fn)(const void* send, void* recv, size_t bytes_per_rank, void* stream, void* user);
+/* buf[0 .. count) fp32 (DEVICE) := elementwise sum over ranks, identical on every rank. */
+typedef int (*slf_allreduce_f32_fn)(void* buf, size_t count, void* stream, void* user);
+slf_status slf_comm_get_unique_id(void* id128);
+slf_status slf_comm_init(slf_comm* out, const void* id128, int rank, int world, int device);
+slf_status slf_comm_init_callbacks(slf_comm* out, int rank, int world, slf_allgather_fn allgather,
+                                   slf_allreduce_f32_fn allreduce, void* user);
+slf_status slf_comm_destroy(slf_comm comm);
+/* HOST *rank, *world of the communicator. */
+slf_status slf_comm_rank(slf_comm comm, int* rank, int* world);
+
+/* Rank k of g owns W rows [V_global*k/g, V_global*(k+1)/g) (contiguous, as even as possible). */
+slf_status slf_shard_bounds(int64_t V_global, int world, int rank, int64_t* vocab_start, int64_t* V_local);
+
+/* Workspace of slf_lce_fwd_bwd_sharded for rank `rank` of `world`: the schedule-S workspace plus
+ * two fp32 dX partials [C, H] (double-buffered so the all-reduce of chunk c overlaps chunk c+1)
+ * and the local / gathered per-row statistics (C*16 and world*C*16 bytes), all within
+ * `budget_bytes` (0: 5 % of the GLOBAL N*V_global*2 logits per GPU).  Host only;
+ * 0 if nothing fits. */
+size_t slf_lce_sharded_workspace_bytes(int64_t N, int64_t H, int64_t V_global, int world, int rank,
+                                       size_t budget_bytes);
+/* Writes the plan (chunk rows, chunks, planner budget, workspace bytes) into HOST `out`. */
+slf_status slf_lce_sharded_plan_describe(int64_t N, int64_t H, int64_t V_global, int world, int rank,
+                                         size_t budget_bytes, char* out, size_t cap);
+
+/* The whole vocab-sharded step on this rank (schedule S, per row chunk c):
+ *   stash GEMM + this shard's row statistics -> all-gather (16 B/row/rank, rank order)
+ *   -> shard-order merge, loss rows, in-place G_P, grouped dX-partial (fp32) / dW (+)= launch
+ *   -> all-reduce of the chunk's fp32 dX (comm stream, overlaps chunk c+1) -> bf16 dhidden rows;
+ *   after the chunks: one-hot dW correction (local targets) and the loss.
+ *   hidden [N, H] bf16, targets [N] int32: identical on every rank            (read)
+ *   weight_shard [V_local, H] bf16: this rank's rows (slf_shard_bounds)       (read)
+ *   loss_out DEVICE fp32 [1] (SUM/MEAN) or [N] (NONE): the global loss, every rank
+ *   dhidden [N, H] bf16: the full (all-reduced) gradient, every rank          (overwritten)
+ *   dweight_shard [V_local, H] bf16: this rank's rows of dW                   (overwritten)
+ *   workspace >= slf_lce_sharded_workspace_bytes(N, H, V_global, world, rank, budget_bytes)
+ * Every rank must make the same sequence of calls with the same N, H, V_global, ignore_index,
+ * reduction and budget.  Results are those of slf_lce_fwd_bwd on the whole W within the
+ * BASELINE tolerance (the shards' dX partials are summed in fp32).  Errors: SLF_ERR_COMM for a
+ * transport failure (the other ranks may then block inside their collectives). */
+slf_status slf_lce_fwd_bwd_sharded(const void* hidden, const void* weight_shard, const int32_t* targets, int64_t N,
+                                   int64_t H, int64_t V_global, int32_t ignore_index, int reduction, float scale,
+                                   float* loss_out, void* dhidden, void* dweight_shard, void* workspace,
+                                   size_t workspace_bytes, size_t budget_bytes, slf_comm comm, void* stream);
 
 /* Debug: copy the per-tile clock64 trace recorded for the launch selected by the environment
  * variable SLF_DEBUG_TRACE=k (the k-th GEMM launch of the process) into HOST `host` (n values,

@@ -14,7 +14,7 @@ SO_PATH = os.path.join(HERE, "libslf_lce.so")
 
 SLF_OK = 0
 STATUS_NAMES = {0: "SLF_OK", 1: "SLF_ERR_ARG", 2: "SLF_ERR_ALIGN", 3: "SLF_ERR_WORKSPACE", 4: "SLF_ERR_CUDA",
-                5: "SLF_ERR_UNSUPPORTED", 6: "SLF_ERR_UNIMPLEMENTED"}
+                5: "SLF_ERR_UNSUPPORTED", 6: "SLF_ERR_UNIMPLEMENTED", 7: "SLF_ERR_COMM"}
 REDUCTIONS = {"sum": 0, "mean": 1, "none": 2}
 SCHEDULES = {"auto": 0, "R": 1, "S": 2}
 
@@ -25,7 +25,9 @@ EXPORTS = ["slf_lce_version", "slf_last_error_string", "slf_lce_workspace_bytes"
            "slf_lce_s_plan", "slf_lce_s_begin", "slf_lce_s_chunk_stats", "slf_lce_s_chunk_bwd", "slf_lce_s_end",
            "slf_lce_s_rowstat", "slf_rmsnorm_workspace_bytes", "slf_rmsnorm_fwd", "slf_rmsnorm_bwd",
            "slf_debug_trace_read", "slf_debug_max_active_clusters", "slf_lce_fwd_bwd_ex", "slf_scale_bf16",
-           "slf_lce_fwd_bwd_host"]
+           "slf_lce_fwd_bwd_host", "slf_comm_get_unique_id", "slf_comm_init", "slf_comm_init_callbacks",
+           "slf_comm_destroy", "slf_comm_rank", "slf_shard_bounds", "slf_lce_sharded_workspace_bytes",
+           "slf_lce_sharded_plan_describe", "slf_lce_fwd_bwd_sharded"]
 PROF_KINDS = ["gemm_stats", "gemm_grad", "gemm_dw", "gemm_dx", "gemm_debug", "prep", "local_combine", "final_combine",
               "dx_finalize", "gemm_group", "combine_transform", "csr", "onehot", "loss_reduce", "rmsnorm", "k15"]
 
@@ -38,6 +40,11 @@ I32 = ctypes.c_int32
 INT = ctypes.c_int
 F32 = ctypes.c_float
 SZ = ctypes.c_size_t
+
+
+# slf_allgather_fn / slf_allreduce_f32_fn (include/slf_lce.h)
+ALLGATHER_FN = ctypes.CFUNCTYPE(INT, P, P, SZ, P, P)
+ALLREDUCE_FN = ctypes.CFUNCTYPE(INT, P, SZ, P, P)
 
 
 class SlfError(RuntimeError):
@@ -77,6 +84,15 @@ def _declare(lib):
         "slf_debug_max_active_clusters": (INT, [INT, ctypes.POINTER(INT)]),
         "slf_rmsnorm_fwd": (INT, [P, P, I64, I64, F32, P, P, P]),
         "slf_rmsnorm_bwd": (INT, [P, P, P, P, I64, I64, P, P, P, SZ, P]),
+        "slf_comm_get_unique_id": (INT, [P]),
+        "slf_comm_init": (INT, [ctypes.POINTER(P), P, INT, INT, INT]),
+        "slf_comm_init_callbacks": (INT, [ctypes.POINTER(P), INT, INT, ALLGATHER_FN, ALLREDUCE_FN, P]),
+        "slf_comm_destroy": (INT, [P]),
+        "slf_comm_rank": (INT, [P, ctypes.POINTER(INT), ctypes.POINTER(INT)]),
+        "slf_shard_bounds": (INT, [I64, INT, INT, ctypes.POINTER(I64), ctypes.POINTER(I64)]),
+        "slf_lce_sharded_workspace_bytes": (SZ, [I64, I64, I64, INT, INT, SZ]),
+        "slf_lce_sharded_plan_describe": (INT, [I64, I64, I64, INT, INT, SZ, ctypes.c_char_p, SZ]),
+        "slf_lce_fwd_bwd_sharded": (INT, [P, P, P, I64, I64, I64, I32, INT, F32, P, P, P, P, SZ, SZ, P, P]),
     }
     for name, (res, args) in sig.items():
         f = getattr(lib, name)

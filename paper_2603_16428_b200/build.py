@@ -9,7 +9,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 SO = os.path.join(HERE, "libslf_lce.so")
 SRC = os.path.join(HERE, "csrc", "slf_lce.cu")
-DEPS = [os.path.join(HERE, "csrc", f) for f in ("slf_lce.cu", "gemm.cuh", "aux_kernels.cuh", "s_kernels.cuh", "rmsnorm.cuh", "ptx.cuh")] + [
+DEPS = [os.path.join(HERE, "csrc", f) for f in ("slf_lce.cu", "gemm.cuh", "aux_kernels.cuh", "s_kernels.cuh", "rmsnorm.cuh", "ptx.cuh", "comm.cuh")] + [
     os.path.join(ROOT, "include", "slf_lce.h")]
 
 NVCC_FLAGS = [
@@ -37,7 +37,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
     if not force and up_to_date():
         return SO
     tmp = SO + ".tmp"
-    cmd = [nvcc(), *NVCC_FLAGS, "-o", tmp, SRC]
+    cmd = [nvcc(), *NVCC_FLAGS, "-o", tmp, SRC, "-ldl"]
     if verbose:
         print(" ".join(cmd), file=sys.stderr)
     subprocess.run(cmd, check=True)

@@ -21,6 +21,7 @@
 #include "gemm.cuh"
 #include "s_kernels.cuh"
 #include "rmsnorm.cuh"
+#include "comm.cuh"
 
 using namespace slf;
 
@@ -1055,6 +1056,176 @@ slf_status setup(Ctx& c, int64_t N, int64_t H, int64_t V_l, size_t budget, void*
   return SLF_OK;
 }
 
+
+// ---- vocab-sharded step with in-library collectives (slf_lce_fwd_bwd_sharded) ------
+void shard_bounds(int64_t V, int g, int k, int64_t* v0, int64_t* vl) {
+  const int64_t a = V * k / g, b = V * (k + 1) / g;
+  *v0 = a;
+  *vl = b - a;
+}
+
+// The rank's workspace: [ schedule-S workspace (planner budget b) | dX partial 0 | dX partial 1 |
+// local stats C*16 | gathered stats g*C*16 ], b the largest planner budget whose total fits.
+struct ShardPlan {
+  Plan p;
+  size_t b, off_dx0, off_dx1, off_st, off_all, total;
+  int64_t v0, V_l;
+};
+
+bool shard_layout(int64_t N, int64_t H, int64_t V_l, int g, size_t b, ShardPlan* sp) {
+  if (!plan_s(N, H, V_l, b, &sp->p)) return false;
+  const int64_t C = sp->p.C;
+  sp->b = b;
+  sp->off_dx0 = align_up(sp->p.total, 1024);
+  sp->off_dx1 = align_up(sp->off_dx0 + (size_t)C * H * 4, 1024);
+  sp->off_st = align_up(sp->off_dx1 + (size_t)C * H * 4, 1024);
+  sp->off_all = align_up(sp->off_st + (size_t)C * 16, 1024);
+  sp->total = sp->off_all + (size_t)g * C * 16;
+  return true;
+}
+
+bool shard_plan(int64_t N, int64_t H, int64_t Vg, int g, int k, size_t budget, ShardPlan* out) {
+  if (N < 1 || H < 8 || Vg < 1 || g < 1 || k < 0 || k >= g || Vg < g) return false;
+  int64_t v0, vl;
+  shard_bounds(Vg, g, k, &v0, &vl);
+  const size_t total = budget ? budget : default_budget(N, Vg);
+  size_t lo = 0, hi = total;  // bisection: the layout grows with the planner budget
+  ShardPlan sp;
+  while (lo < hi) {
+    const size_t mid = lo + (hi - lo + 1) / 2;
+    if (shard_layout(N, H, vl, g, mid, &sp) && sp.total <= total)
+      lo = mid;
+    else
+      hi = mid - 1;
+  }
+  if (!shard_layout(N, H, vl, g, lo, &sp) || sp.total > total) return false;
+  sp.v0 = v0;
+  sp.V_l = vl;
+  *out = sp;
+  return true;
+}
+
+slf_status comm_fail_nccl(ncclResult_t r, const char* what) {
+  NcclApi& api = nccl_api();
+  return fail(SLF_ERR_COMM, "%s: %s", what, api.GetErrorString ? api.GetErrorString(r) : "nccl error");
+}
+
+// All-gather of `bytes` per rank, the result visible to later work on s.
+slf_status comm_allgather(slf_comm cm, const void* send, void* recv, size_t bytes, cudaStream_t s) {
+  if (cm->world == 1) {
+    if (recv != send) SLF_CUDA(cudaMemcpyAsync(recv, send, bytes, cudaMemcpyDeviceToDevice, s));
+    if (!cm->nccl && !cm->cb_allgather) return SLF_OK;
+  }
+  if (cm->cb_allgather) {
+    if (cm->cb_allgather(send, recv, bytes, s, cm->cb_user) != 0) return fail(SLF_ERR_COMM, "allgather callback failed");
+    return SLF_OK;
+  }
+  NcclApi& api = nccl_api();
+  SLF_CUDA(cudaEventRecord(cm->ev_in, s));
+  SLF_CUDA(cudaStreamWaitEvent(cm->cs, cm->ev_in, 0));
+  const ncclResult_t r = api.AllGather(send, recv, bytes, ncclUint8, cm->nccl, cm->cs);
+  if (r != ncclSuccess) return comm_fail_nccl(r, "ncclAllGather");
+  SLF_CUDA(cudaEventRecord(cm->ev_ag, cm->cs));
+  SLF_CUDA(cudaStreamWaitEvent(s, cm->ev_ag, 0));
+  return SLF_OK;
+}
+
+// In-place fp32 sum all-reduce of buf[count], started after the work on s so far; completion is
+// joined to s by comm_join(slot).
+slf_status comm_allreduce_start(slf_comm cm, float* buf, size_t count, int slot, cudaStream_t s) {
+  if (cm->cb_allreduce) {
+    if (cm->cb_allreduce(buf, count, s, cm->cb_user) != 0) return fail(SLF_ERR_COMM, "allreduce callback failed");
+    return SLF_OK;
+  }
+  if (!cm->nccl) return SLF_OK;  // world 1 without a transport: the partial is the sum
+  NcclApi& api = nccl_api();
+  SLF_CUDA(cudaEventRecord(cm->ev_in, s));
+  SLF_CUDA(cudaStreamWaitEvent(cm->cs, cm->ev_in, 0));
+  const ncclResult_t r = api.AllReduce(buf, buf, count, ncclFloat32, ncclSum, cm->nccl, cm->cs);
+  if (r != ncclSuccess) return comm_fail_nccl(r, "ncclAllReduce");
+  SLF_CUDA(cudaEventRecord(cm->ev_ar[slot], cm->cs));
+  return SLF_OK;
+}
+
+slf_status comm_join(slf_comm cm, int slot, cudaStream_t s) {
+  if (cm->nccl && !cm->cb_allreduce) SLF_CUDA(cudaStreamWaitEvent(s, cm->ev_ar[slot], 0));
+  return SLF_OK;
+}
+
+slf_status dx_finalize_rows(Ctx& c, const float* dx32, const slf_rowstat* rs, void* out, int64_t rows, int64_t H) {
+  const int64_t groups = rows * H / 8;
+  const int blocks = (int)std::min<int64_t>((groups + 255) / 256, (int64_t)c.dev->sms * 8);
+  ProfScope ps(SLF_PROF_DX_FINALIZE, c.s, 0.0, (double)rows * H * 6 + rows * 16.0);
+  dx_finalize_kernel<<<blocks, 256, 0, c.s>>>(dx32, rs, reinterpret_cast<uint16_t*>(out), rows, H);
+  SLF_CUDA(cudaGetLastError());
+  return SLF_OK;
+}
+
+// Per chunk: stash GEMM + local stats -> all-gather -> merge/transform + grouped dX-partial/dW
+// launch -> async fp32 all-reduce of the chunk's dX (double-buffered; joined two chunks later, so
+// it overlaps the next chunk's stash GEMM) -> bf16 rows.  Mirrors sharded.VocabShardedLCE (S).
+slf_status phase_sharded(Ctx& c, const ShardPlan& sp, slf_comm cm, const void* X, const void* W, const int32_t* t,
+                         int64_t N, int64_t H, int64_t Vg, int32_t ign, int reduction, float scale, float* loss_out,
+                         void* dX, void* dW) {
+  const Plan& p = c.plan;
+  const int g = cm->world;
+  const SArgs a{X, W, t, N, H, sp.V_l, sp.v0, Vg, ign};
+  float* dxb[2] = {reinterpret_cast<float*>(c.ws + sp.off_dx0), reinterpret_cast<float*>(c.ws + sp.off_dx1)};
+  slf_shardstat* st = reinterpret_cast<slf_shardstat*>(c.ws + sp.off_st);
+  slf_shardstat* st_all = reinterpret_cast<slf_shardstat*>(c.ws + sp.off_all);
+  const slf_rowstat* rs = reinterpret_cast<const slf_rowstat*>(c.ws + p.off_rowstat);
+  SLF_TRY(s_begin(c, a, dW != nullptr));
+  std::vector<SChunk> chunks;
+  for (int64_t ch = 0; ch < p.nCh; ++ch) chunks.push_back(s_plain_chunk(p, N, ch));
+  // LPT tables per chunk shape (full chunks and the tail), uploaded once per call
+  SchedArena arena;
+  int tab[2] = {-1, -1};
+  if (dX || dW) {
+    for (int j = 0; j < 2 && j < (int)chunks.size(); ++j) {
+      SChunk rep = j == 0 ? chunks[0] : chunks.back();
+      if (j == 1 && rep.rows == chunks[0].rows) { tab[1] = tab[0]; break; }
+      rep.index = std::max<int64_t>(rep.index, 1);
+      ProbSpec ps[2];
+      int n = 0;
+      SLF_TRY(s_build_bwd(c, a, rep, dX ? dxb[0] : nullptr, 1, dW, ps, &n));
+      tab[j] = arena.add(ps, n, c.dev->sms / cta_group());
+    }
+    if (arena.fits(c))
+      SLF_TRY(arena.upload(c));
+    else
+      tab[0] = tab[1] = -1;
+  }
+  float* loss_rows = s_loss_rows(c, reduction, loss_out);
+  int64_t pending[2] = {-1, -1};
+  auto finish = [&](int slot) -> slf_status {
+    const SChunk& k = chunks[pending[slot]];
+    SLF_TRY(comm_join(cm, slot, c.s));
+    SLF_TRY(dx_finalize_rows(c, dxb[slot], rs + k.r0, reinterpret_cast<uint8_t*>(dX) + (size_t)k.r0 * H * 2, k.rows,
+                             H));
+    pending[slot] = -1;
+    return SLF_OK;
+  };
+  for (size_t i = 0; i < chunks.size(); ++i) {
+    const SChunk& k = chunks[i];
+    const int slot = (int)(i & 1);
+    SLF_TRY(s_chunk_stats(c, a, k, st));
+    SLF_TRY(comm_allgather(cm, st, st_all, (size_t)k.rows * 16, c.s));
+    if (pending[slot] >= 0) SLF_TRY(finish(slot));
+    const int tb = (i + 1 == chunks.size() && k.rows != chunks[0].rows) ? tab[1] : tab[0];
+    SLF_TRY(s_chunk_bwd(c, a, k, st_all, g, reduction, scale, loss_rows, dX ? dxb[slot] : nullptr, 1, dW,
+                        tb >= 0 ? arena.dev(c, tb) : nullptr, tb >= 0 ? arena.tables[tb].second : 0));
+    if (dX) {
+      SLF_TRY(comm_allreduce_start(cm, dxb[slot], (size_t)k.rows * H, slot, c.s));
+      pending[slot] = (int64_t)i;
+    }
+  }
+  for (int j = 0; j < 2; ++j) {  // the older chunk first
+    const int slot = (int)((chunks.size() + j) & 1);
+    if (pending[slot] >= 0) SLF_TRY(finish(slot));
+  }
+  return s_end(c, a, reduction, scale, loss_out, dW);
+}
+
 }  // namespace
 
 // ---- C ABI ---------------------------------------------------------------------------------------
@@ -1362,6 +1533,139 @@ slf_status slf_lce_s_rowstat(int64_t N, int64_t H, int64_t V_local, size_t budge
   if (!plan_s(N, H, V_local, budget_bytes, &p)) return fail(SLF_ERR_WORKSPACE, "no schedule-S plan fits the budget");
   *out = reinterpret_cast<const slf_rowstat*>(reinterpret_cast<uint8_t*>(workspace) + p.off_rowstat);
   return SLF_OK;
+}
+
+// ---- communicator + vocab-sharded call ------------------------------------------------------------
+slf_status slf_comm_get_unique_id(void* id128) {
+  if (!id128) return fail(SLF_ERR_ARG, "null id buffer");
+  NcclApi& api = nccl_api();
+  if (!api.ok) return fail(SLF_ERR_COMM, "%s", api.why);
+  ncclUniqueId id;
+  const ncclResult_t r = api.GetUniqueId(&id);
+  if (r != ncclSuccess) return comm_fail_nccl(r, "ncclGetUniqueId");
+  static_assert(sizeof(ncclUniqueId) == 128, "ncclUniqueId is 128 bytes");
+  memcpy(id128, &id, 128);
+  return SLF_OK;
+}
+
+static slf_status comm_events(slf_comm_s* c) {
+  SLF_CUDA(cudaStreamCreateWithFlags(&c->cs, cudaStreamNonBlocking));
+  SLF_CUDA(cudaEventCreateWithFlags(&c->ev_in, cudaEventDisableTiming));
+  SLF_CUDA(cudaEventCreateWithFlags(&c->ev_ag, cudaEventDisableTiming));
+  for (auto& e : c->ev_ar) SLF_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  return SLF_OK;
+}
+
+slf_status slf_comm_init(slf_comm* out, const void* id128, int rank, int world, int device) {
+  if (!out || !id128) return fail(SLF_ERR_ARG, "null pointer");
+  if (world < 1 || rank < 0 || rank >= world) return fail(SLF_ERR_ARG, "rank %d of world %d", rank, world);
+  NcclApi& api = nccl_api();
+  if (!api.ok) return fail(SLF_ERR_COMM, "%s", api.why);
+  SLF_CUDA(cudaSetDevice(device));
+  slf_comm_s* c = new slf_comm_s;
+  c->rank = rank;
+  c->world = world;
+  c->device = device;
+  ncclUniqueId id;
+  memcpy(&id, id128, 128);
+  slf_status st = comm_events(c);
+  if (st == SLF_OK) {
+    const ncclResult_t r = api.CommInitRank(&c->nccl, world, id, rank);
+    if (r != ncclSuccess) st = comm_fail_nccl(r, "ncclCommInitRank");
+  }
+  if (st != SLF_OK) {
+    slf_comm_destroy(c);
+    return st;
+  }
+  *out = c;
+  return SLF_OK;
+}
+
+slf_status slf_comm_init_callbacks(slf_comm* out, int rank, int world, slf_allgather_fn allgather,
+                                   slf_allreduce_f32_fn allreduce, void* user) {
+  if (!out || !allgather || !allreduce) return fail(SLF_ERR_ARG, "null pointer");
+  if (world < 1 || rank < 0 || rank >= world) return fail(SLF_ERR_ARG, "rank %d of world %d", rank, world);
+  slf_comm_s* c = new slf_comm_s;
+  c->rank = rank;
+  c->world = world;
+  cudaGetDevice(&c->device);
+  c->cb_allgather = allgather;
+  c->cb_allreduce = allreduce;
+  c->cb_user = user;
+  *out = c;
+  return SLF_OK;
+}
+
+slf_status slf_comm_destroy(slf_comm c) {
+  if (!c) return SLF_OK;
+  slf_status st = SLF_OK;
+  if (c->nccl) {
+    const ncclResult_t r = nccl_api().CommDestroy(c->nccl);
+    if (r != ncclSuccess) st = comm_fail_nccl(r, "ncclCommDestroy");
+  }
+  if (c->cs) cudaStreamDestroy(c->cs);
+  for (cudaEvent_t e : {c->ev_in, c->ev_ag, c->ev_ar[0], c->ev_ar[1]})
+    if (e) cudaEventDestroy(e);
+  delete c;
+  return st;
+}
+
+slf_status slf_comm_rank(slf_comm c, int* rank, int* world) {
+  if (!c || !rank || !world) return fail(SLF_ERR_ARG, "null pointer");
+  *rank = c->rank;
+  *world = c->world;
+  return SLF_OK;
+}
+
+slf_status slf_shard_bounds(int64_t V_global, int world, int rank, int64_t* vocab_start, int64_t* V_local) {
+  if (!vocab_start || !V_local) return fail(SLF_ERR_ARG, "null output");
+  if (world < 1 || rank < 0 || rank >= world || V_global < world) return fail(SLF_ERR_ARG, "bad shard geometry");
+  shard_bounds(V_global, world, rank, vocab_start, V_local);
+  return SLF_OK;
+}
+
+size_t slf_lce_sharded_workspace_bytes(int64_t N, int64_t H, int64_t V_global, int world, int rank,
+                                       size_t budget_bytes) {
+  ShardPlan sp;
+  return shard_plan(N, H, V_global, world, rank, budget_bytes, &sp) ? sp.total : 0;
+}
+
+slf_status slf_lce_sharded_plan_describe(int64_t N, int64_t H, int64_t V_global, int world, int rank,
+                                         size_t budget_bytes, char* out, size_t cap) {
+  if (!out || cap == 0) return fail(SLF_ERR_ARG, "null output buffer");
+  ShardPlan sp;
+  if (!shard_plan(N, H, V_global, world, rank, budget_bytes, &sp)) return fail(SLF_ERR_WORKSPACE, "no plan fits");
+  snprintf(out, cap,
+           "schedule=S sharded world=%d rank=%d vocab_start=%lld V_local=%lld row_chunk=%lld n_chunks=%lld "
+           "planner_budget=%zu stash_bytes=%zu workspace=%zu",
+           world, rank, (long long)sp.v0, (long long)sp.V_l, (long long)sp.p.C, (long long)sp.p.nCh, sp.b,
+           (size_t)sp.p.C * sp.p.ld_stash * 2, sp.total);
+  return SLF_OK;
+}
+
+slf_status slf_lce_fwd_bwd_sharded(const void* hidden, const void* weight_shard, const int32_t* targets, int64_t N,
+                                   int64_t H, int64_t V_global, int32_t ignore_index, int reduction, float scale,
+                                   float* loss_out, void* dhidden, void* dweight_shard, void* workspace,
+                                   size_t workspace_bytes, size_t budget_bytes, slf_comm comm, void* stream) {
+  if (!comm) return fail(SLF_ERR_ARG, "null communicator");
+  if (V_global < comm->world) return fail(SLF_ERR_ARG, "V_global %lld < world %d", (long long)V_global, comm->world);
+  int64_t v0, vl;
+  shard_bounds(V_global, comm->world, comm->rank, &v0, &vl);
+  SLF_TRY(check_common(hidden, weight_shard, targets, N, H, vl, workspace));
+  SLF_TRY(check_outputs(hidden, weight_shard, N, H, vl, dhidden, dweight_shard, workspace, workspace_bytes));
+  if (!loss_out || !aligned16(loss_out)) return fail(SLF_ERR_ALIGN, "loss_out must be a 16-byte aligned pointer");
+  if (reduction < SLF_SUM || reduction > SLF_NONE) return fail(SLF_ERR_ARG, "bad reduction %d", reduction);
+  if ((dhidden && !aligned16(dhidden)) || (dweight_shard && !aligned16(dweight_shard)))
+    return fail(SLF_ERR_ALIGN, "gradient pointers must be 16-byte aligned");
+  ShardPlan sp;
+  if (!shard_plan(N, H, V_global, comm->world, comm->rank, budget_bytes, &sp))
+    return fail(SLF_ERR_WORKSPACE, "no sharded schedule-S plan fits the budget");
+  if (workspace_bytes < sp.total)
+    return fail(SLF_ERR_WORKSPACE, "workspace %zu bytes < required %zu", workspace_bytes, sp.total);
+  Ctx c;
+  SLF_TRY(setup(c, N, H, vl, sp.b, workspace, sp.p.total, stream, SLF_SCHED_S, true));
+  return phase_sharded(c, sp, comm, hidden, weight_shard, targets, N, H, V_global, ignore_index, reduction, scale,
+                       loss_out, dhidden, dweight_shard);
 }
 
 // Debug: how many clusters of `cluster` CTAs of the GEMM kernel (its smem footprint) fit at once.

@@ -343,6 +343,124 @@ def dx_finalize_ptr(dx32, rowstat_ptr: int, out):
     return out
 
 
+# ---- vocab-sharded call with the collectives inside the library (include/slf_lce.h "Comm") ---------
+def comm_unique_id() -> bytes:
+    """128-byte NCCL bootstrap id (rank 0 creates it; ship it to every rank)."""
+    buf = ctypes.create_string_buffer(128)
+    check(lib().slf_comm_get_unique_id(buf), "slf_comm_get_unique_id")
+    return buf.raw
+
+
+class Comm:
+    """slf_comm handle: one process = one GPU = one rank of the vocab-sharded LM head."""
+
+    def __init__(self, handle, rank: int, world: int, keep=None):
+        self.handle, self.rank, self.world = handle, rank, world
+        self._keep = keep  # ctypes callbacks must outlive the handle
+
+    @classmethod
+    def nccl(cls, unique_id: bytes, rank: int, world: int, device: int):
+        h = ctypes.c_void_p(0)
+        check(lib().slf_comm_init(ctypes.byref(h), ctypes.create_string_buffer(bytes(unique_id), 128), rank, world,
+                                  device), "slf_comm_init")
+        return cls(h.value, rank, world)
+
+    @classmethod
+    def from_process_group(cls, group=None, device=None):
+        """NCCL communicator over the ranks of a torch.distributed group (bootstrap id broadcast
+        from the group's first rank; torch is plumbing here, the collectives run in the library)."""
+        import torch.distributed as dist
+        rank, world = dist.get_rank(group), dist.get_world_size(group)
+        obj = [comm_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=dist.get_global_rank(group, 0) if group is not None else 0, group=group)
+        dev = torch.cuda.current_device() if device is None else int(device)
+        return cls.nccl(obj[0], rank, world, dev)
+
+    @classmethod
+    def callbacks(cls, rank: int, world: int, allgather, allreduce_f32):
+        """Caller transport: allgather(send_ptr, recv_ptr, bytes_per_rank, stream_ptr) and
+        allreduce_f32(buf_ptr, count, stream_ptr), device addresses; run synchronously."""
+        from ._lib import ALLGATHER_FN, ALLREDUCE_FN
+
+        def ag(send, recv, nbytes, stream, user):
+            try:
+                allgather(send, recv, nbytes, stream)
+                return 0
+            except Exception as e:  # noqa: BLE001 — reported as SLF_ERR_COMM
+                print(f"allgather callback failed: {e!r}")
+                return 1
+
+        def ar(buf, count, stream, user):
+            try:
+                allreduce_f32(buf, count, stream)
+                return 0
+            except Exception as e:  # noqa: BLE001
+                print(f"allreduce callback failed: {e!r}")
+                return 1
+
+        fa, fr = ALLGATHER_FN(ag), ALLREDUCE_FN(ar)
+        h = ctypes.c_void_p(0)
+        check(lib().slf_comm_init_callbacks(ctypes.byref(h), rank, world, fa, fr, None), "slf_comm_init_callbacks")
+        return cls(h.value, rank, world, keep=(fa, fr))
+
+    def close(self):
+        if self.handle:
+            check(lib().slf_comm_destroy(self.handle), "slf_comm_destroy")
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:  # noqa: BLE001 — interpreter shutdown
+            pass
+
+
+def shard_bounds_native(V_global: int, world: int, rank: int):
+    v0, vl = ctypes.c_int64(0), ctypes.c_int64(0)
+    check(lib().slf_shard_bounds(V_global, world, rank, ctypes.byref(v0), ctypes.byref(vl)), "slf_shard_bounds")
+    return v0.value, v0.value + vl.value
+
+
+def sharded_workspace_bytes(N: int, H: int, V_global: int, world: int, rank: int, budget_bytes: int = 0) -> int:
+    return int(lib().slf_lce_sharded_workspace_bytes(N, H, V_global, world, rank, budget_bytes))
+
+
+def sharded_plan_describe(N: int, H: int, V_global: int, world: int, rank: int, budget_bytes: int = 0) -> str:
+    buf = ctypes.create_string_buffer(512)
+    check(lib().slf_lce_sharded_plan_describe(N, H, V_global, world, rank, budget_bytes, buf, 512),
+          "slf_lce_sharded_plan_describe")
+    return buf.value.decode()
+
+
+def lce_fwd_bwd_sharded(hidden, weight_shard, targets, V_global: int, comm: Comm, ignore_index: int = -100,
+                        reduction: str = "mean", scale: float = 1.0, budget_bytes: int = 0, workspace=None,
+                        out=None, need_dhidden: bool = True, need_dweight: bool = True):
+    """Vocab-sharded fused LCE on this rank (slf_lce_fwd_bwd_sharded): every rank passes the same
+    hidden / targets and its own W rows; returns (global loss, full dhidden, this rank's dW rows)."""
+    hidden, weight_shard, targets = _prep(hidden, weight_shard, targets)
+    N, H = hidden.shape
+    v0, v1 = shard_bounds_native(V_global, comm.world, comm.rank)
+    if weight_shard.shape[0] != v1 - v0:
+        raise ValueError(f"rank {comm.rank} expects {v1 - v0} vocab rows, got {weight_shard.shape[0]}")
+    dev = hidden.device
+    if out is not None:
+        loss, dX, dW = out
+    else:
+        loss = torch.empty(N if reduction == "none" else 1, dtype=torch.float32, device=dev)
+        dX = torch.empty_like(hidden) if need_dhidden else None
+        dW = torch.empty_like(weight_shard) if need_dweight else None
+    if workspace is None:
+        nb = sharded_workspace_bytes(N, H, V_global, comm.world, comm.rank, budget_bytes)
+        if nb == 0:
+            raise RuntimeError(f"no sharded plan fits N={N} H={H} V={V_global} world={comm.world}")
+        workspace = torch.empty(nb, dtype=torch.uint8, device=dev)
+    check(lib().slf_lce_fwd_bwd_sharded(hidden.data_ptr(), weight_shard.data_ptr(), targets.data_ptr(), N, H,
+                                        V_global, ignore_index, REDUCTIONS[reduction], float(scale), loss.data_ptr(),
+                                        _ptr(dX), _ptr(dW), workspace.data_ptr(), workspace.numel(), budget_bytes,
+                                        comm.handle, _stream_ptr(dev)), "slf_lce_fwd_bwd_sharded")
+    return (loss if reduction == "none" else loss[0]), dX, dW
+
+
 class Profile:
     """Context manager over slf_profile_begin/end: per-kernel-kind device ms, launches, FLOPs, bytes."""
 

@@ -128,3 +128,47 @@ def test_sharded_s_budget_covers_module_buffers(L):
         C, _ = lce.s_plan(N, H, m.v1 - m.v0, b)
         total = lce.workspace_bytes(N, H, m.v1 - m.v0, "S", b) + 2 * C * H * 4 + (g + 1) * C * 16
         assert C >= 256 and total <= 0.05 * N * V * 2, (g, C, total)
+
+
+def test_native_sharded_planner(L):
+    """slf_lce_sharded_workspace_bytes: the native sharded call's whole workspace (schedule S +
+    double-buffered fp32 dX partials + local/gathered statistics) fits 5 % of the global logits for
+    every rank at g = 2/4/8 on every BASELINE head, and the shard bounds match the module's."""
+    from paper_2603_16428_b200 import lce
+    from paper_2603_16428_b200.sharded import shard_bounds
+    heads = [(16384, 4096, 128256), (32768, 3584, 152064), (65536, 8192, 128256), (65536, 12288, 32768)]
+    for N, H, V in heads:
+        for g in (2, 4, 8):
+            for r in range(g):
+                assert lce.shard_bounds_native(V, g, r) == shard_bounds(V, g, r)
+                ws = lce.sharded_workspace_bytes(N, H, V, g, r)
+                assert 0 < ws <= 0.05 * N * V * 2, (N, H, V, g, r, ws)
+            d = lce.sharded_plan_describe(N, H, V, g, 0)
+            C = int(d.split("row_chunk=")[1].split()[0])
+            assert C >= 256 and C % 256 == 0, d
+    # an explicit budget is honoured, and too small a budget is reported
+    assert 0 < lce.sharded_workspace_bytes(900, 256, 5000, 2, 1, 3 << 20) <= 3 << 20
+    assert lce.sharded_workspace_bytes(900, 256, 5000, 2, 1, 1 << 20) == 0
+
+
+def test_comm_host_api(L):
+    """Communicator handles without a GPU: callback transport init / rank / destroy; bad ranks are
+    argument errors; the NCCL bootstrap id is 128 bytes when libnccl.so.2 loads."""
+    import ctypes
+    from paper_2603_16428_b200 import _lib, lce
+    c = lce.Comm.callbacks(1, 3, lambda *a: None, lambda *a: None)
+    r, w = ctypes.c_int(-1), ctypes.c_int(-1)
+    _lib.check(L.slf_comm_rank(c.handle, ctypes.byref(r), ctypes.byref(w)), "slf_comm_rank")
+    assert (r.value, w.value) == (1, 3)
+    c.close()
+    h = ctypes.c_void_p(0)
+    f = _lib.ALLGATHER_FN(lambda *a: 0)
+    g = _lib.ALLREDUCE_FN(lambda *a: 0)
+    assert _lib.STATUS_NAMES[L.slf_comm_init_callbacks(ctypes.byref(h), 3, 3, f, g, None)] == "SLF_ERR_ARG"
+    assert _lib.STATUS_NAMES[L.slf_lce_fwd_bwd_sharded(*([16] * 3), 8, 8, 64, -100, 1, 1.0, *([16] * 4), 1 << 20,
+                                                       0, None, None)] == "SLF_ERR_ARG"  # null communicator
+    try:
+        uid = lce.comm_unique_id()
+    except _lib.SlfError as e:
+        pytest.skip(f"no NCCL here: {e}")
+    assert len(uid) == 128

@@ -507,3 +507,71 @@ def test_llama_full_size_dw_rows(slf):
     ref = G.T @ Xo                                               # dW rows vrows
     got = bf16_to_np64(dW[torch.from_numpy(vrows).cuda()])
     assert rel_max_err(got, ref) <= GRAD_TOL
+
+
+# ---- vocab-sharded call with in-library collectives (slf_lce_fwd_bwd_sharded) ---------------------
+@pytest.mark.parametrize("red,ign", [("mean", -100), ("none", -100), ("sum", 0)])
+def test_native_sharded_nccl_world1(slf, red, ign):
+    """The library's own NCCL communicator (dlopen'ed NCCL, comm stream + events) at world size 1:
+    the whole sharded orchestration runs, with 1-rank collectives."""
+    inp = synth.make_inputs(900, 256, 5000, seed=16, alpha=4.0, dist="zipf", ignore_index=ign)
+    X, W, t = to_dev(inp, torch)
+    comm = slf.Comm.nccl(slf.comm_unique_id(), 0, 1, torch.cuda.current_device())
+    try:
+        loss, dX, dW = slf.lce_fwd_bwd_sharded(X, W, t, 5000, comm, ignore_index=ign, reduction=red,
+                                               budget_bytes=6 << 20)
+        torch.cuda.synchronize()
+        assert "n_chunks=1 " not in slf.sharded_plan_describe(900, 256, 5000, 1, 0, 6 << 20)
+        # a second call on the same communicator (events / comm stream reused) is bit-identical
+        loss2, dX2, dW2 = slf.lce_fwd_bwd_sharded(X, W, t, 5000, comm, ignore_index=ign, reduction=red,
+                                                  budget_bytes=6 << 20)
+        torch.cuda.synchronize()
+    finally:
+        comm.close()
+    assert torch.equal(dX.view(torch.int16), dX2.view(torch.int16))
+    assert torch.equal(dW.view(torch.int16), dW2.view(torch.int16))
+    assert torch.equal(loss.view(-1), loss2.view(-1))
+    Xo, Wo, to = oracle_inputs(inp)
+    ref = oracle.lce(Xo, Wo, to, ignore_index=ign, reduction=red)
+    assert_loss_close(loss.detach().cpu().numpy(), ref["loss"], red)
+    assert rel_max_err(bf16_to_np64(dX), ref["dX"]) <= GRAD_TOL
+    assert rel_max_err(bf16_to_np64(dW), ref["dW"]) <= GRAD_TOL
+    assert np.all(dX.view(torch.int16).cpu().numpy()[inp.t == ign] == 0)
+
+
+@pytest.mark.parametrize("g,red,budget", [(2, "mean", 3 << 20), (3, "sum", 3 << 20), (2, "none", 4 << 20)])
+def test_native_sharded_callbacks(slf, tmp_path, g, red, budget):
+    """g ranks of the native sharded call as g processes on this GPU, collectives through a gloo
+    callback transport (tests/native_sharded_worker.py): every rank returns the same loss and
+    dhidden, the dW shards assemble the full dW, all against the oracle."""
+    import os
+    import socket
+    import subprocess
+    import sys
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    env = dict(os.environ, MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    worker = os.path.join(os.path.dirname(os.path.abspath(__file__)), "native_sharded_worker.py")
+    procs = [subprocess.Popen([sys.executable, worker, "--rank", str(r), "--world", str(g), "--out", str(tmp_path),
+                               "--budget", str(budget), "--reduction", red], env=env)
+             for r in range(g)]
+    for p in procs:
+        assert p.wait(timeout=600) == 0
+    res = [np.load(tmp_path / f"rank{r}.npz") for r in range(g)]
+    inp = synth.make_inputs(900, 256, 5000, seed=21, alpha=4.0, dist="zipf")
+    Xo, Wo, to = oracle_inputs(inp)
+    ref = oracle.lce(Xo, Wo, to, reduction=red)
+    nch = int(str(res[0]["plan"]).split("n_chunks=")[1].split()[0])
+    assert nch > 1
+    for r in res:
+        assert int(r["ag"]) == nch and int(r["ar"]) == nch
+        assert np.array_equal(r["loss"], res[0]["loss"]) and np.array_equal(r["dX"], res[0]["dX"])
+    assert_loss_close(res[0]["loss"] if red == "none" else res[0]["loss"][0], ref["loss"], red)
+    tobf = lambda a: a.astype(np.int16).view(np.uint16).astype(np.uint32) << 16  # noqa: E731
+    dX = tobf(res[0]["dX"]).view(np.float32).astype(np.float64)
+    dW = np.concatenate([tobf(r["dW"]).view(np.float32).astype(np.float64) for r in res])
+    assert [int(r["v0"]) for r in res] + [int(res[-1]["v1"])] == [5000 * k // g for k in range(g + 1)]
+    assert rel_max_err(dX, ref["dX"]) <= GRAD_TOL
+    assert rel_max_err(dW, ref["dW"]) <= GRAD_TOL
+    assert np.all(res[0]["dX"][inp.t == -100] == 0)
