@@ -567,7 +567,7 @@ def test_native_sharded_callbacks(slf, tmp_path, g, red, budget):
     for r in res:
         assert int(r["ag"]) == nch and int(r["ar"]) == nch
         assert np.array_equal(r["loss"], res[0]["loss"]) and np.array_equal(r["dX"], res[0]["dX"])
-    assert_loss_close(res[0]["loss"] if red == "none" else res[0]["loss"][0], ref["loss"], red)
+    assert_loss_close(res[0]["loss"] if red == "none" else float(res[0]["loss"].reshape(-1)[0]), ref["loss"], red)
     tobf = lambda a: a.astype(np.int16).view(np.uint16).astype(np.uint32) << 16  # noqa: E731
     dX = tobf(res[0]["dX"]).view(np.float32).astype(np.float64)
     dW = np.concatenate([tobf(r["dW"]).view(np.float32).astype(np.float64) for r in res])
