@@ -116,10 +116,19 @@ def cpu_cores():
     return th or len(os.sched_getaffinity(0))
 
 
+def oracle_rows_for(inp_X, W64, t, seconds: float, cap: int) -> int:
+    """Rows of a bounded oracle sample taking about `seconds`: the oracle has a fixed per-call cost
+    (its fp64 [V, H] dW), so fit time = a + b * rows from two sample sizes."""
+    t8 = oracle_sample_time(inp_X, W64, t, 8)
+    t32 = oracle_sample_time(inp_X, W64, t, 32)
+    b = max((t32 - t8) / 24, 1e-6)
+    a = max(t8 - 8 * b, 0.0)
+    return int(np.clip((seconds - a) / b, 8, cap))
+
+
 def cpu_baseline(inp, cfg_name, target_s=12.0):
     W64 = synth.bf16_bits_to_f64(inp.W)
-    t8 = oracle_sample_time(inp.X, W64, inp.t, 8)
-    rows = int(np.clip(8 * target_s / max(t8, 1e-3), 8, min(1024, inp.N)))
+    rows = oracle_rows_for(inp.X, W64, inp.t, target_s, min(2048, inp.N))
     dt = oracle_sample_time(inp.X, W64, inp.t, rows)
     return {"value": rows / dt, "unit": UNIT, "cores": cpu_cores(), "kind": "oracle",
             "sample": f"{rows} tokens of the {cfg_name} workload at full H={inp.H}, V={inp.V} (numpy fp64, "
@@ -134,8 +143,7 @@ def run_reference(args):
     c = synth.CONFIGS[args.config]
     inp = synth.make_inputs(min(c["N"], 2048), c["H"], c["V"], seed=args.seed, alpha=args.alpha, dist=args.dist)
     W64 = synth.bf16_bits_to_f64(inp.W)
-    t1 = oracle_sample_time(inp.X, W64, inp.t, 4)
-    rows = int(np.clip(4 * 3.0 / max(t1, 1e-3), 4, inp.N))  # ~3 s of CPU work per step
+    rows = oracle_rows_for(inp.X, W64, inp.t, 3.0, inp.N)  # ~3 s of CPU work per step
     for _ in range(args.warmup):
         oracle_sample_time(inp.X, W64, inp.t, rows)
     times = [oracle_sample_time(inp.X, W64, inp.t, rows) for _ in range(args.steps)]
@@ -173,6 +181,9 @@ def main():
                     help="run the multi-GPU module path (NCCL process group) even at world size 1 (testing)")
     ap.add_argument("--parallel", default="vocab", choices=["vocab", "dp"],
                     help="N>1: vocab-sharded W (north star) or token-sharded data parallel (full W per GPU)")
+    ap.add_argument("--comm", default="native", choices=["native", "torch"],
+                    help="vocab-sharded schedule S: collectives inside the library (slf_comm over NCCL, "
+                         "slf_lce_fwd_bwd_sharded) or orchestrated from Python over torch.distributed")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     args = ap.parse_args()
@@ -231,8 +242,13 @@ def main():
         assert (sharded.v0, sharded.v1) == (v0, v1)
         if sharded.schedule == "S":  # the workspace shares the budget with the module's dX buffers
             ws_budget = sharded.s_workspace_budget(N, H)
-    ws = slf.alloc_workspace(N_l, H, V_l, dev, schedule="S" if (multi and not dp and sharded.schedule == "S")
-                             else args.schedule, budget_bytes=ws_budget)
+    native = multi and not dp and sharded.schedule == "S" and args.comm == "native" and G == g
+    if native:  # the library runs the whole sharded step, collectives included (slf_lce_fwd_bwd_sharded)
+        comm = slf.Comm.from_process_group(device=local)
+        ws = torch.empty(slf.sharded_workspace_bytes(N, H, V, g, rank, args.budget), dtype=torch.uint8, device=dev)
+    else:
+        ws = slf.alloc_workspace(N_l, H, V_l, dev, schedule="S" if (multi and not dp and sharded.schedule == "S")
+                                 else args.schedule, budget_bytes=ws_budget)
     loss = torch.empty(1, dtype=torch.float32, device=dev)
     dX = torch.empty(N_l, H, dtype=torch.bfloat16, device=dev)
     dW = torch.empty(V_l, H, dtype=torch.bfloat16, device=dev)
@@ -240,7 +256,7 @@ def main():
     if dp:
         from paper_2603_16428_b200.sharded import TokenShardedLCE
         dpm = TokenShardedLCE(budget_bytes=args.budget, schedule=args.schedule)
-    elif multi:
+    elif multi and not native:
         if sharded.schedule == "S":
             C_s, _ = slf.s_plan(N, H, V_l, ws_budget)
             extra += 2 * C_s * H * 4 + (g + 1) * C_s * 16  # double-buffered fp32 dX partials + statistics
@@ -255,6 +271,10 @@ def main():
         if dp:
             l, _, _ = dpm.forward_backward(Xs, W, ts, n_valid_global=n_valid_global, workspace=ws,
                                            out=(loss, dX, dW))
+            return l
+        if native:
+            l, _, _ = slf.lce_fwd_bwd_sharded(Xs, W, ts, V, comm, workspace=ws, out=(loss, dX, dW),
+                                              budget_bytes=args.budget)
             return l
         l, _, _ = sharded.forward_backward(Xs, W, ts, workspace=ws, dW_out=dW, dX_out=dX)
         return l
@@ -346,6 +366,8 @@ def main():
 
     if rank != 0:
         if multi:
+            if native:
+                comm.close()
             dist.destroy_process_group()
         return
 
@@ -380,8 +402,10 @@ def main():
                    if multi else "single GPU",
                    "targets": args.dist, "logit_std": args.alpha, "ignore_frac": 0.05,
                    "l2": "inputs larger than L2 (W alone is %.2f GB vs 126 MB L2); no flush" % (V_l * H * 2 / 1e9),
-                   "plan": slf.plan_describe(N_l, H, V_l, budget_bytes=ws_budget,
-                                             schedule=args.schedule)},
+                   "plan": slf.sharded_plan_describe(N, H, V, g, rank, args.budget) if native else
+                   slf.plan_describe(N_l, H, V_l, budget_bytes=ws_budget, schedule=args.schedule),
+                   **({"comm": "native (slf_comm NCCL inside libslf_lce.so)" if native else
+                       "torch.distributed NCCL (Python orchestration)"} if multi and not dp else {})},
         "tflops": tflops, "frac_of_peak_burst": tflops / peaks["burst"],
         "frac_of_peak_sustained": tflops / peaks["sustained"],
         "roofline": {"bound": "tensor", "kernel": dom_name, "achieved": achieved, "peak": peaks["sustained"],
@@ -399,6 +423,8 @@ def main():
         out["cpu_baseline"] = cpu_baseline(inp, args.config)
     print(json.dumps(out), file=json_out, flush=True)
     if multi:
+        if native:
+            comm.close()
         dist.destroy_process_group()
 
 
