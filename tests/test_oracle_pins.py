@@ -310,3 +310,67 @@ def test_rmsnorm_torch_crosscheck():
     np.testing.assert_allclose(dx, xt.grad.numpy(), rtol=1e-9, atol=1e-12)
     np.testing.assert_allclose(dg, gt.grad.numpy(), rtol=1e-9, atol=1e-12)
     np.testing.assert_allclose(dW, Wt.grad.numpy(), rtol=1e-9, atol=1e-12)
+
+
+# ---- Layer-Adam oracle (oracle/adam_oracle.py) ------------------------------
+@pytest.mark.parametrize("adamw,wd", [(True, 0.0), (True, 0.1), (False, 0.05)])
+def test_adam_torch_crosscheck(adamw, wd):
+    """torch.optim.AdamW / Adam (float64, CPU) — an independent implementation of the same update —
+    over five steps with changing gradients and a gradient scale."""
+    torch = pytest.importorskip("torch")
+    rng = np.random.default_rng(7)
+    p0 = rng.standard_normal(300)
+    grads = [rng.standard_normal(300) * 10.0 ** rng.uniform(-4, 0, 300) for _ in range(5)]
+    lr, b1, b2, eps, gs = 3e-3, 0.9, 0.95, 1e-8, 0.5
+    p, m, v, _ = oracle.adam_steps(p0, grads, lr, b1, b2, eps, wd, adamw, grad_scale=gs)
+    pt = torch.tensor(p0, requires_grad=True)
+    opt = (torch.optim.AdamW if adamw else torch.optim.Adam)([pt], lr=lr, betas=(b1, b2), eps=eps, weight_decay=wd)
+    for g in grads:
+        pt.grad = torch.tensor(g * gs)
+        opt.step()
+    np.testing.assert_allclose(p, pt.detach().numpy(), rtol=1e-13, atol=1e-15)
+    st = opt.state[pt]
+    np.testing.assert_allclose(m, st["exp_avg"].numpy(), rtol=1e-13, atol=1e-300)
+    np.testing.assert_allclose(v, st["exp_avg_sq"].numpy(), rtol=1e-13, atol=1e-300)
+
+
+def test_adam_first_step_closed_form():
+    """t = 1 from zero moments: m^ = g, v^ = g^2, so p1 = p0 - lr * g / (|g| + eps) (no decay)."""
+    rng = np.random.default_rng(8)
+    p0 = rng.standard_normal(64)
+    g = rng.standard_normal(64)
+    g[:4] = [0.0, 1e-9, -1e-9, 3.0]
+    lr, eps = 1e-2, 1e-8
+    p, _, _ = oracle.adam_step(p0, np.zeros(64), np.zeros(64), g, 1, lr, 0.9, 0.999, eps)
+    np.testing.assert_allclose(p, p0 - lr * g / (np.abs(g) + eps), rtol=0, atol=1e-15)
+
+
+def test_adam_zero_grad_pure_decay():
+    """g = 0 forever: moments stay 0, so AdamW only decays p by (1 - lr wd) per step; Adam-L2 with
+    g = 0 and p = 0 leaves everything at 0."""
+    p0 = np.linspace(-2, 2, 17)
+    lr, wd, T = 1e-2, 0.1, 7
+    p, m, v, _ = oracle.adam_steps(p0, [np.zeros(17)] * T, lr, wd=wd, adamw=True)
+    np.testing.assert_allclose(p, p0 * (1 - lr * wd) ** T, rtol=1e-14)
+    assert not m.any() and not v.any()
+    p2, _, _, _ = oracle.adam_steps(np.zeros(5), [np.zeros(5)] * 3, lr, wd=wd, adamw=False)
+    assert not p2.any()
+
+
+def test_adam_constant_gradient_limit():
+    """A constant gradient c: the bias-corrected moments are exactly c and c^2 at every t, so each
+    step moves p by lr * c / (|c| + eps) (sign descent at rate lr)."""
+    c = np.array([0.3, -2.0, 5e-3])
+    p0 = np.zeros(3)
+    lr, eps, T = 1e-3, 1e-8, 10
+    p, _, _, ups = oracle.adam_steps(p0, [c] * T, lr, 0.9, 0.999, eps)
+    np.testing.assert_allclose(p, -T * lr * c / (np.abs(c) + eps), rtol=1e-12)
+    assert all(u == pytest.approx(max(lr * np.abs(c) / (np.abs(c) + eps)), rel=1e-12) for u in ups)
+
+
+def test_bf16_rne_pins():
+    """RNE to bf16 on hand-picked values: ties to even, carries into the exponent, signs, NaN."""
+    vals = np.array([1.0, 1.0 + 2 ** -8, 1.0 + 3 * 2 ** -8, 1.0 + 2 ** -9, -1.0 - 2 ** -8, 255.5, np.nan,
+                     2.0 - 2 ** -9, 0.0])
+    want = [0x3F80, 0x3F80, 0x3F82, 0x3F80, 0xBF80, 0x4380, 0x7FC0, 0x4000, 0x0000]  # 255.5: tie -> 256 (even)
+    assert list(oracle.bf16_rne(vals)) == want
