@@ -27,7 +27,11 @@ EXPORTS = ["slf_lce_version", "slf_last_error_string", "slf_lce_workspace_bytes"
            "slf_debug_trace_read", "slf_debug_max_active_clusters", "slf_lce_fwd_bwd_ex", "slf_scale_bf16",
            "slf_lce_fwd_bwd_host", "slf_comm_get_unique_id", "slf_comm_init", "slf_comm_init_callbacks",
            "slf_comm_destroy", "slf_comm_rank", "slf_shard_bounds", "slf_lce_sharded_workspace_bytes",
-           "slf_lce_sharded_plan_describe", "slf_lce_fwd_bwd_sharded"]
+           "slf_lce_sharded_plan_describe", "slf_lce_fwd_bwd_sharded",
+           # include/slf_adam.h (Layer-Adam, host)
+           "slf_adam_last_error_string", "slf_adam_simd_width", "slf_adam_create", "slf_adam_destroy",
+           "slf_adam_set_config", "slf_adam_set_params", "slf_adam_get_state", "slf_adam_step_host",
+           "slf_adam_step_device_async", "slf_adam_wait"]
 PROF_KINDS = ["gemm_stats", "gemm_grad", "gemm_dw", "gemm_dx", "gemm_debug", "prep", "local_combine", "final_combine",
               "dx_finalize", "gemm_group", "combine_transform", "csr", "onehot", "loss_reduce", "rmsnorm", "k15"]
 
@@ -93,6 +97,16 @@ def _declare(lib):
         "slf_lce_sharded_workspace_bytes": (SZ, [I64, I64, I64, INT, INT, SZ]),
         "slf_lce_sharded_plan_describe": (INT, [I64, I64, I64, INT, INT, SZ, ctypes.c_char_p, SZ]),
         "slf_lce_fwd_bwd_sharded": (INT, [P, P, P, I64, I64, I64, I32, INT, F32, P, P, P, P, SZ, SZ, P, P]),
+        "slf_adam_last_error_string": (ctypes.c_char_p, []),
+        "slf_adam_simd_width": (INT, []),
+        "slf_adam_create": (INT, [ctypes.POINTER(P), I64, P]),
+        "slf_adam_destroy": (INT, [P]),
+        "slf_adam_set_config": (INT, [P, P]),
+        "slf_adam_set_params": (INT, [P, P, P]),
+        "slf_adam_get_state": (INT, [P, P, P, P, ctypes.POINTER(I64)]),
+        "slf_adam_step_host": (INT, [P, P, F32, P]),
+        "slf_adam_step_device_async": (INT, [P, P, F32, P, P]),
+        "slf_adam_wait": (INT, [P, P]),
     }
     for name, (res, args) in sig.items():
         f = getattr(lib, name)

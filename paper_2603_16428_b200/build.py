@@ -9,13 +9,14 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 SO = os.path.join(HERE, "libslf_lce.so")
 SRC = os.path.join(HERE, "csrc", "slf_lce.cu")
-DEPS = [os.path.join(HERE, "csrc", f) for f in ("slf_lce.cu", "gemm.cuh", "aux_kernels.cuh", "s_kernels.cuh", "rmsnorm.cuh", "ptx.cuh", "comm.cuh")] + [
-    os.path.join(ROOT, "include", "slf_lce.h")]
+SRC_HOST = os.path.join(HERE, "csrc", "layer_adam.cpp")  # Layer-Adam host optimizer (C++/OpenMP/AVX-512)
+DEPS = [os.path.join(HERE, "csrc", f) for f in ("slf_lce.cu", "gemm.cuh", "aux_kernels.cuh", "s_kernels.cuh", "rmsnorm.cuh", "ptx.cuh", "comm.cuh", "layer_adam.cpp")] + [
+    os.path.join(ROOT, "include", "slf_lce.h"), os.path.join(ROOT, "include", "slf_adam.h")]
 
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",
     "-O3", "-std=c++17", "-lineinfo",
-    "-Xcompiler", "-fPIC", "-shared",
+    "-Xcompiler", "-fPIC,-fopenmp,-ffp-contract=off", "-shared",
 ]
 
 
@@ -37,7 +38,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
     if not force and up_to_date():
         return SO
     tmp = SO + ".tmp"
-    cmd = [nvcc(), *NVCC_FLAGS, "-o", tmp, SRC, "-ldl"]
+    cmd = [nvcc(), *NVCC_FLAGS, "-o", tmp, SRC, SRC_HOST, "-ldl", "-lgomp"]
     if verbose:
         print(" ".join(cmd), file=sys.stderr)
     subprocess.run(cmd, check=True)

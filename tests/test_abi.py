@@ -17,7 +17,8 @@ def L():
 
 
 def header_functions():
-    src = open(os.path.join(ROOT, "include", "slf_lce.h")).read()
+    inc = os.path.join(ROOT, "include")
+    src = "".join(open(os.path.join(inc, f)).read() for f in sorted(os.listdir(inc)) if f.endswith(".h"))
     src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
     return sorted(set(re.findall(r"\b(slf_[a-z_0-9]+)\s*\(", src)))
 
