@@ -1,12 +1,12 @@
 """Layer-Adam measurement at an LM-head size: host-step throughput against
-the host's memory bandwidth, and the device-fed pipelined step (d2h of dW, CPU update, h2d of the
-bf16 W) against its three stages run back to back.  Prints one JSON line.
+the host's memory bandwidth (STREAM-style copy / add over all host threads, same run), and the
+device-fed pipelined step (d2h of dW, CPU update, h2d of the bf16 W) against its three stages run back to back.  Prints one JSON line.
 
     python tools/bench_adam.py --config llama8b --steps 3
 
 Algorithmic bytes per element of a host step: read bf16 g (2) + fp32 p, m, v (12), write p, m, v
-(12) + bf16 param copy (2) = 28 B.  The bandwidth denominator is a multi-threaded host copy
-(torch CPU copy_, read + write) of a buffer far larger than the caches, measured in the same run.
+(12) + bf16 param copy (2) = 28 B.  The bandwidth denominator is a STREAM-style copy / add split
+over all host threads on buffers far larger than the caches, measured in the same run.
 """
 import argparse
 import json
@@ -23,18 +23,32 @@ import synth  # noqa: E402
 from paper_2603_16428_b200.adam import LayerAdam, simd_width  # noqa: E402
 
 
-def host_copy_gbs(nbytes: int, reps: int = 3) -> float:
-    a = torch.empty(nbytes // 4, dtype=torch.float32)
-    a.fill_(1.0)
-    b = torch.empty_like(a)
-    b.copy_(a)
-    best = 0.0
-    for _ in range(reps):
-        t0 = time.perf_counter()
-        b.copy_(a)
-        dt = time.perf_counter() - t0
-        best = max(best, 2 * nbytes / dt / 1e9)
-    return best
+def host_stream_gbs(nbytes: int, reps: int = 3) -> dict:
+    """STREAM-style host bandwidth: copy (c = a) and add (c = a + b), each split over all host threads
+    (numpy releases the GIL on large slices).  DRAM bytes per second counting the write-allocate
+    read of c (plain stores, as in the Adam update, whose p, m, v stores hit lines it has just read):
+    copy moves 3 x nbytes, add 4 x nbytes."""
+    from concurrent.futures import ThreadPoolExecutor
+    import numpy as np
+    nt = len(os.sched_getaffinity(0))
+    n = nbytes // 4
+    a = np.ones(n, dtype=np.float32)
+    b = np.ones(n, dtype=np.float32)
+    c = np.zeros(n, dtype=np.float32)
+    cuts = [n * k // nt for k in range(nt + 1)]
+    sl = [slice(cuts[k], cuts[k + 1]) for k in range(nt)]
+    res = {}
+    with ThreadPoolExecutor(nt) as ex:
+        for name, fn, rw in (("copy", lambda s: np.copyto(c[s], a[s]), 3),
+                             ("add", lambda s: np.add(a[s], b[s], out=c[s]), 4)):
+            best = 0.0
+            for _ in range(reps + 1):
+                t0 = time.perf_counter()
+                list(ex.map(fn, sl))
+                best = max(best, rw * nbytes / (time.perf_counter() - t0) / 1e9)
+            res[name] = best
+    res["threads"] = nt
+    return res
 
 
 def main():
@@ -58,7 +72,7 @@ def main():
         opt.step_host(gh, 1.0, out)
         ts.append(time.perf_counter() - t0)
     t_host = min(ts)
-    bw = host_copy_gbs(min(4 << 30, n * 8))
+    bw = host_stream_gbs(min(4 << 30, n * 8))
 
     # device-fed pipelined step
     gd = gh.to(dev)
@@ -93,7 +107,8 @@ def main():
     print(json.dumps({
         "component": "Layer-Adam (host, SURVEY §8(f) NEXT-4)", "config": a.config, "elements": n,
         "simd_width": simd_width(), "threads": a.threads or torch.get_num_threads(),
-        "host_step_ms": t_host * 1e3, "host_step_gbs": gbs, "host_copy_gbs": bw, "frac_of_host_copy": gbs / bw,
+        "host_step_ms": t_host * 1e3, "host_step_gbs": gbs, "host_stream_gbs": bw,
+        "frac_of_host_stream": gbs / max(bw["copy"], bw["add"]),
         "algorithmic_bytes_per_elem": 28,
         "device_fed_step_ms": t_dev * 1e3,
         "stages_serial_ms": {"d2h": t_d2h * 1e3, "update": t_upd * 1e3, "h2d": t_h2d * 1e3,
