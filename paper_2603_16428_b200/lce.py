@@ -61,13 +61,25 @@ def alloc_workspace(N: int, H: int, V: int, device, schedule: str = "auto", budg
 
 def lce_fwd_bwd(hidden, weight, targets, ignore_index: int = -100, reduction: str = "mean", scale: float = 1.0,
                 need_dhidden: bool = True, need_dweight: bool = True, budget_bytes: int = 0, workspace=None,
-                out=None, schedule: str = "auto", accumulate_dw: bool = False):
+                out=None, schedule: str = "auto", accumulate_dw: bool = False, group=None, V_global: int = None):
     """Fused LCE forward + backward.  Returns (loss fp32, dhidden bf16 | None, dweight bf16 | None).
 
     ``out`` may be a (loss, dhidden, dweight) triple of preallocated tensors to write into;
     ``accumulate_dw`` adds dL/dW into the given dweight (gradient accumulation) instead of
-    overwriting it.
+    overwriting it.  With ``group`` (a torch.distributed process group, one rank per GPU) the LM
+    head is vocab-sharded (SURVEY §8(b) "Python"): ``weight`` is this rank's rows
+    [V_global*k/g, V_global*(k+1)/g) and the call is slf_lce_fwd_bwd_sharded over the library's
+    own NCCL communicator for the group (created once and cached); the loss and dhidden are the
+    global ones on every rank, dweight this rank's rows.
     """
+    if group is not None:
+        if V_global is None:
+            raise ValueError("a vocab-sharded call (group=...) needs V_global")
+        if accumulate_dw or schedule == "R":
+            raise NotImplementedError("the sharded call runs schedule S and overwrites dweight")
+        return lce_fwd_bwd_sharded(hidden, weight, targets, V_global, comm_for_group(group, hidden.device),
+                                   ignore_index, reduction, scale, budget_bytes, workspace, out, need_dhidden,
+                                   need_dweight)
     hidden, weight, targets = _prep(hidden, weight, targets)
     N, H = hidden.shape
     V = weight.shape[0]
@@ -413,6 +425,20 @@ class Comm:
             self.close()
         except Exception:  # noqa: BLE001 — interpreter shutdown
             pass
+
+
+_COMMS = {}
+
+
+def comm_for_group(group, device):
+    """The library communicator of a torch.distributed group on `device` (created on first use)."""
+    import torch.distributed as dist
+    key = (id(group), str(device))
+    c = _COMMS.get(key)
+    if c is None or c.handle is None:
+        c = Comm.from_process_group(None if group is dist.group.WORLD else group, device=device.index)
+        _COMMS[key] = c
+    return c
 
 
 def shard_bounds_native(V_global: int, world: int, rank: int):

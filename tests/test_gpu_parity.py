@@ -575,3 +575,30 @@ def test_native_sharded_callbacks(slf, tmp_path, g, red, budget):
     assert rel_max_err(dX, ref["dX"]) <= GRAD_TOL
     assert rel_max_err(dW, ref["dW"]) <= GRAD_TOL
     assert np.all(res[0]["dX"][inp.t == -100] == 0)
+
+
+def test_lce_fwd_bwd_group_world1(slf):
+    """slf.lce_fwd_bwd(..., group=WORLD, V_global=V): the SURVEY §8(b) Python form of the sharded
+    call, over the library's own NCCL communicator for the group (world size 1 here)."""
+    import os
+    import torch.distributed as dist
+    if not dist.is_initialized():
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        os.environ.setdefault("MASTER_PORT", "29541")
+        dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
+    try:
+        inp = synth.make_inputs(700, 256, 4100, seed=17, alpha=4.0, dist="zipf")
+        X, W, t = to_dev(inp, torch)
+        loss, dX, dW = slf.lce_fwd_bwd(X, W, t, group=dist.group.WORLD, V_global=4100, budget_bytes=6 << 20)
+        torch.cuda.synchronize()
+        Xo, Wo, to = oracle_inputs(inp)
+        ref = oracle.lce(Xo, Wo, to)
+        assert_loss_close(float(loss), ref["loss"], "mean")
+        assert rel_max_err(bf16_to_np64(dX), ref["dX"]) <= GRAD_TOL
+        assert rel_max_err(bf16_to_np64(dW), ref["dW"]) <= GRAD_TOL
+    finally:
+        from paper_2603_16428_b200 import lce as L
+        for c in L._COMMS.values():
+            c.close()
+        L._COMMS.clear()
+        dist.destroy_process_group()
