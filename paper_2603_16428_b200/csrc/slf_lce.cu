@@ -1084,21 +1084,33 @@ bool shard_layout(int64_t N, int64_t H, int64_t V_l, int g, size_t b, ShardPlan*
   return true;
 }
 
+// The largest planner budget whose layout fits `total` with a row chunk of at most c_cap (0: any).
+bool shard_fit(int64_t N, int64_t H, int64_t V_l, int g, size_t total, int64_t c_cap, ShardPlan* sp) {
+  auto ok = [&](size_t b) {
+    return shard_layout(N, H, V_l, g, b, sp) && sp->total <= total && (c_cap == 0 || sp->p.C <= c_cap);
+  };
+  size_t lo = 0, hi = total;  // bisection: the layout grows with the planner budget
+  while (lo < hi) {
+    const size_t mid = lo + (hi - lo + 1) / 2;
+    if (ok(mid))
+      lo = mid;
+    else
+      hi = mid - 1;
+  }
+  return ok(lo);
+}
+
+// Every rank must cut the same row chunks (the statistics are exchanged chunk by chunk), but shard
+// sizes differ by one row when g does not divide V: the chunk C is the one the LARGEST shard
+// (ceil(V/g) rows) fits, and each rank takes the largest planner budget giving exactly that C.
 bool shard_plan(int64_t N, int64_t H, int64_t Vg, int g, int k, size_t budget, ShardPlan* out) {
   if (N < 1 || H < 8 || Vg < 1 || g < 1 || k < 0 || k >= g || Vg < g) return false;
   int64_t v0, vl;
   shard_bounds(Vg, g, k, &v0, &vl);
   const size_t total = budget ? budget : default_budget(N, Vg);
-  size_t lo = 0, hi = total;  // bisection: the layout grows with the planner budget
-  ShardPlan sp;
-  while (lo < hi) {
-    const size_t mid = lo + (hi - lo + 1) / 2;
-    if (shard_layout(N, H, vl, g, mid, &sp) && sp.total <= total)
-      lo = mid;
-    else
-      hi = mid - 1;
-  }
-  if (!shard_layout(N, H, vl, g, lo, &sp) || sp.total > total) return false;
+  ShardPlan big, sp;
+  if (!shard_fit(N, H, (Vg + g - 1) / g, g, total, 0, &big)) return false;
+  if (!shard_fit(N, H, vl, g, total, big.p.C, &sp) || sp.p.C != big.p.C) return false;
   sp.v0 = v0;
   sp.V_l = vl;
   *out = sp;

@@ -75,28 +75,42 @@ class VocabShardedLCE:
         """Schedule S: the planner budget for this rank's workspace such that the workspace plus this
         module's per-chunk buffers (two fp32 dX partials [C, H], the gathered statistics g*C*16 B and
         the local ones C*16 B) stay within `budget_bytes` (0: 5 % of the global N*V*2 logits, the
-        lenient reading of SURVEY q7).  So the memory claim covers everything the step allocates."""
+        lenient reading of SURVEY q7).  So the memory claim covers everything the step allocates.
+        Every rank must cut the same row chunks, and shard sizes differ by one row when g does not
+        divide V: C is the one the largest shard (ceil(V/g) rows) fits, and this rank takes the
+        largest budget giving exactly that C."""
         from . import lce
         total = self.budget or int(0.05 * N * self.V * 2)
-        V_l = self.v1 - self.v0
-        def need(b):
+
+        def need(V_l, b):
             ws = lce.workspace_bytes(N, H, V_l, "S", b)
             if ws == 0:
-                return None
+                return None, 0
             C, _n = lce.s_plan(N, H, V_l, b)
-            return ws + 2 * C * H * 4 + (self.g_budget + 1) * C * 16
+            return ws + 2 * C * H * 4 + (self.g_budget + 1) * C * 16, C
 
-        lo, hi = 0, total  # largest planner budget whose total need fits (bisection; need grows with b)
-        for _ in range(40):
-            mid = (lo + hi + 1) // 2
-            nb = need(mid)
-            if nb is not None and nb <= total:
-                lo = mid
-            else:
-                hi = mid - 1
-        if need(lo) is None:
+        def fit(V_l, c_cap):  # largest planner budget whose total need fits (need grows with b)
+            def ok(b):
+                nb, C = need(V_l, b)
+                return nb is not None and nb <= total and (c_cap == 0 or C <= c_cap)
+            lo, hi = 0, total
+            while lo < hi:
+                mid = (lo + hi + 1) // 2
+                if ok(mid):
+                    lo = mid
+                else:
+                    hi = mid - 1
+            return lo if ok(lo) else None
+
+        v_big = -(-self.V // self.g_budget)
+        b_big = fit(v_big, 0)
+        if b_big is None:
             raise RuntimeError(f"no schedule-S plan fits {total} bytes with its dX buffers")
-        return lo
+        C_big = need(v_big, b_big)[1]
+        b = fit(self.v1 - self.v0, C_big)
+        if b is None or need(self.v1 - self.v0, b)[1] != C_big:
+            raise RuntimeError(f"rank {self.rank}: no plan with the common row chunk {C_big}")
+        return b
 
     def _buf(self, key, shape, dtype, device):
         import torch

@@ -173,3 +173,30 @@ def test_comm_host_api(L):
     except _lib.SlfError as e:
         pytest.skip(f"no NCCL here: {e}")
     assert len(uid) == 128
+
+
+@pytest.mark.parametrize("N,H,V,g,budget", [(8192, 512, 30001, 3, 13303808), (4096, 128, 7777, 4, 20054016),
+                                            (900, 256, 5000, 3, 3 << 20), (16384, 4096, 128257, 8, 0)])
+def test_sharded_ranks_share_row_chunks(L, N, H, V, g, budget):
+    """Every rank cuts the same row chunks (the statistics are exchanged chunk by chunk) although
+    shard sizes differ by one row when g does not divide V — the first two shapes made the ranks'
+    planners disagree before the common-chunk rule — in the native planner and in the Python module
+    (VocabShardedLCE.s_workspace_budget), both within the budget."""
+    from paper_2603_16428_b200 import lce
+    from paper_2603_16428_b200.sharded import VocabShardedLCE, shard_bounds
+    total = budget or int(0.05 * N * V * 2)
+    cs_native, cs_mod = [], []
+    for r in range(g):
+        d = lce.sharded_plan_describe(N, H, V, g, r, budget)
+        cs_native.append(int(d.split("row_chunk=")[1].split()[0]))
+        assert 0 < lce.sharded_workspace_bytes(N, H, V, g, r, budget) <= total
+        m = VocabShardedLCE.__new__(VocabShardedLCE)
+        m.g = m.g_budget = g
+        m.V, m.budget, m.rank = V, budget, r
+        m.v0, m.v1 = shard_bounds(V, g, r)
+        b = m.s_workspace_budget(N, H)
+        C, _ = lce.s_plan(N, H, m.v1 - m.v0, b)
+        cs_mod.append(C)
+        assert lce.workspace_bytes(N, H, m.v1 - m.v0, "S", b) + 2 * C * H * 4 + (g + 1) * C * 16 <= total
+    assert len(set(cs_native)) == 1, cs_native
+    assert len(set(cs_mod)) == 1, cs_mod
