@@ -268,6 +268,19 @@ slf_status slf_comm_init_callbacks(slf_comm* out, int rank, int world, slf_allga
 slf_status slf_comm_destroy(slf_comm comm);
 /* HOST *rank, *world of the communicator. */
 slf_status slf_comm_rank(slf_comm comm, int* rank, int* world);
+/* P2P one-shot all-gather of the per-chunk statistics (enable = 1), instead
+ * of the transport's all-gather.  At the next sharded call every rank allocates a receive buffer
+ * [256 B flags | 2 x world x C x 16 B] with cudaMalloc (communicator-owned, like NCCL's own
+ * buffers; freed by slf_comm_destroy or enable = 0), the CUDA IPC handles are exchanged through the
+ * transport and mapped (cudaIpcMemLazyEnablePeerAccess; NVLink peers, or other processes on the
+ * same GPU).  Per chunk one kernel stores the rank's statistics into slot `rank` of every rank's
+ * buffer and bumps a per-source counter there (system-scope release); the consumer waits on its own
+ * counters (acquire).  A wait that exceeds ~30 s gives up and counts a timeout instead of hanging.
+ * All ranks must set the same mode.  world <= 16. */
+slf_status slf_comm_set_p2p(slf_comm comm, int enable);
+/* Synchronising: HOST *p2p_timeouts = 1 if a P2P wait ever timed out on this rank (results of
+ * that call are invalid), else 0. */
+slf_status slf_comm_status(slf_comm comm, int32_t* p2p_timeouts);
 
 /* Rank k of g owns W rows [V_global*k/g, V_global*(k+1)/g) (contiguous, as even as possible). */
 slf_status slf_shard_bounds(int64_t V_global, int world, int rank, int64_t* vocab_start, int64_t* V_local);

@@ -27,7 +27,7 @@ EXPORTS = ["slf_lce_version", "slf_last_error_string", "slf_lce_workspace_bytes"
            "slf_debug_trace_read", "slf_debug_max_active_clusters", "slf_lce_fwd_bwd_ex", "slf_scale_bf16",
            "slf_lce_fwd_bwd_host", "slf_comm_get_unique_id", "slf_comm_init", "slf_comm_init_callbacks",
            "slf_comm_destroy", "slf_comm_rank", "slf_shard_bounds", "slf_lce_sharded_workspace_bytes",
-           "slf_lce_sharded_plan_describe", "slf_lce_fwd_bwd_sharded",
+           "slf_lce_sharded_plan_describe", "slf_lce_fwd_bwd_sharded", "slf_comm_set_p2p", "slf_comm_status",
            # include/slf_adam.h (Layer-Adam, host)
            "slf_adam_last_error_string", "slf_adam_simd_width", "slf_adam_create", "slf_adam_destroy",
            "slf_adam_set_config", "slf_adam_set_params", "slf_adam_get_state", "slf_adam_step_host",
@@ -93,6 +93,8 @@ def _declare(lib):
         "slf_comm_init_callbacks": (INT, [ctypes.POINTER(P), INT, INT, ALLGATHER_FN, ALLREDUCE_FN, P]),
         "slf_comm_destroy": (INT, [P]),
         "slf_comm_rank": (INT, [P, ctypes.POINTER(INT), ctypes.POINTER(INT)]),
+        "slf_comm_set_p2p": (INT, [P, INT]),
+        "slf_comm_status": (INT, [P, ctypes.POINTER(I32)]),
         "slf_shard_bounds": (INT, [I64, INT, INT, ctypes.POINTER(I64), ctypes.POINTER(I64)]),
         "slf_lce_sharded_workspace_bytes": (SZ, [I64, I64, I64, INT, INT, SZ]),
         "slf_lce_sharded_plan_describe": (INT, [I64, I64, I64, INT, INT, SZ, ctypes.c_char_p, SZ]),

@@ -1164,6 +1164,89 @@ slf_status comm_join(slf_comm cm, int slot, cudaStream_t s) {
   return SLF_OK;
 }
 
+void p2p_release(slf_comm cm) {
+  for (int r = 0; r < cm->world && r < P2P_MAX_RANKS; ++r)
+    if (cm->p2p_peer[r] && r != cm->rank) cudaIpcCloseMemHandle(cm->p2p_peer[r]);
+  if (cm->p2p_buf) cudaFree(cm->p2p_buf);
+  cm->p2p_buf = nullptr;
+  memset(cm->p2p_peer, 0, sizeof(cm->p2p_peer));
+  cm->p2p_rows = 0;
+  cm->epoch = 0;
+}
+
+size_t p2p_data_off(const slf_comm_s* cm, unsigned long long epoch) {
+  return P2P_HDR_BYTES + (size_t)(epoch & 1) * cm->world * cm->p2p_rows * 16;
+}
+
+// (Re)allocate this rank's receive buffer for `rows` rows per slot and map every peer's (a
+// collective: every rank reaches it at the same call, their chunk plans being identical).
+slf_status p2p_ensure(slf_comm cm, int64_t rows, cudaStream_t s) {
+  if (cm->p2p_buf && cm->p2p_rows >= rows) return SLF_OK;
+  if (cm->world > P2P_MAX_RANKS) return fail(SLF_ERR_ARG, "P2P statistics exchange supports <= %d ranks", P2P_MAX_RANKS);
+  SLF_CUDA(cudaStreamSynchronize(s));
+  p2p_release(cm);
+  cm->p2p_rows = rows;
+  const size_t bytes = P2P_HDR_BYTES + 2 * (size_t)cm->world * rows * 16;
+  SLF_CUDA(cudaMalloc(&cm->p2p_buf, bytes));
+  SLF_CUDA(cudaMemset(cm->p2p_buf, 0, bytes));
+  SLF_CUDA(cudaDeviceSynchronize());
+  cudaIpcMemHandle_t h;
+  SLF_CUDA(cudaIpcGetMemHandle(&h, cm->p2p_buf));
+  static_assert(sizeof(cudaIpcMemHandle_t) == 64, "IPC handle is 64 bytes");
+  uint8_t* dev = nullptr;  // the handles travel through the communicator's own all-gather
+  SLF_CUDA(cudaMalloc(&dev, 64 * (size_t)(cm->world + 1)));
+  std::vector<uint8_t> all((size_t)64 * cm->world);
+  slf_status st = SLF_OK;
+  if (cudaMemcpy(dev, &h, 64, cudaMemcpyHostToDevice) != cudaSuccess)
+    st = fail(SLF_ERR_CUDA, "handle upload failed");
+  if (st == SLF_OK) st = comm_allgather(cm, dev, dev + 64, 64, s);
+  if (st == SLF_OK && cudaStreamSynchronize(s) != cudaSuccess) st = fail(SLF_ERR_CUDA, "handle exchange failed");
+  if (st == SLF_OK && cudaMemcpy(all.data(), dev + 64, all.size(), cudaMemcpyDeviceToHost) != cudaSuccess)
+    st = fail(SLF_ERR_CUDA, "handle download failed");
+  cudaFree(dev);
+  for (int r = 0; st == SLF_OK && r < cm->world; ++r) {
+    if (r == cm->rank) {
+      cm->p2p_peer[r] = cm->p2p_buf;
+      continue;
+    }
+    cudaIpcMemHandle_t ph;
+    memcpy(&ph, all.data() + (size_t)64 * r, 64);
+    void* p = nullptr;
+    const cudaError_t e = cudaIpcOpenMemHandle(&p, ph, cudaIpcMemLazyEnablePeerAccess);
+    if (e != cudaSuccess) st = fail(SLF_ERR_COMM, "cudaIpcOpenMemHandle(rank %d): %s", r, cudaGetErrorString(e));
+    cm->p2p_peer[r] = static_cast<uint8_t*>(p);
+  }
+  if (st != SLF_OK) {
+    p2p_release(cm);
+    return st;
+  }
+  // every rank has mapped every buffer before anyone pushes into one
+  float* bar = nullptr;
+  SLF_CUDA(cudaMalloc(&bar, 16));
+  SLF_CUDA(cudaMemset(bar, 0, 16));
+  st = comm_allreduce_start(cm, bar, 4, 0, s);
+  if (st == SLF_OK) st = comm_join(cm, 0, s);
+  if (st == SLF_OK && cudaStreamSynchronize(s) != cudaSuccess) st = fail(SLF_ERR_CUDA, "barrier failed");
+  cudaFree(bar);
+  return st;
+}
+
+// One-shot all-gather of this chunk's statistics into every rank's buffer; returns (in *gathered)
+// the local [g][rows] view of this epoch.
+slf_status p2p_allgather_stats(slf_comm cm, const slf_shardstat* st, int64_t rows, cudaStream_t s,
+                               const slf_shardstat** gathered) {
+  const unsigned long long e = ++cm->epoch;
+  PeerPtrs pp{};
+  for (int r = 0; r < cm->world; ++r) pp.p[r] = cm->p2p_peer[r];
+  const size_t off = p2p_data_off(cm, e);
+  p2p_stats_push_kernel<<<cm->world, 256, 0, s>>>(reinterpret_cast<const uint4*>(st), (int)rows, cm->rank, pp, off);
+  SLF_CUDA(cudaGetLastError());
+  p2p_stats_wait_kernel<<<1, 32, 0, s>>>(cm->p2p_buf, cm->world, e);
+  SLF_CUDA(cudaGetLastError());
+  *gathered = reinterpret_cast<const slf_shardstat*>(cm->p2p_buf + off);
+  return SLF_OK;
+}
+
 slf_status dx_finalize_rows(Ctx& c, const float* dx32, const slf_rowstat* rs, void* out, int64_t rows, int64_t H) {
   const int64_t groups = rows * H / 8;
   const int blocks = (int)std::min<int64_t>((groups + 255) / 256, (int64_t)c.dev->sms * 8);
@@ -1186,6 +1269,7 @@ slf_status phase_sharded(Ctx& c, const ShardPlan& sp, slf_comm cm, const void* X
   slf_shardstat* st = reinterpret_cast<slf_shardstat*>(c.ws + sp.off_st);
   slf_shardstat* st_all = reinterpret_cast<slf_shardstat*>(c.ws + sp.off_all);
   const slf_rowstat* rs = reinterpret_cast<const slf_rowstat*>(c.ws + p.off_rowstat);
+  if (cm->p2p) SLF_TRY(p2p_ensure(cm, p.C, c.s));
   SLF_TRY(s_begin(c, a, dW != nullptr));
   std::vector<SChunk> chunks;
   for (int64_t ch = 0; ch < p.nCh; ++ch) chunks.push_back(s_plain_chunk(p, N, ch));
@@ -1221,10 +1305,14 @@ slf_status phase_sharded(Ctx& c, const ShardPlan& sp, slf_comm cm, const void* X
     const SChunk& k = chunks[i];
     const int slot = (int)(i & 1);
     SLF_TRY(s_chunk_stats(c, a, k, st));
-    SLF_TRY(comm_allgather(cm, st, st_all, (size_t)k.rows * 16, c.s));
+    const slf_shardstat* gathered = st_all;
+    if (cm->p2p)
+      SLF_TRY(p2p_allgather_stats(cm, st, k.rows, c.s, &gathered));
+    else
+      SLF_TRY(comm_allgather(cm, st, st_all, (size_t)k.rows * 16, c.s));
     if (pending[slot] >= 0) SLF_TRY(finish(slot));
     const int tb = (i + 1 == chunks.size() && k.rows != chunks[0].rows) ? tab[1] : tab[0];
-    SLF_TRY(s_chunk_bwd(c, a, k, st_all, g, reduction, scale, loss_rows, dX ? dxb[slot] : nullptr, 1, dW,
+    SLF_TRY(s_chunk_bwd(c, a, k, gathered, g, reduction, scale, loss_rows, dX ? dxb[slot] : nullptr, 1, dW,
                         tb >= 0 ? arena.dev(c, tb) : nullptr, tb >= 0 ? arena.tables[tb].second : 0));
     if (dX) {
       SLF_TRY(comm_allreduce_start(cm, dxb[slot], (size_t)k.rows * H, slot, c.s));
@@ -1611,6 +1699,7 @@ slf_status slf_comm_init_callbacks(slf_comm* out, int rank, int world, slf_allga
 slf_status slf_comm_destroy(slf_comm c) {
   if (!c) return SLF_OK;
   slf_status st = SLF_OK;
+  p2p_release(c);
   if (c->nccl) {
     const ncclResult_t r = nccl_api().CommDestroy(c->nccl);
     if (r != ncclSuccess) st = comm_fail_nccl(r, "ncclCommDestroy");
@@ -1620,6 +1709,21 @@ slf_status slf_comm_destroy(slf_comm c) {
     if (e) cudaEventDestroy(e);
   delete c;
   return st;
+}
+
+slf_status slf_comm_set_p2p(slf_comm c, int enable) {
+  if (!c) return fail(SLF_ERR_ARG, "null communicator");
+  if (enable && c->world > P2P_MAX_RANKS) return fail(SLF_ERR_ARG, "P2P supports <= %d ranks", P2P_MAX_RANKS);
+  if (!enable) p2p_release(c);
+  c->p2p = enable != 0;
+  return SLF_OK;
+}
+
+slf_status slf_comm_status(slf_comm c, int32_t* p2p_timeouts) {
+  if (!c || !p2p_timeouts) return fail(SLF_ERR_ARG, "null pointer");
+  *p2p_timeouts = 0;
+  if (c->p2p_buf) SLF_CUDA(cudaMemcpy(p2p_timeouts, c->p2p_buf + 192, 4, cudaMemcpyDeviceToHost));
+  return SLF_OK;
 }
 
 slf_status slf_comm_rank(slf_comm c, int* rank, int* world) {

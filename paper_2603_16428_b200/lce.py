@@ -415,6 +415,16 @@ class Comm:
         check(lib().slf_comm_init_callbacks(ctypes.byref(h), rank, world, fa, fr, None), "slf_comm_init_callbacks")
         return cls(h.value, rank, world, keep=(fa, fr))
 
+    def set_p2p(self, enable: bool = True):
+        """Per-chunk statistics by a P2P one-shot all-gather over CUDA IPC (slf_comm_set_p2p)."""
+        check(lib().slf_comm_set_p2p(self.handle, int(bool(enable))), "slf_comm_set_p2p")
+        return self
+
+    def p2p_timeouts(self) -> int:
+        v = ctypes.c_int32(0)
+        check(lib().slf_comm_status(self.handle, ctypes.byref(v)), "slf_comm_status")
+        return v.value
+
     def close(self):
         if self.handle:
             check(lib().slf_comm_destroy(self.handle), "slf_comm_destroy")

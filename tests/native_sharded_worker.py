@@ -43,6 +43,8 @@ def main():
     ap.add_argument("--budget", type=int, default=3 << 20)
     ap.add_argument("--reduction", default="mean")
     ap.add_argument("--ignore-index", type=int, default=-100)
+    ap.add_argument("--p2p", action="store_true", help="per-chunk statistics by the P2P one-shot all-gather (IPC)")
+    ap.add_argument("--calls", type=int, default=1, help="calls on the same communicator (the last is saved)")
     a = ap.parse_args()
     dist.init_process_group("gloo", rank=a.rank, world_size=a.world)
     torch.cuda.set_device(0)
@@ -71,13 +73,19 @@ def main():
     t = torch.from_numpy(inp.t.astype(np.int32)).cuda()
     v0, v1 = slf.shard_bounds_native(a.V, a.world, a.rank)
     comm = slf.Comm.callbacks(a.rank, a.world, allgather, allreduce)
-    loss, dX, dW = slf.lce_fwd_bwd_sharded(X, W[v0:v1].contiguous(), t, a.V, comm, ignore_index=a.ignore_index,
-                                           reduction=a.reduction, budget_bytes=a.budget)
-    torch.cuda.synchronize()
+    if a.p2p:
+        comm.set_p2p(True)
+    Wl = W[v0:v1].contiguous()
+    for _ in range(a.calls):
+        calls["ag"] = calls["ar"] = 0
+        loss, dX, dW = slf.lce_fwd_bwd_sharded(X, Wl, t, a.V, comm, ignore_index=a.ignore_index,
+                                               reduction=a.reduction, budget_bytes=a.budget)
+        torch.cuda.synchronize()
+    timeouts = comm.p2p_timeouts()
     comm.close()
     np.savez(os.path.join(a.out, f"rank{a.rank}.npz"), loss=loss.detach().cpu().numpy(),
              dX=dX.view(torch.int16).cpu().numpy(), dW=dW.view(torch.int16).cpu().numpy(), v0=v0, v1=v1,
-             ag=calls["ag"], ar=calls["ar"],
+             ag=calls["ag"], ar=calls["ar"], timeouts=timeouts,
              plan=slf.sharded_plan_describe(a.N, a.H, a.V, a.world, a.rank, a.budget))
     dist.destroy_process_group()
 

@@ -520,6 +520,15 @@ def test_native_sharded_nccl_world1(slf, red, ign):
     try:
         loss, dX, dW = slf.lce_fwd_bwd_sharded(X, W, t, 5000, comm, ignore_index=ign, reduction=red,
                                                budget_bytes=6 << 20)
+        comm.set_p2p(True)  # P2P statistics exchange (self only at world 1): the same bits
+        lp, dXp, dWp = slf.lce_fwd_bwd_sharded(X, W, t, 5000, comm, ignore_index=ign, reduction=red,
+                                               budget_bytes=6 << 20)
+        torch.cuda.synchronize()
+        assert comm.p2p_timeouts() == 0
+        assert torch.equal(dX.view(torch.int16), dXp.view(torch.int16))
+        assert torch.equal(dW.view(torch.int16), dWp.view(torch.int16))
+        assert torch.equal(loss.view(-1), lp.view(-1))
+        comm.set_p2p(False)
         torch.cuda.synchronize()
         assert "n_chunks=1 " not in slf.sharded_plan_describe(900, 256, 5000, 1, 0, 6 << 20)
         # a second call on the same communicator (events / comm stream reused) is bit-identical
@@ -539,11 +548,7 @@ def test_native_sharded_nccl_world1(slf, red, ign):
     assert np.all(dX.view(torch.int16).cpu().numpy()[inp.t == ign] == 0)
 
 
-@pytest.mark.parametrize("g,red,budget", [(2, "mean", 3 << 20), (3, "sum", 3 << 20), (2, "none", 4 << 20)])
-def test_native_sharded_callbacks(slf, tmp_path, g, red, budget):
-    """g ranks of the native sharded call as g processes on this GPU, collectives through a gloo
-    callback transport (tests/native_sharded_worker.py): every rank returns the same loss and
-    dhidden, the dW shards assemble the full dW, all against the oracle."""
+def _run_native_ranks(tmp_path, g, red, budget, extra=()):
     import os
     import socket
     import subprocess
@@ -553,12 +558,28 @@ def test_native_sharded_callbacks(slf, tmp_path, g, red, budget):
         port = s.getsockname()[1]
     env = dict(os.environ, MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     worker = os.path.join(os.path.dirname(os.path.abspath(__file__)), "native_sharded_worker.py")
+    tmp_path.mkdir(parents=True, exist_ok=True)
     procs = [subprocess.Popen([sys.executable, worker, "--rank", str(r), "--world", str(g), "--out", str(tmp_path),
-                               "--budget", str(budget), "--reduction", red], env=env)
+                               "--budget", str(budget), "--reduction", red, *extra], env=env)
              for r in range(g)]
-    for p in procs:
-        assert p.wait(timeout=600) == 0
-    res = [np.load(tmp_path / f"rank{r}.npz") for r in range(g)]
+    try:
+        for p in procs:
+            assert p.wait(timeout=600) == 0
+    finally:
+        for p in procs:
+            if p.poll() is None:
+                p.kill()
+    return [np.load(tmp_path / f"rank{r}.npz") for r in range(g)]
+
+
+@pytest.mark.parametrize("g,red,budget", [(2, "mean", 3 << 20), (3, "sum", 3 << 20), (2, "none", 4 << 20)])
+def test_native_sharded_callbacks(slf, tmp_path, g, red, budget):
+    """g ranks of the native sharded call as g processes on this GPU, collectives through a gloo
+    callback transport (tests/native_sharded_worker.py): every rank returns the same loss and
+    dhidden, the dW shards assemble the full dW, all against the oracle.  Then the same ranks with
+    the per-chunk statistics exchanged by the P2P one-shot all-gather over CUDA IPC (NEXT-3; here
+    between processes on one GPU), two calls on one communicator: bit-identical results."""
+    res = _run_native_ranks(tmp_path / "cb", g, red, budget)
     inp = synth.make_inputs(900, 256, 5000, seed=21, alpha=4.0, dist="zipf")
     Xo, Wo, to = oracle_inputs(inp)
     ref = oracle.lce(Xo, Wo, to, reduction=red)
@@ -575,6 +596,12 @@ def test_native_sharded_callbacks(slf, tmp_path, g, red, budget):
     assert rel_max_err(dX, ref["dX"]) <= GRAD_TOL
     assert rel_max_err(dW, ref["dW"]) <= GRAD_TOL
     assert np.all(res[0]["dX"][inp.t == -100] == 0)
+    p2p = _run_native_ranks(tmp_path / "p2p", g, red, budget, ("--p2p", "--calls", "2"))
+    for a, b in zip(res, p2p):
+        assert int(b["timeouts"]) == 0
+        assert int(b["ag"]) == 0 and int(b["ar"]) == nch  # statistics no longer go through the transport
+        for k in ("loss", "dX", "dW"):
+            assert np.array_equal(a[k], b[k]), k
 
 
 def test_lce_fwd_bwd_group_world1(slf):
