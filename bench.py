@@ -184,6 +184,8 @@ def main():
     ap.add_argument("--comm", default="native", choices=["native", "torch"],
                     help="vocab-sharded schedule S: collectives inside the library (slf_comm over NCCL, "
                          "slf_lce_fwd_bwd_sharded) or orchestrated from Python over torch.distributed")
+    ap.add_argument("--p2p-stats", action="store_true",
+                    help="native comm: per-chunk statistics by the P2P one-shot all-gather over CUDA IPC (NEXT-3)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     args = ap.parse_args()
@@ -245,6 +247,8 @@ def main():
     native = multi and not dp and sharded.schedule == "S" and args.comm == "native" and G == g
     if native:  # the library runs the whole sharded step, collectives included (slf_lce_fwd_bwd_sharded)
         comm = slf.Comm.from_process_group(device=local)
+        if args.p2p_stats:
+            comm.set_p2p(True)
         ws = torch.empty(slf.sharded_workspace_bytes(N, H, V, g, rank, args.budget), dtype=torch.uint8, device=dev)
     else:
         ws = slf.alloc_workspace(N_l, H, V_l, dev, schedule="S" if (multi and not dp and sharded.schedule == "S")
@@ -404,7 +408,8 @@ def main():
                    "l2": "inputs larger than L2 (W alone is %.2f GB vs 126 MB L2); no flush" % (V_l * H * 2 / 1e9),
                    "plan": slf.sharded_plan_describe(N, H, V, g, rank, args.budget) if native else
                    slf.plan_describe(N_l, H, V_l, budget_bytes=ws_budget, schedule=args.schedule),
-                   **({"comm": "native (slf_comm NCCL inside libslf_lce.so)" if native else
+                   **({"comm": ("native (slf_comm NCCL inside libslf_lce.so" + (", P2P statistics all-gather)" if
+                                args.p2p_stats else ")")) if native else
                        "torch.distributed NCCL (Python orchestration)"} if multi and not dp else {})},
         "tflops": tflops, "frac_of_peak_burst": tflops / peaks["burst"],
         "frac_of_peak_sustained": tflops / peaks["sustained"],

@@ -1,0 +1,3 @@
+mkdir -p gpurun_out
+export PYTHONUNBUFFERED=1
+timeout 1200 python -m pytest tests/test_gpu_parity.py -m gpu -x -q -k "native_sharded or group_world1" > gpurun_out/pytest_native_r1u.log 2>&1; echo pytest $?; tail -30 gpurun_out/pytest_native_r1u.log
