@@ -245,10 +245,17 @@ def main():
         if sharded.schedule == "S":  # the workspace shares the budget with the module's dX buffers
             ws_budget = sharded.s_workspace_budget(N, H)
     native = multi and not dp and sharded.schedule == "S" and args.comm == "native" and G == g
+    comm_note = None
     if native:  # the library runs the whole sharded step, collectives included (slf_lce_fwd_bwd_sharded)
-        comm = slf.Comm.from_process_group(device=local)
-        if args.p2p_stats:
-            comm.set_p2p(True)
+        try:
+            comm = slf.Comm.from_process_group(device=local)
+            if args.p2p_stats:
+                comm.set_p2p(True)
+        except Exception as e:  # a transport that cannot start: same kernels, Python orchestration
+            native = False
+            comm_note = f"native communicator unavailable ({e}); torch.distributed orchestration"
+            print(comm_note, file=sys.stderr)
+    if native:
         ws = torch.empty(slf.sharded_workspace_bytes(N, H, V, g, rank, args.budget), dtype=torch.uint8, device=dev)
     else:
         ws = slf.alloc_workspace(N_l, H, V_l, dev, schedule="S" if (multi and not dp and sharded.schedule == "S")
@@ -410,7 +417,7 @@ def main():
                    slf.plan_describe(N_l, H, V_l, budget_bytes=ws_budget, schedule=args.schedule),
                    **({"comm": ("native (slf_comm NCCL inside libslf_lce.so" + (", P2P statistics all-gather)" if
                                 args.p2p_stats else ")")) if native else
-                       "torch.distributed NCCL (Python orchestration)"} if multi and not dp else {})},
+                       (comm_note or "torch.distributed NCCL (Python orchestration)")} if multi and not dp else {})},
         "tflops": tflops, "frac_of_peak_burst": tflops / peaks["burst"],
         "frac_of_peak_sustained": tflops / peaks["sustained"],
         "roofline": {"bound": "tensor", "kernel": dom_name, "achieved": achieved, "peak": peaks["sustained"],
