@@ -340,6 +340,60 @@ __device__ __forceinline__ void epilogue_dw_tma(const GemmArgs& a, const CUtenso
   const int nch = min(BN, a.N - n0 + 63) / 64;  // 64-column chunks with at least one valid column
   const bool rmw = a.mode == 1;
   const uint32_t sbase = smem_u32(stg);
+  if (!rmw && !(dbg & 1024)) {
+    // Store / L2 reduce-add (no old values): pull the whole 256-column accumulator row into
+    // registers as bf16 pairs (128 registers) and hand TMEM back to the MMA issuer at once; the
+    // staging-buffer waits on earlier TMA stores then only delay these warps, never the next
+    // tile's MMAs (they have a whole mainloop to finish).
+    uint32_t pk[BN / 2];
+    wait_acc();
+#pragma unroll
+    for (int k = 0; k < BN / 64; ++k) {
+      uint32_t w0[32], w1[32];
+      if (k < nch) {
+        tmem_ld32(taddr + k * 64, w0);
+        tmem_ld32(taddr + k * 64 + 32, w1);
+        tmem_ld_wait();
+#pragma unroll
+        for (int e = 0; e < 16; ++e) {
+          pk[k * 32 + e] = pack_bf16x2(__uint_as_float(w0[2 * e]), __uint_as_float(w0[2 * e + 1]));
+          pk[k * 32 + 16 + e] = pack_bf16x2(__uint_as_float(w1[2 * e]), __uint_as_float(w1[2 * e + 1]));
+        }
+      }
+    }
+    release_tmem();
+#pragma unroll
+    for (int g0 = 0; g0 < BN / 64; g0 += NB) {
+      if (g0 >= nch) break;
+      const int gn = min(NB, nch - g0);
+      if (lead) bulk_wait_read<0>();  // the previous stores have read the staging buffers
+      named_bar_sync(1, 128);
+#pragma unroll
+      for (int j = 0; j < NB; ++j) {
+        if (j < gn) {
+          const uint32_t rowaddr = sbase + j * CHUNK_BYTES + rl * 128;
+#pragma unroll
+          for (int gi = 0; gi < 8; ++gi) {
+            const uint32_t* src = &pk[(g0 + j) * 32 + gi * 4];
+            sts128(rowaddr + ((gi ^ (rl & 7)) << 4), make_uint4(src[0], src[1], src[2], src[3]));
+          }
+        }
+      }
+      fence_proxy_async_smem();
+      named_bar_sync(1, 128);
+      if (lead) {
+        if (dbg & 256) {
+          // timing experiment only: no dW store at all (wrong dW)
+        } else if (a.mode == 2) {
+          for (int j = 0; j < gn; ++j) tma_reduce_add_2d(tmC, stg + j * CHUNK_BYTES, n0 + (g0 + j) * 64, row0);
+        } else {
+          for (int j = 0; j < gn; ++j) tma_store_2d(tmC, stg + j * CHUNK_BYTES, n0 + (g0 + j) * 64, row0);
+        }
+        bulk_commit();
+      }
+    }
+    return;
+  }
   uint32_t v0[32], v1[32];
   for (int g0 = 0; g0 < nch; g0 += NB) {
     const int gn = min(NB, nch - g0);

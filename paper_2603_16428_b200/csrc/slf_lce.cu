@@ -1089,7 +1089,7 @@ bool shard_fit(int64_t N, int64_t H, int64_t V_l, int g, size_t total, int64_t c
   auto ok = [&](size_t b) {
     return shard_layout(N, H, V_l, g, b, sp) && sp->total <= total && (c_cap == 0 || sp->p.C <= c_cap);
   };
-  size_t lo = 0, hi = total;  // bisection: the layout grows with the planner budget
+  size_t lo = 1, hi = total;  // bisection (the layout grows with the budget; 0 would mean the default)
   while (lo < hi) {
     const size_t mid = lo + (hi - lo + 1) / 2;
     if (ok(mid))

@@ -93,7 +93,7 @@ class VocabShardedLCE:
             def ok(b):
                 nb, C = need(V_l, b)
                 return nb is not None and nb <= total and (c_cap == 0 or C <= c_cap)
-            lo, hi = 0, total
+            lo, hi = 1, total  # (a planner budget of 0 would mean the library default)
             while lo < hi:
                 mid = (lo + hi + 1) // 2
                 if ok(mid):

@@ -341,7 +341,7 @@ def test_vocab_sharded_module_world1(slf, sched):
         dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
     inp = synth.make_inputs(900, 256, 5000, seed=15, alpha=4.0, dist="zipf")
     X, W, t = to_dev(inp, torch)
-    m = VocabShardedLCE(5000, budget_bytes=3 << 20, schedule=sched)
+    m = VocabShardedLCE(5000, budget_bytes=6 << 20, schedule=sched)  # fits with the module's dX buffers
     loss, dX, dW = m.forward_backward(X, W, t, reduction="mean")
     torch.cuda.synchronize()
     Xo, Wo, to = oracle_inputs(inp)
