@@ -594,6 +594,7 @@ struct Prob {
   GemmArgs a;
   int epi, a_mn, b_mn, tile_begin;
   int a_split, c_split;
+  int a3d, b3d;  // MN-major operand maps are 3-D {64, K, MN/64}: one TMA box per stage
 };
 
 struct GroupArgs {
@@ -603,7 +604,8 @@ struct GroupArgs {
   int dbg;  // timing-experiment knobs (0 in production): 1 = no L2 prefetch, 2 = late old-dW loads,
             // 4 = record the per-tile trace of unit 0, 8 = L2 prefetch of the next tile's MN-major A,
             // 16 = evict-first dW RMW traffic, 32 = old-dW loads from the first 1024 rows (wrong dW),
-            // 256 = no dW stores (wrong dW)
+            // 256 = no dW stores (wrong dW), 1024 = dW epilogue in the old order (TMEM held until the
+            // staging buffers are free), 2048 = MN-major A operands read from two K-blocks only (wrong)
   const int* sched;  // [units][sched_stride] tile ids, -1 terminated (nullptr: round robin)
   int sched_stride;
 };
@@ -720,7 +722,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
           if (nt >= 0) {
             const int npi = prob_of(g, nt);
             const Prob& Q = g.p[npi];
-            if (Q.a_mn) {
+            if (Q.a_mn && !Q.a3d) {
               int nm, nn;
               tile_coords(nt - Q.tile_begin, Q.a, nm, nn);
               const int nrow = nm * C::TILE_M + (int)rank * BM;
@@ -744,6 +746,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
           // from the second segment's map.
           const CUtensorMap* tAk = tA;
           int a_r = a_row, a_k = kb * BK;
+          if ((g.dbg & 2048) && a_mn) a_k = (kb & 1) * BK;  // timing experiment only: L2-resident MN-major A (wrong)
           if (!a_mn) {
             if (a_r >= P.a_split) { tAk = tA2; a_r -= P.a_split; }
           } else if (a_k >= P.a_split) {
@@ -754,12 +757,16 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
             mbar_arrive_expect_tx(&full[stage], C::STAGE_BYTES);
             if (!a_mn) {
               tma_load_2d(tAk, &full[stage], a_dst, a_k, a_r, pol);
+            } else if (P.a3d) {
+              tma_load_3d(tAk, &full[stage], a_dst, 0, a_k, a_r / 64, pol);
             } else {
 #pragma unroll
               for (int j = 0; j < BM / 64; ++j) tma_load_2d(tAk, &full[stage], a_dst + j * 8192, a_r + j * 64, a_k, pol);
             }
             if (!b_mn) {
               tma_load_2d(tB, &full[stage], b_dst, kb * BK, b_row, pol);
+            } else if (P.b3d) {
+              tma_load_3d(tB, &full[stage], b_dst, 0, kb * BK, b_row / 64, pol);
             } else {
 #pragma unroll
               for (int j = 0; j < C::B_ROWS / 64; ++j)
@@ -771,12 +778,16 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
             const uint32_t fb = mapa_shared(smem_u32(&full[stage]), 0);
             if (!a_mn) {
               tma_load_2d_pair(tAk, fb, a_dst, a_k, a_r, pol);
+            } else if (P.a3d) {
+              tma_load_3d_pair(tAk, fb, a_dst, 0, a_k, a_r / 64, pol);
             } else {
 #pragma unroll
               for (int j = 0; j < BM / 64; ++j) tma_load_2d_pair(tAk, fb, a_dst + j * 8192, a_r + j * 64, a_k, pol);
             }
             if (!b_mn) {
               tma_load_2d_pair(tB, fb, b_dst, kb * BK, b_row, pol);
+            } else if (P.b3d) {
+              tma_load_3d_pair(tB, fb, b_dst, 0, kb * BK, b_row / 64, pol);
             } else {
 #pragma unroll
               for (int j = 0; j < C::B_ROWS / 64; ++j)

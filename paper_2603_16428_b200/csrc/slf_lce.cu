@@ -170,7 +170,47 @@ slf_status make_tmap(CUtensorMap* m, const void* base, uint64_t inner, uint64_t 
 slf_status tmap_kmajor(CUtensorMap* m, const void* base, int64_t K, int64_t rows, int64_t ld, uint32_t box_rows) {
   return make_tmap(m, base, (uint64_t)K, (uint64_t)rows, (uint64_t)ld * 2, 64, box_rows);
 }
-slf_status tmap_mnmajor(CUtensorMap* m, const void* base, int64_t MN, int64_t K, int64_t ld) {
+// MN-major operands with MN % 64 == 0 use a 3-D map {64 MN, K, MN/64} (strides ld*2 and 128 bytes)
+// and one box {64, 64, atoms} per stage: the same bytes and shared-memory layout ([atom][64 K][64
+// MN], atoms 8 KB apart) as `atoms` 2-D boxes, in one TMA instruction.  Two MN-major operands in
+// 2-D boxes issue four TMA loads per stage and ran ~10 % below one K-major operand (debug GEMM,
+// 587 vs 533-543 cycles per K-block); SLF_MN3D=0 keeps the 2-D boxes.
+slf_status make_tmap_mn3d(CUtensorMap* m, const void* base, uint64_t MN, uint64_t K, uint64_t ld_bytes, uint32_t atoms) {
+  auto fn = encode_fn();
+  if (!fn) return fail(SLF_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+  cuuint64_t dims[3] = {64, K, MN / 64};
+  cuuint64_t strides[2] = {ld_bytes, 128};
+  cuuint32_t box[3] = {64, 64, atoms};
+  cuuint32_t estr[3] = {1, 1, 1};
+  CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(base), dims, strides, box, estr,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS)
+    return fail(SLF_ERR_CUDA, "cuTensorMapEncodeTiled (3-D MN-major) failed (%d): MN %llu K %llu ld %llu", (int)r,
+                (unsigned long long)MN, (unsigned long long)K, (unsigned long long)ld_bytes);
+  return SLF_OK;
+}
+
+// Whether 3-D MN-major maps are used (decided once: the environment, then a trial encoding).
+bool mn3d_enabled() {
+  static const bool on = [] {
+    const char* e = getenv("SLF_MN3D");
+    if (e && atoi(e) == 0) return false;
+    static uint16_t probe[64 * 64 * 2];
+    CUtensorMap m;
+    const std::string keep = g_err;
+    const bool ok = make_tmap_mn3d(&m, probe, 128, 64, 128 * 2, 2) == SLF_OK;
+    g_err = keep;
+    return ok;
+  }();
+  return on;
+}
+
+bool mn3d_for(int64_t MN) { return MN % 64 == 0 && mn3d_enabled(); }
+
+// `atoms`: 64-wide MN atoms per stage of this operand (A: BM/64; B: (BN/cta_group)/64).
+slf_status tmap_mnmajor(CUtensorMap* m, const void* base, int64_t MN, int64_t K, int64_t ld, uint32_t atoms = 2) {
+  if (mn3d_for(MN)) return make_tmap_mn3d(m, base, (uint64_t)MN, (uint64_t)K, (uint64_t)ld * 2, atoms);
   return make_tmap(m, base, (uint64_t)MN, (uint64_t)K, (uint64_t)ld * 2, 64, 64);
 }
 
@@ -281,7 +321,8 @@ slf_status launch_group_cfg(DevInfo* dev, ProbSpec* ps, int n, cudaStream_t s, c
     tm.m[MAPS_PER_PROB * np + 2] = ps[p].tc;
     tm.m[MAPS_PER_PROB * np + 3] = ps[p].ta2;
     tm.m[MAPS_PER_PROB * np + 4] = ps[p].tc2;
-    g.p[np] = Prob{a, ps[p].epi, ps[p].a_mn ? 1 : 0, ps[p].b_mn ? 1 : 0, total, ps[p].a_split, ps[p].c_split};
+    g.p[np] = Prob{a, ps[p].epi, ps[p].a_mn ? 1 : 0, ps[p].b_mn ? 1 : 0, total, ps[p].a_split, ps[p].c_split,
+                   (ps[p].a_mn && mn3d_for(a.M)) ? 1 : 0, (ps[p].b_mn && mn3d_for(a.N)) ? 1 : 0};
     total += a.num_tiles;
     flops += 2.0 * a.M * a.N * (double)a.K;
     ++np;
@@ -638,7 +679,7 @@ slf_status phase_backward(Ctx& c, const void* X, const void* W, const slf_rowsta
     if (dW) {  // dW[c0:c0+wc] (+)= G^T X_r : A = G^T (MN-major), B = X_r (MN-major)
       ProbSpec& q = ps[(*n)++];
       SLF_TRY(tmap_mnmajor(&q.ta, G, wc, rows, ldG));
-      SLF_TRY(tmap_mnmajor(&q.tb, Xr, H, rows, H));
+      SLF_TRY(tmap_mnmajor(&q.tb, Xr, H, rows, H, b_box_rows() / 64));
       q.epi = EPI_DW;
       q.a_mn = q.b_mn = true;
       q.a = GemmArgs{};
@@ -654,7 +695,7 @@ slf_status phase_backward(Ctx& c, const void* X, const void* W, const slf_rowsta
     if (dX) {  // dX_r (+)= G W_c : A = G (K-major), B = W_c (MN-major)
       ProbSpec& q = ps[(*n)++];
       SLF_TRY(tmap_kmajor(&q.ta, G, wc, rows, ldG, BM));
-      SLF_TRY(tmap_mnmajor(&q.tb, Wc, H, wc, H));
+      SLF_TRY(tmap_mnmajor(&q.tb, Wc, H, wc, H, b_box_rows() / 64));
       q.epi = EPI_DX;
       q.a_mn = false;
       q.b_mn = true;
@@ -845,7 +886,7 @@ slf_status s_build_bwd(Ctx& c, const SArgs& a, const SChunk& k, void* dXc, int d
       SLF_TRY(tmap_kmajor(&q.ta2, k.ext_base, a.V_l, k.ext, p.ld_stash, BM));
       q.a_split = (int)main_rows;
     }
-    SLF_TRY(tmap_mnmajor(&q.tb, a.W, a.H, a.V_l, a.H));
+    SLF_TRY(tmap_mnmajor(&q.tb, a.W, a.H, a.V_l, a.H, b_box_rows() / 64));
     q.epi = EPI_DXS;
     q.a_mn = false;
     q.b_mn = true;
@@ -869,7 +910,7 @@ slf_status s_build_bwd(Ctx& c, const SArgs& a, const SChunk& k, void* dXc, int d
       SLF_TRY(tmap_mnmajor(&q.ta2, k.ext_base, a.V_l, k.ext, p.ld_stash));
       q.a_split = (int)main_rows;
     }
-    SLF_TRY(tmap_mnmajor(&q.tb, Xr, a.H, rows, a.H));
+    SLF_TRY(tmap_mnmajor(&q.tb, Xr, a.H, rows, a.H, b_box_rows() / 64));
     q.epi = EPI_DW;
     q.a_mn = q.b_mn = true;
     q.a.M = (int)a.V_l;
@@ -1960,7 +2001,7 @@ slf_status slf_debug_gemm(const void* A, const void* B, float* D, int64_t M, int
   else
     SLF_TRY(tmap_kmajor(&ta, A, K, M, K, BM));
   if (b_mn)
-    SLF_TRY(tmap_mnmajor(&tb, B, N, K, N));
+    SLF_TRY(tmap_mnmajor(&tb, B, N, K, N, b_box_rows() / 64));
   else
     SLF_TRY(tmap_kmajor(&tb, B, K, N, K, b_box_rows()));
   GemmArgs a{};

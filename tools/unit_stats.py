@@ -27,6 +27,7 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--what", default="debug")
     ap.add_argument("--chunk", type=int, default=2)
+    ap.add_argument("--mn", default="00", help="debug GEMM: a_mn b_mn (e.g. 11: both operands MN-major)")
     a = ap.parse_args()
     sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
     if a.what == "debug":
@@ -47,15 +48,16 @@ def main():
     from paper_2603_16428_b200._lib import lib
     if a.what == "debug":
         M, N_, K = 256 * 37, 4096, 16384
-        A = torch.randn(M, K, device="cuda").to(torch.bfloat16)
-        B = torch.randn(N_, K, device="cuda").to(torch.bfloat16)
+        am, bm = int(a.mn[0]), int(a.mn[1])
+        A = torch.randn(K if am else M, M if am else K, device="cuda").to(torch.bfloat16)
+        B = torch.randn(K if bm else N_, N_ if bm else K, device="cuda").to(torch.bfloat16)
         for _ in range(5):
-            slf.debug_gemm(A, B, 0, 0, M, N_, K)
+            slf.debug_gemm(A, B, am, bm, M, N_, K)
         torch.cuda.synchronize()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
         for _ in range(20):
-            slf.debug_gemm(A, B, 0, 0, M, N_, K)
+            slf.debug_gemm(A, B, am, bm, M, N_, K)
         e1.record()
         torch.cuda.synchronize()
         print(f"debug GEMM {e0.elapsed_time(e1) / 20:.3f} ms per launch (events)")
