@@ -384,6 +384,7 @@ slf_status slf_lce_dx_finalize(const float* dhidden_fp32, const slf_rowstat* row
 #define SLF_PROF_ONEHOT 12            /* schedule S: dW[v] -= coef * sum x_i               */
 #define SLF_PROF_LOSS_REDUCE 13       /* schedule S: deterministic loss sum               */
 #define SLF_PROF_RMSNORM 14           /* final RMSNorm forward / backward (NEXT-1)        */
+#define SLF_PROF_TRANSPOSE 15         /* schedule S: X_chunk^T for the dW GEMM's B operand */
 slf_status slf_profile_begin(void);
 slf_status slf_profile_end(double* ms, int64_t* launches, double* flops, double* bytes);
 

@@ -821,11 +821,31 @@ slf_status s_begin(Ctx& c, const SArgs& a, bool need_dw) {
 struct SChunk {
   int64_t index, r0, rows, ext;
   uint8_t* ext_base;  // stash rows [rows - ext, rows): row stride ld_stash, or nullptr
+  uint8_t* xt = nullptr;  // X_chunk^T [H][ld_xt] (dW's B operand K-major) in free dhidden rows, or nullptr
+  int64_t ld_xt = 0;
 };
 
 SChunk s_plain_chunk(const Plan& p, int64_t N, int64_t ch) {
   const int64_t r0 = ch * p.C;
-  return SChunk{ch, r0, std::min(p.C, N - r0), 0, nullptr};
+  return SChunk{ch, r0, std::min(p.C, N - r0), 0, nullptr, nullptr, 0};
+}
+
+// X_chunk^T for the dW GEMM's K-major B operand (programmatic dependent launch).
+slf_status launch_transpose_x(Ctx& c, const SArgs& a, const SChunk& k) {
+  ProfScope ps(SLF_PROF_TRANSPOSE, c.s, 0.0, (double)k.rows * a.H * 4);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)((k.rows + 63) / 64), (unsigned)((a.H + 63) / 64));
+  cfg.blockDim = dim3(256);
+  cfg.stream = c.s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  SLF_CUDA(cudaLaunchKernelEx(&cfg, transpose_x_kernel,
+                              reinterpret_cast<const uint16_t*>(a.X) + (size_t)k.r0 * a.H, a.H, (int)k.rows,
+                              reinterpret_cast<uint16_t*>(k.xt), k.ld_xt));
+  return SLF_OK;
 }
 
 // Stash GEMM of a chunk and this shard's per-row statistics of the chunk (out[rows]).
@@ -910,9 +930,15 @@ slf_status s_build_bwd(Ctx& c, const SArgs& a, const SChunk& k, void* dXc, int d
       SLF_TRY(tmap_mnmajor(&q.ta2, k.ext_base, a.V_l, k.ext, p.ld_stash));
       q.a_split = (int)main_rows;
     }
-    SLF_TRY(tmap_mnmajor(&q.tb, Xr, a.H, rows, a.H, b_box_rows() / 64));
     q.epi = EPI_DW;
-    q.a_mn = q.b_mn = true;
+    q.a_mn = true;
+    if (k.xt) {  // B = X_chunk^T [H][ld_xt]: K-major
+      SLF_TRY(tmap_kmajor(&q.tb, k.xt, rows, a.H, k.ld_xt, b_box_rows()));
+      q.b_mn = false;
+    } else {
+      SLF_TRY(tmap_mnmajor(&q.tb, Xr, a.H, rows, a.H, b_box_rows() / 64));
+      q.b_mn = true;
+    }
     q.a.M = (int)a.V_l;
     q.a.N = (int)a.H;
     q.a.K = (int)rows;
@@ -1006,7 +1032,7 @@ std::vector<SChunk> s_chunks(const Plan& p, int64_t N, int64_t H, bool extend, u
   static const int64_t ext_gran = getenv("SLF_S_EXT_GRAN") ? atoi(getenv("SLF_S_EXT_GRAN")) : 256;
   std::vector<SChunk> chunks;
   for (int64_t r0 = 0, ci = 0; r0 < N; ++ci) {
-    SChunk k{ci, r0, std::min(p.C, N - r0), 0, nullptr};
+    SChunk k{ci, r0, std::min(p.C, N - r0), 0, nullptr, nullptr, 0};
     if (extend && !no_ext && k.rows == p.C) {
       const int64_t free_rows = N - r0 - p.C;
       int64_t e = free_rows > 0 ? (free_rows * H) / (p.ld_stash + H) : 0;
@@ -1015,6 +1041,16 @@ std::vector<SChunk> s_chunks(const Plan& p, int64_t N, int64_t H, bool extend, u
         k.ext = e;
         k.rows = p.C + e;
         k.ext_base = dX ? dX + (size_t)(r0 + k.rows) * H * 2 : nullptr;
+      }
+    }
+    // X_chunk^T after the extended stash in dhidden's unwritten rows, when it fits (SLF_XT=0: never)
+    static const bool no_xt = getenv("SLF_XT") && atoi(getenv("SLF_XT")) == 0;
+    if (extend && dX && !no_xt) {
+      const size_t lo = align_up((size_t)(r0 + k.rows) * H * 2 + (size_t)k.ext * p.ld_stash * 2, 1024);
+      const int64_t ld = (k.rows + 7) / 8 * 8;
+      if (lo + (size_t)H * ld * 2 <= (size_t)N * H * 2) {
+        k.xt = dX + lo;
+        k.ld_xt = ld;
       }
     }
     chunks.push_back(k);
@@ -1068,6 +1104,7 @@ slf_status phase_s(Ctx& c, const void* X, const void* W, const int32_t* t, int64
     // dependent launch overlap of the kernel after it.
     if (c.chunk_ready && i <= 2)
       SLF_CUDA(cudaStreamWaitEvent(c.s, c.chunk_ready[i < 2 ? i : chunks.size() - 1], 0));
+    if (k.xt && dW) SLF_TRY(launch_transpose_x(c, a, k));
     SLF_TRY(s_chunk_stats(c, a, k, nullptr));
     SLF_TRY(s_chunk_bwd(c, a, k, nullptr, 1, reduction, scale, loss_rows,
                         dX ? reinterpret_cast<uint8_t*>(dX) + (size_t)k.r0 * H * 2 : nullptr, 0, dW,
