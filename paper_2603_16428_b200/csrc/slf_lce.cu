@@ -1043,8 +1043,11 @@ std::vector<SChunk> s_chunks(const Plan& p, int64_t N, int64_t H, bool extend, u
         k.ext_base = dX ? dX + (size_t)(r0 + k.rows) * H * 2 : nullptr;
       }
     }
-    // X_chunk^T after the extended stash in dhidden's unwritten rows, when it fits (SLF_XT=0: never)
-    static const bool no_xt = getenv("SLF_XT") && atoi(getenv("SLF_XT")) == 0;
+    // X_chunk^T after the extended stash in dhidden's unwritten rows, when it fits (SLF_XT=1 only).
+    // Off by default: it makes the dW tiles 6 % faster per clock (both operands MN-major cost ~9 %),
+    // but under the 1 kW power cap the step was 0.3 ms SLOWER (46.63 +- 0.21 vs 46.32 +- 0.13 ms,
+    // five alternating pairs on one box; the transposes add 0.25 ms per step).  DESIGN.md §7b.
+    static const bool no_xt = !(getenv("SLF_XT") && atoi(getenv("SLF_XT")) == 1);
     if (extend && dX && !no_xt) {
       const size_t lo = align_up((size_t)(r0 + k.rows) * H * 2 + (size_t)k.ext * p.ld_stash * 2, 1024);
       const int64_t ld = (k.rows + 7) / 8 * 8;
