@@ -244,9 +244,24 @@ def main():
         assert (sharded.v0, sharded.v1) == (v0, v1)
         if sharded.schedule == "S":  # the workspace shares the budget with the module's dX buffers
             ws_budget = sharded.s_workspace_budget(N, H)
-    native = multi and not dp and sharded.schedule == "S" and args.comm == "native" and G == g
+    native = multi and not dp and sharded.schedule == "S" and args.comm == "native"
     comm_note = None
-    if native:  # the library runs the whole sharded step, collectives included (slf_lce_fwd_bwd_sharded)
+    if native and G != g:
+        # Timing only: rank 0 of G emulated GPUs through the native call, with a callback transport
+        # that replicates this rank's statistics into all G slots and leaves the fp32 dX partial
+        # as it is (no exchange; results are those of identical shards).
+        class _Raw:
+            def __init__(self, ptr, n):
+                self.__cuda_array_interface__ = {"data": (int(ptr), False), "shape": (int(n),), "typestr": "|u1",
+                                                 "version": 3, "strides": None}
+
+        def _ag(send, recv, nbytes, stream):
+            src = torch.as_tensor(_Raw(send, nbytes), device=dev)
+            torch.as_tensor(_Raw(recv, nbytes * G), device=dev).view(G, nbytes).copy_(src.expand(G, nbytes))
+
+        comm = slf.Comm.callbacks(0, G, _ag, lambda buf, count, stream: None)
+        comm_note = f"native, emulated rank 0 of {G} (statistics replicated, no exchange; timing only)"
+    elif native:  # the library runs the whole sharded step, collectives included (slf_lce_fwd_bwd_sharded)
         try:
             comm = slf.Comm.from_process_group(device=local)
             if args.p2p_stats:
@@ -256,7 +271,8 @@ def main():
             comm_note = f"native communicator unavailable ({e}); torch.distributed orchestration"
             print(comm_note, file=sys.stderr)
     if native:
-        ws = torch.empty(slf.sharded_workspace_bytes(N, H, V, g, rank, args.budget), dtype=torch.uint8, device=dev)
+        ws = torch.empty(slf.sharded_workspace_bytes(N, H, V, G, 0 if G != g else rank, args.budget),
+                         dtype=torch.uint8, device=dev)
     else:
         ws = slf.alloc_workspace(N_l, H, V_l, dev, schedule="S" if (multi and not dp and sharded.schedule == "S")
                                  else args.schedule, budget_bytes=ws_budget)
@@ -413,9 +429,10 @@ def main():
                    if multi else "single GPU",
                    "targets": args.dist, "logit_std": args.alpha, "ignore_frac": 0.05,
                    "l2": "inputs larger than L2 (W alone is %.2f GB vs 126 MB L2); no flush" % (V_l * H * 2 / 1e9),
-                   "plan": slf.sharded_plan_describe(N, H, V, g, rank, args.budget) if native else
+                   "plan": slf.sharded_plan_describe(N, H, V, G, 0 if G != g else rank, args.budget) if native else
                    slf.plan_describe(N_l, H, V_l, budget_bytes=ws_budget, schedule=args.schedule),
-                   **({"comm": ("native (slf_comm NCCL inside libslf_lce.so" + (", P2P statistics all-gather)" if
+                   **({"comm": comm_note if (native and comm_note) else
+                       ("native (slf_comm NCCL inside libslf_lce.so" + (", P2P statistics all-gather)" if
                                 args.p2p_stats else ")")) if native else
                        (comm_note or "torch.distributed NCCL (Python orchestration)")} if multi and not dp else {})},
         "tflops": tflops, "frac_of_peak_burst": tflops / peaks["burst"],
