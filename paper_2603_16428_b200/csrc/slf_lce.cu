@@ -295,6 +295,22 @@ std::vector<int> lpt_table(const ProbSpec* ps, int n, int units, int* stride) {
   return tab;
 }
 
+// SMs the GEMM launches may use.  The vocab-sharded call can leave some to the communicator's
+// kernels: the persistent GEMM CTAs (1 per SM, ~226 KB shared memory, 237 registers per thread)
+// leave no room for an NCCL block, so without reserved SMs the dX all-reduce of chunk c can only
+// run between launches instead of under the next chunk's stash GEMM.  Thread-local:
+// set by phase_sharded for the duration of one call.
+thread_local int tl_reserved_sms = 0;
+int usable_sms(const DevInfo* dev) {
+  const int r = std::min(std::max(tl_reserved_sms, 0), dev->sms - 2);
+  return (dev->sms - r) & ~1;  // whole CTA pairs
+}
+struct ReserveSms {
+  int prev;
+  explicit ReserveSms(int n) : prev(tl_reserved_sms) { tl_reserved_sms = n; }
+  ~ReserveSms() { tl_reserved_sms = prev; }
+};
+
 template <int CG, int NB>
 slf_status launch_group_cfg(DevInfo* dev, ProbSpec* ps, int n, cudaStream_t s, const int* sched, int sched_stride,
                             int prof_kind) {
@@ -339,7 +355,7 @@ slf_status launch_group_cfg(DevInfo* dev, ProbSpec* ps, int n, cudaStream_t s, c
     static int launch_no = 0;
     if (launch_no++ == trace_at) g.dbg |= 4;
   }
-  const int units = sched ? dev->sms / CG : std::min(total, dev->sms / CG);
+  const int units = sched ? usable_sms(dev) / CG : std::min(total, usable_sms(dev) / CG);
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((unsigned)(units * CG));
   cfg.blockDim = dim3(GEMM_THREADS);
@@ -990,7 +1006,7 @@ slf_status s_chunk_bwd(Ctx& c, const SArgs& a, const SChunk& k, const slf_shards
   SLF_TRY(s_build_bwd(c, a, k, dXc, dx_fp32, dW, ps, &n));
   SchedArena arena;
   if (!sched) {
-    const int t = arena.add(ps, n, c.dev->sms / cta_group());
+    const int t = arena.add(ps, n, usable_sms(c.dev) / cta_group());
     SLF_TRY(arena.upload(c));
     sched = arena.dev(c, t);
     sched_stride = arena.tables[t].second;
@@ -1087,7 +1103,7 @@ slf_status phase_s(Ctx& c, const void* X, const void* W, const int32_t* t, int64
         SChunk rep = chunks[i];
         rep.index = std::max<int64_t>(rep.index, 1);  // model the common read-modify-write case
         SLF_TRY(s_build_bwd(c, a, rep, dX ? (uint8_t*)dX + (size_t)rep.r0 * H * 2 : nullptr, 0, dW, ps, &n));
-        found = arena.add(ps, n, c.dev->sms / cta_group());
+        found = arena.add(ps, n, usable_sms(c.dev) / cta_group());
         keys.push_back({key, found});
       }
       tab[i] = found;
@@ -1365,7 +1381,7 @@ slf_status phase_sharded(Ctx& c, const ShardPlan& sp, slf_comm cm, const void* X
       ProbSpec ps[2];
       int n = 0;
       SLF_TRY(s_build_bwd(c, a, rep, dX ? dxb[0] : nullptr, 1, dW, ps, &n));
-      tab[j] = arena.add(ps, n, c.dev->sms / cta_group());
+      tab[j] = arena.add(ps, n, usable_sms(c.dev) / cta_group());
     }
     if (arena.fits(c))
       SLF_TRY(arena.upload(c));
@@ -1861,6 +1877,9 @@ slf_status slf_lce_fwd_bwd_sharded(const void* hidden, const void* weight_shard,
     return fail(SLF_ERR_WORKSPACE, "workspace %zu bytes < required %zu", workspace_bytes, sp.total);
   Ctx c;
   SLF_TRY(setup(c, N, H, vl, sp.b, workspace, sp.p.total, stream, SLF_SCHED_S, true));
+  // SMs left to the communicator's kernels (SLF_COMM_SMS; default 0 — not measured across GPUs here)
+  static const int comm_sms = getenv("SLF_COMM_SMS") ? atoi(getenv("SLF_COMM_SMS")) : 0;
+  ReserveSms reserve(comm->world > 1 || getenv("SLF_COMM_SMS_FORCE") ? comm_sms : 0);
   return phase_sharded(c, sp, comm, hidden, weight_shard, targets, N, H, V_global, ignore_index, reduction, scale,
                        loss_out, dhidden, dweight_shard);
 }

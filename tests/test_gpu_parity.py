@@ -548,7 +548,7 @@ def test_native_sharded_nccl_world1(slf, red, ign):
     assert np.all(dX.view(torch.int16).cpu().numpy()[inp.t == ign] == 0)
 
 
-def _run_native_ranks(tmp_path, g, red, budget, extra=()):
+def _run_native_ranks(tmp_path, g, red, budget, extra=(), env_extra=None):
     import os
     import socket
     import subprocess
@@ -556,7 +556,7 @@ def _run_native_ranks(tmp_path, g, red, budget, extra=()):
     with socket.socket() as s:
         s.bind(("127.0.0.1", 0))
         port = s.getsockname()[1]
-    env = dict(os.environ, MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    env = dict(os.environ, MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), **(env_extra or {}))
     worker = os.path.join(os.path.dirname(os.path.abspath(__file__)), "native_sharded_worker.py")
     tmp_path.mkdir(parents=True, exist_ok=True)
     procs = [subprocess.Popen([sys.executable, worker, "--rank", str(r), "--world", str(g), "--out", str(tmp_path),
@@ -602,6 +602,11 @@ def test_native_sharded_callbacks(slf, tmp_path, g, red, budget):
         assert int(b["ag"]) == 0 and int(b["ar"]) == nch  # statistics no longer go through the transport
         for k in ("loss", "dX", "dW"):
             assert np.array_equal(a[k], b[k]), k
+    if g == 2:  # GEMM launches on 140 of the SMs (8 left to the communicator): same tiles, same bits
+        rs = _run_native_ranks(tmp_path / "rsv", g, red, budget, env_extra={"SLF_COMM_SMS": "8"})
+        for a, b in zip(res, rs):
+            for k in ("loss", "dX", "dW"):
+                assert np.array_equal(a[k], b[k]), k
 
 
 def test_lce_fwd_bwd_group_world1(slf):
