@@ -184,8 +184,9 @@ def main():
     ap.add_argument("--comm", default="native", choices=["native", "torch"],
                     help="vocab-sharded schedule S: collectives inside the library (slf_comm over NCCL, "
                          "slf_lce_fwd_bwd_sharded) or orchestrated from Python over torch.distributed")
-    ap.add_argument("--comm-sms", type=int, default=0,
-                    help="native comm at N>1: SMs the GEMM launches leave to the communicator's kernels")
+    ap.add_argument("--comm-sms", type=int, default=-1,
+                    help="native comm at N>1: SMs the GEMM launches leave to the communicator's kernels "
+                         "(-1: the library default, 8)")
     ap.add_argument("--p2p-stats", action="store_true",
                     help="native comm: per-chunk statistics by the P2P one-shot all-gather over CUDA IPC (NEXT-3)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -197,7 +198,7 @@ def main():
         run_reference(args)
         return
 
-    if args.comm_sms:
+    if args.comm_sms >= 0:
         os.environ["SLF_COMM_SMS"] = str(args.comm_sms)
     # The JSON line is the only thing this process writes to stdout: libraries that print to the C
     # stdout (e.g. NCCL's version banner) are sent to stderr for the rest of the run.

@@ -1877,8 +1877,10 @@ slf_status slf_lce_fwd_bwd_sharded(const void* hidden, const void* weight_shard,
     return fail(SLF_ERR_WORKSPACE, "workspace %zu bytes < required %zu", workspace_bytes, sp.total);
   Ctx c;
   SLF_TRY(setup(c, N, H, vl, sp.b, workspace, sp.p.total, stream, SLF_SCHED_S, true));
-  // SMs left to the communicator's kernels (SLF_COMM_SMS; default 0 — not measured across GPUs here)
-  static const int comm_sms = getenv("SLF_COMM_SMS") ? atoi(getenv("SLF_COMM_SMS")) : 0;
+  // SMs left to the communicator's kernels at world > 1 (SLF_COMM_SMS, default 8): leaving 4 / 8 of
+  // the 148 SMs costs 0.4 / 1.3 % of a Llama-8B step under the power cap (world 1, forced), and it
+  // lets NCCL's all-reduce blocks run beside the persistent GEMMs (not measurable on one GPU).
+  static const int comm_sms = getenv("SLF_COMM_SMS") ? atoi(getenv("SLF_COMM_SMS")) : 8;
   ReserveSms reserve(comm->world > 1 || getenv("SLF_COMM_SMS_FORCE") ? comm_sms : 0);
   return phase_sharded(c, sp, comm, hidden, weight_shard, targets, N, H, V_global, ignore_index, reduction, scale,
                        loss_out, dhidden, dweight_shard);
