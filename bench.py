@@ -360,32 +360,46 @@ def main():
     if not args.no_e2e:
         Xh = torch.from_numpy(inp.X[n0:n1].view(np.int16)).view(torch.bfloat16).pin_memory()
         th = torch.from_numpy(inp.t[n0:n1]).pin_memory()
-        lh = torch.empty(1, dtype=torch.float32).pin_memory()
+        # Two staging sets and pinned loss slots: step k+1's input copy runs under step k, and step
+        # k's loss is read on the host right after step k+1 is enqueued (every step's H2D copy and
+        # loss D2H read are inside the timed region).
+        lh = [torch.empty(1, dtype=torch.float32).pin_memory() for _ in range(2)]
+        done = [torch.cuda.Event() for _ in range(2)]
         Xd = torch.empty_like(X)
         td = torch.empty_like(t)
-        stg = slf.HostStaging(N_l, H, dev) if not multi else None
+        stg = [slf.HostStaging(N_l, H, dev) for _ in range(2)] if not multi else None
+        losses = []
 
-        def e2e_step():
+        def e2e_step(i):
+            k = i % 2
             if not multi:
-                slf.lce_fwd_bwd_host(Xh, W, th, dX=dX, dW=dW, loss_host=lh, staging=stg, workspace=ws,
+                slf.lce_fwd_bwd_host(Xh, W, th, dX=dX, dW=dW, loss_host=lh[k], staging=stg[k], workspace=ws,
                                      budget_bytes=args.budget, schedule=args.schedule)
             else:
                 Xd.copy_(Xh, non_blocking=True)
                 td.copy_(th, non_blocking=True)
                 lo = step(Xd, td)
-                lh.copy_(lo.reshape(1), non_blocking=True)
-            torch.cuda.current_stream(dev).synchronize()
-            return float(lh[0])
+                lh[k].copy_(lo.reshape(1), non_blocking=True)
+            done[k].record(torch.cuda.current_stream(dev))
+            if i > 0:  # the previous step's loss, read on the host
+                done[1 - k].synchronize()
+                losses.append(float(lh[1 - k][0]))
 
-        for _ in range(2):
-            e2e_step()
+        def e2e_drain(i_last):
+            done[i_last % 2].synchronize()
+            losses.append(float(lh[i_last % 2][0]))
+
+        for i in range(2):
+            e2e_step(i)
+        e2e_drain(1)
         barrier()
         torch.cuda.synchronize()
         f0 = torch.cuda.Event(enable_timing=True)
         f1 = torch.cuda.Event(enable_timing=True)
         f0.record(stream)
-        for _ in range(args.steps):
-            e2e_step()
+        for i in range(args.steps):
+            e2e_step(i)
+        e2e_drain(args.steps - 1)
         f1.record(stream)
         torch.cuda.synchronize()
         ems = f0.elapsed_time(f1) / args.steps
@@ -393,7 +407,8 @@ def main():
             tt = torch.tensor([ems], dtype=torch.float64, device=dev)
             dist.all_reduce(tt, op=dist.ReduceOp.MAX)
             ems = float(tt.item())
-        e2e = {"value": N / (ems / 1e3), "unit": UNIT, "ms_per_step": ems,
+        assert all(np.isfinite(losses)) and len(losses) == args.steps + 2
+        e2e = {"value": N / (ems / 1e3), "unit": UNIT, "ms_per_step": ems, "loss_read": "every step, one step late",
                "h2d_bytes_per_step": int(X.numel() * 2 + t.numel() * 4), "d2h_bytes_per_step": 4}
 
     if rank != 0:

@@ -151,8 +151,10 @@ slf_status slf_lce_fwd_bwd_ex(const void* hidden, const void* weight, const int3
  *   weight, dhidden, dweight, workspace: as slf_lce_fwd_bwd_ex (DEVICE)
  *   hidden_dev [N, H] bf16, targets_dev [N] int32, loss_dev fp32 [1] / [N]: caller-owned DEVICE
  *       staging buffers (the library allocates no device memory); overwritten.
- * The copies into the staging buffers start only after the work already enqueued on `stream`
- * (e.g. the previous step reading them) has completed.  Schedule R (when S does not fit) copies
+ * The copies into a staging buffer start once the last call that used the same hidden_dev has
+ * finished with it (tracked per staging pointer; the first time: once the work already enqueued
+ * on `stream` has completed), so alternating two staging sets lets step k+1's input copy run
+ * under step k.  Schedule R (when S does not fit) copies
  * everything up front.  Not thread-safe against another host call on the same device at once
  * (the copy stream and its events are per device). */
 slf_status slf_lce_fwd_bwd_host(const void* hidden_host, const void* weight, const int32_t* targets_host, int64_t N,

@@ -112,6 +112,10 @@ struct DevInfo {
   // slf_lce_fwd_bwd_host: copy stream and per-chunk events (created on first use)
   cudaStream_t copy_stream = nullptr;
   std::vector<cudaEvent_t> copy_events;
+  // per staging buffer (hidden_dev): recorded at the end of the last call that read it, so the next
+  // call's copy into it waits only for that call, not for everything on the stream (double-buffered
+  // staging lets step k+1's input copy run under step k)
+  std::map<const void*, cudaEvent_t> staging_free;
 };
 
 std::mutex g_mu;
@@ -1556,10 +1560,13 @@ slf_status slf_lce_fwd_bwd_host(const void* hidden_host, const void* weight, con
       SLF_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
       d.copy_events.push_back(e);
     }
-    // the staging buffer may still be read by work already on `stream` (the previous step)
-    SLF_CUDA(cudaEventRecord(d.copy_events[chunks.size()], c.s));
-    c.enqueue_inputs = [&]() -> slf_status {
-      SLF_CUDA(cudaStreamWaitEvent(d.copy_stream, d.copy_events[chunks.size()], 0));
+    // The staging buffer may still be read by an earlier call: wait for the end of the last call
+    // that used it (tracked per staging pointer), else for everything already on `stream`.
+    auto it = d.staging_free.find(hidden_dev);
+    const cudaEvent_t free_ev = it != d.staging_free.end() ? it->second : d.copy_events[chunks.size()];
+    if (it == d.staging_free.end()) SLF_CUDA(cudaEventRecord(free_ev, c.s));
+    c.enqueue_inputs = [&d, free_ev, &chunks, hh, hd, row_bytes]() -> slf_status {
+      SLF_CUDA(cudaStreamWaitEvent(d.copy_stream, free_ev, 0));
       for (size_t i = 0; i < chunks.size(); ++i) {
         const size_t off = (size_t)chunks[i].r0 * row_bytes;
         SLF_CUDA(cudaMemcpyAsync(hd + off, hh + off, (size_t)chunks[i].rows * row_bytes, cudaMemcpyHostToDevice,
@@ -1582,6 +1589,11 @@ slf_status slf_lce_fwd_bwd_host(const void* hidden_host, const void* weight, con
   }
   SLF_CUDA(cudaMemcpyAsync(loss_host, loss_dev, (reduction == SLF_NONE ? (size_t)N : 1) * 4, cudaMemcpyDeviceToHost,
                            c.s));
+  if (!chunks.empty()) {  // every reader of hidden_dev is enqueued: mark the staging buffer's release
+    auto& ev = d.staging_free[hidden_dev];
+    if (!ev) SLF_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+    SLF_CUDA(cudaEventRecord(ev, c.s));
+  }
   return SLF_OK;
 }
 

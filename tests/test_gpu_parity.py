@@ -403,6 +403,37 @@ def test_host_input_call_matches_device_call(slf, sched, red, pin):
     assert torch.equal(loss_h2, loss_h) and torch.equal(dX_h2, dX_h)
 
 
+def test_host_input_double_buffered_staging(slf):
+    """Back-to-back host-input calls alternating two staging sets with no host synchronisation:
+    step k+1's input copy may run under step k (the library waits per staging buffer for the last
+    call that read it), and every step still computes on its own inputs (bit-identical to the
+    device call on them)."""
+    inp1 = synth.make_inputs(1100, 256, 3000, seed=24, alpha=4.0, dist="zipf")
+    inp2 = synth.make_inputs(1100, 256, 3000, seed=25, alpha=1.0, dist="uniform")
+    (X1, W, t1), (X2, _, t2) = to_dev(inp1, torch), to_dev(inp2, torch)
+    budget = 2 << 20
+    ref = {}
+    for name, X, t in (("a", X1, t1), ("b", X2, t2)):
+        ref[name] = slf.lce_fwd_bwd(X, W, t, budget_bytes=budget, schedule="S")
+    host = {"a": (X1.cpu().pin_memory(), t1.cpu().pin_memory()), "b": (X2.cpu().pin_memory(), t2.cpu().pin_memory())}
+    stg = [slf.HostStaging(1100, 256, X1.device) for _ in range(2)]
+    ws = slf.alloc_workspace(1100, 256, 3000, X1.device, "S", budget)
+    order = ["a", "b", "b", "a", "a", "b"]
+    outs = []
+    for i, name in enumerate(order):
+        lh = torch.empty(1, dtype=torch.float32).pin_memory()
+        dX = torch.empty_like(X1)
+        dW = torch.empty_like(W)
+        slf.lce_fwd_bwd_host(host[name][0], W, host[name][1], dX=dX, dW=dW, loss_host=lh, staging=stg[i % 2],
+                             workspace=ws, budget_bytes=budget, schedule="S")
+        outs.append((name, lh, dX, dW))
+    torch.cuda.synchronize()
+    for name, lh, dX, dW in outs:
+        loss_d, dX_d, dW_d = ref[name]
+        assert torch.equal(lh, loss_d.reshape(-1).cpu()), name
+        assert torch.equal(dX, dX_d) and torch.equal(dW, dW_d), name
+
+
 # ---- final RMSNorm + LCE (SURVEY §8(f) NEXT-1) ---------------------------------------------------
 @pytest.mark.parametrize("sched", SCHEDS)
 @pytest.mark.parametrize("N,H,V", [(300, 256, 3000), (1000, 520, 4100)])
