@@ -686,10 +686,13 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
       tmem_alloc<TMEM_COLS>(tmem_slot);
   }
   tc_fence_before();
-  if constexpr (CG == 2)
+  if constexpr (CG == 2) {
     cluster_sync();
-  else
+    __syncthreads();  // also a CTA barrier, so race checkers that do not model barrier.cluster see
+                      // the TMEM address written by tcgen05.alloc ordered before the reads below
+  } else {
     __syncthreads();
+  }
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
   // PDL: let the next launch's CTAs start their prologue as soon as SMs free up, and wait for the
