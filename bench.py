@@ -435,6 +435,7 @@ def main():
             traffic = json.load(open(prof_path)).get(args.config, {}).get(dom_name)
         except Exception:
             traffic = None
+    exec_flops = sum(v["flops"] for k, v in kinds.items() if k.startswith("gemm")) / args.steps
     kernels = {k: {"ms_per_step": v["ms"] / args.steps, "launches_per_step": v["launches"] / args.steps,
                    **({"tflops": v["flops"] / (v["ms"] / 1e3) / 1e12} if v["flops"] else {}),
                    **({"gbs": v["bytes"] / (v["ms"] / 1e3) / 1e9} if v["bytes"] else {})}
@@ -455,12 +456,14 @@ def main():
                        ("native (slf_comm NCCL inside libslf_lce.so" + (", P2P statistics all-gather)" if
                                 args.p2p_stats else ")")) if native else
                        (comm_note or "torch.distributed NCCL (Python orchestration)")} if multi and not dp else {})},
-        "tflops": tflops, "frac_of_peak_burst": tflops / peaks["burst"],
+        "tflops": tflops, "tflops_executed": exec_flops / (ms / 1e3) / 1e12,
+        "frac_of_peak_burst": tflops / peaks["burst"],
         "frac_of_peak_sustained": tflops / peaks["sustained"],
         "roofline": {"bound": "tensor", "kernel": dom_name, "achieved": achieved, "peak": peaks["sustained"],
                      "unit": "TFLOP/s", "frac": achieved / peaks["sustained"], "traffic": traffic,
                      "peak_kind": "bf16 sustained (kernel timed inside a long step), " + peaks["source"],
-                     "frac_of_burst": achieved / peaks["burst"]},
+                     "frac_of_burst": achieved / peaks["burst"],
+                     "ncu": "profiles/ncu_r01q.md (tensor pipe active % per kernel, DRAM bytes)"},
         "kernels": kernels,
         "gpu_launches": launches,
         "memory": {"extra_device_bytes": int(extra), "logits_bytes_per_gpu": N_l * V_l * 2,
