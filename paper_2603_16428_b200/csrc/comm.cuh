@@ -18,9 +18,13 @@
 #include <cstdio>
 #include <cstring>
 #include <mutex>
+#include <string>
 #include <type_traits>
+#include <utility>
+#include <vector>
 
 #include "../../include/slf_lce.h"
+#include "ptx.cuh"
 
 namespace slf {
 
@@ -76,7 +80,11 @@ inline NcclApi& nccl_api() {
 // suffice: a peer can only write epoch e+2 after it has seen this rank's epoch e+1 statistics, which
 // this rank pushes after its epoch-e consumer has finished (stream order).
 constexpr int P2P_MAX_RANKS = 16;
-constexpr size_t P2P_HDR_BYTES = 256;  // flags[P2P_MAX_RANKS] u64 + error word at byte 192
+// Header of a rank's receive buffer: statistics counters [16] u64 at 0, the timeout word at 192,
+// dX "partial ready" counters [16] u64 at 256, dX "slice delivered" counters [16] u64 at 384, the
+// exchange kernel's finished-block counter (u32) at 512.
+constexpr size_t P2P_HDR_BYTES = 1024;
+constexpr size_t P2P_ERR_OFF = 192, P2P_DX_READY_OFF = 256, P2P_DX_DONE_OFF = 384, P2P_DX_BLOCKS_OFF = 512;
 struct PeerPtrs {
   uint8_t* p[P2P_MAX_RANKS];
 };
@@ -95,20 +103,104 @@ __global__ void __launch_bounds__(256) p2p_stats_push_kernel(const uint4* __rest
 }
 
 // Thread r < g waits for flags[r] >= target (bounded: ~30 s, then the error word is set and the
-// consumer reads whatever is there — slf_comm_status reports it; no hang).
-__global__ void p2p_stats_wait_kernel(uint8_t* buf, int g, unsigned long long target) {
+// consumer reads whatever is there — slf_comm_status reports it; no hang).  `off`: which counters.
+__global__ void p2p_stats_wait_kernel(uint8_t* buf, int g, unsigned long long target, int off = 0) {
   const int r = threadIdx.x;
   if (r >= g) return;
-  const unsigned long long* flag = reinterpret_cast<const unsigned long long*>(buf) + r;
+  const unsigned long long* flag = reinterpret_cast<const unsigned long long*>(buf + off) + r;
   for (long long spins = 0;; ++spins) {
     unsigned long long v;
     asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(flag) : "memory");
     if (v >= target) break;
     if (spins > (1ll << 27)) {
-      atomicExch(reinterpret_cast<int*>(buf + 192), 1);
+      atomicExch(reinterpret_cast<int*>(buf + P2P_ERR_OFF), 1);
       break;
     }
     __nanosleep(200);
+  }
+}
+
+__device__ __forceinline__ void p2p_spin_geq(const unsigned long long* flag, unsigned long long target, uint8_t* buf) {
+  for (long long spins = 0;; ++spins) {
+    unsigned long long v;
+    asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(flag) : "memory");
+    if (v >= target) return;
+    if (spins > (1ll << 27)) {
+      atomicExch(reinterpret_cast<int*>(buf + P2P_ERR_OFF), 1);
+      return;
+    }
+    __nanosleep(200);
+  }
+}
+
+// The dX exchange of one chunk as one kernel (NEXT-3 / DESIGN.md §9b): on rank k, after this
+// rank's fp32 partial of the chunk is complete, (a) announce it to every rank, (b) wait until every
+// rank's partial is there, (c) for the rows of this rank's slice [s0, s1) of the chunk, sum the g
+// partials in rank order (deterministic; peer memory over NVLink), round to bf16 (ignored rows +0)
+// and store the rows into EVERY rank's dhidden (the all-gather), (d) the last block to finish tells
+// every rank that its partial has been read and its dhidden slice written.  Reduce-scatter +
+// all-gather + finalize in one pass, no NCCL; it runs on the comm stream on the SMs the GEMMs
+// leave free, under the next chunk's stash GEMM.
+struct DxArgs {
+  PeerPtrs part;   // each rank's fp32 partial of this chunk, row 0 ([rows][H])
+  PeerPtrs dx;     // each rank's dhidden at the chunk's row 0 (bf16 [rows][H])
+  PeerPtrs flags;  // each rank's receive buffer (header)
+  const slf_rowstat* rowstat;  // this chunk's row 0
+  uint8_t* mybuf;
+  int g, rank, s0, s1, H;
+  unsigned long long epoch;
+};
+
+__global__ void __launch_bounds__(256) p2p_dx_exchange_kernel(DxArgs a) {
+  if (blockIdx.x == 0 && threadIdx.x < a.g) {  // (a) my partial of this epoch is ready
+    unsigned long long* f = reinterpret_cast<unsigned long long*>(a.flags.p[threadIdx.x] + P2P_DX_READY_OFF) + a.rank;
+    asm volatile("red.release.sys.global.add.u64 [%0], 1;" ::"l"(f) : "memory");
+  }
+  if (threadIdx.x < a.g)  // (b)
+    p2p_spin_geq(reinterpret_cast<const unsigned long long*>(a.mybuf + P2P_DX_READY_OFF) + threadIdx.x, a.epoch,
+                 a.mybuf);
+  __syncthreads();
+  // (c) 8 columns (two 16-byte fp32 loads per rank, one 16-byte bf16 store per rank) per item
+  const int per_row = a.H / 8;
+  const long long items = (long long)(a.s1 - a.s0) * per_row;
+  for (long long it = blockIdx.x * (long long)blockDim.x + threadIdx.x; it < items;
+       it += (long long)gridDim.x * blockDim.x) {
+    const int r = a.s0 + (int)(it / per_row);
+    const int c = (int)(it % per_row) * 8;
+    float acc[8];
+    {
+      const float4* src = reinterpret_cast<const float4*>(reinterpret_cast<const float*>(a.part.p[0]) +
+                                                          (size_t)r * a.H + c);
+      const float4 x0 = src[0], x1 = src[1];
+      acc[0] = x0.x; acc[1] = x0.y; acc[2] = x0.z; acc[3] = x0.w;
+      acc[4] = x1.x; acc[5] = x1.y; acc[6] = x1.z; acc[7] = x1.w;
+    }
+    for (int p = 1; p < a.g; ++p) {  // rank order
+      const float4* src = reinterpret_cast<const float4*>(reinterpret_cast<const float*>(a.part.p[p]) +
+                                                          (size_t)r * a.H + c);
+      const float4 x0 = src[0], x1 = src[1];
+      acc[0] += x0.x; acc[1] += x0.y; acc[2] += x0.z; acc[3] += x0.w;
+      acc[4] += x1.x; acc[5] += x1.y; acc[6] += x1.z; acc[7] += x1.w;
+    }
+    uint4 o = make_uint4(pack_bf16x2(acc[0], acc[1]), pack_bf16x2(acc[2], acc[3]), pack_bf16x2(acc[4], acc[5]),
+                         pack_bf16x2(acc[6], acc[7]));
+    if (!a.rowstat[r].valid) o = make_uint4(0u, 0u, 0u, 0u);
+    for (int p = 0; p < a.g; ++p)
+      *reinterpret_cast<uint4*>(reinterpret_cast<uint16_t*>(a.dx.p[p]) + (size_t)r * a.H + c) = o;
+  }
+  // (d) every store of this block is visible system-wide before the block counts itself done
+  __threadfence_system();
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    unsigned int* cnt = reinterpret_cast<unsigned int*>(a.mybuf + P2P_DX_BLOCKS_OFF);
+    if (atomicAdd(cnt, 1u) == gridDim.x - 1) {
+      *cnt = 0u;  // the next chunk's kernel runs after this one (same stream)
+      __threadfence_system();
+      for (int p = 0; p < a.g; ++p) {
+        unsigned long long* f = reinterpret_cast<unsigned long long*>(a.flags.p[p] + P2P_DX_DONE_OFF) + a.rank;
+        asm volatile("red.release.sys.global.add.u64 [%0], 1;" ::"l"(f) : "memory");
+      }
+    }
   }
 }
 
@@ -121,12 +213,16 @@ struct slf_comm_s {
   ncclComm_t nccl = nullptr;
   cudaStream_t cs = nullptr;  // the communicator's stream
   cudaEvent_t ev_in = nullptr, ev_ag = nullptr, ev_ar[2] = {nullptr, nullptr};
-  // P2P statistics all-gather (slf_comm_set_p2p)
+  // P2P exchanges (slf_comm_set_p2p): bit 0 statistics all-gather, bit 1 dX exchange kernel
   bool p2p = false;
+  int p2p_mode = 0;
   uint8_t* p2p_buf = nullptr;  // this rank's receive buffer (cudaMalloc, communicator-owned)
   int64_t p2p_rows = 0;        // capacity in rows per slot
   uint8_t* p2p_peer[slf::P2P_MAX_RANKS] = {};  // mapped receive buffers of every rank (own = p2p_buf)
   unsigned long long epoch = 0;
+  unsigned long long dx_epoch = 0;  // chunks whose dX went through the exchange kernel
+  // caller buffers mapped from peers: (handle bytes) -> opened base, and this rank's exported bases
+  std::vector<std::pair<std::string, uint8_t*>> ipc_open;
   // callback transport
   slf_allgather_fn cb_allgather = nullptr;
   slf_allreduce_f32_fn cb_allreduce = nullptr;

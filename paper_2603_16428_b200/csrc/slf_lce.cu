@@ -1266,6 +1266,9 @@ slf_status comm_join(slf_comm cm, int slot, cudaStream_t s) {
 }
 
 void p2p_release(slf_comm cm) {
+  for (auto& kv : cm->ipc_open) cudaIpcCloseMemHandle(kv.second);
+  cm->ipc_open.clear();
+  cm->dx_epoch = 0;
   for (int r = 0; r < cm->world && r < P2P_MAX_RANKS; ++r)
     if (cm->p2p_peer[r] && r != cm->rank) cudaIpcCloseMemHandle(cm->p2p_peer[r]);
   if (cm->p2p_buf) cudaFree(cm->p2p_buf);
@@ -1348,6 +1351,77 @@ slf_status p2p_allgather_stats(slf_comm cm, const slf_shardstat* st, int64_t row
   return SLF_OK;
 }
 
+typedef CUresult (*PFN_memGetAddressRange)(CUdeviceptr*, size_t*, CUdeviceptr);
+PFN_memGetAddressRange addr_range_fn() {
+  static PFN_memGetAddressRange fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuMemGetAddressRange", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_memGetAddressRange>(p);
+  });
+  return fn;
+}
+
+// Every rank's address of a caller-owned device buffer (e.g. the workspace, dhidden): the
+// allocation base is exported by CUDA IPC with the offset inside it, the records are all-gathered
+// through the transport, and peers' bases are opened once per handle (cached on the communicator).
+slf_status p2p_map(slf_comm cm, const void* local, cudaStream_t s, uint8_t** peer) {
+  auto fn = addr_range_fn();
+  if (!fn) return fail(SLF_ERR_COMM, "cuMemGetAddressRange unavailable");
+  CUdeviceptr base = 0;
+  size_t size = 0;
+  if (fn(&base, &size, reinterpret_cast<CUdeviceptr>(local)) != CUDA_SUCCESS)
+    return fail(SLF_ERR_COMM, "cuMemGetAddressRange failed for %p", local);
+  struct Rec {
+    cudaIpcMemHandle_t h;
+    uint64_t off, pad;
+  } rec;
+  static_assert(sizeof(Rec) == 80, "80-byte record");
+  memset(&rec, 0, sizeof(rec));
+  SLF_CUDA(cudaIpcGetMemHandle(&rec.h, reinterpret_cast<void*>(base)));
+  rec.off = reinterpret_cast<uint64_t>(local) - (uint64_t)base;
+  uint8_t* dev = nullptr;
+  SLF_CUDA(cudaMalloc(&dev, sizeof(Rec) * (size_t)(cm->world + 1)));
+  std::vector<Rec> all((size_t)cm->world);
+  slf_status st = SLF_OK;
+  if (cudaMemcpy(dev, &rec, sizeof(Rec), cudaMemcpyHostToDevice) != cudaSuccess) st = fail(SLF_ERR_CUDA, "upload");
+  if (st == SLF_OK) st = comm_allgather(cm, dev, dev + sizeof(Rec), sizeof(Rec), s);
+  if (st == SLF_OK && cudaStreamSynchronize(s) != cudaSuccess) st = fail(SLF_ERR_CUDA, "exchange");
+  if (st == SLF_OK && cudaMemcpy(all.data(), dev + sizeof(Rec), sizeof(Rec) * all.size(), cudaMemcpyDeviceToHost) !=
+                          cudaSuccess)
+    st = fail(SLF_ERR_CUDA, "download");
+  cudaFree(dev);
+  for (int r = 0; st == SLF_OK && r < cm->world; ++r) {
+    if (r == cm->rank) {
+      peer[r] = static_cast<uint8_t*>(const_cast<void*>(local));
+      continue;
+    }
+    const std::string key(reinterpret_cast<const char*>(&all[r].h), sizeof(cudaIpcMemHandle_t));
+    uint8_t* b = nullptr;
+    for (auto& kv : cm->ipc_open)
+      if (kv.first == key) b = kv.second;
+    if (!b) {
+      void* p = nullptr;
+      const cudaError_t e = cudaIpcOpenMemHandle(&p, all[r].h, cudaIpcMemLazyEnablePeerAccess);
+      if (e != cudaSuccess) return fail(SLF_ERR_COMM, "cudaIpcOpenMemHandle(rank %d): %s", r, cudaGetErrorString(e));
+      b = static_cast<uint8_t*>(p);
+      cm->ipc_open.emplace_back(key, b);
+    }
+    peer[r] = b + all[r].off;
+  }
+  return st;
+}
+
+// Wait (on stream s) until every rank's counter at `off` in this rank's buffer reached `target`.
+slf_status p2p_wait(slf_comm cm, int off, unsigned long long target, cudaStream_t s) {
+  p2p_stats_wait_kernel<<<1, 32, 0, s>>>(cm->p2p_buf, cm->world, target, off);
+  SLF_CUDA(cudaGetLastError());
+  return SLF_OK;
+}
+
 slf_status dx_finalize_rows(Ctx& c, const float* dx32, const slf_rowstat* rs, void* out, int64_t rows, int64_t H) {
   const int64_t groups = rows * H / 8;
   const int blocks = (int)std::min<int64_t>((groups + 255) / 256, (int64_t)c.dev->sms * 8);
@@ -1370,7 +1444,15 @@ slf_status phase_sharded(Ctx& c, const ShardPlan& sp, slf_comm cm, const void* X
   slf_shardstat* st = reinterpret_cast<slf_shardstat*>(c.ws + sp.off_st);
   slf_shardstat* st_all = reinterpret_cast<slf_shardstat*>(c.ws + sp.off_all);
   const slf_rowstat* rs = reinterpret_cast<const slf_rowstat*>(c.ws + p.off_rowstat);
+  const bool p2p_dx = cm->p2p && (cm->p2p_mode & 2) && dX;
   if (cm->p2p) SLF_TRY(p2p_ensure(cm, p.C, c.s));
+  uint8_t* ws_peer[P2P_MAX_RANKS] = {};
+  uint8_t* dx_peer[P2P_MAX_RANKS] = {};
+  if (p2p_dx) {
+    SLF_TRY(p2p_map(cm, c.ws, c.s, ws_peer));
+    SLF_TRY(p2p_map(cm, dX, c.s, dx_peer));
+  }
+  std::vector<unsigned long long> dx_ep(p.nCh, 0);
   SLF_TRY(s_begin(c, a, dW != nullptr));
   std::vector<SChunk> chunks;
   for (int64_t ch = 0; ch < p.nCh; ++ch) chunks.push_back(s_plain_chunk(p, N, ch));
@@ -1407,17 +1489,52 @@ slf_status phase_sharded(Ctx& c, const ShardPlan& sp, slf_comm cm, const void* X
     const int slot = (int)(i & 1);
     SLF_TRY(s_chunk_stats(c, a, k, st));
     const slf_shardstat* gathered = st_all;
-    if (cm->p2p)
+    if (cm->p2p && (cm->p2p_mode & 1))
       SLF_TRY(p2p_allgather_stats(cm, st, k.rows, c.s, &gathered));
     else
       SLF_TRY(comm_allgather(cm, st, st_all, (size_t)k.rows * 16, c.s));
     if (pending[slot] >= 0) SLF_TRY(finish(slot));
+    // P2P dX: the partial buffer of this slot is rewritten only once every rank has read it (the
+    // exchange kernels of chunk i-2 have all signalled)
+    if (p2p_dx && i >= 2) SLF_TRY(p2p_wait(cm, (int)P2P_DX_DONE_OFF, dx_ep[i - 2], c.s));
     const int tb = (i + 1 == chunks.size() && k.rows != chunks[0].rows) ? tab[1] : tab[0];
     SLF_TRY(s_chunk_bwd(c, a, k, gathered, g, reduction, scale, loss_rows, dX ? dxb[slot] : nullptr, 1, dW,
                         tb >= 0 ? arena.dev(c, tb) : nullptr, tb >= 0 ? arena.tables[tb].second : 0));
-    if (dX) {
+    if (p2p_dx) {  // reduce-scatter + all-gather + bf16 finalize of this chunk, one kernel on the comm stream
+      dx_ep[i] = ++cm->dx_epoch;
+      DxArgs xa{};
+      const size_t off = slot ? sp.off_dx1 : sp.off_dx0;
+      for (int r = 0; r < g; ++r) {
+        xa.part.p[r] = ws_peer[r] + off;
+        xa.dx.p[r] = dx_peer[r] + (size_t)k.r0 * H * 2;
+        xa.flags.p[r] = cm->p2p_peer[r];
+      }
+      xa.rowstat = rs + k.r0;
+      xa.mybuf = cm->p2p_buf;
+      xa.g = g;
+      xa.rank = cm->rank;
+      xa.s0 = (int)(k.rows * cm->rank / g);
+      xa.s1 = (int)(k.rows * (cm->rank + 1) / g);
+      xa.H = (int)H;
+      xa.epoch = dx_ep[i];
+      cudaStream_t xs = cm->cs ? cm->cs : c.s;
+      if (xs != c.s) {
+        SLF_CUDA(cudaEventRecord(cm->ev_in, c.s));
+        SLF_CUDA(cudaStreamWaitEvent(xs, cm->ev_in, 0));
+      }
+      const int blocks = 2 * std::max(8, tl_reserved_sms);
+      p2p_dx_exchange_kernel<<<blocks, 256, 0, xs>>>(xa);
+      SLF_CUDA(cudaGetLastError());
+    } else if (dX) {
       SLF_TRY(comm_allreduce_start(cm, dxb[slot], (size_t)k.rows * H, slot, c.s));
       pending[slot] = (int64_t)i;
+    }
+  }
+  if (p2p_dx && !chunks.empty()) {  // every rank's slices of every chunk are in this rank's dhidden
+    SLF_TRY(p2p_wait(cm, (int)P2P_DX_DONE_OFF, dx_ep[chunks.size() - 1], c.s));
+    if (cm->cs) {
+      SLF_CUDA(cudaEventRecord(cm->ev_ag, cm->cs));
+      SLF_CUDA(cudaStreamWaitEvent(c.s, cm->ev_ag, 0));
     }
   }
   for (int j = 0; j < 2; ++j) {  // the older chunk first
@@ -1822,16 +1939,18 @@ slf_status slf_comm_destroy(slf_comm c) {
 
 slf_status slf_comm_set_p2p(slf_comm c, int enable) {
   if (!c) return fail(SLF_ERR_ARG, "null communicator");
+  if (enable < 0 || enable > 3) return fail(SLF_ERR_ARG, "P2P mode %d (bits: 1 statistics, 2 dX)", enable);
   if (enable && c->world > P2P_MAX_RANKS) return fail(SLF_ERR_ARG, "P2P supports <= %d ranks", P2P_MAX_RANKS);
   if (!enable) p2p_release(c);
   c->p2p = enable != 0;
+  c->p2p_mode = enable;
   return SLF_OK;
 }
 
 slf_status slf_comm_status(slf_comm c, int32_t* p2p_timeouts) {
   if (!c || !p2p_timeouts) return fail(SLF_ERR_ARG, "null pointer");
   *p2p_timeouts = 0;
-  if (c->p2p_buf) SLF_CUDA(cudaMemcpy(p2p_timeouts, c->p2p_buf + 192, 4, cudaMemcpyDeviceToHost));
+  if (c->p2p_buf) SLF_CUDA(cudaMemcpy(p2p_timeouts, c->p2p_buf + P2P_ERR_OFF, 4, cudaMemcpyDeviceToHost));
   return SLF_OK;
 }
 

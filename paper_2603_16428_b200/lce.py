@@ -415,9 +415,10 @@ class Comm:
         check(lib().slf_comm_init_callbacks(ctypes.byref(h), rank, world, fa, fr, None), "slf_comm_init_callbacks")
         return cls(h.value, rank, world, keep=(fa, fr))
 
-    def set_p2p(self, enable: bool = True):
-        """Per-chunk statistics by a P2P one-shot all-gather over CUDA IPC (slf_comm_set_p2p)."""
-        check(lib().slf_comm_set_p2p(self.handle, int(bool(enable))), "slf_comm_set_p2p")
+    def set_p2p(self, enable=True):
+        """P2P exchanges over CUDA IPC (slf_comm_set_p2p): True / 1 the per-chunk statistics
+        all-gather, 2 the dX exchange kernel, 3 both; False / 0 off."""
+        check(lib().slf_comm_set_p2p(self.handle, int(enable)), "slf_comm_set_p2p")
         return self
 
     def p2p_timeouts(self) -> int:

@@ -43,7 +43,7 @@ def main():
     ap.add_argument("--budget", type=int, default=3 << 20)
     ap.add_argument("--reduction", default="mean")
     ap.add_argument("--ignore-index", type=int, default=-100)
-    ap.add_argument("--p2p", action="store_true", help="per-chunk statistics by the P2P one-shot all-gather (IPC)")
+    ap.add_argument("--p2p", type=int, default=0, help="P2P exchanges over IPC: 1 statistics, 2 dX, 3 both")
     ap.add_argument("--calls", type=int, default=1, help="calls on the same communicator (the last is saved)")
     a = ap.parse_args()
     dist.init_process_group("gloo", rank=a.rank, world_size=a.world)
@@ -74,7 +74,7 @@ def main():
     v0, v1 = slf.shard_bounds_native(a.V, a.world, a.rank)
     comm = slf.Comm.callbacks(a.rank, a.world, allgather, allreduce)
     if a.p2p:
-        comm.set_p2p(True)
+        comm.set_p2p(a.p2p)
     Wl = W[v0:v1].contiguous()
     for _ in range(a.calls):
         calls["ag"] = calls["ar"] = 0

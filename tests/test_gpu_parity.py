@@ -551,14 +551,15 @@ def test_native_sharded_nccl_world1(slf, red, ign):
     try:
         loss, dX, dW = slf.lce_fwd_bwd_sharded(X, W, t, 5000, comm, ignore_index=ign, reduction=red,
                                                budget_bytes=6 << 20)
-        comm.set_p2p(True)  # P2P statistics exchange (self only at world 1): the same bits
-        lp, dXp, dWp = slf.lce_fwd_bwd_sharded(X, W, t, 5000, comm, ignore_index=ign, reduction=red,
-                                               budget_bytes=6 << 20)
-        torch.cuda.synchronize()
-        assert comm.p2p_timeouts() == 0
-        assert torch.equal(dX.view(torch.int16), dXp.view(torch.int16))
-        assert torch.equal(dW.view(torch.int16), dWp.view(torch.int16))
-        assert torch.equal(loss.view(-1), lp.view(-1))
+        for mode in (1, 3):  # P2P statistics exchange, then also the dX exchange kernel (self only)
+            comm.set_p2p(mode)
+            lp, dXp, dWp = slf.lce_fwd_bwd_sharded(X, W, t, 5000, comm, ignore_index=ign, reduction=red,
+                                                   budget_bytes=6 << 20)
+            torch.cuda.synchronize()
+            assert comm.p2p_timeouts() == 0
+            assert torch.equal(dX.view(torch.int16), dXp.view(torch.int16)), mode
+            assert torch.equal(dW.view(torch.int16), dWp.view(torch.int16)), mode
+            assert torch.equal(loss.view(-1), lp.view(-1)), mode
         comm.set_p2p(False)
         torch.cuda.synchronize()
         assert "n_chunks=1 " not in slf.sharded_plan_describe(900, 256, 5000, 1, 0, 6 << 20)
@@ -627,12 +628,25 @@ def test_native_sharded_callbacks(slf, tmp_path, g, red, budget):
     assert rel_max_err(dX, ref["dX"]) <= GRAD_TOL
     assert rel_max_err(dW, ref["dW"]) <= GRAD_TOL
     assert np.all(res[0]["dX"][inp.t == -100] == 0)
-    p2p = _run_native_ranks(tmp_path / "p2p", g, red, budget, ("--p2p", "--calls", "2"))
+    p2p = _run_native_ranks(tmp_path / "p2p", g, red, budget, ("--p2p", "1", "--calls", "2"))
     for a, b in zip(res, p2p):
         assert int(b["timeouts"]) == 0
         assert int(b["ag"]) == 0 and int(b["ar"]) == nch  # statistics no longer go through the transport
         for k in ("loss", "dX", "dW"):
             assert np.array_equal(a[k], b[k]), k
+    # statistics AND dX through the P2P exchanges (the dX exchange kernel: rank-order sum of the g
+    # fp32 partials of this rank's row slice, bf16 rows stored into every rank's dhidden)
+    px = _run_native_ranks(tmp_path / "p2pdx", g, red, budget, ("--p2p", "3", "--calls", "2"))
+    for a, b in zip(res, px):
+        assert int(b["timeouts"]) == 0
+        assert int(b["ag"]) == 0 and int(b["ar"]) == 0  # no transport collective at all
+        assert np.array_equal(a["loss"], b["loss"]) and np.array_equal(a["dW"], b["dW"])
+        assert np.array_equal(b["dX"], px[0]["dX"])  # every rank holds the same dhidden
+        if g == 2:  # two partials: a + b in either order, bit-identical to the gloo sum
+            assert np.array_equal(a["dX"], b["dX"])
+    dXp = tobf(px[0]["dX"]).view(np.float32).astype(np.float64)
+    assert rel_max_err(dXp, ref["dX"]) <= GRAD_TOL
+    assert np.all(px[0]["dX"][inp.t == -100] == 0)
     if g == 2:  # GEMM launches on 140 of the SMs (8 left to the communicator): same tiles, same bits
         rs = _run_native_ranks(tmp_path / "rsv", g, red, budget, env_extra={"SLF_COMM_SMS": "8"})
         for a, b in zip(res, rs):
