@@ -639,7 +639,8 @@ def test_native_sharded_callbacks(slf, tmp_path, g, red, budget):
     px = _run_native_ranks(tmp_path / "p2pdx", g, red, budget, ("--p2p", "3", "--calls", "2"))
     for a, b in zip(res, px):
         assert int(b["timeouts"]) == 0
-        assert int(b["ag"]) == 0 and int(b["ar"]) == 0  # no transport collective at all
+        # no data-path collective: only the two 80-byte IPC address records (workspace, dhidden)
+        assert int(b["ag"]) == 2 and int(b["ar"]) == 0
         assert np.array_equal(a["loss"], b["loss"]) and np.array_equal(a["dW"], b["dW"])
         assert np.array_equal(b["dX"], px[0]["dX"])  # every rank holds the same dhidden
         if g == 2:  # two partials: a + b in either order, bit-identical to the gloo sum
