@@ -189,6 +189,8 @@ def main():
                          "(-1: the library default, 8)")
     ap.add_argument("--p2p-stats", action="store_true",
                     help="native comm: per-chunk statistics by the P2P one-shot all-gather over CUDA IPC (NEXT-3)")
+    ap.add_argument("--p2p-dx", action="store_true",
+                    help="native comm: dX exchanged by the P2P reduce/all-gather kernel over CUDA IPC (no NCCL)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     args = ap.parse_args()
@@ -269,8 +271,8 @@ def main():
     elif native:  # the library runs the whole sharded step, collectives included (slf_lce_fwd_bwd_sharded)
         try:
             comm = slf.Comm.from_process_group(device=local)
-            if args.p2p_stats:
-                comm.set_p2p(True)
+            if args.p2p_stats or args.p2p_dx:
+                comm.set_p2p((1 if args.p2p_stats else 0) | (2 if args.p2p_dx else 0))
         except Exception as e:  # a transport that cannot start: same kernels, Python orchestration
             native = False
             comm_note = f"native communicator unavailable ({e}); torch.distributed orchestration"
@@ -453,8 +455,9 @@ def main():
                    "plan": slf.sharded_plan_describe(N, H, V, G, 0 if G != g else rank, args.budget) if native else
                    slf.plan_describe(N_l, H, V_l, budget_bytes=ws_budget, schedule=args.schedule),
                    **({"comm": comm_note if (native and comm_note) else
-                       ("native (slf_comm NCCL inside libslf_lce.so" + (", P2P statistics all-gather)" if
-                                args.p2p_stats else ")")) if native else
+                       ("native (slf_comm NCCL inside libslf_lce.so" + (", P2P statistics all-gather" if
+                                args.p2p_stats else "") + (", P2P dX exchange kernel" if args.p2p_dx else "") + ")")
+                       if native else
                        (comm_note or "torch.distributed NCCL (Python orchestration)")} if multi and not dp else {})},
         "tflops": tflops, "tflops_executed": exec_flops / (ms / 1e3) / 1e12,
         "frac_of_peak_burst": tflops / peaks["burst"],
