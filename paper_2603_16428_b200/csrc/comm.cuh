@@ -175,7 +175,8 @@ __global__ void __launch_bounds__(256) p2p_dx_exchange_kernel(DxArgs a) {
       acc[0] = x0.x; acc[1] = x0.y; acc[2] = x0.z; acc[3] = x0.w;
       acc[4] = x1.x; acc[5] = x1.y; acc[6] = x1.z; acc[7] = x1.w;
     }
-    for (int p = 1; p < a.g; ++p) {  // rank order
+#pragma unroll 4
+    for (int p = 1; p < a.g; ++p) {  // rank order (unrolled: the peers' loads are in flight together)
       const float4* src = reinterpret_cast<const float4*>(reinterpret_cast<const float*>(a.part.p[p]) +
                                                           (size_t)r * a.H + c);
       const float4 x0 = src[0], x1 = src[1];

@@ -1522,7 +1522,7 @@ slf_status phase_sharded(Ctx& c, const ShardPlan& sp, slf_comm cm, const void* X
         SLF_CUDA(cudaEventRecord(cm->ev_in, c.s));
         SLF_CUDA(cudaStreamWaitEvent(xs, cm->ev_in, 0));
       }
-      const int blocks = 2 * std::max(8, tl_reserved_sms);
+      const int blocks = 8 * std::max(8, tl_reserved_sms);  // 8 resident blocks per reserved SM
       p2p_dx_exchange_kernel<<<blocks, 256, 0, xs>>>(xa);
       SLF_CUDA(cudaGetLastError());
     } else if (dX) {
