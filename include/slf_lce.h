@@ -270,8 +270,14 @@ slf_status slf_comm_init_callbacks(slf_comm* out, int rank, int world, slf_allga
 slf_status slf_comm_destroy(slf_comm comm);
 /* HOST *rank, *world of the communicator. */
 slf_status slf_comm_rank(slf_comm comm, int* rank, int* world);
-/* P2P one-shot all-gather of the per-chunk statistics (enable = 1), instead
- * of the transport's all-gather.  At the next sharded call every rank allocates a receive buffer
+/* P2P exchanges over CUDA IPC instead of the transport's collectives;
+ * `enable` is a bit mask: 1 = the per-chunk statistics all-gather (below), 2 = the dX exchange
+ * kernel (per chunk, one kernel on the communicator's stream sums the g ranks' fp32 partials of
+ * this rank's row slice in rank order from peer memory and stores the bf16 rows into every rank's
+ * dhidden — reduce-scatter + all-gather + finalize; the workspace and dhidden are exported as IPC
+ * allocation base + offset each call, so they must come from cudaMalloc, e.g. PyTorch's caching
+ * allocator), 3 = both, 0 = off.
+ * Statistics (bit 1): instead of the transport's all-gather.  At the next sharded call every rank allocates a receive buffer
  * [256 B flags | 2 x world x C x 16 B] with cudaMalloc (communicator-owned, like NCCL's own
  * buffers; freed by slf_comm_destroy or enable = 0), the CUDA IPC handles are exchanged through the
  * transport and mapped (cudaIpcMemLazyEnablePeerAccess; NVLink peers, or other processes on the
