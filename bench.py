@@ -79,7 +79,7 @@ class Clocks:
         return False
 
     def summary(self):
-        sm, mx, reasons = [], None, set()
+        sm, pw, mx, reasons = [], [], None, set()
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         for ln in self.lines:
             parts = [p.strip() for p in ln.split(",")]
@@ -90,11 +90,16 @@ class Clocks:
                 mx = float(parts[1])
             except ValueError:
                 continue
+            try:
+                pw.append(float(parts[2]))
+            except ValueError:
+                pass
             for n, v in zip(names, parts[3:7]):
                 if v.lower().startswith("active"):
                     reasons.add(n)
         return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": mx, "reasons": sorted(reasons),
-                "samples": len(sm)}
+                "samples": len(sm), "power_w_median": float(np.median(pw)) if pw else None,
+                "power_w_max": float(np.max(pw)) if pw else None}
 
 
 # ---- oracle timing (cpu_baseline and --impl reference) ---------------------------------------------
@@ -421,6 +426,12 @@ def main():
         return
 
     peaks = load_peaks()
+    ck = clocks.summary()
+    energy = None
+    if ck.get("power_w_median"):  # the step is power-capped: energy per step is what the kernels trade
+        energy = {"j_per_step": ck["power_w_median"] * ms / 1e3,
+                  "tokens_per_joule": N / (ck["power_w_median"] * ms / 1e3) / g,
+                  "note": "median board power during the timed region x device time per step (per GPU)"}
     flops = 6.0 * N * H * V
     tflops = flops / (ms / 1e3) / 1e12
     kinds = prof.kinds
@@ -472,6 +483,7 @@ def main():
         "memory": {"extra_device_bytes": int(extra), "logits_bytes_per_gpu": N_l * V_l * 2,
                    "frac_of_logits_per_gpu": extra / (N_l * V_l * 2), "frac_of_global_logits": extra / (N * V * 2)},
         "clocks": clocks.summary(),
+        "energy": energy,
         "e2e": e2e,
     }
     if g == 1 and not args.no_cpu_baseline:
