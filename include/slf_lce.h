@@ -324,6 +324,18 @@ slf_status slf_lce_fwd_bwd_sharded(const void* hidden, const void* weight_shard,
                                    float* loss_out, void* dhidden, void* dweight_shard, void* workspace,
                                    size_t workspace_bytes, size_t budget_bytes, slf_comm comm, void* stream);
 
+/* Data-parallel (token-sharded) form (SURVEY §8(e) "alternative partition", §8(f) NEXT-3): rank k
+ * holds its own tokens (hidden [N_local, H], targets [N_local]) and the FULL weight [V, H].  The
+ * fused call runs with the MEAN denominator summed across ranks on the device right after the
+ * target scan (so coef and the loss use the GLOBAL valid count, no host round trip); the loss
+ * (SUM / MEAN) is all-reduced, so every rank returns the global loss; dhidden stays local;
+ * dweight is this rank's partial, or with sync_dweight = 1 the all-reduced sum (bf16, NCCL
+ * transport only: SLF_ERR_UNSUPPORTED otherwise).  Workspace as slf_lce_fwd_bwd for N_local. */
+slf_status slf_lce_fwd_bwd_dp(const void* hidden, const void* weight, const int32_t* targets, int64_t N_local,
+                              int64_t H, int64_t V, int32_t ignore_index, int reduction, float scale, float* loss_out,
+                              void* dhidden, void* dweight, void* workspace, size_t workspace_bytes, int schedule,
+                              size_t budget_bytes, int sync_dweight, slf_comm comm, void* stream);
+
 /* Debug: copy the per-tile clock64 trace recorded for the launch selected by the environment
  * variable SLF_DEBUG_TRACE=k (the k-th GEMM launch of the process) into HOST `host` (n values,
  * 8 per tile: MMA tile start / after TMEM-free wait / issued, epilogue start / accumulator ready /

@@ -28,6 +28,7 @@ EXPORTS = ["slf_lce_version", "slf_last_error_string", "slf_lce_workspace_bytes"
            "slf_lce_fwd_bwd_host", "slf_comm_get_unique_id", "slf_comm_init", "slf_comm_init_callbacks",
            "slf_comm_destroy", "slf_comm_rank", "slf_shard_bounds", "slf_lce_sharded_workspace_bytes",
            "slf_lce_sharded_plan_describe", "slf_lce_fwd_bwd_sharded", "slf_comm_set_p2p", "slf_comm_status",
+           "slf_lce_fwd_bwd_dp",
            # include/slf_adam.h (Layer-Adam, host)
            "slf_adam_last_error_string", "slf_adam_simd_width", "slf_adam_create", "slf_adam_destroy",
            "slf_adam_set_config", "slf_adam_set_params", "slf_adam_get_state", "slf_adam_step_host",
@@ -99,6 +100,7 @@ def _declare(lib):
         "slf_lce_sharded_workspace_bytes": (SZ, [I64, I64, I64, INT, INT, SZ]),
         "slf_lce_sharded_plan_describe": (INT, [I64, I64, I64, INT, INT, SZ, ctypes.c_char_p, SZ]),
         "slf_lce_fwd_bwd_sharded": (INT, [P, P, P, I64, I64, I64, I32, INT, F32, P, P, P, P, SZ, SZ, P, P]),
+        "slf_lce_fwd_bwd_dp": (INT, [P, P, P, I64, I64, I64, I32, INT, F32, P, P, P, P, SZ, INT, SZ, INT, P, P]),
         "slf_adam_last_error_string": (ctypes.c_char_p, []),
         "slf_adam_simd_width": (INT, []),
         "slf_adam_create": (INT, [ctypes.POINTER(P), I64, P]),

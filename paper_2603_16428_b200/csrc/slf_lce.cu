@@ -565,6 +565,7 @@ struct Ctx {
   // schedule S: enqueues the chunked input copies once this call's own small H2D copies (targets,
   // tile tables) are queued — copies share the H2D engine in FIFO order
   std::function<slf_status()> enqueue_inputs;
+  std::function<slf_status()> after_prep;  // e.g. the data-parallel all-reduce of n_valid
 };
 
 WsHeader* hdr_of(uint8_t* ws) { return reinterpret_cast<WsHeader*>(ws); }
@@ -661,6 +662,7 @@ slf_status launch_prep(Ctx& c, const int32_t* t, int64_t N, int32_t ignore_index
   ProfScope ps(SLF_PROF_PREP, c.s, 0.0, (double)N * 4);
   prep_targets_kernel<<<1, 1024, 0, c.s>>>(t, N, ignore_index, V_global, hdr_of(c.ws));
   SLF_CUDA(cudaGetLastError());
+  if (c.after_prep) SLF_TRY(c.after_prep());
   return SLF_OK;
 }
 
@@ -1264,6 +1266,27 @@ slf_status comm_join(slf_comm cm, int slot, cudaStream_t s) {
   if (cm->nccl && !cm->cb_allreduce) SLF_CUDA(cudaStreamWaitEvent(s, cm->ev_ar[slot], 0));
   return SLF_OK;
 }
+
+// ---- data-parallel (token-sharded) step with in-library collectives (slf_lce_fwd_bwd_dp) --------
+// The MEAN denominator must be the GLOBAL valid count: right after the target scan the header's
+// n_valid is summed across ranks on the device (no host round trip), so every later kernel (coef,
+// loss) sees the global count.  Float transports carry it as three 16-bit limbs (exact for any
+// count < 2^48 and up to 256 ranks).
+__global__ void u64_to_limbs_kernel(const unsigned long long* n, float* limbs) {
+  const unsigned long long v = *n;
+  limbs[0] = (float)(v & 0xffffull);
+  limbs[1] = (float)((v >> 16) & 0xffffull);
+  limbs[2] = (float)((v >> 32) & 0xffffull);
+}
+__global__ void limbs_to_u64_kernel(const float* limbs, unsigned long long* n) {
+  *n = (unsigned long long)limbs[0] + ((unsigned long long)limbs[1] << 16) + ((unsigned long long)limbs[2] << 32);
+}
+
+slf_status comm_allreduce_now(slf_comm cm, float* buf, size_t count, cudaStream_t s) {
+  SLF_TRY(comm_allreduce_start(cm, buf, count, 0, s));
+  return comm_join(cm, 0, s);
+}
+
 
 void p2p_release(slf_comm cm) {
   for (auto& kv : cm->ipc_open) cudaIpcCloseMemHandle(kv.second);
@@ -2015,6 +2038,67 @@ slf_status slf_lce_fwd_bwd_sharded(const void* hidden, const void* weight_shard,
   ReserveSms reserve(comm->world > 1 || getenv("SLF_COMM_SMS_FORCE") ? comm_sms : 0);
   return phase_sharded(c, sp, comm, hidden, weight_shard, targets, N, H, V_global, ignore_index, reduction, scale,
                        loss_out, dhidden, dweight_shard);
+}
+
+slf_status slf_lce_fwd_bwd_dp(const void* hidden, const void* weight, const int32_t* targets, int64_t N, int64_t H,
+                              int64_t V, int32_t ignore_index, int reduction, float scale, float* loss_out,
+                              void* dhidden, void* dweight, void* workspace, size_t workspace_bytes, int schedule,
+                              size_t budget_bytes, int sync_dweight, slf_comm comm, void* stream) {
+  if (!comm) return fail(SLF_ERR_ARG, "null communicator");
+  if (sync_dweight && !comm->nccl && comm->world > 1)
+    return fail(SLF_ERR_UNSUPPORTED, "sync_dweight needs the NCCL transport (bf16 all-reduce)");
+  SLF_TRY(check_common(hidden, weight, targets, N, H, V, workspace));
+  SLF_TRY(check_outputs(hidden, weight, N, H, V, dhidden, dweight, workspace, workspace_bytes));
+  if (!loss_out || !aligned16(loss_out)) return fail(SLF_ERR_ALIGN, "loss_out must be a 16-byte aligned pointer");
+  if (reduction < SLF_SUM || reduction > SLF_NONE) return fail(SLF_ERR_ARG, "bad reduction %d", reduction);
+  if (schedule < SLF_SCHED_AUTO || schedule > SLF_SCHED_S) return fail(SLF_ERR_ARG, "schedule %d", schedule);
+  if ((dhidden && !aligned16(dhidden)) || (dweight && !aligned16(dweight)))
+    return fail(SLF_ERR_ALIGN, "gradient pointers must be 16-byte aligned");
+  Ctx c;
+  SLF_TRY(setup(c, N, H, V, budget_bytes, workspace, workspace_bytes, stream, schedule, true));
+  // scratch for the limbs: the header's spare words (WsHeader::pad)
+  WsHeader* hdr = reinterpret_cast<WsHeader*>(hdr_of(c.ws));
+  float* limbs = reinterpret_cast<float*>(&hdr->pad[0]);
+  if (reduction == SLF_MEAN && comm->world > 1) {
+    c.after_prep = [&]() -> slf_status {
+      if (comm->nccl) {
+        NcclApi& api = nccl_api();
+        SLF_CUDA(cudaEventRecord(comm->ev_in, c.s));
+        SLF_CUDA(cudaStreamWaitEvent(comm->cs, comm->ev_in, 0));
+        const ncclResult_t r = api.AllReduce(&hdr->n_valid, &hdr->n_valid, 1, ncclUint64, ncclSum, comm->nccl, comm->cs);
+        if (r != ncclSuccess) return comm_fail_nccl(r, "ncclAllReduce(n_valid)");
+        SLF_CUDA(cudaEventRecord(comm->ev_ag, comm->cs));
+        SLF_CUDA(cudaStreamWaitEvent(c.s, comm->ev_ag, 0));
+        return SLF_OK;
+      }
+      u64_to_limbs_kernel<<<1, 1, 0, c.s>>>(&hdr->n_valid, limbs);
+      SLF_CUDA(cudaGetLastError());
+      SLF_TRY(comm_allreduce_now(comm, limbs, 3, c.s));
+      limbs_to_u64_kernel<<<1, 1, 0, c.s>>>(limbs, &hdr->n_valid);
+      SLF_CUDA(cudaGetLastError());
+      return SLF_OK;
+    };
+  }
+  if (c.plan.sched == SLF_SCHED_S) {
+    SLF_TRY(phase_s(c, hidden, weight, targets, N, H, V, ignore_index, reduction, scale, loss_out, dhidden, dweight));
+  } else {
+    slf_shardstat* st = reinterpret_cast<slf_shardstat*>(c.ws + c.plan.off_shard);
+    slf_rowstat* rs = reinterpret_cast<slf_rowstat*>(c.ws + c.plan.off_rowstat);
+    SLF_TRY(phase_stats(c, hidden, weight, targets, N, H, V, 0, ignore_index, st));
+    SLF_TRY(phase_combine(c, st, 1, targets, N, 0, V, V, ignore_index, reduction, scale, loss_out, rs));
+    SLF_TRY(phase_backward(c, hidden, weight, rs, N, H, V, 1.0f, dhidden, 0, dweight));
+  }
+  if (comm->world > 1 && reduction != SLF_NONE) SLF_TRY(comm_allreduce_now(comm, loss_out, 1, c.s));
+  if (sync_dweight && dweight && comm->world > 1) {  // the ordinary data-parallel gradient sync (bf16)
+    NcclApi& api = nccl_api();
+    SLF_CUDA(cudaEventRecord(comm->ev_in, c.s));
+    SLF_CUDA(cudaStreamWaitEvent(comm->cs, comm->ev_in, 0));
+    const ncclResult_t r = api.AllReduce(dweight, dweight, (size_t)V * H, ncclBfloat16, ncclSum, comm->nccl, comm->cs);
+    if (r != ncclSuccess) return comm_fail_nccl(r, "ncclAllReduce(dW)");
+    SLF_CUDA(cudaEventRecord(comm->ev_ag, comm->cs));
+    SLF_CUDA(cudaStreamWaitEvent(c.s, comm->ev_ag, 0));
+  }
+  return SLF_OK;
 }
 
 // Debug: how many clusters of `cluster` CTAs of the GEMM kernel (its smem footprint) fit at once.

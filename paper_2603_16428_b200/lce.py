@@ -498,6 +498,30 @@ def lce_fwd_bwd_sharded(hidden, weight_shard, targets, V_global: int, comm: Comm
     return (loss if reduction == "none" else loss[0]), dX, dW
 
 
+
+def lce_fwd_bwd_dp(hidden, weight, targets, comm: Comm, ignore_index: int = -100, reduction: str = "mean",
+                   scale: float = 1.0, sync_dweight: bool = False, budget_bytes: int = 0, workspace=None, out=None,
+                   schedule: str = "auto"):
+    """Data-parallel fused LCE on this rank (slf_lce_fwd_bwd_dp): this rank's tokens, the full W;
+    returns (global loss, local dhidden, dW partial — or the all-reduced dW with sync_dweight)."""
+    hidden, weight, targets = _prep(hidden, weight, targets)
+    N, H = hidden.shape
+    V = weight.shape[0]
+    dev = hidden.device
+    if out is not None:
+        loss, dX, dW = out
+    else:
+        loss = torch.empty(N if reduction == "none" else 1, dtype=torch.float32, device=dev)
+        dX = torch.empty_like(hidden)
+        dW = torch.empty_like(weight)
+    if workspace is None:
+        workspace = alloc_workspace(N, H, V, dev, schedule, budget_bytes)
+    check(lib().slf_lce_fwd_bwd_dp(hidden.data_ptr(), weight.data_ptr(), targets.data_ptr(), N, H, V, ignore_index,
+                                   REDUCTIONS[reduction], float(scale), loss.data_ptr(), _ptr(dX), _ptr(dW),
+                                   workspace.data_ptr(), workspace.numel(), SCHEDULES[schedule], budget_bytes,
+                                   int(bool(sync_dweight)), comm.handle, _stream_ptr(dev)), "slf_lce_fwd_bwd_dp")
+    return (loss if reduction == "none" else loss[0]), dX, dW
+
 class Profile:
     """Context manager over slf_profile_begin/end: per-kernel-kind device ms, launches, FLOPs, bytes."""
 

@@ -45,6 +45,8 @@ def main():
     ap.add_argument("--ignore-index", type=int, default=-100)
     ap.add_argument("--p2p", type=int, default=0, help="P2P exchanges over IPC: 1 statistics, 2 dX, 3 both")
     ap.add_argument("--calls", type=int, default=1, help="calls on the same communicator (the last is saved)")
+    ap.add_argument("--mode", default="vocab", choices=["vocab", "dp"],
+                    help="vocab: slf_lce_fwd_bwd_sharded; dp: slf_lce_fwd_bwd_dp on this rank's tokens")
     a = ap.parse_args()
     dist.init_process_group("gloo", rank=a.rank, world_size=a.world)
     torch.cuda.set_device(0)
@@ -76,17 +78,24 @@ def main():
     if a.p2p:
         comm.set_p2p(a.p2p)
     Wl = W[v0:v1].contiguous()
+    n0, n1 = a.N * a.rank // a.world, a.N * (a.rank + 1) // a.world
     for _ in range(a.calls):
         calls["ag"] = calls["ar"] = 0
-        loss, dX, dW = slf.lce_fwd_bwd_sharded(X, Wl, t, a.V, comm, ignore_index=a.ignore_index,
-                                               reduction=a.reduction, budget_bytes=a.budget)
+        if a.mode == "dp":
+            loss, dX, dW = slf.lce_fwd_bwd_dp(X[n0:n1].contiguous(), W, t[n0:n1].contiguous(), comm,
+                                              ignore_index=a.ignore_index, reduction=a.reduction,
+                                              budget_bytes=a.budget)
+            v0, v1 = n0, n1  # saved: this rank's token rows
+        else:
+            loss, dX, dW = slf.lce_fwd_bwd_sharded(X, Wl, t, a.V, comm, ignore_index=a.ignore_index,
+                                                   reduction=a.reduction, budget_bytes=a.budget)
         torch.cuda.synchronize()
     timeouts = comm.p2p_timeouts()
     comm.close()
     np.savez(os.path.join(a.out, f"rank{a.rank}.npz"), loss=loss.detach().cpu().numpy(),
              dX=dX.view(torch.int16).cpu().numpy(), dW=dW.view(torch.int16).cpu().numpy(), v0=v0, v1=v1,
              ag=calls["ag"], ar=calls["ar"], timeouts=timeouts,
-             plan=slf.sharded_plan_describe(a.N, a.H, a.V, a.world, a.rank, a.budget))
+             plan=slf.sharded_plan_describe(a.N, a.H, a.V, a.world, a.rank, a.budget) if a.mode == "vocab" else "dp")
     dist.destroy_process_group()
 
 

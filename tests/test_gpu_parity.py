@@ -707,3 +707,45 @@ def test_no_device_allocation_in_call(slf):
     assert free1 == free0, (free0, free1)
     assert torch.cuda.max_memory_allocated() == peak0
     assert torch.isfinite(out[0]).all()
+
+
+@pytest.mark.parametrize("red", ["mean", "sum", "none"])
+@pytest.mark.parametrize("sched", SCHEDS)
+def test_native_dp_world1(slf, red, sched):
+    """slf_lce_fwd_bwd_dp over the library's NCCL communicator at world size 1 is exactly the fused
+    call (the n_valid and loss all-reduces of one rank are identities)."""
+    inp = synth.make_inputs(700, 256, 3000, seed=26, alpha=4.0, dist="zipf")
+    X, W, t = to_dev(inp, torch)
+    comm = slf.Comm.nccl(slf.comm_unique_id(), 0, 1, torch.cuda.current_device())
+    try:
+        ld, dXd, dWd = slf.lce_fwd_bwd_dp(X, W, t, comm, reduction=red, scale=0.5, sync_dweight=True,
+                                          budget_bytes=2 << 20, schedule=sched)
+        lf, dXf, dWf = slf.lce_fwd_bwd(X, W, t, reduction=red, scale=0.5, budget_bytes=2 << 20, schedule=sched)
+        torch.cuda.synchronize()
+    finally:
+        comm.close()
+    assert torch.equal(ld.reshape(-1), lf.reshape(-1))
+    assert torch.equal(dXd, dXf) and torch.equal(dWd, dWf)
+
+
+@pytest.mark.parametrize("g,red", [(2, "mean"), (3, "mean"), (2, "sum")])
+def test_native_dp_callbacks(slf, tmp_path, g, red):
+    """g ranks of slf_lce_fwd_bwd_dp as g processes on this GPU (gloo callback transport): each rank
+    holds a contiguous token slice and the full W; the MEAN denominator is summed on the device
+    across ranks, every rank returns the global loss; its dhidden rows and the sum of the ranks' dW
+    partials match the oracle on the whole batch."""
+    res = _run_native_ranks(tmp_path, g, red, 2 << 20, ("--mode", "dp"))
+    inp = synth.make_inputs(900, 256, 5000, seed=21, alpha=4.0, dist="zipf")
+    Xo, Wo, to = oracle_inputs(inp)
+    ref = oracle.lce(Xo, Wo, to, reduction=red)
+    for r in res:
+        assert np.array_equal(r["loss"], res[0]["loss"])
+        assert int(r["ar"]) == (2 if red == "mean" else 1)  # n_valid limbs + loss (SUM: loss only)
+    assert_loss_close(float(res[0]["loss"].reshape(-1)[0]), ref["loss"], red)
+    tobf = lambda a: a.astype(np.int16).view(np.uint16).astype(np.uint32) << 16  # noqa: E731
+    dX = np.concatenate([tobf(r["dX"]).view(np.float32).astype(np.float64) for r in res])
+    assert [int(r["v0"]) for r in res] + [int(res[-1]["v1"])] == [900 * k // g for k in range(g + 1)]
+    dW = sum(tobf(r["dW"]).view(np.float32).astype(np.float64) for r in res)
+    assert rel_max_err(dX, ref["dX"]) <= GRAD_TOL
+    assert rel_max_err(dW, ref["dW"]) <= GRAD_TOL
+    assert np.all(np.concatenate([r["dX"] for r in res])[inp.t == -100] == 0)
