@@ -82,7 +82,7 @@ def main():
     for _ in range(a.calls):
         calls["ag"] = calls["ar"] = 0
         if a.mode == "dp":
-            loss, dX, dW = slf.lce_fwd_bwd_dp(X[n0:n1].contiguous(), W, t[n0:n1].contiguous(), comm,
+            loss, dX, dW = slf.lce_fwd_bwd_dp(X[n0:n1].clone(), W, t[n0:n1].clone(), comm,
                                               ignore_index=a.ignore_index, reduction=a.reduction,
                                               budget_bytes=a.budget)
             v0, v1 = n0, n1  # saved: this rank's token rows
