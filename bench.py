@@ -295,6 +295,13 @@ def main():
     if dp:
         from paper_2603_16428_b200.sharded import TokenShardedLCE
         dpm = TokenShardedLCE(budget_bytes=args.budget, schedule=args.schedule)
+        dp_comm = None
+        if args.comm == "native":  # slf_lce_fwd_bwd_dp: global MEAN denominator and syncs inside the library
+            try:
+                dp_comm = slf.Comm.from_process_group(device=local)
+            except Exception as e:
+                comm_note = f"native communicator unavailable ({e}); torch.distributed orchestration"
+                print(comm_note, file=sys.stderr)
     elif multi and not native:
         if sharded.schedule == "S":
             C_s, _ = slf.s_plan(N, H, V_l, ws_budget)
@@ -308,6 +315,10 @@ def main():
                             schedule=args.schedule)
             return loss
         if dp:
+            if dp_comm is not None:
+                l, _, _ = slf.lce_fwd_bwd_dp(Xs, W, ts, dp_comm, sync_dweight=True, workspace=ws, out=(loss, dX, dW),
+                                             budget_bytes=args.budget, schedule=args.schedule)
+                return l
             l, _, _ = dpm.forward_backward(Xs, W, ts, n_valid_global=n_valid_global, workspace=ws,
                                            out=(loss, dX, dW))
             return l
@@ -422,6 +433,8 @@ def main():
         if multi:
             if native:
                 comm.close()
+            if dp and dp_comm is not None:
+                dp_comm.close()
             dist.destroy_process_group()
         return
 
@@ -465,6 +478,8 @@ def main():
                    "l2": "inputs larger than L2 (W alone is %.2f GB vs 126 MB L2); no flush" % (V_l * H * 2 / 1e9),
                    "plan": slf.sharded_plan_describe(N, H, V, G, 0 if G != g else rank, args.budget) if native else
                    slf.plan_describe(N_l, H, V_l, budget_bytes=ws_budget, schedule=args.schedule),
+                   **({"comm": ("native (slf_lce_fwd_bwd_dp, slf_comm NCCL)" if dp_comm is not None else
+                                (comm_note or "torch.distributed NCCL (TokenShardedLCE)"))} if dp else {}),
                    **({"comm": comm_note if (native and comm_note) else
                        ("native (slf_comm NCCL inside libslf_lce.so" + (", P2P statistics all-gather" if
                                 args.p2p_stats else "") + (", P2P dX exchange kernel" if args.p2p_dx else "") + ")")
@@ -492,6 +507,8 @@ def main():
     if multi:
         if native:
             comm.close()
+        if dp and dp_comm is not None:
+            dp_comm.close()
         dist.destroy_process_group()
 
 
