@@ -32,11 +32,14 @@
  *    Data errors (a valid target outside [0, V_global)) are asynchronous: the
  *    loss becomes NaN and slf_lce_status() reports the count.
  *  - No global mutable state except a thread-local last-error string, a
- *    per-device attribute cache and a per-device 8 MB pinned HOST ring that
- *    stages the per-call tile tables (allocated on first use, never freed);
- *    calls on different streams are independent provided they use different
- *    workspaces.  The calls are not CUDA-graph-capture safe (they copy tile
- *    tables from that host ring).
+ *    per-device attribute cache, a per-device 8 MB pinned HOST ring that
+ *    stages the per-call tile tables (allocated on first use, never freed),
+ *    the host-input call's per-device copy stream, events and staging-buffer
+ *    release events, and memoised tile tables; communicators (slf_comm) and
+ *    Layer-Adam handles (slf_adam.h) are explicit objects.  Calls on different
+ *    streams are independent provided they use different workspaces.  The
+ *    calls are not CUDA-graph-capture safe (they copy tile tables from that
+ *    host ring).
  *  - Requirements: H % 8 == 0 (16-byte TMA row strides), N >= 1, V_local >= 1,
  *    an sm_100 device (SLF_ERR_UNSUPPORTED otherwise).
  */
