@@ -67,7 +67,7 @@ class Clocks:
 
     def _read(self):
         for line in self.proc.stdout:
-            self.lines.append(line.strip())
+            self.lines.append((time.perf_counter(), line.strip()))
 
     def __exit__(self, *exc):
         if self.proc:
@@ -78,10 +78,12 @@ class Clocks:
                 self.proc.kill()
         return False
 
-    def summary(self):
+    def summary(self, t0=None, t1=None):
+        """Samples taken inside [t0, t1] (perf_counter seconds; the timed region), else all."""
         sm, pw, mx, reasons = [], [], None, set()
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for ln in self.lines:
+        inside = [ln for ts, ln in self.lines if (t0 is None or ts >= t0) and (t1 is None or ts <= t1)]
+        for ln in (inside or [ln for _, ln in self.lines]):
             parts = [p.strip() for p in ln.split(",")]
             if len(parts) < 7:
                 continue
@@ -347,11 +349,13 @@ def main():
         time.sleep(0.3)
         barrier()
         torch.cuda.synchronize()
+        w0 = time.perf_counter()
         e0.record(stream)
         for _ in range(args.steps):
             step()
         e1.record(stream)
         torch.cuda.synchronize()
+        w1 = time.perf_counter()
         barrier()
     ms = e0.elapsed_time(e1) / args.steps
     # Per-kernel breakdown (roofline): the same K steps again with a CUDA-event pair around every
@@ -439,12 +443,13 @@ def main():
         return
 
     peaks = load_peaks()
-    ck = clocks.summary()
+    ck = clocks.summary(w0, w1)
     energy = None
     if ck.get("power_w_median"):  # the step is power-capped: energy per step is what the kernels trade
         energy = {"j_per_step": ck["power_w_median"] * ms / 1e3,
                   "tokens_per_joule": N / (ck["power_w_median"] * ms / 1e3) / g,
-                  "note": "median board power during the timed region x device time per step (per GPU)"}
+                  "note": "median board power (nvidia-smi power.draw samples inside the timed region) x device "
+                          "time per step (per GPU)"}
     flops = 6.0 * N * H * V
     tflops = flops / (ms / 1e3) / 1e12
     kinds = prof.kinds
@@ -497,7 +502,7 @@ def main():
         "gpu_launches": launches,
         "memory": {"extra_device_bytes": int(extra), "logits_bytes_per_gpu": N_l * V_l * 2,
                    "frac_of_logits_per_gpu": extra / (N_l * V_l * 2), "frac_of_global_logits": extra / (N * V * 2)},
-        "clocks": clocks.summary(),
+        "clocks": ck,
         "energy": energy,
         "e2e": e2e,
     }
