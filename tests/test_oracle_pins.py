@@ -410,3 +410,24 @@ def test_oracle_property_torch(N, H, V, seed, red, ign, p_ign, scale):
     np.testing.assert_allclose(out["dW"], Wt.grad.numpy(), rtol=1e-10, atol=1e-12)
     # invariant: the gradient rows of the logits sum to zero, so sum_v dW_v = 0
     np.testing.assert_allclose(out["dW"].sum(axis=0), 0.0, atol=1e-12 * max(1.0, np.abs(out["dW"]).max()) * V)
+
+
+@settings(max_examples=40, deadline=None, derandomize=True)
+@given(n=st.integers(1, 40), T=st.integers(1, 6), seed=st.integers(0, 2**31 - 1),
+       lr=st.sampled_from([1e-4, 1e-3, 3e-2]), b1=st.sampled_from([0.0, 0.5, 0.9]),
+       b2=st.sampled_from([0.9, 0.999]), eps=st.sampled_from([1e-8, 1e-3]), wd=st.sampled_from([0.0, 0.01, 0.3]),
+       adamw=st.booleans(), gs=st.sampled_from([1.0, 0.25, 4.0]))
+def test_adam_property_torch(n, T, seed, lr, b1, b2, eps, wd, adamw, gs):
+    """The Layer-Adam oracle against torch.optim.AdamW / Adam (float64) over random hyper-parameters,
+    step counts and sizes, including beta1 = 0 and large eps."""
+    torch = pytest.importorskip("torch")
+    rng = np.random.default_rng(seed)
+    p0 = rng.standard_normal(n)
+    grads = [rng.standard_normal(n) * 10.0 ** rng.uniform(-3, 1, n) for _ in range(T)]
+    p, m, v, _ = oracle.adam_steps(p0, grads, lr, b1, b2, eps, wd, adamw, grad_scale=gs)
+    pt = torch.tensor(p0, requires_grad=True)
+    opt = (torch.optim.AdamW if adamw else torch.optim.Adam)([pt], lr=lr, betas=(b1, b2), eps=eps, weight_decay=wd)
+    for g in grads:
+        pt.grad = torch.tensor(g * gs)
+        opt.step()
+    np.testing.assert_allclose(p, pt.detach().numpy(), rtol=1e-12, atol=1e-14)
