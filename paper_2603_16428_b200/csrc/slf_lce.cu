@@ -182,7 +182,7 @@ slf_status tmap_kmajor(CUtensorMap* m, const void* base, int64_t K, int64_t rows
 slf_status make_tmap_mn3d(CUtensorMap* m, const void* base, uint64_t MN, uint64_t K, uint64_t ld_bytes, uint32_t atoms) {
   auto fn = encode_fn();
   if (!fn) return fail(SLF_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
-  cuuint64_t dims[3] = {64, K, MN / 64};
+  cuuint64_t dims[3] = {64, K, (MN + 63) / 64};  // MN % 64 != 0: the last atom reads past MN (see s_build_bwd)
   cuuint64_t strides[2] = {ld_bytes, 128};
   cuuint32_t box[3] = {64, 64, atoms};
   cuuint32_t estr[3] = {1, 1, 1};
@@ -236,6 +236,7 @@ struct ProbSpec {
   int epi = EPI_F32;
   bool a_mn = false, b_mn = false;
   int a_split = NO_SPLIT, c_split = NO_SPLIT;
+  bool a3d_force = false;  // ta is a 3-D MN-major map although M % 64 != 0 (over-read is harmless)
 };
 
 int prof_kind_of(int epi) {
@@ -342,7 +343,8 @@ slf_status launch_group_cfg(DevInfo* dev, ProbSpec* ps, int n, cudaStream_t s, c
     tm.m[MAPS_PER_PROB * np + 3] = ps[p].ta2;
     tm.m[MAPS_PER_PROB * np + 4] = ps[p].tc2;
     g.p[np] = Prob{a, ps[p].epi, ps[p].a_mn ? 1 : 0, ps[p].b_mn ? 1 : 0, total, ps[p].a_split, ps[p].c_split,
-                   (ps[p].a_mn && mn3d_for(a.M)) ? 1 : 0, (ps[p].b_mn && mn3d_for(a.N)) ? 1 : 0};
+                   (ps[p].a_mn && (ps[p].a3d_force || mn3d_for(a.M))) ? 1 : 0,
+                   (ps[p].b_mn && mn3d_for(a.N)) ? 1 : 0};
     total += a.num_tiles;
     flops += 2.0 * a.M * a.N * (double)a.K;
     ++np;
@@ -527,7 +529,7 @@ bool plan_s(int64_t N, int64_t H, int64_t V, size_t budget, Plan* out) {
   int64_t best = 0;
   for (int64_t C = 256; C <= Nmax; C += 256) {
     const size_t part = align_up((size_t)tiles_v * 2 * C * 8, 1024);  // 2C: room for extended chunks
-    const size_t tot = p.off_part + part + (size_t)C * p.ld_stash * 2;
+    const size_t tot = p.off_part + part + (size_t)C * p.ld_stash * 2 + 256;
     if (tot <= budget) best = C;
     else break;
   }
@@ -535,7 +537,7 @@ bool plan_s(int64_t N, int64_t H, int64_t V, size_t budget, Plan* out) {
   p.C = best;
   p.nCh = (N + best - 1) / best;
   p.off_stash = p.off_part + align_up((size_t)tiles_v * 2 * best * 8, 1024);
-  p.total = p.off_stash + (size_t)best * p.ld_stash * 2;
+  p.total = p.off_stash + (size_t)best * p.ld_stash * 2 + 256;  // tail pad: 3-D stash loads over-read < 128 B
   p.fwd_bytes = p.total - p.off_part;
   *out = p;
   return true;
@@ -947,7 +949,16 @@ slf_status s_build_bwd(Ctx& c, const SArgs& a, const SChunk& k, void* dXc, int d
   if (dW) {  // dW (+)= G_P^T X_chunk : A = G_P^T (MN-major; K = rows split ws | ext), B = X_chunk (MN-major)
     ProbSpec& q = ps[(*n)++];
     q = ProbSpec{};
-    SLF_TRY(tmap_mnmajor(&q.ta, stash, a.V_l, main_rows, p.ld_stash));
+    if (!k.ext && a.V_l % 64 && mn3d_enabled()) {
+      // The workspace stash (no second segment): a 3-D map even when V_l % 64 != 0 (e.g. 16032
+      // vocabulary rows per rank at g = 8).  Its last atom reads up to 63 columns past V_l — rows
+      // >= M of the A operand, whose products only reach dW rows >= V_l, which the store map
+      // clips; past the last stash row it reads into the workspace's 256-byte tail pad.
+      SLF_TRY(make_tmap_mn3d(&q.ta, stash, (uint64_t)a.V_l, (uint64_t)main_rows, (uint64_t)p.ld_stash * 2, 2));
+      q.a3d_force = true;
+    } else {
+      SLF_TRY(tmap_mnmajor(&q.ta, stash, a.V_l, main_rows, p.ld_stash));
+    }
     if (k.ext) {
       SLF_TRY(tmap_mnmajor(&q.ta2, k.ext_base, a.V_l, k.ext, p.ld_stash));
       q.a_split = (int)main_rows;
