@@ -21,50 +21,30 @@ __device__ __forceinline__ float coef_of(int reduction, float scale, unsigned lo
   return (reduction == SLF_MEAN) ? (n_valid ? scale / (float)n_valid : 0.f) : scale;
 }
 
-// Block-wide fixed-order (m, s) merge of one row's tile partials [tile][rows] (256 threads).
-__device__ __forceinline__ float2 merge_row_tiles(const float2* __restrict__ partials, int tiles, int rows, int i,
-                                                  float* red) {
-  const int tid = threadIdx.x;
-  float m = -INFINITY;
-  for (int k = tid; k < tiles; k += 256) m = fmaxf(m, partials[(size_t)k * rows + i].x);
-  red[tid] = m;
-  __syncthreads();
-  for (int o = 128; o > 0; o >>= 1) {
-    if (tid < o) red[tid] = fmaxf(red[tid], red[tid + o]);
-    __syncthreads();
-  }
-  const float M = red[0];
-  __syncthreads();
-  float s = 0.f;
-  for (int k = tid; k < tiles; k += 256) {
+// This shard's per-row ShardStat {m, s, z_t, hit} of a chunk, one THREAD per row: the tile partials
+// [tile][row] are read coalesced across the rows of a warp, max then sum in tile order
+// (deterministic).  (A block per row spent most of its time in block-wide barriers for the ~63
+// tiles of a g = 8 shard: 17 us per chunk at C = 3072.)
+__global__ void __launch_bounds__(128) shard_rows_tpr_kernel(const float2* __restrict__ partials, int tiles, int rows,
+                                                             const float* __restrict__ zt,
+                                                             const int32_t* __restrict__ t, int64_t vocab_start,
+                                                             int64_t V_l, int32_t ignore_index,
+                                                             slf_shardstat* __restrict__ out) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= rows) return;
+  float M = -INFINITY;
+#pragma unroll 8
+  for (int k = 0; k < tiles; ++k) M = fmaxf(M, partials[(size_t)k * rows + i].x);
+  float S = 0.f;
+#pragma unroll 8
+  for (int k = 0; k < tiles; ++k) {
     const float2 p = partials[(size_t)k * rows + i];
-    s += p.y * ex2((p.x - M) * LOG2E);
+    S += p.y * ex2((p.x - M) * LOG2E);
   }
-  red[tid] = s;
-  __syncthreads();
-  for (int o = 128; o > 0; o >>= 1) {
-    if (tid < o) red[tid] += red[tid + o];
-    __syncthreads();
-  }
-  const float S = red[0];
-  __syncthreads();
-  return make_float2(M, S);
-}
-
-// This shard's per-row ShardStat {m, s, z_t, hit} of a chunk: one block per row.
-__global__ void __launch_bounds__(256) shard_rows_kernel(const float2* __restrict__ partials, int tiles, int rows,
-                                                        const float* __restrict__ zt, const int32_t* __restrict__ t,
-                                                        int64_t vocab_start, int64_t V_l, int32_t ignore_index,
-                                                        slf_shardstat* __restrict__ out) {
-  __shared__ float red[256];
-  const int i = blockIdx.x;
-  const float2 ms = merge_row_tiles(partials, tiles, rows, i, red);
-  if (threadIdx.x == 0) {
-    const int32_t tt = t[i];
-    const int64_t loc = (int64_t)tt - vocab_start;
-    const bool hit = tt != ignore_index && loc >= 0 && loc < V_l;
-    out[i] = slf_shardstat{ms.x, ms.y, hit ? zt[i] : 0.f, hit ? 1.f : 0.f};
-  }
+  const int32_t tt = t[i];
+  const int64_t loc = (int64_t)tt - vocab_start;
+  const bool hit = tt != ignore_index && loc >= 0 && loc < V_l;
+  out[i] = slf_shardstat{M, S, hit ? zt[i] : 0.f, hit ? 1.f : 0.f};
 }
 
 // One block (256 threads) per row of the chunk.  The row's global statistics come from the g
