@@ -749,3 +749,27 @@ def test_native_dp_callbacks(slf, tmp_path, g, red):
     assert rel_max_err(dX, ref["dX"]) <= GRAD_TOL
     assert rel_max_err(dW, ref["dW"]) <= GRAD_TOL
     assert np.all(np.concatenate([r["dX"] for r in res])[inp.t == -100] == 0)
+
+
+@pytest.mark.parametrize("N,H,V", [(1, 8, 3), (257, 16, 130), (600, 72, 1000)])
+@pytest.mark.parametrize("mode", [0, 3])
+def test_native_sharded_edges_world1(slf, N, H, V, mode):
+    """The native sharded call at edge shapes (one token, tiny vocabulary, H not a multiple of 64,
+    ragged last chunk), over NCCL (mode 0) and over the P2P exchanges (mode 3), against the oracle."""
+    inp = synth.make_inputs(N, H, V, seed=31, alpha=4.0, dist="uniform", ignore_frac=0.2)
+    X, W, t = to_dev(inp, torch)
+    comm = slf.Comm.nccl(slf.comm_unique_id(), 0, 1, torch.cuda.current_device())
+    try:
+        if mode:
+            comm.set_p2p(mode)
+        loss, dX, dW = slf.lce_fwd_bwd_sharded(X, W, t, V, comm, reduction="mean", budget_bytes=1 << 20)
+        torch.cuda.synchronize()
+        assert comm.p2p_timeouts() == 0
+    finally:
+        comm.close()
+    Xo, Wo, to = oracle_inputs(inp)
+    ref = oracle.lce(Xo, Wo, to, reduction="mean")
+    if (inp.t != -100).any():
+        assert_loss_close(float(loss), ref["loss"], "mean")
+    assert rel_max_err(bf16_to_np64(dX), ref["dX"]) <= GRAD_TOL
+    assert rel_max_err(bf16_to_np64(dW), ref["dW"]) <= GRAD_TOL
