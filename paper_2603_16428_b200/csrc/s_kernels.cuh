@@ -143,14 +143,8 @@ __global__ void __launch_bounds__(256) combine_transform_kernel(
   const float cg = sM, lse2 = sLse;
   for (int k = tid; k < tiles; k += 256) r_t[k] = cg * ex2(r_t[k] * LOG2E - lse2);
   __syncthreads();
-  // G_P = p~ * r_t, in place, 8 bf16 per 16-byte access.  Software-pipelined: the next batch's
-  // loads are issued before this batch is scaled and stored, so loads stay in flight during stores.
+  // G_P = p~ * r_t, in place, 8 bf16 per 16-byte access.
   for (int64_t q0 = tid;;) {
-    const int64_t q1 = q0 + 256 * U;
-    uint4 nx[U];
-#pragma unroll
-    for (int u = 0; u < U; ++u)
-      if (q1 + u * 256 < groups) nx[u] = row[q1 + u * 256];
 #pragma unroll
     for (int u = 0; u < U; ++u) {
       const int64_t q = q0 + u * 256;
@@ -164,10 +158,11 @@ __global__ void __launch_bounds__(256) combine_transform_kernel(
         row[q] = x;
       }
     }
-    if (q1 >= groups) break;
-    q0 = q1;
+    q0 += 256 * U;
+    if (q0 >= groups) break;
 #pragma unroll
-    for (int u = 0; u < U; ++u) w[u] = nx[u];
+    for (int u = 0; u < U; ++u)
+      if (q0 + u * 256 < groups) w[u] = row[q0 + u * 256];
   }
 }
 
