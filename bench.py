@@ -133,6 +133,27 @@ def oracle_rows_for(inp_X, W64, t, seconds: float, cap: int) -> int:
     return int(np.clip((seconds - a) / b, 8, cap))
 
 
+def cpu_info():
+    """CPU model (lscpu / /proc/cpuinfo) and the BLAS numpy runs on (threadpoolctl): SURVEY §8(d) d7."""
+    model = None
+    try:
+        for ln in open("/proc/cpuinfo"):
+            if ln.startswith("model name"):
+                model = ln.split(":", 1)[1].strip()
+                break
+    except OSError:
+        pass
+    blas = None
+    try:
+        from threadpoolctl import threadpool_info
+        b = [d for d in threadpool_info() if d.get("user_api") == "blas"]
+        if b:
+            blas = f"{b[0].get('internal_api')} {b[0].get('version')} ({b[0].get('num_threads')} threads)"
+    except Exception:
+        pass
+    return {"cpu_model": model, "blas": blas}
+
+
 def cpu_baseline(inp, cfg_name, target_s=12.0):
     W64 = synth.bf16_bits_to_f64(inp.W)
     rows = oracle_rows_for(inp.X, W64, inp.t, target_s, min(2048, inp.N))
@@ -140,7 +161,7 @@ def cpu_baseline(inp, cfg_name, target_s=12.0):
     return {"value": rows / dt, "unit": UNIT, "cores": cpu_cores(), "kind": "oracle",
             "sample": f"{rows} tokens of the {cfg_name} workload at full H={inp.H}, V={inp.V} (numpy fp64, "
                       f"materialised logits; per-token work is 6*H*V so tokens/s extrapolates linearly)",
-            "seconds": dt}
+            "seconds": dt, **cpu_info()}
 
 
 def run_reference(args):
@@ -164,7 +185,7 @@ def run_reference(args):
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": f"{args.config} LM head N={c['N']} H={c['H']} V={c['V']} (oracle: bounded row sample)",
                    "N": c["N"], "H": c["H"], "V": c["V"], "sample_tokens": rows},
-        "cpu_baseline": {"value": v, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": sample},
+        "cpu_baseline": {"value": v, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": sample, **cpu_info()},
         "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }), flush=True)
 
