@@ -514,6 +514,7 @@ def main():
         "tflops": tflops, "tflops_executed": exec_flops / (ms / 1e3) / 1e12,
         "frac_of_peak_burst": tflops / peaks["burst"],
         "frac_of_peak_sustained": tflops / peaks["sustained"],
+        "frac_of_datasheet_dense_bf16": tflops / 2250.0,  # nominal 2.25 PF dense bf16 (unverified here)
         "roofline": {"bound": "tensor", "kernel": dom_name, "achieved": achieved, "peak": peaks["sustained"],
                      "unit": "TFLOP/s", "frac": achieved / peaks["sustained"], "traffic": traffic,
                      "peak_kind": "bf16 sustained (kernel timed inside a long step), " + peaks["source"],
