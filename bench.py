@@ -523,7 +523,8 @@ def main():
         "kernels": kernels,
         "gpu_launches": launches,
         "memory": {"extra_device_bytes": int(extra), "logits_bytes_per_gpu": N_l * V_l * 2,
-                   "frac_of_logits_per_gpu": extra / (N_l * V_l * 2), "frac_of_global_logits": extra / (N * V * 2)},
+                   "frac_of_logits_per_gpu": extra / (N_l * V_l * 2), "frac_of_global_logits": extra / (N * V * 2),
+                   "frac_of_spec_logits_and_grads": extra / (2 * N_l * V_l * 2)},  # SPEC's 2*N*V*2
         "clocks": ck,
         "energy": energy,
         "e2e": e2e,
