@@ -773,3 +773,34 @@ def test_native_sharded_edges_world1(slf, N, H, V, mode):
         assert_loss_close(float(loss), ref["loss"], "mean")
     assert rel_max_err(bf16_to_np64(dX), ref["dX"]) <= GRAD_TOL
     assert rel_max_err(bf16_to_np64(dW), ref["dW"]) <= GRAD_TOL
+
+
+@pytest.mark.parametrize("V,v0,v1", [(3000, 0, 3000), (5000, 1234, 3900)])
+def test_stats_epilogues_vs_oracle(slf, V, v0, v1):
+    """L0 blocks: the per-shard row statistics (m, s, z_t, hit) from the schedule-R
+    statistics epilogue (slf_lce_fwd_shard_stats) and from the schedule-S stash epilogue + shard
+    merge (slf_lce_s_chunk_stats), against the oracle's fp64 shard statistics; m to fp32 rounding of
+    the bf16-input dot products, s relatively, z_t and hit exactly where the target is in the shard."""
+    from paper_2603_16428_b200 import lce as L
+    N, H = 700, 256
+    inp = synth.make_inputs(N, H, V, seed=33, alpha=4.0, dist="zipf")
+    X, W, t = to_dev(inp, torch)
+    Ws = W[v0:v1].contiguous()
+    Xo, Wo, to = oracle_inputs(inp)
+    ref = oracle.shard_stats(Xo, Wo[v0:v1], to, v0)
+    m_ref, s_ref, z_ref = (np.asarray(a, dtype=np.float64) for a in ref[:3])
+    loc = to - v0
+    hit_ref = (to != -100) & (loc >= 0) & (loc < v1 - v0)
+    st_r = slf.shard_stats(X, Ws, t, v0).cpu().numpy().astype(np.float64)
+    sh = L.SShard(X, Ws, t, v0, V, budget_bytes=2 << 20)
+    sh.begin()
+    st_s = np.concatenate([sh.chunk_stats(ch).cpu().numpy() for ch in range(sh.n_chunks)]).astype(np.float64)
+    torch.cuda.synchronize()
+    assert sh.n_chunks > 1
+    scale_z = np.max(np.abs(m_ref))
+    for st in (st_r, st_s):
+        assert np.max(np.abs(st[:, 0] - m_ref)) <= 1e-5 * scale_z
+        assert np.max(np.abs(st[:, 1] - s_ref) / s_ref) <= 1e-4
+        assert np.array_equal(st[:, 3] == 1.0, hit_ref)
+        assert np.max(np.abs(st[hit_ref, 2] - z_ref[hit_ref])) <= 1e-5 * scale_z
+        assert not st[~hit_ref, 2].any()
