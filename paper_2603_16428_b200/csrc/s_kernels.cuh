@@ -216,14 +216,65 @@ __global__ void csr_count_kernel(const int32_t* __restrict__ t, int64_t N, int32
 // cnt > 0 in increasing row order; n_hits stored in off[V_l + 1].  Each pass covers 8192
 // consecutive entries: eight per thread (coalesced loads, all in flight at once), a serial scan of
 // the thread's eight, warp-shuffle scans of the thread totals and a running carry (integer, exact).
+constexpr int CSR_SCAN_SPAN = 8192;
+
+// Multi-block form, first kernel: per span of 8192 entries, (sum of counts, number of nonzero).
+__global__ void __launch_bounds__(1024) csr_blocksum_kernel(const int32_t* __restrict__ cnt, int64_t V_l,
+                                                           int2* __restrict__ bsum) {
+  __shared__ int32_t ws[32], wh[32];
+  const int tid = threadIdx.x;
+  const int64_t base = (int64_t)blockIdx.x * CSR_SCAN_SPAN;
+  int32_t s = 0, h = 0;
+#pragma unroll
+  for (int k = 0; k < CSR_SCAN_SPAN / 1024; ++k) {
+    const int64_t v = base + k * 1024 + tid;
+    const int32_t c = v < V_l ? cnt[v] : 0;
+    s += c;
+    h += c > 0;
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    s += __shfl_xor_sync(0xffffffffu, s, o);
+    h += __shfl_xor_sync(0xffffffffu, h, o);
+  }
+  if ((tid & 31) == 0) {
+    ws[tid >> 5] = s;
+    wh[tid >> 5] = h;
+  }
+  __syncthreads();
+  if (tid == 0) {
+    int32_t S = 0, Hh = 0;
+    for (int w = 0; w < 32; ++w) {
+      S += ws[w];
+      Hh += wh[w];
+    }
+    bsum[blockIdx.x] = make_int2(S, Hh);
+  }
+}
+
+// With bsum == nullptr: one block scans all spans in turn (a running carry).  With bsum (from
+// csr_blocksum_kernel): block b scans span b only, starting from the sum of the earlier spans'
+// totals; the last block writes the totals.  Integer, exact, the same result either way.
 __global__ void __launch_bounds__(1024) csr_scan_kernel(const int32_t* __restrict__ cnt, int64_t V_l,
-                                                       int32_t* __restrict__ off, int32_t* __restrict__ hits) {
+                                                       int32_t* __restrict__ off, int32_t* __restrict__ hits,
+                                                       const int2* __restrict__ bsum = nullptr) {
   constexpr int PER = 8, SPAN = 1024 * PER;
+  static_assert(SPAN == CSR_SCAN_SPAN, "span");
   __shared__ int32_t stage[SPAN];
   __shared__ int32_t wsum[32], whit[32];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   int32_t carry_s = 0, carry_h = 0;  // identical in every thread
-  for (int64_t base = 0; base < V_l; base += SPAN) {
+  int64_t b0 = 0, b1 = V_l;
+  if (bsum) {
+    b0 = (int64_t)blockIdx.x * SPAN;
+    b1 = min(V_l, b0 + SPAN);
+    for (int b = 0; b < (int)blockIdx.x; ++b) {  // fixed order, every thread (<= V/8192 entries)
+      const int2 q = bsum[b];
+      carry_s += q.x;
+      carry_h += q.y;
+    }
+  }
+  for (int64_t base = b0; base < b1; base += SPAN) {
 #pragma unroll
     for (int k = 0; k < PER; ++k) {  // coalesced: entry base + k*1024 + tid
       const int64_t v = base + k * 1024 + tid;
@@ -280,7 +331,7 @@ __global__ void __launch_bounds__(1024) csr_scan_kernel(const int32_t* __restric
     carry_h += whit[31];
     __syncthreads();  // stage / wsum / whit are rewritten by the next pass
   }
-  if (tid == 0) {
+  if (tid == 0 && (bsum == nullptr || blockIdx.x == gridDim.x - 1)) {
     off[V_l] = carry_s;
     off[V_l + 1] = carry_h;
   }

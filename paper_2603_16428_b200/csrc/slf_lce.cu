@@ -830,7 +830,14 @@ slf_status s_begin(Ctx& c, const SArgs& a, bool need_dw) {
     ProfScope ps(SLF_PROF_CSR, c.s, 0.0, (double)a.V_l * 12 + (double)a.N * 12);
     csr_zero_kernel<<<(unsigned)std::min<int64_t>((a.V_l + 2 + 255) / 256, 1024), 256, 0, c.s>>>(cnt, a.V_l + 2);
     csr_count_kernel<<<(unsigned)((a.N + 255) / 256), 256, 0, c.s>>>(a.t, a.N, a.ign, a.vs, a.V_l, cnt);
-    csr_scan_kernel<<<1, 1024, 0, c.s>>>(cnt, a.V_l, off, hits);
+    const int64_t nspan = (a.V_l + CSR_SCAN_SPAN - 1) / CSR_SCAN_SPAN;
+    if (nspan > 1 && (size_t)nspan * 8 <= (size_t)a.N * 16) {  // span totals in the (idle) ShardStat area
+      int2* bsum = reinterpret_cast<int2*>(c.ws + p.off_shard);
+      csr_blocksum_kernel<<<(unsigned)nspan, 1024, 0, c.s>>>(cnt, a.V_l, bsum);
+      csr_scan_kernel<<<(unsigned)nspan, 1024, 0, c.s>>>(cnt, a.V_l, off, hits, bsum);
+    } else {
+      csr_scan_kernel<<<1, 1024, 0, c.s>>>(cnt, a.V_l, off, hits);
+    }
     csr_scatter_kernel<<<(unsigned)((a.N + CSR_TOK_PER_BLOCK - 1) / CSR_TOK_PER_BLOCK), 256, 0, c.s>>>(
         a.t, a.N, a.ign, a.vs, a.V_l, cnt, off, idx);
     SLF_CUDA(cudaGetLastError());
