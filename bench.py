@@ -519,7 +519,7 @@ def main():
                      "unit": "TFLOP/s", "frac": achieved / peaks["sustained"], "traffic": traffic,
                      "peak_kind": "bf16 sustained (kernel timed inside a long step), " + peaks["source"],
                      "frac_of_burst": achieved / peaks["burst"],
-                     "ncu": "profiles/ncu_r01q.md (tensor pipe active % per kernel, DRAM bytes)"},
+                     "ncu": "profiles/ncu_r01t.md (tensor pipe active % per kernel, DRAM bytes)"},
         "kernels": kernels,
         "gpu_launches": launches,
         "memory": {"extra_device_bytes": int(extra), "logits_bytes_per_gpu": N_l * V_l * 2,
