@@ -200,3 +200,16 @@ def test_sharded_ranks_share_row_chunks(L, N, H, V, g, budget):
         assert lce.workspace_bytes(N, H, m.v1 - m.v0, "S", b) + 2 * C * H * 4 + (g + 1) * C * 16 <= total
     assert len(set(cs_native)) == 1, cs_native
     assert len(set(cs_mod)) == 1, cs_mod
+
+
+def test_comm_and_dp_argument_errors(L):
+    """Host-side argument checks of the communicator and the data-parallel call (no GPU): P2P mode
+    outside the bit mask, a null communicator."""
+    from paper_2603_16428_b200 import _lib, lce
+    c = lce.Comm.callbacks(0, 2, lambda *a: None, lambda *a: None)
+    for bad in (-1, 4, 7):
+        assert _lib.STATUS_NAMES[L.slf_comm_set_p2p(c.handle, bad)] == "SLF_ERR_ARG"
+    c.close()
+    st = L.slf_lce_fwd_bwd_dp(*([16] * 3), 8, 8, 64, -100, 1, 1.0, *([16] * 4), 1 << 20, 0, 0, 0, None, None)
+    assert _lib.STATUS_NAMES[st] == "SLF_ERR_ARG"
+    assert b"communicator" in L.slf_last_error_string()
