@@ -286,11 +286,13 @@ slf_status slf_comm_rank(slf_comm comm, int* rank, int* world);
  * transport and mapped (cudaIpcMemLazyEnablePeerAccess; NVLink peers, or other processes on the
  * same GPU).  Per chunk one kernel stores the rank's statistics into slot `rank` of every rank's
  * buffer and bumps a per-source counter there (system-scope release); the consumer waits on its own
- * counters (acquire).  A wait that exceeds ~30 s gives up and counts a timeout instead of hanging.
+ * counters (acquire).  A wait that exceeds ~30 s gives up instead of hanging: the call's loss is
+ * then NaN (every element for NONE), slf_comm_status reports it, and every later
+ * slf_lce_fwd_bwd_sharded call on this communicator returns SLF_ERR_COMM (sticky; recreate it).
  * All ranks must set the same mode.  world <= 16. */
 slf_status slf_comm_set_p2p(slf_comm comm, int enable);
 /* Synchronising: HOST *p2p_timeouts = 1 if a P2P wait ever timed out on this rank (results of
- * that call are invalid), else 0. */
+ * that call are invalid, its loss NaN), else 0. */
 slf_status slf_comm_status(slf_comm comm, int32_t* p2p_timeouts);
 
 /* Rank k of g owns W rows [V_global*k/g, V_global*(k+1)/g) (contiguous, as even as possible). */

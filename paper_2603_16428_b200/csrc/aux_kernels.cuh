@@ -18,8 +18,10 @@ struct WsHeader {
   unsigned int done;
   unsigned long long pad[6];
 };
-constexpr int MAX_LOSS_BLOCKS = 8192;
-constexpr size_t WS_HEADER_BYTES = 64 * 1024;  // header + block partial sums (double)
+constexpr size_t WS_HEADER_BYTES = 64 * 1024;  // header (256 B) + block partial sums (double)
+// Blocks of 256 rows whose fp64 loss partials fit the header after its first 256 bytes (8160 blocks:
+// N <= 2,088,960 rows per statistics-combine call).
+constexpr int MAX_LOSS_BLOCKS = (int)((WS_HEADER_BYTES - 256) / 8);
 
 // One block of 1024 threads: 16-byte vector loads of the targets.
 __global__ void __launch_bounds__(1024) prep_targets_kernel(const int32_t* __restrict__ t, int64_t N,

@@ -205,6 +205,20 @@ __global__ void __launch_bounds__(256) p2p_dx_exchange_kernel(DxArgs a) {
   }
 }
 
+// After a sharded step with P2P exchanges: if any wait of this rank timed out (error word set), the
+// step's results are invalid — poison the loss with NaN (the ABI's asynchronous data-error
+// convention, as for bad targets) and raise the host-mapped sticky flag that makes the next
+// slf_lce_fwd_bwd_sharded call on this communicator return SLF_ERR_COMM.
+__global__ void p2p_check_kernel(const uint8_t* buf, float* loss, int64_t n_loss, volatile int* host_flag) {
+  if (*reinterpret_cast<const volatile int*>(buf + P2P_ERR_OFF) == 0) return;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n_loss; i += (int64_t)gridDim.x * blockDim.x)
+    loss[i] = __int_as_float(0x7fc00000);
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    *host_flag = 1;
+    __threadfence_system();
+  }
+}
+
 }  // namespace slf
 
 // The handle behind slf_comm (opaque in the header).
@@ -220,6 +234,8 @@ struct slf_comm_s {
   uint8_t* p2p_buf = nullptr;  // this rank's receive buffer (cudaMalloc, communicator-owned)
   int64_t p2p_rows = 0;        // capacity in rows per slot
   uint8_t* p2p_peer[slf::P2P_MAX_RANKS] = {};  // mapped receive buffers of every rank (own = p2p_buf)
+  int* p2p_err_host = nullptr;  // sticky timeout flag, pinned host memory mapped into the device
+  int* p2p_err_dev = nullptr;   // its device alias
   unsigned long long epoch = 0;
   unsigned long long dx_epoch = 0;  // chunks whose dX went through the exchange kernel
   // caller buffers mapped from peers: (handle bytes) -> opened base, and this rank's exported bases

@@ -152,7 +152,7 @@ struct slf_adam_s {
   std::vector<cudaEvent_t> ev_chunk;
   int64_t chunk = 0;
   std::thread worker;
-  bool busy = false, had_device_step = false;
+  bool busy = false, had_device_step = false, pipeline_ready = false;
   slf_status worker_status = SLF_OK;
   std::string worker_err;
 };
@@ -203,19 +203,51 @@ slf_status check_cfg(const slf_adam_config* c) {
   return SLF_OK;
 }
 
+void release_pipeline(slf_adam_s* a) {
+  if (a->g_stage) cudaFreeHost(a->g_stage);
+  if (a->p_stage) cudaFreeHost(a->p_stage);
+  if (a->d2h) cudaStreamDestroy(a->d2h);
+  if (a->h2d) cudaStreamDestroy(a->h2d);
+  if (a->ev_start) cudaEventDestroy(a->ev_start);
+  if (a->ev_done) cudaEventDestroy(a->ev_done);
+  for (auto e : a->ev_chunk)
+    if (e) cudaEventDestroy(e);
+  a->g_stage = a->p_stage = nullptr;
+  a->d2h = a->h2d = nullptr;
+  a->ev_start = a->ev_done = nullptr;
+  a->ev_chunk.clear();
+  a->pipeline_ready = false;
+}
+
+// Creates the device-fed pipeline on first use.  `pipeline_ready` is set only once every resource
+// exists; a failure part-way releases what was created, so the next call retries from scratch
+// instead of running on a half-built pipeline.
 slf_status ensure_pipeline(slf_adam_s* a) {
-  if (a->g_stage) return SLF_OK;
-  ADAM_CUDA(cudaGetDevice(&a->device));
-  ADAM_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&a->g_stage), (size_t)a->n * 2, cudaHostAllocDefault));
-  ADAM_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&a->p_stage), (size_t)a->n * 2, cudaHostAllocDefault));
-  ADAM_CUDA(cudaStreamCreateWithFlags(&a->d2h, cudaStreamNonBlocking));
-  ADAM_CUDA(cudaStreamCreateWithFlags(&a->h2d, cudaStreamNonBlocking));
-  ADAM_CUDA(cudaEventCreateWithFlags(&a->ev_start, cudaEventDisableTiming));
-  ADAM_CUDA(cudaEventCreateWithFlags(&a->ev_done, cudaEventDisableTiming));
+  if (a->pipeline_ready) return SLF_OK;
+  release_pipeline(a);
+  auto fail_release = [a](cudaError_t e, const char* what) {
+    const slf_status st = afail(SLF_ERR_CUDA, "%s: %s", what, cudaGetErrorString(e));
+    release_pipeline(a);
+    return st;
+  };
+#define PIPE_TRY(call)                                   \
+  do {                                                   \
+    const cudaError_t e_ = (call);                       \
+    if (e_ != cudaSuccess) return fail_release(e_, #call); \
+  } while (0)
+  PIPE_TRY(cudaGetDevice(&a->device));
+  PIPE_TRY(cudaHostAlloc(reinterpret_cast<void**>(&a->g_stage), (size_t)a->n * 2, cudaHostAllocDefault));
+  PIPE_TRY(cudaHostAlloc(reinterpret_cast<void**>(&a->p_stage), (size_t)a->n * 2, cudaHostAllocDefault));
+  PIPE_TRY(cudaStreamCreateWithFlags(&a->d2h, cudaStreamNonBlocking));
+  PIPE_TRY(cudaStreamCreateWithFlags(&a->h2d, cudaStreamNonBlocking));
+  PIPE_TRY(cudaEventCreateWithFlags(&a->ev_start, cudaEventDisableTiming));
+  PIPE_TRY(cudaEventCreateWithFlags(&a->ev_done, cudaEventDisableTiming));
   a->chunk = a->cfg.chunk_elems > 0 ? a->cfg.chunk_elems : (int64_t)16 << 20;
   const int64_t nch = (a->n + a->chunk - 1) / a->chunk;
-  a->ev_chunk.resize((size_t)nch);
-  for (auto& e : a->ev_chunk) ADAM_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  a->ev_chunk.assign((size_t)nch, nullptr);
+  for (auto& e : a->ev_chunk) PIPE_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+#undef PIPE_TRY
+  a->pipeline_ready = true;
   return SLF_OK;
 }
 
@@ -251,13 +283,7 @@ slf_status slf_adam_destroy(slf_adam a) {
   free(a->p);
   free(a->m);
   free(a->v);
-  if (a->g_stage) cudaFreeHost(a->g_stage);
-  if (a->p_stage) cudaFreeHost(a->p_stage);
-  if (a->d2h) cudaStreamDestroy(a->d2h);
-  if (a->h2d) cudaStreamDestroy(a->h2d);
-  if (a->ev_start) cudaEventDestroy(a->ev_start);
-  if (a->ev_done) cudaEventDestroy(a->ev_done);
-  for (auto e : a->ev_chunk) cudaEventDestroy(e);
+  release_pipeline(a);
   delete a;
   return SLF_OK;
 }
@@ -269,7 +295,7 @@ slf_status slf_adam_set_config(slf_adam a, const slf_adam_config* cfg) {
   if (s != SLF_OK) return s;
   const int64_t keep_chunk = a->cfg.chunk_elems;
   a->cfg = *cfg;
-  if (a->g_stage) a->cfg.chunk_elems = keep_chunk;  // the pipeline's chunking is fixed once created
+  if (a->pipeline_ready) a->cfg.chunk_elems = keep_chunk;  // the pipeline's chunking is fixed once created
   return SLF_OK;
 }
 

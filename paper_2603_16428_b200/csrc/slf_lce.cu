@@ -672,7 +672,9 @@ slf_status phase_combine(Ctx& c, const slf_shardstat* st, int g, const int32_t* 
                          int64_t V_l, int64_t V_global, int32_t ignore_index, int reduction, float scale,
                          float* loss_out, slf_rowstat* rowstat) {
   const unsigned blocks = (unsigned)((N + 255) / 256);
-  if (blocks > (unsigned)MAX_LOSS_BLOCKS * 4) return fail(SLF_ERR_ARG, "N too large for the loss reduction");
+  if (blocks > (unsigned)MAX_LOSS_BLOCKS)
+    return fail(SLF_ERR_ARG, "N = %lld too large for the loss reduction (at most %lld rows)", (long long)N,
+                (long long)MAX_LOSS_BLOCKS * 256);
   SLF_TRY(launch_prep(c, t, N, ignore_index, V_global));
   ProfScope ps(SLF_PROF_FINAL_COMBINE, c.s, 0.0, (double)N * (g * 16.0 + 4 + 16 + 4));
   final_combine_kernel<<<blocks, 256, 0, c.s>>>(st, g, t, N, vocab_start, V_l, V_global, ignore_index, reduction,
@@ -1332,6 +1334,11 @@ slf_status p2p_ensure(slf_comm cm, int64_t rows, cudaStream_t s) {
   p2p_release(cm);
   cm->p2p_rows = rows;
   const size_t bytes = P2P_HDR_BYTES + 2 * (size_t)cm->world * rows * 16;
+  if (!cm->p2p_err_host) {  // sticky timeout flag readable by the host without a synchronisation
+    SLF_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&cm->p2p_err_host), 64, cudaHostAllocMapped));
+    *cm->p2p_err_host = 0;
+    SLF_CUDA(cudaHostGetDevicePointer(reinterpret_cast<void**>(&cm->p2p_err_dev), cm->p2p_err_host, 0));
+  }
   SLF_CUDA(cudaMalloc(&cm->p2p_buf, bytes));
   SLF_CUDA(cudaMemset(cm->p2p_buf, 0, bytes));
   SLF_CUDA(cudaDeviceSynchronize());
@@ -1487,10 +1494,15 @@ slf_status phase_sharded(Ctx& c, const ShardPlan& sp, slf_comm cm, const void* X
   const slf_rowstat* rs = reinterpret_cast<const slf_rowstat*>(c.ws + p.off_rowstat);
   const bool p2p_dx = cm->p2p && (cm->p2p_mode & 2) && dX;
   if (cm->p2p) SLF_TRY(p2p_ensure(cm, p.C, c.s));
-  uint8_t* ws_peer[P2P_MAX_RANKS] = {};
+  // Peers' fp32 partial buffers are exported themselves (base + offset inside the caller's
+  // allocation), not as this rank's workspace offsets: shard sizes differ by one vocabulary row when
+  // g does not divide V, and the schedule-S layout (stash leading dimension, CSR arrays) before the
+  // partials then differs between ranks.  The second partial follows the first at the same distance
+  // on every rank (the same C and H).
+  uint8_t* part_peer[P2P_MAX_RANKS] = {};
   uint8_t* dx_peer[P2P_MAX_RANKS] = {};
   if (p2p_dx) {
-    SLF_TRY(p2p_map(cm, c.ws, c.s, ws_peer));
+    SLF_TRY(p2p_map(cm, c.ws + sp.off_dx0, c.s, part_peer));
     SLF_TRY(p2p_map(cm, dX, c.s, dx_peer));
   }
   std::vector<unsigned long long> dx_ep(p.nCh, 0);
@@ -1544,9 +1556,9 @@ slf_status phase_sharded(Ctx& c, const ShardPlan& sp, slf_comm cm, const void* X
     if (p2p_dx) {  // reduce-scatter + all-gather + bf16 finalize of this chunk, one kernel on the comm stream
       dx_ep[i] = ++cm->dx_epoch;
       DxArgs xa{};
-      const size_t off = slot ? sp.off_dx1 : sp.off_dx0;
+      const size_t off = slot ? sp.off_dx1 - sp.off_dx0 : 0;
       for (int r = 0; r < g; ++r) {
-        xa.part.p[r] = ws_peer[r] + off;
+        xa.part.p[r] = part_peer[r] + off;
         xa.dx.p[r] = dx_peer[r] + (size_t)k.r0 * H * 2;
         xa.flags.p[r] = cm->p2p_peer[r];
       }
@@ -1582,7 +1594,14 @@ slf_status phase_sharded(Ctx& c, const ShardPlan& sp, slf_comm cm, const void* X
     const int slot = (int)((chunks.size() + j) & 1);
     if (pending[slot] >= 0) SLF_TRY(finish(slot));
   }
-  return s_end(c, a, reduction, scale, loss_out, dW);
+  SLF_TRY(s_end(c, a, reduction, scale, loss_out, dW));
+  if (cm->p2p && cm->p2p_buf) {  // a timed-out wait poisons this call's loss and fails the next call
+    const int64_t n_loss = reduction == SLF_NONE ? N : 1;
+    p2p_check_kernel<<<(int)std::min<int64_t>((n_loss + 255) / 256, 64), 256, 0, c.s>>>(cm->p2p_buf, loss_out, n_loss,
+                                                                                      cm->p2p_err_dev);
+    SLF_CUDA(cudaGetLastError());
+  }
+  return SLF_OK;
 }
 
 }  // namespace
@@ -1972,6 +1991,7 @@ slf_status slf_comm_destroy(slf_comm c) {
     if (r != ncclSuccess) st = comm_fail_nccl(r, "ncclCommDestroy");
   }
   if (c->cs) cudaStreamDestroy(c->cs);
+  if (c->p2p_err_host) cudaFreeHost(c->p2p_err_host);
   for (cudaEvent_t e : {c->ev_in, c->ev_ag, c->ev_ar[0], c->ev_ar[1]})
     if (e) cudaEventDestroy(e);
   delete c;
@@ -1992,6 +2012,7 @@ slf_status slf_comm_status(slf_comm c, int32_t* p2p_timeouts) {
   if (!c || !p2p_timeouts) return fail(SLF_ERR_ARG, "null pointer");
   *p2p_timeouts = 0;
   if (c->p2p_buf) SLF_CUDA(cudaMemcpy(p2p_timeouts, c->p2p_buf + P2P_ERR_OFF, 4, cudaMemcpyDeviceToHost));
+  if (c->p2p_err_host && *reinterpret_cast<volatile int*>(c->p2p_err_host)) *p2p_timeouts = 1;
   return SLF_OK;
 }
 
@@ -2033,6 +2054,9 @@ slf_status slf_lce_fwd_bwd_sharded(const void* hidden, const void* weight_shard,
                                    float* loss_out, void* dhidden, void* dweight_shard, void* workspace,
                                    size_t workspace_bytes, size_t budget_bytes, slf_comm comm, void* stream) {
   if (!comm) return fail(SLF_ERR_ARG, "null communicator");
+  if (comm->p2p_err_host && *reinterpret_cast<volatile int*>(comm->p2p_err_host))
+    return fail(SLF_ERR_COMM, "a P2P wait of an earlier call on this communicator timed out (its loss is NaN); "
+                              "recreate the communicator");
   if (V_global < comm->world) return fail(SLF_ERR_ARG, "V_global %lld < world %d", (long long)V_global, comm->world);
   int64_t v0, vl;
   shard_bounds(V_global, comm->world, comm->rank, &v0, &vl);

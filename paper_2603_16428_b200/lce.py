@@ -127,10 +127,17 @@ def lce_fwd_bwd_host(hidden_host, weight, targets_host, ignore_index: int = -100
     N, H = hidden_host.shape
     V = weight.shape[0]
     dev = weight.device
+    n_loss = N if reduction == "none" else 1
     if staging is None:
         staging = HostStaging(N, H, dev, reduction)
+    elif (tuple(staging.hidden.shape) != (N, H) or staging.targets.numel() < N or staging.loss.numel() < n_loss
+          or staging.hidden.device != dev):
+        raise ValueError(f"staging buffers (hidden {tuple(staging.hidden.shape)}, targets {staging.targets.numel()}, "
+                         f"loss {staging.loss.numel()}) do not fit N={N} H={H} reduction={reduction!r}")
     if loss_host is None:
-        loss_host = torch.empty(N if reduction == "none" else 1, dtype=torch.float32).pin_memory()
+        loss_host = torch.empty(n_loss, dtype=torch.float32).pin_memory()
+    elif loss_host.is_cuda or loss_host.dtype != torch.float32 or loss_host.numel() < n_loss:
+        raise ValueError(f"loss_host must be a CPU float32 tensor of >= {n_loss} elements")
     if dX is None:
         dX = torch.empty(N, H, dtype=torch.bfloat16, device=dev)
     if dW is None and not accumulate_dw:
@@ -369,6 +376,7 @@ class Comm:
     def __init__(self, handle, rank: int, world: int, keep=None):
         self.handle, self.rank, self.world = handle, rank, world
         self._keep = keep  # ctypes callbacks must outlive the handle
+        self.p2p_mode = 0
 
     @classmethod
     def nccl(cls, unique_id: bytes, rank: int, world: int, device: int):
@@ -419,6 +427,7 @@ class Comm:
         """P2P exchanges over CUDA IPC (slf_comm_set_p2p): True / 1 the per-chunk statistics
         all-gather, 2 the dX exchange kernel, 3 both; False / 0 off."""
         check(lib().slf_comm_set_p2p(self.handle, int(enable)), "slf_comm_set_p2p")
+        self.p2p_mode = int(enable)
         return self
 
     def p2p_timeouts(self) -> int:
@@ -471,9 +480,13 @@ def sharded_plan_describe(N: int, H: int, V_global: int, world: int, rank: int, 
 
 def lce_fwd_bwd_sharded(hidden, weight_shard, targets, V_global: int, comm: Comm, ignore_index: int = -100,
                         reduction: str = "mean", scale: float = 1.0, budget_bytes: int = 0, workspace=None,
-                        out=None, need_dhidden: bool = True, need_dweight: bool = True):
+                        out=None, need_dhidden: bool = True, need_dweight: bool = True, check_p2p: bool = True):
     """Vocab-sharded fused LCE on this rank (slf_lce_fwd_bwd_sharded): every rank passes the same
-    hidden / targets and its own W rows; returns (global loss, full dhidden, this rank's dW rows)."""
+    hidden / targets and its own W rows; returns (global loss, full dhidden, this rank's dW rows).
+
+    With P2P exchanges enabled on ``comm`` and ``check_p2p`` (default), the call synchronises and
+    raises if a P2P wait timed out (a peer more than ~30 s late: the results would be stale).  With
+    ``check_p2p=False`` the library still poisons that call's loss with NaN and fails the next call."""
     hidden, weight_shard, targets = _prep(hidden, weight_shard, targets)
     N, H = hidden.shape
     v0, v1 = shard_bounds_native(V_global, comm.world, comm.rank)
@@ -495,6 +508,8 @@ def lce_fwd_bwd_sharded(hidden, weight_shard, targets, V_global: int, comm: Comm
                                         V_global, ignore_index, REDUCTIONS[reduction], float(scale), loss.data_ptr(),
                                         _ptr(dX), _ptr(dW), workspace.data_ptr(), workspace.numel(), budget_bytes,
                                         comm.handle, _stream_ptr(dev)), "slf_lce_fwd_bwd_sharded")
+    if check_p2p and comm.p2p_mode and comm.p2p_timeouts():
+        raise RuntimeError(f"rank {comm.rank}: a P2P exchange wait timed out; this step's results are invalid")
     return (loss if reduction == "none" else loss[0]), dX, dW
 
 

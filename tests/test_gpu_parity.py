@@ -513,31 +513,7 @@ def test_full_size_sampled_rows_all_configs(slf, cfg):
     assert np.all(dX[torch.from_numpy(inp.t == -100).cuda()].view(torch.int16).cpu().numpy() == 0)
 
 
-@pytest.mark.slow
-def test_llama_full_size_dw_rows(slf):
-    """dW rows at the full Llama-3.1-8B size: the oracle forms lse for all 16384 rows (materialised
-    logits, fp64) and checks 12 vocabulary rows of dW, including the most-hit target rows."""
-    inp = synth.make_config("llama8b", seed=2, alpha=4.0, dist="zipf")
-    X, W, t = to_dev(inp, torch)
-    loss, dX, dW = slf.lce_fwd_bwd(X, W, t, reduction="mean")
-    torch.cuda.synchronize()
-    Xo = synth.bf16_bits_to_f64(inp.X)
-    Wo = synth.bf16_bits_to_f64(inp.W)
-    valid, nv, coef = oracle.coef_for(inp.t, -100, "mean", 1.0)
-    hot = np.argsort(-np.bincount(inp.t[valid], minlength=inp.V))[:6]
-    vrows = np.unique(np.concatenate([hot, np.random.default_rng(4).choice(inp.V, 6, replace=False)]))
-    lse = np.empty(inp.N)
-    zt = np.empty(inp.N)
-    for s in range(0, inp.N, 1024):  # row blocks of the materialised logits (plain definition, c1-c2)
-        Z = Xo[s:s + 1024] @ Wo.T
-        m = Z.max(axis=1)
-        lse[s:s + 1024] = m + np.log(np.exp(Z - m[:, None]).sum(axis=1))
-    P = np.exp(Xo @ Wo[vrows].T - lse[:, None])                 # softmax columns of the sampled rows
-    onehot = (inp.t[:, None] == vrows[None, :]).astype(np.float64)
-    G = coef[:, None] * (P - onehot)                             # c3, columns vrows
-    ref = G.T @ Xo                                               # dW rows vrows
-    got = bf16_to_np64(dW[torch.from_numpy(vrows).cuda()])
-    assert rel_max_err(got, ref) <= GRAD_TOL
+# (full-size dW rows of every head: tests/test_gpu_heads.py::test_full_size_dw_and_dx_rows)
 
 
 # ---- vocab-sharded call with in-library collectives (slf_lce_fwd_bwd_sharded) ---------------------
@@ -653,6 +629,29 @@ def test_native_sharded_callbacks(slf, tmp_path, g, red, budget):
         for a, b in zip(res, rs):
             for k in ("loss", "dX", "dW"):
                 assert np.array_equal(a[k], b[k]), k
+
+
+def test_native_sharded_p2p_dx_uneven_shards(slf, tmp_path):
+    """P2P dX exchange when g does not divide V (V=32001, g=2: shards of 16000 / 16001 rows, so the
+    ranks' workspace layouts differ by 8 KB before the fp32 partials): each rank must read its peers'
+    partial buffers at THEIR offsets.  Bit-identical to the gloo all-reduce (two
+    partials), and against the oracle."""
+    V, budget = 32001, 20 << 20
+    assert len({slf.sharded_workspace_bytes(900, 256, V, 2, r, budget) for r in (0, 1)}) == 2
+    base = _run_native_ranks(tmp_path / "cb", 2, "mean", budget, ("--V", str(V)))
+    px = _run_native_ranks(tmp_path / "p2p", 2, "mean", budget, ("--V", str(V), "--p2p", "3", "--calls", "2"))
+    for a, b in zip(base, px):
+        assert int(b["timeouts"]) == 0
+        for k in ("loss", "dX", "dW"):
+            assert np.array_equal(a[k], b[k]), k
+    inp = synth.make_inputs(900, 256, V, seed=21, alpha=4.0, dist="zipf")
+    Xo, Wo, to = oracle_inputs(inp)
+    ref = oracle.lce(Xo, Wo, to, reduction="mean")
+    tobf = lambda a: a.astype(np.int16).view(np.uint16).astype(np.uint32) << 16  # noqa: E731
+    assert_loss_close(float(px[0]["loss"].reshape(-1)[0]), ref["loss"], "mean")
+    assert rel_max_err(tobf(px[1]["dX"]).view(np.float32).astype(np.float64), ref["dX"]) <= GRAD_TOL
+    dW = np.concatenate([tobf(r["dW"]).view(np.float32).astype(np.float64) for r in px])
+    assert rel_max_err(dW, ref["dW"]) <= GRAD_TOL
 
 
 def test_lce_fwd_bwd_group_world1(slf):
