@@ -191,6 +191,53 @@ def run_reference(args):
 
 
 # ---- the GPU arm -----------------------------------------------------------------------------------
+def launcher_cmd(gpus: int, argv, port: int):
+    """The command that runs this script with one rank per GPU (torch.distributed.run, loopback
+    rendezvous), forwarding the original arguments."""
+    return [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={gpus}",
+            "--master-addr", "127.0.0.1", f"--master-port={port}", os.path.abspath(__file__), *argv]
+
+
+def free_port() -> int:
+    import socket
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        return sk.getsockname()[1]
+
+
+def self_launch(gpus: int) -> int:
+    """Spawn `gpus` ranks of this benchmark; rank 0's JSON line reaches our stdout unchanged.  Fails
+    loudly (exit 2) when fewer GPUs are visible than requested."""
+    import torch
+    have = torch.cuda.device_count() if torch.cuda.is_available() else 0
+    if have < gpus and "--dry-run" not in sys.argv[1:]:
+        print(f"bench.py: --gpus {gpus} requested but {have} CUDA device(s) visible", file=sys.stderr)
+        return 2
+    cmd = launcher_cmd(gpus, sys.argv[1:], free_port())
+    print("bench.py: launching " + " ".join(cmd), file=sys.stderr, flush=True)
+    return subprocess.run(cmd).returncode
+
+
+def run_dry(args):
+    """The multi-rank plumbing of the GPU arm without a GPU: process group, barrier, max over ranks,
+    rank 0 alone prints.  No measurement."""
+    import torch
+    import torch.distributed as dist
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+    os.environ.setdefault("MASTER_PORT", str(free_port()))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    dist.barrier()
+    t = torch.tensor([float(rank + 1)], dtype=torch.float64)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    dist.barrier()
+    if rank == 0:
+        print(json.dumps({"dry_run": True, "n_gpus": world, "max_over_ranks": float(t.item()),
+                          "local_rank": int(os.environ.get("LOCAL_RANK", "0"))}), flush=True)
+    dist.destroy_process_group()
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -219,6 +266,9 @@ def main():
                     help="native comm: per-chunk statistics by the P2P one-shot all-gather over CUDA IPC (NEXT-3)")
     ap.add_argument("--p2p-dx", action="store_true",
                     help="native comm: dX exchanged by the P2P reduce/all-gather kernel over CUDA IPC (no NCCL)")
+    ap.add_argument("--dry-run", action="store_true",
+                    help="launcher plumbing only (CPU tests): ranks join a gloo group, exchange a per-rank "
+                         "number with the max-over-ranks reduction the timing uses, rank 0 prints it")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     args = ap.parse_args()
@@ -227,6 +277,23 @@ def main():
     if args.impl == "reference":
         run_reference(args)
         return
+
+    # N > 1 without a launcher: start one rank per GPU ourselves (the same torch.distributed.run
+    # command the driver uses), so `python bench.py --gpus N` is never silently a 1-GPU run.
+    world_env = os.environ.get("WORLD_SIZE")
+    if world_env is None and args.gpus > 1:
+        sys.exit(self_launch(args.gpus))
+    if world_env is not None and int(world_env) != args.gpus and not (args.gpus == 1 and args.module):
+        print(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world_env}; refusing to time a different "
+              f"configuration", file=sys.stderr)
+        sys.exit(2)
+    if args.dry_run:
+        run_dry(args)
+        return
+    if args.gpus > 1 or world_env is not None:
+        # NCCL's INIT lines (ranks, devices, channels, NVLS) on stderr: evidence of the ranks used
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
 
     if args.comm_sms >= 0:
         os.environ["SLF_COMM_SMS"] = str(args.comm_sms)
@@ -345,9 +412,9 @@ def main():
             l, _, _ = dpm.forward_backward(Xs, W, ts, n_valid_global=n_valid_global, workspace=ws,
                                            out=(loss, dX, dW))
             return l
-        if native:
+        if native:  # a P2P timeout poisons the loss; checked once after the timed region
             l, _, _ = slf.lce_fwd_bwd_sharded(Xs, W, ts, V, comm, workspace=ws, out=(loss, dX, dW),
-                                              budget_bytes=args.budget)
+                                              budget_bytes=args.budget, check_p2p=False)
             return l
         l, _, _ = sharded.forward_backward(Xs, W, ts, workspace=ws, dW_out=dW, dX_out=dX)
         return l
@@ -379,6 +446,18 @@ def main():
         w1 = time.perf_counter()
         barrier()
     ms = e0.elapsed_time(e1) / args.steps
+    # Per-step distribution (median and min): the same K steps again with an event
+    # pair around each step (kept out of the timed region: an event between steps forfeits one
+    # programmatic-dependent-launch overlap per step).
+    barrier()
+    torch.cuda.synchronize()
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    for a_, b_ in evs:
+        a_.record(stream)
+        step()
+        b_.record(stream)
+    torch.cuda.synchronize()
+    per_step = np.array([a_.elapsed_time(b_) for a_, b_ in evs])
     # Per-kernel breakdown (roofline): the same K steps again with a CUDA-event pair around every
     # library launch.  Kept out of the timed region above because events between launches also
     # disable programmatic dependent launch.
@@ -390,9 +469,13 @@ def main():
         torch.cuda.synchronize()
     barrier()
     if multi:
-        tt = torch.tensor([ms], dtype=torch.float64, device=dev)
+        tt = torch.tensor([ms, *per_step.tolist()], dtype=torch.float64, device=dev)
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        ms = float(tt.item())
+        ms = float(tt[0].item())
+        per_step = tt[1:].cpu().numpy()
+    p2p_timeouts = comm.p2p_timeouts() if native and comm_note is None and (args.p2p_stats or args.p2p_dx) else 0
+    if p2p_timeouts:
+        raise RuntimeError(f"rank {rank}: a P2P exchange wait timed out during the benchmark")
 
     # End to end through the public API with HOST buffers: per step, the pinned host->device copy
     # of the step's inputs (hidden states, targets), the fused call and a device->host read of the
@@ -474,7 +557,7 @@ def main():
     flops = 6.0 * N * H * V
     tflops = flops / (ms / 1e3) / 1e12
     kinds = prof.kinds
-    launches = int(sum(k["launches"] for k in kinds.values()))
+    launches = int(sum(v["launches"] for k, v in kinds.items() if not k.startswith("comm_")))  # our kernels only
     gemm_kinds = {k: v for k, v in kinds.items() if k.startswith("gemm")}
     dom_name, dom = max(gemm_kinds.items(), key=lambda kv: kv[1]["ms"])
     dom_ms_per_launch = dom["ms"] / dom["launches"]
@@ -495,7 +578,12 @@ def main():
     out = {
         "metric": METRIC, "value": N / (ms / 1e3), "unit": UNIT, "n_gpus": g, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
-        "scaling": "strong" if multi else "weak", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
+        # the same N tokens of one call at every GPU count: strong scaling (dp: the batch split)
+        "scaling": "strong", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
+        "step_ms": {"mean_timed_region": ms, "median": float(np.median(per_step)), "min": float(per_step.min()),
+                    "max": float(per_step.max()),
+                    "note": "median/min/max from a second pass of K steps with an event pair per step"
+                            + (" (max over ranks per step)" if multi else "")},
         "config": {"workload": f"{args.config} LM head N={N} H={H} V={V}", "N": N, "H": H, "V": V,
                    "V_per_gpu": V_l, "N_per_gpu": N_l,
                    "parallelism": (f"token-sharded data parallel x{g}" if dp else f"vocab-sharded x{g}")
@@ -521,6 +609,12 @@ def main():
                      "frac_of_burst": achieved / peaks["burst"],
                      "ncu": "profiles/ncu_r01t.md (tensor pipe active % per kernel, DRAM bytes)"},
         "kernels": kernels,
+        "comm": ({"allgather_ms_per_step": kinds.get("comm_allgather", {}).get("ms", 0.0) / args.steps,
+                  "allreduce_ms_per_step": kinds.get("comm_allreduce", {}).get("ms", 0.0) / args.steps,
+                  "collectives_per_step": sum(kinds.get(k, {}).get("launches", 0)
+                                              for k in ("comm_allgather", "comm_allreduce")) / args.steps,
+                  "note": "NCCL calls inside the library, CUDA events on the communicator's stream (rank 0; they "
+                          "overlap the next chunk's GEMMs)"} if multi else None),
         "gpu_launches": launches,
         "memory": {"extra_device_bytes": int(extra), "logits_bytes_per_gpu": N_l * V_l * 2,
                    "frac_of_logits_per_gpu": extra / (N_l * V_l * 2), "frac_of_global_logits": extra / (N * V * 2),

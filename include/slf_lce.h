@@ -393,7 +393,7 @@ slf_status slf_lce_dx_finalize(const float* dhidden_fp32, const slf_rowstat* row
  * writes per-kind totals into HOST arrays of SLF_PROF_KINDS entries: device milliseconds, launches,
  * algorithmic FLOPs (2*M*N*K of each GEMM launch) and algorithmic bytes (aux kernels: bytes they
  * must read + write).  Kinds: */
-#define SLF_PROF_KINDS 16
+#define SLF_PROF_KINDS 18
 #define SLF_PROF_GEMM_STATS 0 /* forward logits tile GEMM + stats epilogue          */
 #define SLF_PROF_GEMM_GRAD 1  /* backward recompute GEMM + dlogit (G) epilogue      */
 #define SLF_PROF_GEMM_DW 2    /* dW = G^T X                                         */
@@ -410,6 +410,8 @@ slf_status slf_lce_dx_finalize(const float* dhidden_fp32, const slf_rowstat* row
 #define SLF_PROF_LOSS_REDUCE 13       /* schedule S: deterministic loss sum               */
 #define SLF_PROF_RMSNORM 14           /* final RMSNorm forward / backward (NEXT-1)        */
 #define SLF_PROF_TRANSPOSE 15         /* schedule S: X_chunk^T for the dW GEMM's B operand */
+#define SLF_PROF_COMM_ALLGATHER 16    /* NCCL all-gather of per-row statistics (comm stream) */
+#define SLF_PROF_COMM_ALLREDUCE 17    /* NCCL all-reduce (dX partials, counts, loss; comm stream) */
 slf_status slf_profile_begin(void);
 slf_status slf_profile_end(double* ms, int64_t* launches, double* flops, double* bytes);
 

@@ -34,7 +34,8 @@ EXPORTS = ["slf_lce_version", "slf_last_error_string", "slf_lce_workspace_bytes"
            "slf_adam_set_config", "slf_adam_set_params", "slf_adam_get_state", "slf_adam_step_host",
            "slf_adam_step_device_async", "slf_adam_wait"]
 PROF_KINDS = ["gemm_stats", "gemm_grad", "gemm_dw", "gemm_dx", "gemm_debug", "prep", "local_combine", "final_combine",
-              "dx_finalize", "gemm_group", "combine_transform", "csr", "onehot", "loss_reduce", "rmsnorm", "transpose"]
+              "dx_finalize", "gemm_group", "combine_transform", "csr", "onehot", "loss_reduce", "rmsnorm", "transpose",
+              "comm_allgather", "comm_allreduce"]
 
 _lock = threading.Lock()
 _lib = None

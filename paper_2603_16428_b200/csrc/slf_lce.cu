@@ -1258,7 +1258,11 @@ slf_status comm_allgather(slf_comm cm, const void* send, void* recv, size_t byte
   NcclApi& api = nccl_api();
   SLF_CUDA(cudaEventRecord(cm->ev_in, s));
   SLF_CUDA(cudaStreamWaitEvent(cm->cs, cm->ev_in, 0));
-  const ncclResult_t r = api.AllGather(send, recv, bytes, ncclUint8, cm->nccl, cm->cs);
+  ncclResult_t r;
+  {
+    ProfScope ps(SLF_PROF_COMM_ALLGATHER, cm->cs, 0.0, (double)bytes * cm->world);
+    r = api.AllGather(send, recv, bytes, ncclUint8, cm->nccl, cm->cs);
+  }
   if (r != ncclSuccess) return comm_fail_nccl(r, "ncclAllGather");
   SLF_CUDA(cudaEventRecord(cm->ev_ag, cm->cs));
   SLF_CUDA(cudaStreamWaitEvent(s, cm->ev_ag, 0));
@@ -1276,7 +1280,11 @@ slf_status comm_allreduce_start(slf_comm cm, float* buf, size_t count, int slot,
   NcclApi& api = nccl_api();
   SLF_CUDA(cudaEventRecord(cm->ev_in, s));
   SLF_CUDA(cudaStreamWaitEvent(cm->cs, cm->ev_in, 0));
-  const ncclResult_t r = api.AllReduce(buf, buf, count, ncclFloat32, ncclSum, cm->nccl, cm->cs);
+  ncclResult_t r;
+  {
+    ProfScope ps(SLF_PROF_COMM_ALLREDUCE, cm->cs, 0.0, (double)count * 4);
+    r = api.AllReduce(buf, buf, count, ncclFloat32, ncclSum, cm->nccl, cm->cs);
+  }
   if (r != ncclSuccess) return comm_fail_nccl(r, "ncclAllReduce");
   SLF_CUDA(cudaEventRecord(cm->ev_ar[slot], cm->cs));
   return SLF_OK;
@@ -2107,7 +2115,11 @@ slf_status slf_lce_fwd_bwd_dp(const void* hidden, const void* weight, const int3
         NcclApi& api = nccl_api();
         SLF_CUDA(cudaEventRecord(comm->ev_in, c.s));
         SLF_CUDA(cudaStreamWaitEvent(comm->cs, comm->ev_in, 0));
-        const ncclResult_t r = api.AllReduce(&hdr->n_valid, &hdr->n_valid, 1, ncclUint64, ncclSum, comm->nccl, comm->cs);
+        ncclResult_t r;
+        {
+          ProfScope ps(SLF_PROF_COMM_ALLREDUCE, comm->cs, 0.0, 8.0);
+          r = api.AllReduce(&hdr->n_valid, &hdr->n_valid, 1, ncclUint64, ncclSum, comm->nccl, comm->cs);
+        }
         if (r != ncclSuccess) return comm_fail_nccl(r, "ncclAllReduce(n_valid)");
         SLF_CUDA(cudaEventRecord(comm->ev_ag, comm->cs));
         SLF_CUDA(cudaStreamWaitEvent(c.s, comm->ev_ag, 0));
@@ -2135,7 +2147,11 @@ slf_status slf_lce_fwd_bwd_dp(const void* hidden, const void* weight, const int3
     NcclApi& api = nccl_api();
     SLF_CUDA(cudaEventRecord(comm->ev_in, c.s));
     SLF_CUDA(cudaStreamWaitEvent(comm->cs, comm->ev_in, 0));
-    const ncclResult_t r = api.AllReduce(dweight, dweight, (size_t)V * H, ncclBfloat16, ncclSum, comm->nccl, comm->cs);
+    ncclResult_t r;
+    {
+      ProfScope ps(SLF_PROF_COMM_ALLREDUCE, comm->cs, 0.0, (double)V * H * 2);
+      r = api.AllReduce(dweight, dweight, (size_t)V * H, ncclBfloat16, ncclSum, comm->nccl, comm->cs);
+    }
     if (r != ncclSuccess) return comm_fail_nccl(r, "ncclAllReduce(dW)");
     SLF_CUDA(cudaEventRecord(comm->ev_ag, comm->cs));
     SLF_CUDA(cudaStreamWaitEvent(c.s, comm->ev_ag, 0));
