@@ -374,6 +374,24 @@ slf_status slf_rmsnorm_bwd(const void* x, const void* g, const float* rstd, cons
  * workspace, and (in *n_valid, HOST, may be NULL) the number of valid rows. */
 slf_status slf_lce_status(const void* workspace, void* stream, int32_t* bad_targets, int64_t* n_valid);
 
+/* Target CSR of one vocabulary shard (the schedule-S one-hot dW correction reads
+ * it): a stable counting sort of the valid tokens whose target falls in [vocab_start,
+ * vocab_start + V_local) by t_i - vocab_start.  The method itself needs no CSR (PAPER.md l.273 only
+ * fixes the result); it is how dW[v] -= coef * sum_{t_i = v} x_i is formed exactly once per row.
+ *   targets   DEVICE int32 [N], 16-byte aligned                                     (read)
+ *   offsets   DEVICE int32 [V_local + 2]: offsets[v] .. offsets[v+1] delimit row v's tokens in
+ *             token_idx; offsets[V_local] = number of such tokens, offsets[V_local + 1] = number
+ *             of rows with at least one                                             (overwritten)
+ *   token_idx DEVICE int32 [N]: its first offsets[V_local] entries are the token indices grouped by
+ *             row, increasing within a row (stable)                                 (overwritten)
+ *   scratch   DEVICE, >= slf_target_csr_scratch_bytes(N, V_local) bytes, 16-byte aligned
+ * Integer only, deterministic (no atomics decide positions).  Enqueued on `stream`; errors are
+ * synchronous status codes.  The same kernels run inside slf_lce_fwd_bwd (schedule S). */
+size_t slf_target_csr_scratch_bytes(int64_t N, int64_t V_local);
+slf_status slf_target_csr(const int32_t* targets, int64_t N, int32_t ignore_index, int64_t vocab_start,
+                          int64_t V_local, int32_t* offsets, int32_t* token_idx, void* scratch, size_t scratch_bytes,
+                          void* stream);
+
 /* Test entry point: a plain bf16 GEMM D[M,N] (fp32, row-major, ld = N) =
  * A * B through the same tcgen05 core, with A [M,K] (a_mn = 0: K contiguous)
  * or stored as [K,M] (a_mn = 1), B stored [N,K] (b_mn = 0) or [K,N] (b_mn = 1).

@@ -374,6 +374,188 @@ __global__ void __launch_bounds__(256) csr_scatter_kernel(const int32_t* __restr
   if (key >= 0 && part == 0) idx[off[key - vocab_start] + rank] = (int32_t)i;  // valid and in shard
 }
 
+// ---- stable rank by block sort + binary search (replaces the brute-force rank above when the
+// workspace has scratch for N packed keys).  rank_i = #{j < i : t_j = t_i} is split
+// as (earlier token blocks) + (earlier tokens of i's own block).  Kernel 1 sorts each block of
+// CSR_SORT_T tokens by the packed key (t_i - vocab_start) << 12 | (i mod T) in shared memory
+// (bitonic; the packed keys are unique, so the order is the stable order by target); tokens that
+// are ignored or outside the shard sort last as 0xffffffff.  Kernel 2 counts, for a token with a
+// repeated target, the entries of its key in every earlier block and its own block's entries
+// before it with binary searches on the sorted blocks.  Integer and exact; no atomics decide
+// positions.  Needs V_l < 2^20.
+constexpr int CSR_SORT_T = 4096, CSR_SORT_SHIFT = 12;
+
+__global__ void __launch_bounds__(1024) csr_block_sort_kernel(const int32_t* __restrict__ t, int64_t N,
+                                                             int32_t ignore_index, int64_t vocab_start, int64_t V_l,
+                                                             uint32_t* __restrict__ sorted) {
+  __shared__ uint32_t k[CSR_SORT_T];
+  const int64_t b0 = (int64_t)blockIdx.x * CSR_SORT_T;
+#pragma unroll
+  for (int e = 0; e < CSR_SORT_T / 1024; ++e) {
+    const int li = e * 1024 + threadIdx.x;
+    const int64_t i = b0 + li;
+    uint32_t v = 0xffffffffu;
+    if (i < N) {
+      const int32_t tt = t[i];
+      if (in_shard(tt, ignore_index, vocab_start, V_l))
+        v = ((uint32_t)(tt - vocab_start) << CSR_SORT_SHIFT) | (uint32_t)li;
+    }
+    k[li] = v;
+  }
+  __syncthreads();
+  for (int size = 2; size <= CSR_SORT_T; size <<= 1) {
+    for (int stride = size >> 1; stride > 0; stride >>= 1) {
+#pragma unroll
+      for (int e = 0; e < CSR_SORT_T / 2048; ++e) {
+        const int j = e * 1024 + threadIdx.x;               // compare-exchange pair j of T/2
+        const int lo = 2 * j - (j & (stride - 1));          // first index of the pair
+        const int hi = lo + stride;
+        const bool up = (lo & size) == 0;
+        const uint32_t a = k[lo], b = k[hi];
+        if ((a > b) == up) {
+          k[lo] = b;
+          k[hi] = a;
+        }
+      }
+      __syncthreads();
+    }
+  }
+#pragma unroll
+  for (int e = 0; e < CSR_SORT_T / 1024; ++e) sorted[b0 + e * 1024 + threadIdx.x] = k[e * 1024 + threadIdx.x];
+}
+
+__device__ __forceinline__ int lower_bound_u32(const uint32_t* __restrict__ a, int n, uint32_t x) {
+  int lo = 0;
+  while (n > 0) {
+    const int h = n >> 1;
+    if (__ldg(a + lo + h) < x) {
+      lo += h + 1;
+      n -= h + 1;
+    } else {
+      n = h;
+    }
+  }
+  return lo;
+}
+
+__global__ void __launch_bounds__(256) csr_rank_scatter_kernel(const int32_t* __restrict__ t, int64_t N,
+                                                              int32_t ignore_index, int64_t vocab_start, int64_t V_l,
+                                                              const int32_t* __restrict__ cnt,
+                                                              const int32_t* __restrict__ off,
+                                                              const uint32_t* __restrict__ sorted,
+                                                              int32_t* __restrict__ idx) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= N) return;
+  const int32_t tt = t[i];
+  if (!in_shard(tt, ignore_index, vocab_start, V_l)) return;
+  const uint32_t key = (uint32_t)(tt - vocab_start);
+  int32_t rank = 0;
+  if (cnt[key] > 1) {
+    const uint32_t k0 = key << CSR_SORT_SHIFT, k1 = (key + 1) << CSR_SORT_SHIFT;
+    const int64_t b = i / CSR_SORT_T;
+    for (int64_t bb = 0; bb < b; ++bb) {  // every earlier block: its entries with this key
+      const uint32_t* blk = sorted + bb * CSR_SORT_T;
+      rank += lower_bound_u32(blk, CSR_SORT_T, k1) - lower_bound_u32(blk, CSR_SORT_T, k0);
+    }
+    const uint32_t* own = sorted + b * CSR_SORT_T;  // own block: entries of this key before token i
+    rank += lower_bound_u32(own, CSR_SORT_T, k0 | (uint32_t)(i - b * CSR_SORT_T)) - lower_bound_u32(own, CSR_SORT_T, k0);
+  }
+  idx[off[key] + rank] = (int32_t)i;
+}
+
+// ---- one-hot dW correction, segmented: dW[v] -= coef * sum_{t_i = v} x_i.
+// The CSR positions [0, n) (sorted by target, then token) are cut into segments of S positions;
+// pass 1 (one block per segment and 1024-column slab) walks its positions in order, summing x in
+// fp32 per target row: a row that starts and ends inside the segment is applied to dW at once;
+// the part of a row that continues from the previous segment goes to partial slot 0 of the
+// segment, the part of a row that starts here and continues to slot 1.  Pass 2: the segment where
+// such a row starts sums its slot 1 and the following segments' slot 0 in segment order and
+// applies it.  Each row's sum is therefore fp32 in token order within segments, the segment sums
+// added left to right: fixed order, deterministic, and a hot row (thousands of hits under Zipf
+// targets) is spread over many blocks instead of one block's serial loop.
+__device__ __forceinline__ void onehot_apply(uint16_t* __restrict__ dW, int64_t H, int32_t v, int64_t col, float c,
+                                             const float* acc) {
+  uint4* d = reinterpret_cast<uint4*>(dW + (size_t)v * H + col);
+  const uint4 o = *d;
+  *d = make_uint4(pack_bf16x2(bf16lo_to_f32(o.x) - c * acc[0], bf16hi_to_f32(o.x) - c * acc[1]),
+                  pack_bf16x2(bf16lo_to_f32(o.y) - c * acc[2], bf16hi_to_f32(o.y) - c * acc[3]),
+                  pack_bf16x2(bf16lo_to_f32(o.z) - c * acc[4], bf16hi_to_f32(o.z) - c * acc[5]),
+                  pack_bf16x2(bf16lo_to_f32(o.w) - c * acc[6], bf16hi_to_f32(o.w) - c * acc[7]));
+}
+
+__global__ void __launch_bounds__(128) onehot_seg_kernel(const uint16_t* __restrict__ X, int64_t H,
+                                                        const int32_t* __restrict__ t, int64_t vocab_start,
+                                                        const int32_t* __restrict__ off,
+                                                        const int32_t* __restrict__ idx, int64_t V_l, int S,
+                                                        int reduction, float scale, float grad_scale,
+                                                        const WsHeader* __restrict__ hdr, float* __restrict__ part,
+                                                        uint16_t* __restrict__ dW) {
+  const int64_t n = off[V_l];
+  const int64_t p0 = (int64_t)blockIdx.x * S;
+  if (p0 >= n) return;
+  const int64_t p1 = min(p0 + (int64_t)S, n);
+  const int64_t col = ((int64_t)blockIdx.y * 128 + threadIdx.x) * 8;
+  if (col >= H) return;
+  const float c = coef_of(reduction, scale, hdr->n_valid) * grad_scale;
+  int32_t row = t[idx[p0]] - (int32_t)vocab_start;
+  int64_t row_beg = off[row], row_end = off[row + 1];
+  float acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  for (int64_t p = p0; p < p1; ++p) {
+    const uint4 x = *reinterpret_cast<const uint4*>(X + (size_t)idx[p] * H + col);
+    acc[0] += bf16lo_to_f32(x.x); acc[1] += bf16hi_to_f32(x.x);
+    acc[2] += bf16lo_to_f32(x.y); acc[3] += bf16hi_to_f32(x.y);
+    acc[4] += bf16lo_to_f32(x.z); acc[5] += bf16hi_to_f32(x.z);
+    acc[6] += bf16lo_to_f32(x.w); acc[7] += bf16hi_to_f32(x.w);
+    if (p + 1 == row_end || p + 1 == p1) {
+      if (row_beg >= p0 && row_end <= p1) {
+        onehot_apply(dW, H, row, col, c, acc);
+      } else {
+        float* dst = part + ((size_t)blockIdx.x * 2 + (row_beg < p0 ? 0 : 1)) * H + col;
+        *reinterpret_cast<float4*>(dst) = make_float4(acc[0], acc[1], acc[2], acc[3]);
+        *reinterpret_cast<float4*>(dst + 4) = make_float4(acc[4], acc[5], acc[6], acc[7]);
+      }
+#pragma unroll
+      for (int k = 0; k < 8; ++k) acc[k] = 0.f;
+      if (p + 1 < p1) {
+        row = t[idx[p + 1]] - (int32_t)vocab_start;
+        row_beg = off[row];
+        row_end = off[row + 1];
+      }
+    }
+  }
+}
+
+__global__ void __launch_bounds__(128) onehot_join_kernel(int64_t H, const int32_t* __restrict__ t,
+                                                         int64_t vocab_start, const int32_t* __restrict__ off,
+                                                         const int32_t* __restrict__ idx, int64_t V_l, int S,
+                                                         int reduction, float scale, float grad_scale,
+                                                         const WsHeader* __restrict__ hdr,
+                                                         const float* __restrict__ part, uint16_t* __restrict__ dW) {
+  const int64_t n = off[V_l];
+  const int64_t p0 = (int64_t)blockIdx.x * S;
+  if (p0 >= n) return;
+  const int64_t p1 = min(p0 + (int64_t)S, n);
+  const int32_t row = t[idx[p1 - 1]] - (int32_t)vocab_start;  // the segment's last row
+  const int64_t row_beg = off[row], row_end = off[row + 1];
+  if (row_beg < p0 || row_end <= p1) return;  // it does not start here, or ends inside: not ours
+  const int64_t col = ((int64_t)blockIdx.y * 128 + threadIdx.x) * 8;
+  if (col >= H) return;
+  float acc[8];
+  {
+    const float* src = part + ((size_t)blockIdx.x * 2 + 1) * H + col;
+    const float4 a = *reinterpret_cast<const float4*>(src), b = *reinterpret_cast<const float4*>(src + 4);
+    acc[0] = a.x; acc[1] = a.y; acc[2] = a.z; acc[3] = a.w; acc[4] = b.x; acc[5] = b.y; acc[6] = b.z; acc[7] = b.w;
+  }
+  const int64_t q_last = (row_end - 1) / S;
+  for (int64_t q = blockIdx.x + 1; q <= q_last; ++q) {  // following segments' continuation parts, in order
+    const float* src = part + ((size_t)q * 2) * H + col;
+    const float4 a = *reinterpret_cast<const float4*>(src), b = *reinterpret_cast<const float4*>(src + 4);
+    acc[0] += a.x; acc[1] += a.y; acc[2] += a.z; acc[3] += a.w;
+    acc[4] += b.x; acc[5] += b.y; acc[6] += b.z; acc[7] += b.w;
+  }
+  onehot_apply(dW, H, row, col, coef_of(reduction, scale, hdr->n_valid) * grad_scale, acc);
+}
+
 // dW[v] = bf16( f32(dW[v]) - coef * sum_{i in CSR[v]} x_i ), sums in fp32 in token order.
 // grid.x over hit rows (bounded by min(N, V_l); n_hits in off[V_l + 1]), grid.y over 1024-column slabs.
 __global__ void __launch_bounds__(128) onehot_kernel(const uint16_t* __restrict__ X, int64_t H,

@@ -821,28 +821,49 @@ struct SArgs {
   int32_t ign;
 };
 
+// Target CSR of the shard: counts (integer atomics: order-free) -> exclusive
+// scan (offsets, hit rows) -> stable rank -> scatter.  The stable rank sorts blocks of 4096 tokens
+// by packed (target, token) keys in `scratch` (>= round_up(N, 4096) * 4 bytes) and binary-searches
+// them; without that much scratch it falls back to the brute-force rank.  `bsum` (>= 8 bytes per
+// 8192 vocabulary rows, or null) holds the multi-block scan's span totals.
+size_t csr_sort_bytes(int64_t N) { return (size_t)((N + CSR_SORT_T - 1) / CSR_SORT_T) * CSR_SORT_T * 4; }
+
+slf_status build_csr(cudaStream_t st, const int32_t* t, int64_t N, int32_t ign, int64_t vs, int64_t V_l, int32_t* cnt,
+                     int32_t* off, int32_t* hits, int32_t* idx, int2* bsum, size_t bsum_bytes, uint8_t* scratch,
+                     size_t scratch_bytes) {
+  ProfScope ps(SLF_PROF_CSR, st, 0.0, (double)V_l * 12 + (double)N * 12);
+  csr_zero_kernel<<<(unsigned)std::min<int64_t>((V_l + 2 + 255) / 256, 1024), 256, 0, st>>>(cnt, V_l + 2);
+  csr_count_kernel<<<(unsigned)((N + 255) / 256), 256, 0, st>>>(t, N, ign, vs, V_l, cnt);
+  const int64_t nspan = (V_l + CSR_SCAN_SPAN - 1) / CSR_SCAN_SPAN;
+  if (nspan > 1 && bsum && (size_t)nspan * 8 <= bsum_bytes) {
+    csr_blocksum_kernel<<<(unsigned)nspan, 1024, 0, st>>>(cnt, V_l, bsum);
+    csr_scan_kernel<<<(unsigned)nspan, 1024, 0, st>>>(cnt, V_l, off, hits, bsum);
+  } else {
+    csr_scan_kernel<<<1, 1024, 0, st>>>(cnt, V_l, off, hits);
+  }
+  static const bool brute = getenv("SLF_CSR_BRUTE") != nullptr;  // A/B knob: the round-1 rank
+  if (!brute && scratch && scratch_bytes >= csr_sort_bytes(N) && V_l < (1 << (32 - CSR_SORT_SHIFT))) {
+    uint32_t* sorted = reinterpret_cast<uint32_t*>(scratch);
+    csr_block_sort_kernel<<<(unsigned)((N + CSR_SORT_T - 1) / CSR_SORT_T), 1024, 0, st>>>(t, N, ign, vs, V_l, sorted);
+    csr_rank_scatter_kernel<<<(unsigned)((N + 255) / 256), 256, 0, st>>>(t, N, ign, vs, V_l, cnt, off, sorted, idx);
+  } else {
+    csr_scatter_kernel<<<(unsigned)((N + CSR_TOK_PER_BLOCK - 1) / CSR_TOK_PER_BLOCK), 256, 0, st>>>(t, N, ign, vs,
+                                                                                                  V_l, cnt, off, idx);
+  }
+  SLF_CUDA(cudaGetLastError());
+  return SLF_OK;
+}
+
 slf_status s_begin(Ctx& c, const SArgs& a, bool need_dw) {
   const Plan& p = c.plan;
   SLF_TRY(launch_prep(c, a.t, a.N, a.ign, a.Vg));
   if (need_dw) {
-    int32_t* cnt = reinterpret_cast<int32_t*>(c.ws + p.off_cnt);
-    int32_t* off = reinterpret_cast<int32_t*>(c.ws + p.off_off);
-    int32_t* hits = reinterpret_cast<int32_t*>(c.ws + p.off_hits);
-    int32_t* idx = reinterpret_cast<int32_t*>(c.ws + p.off_idx);
-    ProfScope ps(SLF_PROF_CSR, c.s, 0.0, (double)a.V_l * 12 + (double)a.N * 12);
-    csr_zero_kernel<<<(unsigned)std::min<int64_t>((a.V_l + 2 + 255) / 256, 1024), 256, 0, c.s>>>(cnt, a.V_l + 2);
-    csr_count_kernel<<<(unsigned)((a.N + 255) / 256), 256, 0, c.s>>>(a.t, a.N, a.ign, a.vs, a.V_l, cnt);
-    const int64_t nspan = (a.V_l + CSR_SCAN_SPAN - 1) / CSR_SCAN_SPAN;
-    if (nspan > 1 && (size_t)nspan * 8 <= (size_t)a.N * 16) {  // span totals in the (idle) ShardStat area
-      int2* bsum = reinterpret_cast<int2*>(c.ws + p.off_shard);
-      csr_blocksum_kernel<<<(unsigned)nspan, 1024, 0, c.s>>>(cnt, a.V_l, bsum);
-      csr_scan_kernel<<<(unsigned)nspan, 1024, 0, c.s>>>(cnt, a.V_l, off, hits, bsum);
-    } else {
-      csr_scan_kernel<<<1, 1024, 0, c.s>>>(cnt, a.V_l, off, hits);
-    }
-    csr_scatter_kernel<<<(unsigned)((a.N + CSR_TOK_PER_BLOCK - 1) / CSR_TOK_PER_BLOCK), 256, 0, c.s>>>(
-        a.t, a.N, a.ign, a.vs, a.V_l, cnt, off, idx);
-    SLF_CUDA(cudaGetLastError());
+    // scratch: the tile-partials + stash region, idle until the first chunk's stash GEMM; span
+    // totals in the (idle) ShardStat area
+    SLF_TRY(build_csr(c.s, a.t, a.N, a.ign, a.vs, a.V_l, reinterpret_cast<int32_t*>(c.ws + p.off_cnt),
+                      reinterpret_cast<int32_t*>(c.ws + p.off_off), reinterpret_cast<int32_t*>(c.ws + p.off_hits),
+                      reinterpret_cast<int32_t*>(c.ws + p.off_idx), reinterpret_cast<int2*>(c.ws + p.off_shard),
+                      (size_t)a.N * 16, c.ws + p.off_part, p.total - p.off_part));
   }
   return SLF_OK;
 }
@@ -1044,12 +1065,29 @@ slf_status s_end(Ctx& c, const SArgs& a, int reduction, float scale, float* loss
   const Plan& p = c.plan;
   if (dW) {
     ProfScope ps(SLF_PROF_ONEHOT, c.s, 0.0, (double)a.N * a.H * 2 * 2);
-    dim3 grid((unsigned)std::min<int64_t>(a.N, a.V_l), (unsigned)((a.H + 1023) / 1024));
-    onehot_kernel<<<grid, 128, 0, c.s>>>(reinterpret_cast<const uint16_t*>(a.X), a.H,
-                                         reinterpret_cast<const int32_t*>(c.ws + p.off_off),
-                                         reinterpret_cast<const int32_t*>(c.ws + p.off_idx),
-                                         reinterpret_cast<const int32_t*>(c.ws + p.off_hits), a.V_l, reduction, scale,
-                                         1.0f, hdr_of(c.ws), reinterpret_cast<uint16_t*>(dW));
+    static const bool serial = getenv("SLF_ONEHOT_SERIAL") != nullptr;  // A/B knob: the round-1 kernel
+    // segment partials in the tile-partials + stash region (idle after the last chunk): S positions
+    // per segment, doubled until [segments][2][H] fp32 fits
+    const size_t scratch = p.total - p.off_part;
+    int S = 32;
+    while ((size_t)((a.N + S - 1) / S) * 8 * a.H > scratch && S < (1 << 30)) S *= 2;
+    const unsigned segs = (unsigned)((a.N + S - 1) / S), slabs = (unsigned)((a.H + 1023) / 1024);
+    const int32_t* off = reinterpret_cast<const int32_t*>(c.ws + p.off_off);
+    const int32_t* idx = reinterpret_cast<const int32_t*>(c.ws + p.off_idx);
+    if (serial) {
+      dim3 grid((unsigned)std::min<int64_t>(a.N, a.V_l), slabs);
+      onehot_kernel<<<grid, 128, 0, c.s>>>(reinterpret_cast<const uint16_t*>(a.X), a.H, off, idx,
+                                           reinterpret_cast<const int32_t*>(c.ws + p.off_hits), a.V_l, reduction,
+                                           scale, 1.0f, hdr_of(c.ws), reinterpret_cast<uint16_t*>(dW));
+    } else {
+      float* part = reinterpret_cast<float*>(c.ws + p.off_part);
+      onehot_seg_kernel<<<dim3(segs, slabs), 128, 0, c.s>>>(reinterpret_cast<const uint16_t*>(a.X), a.H, a.t, a.vs,
+                                                             off, idx, a.V_l, S, reduction, scale, 1.0f, hdr_of(c.ws),
+                                                             part, reinterpret_cast<uint16_t*>(dW));
+      onehot_join_kernel<<<dim3(segs, slabs), 128, 0, c.s>>>(a.H, a.t, a.vs, off, idx, a.V_l, S, reduction, scale,
+                                                              1.0f, hdr_of(c.ws), part,
+                                                              reinterpret_cast<uint16_t*>(dW));
+    }
     SLF_CUDA(cudaGetLastError());
   }
   if (reduction != SLF_NONE) {
@@ -2272,6 +2310,38 @@ slf_status slf_lce_status(const void* workspace, void* stream, int32_t* bad_targ
   *bad_targets = h.bad;
   if (n_valid) *n_valid = (int64_t)h.n_valid;
   return SLF_OK;
+}
+
+// scratch: counts [V_l + 2] | hit rows [min(N, V_l)] | span totals | packed sort keys
+static void csr_scratch_layout(int64_t N, int64_t V_l, size_t* o_hits, size_t* o_bsum, size_t* o_sort, size_t* total) {
+  *o_hits = align_up((size_t)(V_l + 2) * 4, 256);
+  *o_bsum = align_up(*o_hits + (size_t)std::min(N, V_l) * 4, 256);
+  *o_sort = align_up(*o_bsum + (size_t)((V_l + CSR_SCAN_SPAN - 1) / CSR_SCAN_SPAN) * 8, 256);
+  *total = *o_sort + csr_sort_bytes(N);
+}
+
+size_t slf_target_csr_scratch_bytes(int64_t N, int64_t V_local) {
+  if (N < 1 || V_local < 1) return 0;
+  size_t a, b, c, t;
+  csr_scratch_layout(N, V_local, &a, &b, &c, &t);
+  return t;
+}
+
+slf_status slf_target_csr(const int32_t* targets, int64_t N, int32_t ignore_index, int64_t vocab_start,
+                          int64_t V_local, int32_t* offsets, int32_t* token_idx, void* scratch, size_t scratch_bytes,
+                          void* stream) {
+  if (!targets || !offsets || !token_idx || !scratch) return fail(SLF_ERR_ARG, "null pointer");
+  if (N < 1 || V_local < 1 || vocab_start < 0 || N > (1ll << 31) - 1 || V_local >= (1ll << 20))
+    return fail(SLF_ERR_ARG, "bad sizes N=%lld V_local=%lld", (long long)N, (long long)V_local);
+  if (!aligned16(targets) || !aligned16(scratch)) return fail(SLF_ERR_ALIGN, "targets / scratch must be 16-byte aligned");
+  size_t o_hits, o_bsum, o_sort, total;
+  csr_scratch_layout(N, V_local, &o_hits, &o_bsum, &o_sort, &total);
+  if (scratch_bytes < total) return fail(SLF_ERR_WORKSPACE, "scratch %zu bytes < required %zu", scratch_bytes, total);
+  uint8_t* sc = reinterpret_cast<uint8_t*>(scratch);
+  int32_t* cnt = reinterpret_cast<int32_t*>(sc);
+  return build_csr(reinterpret_cast<cudaStream_t>(stream), targets, N, ignore_index, vocab_start, V_local, cnt, offsets,
+                   reinterpret_cast<int32_t*>(sc + o_hits), token_idx, reinterpret_cast<int2*>(sc + o_bsum),
+                   o_sort - o_bsum, sc + o_sort, total - o_sort);
 }
 
 slf_status slf_lce_dx_finalize(const float* dhidden_fp32, const slf_rowstat* rowstat, void* dhidden, int64_t N,

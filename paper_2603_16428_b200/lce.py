@@ -240,6 +240,22 @@ def status(workspace, device=None):
     return bad.value, nv.value
 
 
+def target_csr(targets, V_local: int, vocab_start: int = 0, ignore_index: int = -100):
+    """Target CSR of a vocabulary shard (slf_target_csr): returns (offsets [V_local + 2] int32,
+    token_idx [N] int32) on the targets' device; see include/slf_lce.h."""
+    if not targets.is_cuda or targets.dtype != torch.int32 or not targets.is_contiguous():
+        raise TypeError("targets must be a contiguous CUDA int32 tensor")
+    N = targets.numel()
+    dev = targets.device
+    offsets = torch.empty(V_local + 2, dtype=torch.int32, device=dev)
+    idx = torch.empty(N, dtype=torch.int32, device=dev)
+    nb = lib().slf_target_csr_scratch_bytes(N, V_local)
+    scratch = torch.empty(max(nb, 16), dtype=torch.uint8, device=dev)
+    check(lib().slf_target_csr(targets.data_ptr(), N, ignore_index, vocab_start, V_local, offsets.data_ptr(),
+                               idx.data_ptr(), scratch.data_ptr(), scratch.numel(), _stream_ptr(dev)), "slf_target_csr")
+    return offsets, idx
+
+
 def dx_finalize(dx32, rowstat, out=None):
     """bf16 dhidden from the fp32 sum of shard partials (ignored rows -> +0.0)."""
     N, H = dx32.shape

@@ -803,3 +803,34 @@ def test_stats_epilogues_vs_oracle(slf, V, v0, v1):
         assert np.array_equal(st[:, 3] == 1.0, hit_ref)
         assert np.max(np.abs(st[hit_ref, 2] - z_ref[hit_ref])) <= 1e-5 * scale_z
         assert not st[~hit_ref, 2].any()
+
+
+# ---- target CSR: bit-exact against a stable sort ------------------------------
+@pytest.mark.parametrize("N,V,v0,Vl,dist,ign", [
+    (1, 10, 0, 10, "uniform", 0.0), (1000, 5000, 0, 5000, "zipf", 0.05), (4097, 300, 0, 300, "zipf", 0.1),
+    (16384, 128256, 0, 128256, "zipf", 0.05), (16384, 128256, 64128, 16032, "uniform", 0.05),
+    (65536, 32768, 0, 32768, "zipf", 0.05), (20000, 7, 0, 7, "uniform", 0.3), (9000, 5000, 1234, 2000, "same", 0.05),
+    (5000, 5000, 0, 5000, "ignored", 0.0)])
+def test_target_csr_bit_exact(slf, N, V, v0, Vl, dist, ign):
+    """offsets = exclusive scan of the in-shard target histogram, token_idx = the in-shard valid
+    tokens ordered by (target, token index) — numpy's stable argsort — every entry bit-exact,
+    including the hit-row count; hot Zipf rows, one repeated target, all ignored, tiny V."""
+    if dist in ("same", "ignored"):
+        t = np.full(N, v0 + 7 if dist == "same" else -100, dtype=np.int32)
+        t[::20] = -100
+    else:
+        t = synth.make_targets(N, V, seed=N + Vl, dist=dist, ignore_frac=ign)
+    td = torch.from_numpy(t).cuda()
+    off, idx = slf.target_csr(td, Vl, vocab_start=v0)
+    torch.cuda.synchronize()
+    off, idx = off.cpu().numpy(), idx.cpu().numpy()
+    loc = t.astype(np.int64) - v0
+    sel = (t != -100) & (loc >= 0) & (loc < Vl)
+    counts = np.bincount(loc[sel], minlength=Vl)
+    ref_off = np.concatenate([[0], np.cumsum(counts)])
+    n = int(sel.sum())
+    tok = np.nonzero(sel)[0]
+    ref_idx = tok[np.argsort(loc[sel], kind="stable")]
+    assert np.array_equal(off[:Vl + 1], ref_off)
+    assert off[Vl + 1] == int((counts > 0).sum())
+    assert np.array_equal(idx[:n], ref_idx)
