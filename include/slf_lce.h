@@ -369,6 +369,28 @@ slf_status slf_rmsnorm_fwd(const void* x, const void* g, int64_t N, int64_t H, f
 slf_status slf_rmsnorm_bwd(const void* x, const void* g, const float* rstd, const void* dy, int64_t N, int64_t H,
                            void* dx, float* dg, void* workspace, size_t workspace_bytes, void* stream);
 
+/* The final RMSNorm fused into the LCE (PAPER.md l.273 lists RMSNorm among the
+ * fused Triton kernels): loss, dx = d loss / d x, dg = d loss / d g and dW of
+ *     loss = LCE(rmsnorm(x, g, eps) W^T, targets)
+ * in one call, schedule S, without the [N, H] normalised activations: per row chunk one launch
+ * forms the chunk's y = bf16(x * rstd * g) (the same bits as slf_rmsnorm_fwd) into a chunk buffer
+ * in the workspace, the stash / dX / dW GEMMs read it there, and the next launch turns the chunk's
+ * dy (the group's bf16 dX output, in `dx`) into dx in place and accumulates dg (fp32, fixed order).
+ * The one-hot dW term recomputes y from x, rstd and g.
+ *   x [N, H] bf16, g [H] bf16, weight [V, H] bf16, targets [N] int32                    (read)
+ *   loss_out [1] (SUM/MEAN) or [N] (NONE) fp32; dx [N, H] bf16; dg [H] fp32; dweight [V, H] bf16
+ *                                                                                        (overwritten)
+ *   workspace >= slf_rmsnorm_lce_workspace_bytes(N, H, V, budget_bytes): budget 0 = the LCE's default
+ *   plan (5 % of N*V*2) plus the chunk buffers; else the whole layout fits within budget_bytes.
+ * All DEVICE pointers, 16-byte aligned, non-null; H % 8 == 0, H <= 16384.  Errors as slf_lce_fwd_bwd
+ * (SLF_ERR_WORKSPACE if no schedule-S plan fits). */
+size_t slf_rmsnorm_lce_workspace_bytes(int64_t N, int64_t H, int64_t V, size_t budget_bytes);
+slf_status slf_rmsnorm_lce_plan_describe(int64_t N, int64_t H, int64_t V, size_t budget_bytes, char* out, size_t cap);
+slf_status slf_rmsnorm_lce_fwd_bwd(const void* x, const void* g, float eps, const void* weight, const int32_t* targets,
+                                   int64_t N, int64_t H, int64_t V, int32_t ignore_index, int reduction, float scale,
+                                   float* loss_out, void* dx, float* dg, void* dweight, void* workspace,
+                                   size_t workspace_bytes, size_t budget_bytes, void* stream);
+
 /* Synchronises `stream` and returns (in *bad_targets, HOST) the number of
  * valid targets outside [0, V_global) seen by the last call that used this
  * workspace, and (in *n_valid, HOST, may be NULL) the number of valid rows. */

@@ -483,13 +483,30 @@ __device__ __forceinline__ void onehot_apply(uint16_t* __restrict__ dW, int64_t 
                   pack_bf16x2(bf16lo_to_f32(o.w) - c * acc[6], bf16hi_to_f32(o.w) - c * acc[7]));
 }
 
+// The CSR row holding position p: the largest r with off[r] <= p (its off[r + 1] > p, so r has hits).
+__device__ __forceinline__ int32_t csr_row_of(const int32_t* __restrict__ off, int64_t V_l, int64_t p) {
+  int64_t lo = 0, n = V_l;  // search off[0 .. V_l): first index with off > p, minus one
+  while (n > 0) {
+    const int64_t h = n >> 1;
+    if (off[lo + h] <= p) {
+      lo += h + 1;
+      n -= h + 1;
+    } else {
+      n = h;
+    }
+  }
+  return (int32_t)(lo - 1);
+}
+
 __global__ void __launch_bounds__(128) onehot_seg_kernel(const uint16_t* __restrict__ X, int64_t H,
-                                                        const int32_t* __restrict__ t, int64_t vocab_start,
                                                         const int32_t* __restrict__ off,
                                                         const int32_t* __restrict__ idx, int64_t V_l, int S,
                                                         int reduction, float scale, float grad_scale,
                                                         const WsHeader* __restrict__ hdr, float* __restrict__ part,
-                                                        uint16_t* __restrict__ dW) {
+                                                        uint16_t* __restrict__ dW, const float* __restrict__ rstd,
+                                                        const uint16_t* __restrict__ gam) {
+  // rstd / gam (fused final RMSNorm, else null): the GEMMs' rows are y = bf16(x * rstd * g), so the
+  // one-hot term sums exactly those bf16 values, recomputed here with the forward's fp32 ops.
   const int64_t n = off[V_l];
   const int64_t p0 = (int64_t)blockIdx.x * S;
   if (p0 >= n) return;
@@ -497,11 +514,25 @@ __global__ void __launch_bounds__(128) onehot_seg_kernel(const uint16_t* __restr
   const int64_t col = ((int64_t)blockIdx.y * 128 + threadIdx.x) * 8;
   if (col >= H) return;
   const float c = coef_of(reduction, scale, hdr->n_valid) * grad_scale;
-  int32_t row = t[idx[p0]] - (int32_t)vocab_start;
+  float gw[8];
+  if (rstd) {
+    const uint4 q = *reinterpret_cast<const uint4*>(gam + col);
+    gw[0] = bf16lo_to_f32(q.x); gw[1] = bf16hi_to_f32(q.x); gw[2] = bf16lo_to_f32(q.y); gw[3] = bf16hi_to_f32(q.y);
+    gw[4] = bf16lo_to_f32(q.z); gw[5] = bf16hi_to_f32(q.z); gw[6] = bf16lo_to_f32(q.w); gw[7] = bf16hi_to_f32(q.w);
+  }
+  int32_t row = csr_row_of(off, V_l, p0);
   int64_t row_beg = off[row], row_end = off[row + 1];
   float acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
   for (int64_t p = p0; p < p1; ++p) {
-    const uint4 x = *reinterpret_cast<const uint4*>(X + (size_t)idx[p] * H + col);
+    const int32_t tok = idx[p];
+    uint4 x = *reinterpret_cast<const uint4*>(X + (size_t)tok * H + col);
+    if (rstd) {
+      const float r = rstd[tok];
+      x = make_uint4(pack_bf16x2(bf16lo_to_f32(x.x) * r * gw[0], bf16hi_to_f32(x.x) * r * gw[1]),
+                     pack_bf16x2(bf16lo_to_f32(x.y) * r * gw[2], bf16hi_to_f32(x.y) * r * gw[3]),
+                     pack_bf16x2(bf16lo_to_f32(x.z) * r * gw[4], bf16hi_to_f32(x.z) * r * gw[5]),
+                     pack_bf16x2(bf16lo_to_f32(x.w) * r * gw[6], bf16hi_to_f32(x.w) * r * gw[7]));
+    }
     acc[0] += bf16lo_to_f32(x.x); acc[1] += bf16hi_to_f32(x.x);
     acc[2] += bf16lo_to_f32(x.y); acc[3] += bf16hi_to_f32(x.y);
     acc[4] += bf16lo_to_f32(x.z); acc[5] += bf16hi_to_f32(x.z);
@@ -517,7 +548,7 @@ __global__ void __launch_bounds__(128) onehot_seg_kernel(const uint16_t* __restr
 #pragma unroll
       for (int k = 0; k < 8; ++k) acc[k] = 0.f;
       if (p + 1 < p1) {
-        row = t[idx[p + 1]] - (int32_t)vocab_start;
+        row = csr_row_of(off, V_l, p + 1);
         row_beg = off[row];
         row_end = off[row + 1];
       }
@@ -525,9 +556,7 @@ __global__ void __launch_bounds__(128) onehot_seg_kernel(const uint16_t* __restr
   }
 }
 
-__global__ void __launch_bounds__(128) onehot_join_kernel(int64_t H, const int32_t* __restrict__ t,
-                                                         int64_t vocab_start, const int32_t* __restrict__ off,
-                                                         const int32_t* __restrict__ idx, int64_t V_l, int S,
+__global__ void __launch_bounds__(128) onehot_join_kernel(int64_t H, const int32_t* __restrict__ off, int64_t V_l, int S,
                                                          int reduction, float scale, float grad_scale,
                                                          const WsHeader* __restrict__ hdr,
                                                          const float* __restrict__ part, uint16_t* __restrict__ dW) {
@@ -535,7 +564,7 @@ __global__ void __launch_bounds__(128) onehot_join_kernel(int64_t H, const int32
   const int64_t p0 = (int64_t)blockIdx.x * S;
   if (p0 >= n) return;
   const int64_t p1 = min(p0 + (int64_t)S, n);
-  const int32_t row = t[idx[p1 - 1]] - (int32_t)vocab_start;  // the segment's last row
+  const int32_t row = csr_row_of(off, V_l, p1 - 1);  // the segment's last row
   const int64_t row_beg = off[row], row_end = off[row + 1];
   if (row_beg < p0 || row_end <= p1) return;  // it does not start here, or ends inside: not ours
   const int64_t col = ((int64_t)blockIdx.y * 128 + threadIdx.x) * 8;

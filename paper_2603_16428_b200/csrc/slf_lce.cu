@@ -877,6 +877,7 @@ struct SChunk {
   uint8_t* ext_base;  // stash rows [rows - ext, rows): row stride ld_stash, or nullptr
   uint8_t* xt = nullptr;  // X_chunk^T [H][ld_xt] (dW's B operand K-major) in free dhidden rows, or nullptr
   int64_t ld_xt = 0;
+  const uint8_t* xrows = nullptr;  // the chunk's hidden rows when not X + r0 (fused RMSNorm: its y buffer)
 };
 
 SChunk s_plain_chunk(const Plan& p, int64_t N, int64_t ch) {
@@ -909,7 +910,8 @@ slf_status s_chunk_stats(Ctx& c, const SArgs& a, const SChunk& k, slf_shardstat*
   float* zt = reinterpret_cast<float*>(c.ws + p.off_zt);
   float2* part = reinterpret_cast<float2*>(c.ws + p.off_part);
   ProbSpec ps;
-  SLF_TRY(tmap_kmajor(&ps.ta, reinterpret_cast<const uint8_t*>(a.X) + (size_t)r0 * a.H * 2, a.H, rows, a.H, BM));
+  const uint8_t* Xr = k.xrows ? k.xrows : reinterpret_cast<const uint8_t*>(a.X) + (size_t)r0 * a.H * 2;
+  SLF_TRY(tmap_kmajor(&ps.ta, Xr, a.H, rows, a.H, BM));
   SLF_TRY(tmap_kmajor(&ps.tb, a.W, a.H, a.V_l, a.H, b_box_rows()));
   GemmArgs g{};
   g.M = (int)rows;
@@ -948,7 +950,7 @@ slf_status s_build_bwd(Ctx& c, const SArgs& a, const SChunk& k, void* dXc, int d
   const Plan& p = c.plan;
   const int cg = cta_group();
   const int64_t r0 = k.r0, rows = k.rows, main_rows = rows - k.ext;
-  const uint8_t* Xr = reinterpret_cast<const uint8_t*>(a.X) + (size_t)r0 * a.H * 2;
+  const uint8_t* Xr = k.xrows ? k.xrows : reinterpret_cast<const uint8_t*>(a.X) + (size_t)r0 * a.H * 2;
   uint8_t* stash = c.ws + p.off_stash;
   slf_rowstat* rs = reinterpret_cast<slf_rowstat*>(c.ws + p.off_rowstat);
   *n = 0;
@@ -1061,7 +1063,8 @@ slf_status s_chunk_bwd(Ctx& c, const SArgs& a, const SChunk& k, const slf_shards
   return launch_group(c.dev, ps, n, c.s, sched, sched_stride, n == 2 ? SLF_PROF_GEMM_GROUP : -1);
 }
 
-slf_status s_end(Ctx& c, const SArgs& a, int reduction, float scale, float* loss_out, void* dW) {
+slf_status s_end(Ctx& c, const SArgs& a, int reduction, float scale, float* loss_out, void* dW,
+                 const float* rstd = nullptr, const void* gam = nullptr) {
   const Plan& p = c.plan;
   if (dW) {
     ProfScope ps(SLF_PROF_ONEHOT, c.s, 0.0, (double)a.N * a.H * 2 * 2);
@@ -1074,17 +1077,18 @@ slf_status s_end(Ctx& c, const SArgs& a, int reduction, float scale, float* loss
     const unsigned segs = (unsigned)((a.N + S - 1) / S), slabs = (unsigned)((a.H + 1023) / 1024);
     const int32_t* off = reinterpret_cast<const int32_t*>(c.ws + p.off_off);
     const int32_t* idx = reinterpret_cast<const int32_t*>(c.ws + p.off_idx);
-    if (serial) {
+    if (serial && !rstd) {
       dim3 grid((unsigned)std::min<int64_t>(a.N, a.V_l), slabs);
       onehot_kernel<<<grid, 128, 0, c.s>>>(reinterpret_cast<const uint16_t*>(a.X), a.H, off, idx,
                                            reinterpret_cast<const int32_t*>(c.ws + p.off_hits), a.V_l, reduction,
                                            scale, 1.0f, hdr_of(c.ws), reinterpret_cast<uint16_t*>(dW));
     } else {
       float* part = reinterpret_cast<float*>(c.ws + p.off_part);
-      onehot_seg_kernel<<<dim3(segs, slabs), 128, 0, c.s>>>(reinterpret_cast<const uint16_t*>(a.X), a.H, a.t, a.vs,
+      onehot_seg_kernel<<<dim3(segs, slabs), 128, 0, c.s>>>(reinterpret_cast<const uint16_t*>(a.X), a.H,
                                                              off, idx, a.V_l, S, reduction, scale, 1.0f, hdr_of(c.ws),
-                                                             part, reinterpret_cast<uint16_t*>(dW));
-      onehot_join_kernel<<<dim3(segs, slabs), 128, 0, c.s>>>(a.H, a.t, a.vs, off, idx, a.V_l, S, reduction, scale,
+                                                             part, reinterpret_cast<uint16_t*>(dW), rstd,
+                                                             reinterpret_cast<const uint16_t*>(gam));
+      onehot_join_kernel<<<dim3(segs, slabs), 128, 0, c.s>>>(a.H, off, a.V_l, S, reduction, scale,
                                                               1.0f, hdr_of(c.ws), part,
                                                               reinterpret_cast<uint16_t*>(dW));
     }
@@ -1145,12 +1149,89 @@ std::vector<SChunk> s_chunks(const Plan& p, int64_t N, int64_t H, bool extend, u
 // The fused single-GPU call under schedule S (g = 1: a chunk's statistics are its own).  When dX
 // is requested, the chunks are extended into dhidden's not-yet-written rows (s_chunks): fewer
 // chunks, fewer dW accumulation passes and longer dW K, at no extra memory.
+// The final RMSNorm fused into the chunk loop (slf_rmsnorm_lce_fwd_bwd): X is the
+// RMSNorm input x; each chunk's y rows are formed into `ybuf` right before its stash GEMM and the
+// chunk's dx / dg right after its grouped GEMMs (rms_step_kernel, one launch per chunk boundary).
+struct RmsFuse {
+  const void* g;
+  float eps;
+  float* dg;        // caller's fp32 [H]
+  uint8_t* ybuf;    // [max chunk rows][H] bf16
+  float* rstd;      // [N]
+  float* part[2];   // [nb_max][H] fp32 dg partials, double-buffered by chunk parity
+  int nb_max;
+};
+
+constexpr int RMS_NB_MAX = 148;  // backward blocks per chunk (one per B200 SM); sizes the dg partials
+
+int rms_blocks(const DevInfo* dev, int64_t rows, int* rpb) {
+  const int64_t nb = std::max<int64_t>(1, std::min<int64_t>(rows, std::min(dev->sms, RMS_NB_MAX)));
+  *rpb = (int)((rows + nb - 1) / nb);
+  return (int)((rows + *rpb - 1) / *rpb);
+}
+
+// One rms_step launch: backward of chunk `kb` (or none), forward of chunk `kf` (or none), dg
+// reduction of chunk `kr` (or none).
+slf_status launch_rms_step(Ctx& c, const SArgs& a, const RmsFuse& rf, void* dX, const SChunk* kb, const SChunk* kf,
+                           const SChunk* kr, int nb_kr, bool red_first) {
+  RmsStep r{};
+  r.x = reinterpret_cast<const uint16_t*>(a.X);
+  r.g = reinterpret_cast<const uint16_t*>(rf.g);
+  r.H = a.H;
+  r.eps = rf.eps;
+  r.rstd = rf.rstd;
+  r.dx = reinterpret_cast<uint16_t*>(dX);
+  if (kb) {
+    r.b_r0 = kb->r0;
+    r.b_rows = kb->rows;
+    r.nb_bwd = rms_blocks(c.dev, kb->rows, &r.b_rpb);
+    r.part_b = rf.part[kb->index & 1];
+  }
+  if (kf) {
+    r.f_r0 = kf->r0;
+    r.f_rows = kf->rows;
+    r.ybuf = reinterpret_cast<uint16_t*>(rf.ybuf);
+  }
+  if (kr) {
+    r.nb_red = (int)((a.H + RMS_THREADS - 1) / RMS_THREADS);
+    r.red_nblk = nb_kr;
+    r.red_first = red_first ? 1 : 0;
+    r.part_r = rf.part[kr->index & 1];
+    r.dg = rf.dg;
+  }
+  const unsigned blocks = (unsigned)(r.nb_bwd + r.f_rows + r.nb_red);
+  if (!blocks) return SLF_OK;
+  ProfScope ps(SLF_PROF_RMSNORM, c.s, 0.0,
+               (kb ? (double)kb->rows * a.H * 8 : 0.0) + (kf ? (double)kf->rows * a.H * 4 : 0.0));
+  const size_t smem = (size_t)a.H * 4;
+  if (smem > 48 * 1024)
+    SLF_CUDA(cudaFuncSetAttribute(rms_step_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(blocks);
+  cfg.blockDim = dim3(RMS_THREADS);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = c.s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  SLF_CUDA(cudaLaunchKernelEx(&cfg, rms_step_kernel, r));
+  return SLF_OK;
+}
+
 slf_status phase_s(Ctx& c, const void* X, const void* W, const int32_t* t, int64_t N, int64_t H, int64_t V,
-                   int32_t ignore_index, int reduction, float scale, float* loss_out, void* dX, void* dW) {
+                   int32_t ignore_index, int reduction, float scale, float* loss_out, void* dX, void* dW,
+                   const RmsFuse* rf = nullptr) {
   const Plan& p = c.plan;
   const SArgs a{X, W, t, N, H, V, 0, V, ignore_index};
   SLF_TRY(s_begin(c, a, dW != nullptr));
-  const std::vector<SChunk> chunks = s_chunks(p, N, H, dX != nullptr, reinterpret_cast<uint8_t*>(dX));
+  std::vector<SChunk> chunks = s_chunks(p, N, H, dX != nullptr, reinterpret_cast<uint8_t*>(dX));
+  if (rf)
+    for (auto& k : chunks) {  // the chunk's y rows (dW's B operand too); no X^T variant
+      k.xrows = rf->ybuf;
+      k.xt = nullptr;
+    }
   // LPT tables per distinct chunk shape (rows, ext, first/RMW), uploaded once.
   SchedArena arena;
   std::vector<std::pair<std::pair<int64_t, int64_t>, int>> keys;
@@ -1188,10 +1269,26 @@ slf_status phase_s(Ctx& c, const void* X, const void* W, const int32_t* t, int64
     if (c.chunk_ready && i <= 2)
       SLF_CUDA(cudaStreamWaitEvent(c.s, c.chunk_ready[i < 2 ? i : chunks.size() - 1], 0));
     if (k.xt && dW) SLF_TRY(launch_transpose_x(c, a, k));
+    if (rf) {  // y of this chunk; dx / dg partials of the previous one; dg sum of the one before
+      int rpb;
+      const SChunk* kr = i >= 2 ? &chunks[i - 2] : nullptr;
+      SLF_TRY(launch_rms_step(c, a, *rf, dX, i >= 1 ? &chunks[i - 1] : nullptr, &k, kr,
+                              kr ? rms_blocks(c.dev, kr->rows, &rpb) : 0, i == 2));
+    }
     SLF_TRY(s_chunk_stats(c, a, k, nullptr));
     SLF_TRY(s_chunk_bwd(c, a, k, nullptr, 1, reduction, scale, loss_rows,
                         dX ? reinterpret_cast<uint8_t*>(dX) + (size_t)k.r0 * H * 2 : nullptr, 0, dW,
                         tab[i] >= 0 ? arena.dev(c, tab[i]) : nullptr, tab[i] >= 0 ? arena.tables[tab[i]].second : 0));
+  }
+  if (rf) {  // the last chunk's backward, then the last two dg reductions
+    const size_t n = chunks.size();
+    int rpb;
+    const SChunk* kr = n >= 2 ? &chunks[n - 2] : nullptr;
+    SLF_TRY(launch_rms_step(c, a, *rf, dX, &chunks[n - 1], nullptr, kr, kr ? rms_blocks(c.dev, kr->rows, &rpb) : 0,
+                            n == 2));
+    SLF_TRY(launch_rms_step(c, a, *rf, dX, nullptr, nullptr, &chunks[n - 1], rms_blocks(c.dev, chunks[n - 1].rows, &rpb),
+                            n == 1));
+    return s_end(c, a, reduction, scale, loss_out, dW, rf->rstd, rf->g);
   }
   return s_end(c, a, reduction, scale, loss_out, dW);
 }
@@ -1648,6 +1745,44 @@ slf_status phase_sharded(Ctx& c, const ShardPlan& sp, slf_comm cm, const void* X
     SLF_CUDA(cudaGetLastError());
   }
   return SLF_OK;
+}
+
+// ---- final RMSNorm fused into schedule S (slf_rmsnorm_lce_fwd_bwd) ------------------
+// Workspace: [ schedule-S workspace (planner budget b) | y chunk buffer [max chunk rows][H] bf16 |
+// rstd [N] fp32 | dg partials 2 x [RMS_NB_MAX][H] fp32 ].  With budget 0 the LCE part takes its
+// default 5 % plan and the RMSNorm buffers come on top; otherwise the whole layout fits `budget`.
+struct RmsPlan {
+  Plan p;
+  size_t off_y, off_rstd, off_part0, off_part1, total;
+};
+
+bool rms_layout(int64_t N, int64_t H, int64_t V, size_t b, RmsPlan* rp) {
+  if (!plan_s(N, H, V, b, &rp->p)) return false;
+  int64_t ymax = 0;
+  for (const SChunk& k : s_chunks(rp->p, N, H, true, nullptr)) ymax = std::max(ymax, k.rows);
+  rp->off_y = align_up(rp->p.total, 1024);
+  rp->off_rstd = align_up(rp->off_y + (size_t)ymax * H * 2, 1024);
+  rp->off_part0 = align_up(rp->off_rstd + (size_t)N * 4, 1024);
+  rp->off_part1 = align_up(rp->off_part0 + (size_t)RMS_NB_MAX * H * 4, 1024);
+  rp->total = rp->off_part1 + (size_t)RMS_NB_MAX * H * 4;
+  return true;
+}
+
+bool rms_plan(int64_t N, int64_t H, int64_t V, size_t budget, RmsPlan* out) {
+  if (N < 1 || H < 8 || V < 1) return false;
+  if (budget == 0) return rms_layout(N, H, V, 0, out);
+  RmsPlan rp;
+  if (!rms_layout(N, H, V, budget, &rp)) return false;
+  size_t b = budget;
+  for (int it = 0; it < 8 && rp.total > budget; ++it) {  // shrink the LCE part by the overshoot
+    const size_t over = rp.total - budget;
+    if (over >= b) return false;
+    b -= over;
+    if (!rms_layout(N, H, V, b, &rp)) return false;
+  }
+  if (rp.total > budget) return false;
+  *out = rp;
+  return true;
 }
 
 }  // namespace
@@ -2299,6 +2434,53 @@ slf_status slf_rmsnorm_bwd(const void* x, const void* g, const float* rstd, cons
     rmsnorm_dg_reduce_kernel<<<(unsigned)((H + 255) / 256), 256, 0, s>>>(part, blocks, H, dg);
     SLF_CUDA(cudaGetLastError());
   }
+  return SLF_OK;
+}
+
+size_t slf_rmsnorm_lce_workspace_bytes(int64_t N, int64_t H, int64_t V, size_t budget_bytes) {
+  RmsPlan rp;
+  return rms_plan(N, H, V, budget_bytes, &rp) ? rp.total : 0;
+}
+
+slf_status slf_rmsnorm_lce_fwd_bwd(const void* x, const void* g, float eps, const void* weight, const int32_t* targets,
+                                   int64_t N, int64_t H, int64_t V, int32_t ignore_index, int reduction, float scale,
+                                   float* loss_out, void* dx, float* dg, void* dweight, void* workspace,
+                                   size_t workspace_bytes, size_t budget_bytes, void* stream) {
+  SLF_TRY(check_common(x, weight, targets, N, H, V, workspace));
+  if (!g || !dx || !dg || !dweight || !loss_out) return fail(SLF_ERR_ARG, "null pointer (g, dx, dg, dweight, loss)");
+  if (!aligned16(g) || !aligned16(dx) || !aligned16(dg) || !aligned16(dweight) || !aligned16(loss_out))
+    return fail(SLF_ERR_ALIGN, "pointers must be 16-byte aligned");
+  if (H > 16384) return fail(SLF_ERR_ARG, "H %lld > 16384", (long long)H);
+  if (reduction < SLF_SUM || reduction > SLF_NONE) return fail(SLF_ERR_ARG, "bad reduction %d", reduction);
+  if (!(eps >= 0.f)) return fail(SLF_ERR_ARG, "eps must be >= 0");
+  SLF_TRY(check_outputs(x, weight, N, H, V, dx, dweight, workspace, workspace_bytes));
+  RmsPlan rp;
+  if (!rms_plan(N, H, V, budget_bytes, &rp)) return fail(SLF_ERR_WORKSPACE, "no schedule-S plan fits the budget");
+  if (workspace_bytes < rp.total)
+    return fail(SLF_ERR_WORKSPACE, "workspace %zu bytes < required %zu", workspace_bytes, rp.total);
+  Ctx c;
+  SLF_TRY(device_info(&c.dev));
+  c.plan = rp.p;
+  c.s = reinterpret_cast<cudaStream_t>(stream);
+  c.ws = reinterpret_cast<uint8_t*>(workspace);
+  RmsFuse rf{};
+  rf.g = g;
+  rf.eps = eps;
+  rf.dg = dg;
+  rf.ybuf = c.ws + rp.off_y;
+  rf.rstd = reinterpret_cast<float*>(c.ws + rp.off_rstd);
+  rf.part[0] = reinterpret_cast<float*>(c.ws + rp.off_part0);
+  rf.part[1] = reinterpret_cast<float*>(c.ws + rp.off_part1);
+  rf.nb_max = RMS_NB_MAX;
+  return phase_s(c, x, weight, targets, N, H, V, ignore_index, reduction, scale, loss_out, dx, dweight, &rf);
+}
+
+slf_status slf_rmsnorm_lce_plan_describe(int64_t N, int64_t H, int64_t V, size_t budget_bytes, char* out, size_t cap) {
+  if (!out || cap == 0) return fail(SLF_ERR_ARG, "null output buffer");
+  RmsPlan rp;
+  if (!rms_plan(N, H, V, budget_bytes, &rp)) return fail(SLF_ERR_WORKSPACE, "no plan fits");
+  snprintf(out, cap, "schedule=S rmsnorm_fused row_chunk=%lld n_chunks=%lld lce_workspace=%zu y_chunk_bytes=%zu "
+                     "workspace=%zu", (long long)rp.p.C, (long long)rp.p.nCh, rp.p.total, rp.off_rstd - rp.off_y, rp.total);
   return SLF_OK;
 }
 

@@ -344,25 +344,66 @@ def rmsnorm_fwd(x, g, eps: float = 1e-5):
     return y, rstd
 
 
-def rmsnorm_bwd(x, g, rstd, dy, dx=None):
-    """RMSNorm VJP: (dx bf16 [N, H], dg fp32 [H]).  dx may be dy (in place)."""
+def rmsnorm_workspace_bytes(N: int, H: int) -> int:
+    return int(lib().slf_rmsnorm_workspace_bytes(N, H))
+
+
+def rmsnorm_bwd(x, g, rstd, dy, dx=None, workspace=None, dg=None):
+    """RMSNorm VJP: (dx bf16 [N, H], dg fp32 [H]).  dx may be dy (in place).  `workspace` (uint8,
+    >= rmsnorm_workspace_bytes(N, H)) avoids an allocation per call."""
     x = x.contiguous()
     N, H = x.shape
     dx = dx if dx is not None else torch.empty_like(x)
-    dg = torch.empty(H, dtype=torch.float32, device=x.device)
-    ws = torch.empty(int(lib().slf_rmsnorm_workspace_bytes(N, H)), dtype=torch.uint8, device=x.device)
+    dg = dg if dg is not None else torch.empty(H, dtype=torch.float32, device=x.device)
+    ws = workspace if workspace is not None else torch.empty(rmsnorm_workspace_bytes(N, H), dtype=torch.uint8,
+                                                            device=x.device)
     check(lib().slf_rmsnorm_bwd(x.data_ptr(), g.contiguous().data_ptr(), rstd.data_ptr(), dy.data_ptr(), N, H,
                                 dx.data_ptr(), dg.data_ptr(), ws.data_ptr(), ws.numel(), _stream_ptr(x.device)),
           "slf_rmsnorm_bwd")
     return dx, dg
 
 
+def rmsnorm_lce_workspace_bytes(N: int, H: int, V: int, budget_bytes: int = 0) -> int:
+    return int(lib().slf_rmsnorm_lce_workspace_bytes(N, H, V, budget_bytes))
+
+
+def rmsnorm_lce_plan_describe(N: int, H: int, V: int, budget_bytes: int = 0) -> str:
+    buf = ctypes.create_string_buffer(512)
+    check(lib().slf_rmsnorm_lce_plan_describe(N, H, V, budget_bytes, buf, 512), "slf_rmsnorm_lce_plan_describe")
+    return buf.value.decode()
+
+
 def rmsnorm_lce_fwd_bwd(x, g, weight, targets, eps: float = 1e-5, ignore_index: int = -100,
                         reduction: str = "mean", scale: float = 1.0, budget_bytes: int = 0, workspace=None,
-                        schedule: str = "auto"):
+                        schedule: str = "auto", fused: bool = True, out=None):
     """Final RMSNorm + fused LCE, forward and backward: (loss, dx (pre-norm), dg fp32, dW).
 
-    y = RMSNorm(x; g) feeds the LM head; the LCE's dhidden is fed through the RMSNorm VJP in place."""
+    fused (default; schedule auto/S): one library call, slf_rmsnorm_lce_fwd_bwd — y only ever exists
+    for one row chunk.  fused=False or schedule R: the composition rmsnorm_fwd -> lce_fwd_bwd ->
+    rmsnorm_bwd (y [N, H] materialised; the LCE's dhidden fed through the VJP in place)."""
+    if fused and schedule in ("auto", "S"):
+        x, weight, targets = _prep(x, weight, targets)
+        N, H = x.shape
+        V = weight.shape[0]
+        dev = x.device
+        if out is not None:
+            loss, dx, dg, dW = out
+        else:
+            loss = torch.empty(N if reduction == "none" else 1, dtype=torch.float32, device=dev)
+            dx = torch.empty_like(x)
+            dg = torch.empty(H, dtype=torch.float32, device=dev)
+            dW = torch.empty_like(weight)
+        if workspace is None:
+            nb = rmsnorm_lce_workspace_bytes(N, H, V, budget_bytes)
+            if nb == 0:
+                raise RuntimeError(f"no fused RMSNorm+LCE plan fits N={N} H={H} V={V} budget={budget_bytes}")
+            workspace = torch.empty(nb, dtype=torch.uint8, device=dev)
+        check(lib().slf_rmsnorm_lce_fwd_bwd(x.data_ptr(), g.contiguous().data_ptr(), float(eps), weight.data_ptr(),
+                                            targets.data_ptr(), N, H, V, ignore_index, REDUCTIONS[reduction],
+                                            float(scale), loss.data_ptr(), dx.data_ptr(), dg.data_ptr(),
+                                            dW.data_ptr(), workspace.data_ptr(), workspace.numel(), budget_bytes,
+                                            _stream_ptr(dev)), "slf_rmsnorm_lce_fwd_bwd")
+        return (loss if reduction == "none" else loss[0]), dx, dg, dW
     y, rstd = rmsnorm_fwd(x, g, eps)
     loss, dy, dW = lce_fwd_bwd(y, weight, targets, ignore_index, reduction, scale, budget_bytes=budget_bytes,
                                workspace=workspace, schedule=schedule)

@@ -435,15 +435,21 @@ def test_host_input_double_buffered_staging(slf):
 
 
 # ---- final RMSNorm + LCE ---------------------------------------------------
-@pytest.mark.parametrize("sched", SCHEDS)
-@pytest.mark.parametrize("N,H,V", [(300, 256, 3000), (1000, 520, 4100)])
-def test_rmsnorm_lce_parity(slf, sched, N, H, V):
+@pytest.mark.parametrize("sched,fused", [("R", False), ("S", False), ("S", True)])
+@pytest.mark.parametrize("N,H,V,budget", [(300, 256, 3000, 0), (1000, 520, 4100, 0), (2000, 512, 1536, 3 << 20)])
+def test_rmsnorm_lce_parity(slf, sched, fused, N, H, V, budget):
+    """Final RMSNorm + LCE against oracle.rmsnorm_lce: the composition (R / S) and the fused call
+    (slf_rmsnorm_lce_fwd_bwd; with a small budget: several extended chunks, so the per-chunk y
+    buffer, the in-place dy -> dx and the chunk-ordered dg sum all run)."""
     inp = synth.make_inputs(N, H, V, seed=16, alpha=3.0, dist="zipf")
     x, W, t = to_dev(inp, torch)
     rng = np.random.default_rng(5)
     g_np = synth.f32_to_bf16_bits((1 + 0.2 * rng.standard_normal(H)).astype(np.float32))
     g = torch.from_numpy(g_np.view(np.int16)).view(torch.bfloat16).cuda()
-    loss, dx, dg, dW = slf.rmsnorm_lce_fwd_bwd(x, g, W, t, eps=1e-5, reduction="mean", schedule=sched)
+    if fused and budget:
+        assert "n_chunks=1 " not in slf.rmsnorm_lce_plan_describe(N, H, V, budget)
+    loss, dx, dg, dW = slf.rmsnorm_lce_fwd_bwd(x, g, W, t, eps=1e-5, reduction="mean", schedule=sched, fused=fused,
+                                               budget_bytes=budget)
     torch.cuda.synchronize()
     xo, Wo, to = oracle_inputs(inp)
     ref_loss, ref_dx, ref_dg, ref_dW = oracle.rmsnorm_lce(xo, synth.bf16_bits_to_f64(g_np), Wo, to, eps=1e-5,
@@ -452,6 +458,49 @@ def test_rmsnorm_lce_parity(slf, sched, N, H, V):
     assert rel_max_err(bf16_to_np64(dx), ref_dx) <= GRAD_TOL
     assert rel_max_err(dg.cpu().numpy(), ref_dg) <= GRAD_TOL
     assert rel_max_err(bf16_to_np64(dW), ref_dW) <= GRAD_TOL
+    assert np.all(dx.view(torch.int16).cpu().numpy()[inp.t == -100] == 0)
+
+
+@pytest.mark.parametrize("red", ["mean", "none"])
+def test_rmsnorm_lce_fused_matches_composition(slf, red):
+    """The fused call forms exactly the composition's y (same fp32 ops, same bf16 rounding) and runs
+    the same plan: loss, dx and dW are bit-identical to rmsnorm_fwd -> lce_fwd_bwd -> rmsnorm_bwd;
+    dg differs only in the grouping of its fp32 row sums."""
+    inp = synth.make_inputs(3000, 512, 2000, seed=27, alpha=3.0, dist="zipf")
+    x, W, t = to_dev(inp, torch)
+    g = (1 + 0.1 * torch.randn(512, generator=torch.Generator().manual_seed(1))).to(torch.bfloat16).cuda()
+    a = slf.rmsnorm_lce_fwd_bwd(x, g, W, t, reduction=red, schedule="S", fused=True)
+    b = slf.rmsnorm_lce_fwd_bwd(x, g, W, t, reduction=red, schedule="S", fused=False)
+    torch.cuda.synchronize()
+    assert torch.equal(a[0].view(-1), b[0].view(-1))
+    assert torch.equal(a[1].view(torch.int16), b[1].view(torch.int16))
+    assert torch.equal(a[3].view(torch.int16), b[3].view(torch.int16))
+    assert rel_max_err(a[2].cpu().numpy(), b[2].cpu().numpy()) < 1e-5
+
+
+@pytest.mark.slow
+def test_rmsnorm_lce_fused_llama_reduced_n(slf):
+    """Fused RMSNorm + LCE at the Llama-3.1-8B head (H=4096, V=128256), N=1024, a budget forcing
+    several chunks: every element of loss, dx, dg, dW against oracle.rmsnorm_lce."""
+    N, H, V = 1024, 4096, 128256
+    budget = 90 << 20
+    desc = slf.rmsnorm_lce_plan_describe(N, H, V, budget)
+    assert "n_chunks=1 " not in desc, desc
+    inp = synth.make_config("llama8b", seed=28, alpha=4.0, dist="zipf", N=N)
+    x, W, t = to_dev(inp, torch)
+    rng = np.random.default_rng(6)
+    g_np = synth.f32_to_bf16_bits((1 + 0.2 * rng.standard_normal(H)).astype(np.float32))
+    g = torch.from_numpy(g_np.view(np.int16)).view(torch.bfloat16).cuda()
+    loss, dx, dg, dW = slf.rmsnorm_lce_fwd_bwd(x, g, W, t, reduction="mean", budget_bytes=budget)
+    torch.cuda.synchronize()
+    xo, Wo, to = oracle_inputs(inp)
+    ref_loss, ref_dx, ref_dg, ref_dW = oracle.rmsnorm_lce(xo, synth.bf16_bits_to_f64(g_np), Wo, to, eps=1e-5,
+                                                          reduction="mean")
+    assert_loss_close(float(loss), ref_loss, "mean")
+    assert rel_max_err(bf16_to_np64(dx), ref_dx) <= GRAD_TOL
+    assert rel_max_err(dg.cpu().numpy(), ref_dg) <= GRAD_TOL
+    assert rel_max_err(bf16_to_np64(dW), ref_dW) <= GRAD_TOL
+    print(f"fused rmsnorm+lce llama8b N={N} [{desc}]")
 
 
 # ---- gradient accumulation and the fused autograd function (SURVEY §8(f) NEXT-2) ----------------
