@@ -352,6 +352,15 @@ slf_status slf_debug_trace_read(uint64_t* host, int64_t n);
 /* p[i] = bf16(p[i] * s) for a DEVICE bf16 array of n elements (n % 8 == 0, 16-byte aligned):
  * applies an autograd grad_output to gradients formed during the forward (LCEFunctionFused). */
 slf_status slf_scale_bf16(void* p, int64_t n, float s, void* stream);
+/* The same with the factor in DEVICE memory (s_dev[0], fp32): no host read of an autograd
+ * grad_output; a no-op pass when it is exactly 1. */
+slf_status slf_scale_bf16_dev(void* p, int64_t n, const float* s_dev, void* stream);
+/* RowStat out[i] = in[i] with coef multiplied by grad[0] (per_row = 0: SUM / MEAN grad_output) or
+ * grad[i] (per_row = 1: reduction NONE, one upstream gradient per row); DEVICE pointers, N rows,
+ * in / out may alias.  slf_lce_bwd on `out` with grad_scale = 1 then yields the gradients of
+ * sum_i grad_i * loss_i: the autograd backward without a host synchronisation (LCEFunction). */
+slf_status slf_rowstat_scale(const slf_rowstat* in, const float* grad, int per_row, int64_t N, slf_rowstat* out,
+                             void* stream);
 
 /* Debug: number of clusters of `cluster` CTAs of the GEMM kernel that can be co-resident (HOST
  * *out), from cudaOccupancyMaxActiveClusters with the kernel's shared-memory footprint. */

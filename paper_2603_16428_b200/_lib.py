@@ -30,6 +30,7 @@ EXPORTS = ["slf_lce_version", "slf_last_error_string", "slf_lce_workspace_bytes"
            "slf_lce_sharded_plan_describe", "slf_lce_fwd_bwd_sharded", "slf_comm_set_p2p", "slf_comm_status",
            "slf_lce_fwd_bwd_dp", "slf_target_csr_scratch_bytes", "slf_target_csr",
            "slf_rmsnorm_lce_workspace_bytes", "slf_rmsnorm_lce_plan_describe", "slf_rmsnorm_lce_fwd_bwd",
+           "slf_scale_bf16_dev", "slf_rowstat_scale",
            # include/slf_adam.h (Layer-Adam, host)
            "slf_adam_last_error_string", "slf_adam_simd_width", "slf_adam_create", "slf_adam_destroy",
            "slf_adam_set_config", "slf_adam_set_params", "slf_adam_get_state", "slf_adam_step_host",
@@ -74,6 +75,8 @@ def _declare(lib):
         "slf_lce_dx_finalize": (INT, [P, P, P, I64, I64, P]),
         "slf_target_csr_scratch_bytes": (SZ, [I64, I64]),
         "slf_target_csr": (INT, [P, I64, I32, I64, I64, P, P, P, SZ, P]),
+        "slf_scale_bf16_dev": (INT, [P, I64, P, P]),
+        "slf_rowstat_scale": (INT, [P, P, INT, I64, P, P]),
         "slf_rmsnorm_lce_workspace_bytes": (SZ, [I64, I64, I64, SZ]),
         "slf_rmsnorm_lce_plan_describe": (INT, [I64, I64, I64, SZ, ctypes.c_char_p, SZ]),
         "slf_rmsnorm_lce_fwd_bwd": (INT, [P, P, F32, P, P, I64, I64, I64, I32, INT, F32, P, P, P, P, P, SZ, SZ, P]),

@@ -24,6 +24,8 @@ __device__ __forceinline__ float block_sum_256(float v, float* red) {
   return t;
 }
 
+__device__ __forceinline__ float bf16_bits_to_f32(uint16_t v) { return __uint_as_float((uint32_t)v << 16); }
+
 __device__ __forceinline__ void unpack8(const uint4 q, float (&f)[8]) {
   f[0] = bf16lo_to_f32(q.x); f[1] = bf16hi_to_f32(q.x);
   f[2] = bf16lo_to_f32(q.y); f[3] = bf16hi_to_f32(q.y);
@@ -118,84 +120,92 @@ __global__ void __launch_bounds__(256) rmsnorm_dg_reduce_kernel(const float* __r
 }
 
 // ---- final RMSNorm fused into the schedule-S chunk loop (slf_rmsnorm_lce_fwd_bwd) ----
-// One launch between chunk k-1's grouped dX/dW GEMMs and chunk k's stash GEMM does three disjoint
-// jobs, by block index:
-//   [0, nb_bwd)                    backward of chunk k-1's rows: dy (bf16, the group's dX output in
-//                                  the caller's dx rows) -> dx in place, and this block's fp32 dg
-//                                  partial over its rows -> part_b[block][H]
-//   [nb_bwd, nb_bwd + f_rows)      forward of chunk k's rows: y = bf16(x * rstd * g) into the chunk
-//                                  buffer ybuf (the GEMMs' A / B operand), rstd kept for the backward
-//   [.., + nb_red)                 dg += sum_b part_r[b][:] for chunk k-2 (its partials complete:
-//                                  an earlier launch), 256 columns per block, block order
-// y never exists for all N rows: only the chunk's rows, which stay in L2 between the kernels that
-// read them.  Launched with programmatic dependent launch; every block waits for the previous grid.
+// The RMSNorm work of the chunk loop rides in the blocks of launches the loop makes anyway (chunk
+// k's combine_transform, which waits for chunk k's stash GEMM and hence for chunk k-1's grouped
+// GEMMs), so the fusion adds no kernel boundary per chunk.  Jobs, by block range after the host
+// launch's own blocks:
+//   dx   chunk k-2: dx = rstd * (g*dy - xhat * mean(xhat*g*dy)) in place over dy (the group's bf16
+//        dX output in the caller's dx rows; its dg partial was taken one launch earlier)   1 row / block
+//   dgp  chunk k-1: part[rowgroup][col] = sum over the group's RMS_RG rows of dy * xhat, in row
+//        order                                                       (row group x 256 columns) / block
+//   fwd  chunk k+1: y = bf16(x * rstd * g) into its chunk buffer (double-buffered by parity), rstd  1 row / block
+//   red  chunk k-2: dg (+)= sum over its row groups of part, in row-group order    256 columns / block
+// Every job reads only what an earlier, completed launch wrote; y never exists for all N rows.
+constexpr int RMS_RG = 32;  // rows per dg partial
+
 struct RmsStep {
   const uint16_t* x;
   const uint16_t* g;
   int64_t H;
   float eps;
-  float* rstd;  // [N]
-  // backward part
-  int64_t b_r0, b_rows;
-  int b_rpb, nb_bwd;
-  uint16_t* dx;  // [N][H]: dy in, dx out (row-owned, in place)
-  float* part_b;
-  // forward part
-  int64_t f_r0, f_rows;
-  uint16_t* ybuf;  // [f_rows][H]
-  // dg reduction part
-  int nb_red, red_nblk, red_first;
+  float* rstd;    // [N]
+  uint16_t* dx;   // [N][H]: dy in, dx out (row-owned, in place)
+  int64_t x_r0, x_rows;     // dx job rows
+  int64_t p_r0, p_rows;     // dg-partial job rows
+  float* part_w;            // [ceil(p_rows / RMS_RG)][H]
+  int64_t f_r0, f_rows;     // fwd job rows
+  uint16_t* ybuf;           // [f_rows][H]
+  int red_ngroups, red_first;  // red job: row groups to sum (0: none)
   const float* part_r;
   float* dg;
 };
 
-__global__ void __launch_bounds__(RMS_THREADS) rms_step_kernel(RmsStep a) {
-  griddep_wait();
+__host__ __device__ inline int rms_nslab(int64_t H) { return (int)((H + 255) / 256); }
+__host__ __device__ inline int64_t rms_blocks_of(const RmsStep& a) {
+  const int slabs = rms_nslab(a.H);
+  return a.x_rows + ((a.p_rows + RMS_RG - 1) / RMS_RG) * slabs + a.f_rows + (a.red_ngroups ? slabs : 0);
+}
+
+__device__ __forceinline__ void rms_block(const RmsStep& a, int64_t b) {
   __shared__ float red[RMS_THREADS / 32];
-  extern __shared__ float dg_acc[];
   const int64_t groups = a.H / 8;
   const uint4* gr = reinterpret_cast<const uint4*>(a.g);
-  int b = blockIdx.x;
-  if (b < a.nb_bwd) {  // backward rows [b_r0 + b*rpb, ...)
-    for (int64_t j = threadIdx.x; j < a.H; j += RMS_THREADS) dg_acc[j] = 0.f;
-    __syncthreads();
-    const int64_t r0 = a.b_r0 + (int64_t)b * a.b_rpb, r1 = min(r0 + a.b_rpb, a.b_r0 + a.b_rows);
-    for (int64_t row = r0; row < r1; ++row) {
-      const float r = a.rstd[row];
-      const uint4* xr = reinterpret_cast<const uint4*>(a.x + row * a.H);
-      const uint4* dr = reinterpret_cast<const uint4*>(a.dx + row * a.H);
-      float dot = 0.f;
-      for (int64_t q = threadIdx.x; q < groups; q += RMS_THREADS) {
-        float f[8], w[8], d[8];
-        unpack8(xr[q], f);
-        unpack8(gr[q], w);
-        unpack8(dr[q], d);
+  const int slabs = rms_nslab(a.H);
+  if (b < a.x_rows) {  // dx of one row, in place
+    const int64_t row = a.x_r0 + b;
+    const float r = a.rstd[row];
+    const uint4* xr = reinterpret_cast<const uint4*>(a.x + row * a.H);
+    uint4* dr = reinterpret_cast<uint4*>(a.dx + row * a.H);
+    float dot = 0.f;
+    for (int64_t q = threadIdx.x; q < groups; q += RMS_THREADS) {
+      float f[8], w[8], d[8];
+      unpack8(xr[q], f);
+      unpack8(gr[q], w);
+      unpack8(dr[q], d);
 #pragma unroll
-        for (int e = 0; e < 8; ++e) {
-          const float xh = f[e] * r;
-          dot = fmaf(xh, w[e] * d[e], dot);
-          dg_acc[q * 8 + e] += d[e] * xh;
-        }
-      }
-      const float c = block_sum_256(dot, red) / (float)a.H;
-      uint4* xo = reinterpret_cast<uint4*>(a.dx + row * a.H);
-      for (int64_t q = threadIdx.x; q < groups; q += RMS_THREADS) {
-        float f[8], w[8], d[8], o[8];
-        unpack8(xr[q], f);
-        unpack8(gr[q], w);
-        unpack8(dr[q], d);
-#pragma unroll
-        for (int e = 0; e < 8; ++e) o[e] = r * (w[e] * d[e] - f[e] * r * c);
-        xo[q] = make_uint4(pack_bf16x2(o[0], o[1]), pack_bf16x2(o[2], o[3]), pack_bf16x2(o[4], o[5]),
-                           pack_bf16x2(o[6], o[7]));
-      }
+      for (int e = 0; e < 8; ++e) dot = fmaf(f[e] * r, w[e] * d[e], dot);
     }
-    __syncthreads();
-    for (int64_t j = threadIdx.x; j < a.H; j += RMS_THREADS) a.part_b[(size_t)b * a.H + j] = dg_acc[j];
+    const float c = block_sum_256(dot, red) / (float)a.H;
+    for (int64_t q = threadIdx.x; q < groups; q += RMS_THREADS) {
+      float f[8], w[8], d[8], o[8];
+      unpack8(xr[q], f);
+      unpack8(gr[q], w);
+      unpack8(dr[q], d);
+#pragma unroll
+      for (int e = 0; e < 8; ++e) o[e] = r * (w[e] * d[e] - f[e] * r * c);
+      dr[q] = make_uint4(pack_bf16x2(o[0], o[1]), pack_bf16x2(o[2], o[3]), pack_bf16x2(o[4], o[5]),
+                         pack_bf16x2(o[6], o[7]));
+    }
     return;
   }
-  b -= a.nb_bwd;
-  if (b < a.f_rows) {  // forward row f_r0 + b
+  b -= a.x_rows;
+  const int64_t npb = ((a.p_rows + RMS_RG - 1) / RMS_RG) * slabs;
+  if (b < npb) {  // dg partial: one row group x 256 columns, thread = column, rows in order
+    const int64_t grp = b / slabs;
+    const int64_t col = (b % slabs) * 256 + threadIdx.x;
+    if (col >= a.H) return;
+    const int64_t r0 = a.p_r0 + grp * RMS_RG, r1 = min(r0 + RMS_RG, a.p_r0 + a.p_rows);
+    float acc = 0.f;
+#pragma unroll 8
+    for (int64_t row = r0; row < r1; ++row) {
+      const float xv = bf16_bits_to_f32(a.x[row * a.H + col]) * a.rstd[row];
+      acc += bf16_bits_to_f32(a.dx[row * a.H + col]) * xv;
+    }
+    a.part_w[grp * a.H + col] = acc;
+    return;
+  }
+  b -= npb;
+  if (b < a.f_rows) {  // forward of one row
     const int64_t row = a.f_r0 + b;
     const uint4* xr = reinterpret_cast<const uint4*>(a.x + row * a.H);
     float ss = 0.f;
@@ -207,7 +217,7 @@ __global__ void __launch_bounds__(RMS_THREADS) rms_step_kernel(RmsStep a) {
     }
     const float r = rsqrtf(block_sum_256(ss, red) / (float)a.H + a.eps);
     if (threadIdx.x == 0) a.rstd[row] = r;
-    uint4* yr = reinterpret_cast<uint4*>(a.ybuf + (int64_t)b * a.H);
+    uint4* yr = reinterpret_cast<uint4*>(a.ybuf + b * a.H);
     for (int64_t q = threadIdx.x; q < groups; q += RMS_THREADS) {
       float f[8], w[8];
       unpack8(xr[q], f);
@@ -217,12 +227,19 @@ __global__ void __launch_bounds__(RMS_THREADS) rms_step_kernel(RmsStep a) {
     }
     return;
   }
-  b -= (int)a.f_rows;
-  const int64_t j = (int64_t)b * RMS_THREADS + threadIdx.x;  // dg reduction: column j
-  if (j >= a.H) return;
+  b -= a.f_rows;
+  const int64_t col = b * 256 + threadIdx.x;  // dg reduction of one 256-column slab
+  if (col >= a.H) return;
   float sum = 0.f;
-  for (int k = 0; k < a.red_nblk; ++k) sum += a.part_r[(size_t)k * a.H + j];
-  a.dg[j] = a.red_first ? sum : a.dg[j] + sum;
+  for (int k = 0; k < a.red_ngroups; ++k) sum += a.part_r[(size_t)k * a.H + col];
+  a.dg[col] = a.red_first ? sum : a.dg[col] + sum;
+}
+
+// Standalone form (the loop's first forward and its tail), programmatic dependent launch.
+__global__ void __launch_bounds__(RMS_THREADS) rms_step_kernel(RmsStep a) {
+  griddep_launch_dependents();
+  griddep_wait();
+  rms_block(a, blockIdx.x);
 }
 
 // p[i] = bf16(p[i] * s), 8 elements per thread-iteration.
@@ -233,6 +250,32 @@ __global__ void __launch_bounds__(256) scale_bf16_kernel(uint4* __restrict__ p, 
     p[q] = make_uint4(pack_bf16x2(f[0] * s, f[1] * s), pack_bf16x2(f[2] * s, f[3] * s), pack_bf16x2(f[4] * s, f[5] * s),
                       pack_bf16x2(f[6] * s, f[7] * s));
   }
+}
+
+// p[i] = bf16(p[i] * s[0]) with the factor on the device (an autograd grad_output, no host read);
+// every block returns at once when it is exactly 1 (the common loss.backward()).
+__global__ void __launch_bounds__(256) scale_bf16_dev_kernel(uint4* __restrict__ p, int64_t groups,
+                                                            const float* __restrict__ s_dev) {
+  const float s = *s_dev;
+  if (s == 1.0f) return;
+  for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < groups; q += (int64_t)gridDim.x * blockDim.x) {
+    float f[8];
+    unpack8(p[q], f);
+    p[q] = make_uint4(pack_bf16x2(f[0] * s, f[1] * s), pack_bf16x2(f[2] * s, f[3] * s), pack_bf16x2(f[4] * s, f[5] * s),
+                      pack_bf16x2(f[6] * s, f[7] * s));
+  }
+}
+
+// RowStat out[i] = in[i] with coef *= grad[per_row ? i : 0]: the upstream gradient of the loss
+// (scalar for SUM/MEAN, per row for NONE) folded into the backward's per-row coefficient, on the
+// device.  in / out: 16-byte records {lse2, coef, tloc, valid}.
+__global__ void __launch_bounds__(256) rowstat_scale_kernel(const float4* __restrict__ in, const float* __restrict__ grad,
+                                                           int per_row, int64_t N, float4* __restrict__ out) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= N) return;
+  float4 r = in[i];
+  r.y *= per_row ? grad[i] : grad[0];
+  out[i] = r;
 }
 
 }  // namespace slf

@@ -14,6 +14,7 @@
 #include "../../include/slf_lce.h"
 #include "aux_kernels.cuh"
 #include "ptx.cuh"
+#include "rmsnorm.cuh"
 
 namespace slf {
 
@@ -67,11 +68,15 @@ __global__ void __launch_bounds__(256) combine_transform_kernel(
     const float* __restrict__ zt, const int32_t* __restrict__ t, int64_t vocab_start, int64_t V_l, int64_t V_global,
     int64_t ld_stash, int32_t ignore_index, int reduction, float scale, float grad_scale,
     const WsHeader* __restrict__ hdr, float* __restrict__ loss_rows, slf_rowstat* __restrict__ rowstat,
-    uint16_t* __restrict__ stash, uint16_t* __restrict__ stash2, int split) {
+    uint16_t* __restrict__ stash, uint16_t* __restrict__ stash2, int split, RmsStep rms) {
   // rows [0, split) of the chunk's stash are in `stash`, rows [split, rows) in `stash2` (same stride)
   extern __shared__ float r_t[];  // [tiles]: first the tile maxima m_t, then the factors r_t
   griddep_launch_dependents();
   griddep_wait();  // PDL: everything below reads the previous kernel's outputs
+  if ((int)blockIdx.x >= rows) {  // the fused final RMSNorm's jobs riding in this launch (rmsnorm.cuh)
+    rms_block(rms, (int64_t)blockIdx.x - rows);
+    return;
+  }
   __shared__ float sM, sLse, wm[8], ws[8];
   const int i = blockIdx.x;
   const int tid = threadIdx.x;

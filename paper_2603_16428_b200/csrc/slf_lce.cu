@@ -19,8 +19,8 @@
 #include "../../include/slf_lce.h"
 #include "aux_kernels.cuh"
 #include "gemm.cuh"
-#include "s_kernels.cuh"
 #include "rmsnorm.cuh"
+#include "s_kernels.cuh"
 #include "comm.cuh"
 
 using namespace slf;
@@ -598,6 +598,23 @@ std::vector<int> lpt_table_cached(const ProbSpec* ps, int n, int units, int* str
   return it->second.first;  // a copy, taken under the lock
 }
 
+// Pinned copies of tile tables referenced by captured CUDA graphs (content-keyed, never freed).
+const uint8_t* captured_table(const std::vector<int>& host, size_t bytes) {
+  static std::vector<std::pair<std::vector<int>, uint8_t*>> pool;
+  for (auto& e : pool)
+    if (e.first == host) return e.second;
+  uint8_t* p = nullptr;
+  // the allocation is not a stream operation: relaxed capture mode for this thread while it runs
+  cudaStreamCaptureMode mode = cudaStreamCaptureModeRelaxed;
+  cudaThreadExchangeStreamCaptureMode(&mode);
+  const cudaError_t e = cudaHostAlloc(reinterpret_cast<void**>(&p), bytes, cudaHostAllocDefault);
+  cudaThreadExchangeStreamCaptureMode(&mode);
+  if (e != cudaSuccess) return nullptr;
+  memcpy(p, host.data(), bytes);
+  pool.emplace_back(host, p);
+  return p;
+}
+
 struct SchedArena {
   std::vector<int> host;
   std::vector<std::pair<size_t, int>> tables;  // (offset in ints, stride)
@@ -614,6 +631,18 @@ struct SchedArena {
     if (!fits(c)) return fail(SLF_ERR_WORKSPACE, "tile schedule arena overflow");
     const size_t bytes = host.size() * 4;
     std::lock_guard<std::mutex> lk(g_mu);
+    cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+    SLF_CUDA(cudaStreamIsCapturing(c.s, &cap));
+    if (cap == cudaStreamCaptureStatusActive) {
+      // CUDA-graph capture: the copy becomes a graph node that reads its host source at every
+      // replay, so the source must outlive the graph and never change — a pinned buffer per
+      // distinct table content, kept for the life of the process (no events: a capture cannot
+      // wait on the ring's).
+      const uint8_t* src = captured_table(host, bytes);
+      if (!src) return fail(SLF_ERR_CUDA, "cannot allocate pinned memory for a captured tile table");
+      SLF_CUDA(cudaMemcpyAsync(c.ws + c.plan.off_sched, src, bytes, cudaMemcpyHostToDevice, c.s));
+      return SLF_OK;
+    }
     PinnedRing& r = c.dev->ring;
     if (!r.buf) {
       SLF_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&r.buf), (size_t)RING_SLOTS * SCHED_ARENA_MAX,
@@ -1024,7 +1053,7 @@ slf_status s_build_bwd(Ctx& c, const SArgs& a, const SChunk& k, void* dXc, int d
 // summed across shards).  `sched` (optional) is a prebuilt LPT table for this chunk shape.
 slf_status s_chunk_bwd(Ctx& c, const SArgs& a, const SChunk& k, const slf_shardstat* st, int g, int reduction,
                        float scale, float* loss_rows_all, void* dXc, int dx_fp32, void* dW, const int* sched = nullptr,
-                       int sched_stride = 0) {
+                       int sched_stride = 0, const RmsStep* rms = nullptr) {
   const Plan& p = c.plan;
   const int64_t r0 = k.r0, rows = k.rows;
   const int tiles_v = (int)((a.V_l + BN - 1) / BN);
@@ -1033,7 +1062,7 @@ slf_status s_chunk_bwd(Ctx& c, const SArgs& a, const SChunk& k, const slf_shards
     ProfScope ps(SLF_PROF_COMBINE_TRANSFORM, c.s, 0.0, (double)rows * (tiles_v * 8.0 + a.V_l * 4.0 + 16.0 * g + 24));
     // Programmatic dependent launch: blocks start while the stash GEMM drains and wait in-kernel.
     cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3((unsigned)rows);
+    cfg.gridDim = dim3((unsigned)(rows + (rms ? rms_blocks_of(*rms) : 0)));
     cfg.blockDim = dim3(256);
     cfg.dynamicSmemBytes = tiles_v * sizeof(float);
     cfg.stream = c.s;
@@ -1047,7 +1076,7 @@ slf_status s_chunk_bwd(Ctx& c, const SArgs& a, const SChunk& k, const slf_shards
         reinterpret_cast<const float*>(c.ws + p.off_zt) + r0, a.t + r0, a.vs, a.V_l, a.Vg, p.ld_stash, a.ign,
         reduction, scale, 1.0f, (const WsHeader*)hdr_of(c.ws), loss_rows_all + r0,
         reinterpret_cast<slf_rowstat*>(c.ws + p.off_rowstat) + r0, reinterpret_cast<uint16_t*>(c.ws + p.off_stash),
-        reinterpret_cast<uint16_t*>(k.ext_base), (int)(rows - k.ext)));
+        reinterpret_cast<uint16_t*>(k.ext_base), (int)(rows - k.ext), rms ? *rms : RmsStep{}));
   }
   if (!dXc && !dW) return SLF_OK;
   ProbSpec ps[2];
@@ -1150,30 +1179,24 @@ std::vector<SChunk> s_chunks(const Plan& p, int64_t N, int64_t H, bool extend, u
 // is requested, the chunks are extended into dhidden's not-yet-written rows (s_chunks): fewer
 // chunks, fewer dW accumulation passes and longer dW K, at no extra memory.
 // The final RMSNorm fused into the chunk loop (slf_rmsnorm_lce_fwd_bwd): X is the
-// RMSNorm input x; each chunk's y rows are formed into `ybuf` right before its stash GEMM and the
-// chunk's dx / dg right after its grouped GEMMs (rms_step_kernel, one launch per chunk boundary).
+// RMSNorm input x; chunk k's y rows live in ybuf[k & 1].  The RMSNorm jobs of a chunk boundary ride
+// in chunk k's combine_transform launch (rmsnorm.cuh RmsStep): dx of chunk k-2, dg partials of
+// chunk k-1, y of chunk k+1, the dg sum of chunk k-2; one launch before the loop (y of chunk 0)
+// and two after it.
 struct RmsFuse {
   const void* g;
   float eps;
-  float* dg;        // caller's fp32 [H]
-  uint8_t* ybuf;    // [max chunk rows][H] bf16
-  float* rstd;      // [N]
-  float* part[2];   // [nb_max][H] fp32 dg partials, double-buffered by chunk parity
-  int nb_max;
+  float* dg;          // caller's fp32 [H]
+  uint8_t* ybuf[2];   // [max chunk rows][H] bf16, by chunk parity
+  float* rstd;        // [N]
+  float* part[2];     // [max row groups][H] fp32 dg partials, by chunk parity
 };
 
-constexpr int RMS_NB_MAX = 148;  // backward blocks per chunk (one per B200 SM); sizes the dg partials
-
-int rms_blocks(const DevInfo* dev, int64_t rows, int* rpb) {
-  const int64_t nb = std::max<int64_t>(1, std::min<int64_t>(rows, std::min(dev->sms, RMS_NB_MAX)));
-  *rpb = (int)((rows + nb - 1) / nb);
-  return (int)((rows + *rpb - 1) / *rpb);
-}
-
-// One rms_step launch: backward of chunk `kb` (or none), forward of chunk `kf` (or none), dg
-// reduction of chunk `kr` (or none).
-slf_status launch_rms_step(Ctx& c, const SArgs& a, const RmsFuse& rf, void* dX, const SChunk* kb, const SChunk* kf,
-                           const SChunk* kr, int nb_kr, bool red_first) {
+// The RMSNorm jobs of one launch, for chunks (by index; -1 = none): dx of cx, dg partials of cp,
+// y of cf, dg sum of cr.
+RmsStep rms_jobs(const SArgs& a, const RmsFuse& rf, void* dX, const std::vector<SChunk>& ch, int64_t cx, int64_t cp,
+                 int64_t cf, int64_t cr) {
+  const int64_t n = (int64_t)ch.size();
   RmsStep r{};
   r.x = reinterpret_cast<const uint16_t*>(a.X);
   r.g = reinterpret_cast<const uint16_t*>(rf.g);
@@ -1181,35 +1204,37 @@ slf_status launch_rms_step(Ctx& c, const SArgs& a, const RmsFuse& rf, void* dX, 
   r.eps = rf.eps;
   r.rstd = rf.rstd;
   r.dx = reinterpret_cast<uint16_t*>(dX);
-  if (kb) {
-    r.b_r0 = kb->r0;
-    r.b_rows = kb->rows;
-    r.nb_bwd = rms_blocks(c.dev, kb->rows, &r.b_rpb);
-    r.part_b = rf.part[kb->index & 1];
+  if (cx >= 0 && cx < n) {
+    r.x_r0 = ch[cx].r0;
+    r.x_rows = ch[cx].rows;
   }
-  if (kf) {
-    r.f_r0 = kf->r0;
-    r.f_rows = kf->rows;
-    r.ybuf = reinterpret_cast<uint16_t*>(rf.ybuf);
+  if (cp >= 0 && cp < n) {
+    r.p_r0 = ch[cp].r0;
+    r.p_rows = ch[cp].rows;
+    r.part_w = rf.part[cp & 1];
   }
-  if (kr) {
-    r.nb_red = (int)((a.H + RMS_THREADS - 1) / RMS_THREADS);
-    r.red_nblk = nb_kr;
-    r.red_first = red_first ? 1 : 0;
-    r.part_r = rf.part[kr->index & 1];
+  if (cf >= 0 && cf < n) {
+    r.f_r0 = ch[cf].r0;
+    r.f_rows = ch[cf].rows;
+    r.ybuf = reinterpret_cast<uint16_t*>(rf.ybuf[cf & 1]);
+  }
+  if (cr >= 0 && cr < n) {
+    r.red_ngroups = (int)((ch[cr].rows + RMS_RG - 1) / RMS_RG);
+    r.red_first = cr == 0;
+    r.part_r = rf.part[cr & 1];
     r.dg = rf.dg;
   }
-  const unsigned blocks = (unsigned)(r.nb_bwd + r.f_rows + r.nb_red);
+  return r;
+}
+
+slf_status launch_rms_step(Ctx& c, const RmsStep& r) {
+  const int64_t blocks = rms_blocks_of(r);
   if (!blocks) return SLF_OK;
   ProfScope ps(SLF_PROF_RMSNORM, c.s, 0.0,
-               (kb ? (double)kb->rows * a.H * 8 : 0.0) + (kf ? (double)kf->rows * a.H * 4 : 0.0));
-  const size_t smem = (size_t)a.H * 4;
-  if (smem > 48 * 1024)
-    SLF_CUDA(cudaFuncSetAttribute(rms_step_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+               (double)(r.x_rows * 3 + r.p_rows * 2 + r.f_rows * 2) * r.H * 2);
   cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(blocks);
+  cfg.gridDim = dim3((unsigned)blocks);
   cfg.blockDim = dim3(RMS_THREADS);
-  cfg.dynamicSmemBytes = smem;
   cfg.stream = c.s;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
@@ -1229,7 +1254,7 @@ slf_status phase_s(Ctx& c, const void* X, const void* W, const int32_t* t, int64
   std::vector<SChunk> chunks = s_chunks(p, N, H, dX != nullptr, reinterpret_cast<uint8_t*>(dX));
   if (rf)
     for (auto& k : chunks) {  // the chunk's y rows (dW's B operand too); no X^T variant
-      k.xrows = rf->ybuf;
+      k.xrows = rf->ybuf[k.index & 1];
       k.xt = nullptr;
     }
   // LPT tables per distinct chunk shape (rows, ext, first/RMW), uploaded once.
@@ -1269,25 +1294,19 @@ slf_status phase_s(Ctx& c, const void* X, const void* W, const int32_t* t, int64
     if (c.chunk_ready && i <= 2)
       SLF_CUDA(cudaStreamWaitEvent(c.s, c.chunk_ready[i < 2 ? i : chunks.size() - 1], 0));
     if (k.xt && dW) SLF_TRY(launch_transpose_x(c, a, k));
-    if (rf) {  // y of this chunk; dx / dg partials of the previous one; dg sum of the one before
-      int rpb;
-      const SChunk* kr = i >= 2 ? &chunks[i - 2] : nullptr;
-      SLF_TRY(launch_rms_step(c, a, *rf, dX, i >= 1 ? &chunks[i - 1] : nullptr, &k, kr,
-                              kr ? rms_blocks(c.dev, kr->rows, &rpb) : 0, i == 2));
-    }
+    if (rf && i == 0) SLF_TRY(launch_rms_step(c, rms_jobs(a, *rf, dX, chunks, -1, -1, 0, -1)));  // y of chunk 0
     SLF_TRY(s_chunk_stats(c, a, k, nullptr));
+    const int64_t ki = (int64_t)i;
+    const RmsStep jobs = rf ? rms_jobs(a, *rf, dX, chunks, ki - 2, ki - 1, ki + 1, ki - 2) : RmsStep{};
     SLF_TRY(s_chunk_bwd(c, a, k, nullptr, 1, reduction, scale, loss_rows,
                         dX ? reinterpret_cast<uint8_t*>(dX) + (size_t)k.r0 * H * 2 : nullptr, 0, dW,
-                        tab[i] >= 0 ? arena.dev(c, tab[i]) : nullptr, tab[i] >= 0 ? arena.tables[tab[i]].second : 0));
+                        tab[i] >= 0 ? arena.dev(c, tab[i]) : nullptr, tab[i] >= 0 ? arena.tables[tab[i]].second : 0,
+                        rf ? &jobs : nullptr));
   }
-  if (rf) {  // the last chunk's backward, then the last two dg reductions
-    const size_t n = chunks.size();
-    int rpb;
-    const SChunk* kr = n >= 2 ? &chunks[n - 2] : nullptr;
-    SLF_TRY(launch_rms_step(c, a, *rf, dX, &chunks[n - 1], nullptr, kr, kr ? rms_blocks(c.dev, kr->rows, &rpb) : 0,
-                            n == 2));
-    SLF_TRY(launch_rms_step(c, a, *rf, dX, nullptr, nullptr, &chunks[n - 1], rms_blocks(c.dev, chunks[n - 1].rows, &rpb),
-                            n == 1));
+  if (rf) {  // dx of the last two chunks, dg partials of the last, the last two dg sums
+    const int64_t n = (int64_t)chunks.size();
+    SLF_TRY(launch_rms_step(c, rms_jobs(a, *rf, dX, chunks, n - 2, n - 1, -1, n - 2)));
+    SLF_TRY(launch_rms_step(c, rms_jobs(a, *rf, dX, chunks, n - 1, -1, -1, n - 1)));
     return s_end(c, a, reduction, scale, loss_out, dW, rf->rstd, rf->g);
   }
   return s_end(c, a, reduction, scale, loss_out, dW);
@@ -1748,23 +1767,25 @@ slf_status phase_sharded(Ctx& c, const ShardPlan& sp, slf_comm cm, const void* X
 }
 
 // ---- final RMSNorm fused into schedule S (slf_rmsnorm_lce_fwd_bwd) ------------------
-// Workspace: [ schedule-S workspace (planner budget b) | y chunk buffer [max chunk rows][H] bf16 |
-// rstd [N] fp32 | dg partials 2 x [RMS_NB_MAX][H] fp32 ].  With budget 0 the LCE part takes its
+// Workspace: [ schedule-S workspace (planner budget b) | 2 y chunk buffers [max chunk rows][H] bf16 |
+// rstd [N] fp32 | 2 dg partial buffers [max chunk rows / RMS_RG][H] fp32 ].  With budget 0 the LCE part takes its
 // default 5 % plan and the RMSNorm buffers come on top; otherwise the whole layout fits `budget`.
 struct RmsPlan {
   Plan p;
-  size_t off_y, off_rstd, off_part0, off_part1, total;
+  size_t off_y0, off_y1, off_rstd, off_part0, off_part1, total;
 };
 
 bool rms_layout(int64_t N, int64_t H, int64_t V, size_t b, RmsPlan* rp) {
   if (!plan_s(N, H, V, b, &rp->p)) return false;
   int64_t ymax = 0;
   for (const SChunk& k : s_chunks(rp->p, N, H, true, nullptr)) ymax = std::max(ymax, k.rows);
-  rp->off_y = align_up(rp->p.total, 1024);
-  rp->off_rstd = align_up(rp->off_y + (size_t)ymax * H * 2, 1024);
+  const size_t yb = (size_t)ymax * H * 2, pb = (size_t)((ymax + RMS_RG - 1) / RMS_RG) * H * 4;
+  rp->off_y0 = align_up(rp->p.total, 1024);
+  rp->off_y1 = align_up(rp->off_y0 + yb, 1024);
+  rp->off_rstd = align_up(rp->off_y1 + yb, 1024);
   rp->off_part0 = align_up(rp->off_rstd + (size_t)N * 4, 1024);
-  rp->off_part1 = align_up(rp->off_part0 + (size_t)RMS_NB_MAX * H * 4, 1024);
-  rp->total = rp->off_part1 + (size_t)RMS_NB_MAX * H * 4;
+  rp->off_part1 = align_up(rp->off_part0 + pb, 1024);
+  rp->total = rp->off_part1 + pb;
   return true;
 }
 
@@ -2370,6 +2391,30 @@ slf_status slf_scale_bf16(void* p, int64_t n, float s, void* stream) {
   return SLF_OK;
 }
 
+slf_status slf_scale_bf16_dev(void* p, int64_t n, const float* s_dev, void* stream) {
+  if (!p || !s_dev || n < 0 || (n % 8)) return fail(SLF_ERR_ARG, "p, s must be non-null and n a multiple of 8");
+  if (!aligned16(p)) return fail(SLF_ERR_ALIGN, "pointer must be 16-byte aligned");
+  DevInfo* dev;
+  SLF_TRY(device_info(&dev));
+  if (n == 0) return SLF_OK;
+  const int64_t groups = n / 8;
+  const int blocks = (int)std::min<int64_t>((groups + 255) / 256, (int64_t)dev->sms * 8);
+  scale_bf16_dev_kernel<<<blocks, 256, 0, reinterpret_cast<cudaStream_t>(stream)>>>(reinterpret_cast<uint4*>(p), groups,
+                                                                                   s_dev);
+  SLF_CUDA(cudaGetLastError());
+  return SLF_OK;
+}
+
+slf_status slf_rowstat_scale(const slf_rowstat* in, const float* grad, int per_row, int64_t N, slf_rowstat* out,
+                             void* stream) {
+  if (!in || !grad || !out || N < 1) return fail(SLF_ERR_ARG, "null pointer or N < 1");
+  if (!aligned16(in) || !aligned16(out)) return fail(SLF_ERR_ALIGN, "rowstat pointers must be 16-byte aligned");
+  rowstat_scale_kernel<<<(unsigned)((N + 255) / 256), 256, 0, reinterpret_cast<cudaStream_t>(stream)>>>(
+      reinterpret_cast<const float4*>(in), grad, per_row, N, reinterpret_cast<float4*>(out));
+  SLF_CUDA(cudaGetLastError());
+  return SLF_OK;
+}
+
 // ---- debug trace (SLF_DEBUG_TRACE) ------------------------------------------------------------------
 slf_status slf_debug_trace_read(uint64_t* host, int64_t n) {
   if (!host || n < 0) return fail(SLF_ERR_ARG, "bad arguments");
@@ -2467,11 +2512,11 @@ slf_status slf_rmsnorm_lce_fwd_bwd(const void* x, const void* g, float eps, cons
   rf.g = g;
   rf.eps = eps;
   rf.dg = dg;
-  rf.ybuf = c.ws + rp.off_y;
+  rf.ybuf[0] = c.ws + rp.off_y0;
+  rf.ybuf[1] = c.ws + rp.off_y1;
   rf.rstd = reinterpret_cast<float*>(c.ws + rp.off_rstd);
   rf.part[0] = reinterpret_cast<float*>(c.ws + rp.off_part0);
   rf.part[1] = reinterpret_cast<float*>(c.ws + rp.off_part1);
-  rf.nb_max = RMS_NB_MAX;
   return phase_s(c, x, weight, targets, N, H, V, ignore_index, reduction, scale, loss_out, dx, dweight, &rf);
 }
 
@@ -2480,7 +2525,7 @@ slf_status slf_rmsnorm_lce_plan_describe(int64_t N, int64_t H, int64_t V, size_t
   RmsPlan rp;
   if (!rms_plan(N, H, V, budget_bytes, &rp)) return fail(SLF_ERR_WORKSPACE, "no plan fits");
   snprintf(out, cap, "schedule=S rmsnorm_fused row_chunk=%lld n_chunks=%lld lce_workspace=%zu y_chunk_bytes=%zu "
-                     "workspace=%zu", (long long)rp.p.C, (long long)rp.p.nCh, rp.p.total, rp.off_rstd - rp.off_y, rp.total);
+                     "workspace=%zu", (long long)rp.p.C, (long long)rp.p.nCh, rp.p.total, rp.off_y1 - rp.off_y0, rp.total);
   return SLF_OK;
 }
 

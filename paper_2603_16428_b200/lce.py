@@ -630,9 +630,31 @@ def scale_(t, s: float):
     return t
 
 
+def scale_dev_(t, s_dev):
+    """In-place t *= s_dev[0] (a CUDA fp32 scalar tensor, read on the device); no-op pass for 1."""
+    if t is None:
+        return t
+    s_dev = s_dev.detach().reshape(-1).to(torch.float32).contiguous()
+    check(lib().slf_scale_bf16_dev(t.data_ptr(), t.numel(), s_dev.data_ptr(), _stream_ptr(t.device)),
+          "slf_scale_bf16_dev")
+    return t
+
+
+def rowstat_scale(rowstat, grad, per_row: bool):
+    """RowStat copy with coef *= grad (scalar or per row), on the device (slf_rowstat_scale)."""
+    N = rowstat.numel() // 16
+    grad = grad.detach().reshape(-1).to(torch.float32).contiguous()
+    out = torch.empty_like(rowstat)
+    check(lib().slf_rowstat_scale(rowstat.data_ptr(), grad.data_ptr(), int(per_row), N, out.data_ptr(),
+                                  _stream_ptr(rowstat.device)), "slf_rowstat_scale")
+    return out
+
+
 class LCEFunctionFused(torch.autograd.Function):
     """autograd wrapper on the fused call (schedule S when it fits): the gradients are formed during
-    the forward (no recompute) and scaled by grad_output in backward (a no-op for grad_output == 1)."""
+    the forward (no recompute) and scaled by grad_output in backward on the device (no host read; a
+    no-op pass for grad_output == 1, otherwise one more bf16 rounding of the stored gradients —
+    exact for powers of two; use LCEFunction to fold grad_output into the gradients' formation)."""
 
     @staticmethod
     def forward(ctx, hidden, weight, targets, ignore_index=-100, reduction="mean"):
@@ -647,8 +669,7 @@ class LCEFunctionFused(torch.autograd.Function):
     def backward(ctx, grad_out):
         dX, dW = ctx.grads
         ctx.grads = None
-        g = float(grad_out.item())
-        return scale_(dX, g), scale_(dW, g), None, None, None
+        return scale_dev_(dX, grad_out), scale_dev_(dW, grad_out), None, None, None
 
 
 class LCEFunction(torch.autograd.Function):
@@ -664,8 +685,8 @@ class LCEFunction(torch.autograd.Function):
     @staticmethod
     def backward(ctx, grad_out):
         hidden, weight, targets, rowstat = ctx.saved_tensors
-        if ctx.reduction == "none":
-            raise NotImplementedError("reduction='none' backward needs a per-row grad; use lce_bwd")
-        g = float(grad_out.item())
-        dX, dW = lce_bwd(hidden, weight, targets, rowstat, g, ctx.needs_input_grad[0], ctx.needs_input_grad[1])
+        # grad_output folded into the per-row coefficients on the device (per row for 'none'): the
+        # gradients are formed once, in fp32, already scaled; no host synchronisation.
+        rs = rowstat_scale(rowstat, grad_out, per_row=ctx.reduction == "none")
+        dX, dW = lce_bwd(hidden, weight, targets, rs, 1.0, ctx.needs_input_grad[0], ctx.needs_input_grad[1])
         return dX, dW, None, None, None
