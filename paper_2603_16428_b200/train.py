@@ -61,18 +61,23 @@ class LMHeadTrainer:
             self._bufs = {N: b}  # one batch shape at a time (the workspace is sized for it)
         return b
 
-    def step(self, x: torch.Tensor, targets: torch.Tensor):
+    def step(self, x: torch.Tensor, targets: torch.Tensor, events=None):
         """One step on the batch (x, targets): returns (loss [1] fp32, dx, dg) as device tensors.  The
-        dW of this step is being applied to W when it returns; the next step (or finish()) waits."""
+        dW of this step is being applied to W when it returns; the next step (or finish()) waits.
+        `events` (optional pair of CUDA events) are recorded around the fused call (timing)."""
         b = self._buffers(x.shape[0])
         if self._pending:  # the forward reads W: the previous update's h2d copies first (stream wait)
             self.adam.wait(self.W.device)
             self._pending = False
+        if events is not None:
+            events[0].record()
         # dx / dW buffers are rewritten by this call: the previous update must have read its dW
         loss, dx, dg, dW = rmsnorm_lce_fwd_bwd(x, self.g, self.W, targets, eps=self.rms_eps,
                                                ignore_index=self.ignore_index, reduction=self.reduction,
                                                budget_bytes=self.budget, workspace=b["ws"],
                                                out=(b["loss"], b["dx"], b["dg"], b["dW"]))
+        if events is not None:
+            events[1].record()
         self.adam.step_device_async(dW, self.W)
         self._pending = True
         self.steps += 1

@@ -23,12 +23,18 @@ def slf():
 def test_train_loop_vs_oracle_loop(slf):
     """K = 3 steps of LMHeadTrainer on the tiny config (a fresh seeded batch per step) against the
     oracle loop: loss_k, dW_k = oracle.rmsnorm_lce(x_k, g, bf16(p)), p = oracle.adam_step(p, dW_k).
-    Adam eps = 1e-4 (the scale of the small dW entries) keeps the update Lipschitz in the gradient, so
-    the north-star gradient tolerance carries over to the parameters; with eps -> 0 the first Adam
-    step is lr * sign(g), and entries whose |g| is below the bf16 gradient error flip sign — an
-    ill-conditioned comparison rather than a defect."""
+
+    Tolerance, derived from the north-star gradient bound: the Adam update
+    u = lr m^/(sqrt(v^) + eps) changes by at most lr/eps per unit change of m^ and of sqrt(v^), and
+    both move by at most the gradient error d_k = GRAD_TOL * max|dW_k| (max norm), so after K steps
+    |p_gpu - p_oracle| <= sum_k 2 lr max_{j<=k} d_j / eps.  eps = 1e-2 (above the largest |dW|
+    here, ~4e-3) makes that bound a few % of the parameters' movement; as eps -> 0 the first Adam step
+    becomes lr * sign(g) and entries whose |g| is below the bf16 gradient error can flip — the bound
+    grows as 1/eps, i.e. the comparison, not the code, becomes ill-conditioned.  The worst-case
+    bound is loose (about half the movement here); the error is also held to GRAD_TOL of the
+    movement (observed on the B200: 1.8e-5 against 1.9e-3, about 1 %)."""
     from paper_2603_16428_b200.train import LMHeadTrainer
-    K, lr, eps = 3, 1e-3, 1e-4
+    K, lr, eps = 3, 1e-3, 1e-2
     base = synth.make_config("tiny", seed=50, alpha=4.0, dist="zipf")
     H = base.H
     g_np = synth.f32_to_bf16_bits((1 + 0.2 * np.random.default_rng(7).standard_normal(H)).astype(np.float32))
@@ -54,16 +60,21 @@ def test_train_loop_vs_oracle_loop(slf):
     m = np.zeros_like(p)
     v = np.zeros_like(p)
     gw = synth.bf16_bits_to_f64(g_np)
+    bound, dmax = 0.0, 0.0
     for k, b in enumerate(batches):
         W_used = synth.bf16_bits_to_f64(oracle.bf16_rne(p)).reshape(base.V, H)
         xo, _, to = oracle_inputs(b)
         loss_k, _, _, dW = oracle.rmsnorm_lce(xo, gw, W_used, to, eps=1e-5, reduction="mean")
         assert_loss_close(losses[k], loss_k, "mean")
         p, m, v = oracle.adam_step(p, m, v, dW.reshape(-1), k + 1, lr, eps=eps)
+        dmax = max(dmax, GRAD_TOL * np.max(np.abs(dW)))
+        bound += 2 * lr * dmax / eps
     moved = np.max(np.abs(p - p0))
     err = np.max(np.abs(p_gpu.numpy().astype(np.float64) - p))
-    print(f"train loop: max |p_gpu - p_oracle| = {err:.3e}, max movement {moved:.3e}, losses {losses}")
-    assert err <= GRAD_TOL * moved
+    print(f"train loop: max |p_gpu - p_oracle| = {err:.3e} (bound {bound:.3e}), max movement {moved:.3e}, "
+          f"losses {losses}")
+    assert err <= bound
+    assert err <= GRAD_TOL * moved  # and, observed, within the gradient tolerance of the movement
     assert not torch.equal(W, W0)
     tr.close()
 

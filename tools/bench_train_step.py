@@ -54,9 +54,7 @@ def main():
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(a.steps)]
     w0 = time.perf_counter()
     for k in range(a.steps):
-        ev[k][0].record()
-        loss, dx, dg = tr.step(*batches[k % nb])
-        ev[k][1].record()
+        loss, dx, dg = tr.step(*batches[k % nb], events=ev[k])
         losses.append(loss.clone())
     tr.finish()
     torch.cuda.synchronize()
