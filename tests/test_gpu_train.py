@@ -28,7 +28,7 @@ def test_train_loop_vs_oracle_loop(slf):
     u = lr m^/(sqrt(v^) + eps) changes by at most lr/eps per unit change of m^ and of sqrt(v^), and
     both move by at most the gradient error d_k = GRAD_TOL * max|dW_k| (max norm), so after K steps
     |p_gpu - p_oracle| <= sum_k 2 lr max_{j<=k} d_j / eps.  eps = 1e-2 (above the largest |dW|
-    here, ~4e-3) makes that bound a few % of the parameters' movement; as eps -> 0 the first Adam step
+    here, ~4e-3) keeps that bound below the parameters' movement; as eps -> 0 the first Adam step
     becomes lr * sign(g) and entries whose |g| is below the bf16 gradient error can flip — the bound
     grows as 1/eps, i.e. the comparison, not the code, becomes ill-conditioned.  The worst-case
     bound is loose (about half the movement here); the error is also held to GRAD_TOL of the
