@@ -80,7 +80,16 @@ struct GemmArgs {
   int tma_out;  // EPI_STASH: write the stash through the output tensor map (TMA-staged stores)
   void* out2;  // DX final bf16 destination (row 0 of the GEMM)
   int64_t ld_out2;
+  // Schedule S with a per-row stash reference: EPI_STASH stores exp(z - mref[r])
+  // instead of exp(z - m_tile) wherever m_tile - mref[r] <= STASH_REF_SLACK (else the tile keeps its
+  // own max); EPI_DXS multiplies the row's accumulator by fac[r].  Null: per-tile max / factor 1.
+  const float* mref;
+  const float* fac;
 };
+
+// A tile whose max exceeds the row reference by more than this keeps its own max in the stash
+// (exp(70) = 2.5e30: far from the bf16 / fp32 overflow at exp(88.7)).
+constexpr float STASH_REF_SLACK = 70.f;
 
 __device__ __forceinline__ void tile_coords(int tile, const GemmArgs& a, int& m_blk, int& n_blk) {
   // Grouped raster: walk group_m row tiles down before stepping to the next column tile, so one
@@ -158,6 +167,11 @@ __device__ __forceinline__ void epilogue_tile(const GemmArgs& a, uint32_t taddr,
         if (c * 32 + i < ncols) mx = fmaxf(mx, __uint_as_float(v[i]));
     }
     const float mb = mx * LOG2E;
+    float cmul = 1.f;  // stash relative to the row reference: exp(z - m) * exp(m - mref)
+    if (a.mref && row_ok) {
+      const float M = a.mref[r];
+      if (!(mx - M > STASH_REF_SLACK)) cmul = ex2((mx - M) * LOG2E);
+    }
     float s = 0.f, zt = 0.f;
     uint16_t* out = reinterpret_cast<uint16_t*>(a.out) + (size_t)r * a.ld_out + n0;
 #pragma unroll 1
@@ -175,7 +189,7 @@ __device__ __forceinline__ void epilogue_tile(const GemmArgs& a, uint32_t taddr,
         s += e0 + e1;
         zt = (c * 32 + i == tl) ? z0 : zt;
         zt = (c * 32 + i + 1 == tl) ? z1 : zt;
-        p[i / 2] = pack_bf16x2(e0, e1);
+        p[i / 2] = pack_bf16x2(e0 * cmul, e1 * cmul);
       }
       if (row_ok && !(a.mode & 32)) {  // mode bit 32: skip the stash stores (timing experiment only)
 #pragma unroll
@@ -201,6 +215,7 @@ __device__ __forceinline__ void epilogue_tile(const GemmArgs& a, uint32_t taddr,
       valid = rs.valid != 0;
     }
     const uint16_t* wt = a.wrow + (size_t)(tl >= 0 ? tl : 0) * a.ld_w + n0;
+    const float fr = (a.fac && row_ok) ? a.fac[r] : 1.f;  // per-row stash reference factor
 #pragma unroll 1
     for (int c = 0; c < BN / 32; ++c) {
       if (c * 32 >= ncols) break;
@@ -213,7 +228,7 @@ __device__ __forceinline__ void epilogue_tile(const GemmArgs& a, uint32_t taddr,
           if (j < ncols) {
             float f[8];
 #pragma unroll
-            for (int e = 0; e < 8; ++e) f[e] = __uint_as_float(v[q * 8 + e]);
+            for (int e = 0; e < 8; ++e) f[e] = __uint_as_float(v[q * 8 + e]) * fr;
             if (tl >= 0) {
               const uint4 w = *reinterpret_cast<const uint4*>(wt + j);
               f[0] -= coef * bf16lo_to_f32(w.x); f[1] -= coef * bf16hi_to_f32(w.x);
@@ -491,6 +506,11 @@ __device__ __forceinline__ void epilogue_stash_tma(const GemmArgs& a, const CUte
       if (c * 32 + i < ncols) mx = fmaxf(mx, __uint_as_float(v[i]));
   }
   const float mb = mx * LOG2E;
+  float cmul = 1.f;  // stash relative to the row reference: exp(z - m) * exp(m - mref)
+  if (a.mref && row_ok) {
+    const float M = a.mref[r];
+    if (!(mx - M > STASH_REF_SLACK)) cmul = ex2((mx - M) * LOG2E);
+  }
   float s = 0.f, zt = 0.f;
   // 64-column chunks are staged NB at a time
 #pragma unroll 1
@@ -520,7 +540,7 @@ __device__ __forceinline__ void epilogue_stash_tma(const GemmArgs& a, const CUte
       s += e0 + e1;
       zt = (c * 32 + i == tl) ? z0 : zt;
       zt = (c * 32 + i + 1 == tl) ? z1 : zt;
-      p[i / 2] = pack_bf16x2(e0, e1);
+      p[i / 2] = pack_bf16x2(e0 * cmul, e1 * cmul);
     }
     const uint32_t rowaddr = sbase + ((c >> 1) % NB) * CHUNK_BYTES + rl * 128;
 #pragma unroll

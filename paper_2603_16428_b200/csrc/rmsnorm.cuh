@@ -148,6 +148,14 @@ struct RmsStep {
   int red_ngroups, red_first;  // red job: row groups to sum (0: none)
   const float* part_r;
   float* dg;
+  // fwd job, per-row stash reference (s_kernels.cuh mref_kernel; null: not needed): mref[row] =
+  // y_row . W[t_row] + shift, or +inf for ignored / out-of-range targets
+  const uint16_t* W;
+  const int32_t* t;
+  int32_t ignore_index;
+  int64_t V;
+  float shift;
+  float* mref;
 };
 
 __host__ __device__ inline int rms_nslab(int64_t H) { return (int)((H + 255) / 256); }
@@ -218,12 +226,31 @@ __device__ __forceinline__ void rms_block(const RmsStep& a, int64_t b) {
     const float r = rsqrtf(block_sum_256(ss, red) / (float)a.H + a.eps);
     if (threadIdx.x == 0) a.rstd[row] = r;
     uint4* yr = reinterpret_cast<uint4*>(a.ybuf + b * a.H);
+    int64_t loc = -1;
+    if (a.mref) {
+      const int32_t tt = a.t[row];
+      loc = (tt == a.ignore_index || tt < 0 || (int64_t)tt >= a.V) ? -1 : (int64_t)tt;
+    }
+    const uint4* wr = reinterpret_cast<const uint4*>(a.W + (loc >= 0 ? loc : 0) * a.H);
+    float dot = 0.f;
     for (int64_t q = threadIdx.x; q < groups; q += RMS_THREADS) {
       float f[8], w[8];
       unpack8(xr[q], f);
       unpack8(gr[q], w);
-      yr[q] = make_uint4(pack_bf16x2(f[0] * r * w[0], f[1] * r * w[1]), pack_bf16x2(f[2] * r * w[2], f[3] * r * w[3]),
-                         pack_bf16x2(f[4] * r * w[4], f[5] * r * w[5]), pack_bf16x2(f[6] * r * w[6], f[7] * r * w[7]));
+      const uint4 y = make_uint4(pack_bf16x2(f[0] * r * w[0], f[1] * r * w[1]), pack_bf16x2(f[2] * r * w[2], f[3] * r * w[3]),
+                                 pack_bf16x2(f[4] * r * w[4], f[5] * r * w[5]), pack_bf16x2(f[6] * r * w[6], f[7] * r * w[7]));
+      yr[q] = y;
+      if (loc >= 0) {
+        float yv[8], wv[8];
+        unpack8(y, yv);
+        unpack8(wr[q], wv);
+#pragma unroll
+        for (int e = 0; e < 8; ++e) dot = fmaf(yv[e], wv[e], dot);
+      }
+    }
+    if (a.mref) {
+      const float d = block_sum_256(dot, red);  // block-uniform branch (loc is per row)
+      if (threadIdx.x == 0) a.mref[row] = loc >= 0 ? d + a.shift : INFINITY;
     }
     return;
   }

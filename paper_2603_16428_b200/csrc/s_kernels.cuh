@@ -171,6 +171,160 @@ __global__ void __launch_bounds__(256) combine_transform_kernel(
   }
 }
 
+// ---- per-row stash reference ----------------------------------------------------
+// The stash GEMM can store p~ = exp(z - M_i) against a per-row reference M_i fixed BEFORE the GEMM
+// instead of each tile's own max; then G_P = coef * exp(z - lse) = p~ * f_i with one factor per row,
+// f_i = coef * exp(M_i - lse_i), which the grouped GEMMs apply without touching the stash: dX's
+// epilogue multiplies the row's accumulator by f_i, and dW's B operand is X'_chunk = bf16(f ⊙ X).
+// M_i = z_{i,t_i} + STASH_REF_SHIFT (the target logit, a dot product per row): the row max is then at
+// most M_i + 88 unless the target's loss exceeds ~128 nats, and entries below M_i - 87 (lost to
+// underflow) have softmax < e^-47.  Rows that are ignored or whose target is out of range get
+// M_i = +inf: their stash row is exactly 0 (and coef = 0).
+constexpr float STASH_REF_SHIFT = 40.f;
+
+// One warp per row: M_i = x_i . W[t_i - vocab_start] + STASH_REF_SHIFT (fp32, 16-byte loads).
+__global__ void __launch_bounds__(256) mref_kernel(const uint16_t* __restrict__ X, const uint16_t* __restrict__ W,
+                                                  const int32_t* __restrict__ t, int64_t N, int64_t H,
+                                                  int32_t ignore_index, int64_t vocab_start, int64_t V_l,
+                                                  float* __restrict__ mref) {
+  const int64_t row = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (row >= N) return;
+  const int32_t tt = t[row];
+  const int64_t loc = (int64_t)tt - vocab_start;
+  if (tt == ignore_index || loc < 0 || loc >= V_l) {
+    if (lane == 0) mref[row] = INFINITY;
+    return;
+  }
+  const uint4* xr = reinterpret_cast<const uint4*>(X + row * H);
+  const uint4* wr = reinterpret_cast<const uint4*>(W + loc * H);
+  float acc = 0.f;
+  for (int64_t q = lane; q < H / 8; q += 32) {
+    const uint4 a = xr[q], b = wr[q];
+    acc = fmaf(bf16lo_to_f32(a.x), bf16lo_to_f32(b.x), acc); acc = fmaf(bf16hi_to_f32(a.x), bf16hi_to_f32(b.x), acc);
+    acc = fmaf(bf16lo_to_f32(a.y), bf16lo_to_f32(b.y), acc); acc = fmaf(bf16hi_to_f32(a.y), bf16hi_to_f32(b.y), acc);
+    acc = fmaf(bf16lo_to_f32(a.z), bf16lo_to_f32(b.z), acc); acc = fmaf(bf16hi_to_f32(a.z), bf16hi_to_f32(b.z), acc);
+    acc = fmaf(bf16lo_to_f32(a.w), bf16lo_to_f32(b.w), acc); acc = fmaf(bf16hi_to_f32(a.w), bf16hi_to_f32(b.w), acc);
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+  if (lane == 0) mref[row] = acc + STASH_REF_SHIFT;
+}
+
+// One block per row of the chunk (single GPU): the row's lse / loss / RowStat from its tile
+// partials (as combine_transform), then the row factor f_i and X'_i = bf16(f_i * x_i).  The stash
+// is not touched, except for rare rows where the per-row reference does not fit (a tile kept its
+// own max, or f_i is outside [1e-30, 1e30]): those are rescaled in place to G_P tile by tile and get
+// f_i = 1, X'_i = x_i.  xs may alias xrows (the fused RMSNorm's y buffer): each block owns its row.
+__global__ void __launch_bounds__(256) combine_scale_kernel(
+    const float2* __restrict__ partials, int tiles, int rows, const float* __restrict__ zt,
+    const int32_t* __restrict__ t, int64_t V_l, int64_t ld_stash, int32_t ignore_index, int reduction, float scale,
+    float grad_scale, const WsHeader* __restrict__ hdr, float* __restrict__ loss_rows,
+    slf_rowstat* __restrict__ rowstat, uint16_t* __restrict__ stash, uint16_t* __restrict__ stash2, int split,
+    const float* __restrict__ mref, float* __restrict__ fac, const uint16_t* xrows, uint16_t* xs, int64_t H,
+    RmsStep rms) {
+  extern __shared__ float r_t[];  // [tiles]: the tile maxima m_t
+  griddep_launch_dependents();
+  griddep_wait();  // PDL: everything below reads the previous kernel's outputs
+  if ((int)blockIdx.x >= rows) {  // the fused final RMSNorm's jobs riding in this launch (rmsnorm.cuh)
+    rms_block(rms, (int64_t)blockIdx.x - rows);
+    return;
+  }
+  __shared__ float sLse, sF, sCoef, wm[8], ws[8];
+  __shared__ int sFb;
+  const int i = blockIdx.x;
+  const int tid = threadIdx.x;
+  const float M = mref[i];
+  float m = -INFINITY, sum = 0.f;
+  int fb = 0;
+  for (int k = tid; k < tiles; k += 256) {
+    const float2 p = partials[(size_t)k * rows + i];
+    r_t[k] = p.x;
+    fb |= (p.x - M > STASH_REF_SLACK) ? 1 : 0;
+    const float nm = fmaxf(m, p.x);
+    sum = sum * ex2((m - nm) * LOG2E) + p.y * ex2((p.x - nm) * LOG2E);
+    m = nm;
+  }
+  fb = __syncthreads_or(fb);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const float om = __shfl_down_sync(0xffffffffu, m, o), os = __shfl_down_sync(0xffffffffu, sum, o);
+    const float nm = fmaxf(m, om);
+    sum = (m == -INFINITY ? 0.f : sum * ex2((m - nm) * LOG2E)) + (om == -INFINITY ? 0.f : os * ex2((om - nm) * LOG2E));
+    m = nm;
+  }
+  if ((tid & 31) == 0) {
+    wm[tid >> 5] = m;
+    ws[tid >> 5] = sum;
+  }
+  __syncthreads();
+  if (tid == 0) {
+    float Mx = -INFINITY, S = 0.f, z = 0.f;
+    const int32_t tt = t[i];
+    for (int k = 0; k < 8; ++k) Mx = fmaxf(Mx, wm[k]);
+    for (int k = 0; k < 8; ++k)
+      if (wm[k] != -INFINITY) S += ws[k] * ex2((wm[k] - Mx) * LOG2E);
+    if (tt != ignore_index && tt >= 0 && (int64_t)tt < V_l) z = zt[i];
+    const float lse = Mx + logf(S);
+    const bool valid = tt != ignore_index;
+    const bool bad = valid && (tt < 0 || (int64_t)tt >= V_l);
+    const float coef = (valid && !bad) ? coef_of(reduction, scale, hdr->n_valid) : 0.f;
+    float l = valid ? (lse - z) : 0.f;
+    if (bad) l = __int_as_float(0x7fc00000);
+    loss_rows[i] = l;
+    const int32_t tloc = (valid && !bad) ? tt : -1;
+    rowstat[i] = slf_rowstat{lse * LOG2E, coef, tloc, valid ? 1 : 0};
+    const float cg = coef * grad_scale;
+    float f = 0.f;
+    int rfb = fb;
+    if (cg != 0.f) {
+      f = cg * ex2((M - lse) * LOG2E);
+      if (!(fabsf(f) >= 1e-30f && fabsf(f) <= 1e30f)) rfb = 1;
+    }
+    sLse = lse;
+    sCoef = cg;
+    sFb = rfb;
+    sF = rfb ? 1.f : f;
+    fac[i] = rfb ? 1.f : f;
+  }
+  __syncthreads();
+  const float f = sF;
+  if (sFb) {  // rare: rescale this stash row in place to G_P, tile by tile
+    const float lse = sLse, cg = sCoef;
+    for (int k = tid; k < tiles; k += 256) {
+      const float mt = r_t[k];
+      float r;
+      if (mt - M > STASH_REF_SLACK) r = cg * ex2((mt - lse) * LOG2E);          // tile stored exp(z - m_t)
+      else if (M - mt > 80.f) r = 0.f;                                         // its entries < e^-40 of the max
+      else r = cg * ex2((M - mt) * LOG2E) * ex2((mt - lse) * LOG2E);            // stored exp(z - M)
+      r_t[k] = r;
+    }
+    __syncthreads();
+    uint4* row = reinterpret_cast<uint4*>(i < split ? stash + (size_t)i * ld_stash
+                                                    : stash2 + (size_t)(i - split) * ld_stash);
+    const int64_t groups = (V_l + 7) / 8;
+    for (int64_t q = tid; q < groups; q += 256) {
+      const float r = r_t[(q * 8) / 256];
+      uint4 x = row[q];
+      x.x = pack_bf16x2(bf16lo_to_f32(x.x) * r, bf16hi_to_f32(x.x) * r);
+      x.y = pack_bf16x2(bf16lo_to_f32(x.y) * r, bf16hi_to_f32(x.y) * r);
+      x.z = pack_bf16x2(bf16lo_to_f32(x.z) * r, bf16hi_to_f32(x.z) * r);
+      x.w = pack_bf16x2(bf16lo_to_f32(x.w) * r, bf16hi_to_f32(x.w) * r);
+      row[q] = x;
+    }
+  }
+  // X'_i = bf16(f * x_i) (f = 1 for the rescaled rows: an exact copy)
+  const uint4* xr = reinterpret_cast<const uint4*>(xrows + (size_t)i * H);
+  uint4* xo = reinterpret_cast<uint4*>(xs + (size_t)i * H);
+  for (int64_t q = tid; q < H / 8; q += 256) {
+    const uint4 x = xr[q];
+    xo[q] = make_uint4(pack_bf16x2(bf16lo_to_f32(x.x) * f, bf16hi_to_f32(x.x) * f),
+                       pack_bf16x2(bf16lo_to_f32(x.y) * f, bf16hi_to_f32(x.y) * f),
+                       pack_bf16x2(bf16lo_to_f32(x.z) * f, bf16hi_to_f32(x.z) * f),
+                       pack_bf16x2(bf16lo_to_f32(x.w) * f, bf16hi_to_f32(x.w) * f));
+  }
+}
+
 // ---- target CSR ------------------------------------------------------------------------------
 __device__ __forceinline__ bool in_shard(int32_t tt, int32_t ignore_index, int64_t vocab_start, int64_t V_l) {
   const int64_t loc = (int64_t)tt - vocab_start;

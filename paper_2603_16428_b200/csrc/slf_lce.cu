@@ -435,6 +435,7 @@ struct Plan {
   size_t sched_bytes = 0;
   size_t off_sched = 0, off_rowstat = 0, off_shard = 0, off_zt = 0, off_union = 0, off_dxacc = 0;
   size_t off_loss = 0, off_cnt = 0, off_off = 0, off_hits = 0, off_idx = 0, off_part = 0, off_stash = 0;
+  size_t off_mref = 0, off_fac = 0;  // schedule S: per-row stash reference and row factor [N] fp32
   size_t fwd_bytes = 0, bwd_bytes = 0, total = 0;
 };
 
@@ -505,8 +506,8 @@ bool plan_r(int64_t N, int64_t H, int64_t V, size_t budget, Plan* out) {
 }
 
 // Schedule S layout: header | sched arena | RowStat [N] | z_t [N] | row losses [N] | CSR counts
-// [V+2] | CSR offsets [V+2] | hit rows [min(N,V)] | CSR token idx [N] | tile partials [tiles][2C] |
-// stash [C][ld_stash] bf16.  C = the largest multiple of 256 rows that fits the budget.
+// [V+2] | CSR offsets [V+2] | hit rows [min(N,V)] | CSR token idx [N] | ShardStat [N] | stash
+// reference [N] | row factor [N] | tile partials [tiles][2C] | stash [C][ld_stash] bf16.  C = the largest multiple of 256 rows that fits the budget.
 bool plan_s(int64_t N, int64_t H, int64_t V, size_t budget, Plan* out) {
   if (N < 1 || H < 8 || V < 1) return false;
   if (budget == 0) budget = default_budget(N, V);
@@ -522,7 +523,9 @@ bool plan_s(int64_t N, int64_t H, int64_t V, size_t budget, Plan* out) {
   p.off_hits = align_up(p.off_off + (size_t)(V + 2) * 4, 1024);
   p.off_idx = align_up(p.off_hits + (size_t)std::min(N, V) * 4, 1024);
   p.off_shard = align_up(p.off_idx + (size_t)N * 4, 1024);  // per-chunk ShardStat (g = 1 path)
-  p.off_part = align_up(p.off_shard + (size_t)N * 16, 1024);
+  p.off_mref = align_up(p.off_shard + (size_t)N * 16, 1024);
+  p.off_fac = align_up(p.off_mref + (size_t)N * 4, 1024);
+  p.off_part = align_up(p.off_fac + (size_t)N * 4, 1024);
   const int64_t tiles_v = (V + BN - 1) / BN;
   p.ld_stash = (int64_t)align_up((size_t)V, 8);
   const int64_t Nmax = (int64_t)align_up((size_t)N, 256);
@@ -907,6 +910,8 @@ struct SChunk {
   uint8_t* xt = nullptr;  // X_chunk^T [H][ld_xt] (dW's B operand K-major) in free dhidden rows, or nullptr
   int64_t ld_xt = 0;
   const uint8_t* xrows = nullptr;  // the chunk's hidden rows when not X + r0 (fused RMSNorm: its y buffer)
+  uint8_t* xs = nullptr;  // per-row stash reference: X'_chunk = bf16(f ⊙ X) [rows][H], the
+                          // dW GEMM's B operand; null: the stash is rescaled in place (combine_transform)
 };
 
 SChunk s_plain_chunk(const Plan& p, int64_t N, int64_t ch) {
@@ -953,6 +958,7 @@ slf_status s_chunk_stats(Ctx& c, const SArgs& a, const SChunk& k, slf_shardstat*
   g.zt = zt + r0;
   g.out = c.ws + p.off_stash;
   g.ld_out = p.ld_stash;
+  if (k.xs) g.mref = reinterpret_cast<const float*>(c.ws + p.off_mref) + r0;
   static const int dbg = getenv("SLF_DEBUG_EPI") ? atoi(getenv("SLF_DEBUG_EPI")) : 0;
   g.mode = (dbg & 64) ? 32 : 0;  // timing experiment only (SLF_DEBUG_EPI=64): skip the stash stores
   g.tma_out = 1;      // the stash is written through TMA-staged stores
@@ -1005,6 +1011,7 @@ slf_status s_build_bwd(Ctx& c, const SArgs& a, const SChunk& k, void* dXc, int d
     q.a.out = dXc;
     q.a.ld_out = a.H;
     q.a.mode = dx_fp32 ? 1 : 0;
+    if (k.xs) q.a.fac = reinterpret_cast<const float*>(c.ws + p.off_fac) + r0;
     finish_geometry(q.a, cg);
   }
   if (dW) {  // dW (+)= G_P^T X_chunk : A = G_P^T (MN-major; K = rows split ws | ext), B = X_chunk (MN-major)
@@ -1030,7 +1037,7 @@ slf_status s_build_bwd(Ctx& c, const SArgs& a, const SChunk& k, void* dXc, int d
       SLF_TRY(tmap_kmajor(&q.tb, k.xt, rows, a.H, k.ld_xt, b_box_rows()));
       q.b_mn = false;
     } else {
-      SLF_TRY(tmap_mnmajor(&q.tb, Xr, a.H, rows, a.H, b_box_rows() / 64));
+      SLF_TRY(tmap_mnmajor(&q.tb, k.xs ? k.xs : Xr, a.H, rows, a.H, b_box_rows() / 64));
       q.b_mn = true;
     }
     q.a.M = (int)a.V_l;
@@ -1058,7 +1065,27 @@ slf_status s_chunk_bwd(Ctx& c, const SArgs& a, const SChunk& k, const slf_shards
   const int64_t r0 = k.r0, rows = k.rows;
   const int tiles_v = (int)((a.V_l + BN - 1) / BN);
   static const bool skip_ct = getenv("SLF_DEBUG_EPI") && (atoi(getenv("SLF_DEBUG_EPI")) & 512);  // timing only
-  if (!skip_ct) {
+  if (k.xs && !skip_ct) {  // per-row stash reference: factors and X'_chunk, the stash stays as is
+    ProfScope ps(SLF_PROF_COMBINE_TRANSFORM, c.s, 0.0, (double)rows * (tiles_v * 8.0 + a.H * 4.0 + 40.0));
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)(rows + (rms ? rms_blocks_of(*rms) : 0)));
+    cfg.blockDim = dim3(256);
+    cfg.dynamicSmemBytes = tiles_v * sizeof(float);
+    cfg.stream = c.s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    const uint8_t* xr = k.xrows ? k.xrows : reinterpret_cast<const uint8_t*>(a.X) + (size_t)r0 * a.H * 2;
+    SLF_CUDA(cudaLaunchKernelEx(
+        &cfg, combine_scale_kernel, reinterpret_cast<const float2*>(c.ws + p.off_part), tiles_v, (int)rows,
+        reinterpret_cast<const float*>(c.ws + p.off_zt) + r0, a.t + r0, a.V_l, p.ld_stash, a.ign, reduction, scale, 1.0f,
+        (const WsHeader*)hdr_of(c.ws), loss_rows_all + r0, reinterpret_cast<slf_rowstat*>(c.ws + p.off_rowstat) + r0,
+        reinterpret_cast<uint16_t*>(c.ws + p.off_stash), reinterpret_cast<uint16_t*>(k.ext_base), (int)(rows - k.ext),
+        reinterpret_cast<const float*>(c.ws + p.off_mref) + r0, reinterpret_cast<float*>(c.ws + p.off_fac) + r0,
+        reinterpret_cast<const uint16_t*>(xr), reinterpret_cast<uint16_t*>(k.xs), a.H, rms ? *rms : RmsStep{}));
+  } else if (!skip_ct) {
     ProfScope ps(SLF_PROF_COMBINE_TRANSFORM, c.s, 0.0, (double)rows * (tiles_v * 8.0 + a.V_l * 4.0 + 16.0 * g + 24));
     // Programmatic dependent launch: blocks start while the stash GEMM drains and wait in-kernel.
     cudaLaunchConfig_t cfg = {};
@@ -1190,6 +1217,7 @@ struct RmsFuse {
   uint8_t* ybuf[2];   // [max chunk rows][H] bf16, by chunk parity
   float* rstd;        // [N]
   float* part[2];     // [max row groups][H] fp32 dg partials, by chunk parity
+  float* mref;        // [N] per-row stash reference (the plan's array)
 };
 
 // The RMSNorm jobs of one launch, for chunks (by index; -1 = none): dx of cx, dg partials of cp,
@@ -1217,6 +1245,14 @@ RmsStep rms_jobs(const SArgs& a, const RmsFuse& rf, void* dX, const std::vector<
     r.f_r0 = ch[cf].r0;
     r.f_rows = ch[cf].rows;
     r.ybuf = reinterpret_cast<uint16_t*>(rf.ybuf[cf & 1]);
+    if (ch[cf].xs) {  // the chunk's per-row stash reference from its y rows
+      r.W = reinterpret_cast<const uint16_t*>(a.W);
+      r.t = a.t;
+      r.ignore_index = a.ign;
+      r.V = a.V_l;
+      r.shift = STASH_REF_SHIFT;
+      r.mref = rf.mref;
+    }
   }
   if (cr >= 0 && cr < n) {
     r.red_ngroups = (int)((ch[cr].rows + RMS_RG - 1) / RMS_RG);
@@ -1252,11 +1288,38 @@ slf_status phase_s(Ctx& c, const void* X, const void* W, const int32_t* t, int64
   const SArgs a{X, W, t, N, H, V, 0, V, ignore_index};
   SLF_TRY(s_begin(c, a, dW != nullptr));
   std::vector<SChunk> chunks = s_chunks(p, N, H, dX != nullptr, reinterpret_cast<uint8_t*>(dX));
+  // Per-row stash reference (SLF_S_CLASSIC=1: the in-place rescale for every chunk).
+  // X'_chunk goes over the fused RMSNorm's y buffer, else into dhidden's unwritten rows after the
+  // chunk's rows and extended stash when it fits there (the last chunks keep the in-place rescale).
+  static const bool classic = getenv("SLF_S_CLASSIC") != nullptr;
+  bool any_ref = false;
   if (rf)
     for (auto& k : chunks) {  // the chunk's y rows (dW's B operand too); no X^T variant
       k.xrows = rf->ybuf[k.index & 1];
       k.xt = nullptr;
+      if (!classic && dX) k.xs = rf->ybuf[k.index & 1];
+      any_ref |= k.xs != nullptr;
     }
+  else if (!classic && dX && dW)
+    for (auto& k : chunks) {
+      const size_t lo = align_up((size_t)(k.r0 + k.rows) * H * 2 + (size_t)k.ext * p.ld_stash * 2, 1024);
+      if (!k.xt && lo + (size_t)k.rows * H * 2 <= (size_t)N * H * 2) {
+        k.xs = reinterpret_cast<uint8_t*>(dX) + lo;
+        any_ref = true;
+      }
+    }
+  // M_i = x_i . W[t_i] + shift: for every row at once when the inputs are resident; chunk by chunk,
+  // after the chunk's rows arrived, in the host-input call
+  auto launch_mref = [&](int64_t r0, int64_t rows) -> slf_status {
+    ProfScope ps(SLF_PROF_PREP, c.s, 2.0 * rows * H, (double)rows * H * 4);
+    mref_kernel<<<(unsigned)((rows * 32 + 255) / 256), 256, 0, c.s>>>(
+        reinterpret_cast<const uint16_t*>(X) + (size_t)r0 * H, reinterpret_cast<const uint16_t*>(W), t + r0, rows, H,
+        ignore_index, 0, V, reinterpret_cast<float*>(c.ws + p.off_mref) + r0);
+    SLF_CUDA(cudaGetLastError());
+    return SLF_OK;
+  };
+  const bool mref_per_chunk = any_ref && !rf && c.chunk_ready;
+  if (any_ref && !rf && !mref_per_chunk) SLF_TRY(launch_mref(0, N));
   // LPT tables per distinct chunk shape (rows, ext, first/RMW), uploaded once.
   SchedArena arena;
   std::vector<std::pair<std::pair<int64_t, int64_t>, int>> keys;
@@ -1294,6 +1357,7 @@ slf_status phase_s(Ctx& c, const void* X, const void* W, const int32_t* t, int64
     if (c.chunk_ready && i <= 2)
       SLF_CUDA(cudaStreamWaitEvent(c.s, c.chunk_ready[i < 2 ? i : chunks.size() - 1], 0));
     if (k.xt && dW) SLF_TRY(launch_transpose_x(c, a, k));
+    if (mref_per_chunk && k.xs) SLF_TRY(launch_mref(k.r0, k.rows));
     if (rf && i == 0) SLF_TRY(launch_rms_step(c, rms_jobs(a, *rf, dX, chunks, -1, -1, 0, -1)));  // y of chunk 0
     SLF_TRY(s_chunk_stats(c, a, k, nullptr));
     const int64_t ki = (int64_t)i;
@@ -2517,6 +2581,7 @@ slf_status slf_rmsnorm_lce_fwd_bwd(const void* x, const void* g, float eps, cons
   rf.rstd = reinterpret_cast<float*>(c.ws + rp.off_rstd);
   rf.part[0] = reinterpret_cast<float*>(c.ws + rp.off_part0);
   rf.part[1] = reinterpret_cast<float*>(c.ws + rp.off_part1);
+  rf.mref = reinterpret_cast<float*>(c.ws + rp.p.off_mref);
   return phase_s(c, x, weight, targets, N, H, V, ignore_index, reduction, scale, loss_out, dx, dweight, &rf);
 }
 
