@@ -332,7 +332,6 @@ def main():
     X = torch.from_numpy(inp.X[n0:n1].view(np.int16)).view(torch.bfloat16).to(dev)
     W = torch.from_numpy(inp.W[v0:v1].view(np.int16)).view(torch.bfloat16).to(dev)
     t = torch.from_numpy(inp.t[n0:n1]).to(dev)
-    n_valid_global = int((inp.t != -100).sum())  # known when the batch is built (DP mean denominator)
 
     if multi and args.budget == 0 and not dp:
         # Sharded runs: 5% of the GLOBAL N*V*2 logits per GPU (SURVEY q7 "lenient" reading; both
@@ -382,16 +381,8 @@ def main():
     dX = torch.empty(N_l, H, dtype=torch.bfloat16, device=dev)
     dW = torch.empty(V_l, H, dtype=torch.bfloat16, device=dev)
     extra = ws.numel()
-    if dp:
-        from paper_2603_16428_b200.sharded import TokenShardedLCE
-        dpm = TokenShardedLCE(budget_bytes=args.budget, schedule=args.schedule)
-        dp_comm = None
-        if args.comm == "native":  # slf_lce_fwd_bwd_dp: global MEAN denominator and syncs inside the library
-            try:
-                dp_comm = slf.Comm.from_process_group(device=local)
-            except Exception as e:
-                comm_note = f"native communicator unavailable ({e}); torch.distributed orchestration"
-                print(comm_note, file=sys.stderr)
+    if dp:  # slf_lce_fwd_bwd_dp: global MEAN denominator, loss and dW syncs inside the library
+        dp_comm = slf.Comm.from_process_group(device=local)
     elif multi and not native:
         if sharded.schedule == "S":
             C_s, _ = slf.s_plan(N, H, V_l, ws_budget)
@@ -405,12 +396,8 @@ def main():
                             schedule=args.schedule)
             return loss
         if dp:
-            if dp_comm is not None:
-                l, _, _ = slf.lce_fwd_bwd_dp(Xs, W, ts, dp_comm, sync_dweight=True, workspace=ws, out=(loss, dX, dW),
-                                             budget_bytes=args.budget, schedule=args.schedule)
-                return l
-            l, _, _ = dpm.forward_backward(Xs, W, ts, n_valid_global=n_valid_global, workspace=ws,
-                                           out=(loss, dX, dW))
+            l, _, _ = slf.lce_fwd_bwd_dp(Xs, W, ts, dp_comm, sync_dweight=True, workspace=ws, out=(loss, dX, dW),
+                                         budget_bytes=args.budget, schedule=args.schedule)
             return l
         if native:  # a P2P timeout poisons the loss; checked once after the timed region
             l, _, _ = slf.lce_fwd_bwd_sharded(Xs, W, ts, V, comm, workspace=ws, out=(loss, dX, dW),
@@ -592,8 +579,7 @@ def main():
                    "l2": "inputs larger than L2 (W alone is %.2f GB vs 126 MB L2); no flush" % (V_l * H * 2 / 1e9),
                    "plan": slf.sharded_plan_describe(N, H, V, G, 0 if G != g else rank, args.budget) if native else
                    slf.plan_describe(N_l, H, V_l, budget_bytes=ws_budget, schedule=args.schedule),
-                   **({"comm": ("native (slf_lce_fwd_bwd_dp, slf_comm NCCL)" if dp_comm is not None else
-                                (comm_note or "torch.distributed NCCL (TokenShardedLCE)"))} if dp else {}),
+                   **({"comm": "native (slf_lce_fwd_bwd_dp, slf_comm NCCL)"} if dp else {}),
                    **({"comm": comm_note if (native and comm_note) else
                        ("native (slf_comm NCCL inside libslf_lce.so" + (", P2P statistics all-gather" if
                                 args.p2p_stats else "") + (", P2P dX exchange kernel" if args.p2p_dx else "") + ")")

@@ -211,11 +211,17 @@ __global__ void __launch_bounds__(256) mref_kernel(const uint16_t* __restrict__ 
   if (lane == 0) mref[row] = acc + STASH_REF_SHIFT;
 }
 
-// One block per row of the chunk (single GPU): the row's lse / loss / RowStat from its tile
-// partials (as combine_transform), then the row factor f_i and X'_i = bf16(f_i * x_i).  The stash
-// is not touched, except for rare rows where the per-row reference does not fit (a tile kept its
-// own max, or f_i is outside [1e-30, 1e30]): those are rescaled in place to G_P tile by tile and get
-// f_i = 1, X'_i = x_i.  xs may alias xrows (the fused RMSNorm's y buffer): each block owns its row.
+// 16 rows per block of 256 threads (single GPU): each row's lse / loss / RowStat from its tile
+// partials — 16 lanes per row merge interleaved tiles (lane p: tiles p, p+16, ...; for a fixed tile
+// the 16 rows' lanes read 16 consecutive partials), then one thread per row merges the 16 lane
+// results in lane order (fixed, deterministic) — then the row factor f_i and, by the whole block,
+// X'_i = bf16(f_i * x_i) for its 16 rows (16-byte coalesced).  The stash is not touched, except
+// for rare rows where the per-row reference does not fit (a tile kept its own max, or f_i is
+// outside [1e-30, 1e30]): those are rescaled in place to G_P tile by tile and get f_i = 1,
+// X'_i = x_i.  xs may alias xrows (the fused RMSNorm's y buffer): each row is read then written by
+// the same thread.
+constexpr int CS_ROWS = 16, CS_LANES = 16;
+
 __global__ void __launch_bounds__(256) combine_scale_kernel(
     const float2* __restrict__ partials, int tiles, int rows, const float* __restrict__ zt,
     const int32_t* __restrict__ t, int64_t V_l, int64_t ld_stash, int32_t ignore_index, int reduction, float scale,
@@ -223,105 +229,115 @@ __global__ void __launch_bounds__(256) combine_scale_kernel(
     slf_rowstat* __restrict__ rowstat, uint16_t* __restrict__ stash, uint16_t* __restrict__ stash2, int split,
     const float* __restrict__ mref, float* __restrict__ fac, const uint16_t* xrows, uint16_t* xs, int64_t H,
     RmsStep rms) {
-  extern __shared__ float r_t[];  // [tiles]: the tile maxima m_t
+  extern __shared__ float r_t[];  // [tiles]: per-tile factors of a fallback row
   griddep_launch_dependents();
   griddep_wait();  // PDL: everything below reads the previous kernel's outputs
-  if ((int)blockIdx.x >= rows) {  // the fused final RMSNorm's jobs riding in this launch (rmsnorm.cuh)
-    rms_block(rms, (int64_t)blockIdx.x - rows);
+  const int nblk = (rows + CS_ROWS - 1) / CS_ROWS;
+  if ((int)blockIdx.x >= nblk) {  // the fused final RMSNorm's jobs riding in this launch (rmsnorm.cuh)
+    rms_block(rms, (int64_t)blockIdx.x - nblk);
     return;
   }
-  __shared__ float sLse, sF, sCoef, wm[8], ws[8];
-  __shared__ int sFb;
-  const int i = blockIdx.x;
+  __shared__ float lm[CS_LANES][CS_ROWS], ls[CS_LANES][CS_ROWS];
+  __shared__ int lfb[CS_LANES][CS_ROWS];
+  __shared__ float sF[CS_ROWS], sLse[CS_ROWS], sCg[CS_ROWS];
+  __shared__ int sFb[CS_ROWS];
   const int tid = threadIdx.x;
-  const float M = mref[i];
-  float m = -INFINITY, sum = 0.f;
-  int fb = 0;
-  for (int k = tid; k < tiles; k += 256) {
-    const float2 p = partials[(size_t)k * rows + i];
-    r_t[k] = p.x;
-    fb |= (p.x - M > STASH_REF_SLACK) ? 1 : 0;
-    const float nm = fmaxf(m, p.x);
-    sum = sum * ex2((m - nm) * LOG2E) + p.y * ex2((p.x - nm) * LOG2E);
-    m = nm;
-  }
-  fb = __syncthreads_or(fb);
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) {
-    const float om = __shfl_down_sync(0xffffffffu, m, o), os = __shfl_down_sync(0xffffffffu, sum, o);
-    const float nm = fmaxf(m, om);
-    sum = (m == -INFINITY ? 0.f : sum * ex2((m - nm) * LOG2E)) + (om == -INFINITY ? 0.f : os * ex2((om - nm) * LOG2E));
-    m = nm;
-  }
-  if ((tid & 31) == 0) {
-    wm[tid >> 5] = m;
-    ws[tid >> 5] = sum;
+  const int rl = tid % CS_ROWS, lane = tid / CS_ROWS;
+  const int i0 = blockIdx.x * CS_ROWS;
+  {
+    const int i = i0 + rl;
+    float m = -INFINITY, sum = 0.f;
+    int fb = 0;
+    if (i < rows) {
+      const float M = mref[i];
+      for (int k = lane; k < tiles; k += CS_LANES) {
+        const float2 p = partials[(size_t)k * rows + i];
+        fb |= (p.x - M > STASH_REF_SLACK) ? 1 : 0;
+        const float nm = fmaxf(m, p.x);
+        sum = (m == -INFINITY ? 0.f : sum * ex2((m - nm) * LOG2E)) + p.y * ex2((p.x - nm) * LOG2E);
+        m = nm;
+      }
+    }
+    lm[lane][rl] = m;
+    ls[lane][rl] = sum;
+    lfb[lane][rl] = fb;
   }
   __syncthreads();
-  if (tid == 0) {
-    float Mx = -INFINITY, S = 0.f, z = 0.f;
+  if (tid < CS_ROWS && i0 + tid < rows) {  // one thread per row: lanes in order
+    const int i = i0 + tid;
+    float Mx = -INFINITY, S = 0.f;
+    int fb = 0;
+    for (int p = 0; p < CS_LANES; ++p) {
+      Mx = fmaxf(Mx, lm[p][tid]);
+      fb |= lfb[p][tid];
+    }
+    for (int p = 0; p < CS_LANES; ++p)
+      if (lm[p][tid] != -INFINITY) S += ls[p][tid] * ex2((lm[p][tid] - Mx) * LOG2E);
     const int32_t tt = t[i];
-    for (int k = 0; k < 8; ++k) Mx = fmaxf(Mx, wm[k]);
-    for (int k = 0; k < 8; ++k)
-      if (wm[k] != -INFINITY) S += ws[k] * ex2((wm[k] - Mx) * LOG2E);
-    if (tt != ignore_index && tt >= 0 && (int64_t)tt < V_l) z = zt[i];
-    const float lse = Mx + logf(S);
     const bool valid = tt != ignore_index;
     const bool bad = valid && (tt < 0 || (int64_t)tt >= V_l);
+    const float z = (valid && !bad) ? zt[i] : 0.f;
+    const float lse = Mx + logf(S);
     const float coef = (valid && !bad) ? coef_of(reduction, scale, hdr->n_valid) : 0.f;
     float l = valid ? (lse - z) : 0.f;
     if (bad) l = __int_as_float(0x7fc00000);
     loss_rows[i] = l;
-    const int32_t tloc = (valid && !bad) ? tt : -1;
-    rowstat[i] = slf_rowstat{lse * LOG2E, coef, tloc, valid ? 1 : 0};
+    rowstat[i] = slf_rowstat{lse * LOG2E, coef, (valid && !bad) ? tt : -1, valid ? 1 : 0};
     const float cg = coef * grad_scale;
     float f = 0.f;
-    int rfb = fb;
     if (cg != 0.f) {
-      f = cg * ex2((M - lse) * LOG2E);
-      if (!(fabsf(f) >= 1e-30f && fabsf(f) <= 1e30f)) rfb = 1;
+      f = cg * ex2((mref[i] - lse) * LOG2E);
+      if (!(fabsf(f) >= 1e-30f && fabsf(f) <= 1e30f)) fb = 1;
     }
-    sLse = lse;
-    sCoef = cg;
-    sFb = rfb;
-    sF = rfb ? 1.f : f;
-    fac[i] = rfb ? 1.f : f;
+    sLse[tid] = lse;
+    sCg[tid] = cg;
+    sFb[tid] = fb;
+    sF[tid] = fb ? 1.f : f;
+    fac[i] = fb ? 1.f : f;
   }
   __syncthreads();
-  const float f = sF;
-  if (sFb) {  // rare: rescale this stash row in place to G_P, tile by tile
-    const float lse = sLse, cg = sCoef;
+  for (int r = 0; r < CS_ROWS && i0 + r < rows; ++r) {  // rare: rescale a stash row in place to G_P
+    if (!sFb[r]) continue;
+    const int i = i0 + r;
+    const float M = mref[i], lse = sLse[r], cg = sCg[r];
     for (int k = tid; k < tiles; k += 256) {
-      const float mt = r_t[k];
-      float r;
-      if (mt - M > STASH_REF_SLACK) r = cg * ex2((mt - lse) * LOG2E);          // tile stored exp(z - m_t)
-      else if (M - mt > 80.f) r = 0.f;                                         // its entries < e^-40 of the max
-      else r = cg * ex2((M - mt) * LOG2E) * ex2((mt - lse) * LOG2E);            // stored exp(z - M)
-      r_t[k] = r;
+      const float mt = partials[(size_t)k * rows + i].x;
+      float f;
+      if (mt - M > STASH_REF_SLACK) f = cg * ex2((mt - lse) * LOG2E);  // the tile stored exp(z - m_t)
+      else if (M - mt > 80.f) f = 0.f;                                 // its entries < e^-40 of the max
+      else f = cg * ex2((M - mt) * LOG2E) * ex2((mt - lse) * LOG2E);    // it stored exp(z - M)
+      r_t[k] = f;
     }
     __syncthreads();
     uint4* row = reinterpret_cast<uint4*>(i < split ? stash + (size_t)i * ld_stash
                                                     : stash2 + (size_t)(i - split) * ld_stash);
     const int64_t groups = (V_l + 7) / 8;
     for (int64_t q = tid; q < groups; q += 256) {
-      const float r = r_t[(q * 8) / 256];
+      const float f = r_t[(q * 8) / 256];
       uint4 x = row[q];
-      x.x = pack_bf16x2(bf16lo_to_f32(x.x) * r, bf16hi_to_f32(x.x) * r);
-      x.y = pack_bf16x2(bf16lo_to_f32(x.y) * r, bf16hi_to_f32(x.y) * r);
-      x.z = pack_bf16x2(bf16lo_to_f32(x.z) * r, bf16hi_to_f32(x.z) * r);
-      x.w = pack_bf16x2(bf16lo_to_f32(x.w) * r, bf16hi_to_f32(x.w) * r);
+      x.x = pack_bf16x2(bf16lo_to_f32(x.x) * f, bf16hi_to_f32(x.x) * f);
+      x.y = pack_bf16x2(bf16lo_to_f32(x.y) * f, bf16hi_to_f32(x.y) * f);
+      x.z = pack_bf16x2(bf16lo_to_f32(x.z) * f, bf16hi_to_f32(x.z) * f);
+      x.w = pack_bf16x2(bf16lo_to_f32(x.w) * f, bf16hi_to_f32(x.w) * f);
       row[q] = x;
     }
+    __syncthreads();
   }
-  // X'_i = bf16(f * x_i) (f = 1 for the rescaled rows: an exact copy)
-  const uint4* xr = reinterpret_cast<const uint4*>(xrows + (size_t)i * H);
-  uint4* xo = reinterpret_cast<uint4*>(xs + (size_t)i * H);
-  for (int64_t q = tid; q < H / 8; q += 256) {
-    const uint4 x = xr[q];
-    xo[q] = make_uint4(pack_bf16x2(bf16lo_to_f32(x.x) * f, bf16hi_to_f32(x.x) * f),
-                       pack_bf16x2(bf16lo_to_f32(x.y) * f, bf16hi_to_f32(x.y) * f),
-                       pack_bf16x2(bf16lo_to_f32(x.z) * f, bf16hi_to_f32(x.z) * f),
-                       pack_bf16x2(bf16lo_to_f32(x.w) * f, bf16hi_to_f32(x.w) * f));
+  // X'_i = bf16(f * x_i) for the block's rows (f = 1 for the rescaled rows: an exact copy); none
+  // without a dW GEMM
+  if (!xs) return;
+  const int64_t per_row = H / 8;
+  const int nr = min(CS_ROWS, rows - i0);
+  for (int64_t q = tid; q < (int64_t)nr * per_row; q += 256) {
+    const int r = (int)(q / per_row);
+    const int64_t c = q - (int64_t)r * per_row;
+    const float f = sF[r];
+    const uint4 x = reinterpret_cast<const uint4*>(xrows + (size_t)(i0 + r) * H)[c];
+    reinterpret_cast<uint4*>(xs + (size_t)(i0 + r) * H)[c] =
+        make_uint4(pack_bf16x2(bf16lo_to_f32(x.x) * f, bf16hi_to_f32(x.x) * f),
+                   pack_bf16x2(bf16lo_to_f32(x.y) * f, bf16hi_to_f32(x.y) * f),
+                   pack_bf16x2(bf16lo_to_f32(x.z) * f, bf16hi_to_f32(x.z) * f),
+                   pack_bf16x2(bf16lo_to_f32(x.w) * f, bf16hi_to_f32(x.w) * f));
   }
 }
 

@@ -910,8 +910,8 @@ struct SChunk {
   uint8_t* xt = nullptr;  // X_chunk^T [H][ld_xt] (dW's B operand K-major) in free dhidden rows, or nullptr
   int64_t ld_xt = 0;
   const uint8_t* xrows = nullptr;  // the chunk's hidden rows when not X + r0 (fused RMSNorm: its y buffer)
-  uint8_t* xs = nullptr;  // per-row stash reference: X'_chunk = bf16(f ⊙ X) [rows][H], the
-                          // dW GEMM's B operand; null: the stash is rescaled in place (combine_transform)
+  bool ref = false;       // per-row stash reference; false: the stash is rescaled in place
+  uint8_t* xs = nullptr;  // with ref and dW: X'_chunk = bf16(f ⊙ X) [rows][H], the dW GEMM's B operand
 };
 
 SChunk s_plain_chunk(const Plan& p, int64_t N, int64_t ch) {
@@ -958,7 +958,7 @@ slf_status s_chunk_stats(Ctx& c, const SArgs& a, const SChunk& k, slf_shardstat*
   g.zt = zt + r0;
   g.out = c.ws + p.off_stash;
   g.ld_out = p.ld_stash;
-  if (k.xs) g.mref = reinterpret_cast<const float*>(c.ws + p.off_mref) + r0;
+  if (k.ref) g.mref = reinterpret_cast<const float*>(c.ws + p.off_mref) + r0;
   static const int dbg = getenv("SLF_DEBUG_EPI") ? atoi(getenv("SLF_DEBUG_EPI")) : 0;
   g.mode = (dbg & 64) ? 32 : 0;  // timing experiment only (SLF_DEBUG_EPI=64): skip the stash stores
   g.tma_out = 1;      // the stash is written through TMA-staged stores
@@ -1011,7 +1011,7 @@ slf_status s_build_bwd(Ctx& c, const SArgs& a, const SChunk& k, void* dXc, int d
     q.a.out = dXc;
     q.a.ld_out = a.H;
     q.a.mode = dx_fp32 ? 1 : 0;
-    if (k.xs) q.a.fac = reinterpret_cast<const float*>(c.ws + p.off_fac) + r0;
+    if (k.ref) q.a.fac = reinterpret_cast<const float*>(c.ws + p.off_fac) + r0;
     finish_geometry(q.a, cg);
   }
   if (dW) {  // dW (+)= G_P^T X_chunk : A = G_P^T (MN-major; K = rows split ws | ext), B = X_chunk (MN-major)
@@ -1065,10 +1065,10 @@ slf_status s_chunk_bwd(Ctx& c, const SArgs& a, const SChunk& k, const slf_shards
   const int64_t r0 = k.r0, rows = k.rows;
   const int tiles_v = (int)((a.V_l + BN - 1) / BN);
   static const bool skip_ct = getenv("SLF_DEBUG_EPI") && (atoi(getenv("SLF_DEBUG_EPI")) & 512);  // timing only
-  if (k.xs && !skip_ct) {  // per-row stash reference: factors and X'_chunk, the stash stays as is
+  if (k.ref && !skip_ct) {  // per-row stash reference: factors and X'_chunk, the stash stays as is
     ProfScope ps(SLF_PROF_COMBINE_TRANSFORM, c.s, 0.0, (double)rows * (tiles_v * 8.0 + a.H * 4.0 + 40.0));
     cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3((unsigned)(rows + (rms ? rms_blocks_of(*rms) : 0)));
+    cfg.gridDim = dim3((unsigned)((rows + CS_ROWS - 1) / CS_ROWS + (rms ? rms_blocks_of(*rms) : 0)));
     cfg.blockDim = dim3(256);
     cfg.dynamicSmemBytes = tiles_v * sizeof(float);
     cfg.stream = c.s;
@@ -1245,7 +1245,7 @@ RmsStep rms_jobs(const SArgs& a, const RmsFuse& rf, void* dX, const std::vector<
     r.f_r0 = ch[cf].r0;
     r.f_rows = ch[cf].rows;
     r.ybuf = reinterpret_cast<uint16_t*>(rf.ybuf[cf & 1]);
-    if (ch[cf].xs) {  // the chunk's per-row stash reference from its y rows
+    if (ch[cf].ref) {  // the chunk's per-row stash reference from its y rows
       r.W = reinterpret_cast<const uint16_t*>(a.W);
       r.t = a.t;
       r.ignore_index = a.ign;
@@ -1297,15 +1297,21 @@ slf_status phase_s(Ctx& c, const void* X, const void* W, const int32_t* t, int64
     for (auto& k : chunks) {  // the chunk's y rows (dW's B operand too); no X^T variant
       k.xrows = rf->ybuf[k.index & 1];
       k.xt = nullptr;
-      if (!classic && dX) k.xs = rf->ybuf[k.index & 1];
-      any_ref |= k.xs != nullptr;
+      k.ref = !classic;
+      if (k.ref && dW) k.xs = rf->ybuf[k.index & 1];
+      any_ref |= k.ref;
     }
-  else if (!classic && dX && dW)
+  else if (!classic && dX)
     for (auto& k : chunks) {
+      if (k.xt) continue;
+      if (!dW) {  // dX only: no X' needed (the same numerics as with dW, so dX is the same bits)
+        k.ref = any_ref = true;
+        continue;
+      }
       const size_t lo = align_up((size_t)(k.r0 + k.rows) * H * 2 + (size_t)k.ext * p.ld_stash * 2, 1024);
-      if (!k.xt && lo + (size_t)k.rows * H * 2 <= (size_t)N * H * 2) {
+      if (lo + (size_t)k.rows * H * 2 <= (size_t)N * H * 2) {
         k.xs = reinterpret_cast<uint8_t*>(dX) + lo;
-        any_ref = true;
+        k.ref = any_ref = true;
       }
     }
   // M_i = x_i . W[t_i] + shift: for every row at once when the inputs are resident; chunk by chunk,
@@ -1357,7 +1363,7 @@ slf_status phase_s(Ctx& c, const void* X, const void* W, const int32_t* t, int64
     if (c.chunk_ready && i <= 2)
       SLF_CUDA(cudaStreamWaitEvent(c.s, c.chunk_ready[i < 2 ? i : chunks.size() - 1], 0));
     if (k.xt && dW) SLF_TRY(launch_transpose_x(c, a, k));
-    if (mref_per_chunk && k.xs) SLF_TRY(launch_mref(k.r0, k.rows));
+    if (mref_per_chunk && k.ref) SLF_TRY(launch_mref(k.r0, k.rows));
     if (rf && i == 0) SLF_TRY(launch_rms_step(c, rms_jobs(a, *rf, dX, chunks, -1, -1, 0, -1)));  // y of chunk 0
     SLF_TRY(s_chunk_stats(c, a, k, nullptr));
     const int64_t ki = (int64_t)i;

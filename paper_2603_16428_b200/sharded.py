@@ -194,72 +194,3 @@ class VocabShardedLCE:
 def token_bounds(N: int, g: int, rank: int):
     """Contiguous, as-even-as-possible token rows [n0, n1) of `rank` among `g` data-parallel ranks."""
     return shard_bounds(N, g, rank)
-
-
-def fused_ops():
-    from . import lce
-    return types.SimpleNamespace(lce_fwd_bwd=lce.lce_fwd_bwd)
-
-
-class TokenShardedLCE:
-    """Data-parallel (token-sharded) LCE, SURVEY §8(e) "alternative partition" / §8(f) NEXT-3.
-
-    Rank k holds its own tokens X_k [N_k, H], t_k and a full copy of W.  No collective runs inside
-    the LCE: each rank runs the fused single-GPU call with reduction SUM and
-    scale' = scale / n_valid_global for MEAN (the denominator must be global), then
-      loss  = all_reduce(sum of local losses) (/ n_valid_global for MEAN),
-      dW    = all_reduce(local dW)   — the ordinary data-parallel gradient sync (bf16 on the GPU),
-      dX_k  stays local.
-    n_valid_global comes from one int64 all-reduce of the local valid counts (a host read), unless
-    the caller passes it (it is known when the batch is built).  Communication per step is V*H*2
-    bytes (dW) against N*H*4 (dX fp32) for vocab sharding, so this mode wins when 2N > V
-    (e.g. Mistral-Large, V = 32768).  reduction NONE returns the local per-token losses.
-    """
-
-    def __init__(self, group=None, ops=None, budget_bytes: int = 0, schedule: str = "auto",
-                 sync_dweight: bool = True):
-        import torch.distributed as dist
-        self.dist = dist
-        self.group = group
-        self.g = dist.get_world_size(group)
-        self.rank = dist.get_rank(group)
-        self.ops = ops or fused_ops()
-        self.budget = budget_bytes
-        self.schedule = schedule
-        self.sync_dweight = sync_dweight
-
-    def n_valid_global(self, t, ignore_index: int = -100) -> int:
-        import torch
-        n = (t != ignore_index).sum().to(torch.int64).reshape(1)
-        self.dist.all_reduce(n, group=self.group)
-        return int(n.item())
-
-    def forward_backward(self, X_local, W, t_local, ignore_index: int = -100, reduction: str = "mean",
-                         scale: float = 1.0, n_valid_global: int | None = None, workspace=None, out=None):
-        """Returns (loss, dX_local [N_k, H], dW [V, H] summed over ranks)."""
-        if reduction not in ("sum", "mean", "none"):
-            raise ValueError(f"bad reduction {reduction!r}")
-        s, inv_nv = scale, 1.0
-        if reduction == "mean":
-            nv = self.n_valid_global(t_local, ignore_index) if n_valid_global is None else int(n_valid_global)
-            inv_nv = 0.0 if nv == 0 else 1.0 / nv  # DESIGN.md R2: MEAN over no valid token is 0
-            s = scale * inv_nv
-        kw = dict(ignore_index=ignore_index, reduction="none" if reduction == "none" else "sum", scale=s)
-        if workspace is not None:
-            kw["workspace"] = workspace
-        if out is not None:
-            kw["out"] = out
-        if self.budget:
-            kw["budget_bytes"] = self.budget
-        if self.schedule != "auto":
-            kw["schedule"] = self.schedule
-        loss, dX, dW = self.ops.lce_fwd_bwd(X_local, W, t_local, **kw)
-        if reduction != "none":
-            lv = loss.reshape(1)
-            self.dist.all_reduce(lv, group=self.group)
-            if reduction == "mean":
-                lv.mul_(inv_nv)
-            loss = lv[0]
-        if self.sync_dweight:
-            self.dist.all_reduce(dW, group=self.group)
-        return loss, dX, dW
