@@ -228,7 +228,8 @@ __global__ void __launch_bounds__(256) combine_scale_kernel(
     float grad_scale, const WsHeader* __restrict__ hdr, float* __restrict__ loss_rows,
     slf_rowstat* __restrict__ rowstat, uint16_t* __restrict__ stash, uint16_t* __restrict__ stash2, int split,
     const float* __restrict__ mref, float* __restrict__ fac, const uint16_t* xrows, uint16_t* xs, int64_t H,
-    RmsStep rms) {
+    int64_t ld_xst, RmsStep rms) {
+  // ld_xst > 0: X' is written transposed, X'^T [H][ld_xst] (the dW GEMM's B operand K-major)
   extern __shared__ float r_t[];  // [tiles]: per-tile factors of a fallback row
   griddep_launch_dependents();
   griddep_wait();  // PDL: everything below reads the previous kernel's outputs
@@ -326,8 +327,27 @@ __global__ void __launch_bounds__(256) combine_scale_kernel(
   // X'_i = bf16(f * x_i) for the block's rows (f = 1 for the rescaled rows: an exact copy); none
   // without a dW GEMM
   if (!xs) return;
-  const int64_t per_row = H / 8;
   const int nr = min(CS_ROWS, rows - i0);
+  if (ld_xst > 0) {  // X'^T[h][i0 .. i0 + nr): 32 contiguous bytes per column h (two 16-byte stores)
+    for (int64_t h = tid; h < H; h += 256) {
+      uint32_t w[CS_ROWS / 2];
+#pragma unroll
+      for (int r = 0; r < CS_ROWS; r += 2) {
+        const float a = r < nr ? bf16_bits_to_f32(xrows[(size_t)(i0 + r) * H + h]) * sF[r] : 0.f;
+        const float b = r + 1 < nr ? bf16_bits_to_f32(xrows[(size_t)(i0 + r + 1) * H + h]) * sF[r + 1] : 0.f;
+        w[r / 2] = pack_bf16x2(a, b);
+      }
+      uint16_t* dst = xs + (size_t)h * ld_xst + i0;
+      if (nr == CS_ROWS) {
+        reinterpret_cast<uint4*>(dst)[0] = make_uint4(w[0], w[1], w[2], w[3]);
+        reinterpret_cast<uint4*>(dst)[1] = make_uint4(w[4], w[5], w[6], w[7]);
+      } else {
+        for (int r = 0; r < nr; ++r) dst[r] = (uint16_t)(w[r / 2] >> ((r & 1) * 16));
+      }
+    }
+    return;
+  }
+  const int64_t per_row = H / 8;
   for (int64_t q = tid; q < (int64_t)nr * per_row; q += 256) {
     const int r = (int)(q / per_row);
     const int64_t c = q - (int64_t)r * per_row;

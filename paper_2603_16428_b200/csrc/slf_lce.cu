@@ -1084,7 +1084,8 @@ slf_status s_chunk_bwd(Ctx& c, const SArgs& a, const SChunk& k, const slf_shards
         (const WsHeader*)hdr_of(c.ws), loss_rows_all + r0, reinterpret_cast<slf_rowstat*>(c.ws + p.off_rowstat) + r0,
         reinterpret_cast<uint16_t*>(c.ws + p.off_stash), reinterpret_cast<uint16_t*>(k.ext_base), (int)(rows - k.ext),
         reinterpret_cast<const float*>(c.ws + p.off_mref) + r0, reinterpret_cast<float*>(c.ws + p.off_fac) + r0,
-        reinterpret_cast<const uint16_t*>(xr), reinterpret_cast<uint16_t*>(k.xs), a.H, rms ? *rms : RmsStep{}));
+        reinterpret_cast<const uint16_t*>(xr), reinterpret_cast<uint16_t*>(k.xt ? k.xt : k.xs), a.H,
+        k.xt ? k.ld_xt : 0, rms ? *rms : RmsStep{}));
   } else if (!skip_ct) {
     ProfScope ps(SLF_PROF_COMBINE_TRANSFORM, c.s, 0.0, (double)rows * (tiles_v * 8.0 + a.V_l * 4.0 + 16.0 * g + 24));
     // Programmatic dependent launch: blocks start while the stash GEMM drains and wait in-kernel.
@@ -1301,19 +1302,29 @@ slf_status phase_s(Ctx& c, const void* X, const void* W, const int32_t* t, int64
       if (k.ref && dW) k.xs = rf->ybuf[k.index & 1];
       any_ref |= k.ref;
     }
-  else if (!classic && dX)
+  else if (!classic && dX) {
+    // X' is written transposed (X'^T [H][rows rounded to 8]: dW's B operand K-major, one MN-major
+    // operand instead of two) unless SLF_XS_T=0
+    static const bool xs_t = !(getenv("SLF_XS_T") && atoi(getenv("SLF_XS_T")) == 0);
     for (auto& k : chunks) {
-      if (k.xt) continue;
-      if (!dW) {  // dX only: no X' needed (the same numerics as with dW, so dX is the same bits)
-        k.ref = any_ref = true;
-        continue;
-      }
+      // the chunk takes the reference where X' fits — with or without dW, so that a dX-only call
+      // runs the same numerics chunk by chunk (and returns the same bits) as a dX + dW call
       const size_t lo = align_up((size_t)(k.r0 + k.rows) * H * 2 + (size_t)k.ext * p.ld_stash * 2, 1024);
-      if (lo + (size_t)k.rows * H * 2 <= (size_t)N * H * 2) {
-        k.xs = reinterpret_cast<uint8_t*>(dX) + lo;
+      const int64_t ld = (k.rows + 7) / 8 * 8;
+      const size_t need = xs_t ? (size_t)H * ld * 2 : (size_t)k.rows * H * 2;
+      if (lo + need <= (size_t)N * H * 2) {
+        k.xt = nullptr;
         k.ref = any_ref = true;
+        if (!dW) continue;
+        if (xs_t) {
+          k.xt = reinterpret_cast<uint8_t*>(dX) + lo;
+          k.ld_xt = ld;
+        } else {
+          k.xs = reinterpret_cast<uint8_t*>(dX) + lo;
+        }
       }
     }
+  }
   // M_i = x_i . W[t_i] + shift: for every row at once when the inputs are resident; chunk by chunk,
   // after the chunk's rows arrived, in the host-input call
   auto launch_mref = [&](int64_t r0, int64_t rows) -> slf_status {
@@ -1362,7 +1373,7 @@ slf_status phase_s(Ctx& c, const void* X, const void* W, const int32_t* t, int64
     // dependent launch overlap of the kernel after it.
     if (c.chunk_ready && i <= 2)
       SLF_CUDA(cudaStreamWaitEvent(c.s, c.chunk_ready[i < 2 ? i : chunks.size() - 1], 0));
-    if (k.xt && dW) SLF_TRY(launch_transpose_x(c, a, k));
+    if (k.xt && dW && !k.ref) SLF_TRY(launch_transpose_x(c, a, k));
     if (mref_per_chunk && k.ref) SLF_TRY(launch_mref(k.r0, k.rows));
     if (rf && i == 0) SLF_TRY(launch_rms_step(c, rms_jobs(a, *rf, dX, chunks, -1, -1, 0, -1)));  // y of chunk 0
     SLF_TRY(s_chunk_stats(c, a, k, nullptr));
