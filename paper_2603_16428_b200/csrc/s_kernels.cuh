@@ -211,16 +211,16 @@ __global__ void __launch_bounds__(256) mref_kernel(const uint16_t* __restrict__ 
   if (lane == 0) mref[row] = acc + STASH_REF_SHIFT;
 }
 
-// 16 rows per block of 256 threads (single GPU): each row's lse / loss / RowStat from its tile
-// partials — 16 lanes per row merge interleaved tiles (lane p: tiles p, p+16, ...; for a fixed tile
-// the 16 rows' lanes read 16 consecutive partials), then one thread per row merges the 16 lane
-// results in lane order (fixed, deterministic) — then the row factor f_i and, by the whole block,
-// X'_i = bf16(f_i * x_i) for its 16 rows (16-byte coalesced).  The stash is not touched, except
+// CS_ROWS = 4 rows per block of 256 threads (single GPU): each row's lse / loss / RowStat from its
+// tile partials — 64 lanes per row merge interleaved tiles (lane p: tiles p, p+64, ...; for a fixed
+// tile the 4 rows' lanes read 4 consecutive partials, one 32-byte sector), then one thread per row
+// merges the 64 lane results in lane order (fixed, deterministic) — then the row factor f_i and, by
+// the whole block, X'_i = bf16(f_i * x_i) for its rows.  The stash is not touched, except
 // for rare rows where the per-row reference does not fit (a tile kept its own max, or f_i is
 // outside [1e-30, 1e30]): those are rescaled in place to G_P tile by tile and get f_i = 1,
 // X'_i = x_i.  xs may alias xrows (the fused RMSNorm's y buffer): each row is read then written by
 // the same thread.
-constexpr int CS_ROWS = 16, CS_LANES = 16;
+constexpr int CS_ROWS = 4, CS_LANES = 64;
 
 __global__ void __launch_bounds__(256) combine_scale_kernel(
     const float2* __restrict__ partials, int tiles, int rows, const float* __restrict__ zt,
@@ -328,9 +328,10 @@ __global__ void __launch_bounds__(256) combine_scale_kernel(
   // without a dW GEMM
   if (!xs) return;
   const int nr = min(CS_ROWS, rows - i0);
-  if (ld_xst > 0) {  // X'^T[h][i0 .. i0 + nr): 32 contiguous bytes per column h (two 16-byte stores)
+  if (ld_xst > 0) {  // X'^T[h][i0 .. i0 + nr): 8 contiguous bytes per column h
+    static_assert(CS_ROWS == 4, "one 8-byte store per column");
     for (int64_t h = tid; h < H; h += 256) {
-      uint32_t w[CS_ROWS / 2];
+      uint32_t w[2];
 #pragma unroll
       for (int r = 0; r < CS_ROWS; r += 2) {
         const float a = r < nr ? bf16_bits_to_f32(xrows[(size_t)(i0 + r) * H + h]) * sF[r] : 0.f;
@@ -339,8 +340,7 @@ __global__ void __launch_bounds__(256) combine_scale_kernel(
       }
       uint16_t* dst = xs + (size_t)h * ld_xst + i0;
       if (nr == CS_ROWS) {
-        reinterpret_cast<uint4*>(dst)[0] = make_uint4(w[0], w[1], w[2], w[3]);
-        reinterpret_cast<uint4*>(dst)[1] = make_uint4(w[4], w[5], w[6], w[7]);
+        *reinterpret_cast<uint2*>(dst) = make_uint2(w[0], w[1]);
       } else {
         for (int r = 0; r < nr; ++r) dst[r] = (uint16_t)(w[r / 2] >> ((r & 1) * 16));
       }
