@@ -437,18 +437,19 @@ def test_rmsnorm_lce_parity(slf, sched, fused, N, H, V, budget):
 @pytest.mark.parametrize("red", ["mean", "none"])
 def test_rmsnorm_lce_fused_matches_composition(slf, red):
     """The fused call forms exactly the composition's y (same fp32 ops, same bf16 rounding) and runs
-    the same chunk plan: the loss is bit-identical to rmsnorm_fwd -> lce_fwd_bwd -> rmsnorm_bwd (the
-    statistics do not depend on how the stash is scaled).  dx, dW, dg agree to bf16 rounding: the
-    fused call writes X' over its y buffer in every chunk, the composition into
-    dhidden's free rows where they fit, so its last chunk rescales the stash instead, and dg groups
-    its fp32 row sums differently."""
+    the same chunk plan, so the per-tile statistics are the same bits; the loss agrees to fp32
+    rounding (the two combine kernels merge a row's tile statistics in different fixed orders).
+    dx, dW, dg agree to bf16 rounding: the fused call writes X' over its y buffer in every chunk
+    (DESIGN.md §5d), the composition into dhidden's free rows where they fit, so its last chunk
+    rescales the stash instead, and dg groups its fp32 row sums differently."""
     inp = synth.make_inputs(3000, 512, 2000, seed=27, alpha=3.0, dist="zipf")
     x, W, t = to_dev(inp, torch)
     g = (1 + 0.1 * torch.randn(512, generator=torch.Generator().manual_seed(1))).to(torch.bfloat16).cuda()
     a = slf.rmsnorm_lce_fwd_bwd(x, g, W, t, reduction=red, schedule="S", fused=True)
     b = slf.rmsnorm_lce_fwd_bwd(x, g, W, t, reduction=red, schedule="S", fused=False)
     torch.cuda.synchronize()
-    assert torch.equal(a[0].view(-1), b[0].view(-1))
+    la, lb = a[0].view(-1).double().cpu().numpy(), b[0].view(-1).double().cpu().numpy()
+    assert np.max(np.abs(la - lb)) <= 1e-6 * np.max(np.abs(lb))
     assert rel_max_err(bf16_to_np64(a[1]), bf16_to_np64(b[1])) < 1e-2
     assert rel_max_err(bf16_to_np64(a[3]), bf16_to_np64(b[3])) < 1e-2
     assert rel_max_err(a[2].cpu().numpy(), b[2].cpu().numpy()) < 1e-2
