@@ -183,17 +183,19 @@ __global__ void __launch_bounds__(256) combine_transform_kernel(
 constexpr float STASH_REF_SHIFT = 40.f;
 
 // One warp per row: M_i = x_i . W[t_i - vocab_start] + STASH_REF_SHIFT (fp32, 16-byte loads).
+// partial = 1 (vocab shards): this shard's target-logit contribution (0 for targets elsewhere), to be
+// summed across shards and finished by mref_finish_kernel.
 __global__ void __launch_bounds__(256) mref_kernel(const uint16_t* __restrict__ X, const uint16_t* __restrict__ W,
                                                   const int32_t* __restrict__ t, int64_t N, int64_t H,
                                                   int32_t ignore_index, int64_t vocab_start, int64_t V_l,
-                                                  float* __restrict__ mref) {
+                                                  float* __restrict__ mref, int partial = 0) {
   const int64_t row = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   if (row >= N) return;
   const int32_t tt = t[row];
   const int64_t loc = (int64_t)tt - vocab_start;
   if (tt == ignore_index || loc < 0 || loc >= V_l) {
-    if (lane == 0) mref[row] = INFINITY;
+    if (lane == 0) mref[row] = partial ? 0.f : INFINITY;
     return;
   }
   const uint4* xr = reinterpret_cast<const uint4*>(X + row * H);
@@ -208,7 +210,18 @@ __global__ void __launch_bounds__(256) mref_kernel(const uint16_t* __restrict__ 
   }
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-  if (lane == 0) mref[row] = acc + STASH_REF_SHIFT;
+  if (lane == 0) mref[row] = partial ? acc : acc + STASH_REF_SHIFT;
+}
+
+// After the cross-shard sum of the partial target logits: M_i = z_t + shift, or +inf for ignored
+// rows and targets outside [0, V_global).
+__global__ void __launch_bounds__(256) mref_finish_kernel(const int32_t* __restrict__ t, int64_t N,
+                                                         int32_t ignore_index, int64_t V_global,
+                                                         float* __restrict__ mref) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= N) return;
+  const int32_t tt = t[i];
+  mref[i] = (tt == ignore_index || tt < 0 || (int64_t)tt >= V_global) ? INFINITY : mref[i] + STASH_REF_SHIFT;
 }
 
 // CS_ROWS = 4 rows per block of 256 threads (single GPU): each row's lse / loss / RowStat from its
@@ -228,7 +241,10 @@ __global__ void __launch_bounds__(256) combine_scale_kernel(
     float grad_scale, const WsHeader* __restrict__ hdr, float* __restrict__ loss_rows,
     slf_rowstat* __restrict__ rowstat, uint16_t* __restrict__ stash, uint16_t* __restrict__ stash2, int split,
     const float* __restrict__ mref, float* __restrict__ fac, const uint16_t* xrows, uint16_t* xs, int64_t H,
-    int64_t ld_xst, RmsStep rms) {
+    int64_t ld_xst, RmsStep rms, const slf_shardstat* __restrict__ st = nullptr, int g = 1, int64_t vocab_start = 0,
+    int64_t V_global = 0) {
+  // st (vocab shards): the row's lse comes from the g shards' statistics (shard order, as
+  // combine_transform); this shard's tile partials still decide which of its tiles kept their max.
   // ld_xst > 0: X' is written transposed, X'^T [H][ld_xst] (the dW GEMM's B operand K-major)
   extern __shared__ float r_t[];  // [tiles]: per-tile factors of a fallback row
   griddep_launch_dependents();
@@ -275,15 +291,29 @@ __global__ void __launch_bounds__(256) combine_scale_kernel(
     for (int p = 0; p < CS_LANES; ++p)
       if (lm[p][tid] != -INFINITY) S += ls[p][tid] * ex2((lm[p][tid] - Mx) * LOG2E);
     const int32_t tt = t[i];
+    const int64_t Vg = st ? V_global : V_l;
     const bool valid = tt != ignore_index;
-    const bool bad = valid && (tt < 0 || (int64_t)tt >= V_l);
-    const float z = (valid && !bad) ? zt[i] : 0.f;
+    const bool bad = valid && (tt < 0 || (int64_t)tt >= Vg);
+    const int64_t loc = (int64_t)tt - vocab_start;
+    const bool here = valid && !bad && loc >= 0 && loc < V_l;
+    float z = here ? zt[i] : 0.f;
+    if (st) {  // the global row statistics from the g shards, in shard order
+      Mx = -INFINITY;
+      S = 0.f;
+      z = 0.f;
+      for (int k = 0; k < g; ++k) Mx = fmaxf(Mx, st[(size_t)k * rows + i].m);
+      for (int k = 0; k < g; ++k) {
+        const slf_shardstat q = st[(size_t)k * rows + i];
+        S += q.s * ex2((q.m - Mx) * LOG2E);
+        z += q.zt;  // exactly one shard has the target (the others store 0)
+      }
+    }
     const float lse = Mx + logf(S);
     const float coef = (valid && !bad) ? coef_of(reduction, scale, hdr->n_valid) : 0.f;
     float l = valid ? (lse - z) : 0.f;
     if (bad) l = __int_as_float(0x7fc00000);
     loss_rows[i] = l;
-    rowstat[i] = slf_rowstat{lse * LOG2E, coef, (valid && !bad) ? tt : -1, valid ? 1 : 0};
+    rowstat[i] = slf_rowstat{lse * LOG2E, coef, here ? (int32_t)loc : -1, valid ? 1 : 0};
     const float cg = coef * grad_scale;
     float f = 0.f;
     if (cg != 0.f) {

@@ -1085,7 +1085,7 @@ slf_status s_chunk_bwd(Ctx& c, const SArgs& a, const SChunk& k, const slf_shards
         reinterpret_cast<uint16_t*>(c.ws + p.off_stash), reinterpret_cast<uint16_t*>(k.ext_base), (int)(rows - k.ext),
         reinterpret_cast<const float*>(c.ws + p.off_mref) + r0, reinterpret_cast<float*>(c.ws + p.off_fac) + r0,
         reinterpret_cast<const uint16_t*>(xr), reinterpret_cast<uint16_t*>(k.xt ? k.xt : k.xs), a.H,
-        k.xt ? k.ld_xt : 0, rms ? *rms : RmsStep{}));
+        k.xt ? k.ld_xt : 0, rms ? *rms : RmsStep{}, st, g, a.vs, a.Vg));
   } else if (!skip_ct) {
     ProfScope ps(SLF_PROF_COMBINE_TRANSFORM, c.s, 0.0, (double)rows * (tiles_v * 8.0 + a.V_l * 4.0 + 16.0 * g + 24));
     // Programmatic dependent launch: blocks start while the stash GEMM drains and wait in-kernel.
@@ -1752,6 +1752,36 @@ slf_status phase_sharded(Ctx& c, const ShardPlan& sp, slf_comm cm, const void* X
   SLF_TRY(s_begin(c, a, dW != nullptr));
   std::vector<SChunk> chunks;
   for (int64_t ch = 0; ch < p.nCh; ++ch) chunks.push_back(s_plain_chunk(p, N, ch));
+  // Per-row stash reference where X'^T fits in dhidden's rows after the chunk (not
+  // finalised yet); M_i needs the global target logit: each shard's contribution, one all-reduce.
+  static const bool classic = getenv("SLF_S_CLASSIC") != nullptr;
+  bool any_ref = false;
+  if (!classic && dX) {
+    for (auto& k : chunks) {
+      const size_t lo = align_up((size_t)(k.r0 + k.rows) * H * 2, 1024);
+      const int64_t ld = (k.rows + 7) / 8 * 8;
+      if (lo + (size_t)H * ld * 2 <= (size_t)N * H * 2) {
+        k.ref = any_ref = true;
+        if (dW) {
+          k.xt = reinterpret_cast<uint8_t*>(dX) + lo;
+          k.ld_xt = ld;
+        }
+      }
+    }
+  }
+  if (any_ref) {
+    float* mref = reinterpret_cast<float*>(c.ws + p.off_mref);
+    {
+      ProfScope ps(SLF_PROF_PREP, c.s, 2.0 * N * H, (double)N * H * 4);
+      mref_kernel<<<(unsigned)((N * 32 + 255) / 256), 256, 0, c.s>>>(
+          reinterpret_cast<const uint16_t*>(X), reinterpret_cast<const uint16_t*>(W), t, N, H, ign, sp.v0, sp.V_l,
+          mref, 1);
+      SLF_CUDA(cudaGetLastError());
+    }
+    SLF_TRY(comm_allreduce_now(cm, mref, (size_t)N, c.s));
+    mref_finish_kernel<<<(unsigned)((N + 255) / 256), 256, 0, c.s>>>(t, N, ign, Vg, mref);
+    SLF_CUDA(cudaGetLastError());
+  }
   // LPT tables per chunk shape (full chunks and the tail), uploaded once per call
   SchedArena arena;
   int tab[2] = {-1, -1};
