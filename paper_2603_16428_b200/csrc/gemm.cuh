@@ -347,7 +347,7 @@ __device__ __forceinline__ void epilogue_tile(const GemmArgs& a, uint32_t taddr,
 template <int NB, typename WaitAcc, typename ReleaseTmem>
 __device__ __forceinline__ void epilogue_dw_tma(const GemmArgs& a, const CUtensorMap* tmC, uint32_t taddr, int row0,
                                                 int n_blk, int rl, uint8_t* stg, uint64_t* sbar, uint32_t& sphase,
-                                                bool lead, WaitAcc wait_acc, ReleaseTmem release_tmem,
+                                                uint32_t& sq, bool lead, WaitAcc wait_acc, ReleaseTmem release_tmem,
                                                 int dbg = 0) {
   constexpr uint32_t CHUNK_BYTES = BM * 64 * 2;
   // chunks are processed NB at a time through the NB staging buffers
@@ -377,6 +377,39 @@ __device__ __forceinline__ void epilogue_dw_tma(const GemmArgs& a, const CUtenso
       }
     }
     release_tmem();
+    if (!(dbg & 4096)) {
+      // Chunk-pipelined staging: one bulk group per 64-column chunk, buffers used round-robin by a
+      // sequence number that runs on across tiles (sq), and before refilling a buffer only the store
+      // that last read it must be done (at most NB-1 newer groups pending) — the TMA reads chunk k
+      // while the warps fill chunk k+1, instead of NB chunks filled, stored, and all waited for.
+#pragma unroll
+      for (int k = 0; k < BN / 64; ++k) {
+        if (k >= nch) break;
+        const int j = (int)(sq % NB);
+        if (lead) bulk_wait_read<NB - 1>();
+        named_bar_sync(1, 128);
+        const uint32_t rowaddr = sbase + j * CHUNK_BYTES + rl * 128;
+#pragma unroll
+        for (int gi = 0; gi < 8; ++gi) {
+          const uint32_t* src = &pk[k * 32 + gi * 4];
+          sts128(rowaddr + ((gi ^ (rl & 7)) << 4), make_uint4(src[0], src[1], src[2], src[3]));
+        }
+        fence_proxy_async_smem();
+        named_bar_sync(1, 128);
+        if (lead) {
+          if (dbg & 256) {
+            // timing experiment only: no dW store at all (wrong dW)
+          } else if (a.mode == 2) {
+            tma_reduce_add_2d(tmC, stg + j * CHUNK_BYTES, n0 + k * 64, row0);
+          } else {
+            tma_store_2d(tmC, stg + j * CHUNK_BYTES, n0 + k * 64, row0);
+          }
+          bulk_commit();
+        }
+        ++sq;
+      }
+      return;
+    }
 #pragma unroll
     for (int g0 = 0; g0 < BN / 64; g0 += NB) {
       if (g0 >= nch) break;
@@ -899,6 +932,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     const uint32_t ew = warp - 4;
     uint32_t local = 0;
     uint32_t sphase = 0;  // parity bits of the two staging barriers
+    uint32_t sq = 0;      // staging-buffer sequence of the chunk-pipelined dW epilogue
     TileIter it(g, unit, units);
     for (int tile = it.next(); tile >= 0; tile = it.next(), ++local) {
       const int pi = prob_of(g, tile);
@@ -942,7 +976,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
           }
         }
         epilogue_dw_tma<NB>(P.a, &tm.m[MAPS_PER_PROB * pi + 2], taddr, m_blk * C::TILE_M + (int)rank * BM, n_blk,
-                        ew * 32 + lane, stg, sbar, sphase, ew == 0 && lane == 0, wait_acc, release, g.dbg);
+                        ew * 32 + lane, stg, sbar, sphase, sq, ew == 0 && lane == 0, wait_acc, release, g.dbg);
       } else if (P.epi == EPI_STASH && P.a.tma_out) {  // a stash tensor map is provided
         const int row0 = m_blk * C::TILE_M + (int)rank * BM;  // output rows >= c_split go to map C2
         const bool seg2 = row0 >= P.c_split;
