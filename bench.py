@@ -593,7 +593,7 @@ def main():
                      "unit": "TFLOP/s", "frac": achieved / peaks["sustained"], "traffic": traffic,
                      "peak_kind": "bf16 sustained (kernel timed inside a long step), " + peaks["source"],
                      "frac_of_burst": achieved / peaks["burst"],
-                     "ncu": "profiles/ncu_r01t.md (tensor pipe active % per kernel, DRAM bytes)"},
+                     "ncu": "profiles/ncu_r02a.md (tensor pipe active % per kernel, DRAM bytes)"},
         "kernels": kernels,
         "comm": ({"allgather_ms_per_step": kinds.get("comm_allgather", {}).get("ms", 0.0) / args.steps,
                   "allreduce_ms_per_step": kinds.get("comm_allreduce", {}).get("ms", 0.0) / args.steps,

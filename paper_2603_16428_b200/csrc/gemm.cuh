@@ -511,7 +511,8 @@ __device__ __forceinline__ void epilogue_dw_tma(const GemmArgs& a, const CUtenso
 template <int NB, typename WaitAcc, typename ReleaseTmem>
 __device__ __forceinline__ void epilogue_stash_tma(const GemmArgs& a, const CUtensorMap* tmC, uint32_t taddr,
                                                    int row0, int n_blk, int rl, uint8_t* stg, bool lead,
-                                                   WaitAcc wait_acc, ReleaseTmem release_tmem, int c_off = 0) {
+                                                   WaitAcc wait_acc, ReleaseTmem release_tmem, uint32_t& sq,
+                                                   int c_off = 0) {
   constexpr uint32_t CHUNK_BYTES = BM * 64 * 2;
   const int r = row0 + rl;
   const bool row_ok = r < a.M;
@@ -524,8 +525,6 @@ __device__ __forceinline__ void epilogue_stash_tma(const GemmArgs& a, const CUte
     const int64_t loc = (int64_t)t - a.tcol0 - n0;
     tl = (t != a.ignore_index && loc >= 0 && loc < ncols) ? (int)loc : -1;
   }
-  if (lead) bulk_wait_read<0>();  // the previous tile's stores have read the staging buffers
-  named_bar_sync(1, 128);
   wait_acc();
   uint32_t v[32];
   float mx = -INFINITY;
@@ -544,57 +543,57 @@ __device__ __forceinline__ void epilogue_stash_tma(const GemmArgs& a, const CUte
     const float M = a.mref[r];
     if (!(mx - M > STASH_REF_SLACK)) cmul = ex2((mx - M) * LOG2E);
   }
+  // Per 64-column chunk: two 32-column TMEM loads -> exp -> bf16 pairs -> one staging buffer ->
+  // one TMA store, chunk-pipelined as the dW epilogue: one bulk group per chunk, buffers by a running
+  // sequence, a buffer is refilled once the store that last read it is done.  TMEM is released
+  // after the last load.
   float s = 0.f, zt = 0.f;
-  // 64-column chunks are staged NB at a time
+  const int nch = (ncols + 63) / 64;
 #pragma unroll 1
-  for (int c = 0; c < BN / 32; ++c) {
-    if (c * 32 >= ncols) break;
-    if (c > 0 && (c % (2 * NB)) == 0) {  // staging full: store this group, wait until it is read
-      fence_proxy_async_smem();
-      named_bar_sync(1, 128);
-      if (lead) {
-        if (!(a.mode & 32))
-          for (int k = c / 2 - NB; k < c / 2; ++k)
-            tma_store_2d(tmC, stg + (k % NB) * CHUNK_BYTES, n0 + k * 64, row0 - c_off);
-        bulk_commit();
-        bulk_wait_read<0>();
+  for (int k = 0; k < BN / 64; ++k) {
+    if (k >= nch) break;
+    uint32_t p[32];
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int c = 2 * k + h;
+      if (c * 32 < ncols) {
+        tmem_ld32(taddr + c * 32, v);
+        tmem_ld_wait();
+#pragma unroll
+        for (int i = 0; i < 32; i += 2) {
+          const float z0 = __uint_as_float(v[i]), z1 = __uint_as_float(v[i + 1]);
+          float e0 = ex2(fmaf(z0, LOG2E, -mb)), e1 = ex2(fmaf(z1, LOG2E, -mb));
+          e0 = (c * 32 + i < ncols) ? e0 : 0.f;
+          e1 = (c * 32 + i + 1 < ncols) ? e1 : 0.f;
+          s += e0 + e1;
+          zt = (c * 32 + i == tl) ? z0 : zt;
+          zt = (c * 32 + i + 1 == tl) ? z1 : zt;
+          p[h * 16 + i / 2] = pack_bf16x2(e0 * cmul, e1 * cmul);
+        }
+      } else {
+#pragma unroll
+        for (int i = 0; i < 16; ++i) p[h * 16 + i] = 0u;
       }
-      named_bar_sync(1, 128);
     }
-    tmem_ld32(taddr + c * 32, v);
-    tmem_ld_wait();
-    uint32_t p[16];
+    if (k == nch - 1) release_tmem();
+    const int j = (int)(sq % NB);
+    if (lead) bulk_wait_read<NB - 1>();
+    named_bar_sync(1, 128);
+    const uint32_t rowaddr = sbase + j * CHUNK_BYTES + rl * 128;
 #pragma unroll
-    for (int i = 0; i < 32; i += 2) {
-      const float z0 = __uint_as_float(v[i]), z1 = __uint_as_float(v[i + 1]);
-      float e0 = ex2(fmaf(z0, LOG2E, -mb)), e1 = ex2(fmaf(z1, LOG2E, -mb));
-      e0 = (c * 32 + i < ncols) ? e0 : 0.f;
-      e1 = (c * 32 + i + 1 < ncols) ? e1 : 0.f;
-      s += e0 + e1;
-      zt = (c * 32 + i == tl) ? z0 : zt;
-      zt = (c * 32 + i + 1 == tl) ? z1 : zt;
-      p[i / 2] = pack_bf16x2(e0 * cmul, e1 * cmul);
+    for (int gi = 0; gi < 8; ++gi)
+      sts128(rowaddr + ((gi ^ (rl & 7)) << 4), make_uint4(p[gi * 4], p[gi * 4 + 1], p[gi * 4 + 2], p[gi * 4 + 3]));
+    fence_proxy_async_smem();
+    named_bar_sync(1, 128);
+    if (lead) {
+      if (!(a.mode & 32)) tma_store_2d(tmC, stg + j * CHUNK_BYTES, n0 + k * 64, row0 - c_off);  // 32: timing only
+      bulk_commit();
     }
-    const uint32_t rowaddr = sbase + ((c >> 1) % NB) * CHUNK_BYTES + rl * 128;
-#pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      const int gi = (c & 1) * 4 + q;
-      sts128(rowaddr + ((gi ^ (rl & 7)) << 4), make_uint4(p[4 * q], p[4 * q + 1], p[4 * q + 2], p[4 * q + 3]));
-    }
+    ++sq;
   }
-  release_tmem();
   if (row_ok) {
     a.partials[(size_t)n_blk * a.M + r] = make_float2(mx, s);
     if (tl >= 0) a.zt[r] = zt;
-  }
-  fence_proxy_async_smem();
-  named_bar_sync(1, 128);
-  if (lead) {
-    const int nch = (ncols + 63) / 64;
-    if (!(a.mode & 32))  // mode bit 32: skip the stash stores (timing experiment only)
-      for (int k = (nch - 1) / NB * NB; k < nch; ++k)
-        tma_store_2d(tmC, stg + (k % NB) * CHUNK_BYTES, n0 + k * 64, row0 - c_off);
-    bulk_commit();
   }
 }
 
@@ -981,7 +980,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
         const int row0 = m_blk * C::TILE_M + (int)rank * BM;  // output rows >= c_split go to map C2
         const bool seg2 = row0 >= P.c_split;
         epilogue_stash_tma<NB>(P.a, &tm.m[MAPS_PER_PROB * pi + (seg2 ? 4 : 2)], taddr, row0, n_blk, ew * 32 + lane,
-                           stg, ew == 0 && lane == 0, wait_acc, release, seg2 ? P.c_split : 0);
+                           stg, ew == 0 && lane == 0, wait_acc, release, sq, seg2 ? P.c_split : 0);
       } else {
         wait_acc();
         epilogue_dispatch(P.epi, P.a, taddr, m_blk * C::TILE_M + (int)rank * BM, n_blk, ew * 32 + lane);
