@@ -619,10 +619,13 @@ def test_native_sharded_callbacks(slf, tmp_path, g, red, budget):
     ref = oracle.lce(Xo, Wo, to, reduction=red)
     nch = int(str(res[0]["plan"]).split("n_chunks=")[1].split()[0])
     assert nch > 1
+    # per chunk: one statistics all-gather and one dX all-reduce; per call: one all-reduce of the
+    # rows' target logits when any chunk takes the per-row stash reference (it needs
+    # room for X' in dhidden's later rows, so not at every shape)
+    n_ref = int(res[0]["ar"]) - nch
+    assert n_ref in (0, 1)
     for r in res:
-        # per chunk: one statistics all-gather and one dX all-reduce; per call: one all-reduce of the
-        # rows' target logits (the per-row stash reference)
-        assert int(r["ag"]) == nch and int(r["ar"]) == nch + 1
+        assert int(r["ag"]) == nch and int(r["ar"]) == nch + n_ref
         assert np.array_equal(r["loss"], res[0]["loss"]) and np.array_equal(r["dX"], res[0]["dX"])
     assert_loss_close(res[0]["loss"] if red == "none" else float(res[0]["loss"].reshape(-1)[0]), ref["loss"], red)
     tobf = lambda a: a.astype(np.int16).view(np.uint16).astype(np.uint32) << 16  # noqa: E731
@@ -635,7 +638,7 @@ def test_native_sharded_callbacks(slf, tmp_path, g, red, budget):
     p2p = _run_native_ranks(tmp_path / "p2p", g, red, budget, ("--p2p", "1", "--calls", "2"))
     for a, b in zip(res, p2p):
         assert int(b["timeouts"]) == 0
-        assert int(b["ag"]) == 0 and int(b["ar"]) == nch + 1  # statistics no longer go through the transport
+        assert int(b["ag"]) == 0 and int(b["ar"]) == nch + n_ref  # statistics no longer go through the transport
         for k in ("loss", "dX", "dW"):
             assert np.array_equal(a[k], b[k]), k
     # statistics AND dX through the P2P exchanges (the dX exchange kernel: rank-order sum of the g
@@ -645,7 +648,7 @@ def test_native_sharded_callbacks(slf, tmp_path, g, red, budget):
         assert int(b["timeouts"]) == 0
         # no per-chunk collective: the two 80-byte IPC address records (dX partials, dhidden) and the
         # per-call target-logit all-reduce
-        assert int(b["ag"]) == 2 and int(b["ar"]) == 1
+        assert int(b["ag"]) == 2 and int(b["ar"]) == n_ref
         assert np.array_equal(a["loss"], b["loss"]) and np.array_equal(a["dW"], b["dW"])
         assert np.array_equal(b["dX"], px[0]["dX"])  # every rank holds the same dhidden
         if g == 2:  # two partials: a + b in either order, bit-identical to the gloo sum
