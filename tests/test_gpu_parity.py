@@ -624,6 +624,8 @@ def test_native_sharded_callbacks(slf, tmp_path, g, red, budget):
     # room for X' in dhidden's later rows, so not at every shape)
     n_ref = int(res[0]["ar"]) - nch
     assert n_ref in (0, 1)
+    if (g, red) == (2, "mean"):
+        assert n_ref == 1  # this shape runs the per-row reference path across ranks
     for r in res:
         assert int(r["ag"]) == nch and int(r["ar"]) == nch + n_ref
         assert np.array_equal(r["loss"], res[0]["loss"]) and np.array_equal(r["dX"], res[0]["dX"])
