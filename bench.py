@@ -38,9 +38,11 @@ def load_peaks():
     try:
         d = json.load(open(p))
         return dict(burst=float(d["bf16_tflops"]), sustained=float(d["bf16_tflops_sustained"]),
-                    hbm=float(d["hbm_gbs"]), source="MEASURED_PEAKS.json (measured)")
+                    hbm=float(d["hbm_gbs"]), source="MEASURED_PEAKS.json (measured)",
+                    sustained_mhz=(d.get("clocks_under_load") or {}).get("sm_mhz_median"))
     except Exception:
-        return dict(burst=1590.0, sustained=1400.0, hbm=6650.0, source="B200_PROFILING.md fallback")
+        return dict(burst=1590.0, sustained=1400.0, hbm=6650.0, source="B200_PROFILING.md fallback",
+                    sustained_mhz=None)
 
 
 # ---- clocks sampler ---------------------------------------------------------------------------------
@@ -593,6 +595,11 @@ def main():
                      "unit": "TFLOP/s", "frac": achieved / peaks["sustained"], "traffic": traffic,
                      "peak_kind": "bf16 sustained (kernel timed inside a long step), " + peaks["source"],
                      "frac_of_burst": achieved / peaks["burst"],
+                     # context, not the roofline: the sustained peak was measured at the peak run's
+                     # median SM clock; this step ran at ck["sm_mhz"] (both power-capped)
+                     **({"frac_at_this_clock": achieved / (peaks["sustained"] * ck["sm_mhz"] / peaks["sustained_mhz"]),
+                         "clock_mhz_peak_run": peaks["sustained_mhz"], "clock_mhz_this_run": ck["sm_mhz"]}
+                        if peaks.get("sustained_mhz") and ck.get("sm_mhz") else {}),
                      "ncu": "profiles/ncu_r02a.md (tensor pipe active % per kernel, DRAM bytes)"},
         "kernels": kernels,
         "comm": ({"allgather_ms_per_step": kinds.get("comm_allgather", {}).get("ms", 0.0) / args.steps,
