@@ -1903,16 +1903,18 @@ bool rms_layout(int64_t N, int64_t H, int64_t V, size_t b, RmsPlan* rp) {
 bool rms_plan(int64_t N, int64_t H, int64_t V, size_t budget, RmsPlan* out) {
   if (N < 1 || H < 8 || V < 1) return false;
   if (budget == 0) return rms_layout(N, H, V, 0, out);
+  // the largest LCE budget whose whole layout fits (bisection; the layout grows with the budget)
   RmsPlan rp;
-  if (!rms_layout(N, H, V, budget, &rp)) return false;
-  size_t b = budget;
-  for (int it = 0; it < 8 && rp.total > budget; ++it) {  // shrink the LCE part by the overshoot
-    const size_t over = rp.total - budget;
-    if (over >= b) return false;
-    b -= over;
-    if (!rms_layout(N, H, V, b, &rp)) return false;
+  auto ok = [&](size_t b) { return rms_layout(N, H, V, b, &rp) && rp.total <= budget; };
+  size_t lo = 1, hi = budget;
+  while (lo < hi) {
+    const size_t mid = lo + (hi - lo + 1) / 2;
+    if (ok(mid))
+      lo = mid;
+    else
+      hi = mid - 1;
   }
-  if (rp.total > budget) return false;
+  if (!ok(lo)) return false;
   *out = rp;
   return true;
 }

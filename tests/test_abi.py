@@ -213,3 +213,24 @@ def test_comm_and_dp_argument_errors(L):
     st = L.slf_lce_fwd_bwd_dp(*([16] * 3), 8, 8, 64, -100, 1, 1.0, *([16] * 4), 1 << 20, 0, 0, 0, None, None)
     assert _lib.STATUS_NAMES[st] == "SLF_ERR_ARG"
     assert b"communicator" in L.slf_last_error_string()
+
+
+@pytest.mark.parametrize("cfg", ["tiny", "llama8b", "mistral123b"])
+def test_rmsnorm_lce_planner(L, cfg):
+    """The fused RMSNorm + LCE workspace: with budget 0 the LCE's default plan plus the RMSNorm
+    chunk buffers (two y buffers, rstd, two dg-partial buffers); with a budget the whole layout fits
+    it (the LCE part shrinks).  Host only."""
+    import synth
+    from paper_2603_16428_b200 import lce
+    c = synth.CONFIGS[cfg]
+    N, H, V = c["N"], c["H"], c["V"]
+    base = lce.workspace_bytes(N, H, V, schedule="S")
+    fused = lce.rmsnorm_lce_workspace_bytes(N, H, V)
+    assert fused > base
+    extra = fused - base
+    assert extra <= 2 * 2 * 2 * N * H + N * 4 + 2 * (2 * N // 32 + 1) * H * 4 + 8192  # never beyond 2 y chunks of all rows
+    budget = max(int(0.05 * N * V * 2), 16 << 20)
+    capped = lce.rmsnorm_lce_workspace_bytes(N, H, V, budget)
+    assert 0 < capped <= budget
+    desc = lce.rmsnorm_lce_plan_describe(N, H, V, budget)
+    assert desc.startswith("schedule=S rmsnorm_fused") and f"workspace={capped}" in desc
