@@ -660,6 +660,15 @@ struct GroupArgs {
             // staging buffers are free), 2048 = MN-major A operands read from two K-blocks only (wrong)
   const int* sched;  // [units][sched_stride] tile ids, -1 terminated (nullptr: round robin)
   int sched_stride;
+  // il = 1: the table holds (tile, seg) int pairs — a K-block range [kb0, kb1) of the tile, whether it
+  // starts / ends the tile's accumulation, and its TMEM accumulator slot (the dX tiles
+  // split into K segments interleaved with the dW tiles of the same vocabulary range)
+  int il;
+};
+
+// One work item of a unit: a whole tile (il = 0), or a K segment of one (il = 1).
+struct Item {
+  int tile, kb0, kb1, first, last, slot;  // slot -1: alternate accumulators by tile (il = 0)
 };
 
 struct TMaps {
@@ -681,7 +690,30 @@ struct TileIter {
     return t;
   }
   __device__ __forceinline__ int next() { return at(i++); }
-  __device__ __forceinline__ int peek() const { return at(i); }
+  __device__ __forceinline__ int peek() const {
+    if (!g.il) return at(i);
+    return 2 * i < g.sched_stride ? __ldg(g.sched + (size_t)unit * g.sched_stride + 2 * i) : -1;
+  }
+  __device__ __forceinline__ Item next_item() {
+    Item r;
+    if (!g.il) {
+      r.tile = at(i++);
+      r.kb0 = 0;
+      r.kb1 = 0;  // the caller's problem K
+      r.first = r.last = 1;
+      r.slot = -1;
+      return r;
+    }
+    const int k = i++;
+    r.tile = 2 * k < g.sched_stride ? __ldg(g.sched + (size_t)unit * g.sched_stride + 2 * k) : -1;
+    const int sg = r.tile >= 0 ? __ldg(g.sched + (size_t)unit * g.sched_stride + 2 * k + 1) : 0;
+    r.kb0 = sg & 4095;
+    r.kb1 = (sg >> 12) & 4095;
+    r.first = (sg >> 24) & 1;
+    r.last = (sg >> 25) & 1;
+    r.slot = (sg >> 26) & 1;
+    return r;
+  }
 };
 
 __device__ __forceinline__ int prob_of(const GroupArgs& g, int tile) {
@@ -760,7 +792,8 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
       unsigned long long u_ew = 0;
       const bool tu = (g.dbg & 4) && unit < TRACE_UNITS && rank == 0;
       TileIter it(g, unit, units);
-      for (int tile = it.next(); tile >= 0; tile = it.next()) {
+      for (Item item = it.next_item(); item.tile >= 0; item = it.next_item()) {
+        const int tile = item.tile;
         const int pi = prob_of(g, tile);
         const Prob& P = g.p[pi];
         const CUtensorMap* tA = &tm.m[MAPS_PER_PROB * pi];
@@ -770,7 +803,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
         tile_coords(tile - P.tile_begin, P.a, m_blk, n_blk);
         const int a_row = m_blk * C::TILE_M + (int)rank * BM;
         const int b_row = n_blk * BN + (int)rank * C::B_ROWS;
-        const int num_kb = (P.a.K + BK - 1) / BK;
+        const int kb_beg = item.kb0, kb_end = g.il ? item.kb1 : (P.a.K + BK - 1) / BK;
         const bool a_mn = P.a_mn, b_mn = P.b_mn;
         if (g.dbg & 8) {  // experiment: pull the next tile's MN-major A operand (all of K) into L2
           const int nt = it.peek();
@@ -791,7 +824,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
             }
           }
         }
-        for (int kb = 0; kb < num_kb; ++kb) {
+        for (int kb = kb_beg; kb < kb_end; ++kb) {
           unsigned long long c0 = tu ? clk() : 0;
           mbar_wait(&empty[stage], phase ^ 1);
           if (tu) u_ew += clk() - c0;
@@ -857,15 +890,19 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
   } else if (warp == 1) {
     if (lane == 0 && rank == 0) {
       // ===== tcgen05.mma issuer (pair leader only) =====
-      uint32_t stage = 0, phase = 0, local = 0;
+      uint32_t stage = 0, phase = 0, local = 0, ntiles = 0;
+      uint32_t uses0 = 0, uses1 = 0;  // completed accumulations per TMEM slot (scalars: no local memory)
       unsigned long long u_fw = 0, u_tw = 0, u_kb = 0, u_first = 0, u_gt0 = 0;
       TileIter it(g, unit, units);
-      for (int tile = it.next(); tile >= 0; tile = it.next(), ++local) {
+      for (Item item = it.next_item(); item.tile >= 0; item = it.next_item(), ++local) {
+        const int tile = item.tile;
         const Prob& P = g.p[prob_of(g, tile)];
         const bool a_mn = P.a_mn, b_mn = P.b_mn;
         const uint32_t idesc = make_idesc_bf16(C::TILE_M, BN, a_mn, b_mn);
-        const int num_kb = (P.a.K + BK - 1) / BK;
-        const uint32_t acc = local & 1, acc_phase = (local >> 1) & 1;
+        const int kb_beg = item.kb0, kb_end = g.il ? item.kb1 : (P.a.K + BK - 1) / BK;
+        const uint32_t acc = item.slot >= 0 ? (uint32_t)item.slot : (ntiles & 1);
+        if (item.first) ++ntiles;
+        const uint32_t acc_phase = (acc ? uses1 : uses0) & 1;
         const bool tr = (g.dbg & 4) && blockIdx.x == 0 && local < TRACE_TILES;
         const bool tu = (g.dbg & 4) && unit < TRACE_UNITS;
         unsigned long long c0 = 0;
@@ -877,12 +914,14 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
           }
         }
         if (tr) g_trace[local * 8 + 0] = clk();
-        mbar_wait(&tempty[acc], acc_phase ^ 1);
-        tc_fence_after();
+        if (item.first) {  // the accumulator must be free (its previous tile's epilogue released it)
+          mbar_wait(&tempty[acc], acc_phase ^ 1);
+          tc_fence_after();
+        }
         if (tu) u_tw += clk() - c0;
         if (tr) g_trace[local * 8 + 1] = clk();
         const uint32_t d_tmem = tmem_base + acc * BN;
-        for (int kb = 0; kb < num_kb; ++kb) {
+        for (int kb = kb_beg; kb < kb_end; ++kb) {
           if (tu) c0 = clk();
           mbar_wait(&full[stage], phase);
           tc_fence_after();
@@ -896,10 +935,11 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
           for (int k = 0; k < BK / 16; ++k) {
             const uint64_t ad = a_mn ? make_sdesc(a_base + k * 2048, 8192, 1024) : make_sdesc(a_base + k * 32, 16, 1024);
             const uint64_t bd = b_mn ? make_sdesc(b_base + k * 2048, 8192, 1024) : make_sdesc(b_base + k * 32, 16, 1024);
+            const bool accum = !(item.first && kb == kb_beg && k == 0);
             if constexpr (CG == 2)
-              mma_bf16_pair(d_tmem, ad, bd, idesc, (kb | k) != 0);
+              mma_bf16_pair(d_tmem, ad, bd, idesc, accum);
             else
-              mma_bf16(d_tmem, ad, bd, idesc, (kb | k) != 0);
+              mma_bf16(d_tmem, ad, bd, idesc, accum);
           }
           // frees the smem slot (in both CTAs) once these MMAs have read it
           if constexpr (CG == 2)
@@ -908,11 +948,14 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
             mma_commit(&empty[stage]);
           if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
         }
-        // accumulator ready for the epilogue warps (of both CTAs)
-        if constexpr (CG == 2)
-          mma_commit_pair(&tfull[acc], 0x3);
-        else
-          mma_commit(&tfull[acc]);
+        // accumulator ready for the epilogue warps (of both CTAs) once the tile's last segment is in
+        if (item.last) {
+          if constexpr (CG == 2)
+            mma_commit_pair(&tfull[acc], 0x3);
+          else
+            mma_commit(&tfull[acc]);
+          if (acc) ++uses1; else ++uses0;
+        }
         if (tr) g_trace[local * 8 + 2] = clk();
       }
       if ((g.dbg & 4) && unit < TRACE_UNITS) {
@@ -932,13 +975,18 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     uint32_t local = 0;
     uint32_t sphase = 0;  // parity bits of the two staging barriers
     uint32_t sq = 0;      // staging-buffer sequence of the chunk-pipelined dW epilogue
+    uint32_t ntiles = 0, uses0 = 0, uses1 = 0;
     TileIter it(g, unit, units);
-    for (int tile = it.next(); tile >= 0; tile = it.next(), ++local) {
+    for (Item item = it.next_item(); item.tile >= 0; item = it.next_item()) {
+      const int tile = item.tile;
+      const uint32_t acc = item.slot >= 0 ? (uint32_t)item.slot : (ntiles & 1);
+      if (item.first) ++ntiles;
+      if (!item.last) continue;  // an interior K segment: the accumulation goes on
+      const uint32_t acc_phase = (acc ? uses1++ : uses0++) & 1;
       const int pi = prob_of(g, tile);
       const Prob& P = g.p[pi];
       int m_blk, n_blk;
       tile_coords(tile - P.tile_begin, P.a, m_blk, n_blk);
-      const uint32_t acc = local & 1, acc_phase = (local >> 1) & 1;
       const bool tr = (g.dbg & 4) && blockIdx.x == 0 && local < TRACE_TILES && ew == 0 && lane == 0;
       if (tr) {
         g_trace[local * 8 + 3] = clk();
@@ -987,6 +1035,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
         release();
       }
       if (tr) g_trace[local * 8 + 6] = clk();
+      ++local;
     }
   }
   if (warp == 4 && lane == 0) bulk_wait<0>();  // epilogue TMA stores complete before exit

@@ -260,10 +260,78 @@ void finish_geometry(GemmArgs& a, int cg) {
   a.group_m = std::max(1, std::min(a.tiles_m, gm));
 }
 
+// Interleaved schedule of a schedule-S group (the chunk's dX GEMM, K = V, and dW GEMM, K = rows),
+// each of the T0 <= units dX tiles belongs to one unit and is split into K segments of
+// L K-blocks; after segment s of every dX tile, the dW tiles whose vocabulary rows are that segment's
+// K range (the same stash columns) go to the least-loaded units.  The stash slab and the W rows a
+// segment streams are then read again by those dW tiles while they are still in L2, instead of
+// long after (round 1: all dX tiles first, dW tiles afterwards); a dX accumulation stays open in TMEM
+// slot 0 across its segments while its unit's dW tiles use slot 1 (their epilogues overlap the next
+// segment).  Returns (tile, seg) int pairs per unit and a NEGATIVE stride (the kernel's il mode), or
+// an empty table when the group does not have that shape.
+int host_m_blk(const GemmArgs& a, int tile) {
+  const int per_group = a.group_m * a.tiles_n;
+  const int gi = tile / per_group;
+  const int first_m = gi * a.group_m;
+  const int gm = std::min(a.group_m, a.tiles_m - first_m);
+  return first_m + (tile - gi * per_group) % gm;
+}
+
+std::vector<int> interleave_table(const ProbSpec* ps, int n, int units, int* stride) {
+  static const int seg_env = getenv("SLF_IL_SEG") ? atoi(getenv("SLF_IL_SEG")) : 16;
+  static const bool off = getenv("SLF_INTERLEAVE") && atoi(getenv("SLF_INTERLEAVE")) == 0;
+  if (off || n != 2 || ps[0].epi != EPI_DXS || ps[1].epi != EPI_DW) return {};
+  const GemmArgs &ax = ps[0].a, &aw = ps[1].a;
+  const int T0 = ax.num_tiles, T1 = aw.num_tiles;
+  const int KB0 = (ax.K + BK - 1) / BK, KB1 = (aw.K + BK - 1) / BK;
+  const int mkb = BM * cta_group() / BK;  // dX K-blocks per dW row tile (the same vocabulary rows)
+  const int L = std::max(mkb, seg_env / mkb * mkb);
+  if (T0 < 1 || T0 > units || T1 < 1 || KB0 >= 4096 || KB1 >= 4096 || aw.M * 1LL != ax.K * 1LL) return {};
+  const int S = (KB0 + L - 1) / L;
+  std::vector<std::vector<int>> bucket(S);
+  for (int t = 0; t < T1; ++t) bucket[std::min(S - 1, host_m_blk(aw, t) * mkb / L)].push_back(t);
+  std::vector<std::vector<int>> items(units);
+  std::vector<long long> load(units, 0);
+  std::vector<int> alt(units, 0);
+  static const int ovh = getenv("SLF_LPT_OVH") ? atoi(getenv("SLF_LPT_OVH")) : 4;
+  auto seg = [](int kb0, int kb1, int first, int last, int slot) {
+    return kb0 | (kb1 << 12) | (first << 24) | (last << 25) | (slot << 26);
+  };
+  for (int s = 0; s < S; ++s) {
+    for (int u = 0; u < T0; ++u) {
+      const int kb0 = s * L, kb1 = std::min(KB0, kb0 + L);
+      items[u].push_back(u);
+      items[u].push_back(seg(kb0, kb1, s == 0, kb1 == KB0, 0));
+      load[u] += kb1 - kb0;
+    }
+    for (int t : bucket[s]) {
+      int best = 0;
+      for (int u = 1; u < units; ++u)
+        if (load[u] < load[best]) best = u;
+      const int slot = best < T0 ? 1 : (alt[best]++ & 1);
+      items[best].push_back(T0 + t);
+      items[best].push_back(seg(0, KB1, 1, 1, slot));
+      load[best] += KB1 + ovh;
+    }
+  }
+  size_t mx = 2;
+  for (auto& l : items) mx = std::max(mx, l.size() + 2);
+  std::vector<int> tab((size_t)units * mx, -1);
+  for (int u = 0; u < units; ++u)
+    for (size_t i = 0; i < items[u].size(); ++i) tab[(size_t)u * mx + i] = items[u][i];
+  *stride = -(int)mx;
+  return tab;
+}
+
 // Longest-processing-time-first assignment of the tiles of a group to `units` persistent units:
 // tiles sorted by K-blocks (descending, stable by id), each given to the least-loaded unit.
-// Returns a [units][stride] table of tile ids, -1 padded.
+// Returns a [units][stride] table of tile ids, -1 padded.  (A schedule-S dX + dW group gets the
+// interleaved table above instead.)
 std::vector<int> lpt_table(const ProbSpec* ps, int n, int units, int* stride) {
+  {
+    std::vector<int> il = interleave_table(ps, n, units, stride);
+    if (!il.empty()) return il;
+  }
   std::vector<std::pair<int, int>> tiles;  // (kblocks, id)
   int id = 0;
   for (int p = 0; p < n; ++p) {
@@ -353,7 +421,8 @@ slf_status launch_group_cfg(DevInfo* dev, ProbSpec* ps, int n, cudaStream_t s, c
   g.nprob = np;
   g.num_tiles = total;
   g.sched = sched;
-  g.sched_stride = sched_stride;
+  g.sched_stride = sched_stride < 0 ? -sched_stride : sched_stride;  // negative: interleaved (seg) table
+  g.il = sched && sched_stride < 0 ? 1 : 0;
   static const int dbg = getenv("SLF_DEBUG_EPI") ? atoi(getenv("SLF_DEBUG_EPI")) : 0;  // timing experiments only
   g.dbg = dbg & ~4;
   {  // SLF_DEBUG_TRACE=k: record the per-tile trace of the k-th group launch of this process
