@@ -261,7 +261,7 @@ void finish_geometry(GemmArgs& a, int cg) {
 }
 
 // Interleaved schedule of a schedule-S group (the chunk's dX GEMM, K = V, and dW GEMM, K = rows),
-// each of the T0 <= units dX tiles belongs to one unit and is split into K segments of
+// DESIGN.md §6 (experiment, SLF_INTERLEAVE=1): each of the T0 <= units dX tiles belongs to one unit and is split into K segments of
 // L K-blocks; after segment s of every dX tile, the dW tiles whose vocabulary rows are that segment's
 // K range (the same stash columns) go to the least-loaded units.  The stash slab and the W rows a
 // segment streams are then read again by those dW tiles while they are still in L2, instead of
@@ -279,7 +279,9 @@ int host_m_blk(const GemmArgs& a, int tile) {
 
 std::vector<int> interleave_table(const ProbSpec* ps, int n, int units, int* stride) {
   static const int seg_env = getenv("SLF_IL_SEG") ? atoi(getenv("SLF_IL_SEG")) : 16;
-  static const bool off = getenv("SLF_INTERLEAVE") && atoi(getenv("SLF_INTERLEAVE")) == 0;
+  // Off by default (SLF_INTERLEAVE=1 selects it): it cuts the group's DRAM reads by 10 % but issues
+  // 5–10 % fewer MMAs per clock (measured), so the step is not faster.
+  static const bool off = !(getenv("SLF_INTERLEAVE") && atoi(getenv("SLF_INTERLEAVE")) == 1);
   if (off || n != 2 || ps[0].epi != EPI_DXS || ps[1].epi != EPI_DW) return {};
   const GemmArgs &ax = ps[0].a, &aw = ps[1].a;
   const int T0 = ax.num_tiles, T1 = aw.num_tiles;
@@ -325,8 +327,8 @@ std::vector<int> interleave_table(const ProbSpec* ps, int n, int units, int* str
 
 // Longest-processing-time-first assignment of the tiles of a group to `units` persistent units:
 // tiles sorted by K-blocks (descending, stable by id), each given to the least-loaded unit.
-// Returns a [units][stride] table of tile ids, -1 padded.  (A schedule-S dX + dW group gets the
-// interleaved table above instead.)
+// Returns a [units][stride] table of tile ids, -1 padded.  (With SLF_INTERLEAVE=1 a schedule-S
+// dX + dW group gets the interleaved table above instead.)
 std::vector<int> lpt_table(const ProbSpec* ps, int n, int units, int* stride) {
   {
     std::vector<int> il = interleave_table(ps, n, units, stride);
