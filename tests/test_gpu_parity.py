@@ -885,3 +885,32 @@ def test_stash_reference_fallback_rows(slf, alpha, red):
     loss, dX, dW = slf.lce_fwd_bwd(X, W, t, reduction=red, schedule="S", budget_bytes=4 << 20)
     torch.cuda.synchronize()
     assert torch.isfinite(dX.float()).all() and torch.isfinite(dW.float()).all()
+
+
+def test_interleaved_schedule_bit_identical(slf, tmp_path):
+    """The experimental interleaved group schedule (SLF_INTERLEAVE=1: dX tiles in K segments with
+    the dW tiles of each segment's vocabulary rows in between) accumulates every tile in
+    the same K order, so loss, dX and dW are the same bits as under the default LPT schedule."""
+    import os
+    import subprocess
+    import sys
+    code = r"""
+import sys, numpy as np, torch
+sys.path.insert(0, sys.argv[1]); sys.path.insert(0, sys.argv[1] + '/tests')
+import synth, paper_2603_16428_b200 as slf
+from gpu_util import to_dev
+inp = synth.make_inputs(1500, 512, 6000, seed=35, alpha=4.0, dist='zipf')
+X, W, t = to_dev(inp, torch)
+l, dX, dW = slf.lce_fwd_bwd(X, W, t, budget_bytes=6 << 20, schedule='S')
+torch.cuda.synchronize()
+np.savez(sys.argv[2], l=l.cpu().numpy(), dX=dX.view(torch.int16).cpu().numpy(), dW=dW.view(torch.int16).cpu().numpy())
+"""
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    out = {}
+    for mode in ("0", "1"):
+        f = str(tmp_path / f"il{mode}.npz")
+        env = dict(os.environ, SLF_INTERLEAVE=mode)
+        subprocess.run([sys.executable, "-c", code, root, f], check=True, env=env, timeout=300)
+        out[mode] = np.load(f)
+    for k in ("l", "dX", "dW"):
+        assert np.array_equal(out["0"][k], out["1"][k]), k
