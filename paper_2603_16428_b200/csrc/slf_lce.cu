@@ -1518,10 +1518,13 @@ bool shard_fit(int64_t N, int64_t H, int64_t V_l, int g, size_t total, int64_t c
   auto ok = [&](size_t b) {
     return shard_layout(N, H, V_l, g, b, sp) && sp->total <= total && (c_cap == 0 || sp->p.C <= c_cap);
   };
-  size_t lo = 1, hi = total;  // bisection (the layout grows with the budget; 0 would mean the default)
+  // bisection (the layout grows with the budget; 0 would mean the default): below the smallest
+  // feasible planner budget the predicate counts as "go larger", so it is monotone
+  auto below_or_ok = [&](size_t b) { return !shard_layout(N, H, V_l, g, b, sp) || ok(b); };
+  size_t lo = 1, hi = total;
   while (lo < hi) {
     const size_t mid = lo + (hi - lo + 1) / 2;
-    if (ok(mid))
+    if (below_or_ok(mid))
       lo = mid;
     else
       hi = mid - 1;
@@ -1974,18 +1977,19 @@ bool rms_layout(int64_t N, int64_t H, int64_t V, size_t b, RmsPlan* rp) {
 bool rms_plan(int64_t N, int64_t H, int64_t V, size_t budget, RmsPlan* out) {
   if (N < 1 || H < 8 || V < 1) return false;
   if (budget == 0) return rms_layout(N, H, V, 0, out);
-  // the largest LCE budget whose whole layout fits (bisection; the layout grows with the budget)
+  // The largest LCE budget whose whole layout fits (bisection): below the smallest feasible LCE plan
+  // the predicate counts as "go larger", above it the layout grows with the budget.
   RmsPlan rp;
-  auto ok = [&](size_t b) { return rms_layout(N, H, V, b, &rp) && rp.total <= budget; };
+  auto below_or_fits = [&](size_t b) { return !rms_layout(N, H, V, b, &rp) || rp.total <= budget; };
   size_t lo = 1, hi = budget;
   while (lo < hi) {
     const size_t mid = lo + (hi - lo + 1) / 2;
-    if (ok(mid))
+    if (below_or_fits(mid))
       lo = mid;
     else
       hi = mid - 1;
   }
-  if (!ok(lo)) return false;
+  if (!rms_layout(N, H, V, lo, &rp) || rp.total > budget) return false;
   *out = rp;
   return true;
 }
