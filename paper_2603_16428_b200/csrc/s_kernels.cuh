@@ -233,7 +233,7 @@ __global__ void __launch_bounds__(256) mref_finish_kernel(const int32_t* __restr
 // outside [1e-30, 1e30]): those are rescaled in place to G_P tile by tile and get f_i = 1,
 // X'_i = x_i.  xs may alias xrows (the fused RMSNorm's y buffer): each row is read then written by
 // the same thread.
-constexpr int CS_ROWS = 4, CS_LANES = 64;
+constexpr int CS_ROWS = 8, CS_LANES = 32;
 
 __global__ void __launch_bounds__(256) combine_scale_kernel(
     const float2* __restrict__ partials, int tiles, int rows, const float* __restrict__ zt,
@@ -358,10 +358,10 @@ __global__ void __launch_bounds__(256) combine_scale_kernel(
   // without a dW GEMM
   if (!xs) return;
   const int nr = min(CS_ROWS, rows - i0);
-  if (ld_xst > 0) {  // X'^T[h][i0 .. i0 + nr): 8 contiguous bytes per column h
-    static_assert(CS_ROWS == 4, "one 8-byte store per column");
+  if (ld_xst > 0) {  // X'^T[h][i0 .. i0 + nr): CS_ROWS * 2 contiguous bytes per column h
+    static_assert(CS_ROWS == 4 || CS_ROWS == 8, "one 8- or 16-byte store per column");
     for (int64_t h = tid; h < H; h += 256) {
-      uint32_t w[2];
+      uint32_t w[CS_ROWS / 2];
 #pragma unroll
       for (int r = 0; r < CS_ROWS; r += 2) {
         const float a = r < nr ? bf16_bits_to_f32(xrows[(size_t)(i0 + r) * H + h]) * sF[r] : 0.f;
@@ -370,7 +370,10 @@ __global__ void __launch_bounds__(256) combine_scale_kernel(
       }
       uint16_t* dst = xs + (size_t)h * ld_xst + i0;
       if (nr == CS_ROWS) {
-        *reinterpret_cast<uint2*>(dst) = make_uint2(w[0], w[1]);
+        if constexpr (CS_ROWS == 8)
+          *reinterpret_cast<uint4*>(dst) = make_uint4(w[0], w[1], w[CS_ROWS / 2 - 2], w[CS_ROWS / 2 - 1]);
+        else
+          *reinterpret_cast<uint2*>(dst) = make_uint2(w[0], w[1]);
       } else {
         for (int r = 0; r < nr; ++r) dst[r] = (uint16_t)(w[r / 2] >> ((r & 1) * 16));
       }
