@@ -229,7 +229,8 @@ __global__ void __launch_bounds__(256) mref_finish_kernel(const int32_t* __restr
 // tile the 8 rows' lanes read 8 consecutive partials, two 32-byte sectors), then one thread per row
 // merges the 32 lane results in lane order (fixed, deterministic) — then the row factor f_i and, by
 // the whole block, X'_i = bf16(f_i * x_i) for its rows (X'^T: one 16-byte store per column).
-// 4 rows per block measured the same (0.74–0.76 ms per Llama-8B step): the kernel is latency-bound.  The stash is not touched, except
+// 4 rows per block measured the same (0.74–0.76 ms per Llama-8B step with per-column stores); the
+// 16-byte transpose below brought it to 0.63 ms.  The stash is not touched, except
 // for rare rows where the per-row reference does not fit (a tile kept its own max, or f_i is
 // outside [1e-30, 1e30]): those are rescaled in place to G_P tile by tile and get f_i = 1,
 // X'_i = x_i.  xs may alias xrows (the fused RMSNorm's y buffer): each row is read then written by
@@ -268,6 +269,7 @@ __global__ void __launch_bounds__(256) combine_scale_kernel(
     int fb = 0;
     if (i < rows) {
       const float M = mref[i];
+#pragma unroll 4
       for (int k = lane; k < tiles; k += CS_LANES) {
         const float2 p = partials[(size_t)k * rows + i];
         fb |= (p.x - M > STASH_REF_SLACK) ? 1 : 0;
@@ -359,6 +361,28 @@ __global__ void __launch_bounds__(256) combine_scale_kernel(
   // without a dW GEMM
   if (!xs) return;
   const int nr = min(CS_ROWS, rows - i0);
+  if (ld_xst > 0 && CS_ROWS == 8 && nr == CS_ROWS) {
+    // X'^T[h][i0 .. i0 + 8) for 8 consecutive columns h per thread: eight 16-byte row loads, a
+    // register transpose, eight 16-byte column stores
+    for (int64_t h0 = (int64_t)tid * 8; h0 < H; h0 += 256 * 8) {
+      float v[CS_ROWS][8];
+#pragma unroll
+      for (int r = 0; r < CS_ROWS; ++r) {
+        const uint4 q = *reinterpret_cast<const uint4*>(xrows + (size_t)(i0 + r) * H + h0);
+        const float f = sF[r];
+        v[r][0] = bf16lo_to_f32(q.x) * f; v[r][1] = bf16hi_to_f32(q.x) * f;
+        v[r][2] = bf16lo_to_f32(q.y) * f; v[r][3] = bf16hi_to_f32(q.y) * f;
+        v[r][4] = bf16lo_to_f32(q.z) * f; v[r][5] = bf16hi_to_f32(q.z) * f;
+        v[r][6] = bf16lo_to_f32(q.w) * f; v[r][7] = bf16hi_to_f32(q.w) * f;
+      }
+#pragma unroll
+      for (int c = 0; c < 8; ++c)
+        *reinterpret_cast<uint4*>(xs + (size_t)(h0 + c) * ld_xst + i0) =
+            make_uint4(pack_bf16x2(v[0][c], v[1][c]), pack_bf16x2(v[2][c], v[3][c]), pack_bf16x2(v[4][c], v[5][c]),
+                       pack_bf16x2(v[6][c], v[7][c]));
+    }
+    return;
+  }
   if (ld_xst > 0) {  // X'^T[h][i0 .. i0 + nr): CS_ROWS * 2 contiguous bytes per column h
     static_assert(CS_ROWS == 4 || CS_ROWS == 8, "one 8- or 16-byte store per column");
     for (int64_t h = tid; h < H; h += 256) {
