@@ -751,8 +751,26 @@ __device__ __forceinline__ int32_t csr_row_of(const int32_t* __restrict__ off, i
   return (int32_t)(lo - 1);
 }
 
+// The hit-row index holding position p: the largest h with off[hits[h]] <= p (hits: the rows with
+// at least one token, increasing; n_hits of them).
+__device__ __forceinline__ int64_t csr_hit_of(const int32_t* __restrict__ off, const int32_t* __restrict__ hits,
+                                              int64_t n_hits, int64_t p) {
+  int64_t lo = 0, n = n_hits;
+  while (n > 0) {
+    const int64_t h = n >> 1;
+    if (off[hits[lo + h]] <= p) {
+      lo += h + 1;
+      n -= h + 1;
+    } else {
+      n = h;
+    }
+  }
+  return lo - 1;
+}
+
 __global__ void __launch_bounds__(128) onehot_seg_kernel(const uint16_t* __restrict__ X, int64_t H,
                                                         const int32_t* __restrict__ off,
+                                                        const int32_t* __restrict__ hits,
                                                         const int32_t* __restrict__ idx, int64_t V_l, int S,
                                                         int reduction, float scale, float grad_scale,
                                                         const WsHeader* __restrict__ hdr, float* __restrict__ part,
@@ -773,7 +791,10 @@ __global__ void __launch_bounds__(128) onehot_seg_kernel(const uint16_t* __restr
     gw[0] = bf16lo_to_f32(q.x); gw[1] = bf16hi_to_f32(q.x); gw[2] = bf16lo_to_f32(q.y); gw[3] = bf16hi_to_f32(q.y);
     gw[4] = bf16lo_to_f32(q.z); gw[5] = bf16hi_to_f32(q.z); gw[6] = bf16lo_to_f32(q.w); gw[7] = bf16hi_to_f32(q.w);
   }
-  int32_t row = csr_row_of(off, V_l, p0);
+  // rows in position order are consecutive entries of the hit list: one search per segment, then
+  // the next row is hits[h + 1] (round 2's first version searched the offsets at every row change)
+  int64_t h = csr_hit_of(off, hits, off[V_l + 1], p0);
+  int32_t row = hits[h];
   int64_t row_beg = off[row], row_end = off[row + 1];
   float acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
   for (int64_t p = p0; p < p1; ++p) {
@@ -801,7 +822,7 @@ __global__ void __launch_bounds__(128) onehot_seg_kernel(const uint16_t* __restr
 #pragma unroll
       for (int k = 0; k < 8; ++k) acc[k] = 0.f;
       if (p + 1 < p1) {
-        row = csr_row_of(off, V_l, p + 1);
+        row = hits[++h];
         row_beg = off[row];
         row_end = off[row + 1];
       }

@@ -1213,7 +1213,8 @@ slf_status s_end(Ctx& c, const SArgs& a, int reduction, float scale, float* loss
     } else {
       float* part = reinterpret_cast<float*>(c.ws + p.off_part);
       onehot_seg_kernel<<<dim3(segs, slabs), 128, 0, c.s>>>(reinterpret_cast<const uint16_t*>(a.X), a.H,
-                                                             off, idx, a.V_l, S, reduction, scale, 1.0f, hdr_of(c.ws),
+                                                             off, reinterpret_cast<const int32_t*>(c.ws + p.off_hits),
+                                                             idx, a.V_l, S, reduction, scale, 1.0f, hdr_of(c.ws),
                                                              part, reinterpret_cast<uint16_t*>(dW), rstd,
                                                              reinterpret_cast<const uint16_t*>(gam));
       onehot_join_kernel<<<dim3(segs, slabs), 128, 0, c.s>>>(a.H, off, a.V_l, S, reduction, scale,
