@@ -1494,24 +1494,36 @@ void shard_bounds(int64_t V, int g, int k, int64_t* v0, int64_t* vl) {
   *vl = b - a;
 }
 
-// The rank's workspace: [ schedule-S workspace (planner budget b) | dX partial 0 | dX partial 1 |
-// local stats C*16 | gathered stats g*C*16 ], b the largest planner budget whose total fits.
+// The rank's workspace: [ schedule-S workspace (planner budget b) | dX partial [2C][H] fp32 |
+// local stats 2C*16 | gathered stats g*2C*16 ], b the largest planner budget whose total fits.
+// Chunks are extended into dhidden's unwritten rows as in the fused call (up to 2C rows), so the
+// partial and the statistics buffers hold 2C rows; the partial is single-buffered (the chunk's dX
+// all-reduce shares the communicator stream with the next chunk's statistics all-gather, so it is
+// complete by the time the next chunk's combine runs anyway).
 struct ShardPlan {
   Plan p;
-  size_t b, off_dx0, off_dx1, off_st, off_all, total;
+  size_t b, off_dx, off_st, off_all, total;
   int64_t v0, V_l;
 };
 
 bool shard_layout(int64_t N, int64_t H, int64_t V_l, int g, size_t b, ShardPlan* sp) {
   if (!plan_s(N, H, V_l, b, &sp->p)) return false;
-  const int64_t C = sp->p.C;
+  const int64_t C2 = 2 * sp->p.C;
   sp->b = b;
-  sp->off_dx0 = align_up(sp->p.total, 1024);
-  sp->off_dx1 = align_up(sp->off_dx0 + (size_t)C * H * 4, 1024);
-  sp->off_st = align_up(sp->off_dx1 + (size_t)C * H * 4, 1024);
-  sp->off_all = align_up(sp->off_st + (size_t)C * 16, 1024);
-  sp->total = sp->off_all + (size_t)g * C * 16;
+  sp->off_dx = align_up(sp->p.total, 1024);
+  sp->off_st = align_up(sp->off_dx + (size_t)C2 * H * 4, 1024);
+  sp->off_all = align_up(sp->off_st + (size_t)C2 * 16, 1024);
+  sp->total = sp->off_all + (size_t)g * C2 * 16;
   return true;
+}
+
+// The chunks every rank cuts (identical on all ranks: the extension is computed with the largest
+// shard's stash row pitch).
+std::vector<SChunk> shard_chunks(const ShardPlan& sp, int64_t N, int64_t H, int64_t Vg, int g, bool extend,
+                                 uint8_t* dX) {
+  Plan pe = sp.p;
+  pe.ld_stash = (int64_t)align_up((size_t)((Vg + g - 1) / g), 8);
+  return s_chunks(pe, N, H, extend, dX);
 }
 
 // The largest planner budget whose layout fits `total` with a row chunk of at most c_cap (0: any).
@@ -1806,34 +1818,35 @@ slf_status phase_sharded(Ctx& c, const ShardPlan& sp, slf_comm cm, const void* X
   const Plan& p = c.plan;
   const int g = cm->world;
   const SArgs a{X, W, t, N, H, sp.V_l, sp.v0, Vg, ign};
-  float* dxb[2] = {reinterpret_cast<float*>(c.ws + sp.off_dx0), reinterpret_cast<float*>(c.ws + sp.off_dx1)};
+  float* dxp = reinterpret_cast<float*>(c.ws + sp.off_dx);  // this chunk's fp32 dX partial
   slf_shardstat* st = reinterpret_cast<slf_shardstat*>(c.ws + sp.off_st);
   slf_shardstat* st_all = reinterpret_cast<slf_shardstat*>(c.ws + sp.off_all);
   const slf_rowstat* rs = reinterpret_cast<const slf_rowstat*>(c.ws + p.off_rowstat);
   const bool p2p_dx = cm->p2p && (cm->p2p_mode & 2) && dX;
-  if (cm->p2p) SLF_TRY(p2p_ensure(cm, p.C, c.s));
+  if (cm->p2p) SLF_TRY(p2p_ensure(cm, 2 * p.C, c.s));
   // Peers' fp32 partial buffers are exported themselves (base + offset inside the caller's
   // allocation), not as this rank's workspace offsets: shard sizes differ by one vocabulary row when
   // g does not divide V, and the schedule-S layout (stash leading dimension, CSR arrays) before the
-  // partials then differs between ranks.  The second partial follows the first at the same distance
-  // on every rank (the same C and H).
+  // partials then differs between ranks.
   uint8_t* part_peer[P2P_MAX_RANKS] = {};
   uint8_t* dx_peer[P2P_MAX_RANKS] = {};
   if (p2p_dx) {
-    SLF_TRY(p2p_map(cm, c.ws + sp.off_dx0, c.s, part_peer));
+    SLF_TRY(p2p_map(cm, c.ws + sp.off_dx, c.s, part_peer));
     SLF_TRY(p2p_map(cm, dX, c.s, dx_peer));
   }
-  std::vector<unsigned long long> dx_ep(p.nCh, 0);
   SLF_TRY(s_begin(c, a, dW != nullptr));
-  std::vector<SChunk> chunks;
-  for (int64_t ch = 0; ch < p.nCh; ++ch) chunks.push_back(s_plain_chunk(p, N, ch));
-  // Per-row stash reference where X'^T fits in dhidden's rows after the chunk (not
-  // finalised yet); M_i needs the global target logit: each shard's contribution, one all-reduce.
+  // Extended chunks (as the fused call): the same on every rank.
+  std::vector<SChunk> chunks = shard_chunks(sp, N, H, Vg, g, dX != nullptr, reinterpret_cast<uint8_t*>(dX));
+  std::vector<unsigned long long> dx_ep(chunks.size(), 0);
+  const int64_t ld_max = (int64_t)align_up((size_t)((Vg + g - 1) / g), 8);
+  // Per-row stash reference where X'^T fits in dhidden's rows after the chunk and
+  // its extended stash (not finalised yet); M_i needs the global target logit: each shard's
+  // contribution, one all-reduce.
   static const bool classic = getenv("SLF_S_CLASSIC") != nullptr;
   bool any_ref = false;
   if (!classic && dX) {
     for (auto& k : chunks) {
-      const size_t lo = align_up((size_t)(k.r0 + k.rows) * H * 2, 1024);
+      const size_t lo = align_up((size_t)(k.r0 + k.rows) * H * 2 + (size_t)k.ext * ld_max * 2, 1024);
       const int64_t ld = (k.rows + 7) / 8 * 8;
       if (lo + (size_t)H * ld * 2 <= (size_t)N * H * 2) {
         k.ref = any_ref = true;
@@ -1857,56 +1870,63 @@ slf_status phase_sharded(Ctx& c, const ShardPlan& sp, slf_comm cm, const void* X
     mref_finish_kernel<<<(unsigned)((N + 255) / 256), 256, 0, c.s>>>(t, N, ign, Vg, mref);
     SLF_CUDA(cudaGetLastError());
   }
-  // LPT tables per chunk shape (full chunks and the tail), uploaded once per call
+  // LPT tables per distinct chunk shape (rows, ext), uploaded once per call
   SchedArena arena;
-  int tab[2] = {-1, -1};
+  std::vector<std::pair<std::pair<int64_t, int64_t>, int>> keys;
+  std::vector<int> tab(chunks.size(), -1);
   if (dX || dW) {
-    for (int j = 0; j < 2 && j < (int)chunks.size(); ++j) {
-      SChunk rep = j == 0 ? chunks[0] : chunks.back();
-      if (j == 1 && rep.rows == chunks[0].rows) { tab[1] = tab[0]; break; }
-      rep.index = std::max<int64_t>(rep.index, 1);
-      ProbSpec ps[2];
-      int n = 0;
-      SLF_TRY(s_build_bwd(c, a, rep, dX ? dxb[0] : nullptr, 1, dW, ps, &n));
-      tab[j] = arena.add(ps, n, usable_sms(c.dev) / cta_group());
+    for (size_t i = 0; i < chunks.size(); ++i) {
+      const auto key = std::make_pair(chunks[i].rows, chunks[i].ext);
+      int found = -1;
+      for (auto& kk : keys)
+        if (kk.first == key) found = kk.second;
+      if (found < 0) {
+        SChunk rep = chunks[i];
+        rep.index = std::max<int64_t>(rep.index, 1);
+        ProbSpec ps[2];
+        int n = 0;
+        SLF_TRY(s_build_bwd(c, a, rep, dX ? dxp : nullptr, 1, dW, ps, &n));
+        found = arena.add(ps, n, usable_sms(c.dev) / cta_group());
+        keys.push_back({key, found});
+      }
+      tab[i] = found;
     }
     if (arena.fits(c))
       SLF_TRY(arena.upload(c));
     else
-      tab[0] = tab[1] = -1;
+      std::fill(tab.begin(), tab.end(), -1);
   }
   float* loss_rows = s_loss_rows(c, reduction, loss_out);
-  int64_t pending[2] = {-1, -1};
-  auto finish = [&](int slot) -> slf_status {
-    const SChunk& k = chunks[pending[slot]];
-    SLF_TRY(comm_join(cm, slot, c.s));
-    SLF_TRY(dx_finalize_rows(c, dxb[slot], rs + k.r0, reinterpret_cast<uint8_t*>(dX) + (size_t)k.r0 * H * 2, k.rows,
-                             H));
-    pending[slot] = -1;
+  int64_t pending = -1;  // the chunk whose dX all-reduce is in flight (NCCL / callback path)
+  auto finish = [&]() -> slf_status {
+    const SChunk& k = chunks[pending];
+    SLF_TRY(comm_join(cm, 0, c.s));
+    SLF_TRY(dx_finalize_rows(c, dxp, rs + k.r0, reinterpret_cast<uint8_t*>(dX) + (size_t)k.r0 * H * 2, k.rows, H));
+    pending = -1;
     return SLF_OK;
   };
   for (size_t i = 0; i < chunks.size(); ++i) {
     const SChunk& k = chunks[i];
-    const int slot = (int)(i & 1);
     SLF_TRY(s_chunk_stats(c, a, k, st));
     const slf_shardstat* gathered = st_all;
     if (cm->p2p && (cm->p2p_mode & 1))
       SLF_TRY(p2p_allgather_stats(cm, st, k.rows, c.s, &gathered));
     else
       SLF_TRY(comm_allgather(cm, st, st_all, (size_t)k.rows * 16, c.s));
-    if (pending[slot] >= 0) SLF_TRY(finish(slot));
-    // P2P dX: the partial buffer of this slot is rewritten only once every rank has read it (the
-    // exchange kernels of chunk i-2 have all signalled)
-    if (p2p_dx && i >= 2) SLF_TRY(p2p_wait(cm, (int)P2P_DX_DONE_OFF, dx_ep[i - 2], c.s));
-    const int tb = (i + 1 == chunks.size() && k.rows != chunks[0].rows) ? tab[1] : tab[0];
-    SLF_TRY(s_chunk_bwd(c, a, k, gathered, g, reduction, scale, loss_rows, dX ? dxb[slot] : nullptr, 1, dW,
+    // the previous chunk's all-reduce is complete and its rows are written before this chunk's
+    // group rewrites the partial
+    if (pending >= 0) SLF_TRY(finish());
+    // P2P dX: the partial is rewritten only once every rank has read it (the exchange kernels of
+    // chunk i-1 have all signalled)
+    if (p2p_dx && i >= 1) SLF_TRY(p2p_wait(cm, (int)P2P_DX_DONE_OFF, dx_ep[i - 1], c.s));
+    const int tb = tab[i];
+    SLF_TRY(s_chunk_bwd(c, a, k, gathered, g, reduction, scale, loss_rows, dX ? dxp : nullptr, 1, dW,
                         tb >= 0 ? arena.dev(c, tb) : nullptr, tb >= 0 ? arena.tables[tb].second : 0));
     if (p2p_dx) {  // reduce-scatter + all-gather + bf16 finalize of this chunk, one kernel on the comm stream
       dx_ep[i] = ++cm->dx_epoch;
       DxArgs xa{};
-      const size_t off = slot ? sp.off_dx1 - sp.off_dx0 : 0;
       for (int r = 0; r < g; ++r) {
-        xa.part.p[r] = part_peer[r] + off;
+        xa.part.p[r] = part_peer[r];
         xa.dx.p[r] = dx_peer[r] + (size_t)k.r0 * H * 2;
         xa.flags.p[r] = cm->p2p_peer[r];
       }
@@ -1927,8 +1947,8 @@ slf_status phase_sharded(Ctx& c, const ShardPlan& sp, slf_comm cm, const void* X
       p2p_dx_exchange_kernel<<<blocks, 256, 0, xs>>>(xa);
       SLF_CUDA(cudaGetLastError());
     } else if (dX) {
-      SLF_TRY(comm_allreduce_start(cm, dxb[slot], (size_t)k.rows * H, slot, c.s));
-      pending[slot] = (int64_t)i;
+      SLF_TRY(comm_allreduce_start(cm, dxp, (size_t)k.rows * H, 0, c.s));
+      pending = (int64_t)i;
     }
   }
   if (p2p_dx && !chunks.empty()) {  // every rank's slices of every chunk are in this rank's dhidden
@@ -1938,10 +1958,7 @@ slf_status phase_sharded(Ctx& c, const ShardPlan& sp, slf_comm cm, const void* X
       SLF_CUDA(cudaStreamWaitEvent(c.s, cm->ev_ag, 0));
     }
   }
-  for (int j = 0; j < 2; ++j) {  // the older chunk first
-    const int slot = (int)((chunks.size() + j) & 1);
-    if (pending[slot] >= 0) SLF_TRY(finish(slot));
-  }
+  if (pending >= 0) SLF_TRY(finish());
   SLF_TRY(s_end(c, a, reduction, scale, loss_out, dW));
   if (cm->p2p && cm->p2p_buf) {  // a timed-out wait poisons this call's loss and fails the next call
     const int64_t n_loss = reduction == SLF_NONE ? N : 1;
@@ -2432,11 +2449,12 @@ slf_status slf_lce_sharded_plan_describe(int64_t N, int64_t H, int64_t V_global,
   if (!out || cap == 0) return fail(SLF_ERR_ARG, "null output buffer");
   ShardPlan sp;
   if (!shard_plan(N, H, V_global, world, rank, budget_bytes, &sp)) return fail(SLF_ERR_WORKSPACE, "no plan fits");
+  const size_t ext_chunks = shard_chunks(sp, N, H, V_global, world, true, nullptr).size();
   snprintf(out, cap,
            "schedule=S sharded world=%d rank=%d vocab_start=%lld V_local=%lld row_chunk=%lld n_chunks=%lld "
-           "planner_budget=%zu stash_bytes=%zu workspace=%zu",
-           world, rank, (long long)sp.v0, (long long)sp.V_l, (long long)sp.p.C, (long long)sp.p.nCh, sp.b,
-           (size_t)sp.p.C * sp.p.ld_stash * 2, sp.total);
+           "chunks_with_dhidden=%zu planner_budget=%zu stash_bytes=%zu workspace=%zu",
+           world, rank, (long long)sp.v0, (long long)sp.V_l, (long long)sp.p.C, (long long)sp.p.nCh, ext_chunks,
+           sp.b, (size_t)sp.p.C * sp.p.ld_stash * 2, sp.total);
   return SLF_OK;
 }
 

@@ -617,7 +617,7 @@ def test_native_sharded_callbacks(slf, tmp_path, g, red, budget):
     inp = synth.make_inputs(900, 256, 5000, seed=21, alpha=4.0, dist="zipf")
     Xo, Wo, to = oracle_inputs(inp)
     ref = oracle.lce(Xo, Wo, to, reduction=red)
-    nch = int(str(res[0]["plan"]).split("n_chunks=")[1].split()[0])
+    nch = int(str(res[0]["plan"]).split("chunks_with_dhidden=")[1].split()[0])  # extended chunks (§9)
     assert nch > 1
     # per chunk: one statistics all-gather and one dX all-reduce; per call: one all-reduce of the
     # rows' target logits when any chunk takes the per-row stash reference (it needs
@@ -661,6 +661,38 @@ def test_native_sharded_callbacks(slf, tmp_path, g, red, budget):
     if g == 2:  # GEMM launches on 140 of the SMs (8 left to the communicator): same tiles, same bits
         rs = _run_native_ranks(tmp_path / "rsv", g, red, budget, env_extra={"SLF_COMM_SMS": "8"})
         for a, b in zip(res, rs):
+            for k in ("loss", "dX", "dW"):
+                assert np.array_equal(a[k], b[k]), k
+
+
+@pytest.mark.parametrize("g,V,red", [(2, 3000, "mean"), (3, 3001, "none")])
+def test_native_sharded_extended_chunks(slf, tmp_path, g, V, red):
+    """The sharded call with chunks extended into dhidden's unwritten rows (N=2000, H=512: 8 plain
+    chunks become 6; V=3001 at g=3 makes the shards' stash pitches differ, and every rank must still
+    cut the same chunks): gloo callback transport, then the P2P statistics + dX exchanges — loss,
+    dhidden and dW bit-identical between the two for g=2 (two partials), against the oracle."""
+    N, H, budget = 2000, 512, 3 << 20
+    descs = [slf.sharded_plan_describe(N, H, V, g, r, budget) for r in range(g)]
+    nch = {int(d.split("chunks_with_dhidden=")[1].split()[0]) for d in descs}
+    plain = int(descs[0].split("n_chunks=")[1].split()[0])
+    assert len(nch) == 1 and nch.pop() < plain, descs
+    args = ("--N", str(N), "--H", str(H), "--V", str(V))
+    base = _run_native_ranks(tmp_path / "cb", g, red, budget, args)
+    px = _run_native_ranks(tmp_path / "p2p", g, red, budget, (*args, "--p2p", "3", "--calls", "2"))
+    inp = synth.make_inputs(N, H, V, seed=21, alpha=4.0, dist="zipf")
+    Xo, Wo, to = oracle_inputs(inp)
+    ref = oracle.lce(Xo, Wo, to, reduction=red)
+    tobf = lambda a: a.astype(np.int16).view(np.uint16).astype(np.uint32) << 16  # noqa: E731
+    for res in (base, px):
+        for r in res:
+            assert np.array_equal(r["loss"], res[0]["loss"]) and np.array_equal(r["dX"], res[0]["dX"])
+        assert_loss_close(res[0]["loss"] if red == "none" else float(res[0]["loss"].reshape(-1)[0]), ref["loss"], red)
+        assert rel_max_err(tobf(res[0]["dX"]).view(np.float32).astype(np.float64), ref["dX"]) <= GRAD_TOL
+        dW = np.concatenate([tobf(r["dW"]).view(np.float32).astype(np.float64) for r in res])
+        assert rel_max_err(dW, ref["dW"]) <= GRAD_TOL
+        assert np.all(res[0]["dX"][inp.t == -100] == 0)
+    if g == 2:
+        for a, b in zip(base, px):
             for k in ("loss", "dX", "dW"):
                 assert np.array_equal(a[k], b[k]), k
 
