@@ -22,42 +22,47 @@ __device__ __forceinline__ float coef_of(int reduction, float scale, unsigned lo
   return (reduction == SLF_MEAN) ? (n_valid ? scale / (float)n_valid : 0.f) : scale;
 }
 
-// This shard's per-row ShardStat {m, s, z_t, hit} of a chunk, FOUR lanes per row: lane q reads tiles
-// k = q, q+4, ... of the [tile][row] partials (coalesced across rows), max then sum, and the four
-// lanes combine with fixed-order shuffles (deterministic).  (A block per row spent most of its
-// time in block-wide barriers for the ~63 tiles of a g = 8 shard; one thread per row in its
-// dependent loads: both ~17 us per chunk at C = 3072.)
-__global__ void __launch_bounds__(128) shard_rows_tpr_kernel(const float2* __restrict__ partials, int tiles, int rows,
+// This shard's per-row ShardStat {m, s, z_t, hit} of a chunk: 8 rows per block of 256 threads, 32
+// lanes per row; lane p merges tiles p, p+32, ... of the [tile][row] partials online (for a fixed
+// tile the 8 rows' lanes read 8 consecutive partials, 64 bytes), then one thread per row merges the
+// 32 lane results in lane order (fixed, deterministic).  Round 1 used four lanes per row over 32
+// rows per block: fine for the ~63 tiles of a g = 8 shard, latency-bound for the 250-500 tiles of
+// g <= 2 (41 us per 1024-row chunk at world 1).
+constexpr int SR_ROWS = 8, SR_LANES = 32;
+__global__ void __launch_bounds__(256) shard_rows_tpr_kernel(const float2* __restrict__ partials, int tiles, int rows,
                                                              const float* __restrict__ zt,
                                                              const int32_t* __restrict__ t, int64_t vocab_start,
                                                              int64_t V_l, int32_t ignore_index,
                                                              slf_shardstat* __restrict__ out) {
-  const int q = threadIdx.x & 3;
-  const int i = blockIdx.x * 32 + (threadIdx.x >> 2);
-  const bool ok = i < rows;
-  float M = -INFINITY;
-  if (ok)
+  __shared__ float lm[SR_LANES][SR_ROWS], ls[SR_LANES][SR_ROWS];
+  const int rl = threadIdx.x % SR_ROWS, lane = threadIdx.x / SR_ROWS;
+  const int i0 = blockIdx.x * SR_ROWS;
+  {
+    const int i = i0 + rl;
+    float m = -INFINITY, sum = 0.f;
+    if (i < rows) {
 #pragma unroll 4
-    for (int k = q; k < tiles; k += 4) M = fmaxf(M, partials[(size_t)k * rows + i].x);
-  M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, 1));
-  M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, 2));
-  float S = 0.f;
-  if (ok)
-#pragma unroll 4
-    for (int k = q; k < tiles; k += 4) {
-      const float2 p = partials[(size_t)k * rows + i];
-      S += p.y * ex2((p.x - M) * LOG2E);
+      for (int k = lane; k < tiles; k += SR_LANES) {
+        const float2 p = partials[(size_t)k * rows + i];
+        const float nm = fmaxf(m, p.x);
+        sum = (m == -INFINITY ? 0.f : sum * ex2((m - nm) * LOG2E)) + p.y * ex2((p.x - nm) * LOG2E);
+        m = nm;
+      }
     }
-  // fixed order: (lane0 + lane1) + (lane2 + lane3)
-  const float s1 = __shfl_xor_sync(0xffffffffu, S, 1);
-  const float pair = (q & 1) ? s1 + S : S + s1;
-  const float s2 = __shfl_xor_sync(0xffffffffu, pair, 2);
-  const float tot = (q & 2) ? s2 + pair : pair + s2;
-  if (!ok || q != 0) return;
+    lm[lane][rl] = m;
+    ls[lane][rl] = sum;
+  }
+  __syncthreads();
+  if (threadIdx.x >= SR_ROWS || i0 + (int)threadIdx.x >= rows) return;
+  const int r = threadIdx.x, i = i0 + r;
+  float M = -INFINITY, S = 0.f;
+  for (int p = 0; p < SR_LANES; ++p) M = fmaxf(M, lm[p][r]);
+  for (int p = 0; p < SR_LANES; ++p)
+    if (lm[p][r] != -INFINITY) S += ls[p][r] * ex2((lm[p][r] - M) * LOG2E);
   const int32_t tt = t[i];
   const int64_t loc = (int64_t)tt - vocab_start;
   const bool hit = tt != ignore_index && loc >= 0 && loc < V_l;
-  out[i] = slf_shardstat{M, tot, hit ? zt[i] : 0.f, hit ? 1.f : 0.f};
+  out[i] = slf_shardstat{M, S, hit ? zt[i] : 0.f, hit ? 1.f : 0.f};
 }
 
 // One block (256 threads) per row of the chunk.  The row's global statistics come from the g

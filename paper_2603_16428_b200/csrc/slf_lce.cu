@@ -1044,8 +1044,8 @@ slf_status s_chunk_stats(Ctx& c, const SArgs& a, const SChunk& k, slf_shardstat*
   if (out) {  // shard statistics for the all-gather (vocab shards); one GPU merges in combine_transform
     const int tiles_v = (int)((a.V_l + BN - 1) / BN);
     ProfScope pr(SLF_PROF_LOCAL_COMBINE, c.s, 0.0, (double)rows * (tiles_v * 8.0 + 24));
-    shard_rows_tpr_kernel<<<(unsigned)((rows + 31) / 32), 128, 0, c.s>>>(part, tiles_v, (int)rows, zt + r0, a.t + r0,
-                                                                        a.vs, a.V_l, a.ign, out);
+    shard_rows_tpr_kernel<<<(unsigned)((rows + SR_ROWS - 1) / SR_ROWS), 256, 0, c.s>>>(
+        part, tiles_v, (int)rows, zt + r0, a.t + r0, a.vs, a.V_l, a.ign, out);
     SLF_CUDA(cudaGetLastError());
   }
   return SLF_OK;
