@@ -595,12 +595,13 @@ def main():
                      "unit": "TFLOP/s", "frac": achieved / peaks["sustained"], "traffic": traffic,
                      "peak_kind": "bf16 sustained (kernel timed inside a long step), " + peaks["source"],
                      "frac_of_burst": achieved / peaks["burst"],
-                     # context, not the roofline: the sustained peak was measured at the peak run's
-                     # median SM clock; this step ran at ck["sm_mhz"] (both power-capped)
-                     **({"frac_at_this_clock": achieved / (peaks["sustained"] * ck["sm_mhz"] / peaks["sustained_mhz"]),
-                         "clock_mhz_peak_run": peaks["sustained_mhz"], "clock_mhz_this_run": ck["sm_mhz"]}
+                     # context: the sustained peak was measured at the peak run's median SM clock
+                     # (nvidia-smi samples; under the power cap they lag the kernels' own clock, so no
+                     # clock-normalised fraction is derived from them — DESIGN.md §7b uses in-kernel
+                     # clock64 / globaltimer counters instead)
+                     **({"clock_mhz_peak_run": peaks["sustained_mhz"], "clock_mhz_this_run": ck["sm_mhz"]}
                         if peaks.get("sustained_mhz") and ck.get("sm_mhz") else {}),
-                     "ncu": "profiles/ncu_r02c.md (tensor pipe active % per kernel, DRAM bytes)"},
+                     "ncu": "profiles/ncu_r02e.md (tensor pipe active % per kernel, DRAM bytes)"},
         "kernels": kernels,
         "comm": ({"allgather_ms_per_step": kinds.get("comm_allgather", {}).get("ms", 0.0) / args.steps,
                   "allreduce_ms_per_step": kinds.get("comm_allreduce", {}).get("ms", 0.0) / args.steps,
