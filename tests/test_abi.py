@@ -176,7 +176,8 @@ def test_comm_host_api(L):
 
 
 @pytest.mark.parametrize("N,H,V,g,budget", [(8192, 512, 30001, 3, 13303808), (4096, 128, 7777, 4, 20054016),
-                                            (900, 256, 5000, 3, 3 << 20), (16384, 4096, 128257, 8, 0)])
+                                            (900, 256, 5000, 3, 3 << 20), (16384, 4096, 128257, 8, 0),
+                                            (2000, 512, 3001, 3, 3 << 20), (16384, 4096, 128255, 7, 0)])
 def test_sharded_ranks_share_row_chunks(L, N, H, V, g, budget):
     """Every rank cuts the same row chunks (the statistics are exchanged chunk by chunk) although
     shard sizes differ by one row when g does not divide V — the first two shapes made the ranks'
@@ -200,6 +201,11 @@ def test_sharded_ranks_share_row_chunks(L, N, H, V, g, budget):
         assert lce.workspace_bytes(N, H, m.v1 - m.v0, "S", b) + 2 * C * H * 4 + (g + 1) * C * 16 <= total
     assert len(set(cs_native)) == 1, cs_native
     assert len(set(cs_mod)) == 1, cs_mod
+    # the extended chunks are the same on every rank too: the extension uses the
+    # largest shard's stash pitch, not the rank's own
+    ext = {int(lce.sharded_plan_describe(N, H, V, g, r, budget).split("chunks_with_dhidden=")[1].split()[0])
+           for r in range(g)}
+    assert len(ext) == 1, ext
 
 
 def test_comm_and_dp_argument_errors(L):
