@@ -340,7 +340,9 @@ std::vector<int> lpt_table(const ProbSpec* ps, int n, int units, int* stride) {
     const int kb = (ps[p].a.K + BK - 1) / BK;
     // Cost in K-blocks plus a per-tile epilogue/pipeline overhead; a dW read-modify-write tile
     // pays extra for streaming the old partial (SLF_LPT_OVH / SLF_LPT_RMW tune the model).
-    static const int ovh = getenv("SLF_LPT_OVH") ? atoi(getenv("SLF_LPT_OVH")) : 4;
+    // 3: per-unit MMA spans of a Llama-8B group within 2 % (4: the dX units ended 3.5 % after the
+    // dW-only units; group 29.6 vs 29.9 ms per step, profiles/r02/lpt_ovh.md)
+    static const int ovh = getenv("SLF_LPT_OVH") ? atoi(getenv("SLF_LPT_OVH")) : 3;
     static const int rmw = getenv("SLF_LPT_RMW") ? atoi(getenv("SLF_LPT_RMW")) : 0;
     const int cost = kb + ovh + ((ps[p].epi == EPI_DW && ps[p].a.mode == 1) ? rmw : 0);
     for (int t = 0; t < ps[p].a.num_tiles; ++t) tiles.push_back({cost, id++});

@@ -92,6 +92,15 @@ def main():
     order = np.argsort(cpk)
     print("  slowest units:", [(int(i), round(float(cpk[i]))) for i in order[-6:]])
     print("  fastest units:", [(int(i), round(float(cpk[i]))) for i in order[:6]])
+    # load balance: each unit's MMA span (first to last issue) and work
+    ns = u[:, 7].astype(np.float64)
+    q = np.percentile(ns / 1e6, [0, 50, 100])
+    print(f"  unit MMA span ms           min {q[0]:.3f} med {q[1]:.3f} max {q[2]:.3f}")
+    by_span = np.argsort(ns)
+    print("  longest units (unit, span ms, tiles, K-blocks):",
+          [(int(i), round(float(ns[i]) / 1e6, 3), int(u[i, 6]), int(kb[i])) for i in by_span[-5:]])
+    print("  shortest units (unit, span ms, tiles, K-blocks):",
+          [(int(i), round(float(ns[i]) / 1e6, 3), int(u[i, 6]), int(kb[i])) for i in by_span[:5]])
 
 
 if __name__ == "__main__":
