@@ -298,21 +298,31 @@ slf_status slf_comm_status(slf_comm comm, int32_t* p2p_timeouts);
 /* Rank k of g owns W rows [V_global*k/g, V_global*(k+1)/g) (contiguous, as even as possible). */
 slf_status slf_shard_bounds(int64_t V_global, int world, int rank, int64_t* vocab_start, int64_t* V_local);
 
-/* Workspace of slf_lce_fwd_bwd_sharded for rank `rank` of `world`: the schedule-S workspace plus
- * two fp32 dX partials [C, H] (double-buffered so the all-reduce of chunk c overlaps chunk c+1)
- * and the local / gathered per-row statistics (C*16 and world*C*16 bytes), all within
- * `budget_bytes` (0: 5 % of the GLOBAL N*V_global*2 logits per GPU).  Host only;
- * 0 if nothing fits. */
+/* Workspace of slf_lce_fwd_bwd_sharded for rank `rank` of `world`: the schedule-S workspace and
+ * the local / gathered per-row statistics (2C*16 and world*2C*16 bytes), plus — only when that
+ * placement cuts fewer row chunks — a dedicated fp32 dX partial [2C, H]; otherwise each chunk's
+ * fp32 partial lives in dhidden's not-yet-written top rows, or (the last chunks) in the tail of the
+ * workspace stash.  All within `budget_bytes` (0: 5 % of the GLOBAL N*V_global*2
+ * logits per GPU).  Host only; 0 if nothing fits. */
 size_t slf_lce_sharded_workspace_bytes(int64_t N, int64_t H, int64_t V_global, int world, int rank,
                                        size_t budget_bytes);
-/* Writes the plan (chunk rows, chunks, planner budget, workspace bytes) into HOST `out`. */
+/* Writes the plan (chunk rows, chunks, partial placement, planner budget, workspace bytes) into
+ * HOST `out`. */
 slf_status slf_lce_sharded_plan_describe(int64_t N, int64_t H, int64_t V_global, int world, int rank,
                                          size_t budget_bytes, char* out, size_t cap);
+/* The row chunks the sharded call cuts when dhidden is requested (the same on every rank), as HOST
+ * int64 rows of 6: (first row, rows, extended-stash rows in dhidden, partial placement: byte offset
+ * into dhidden or -1 = workspace stash tail or -2 = workspace region, end in bytes of the dhidden
+ * rows X'^T may use, stash row pitch used for the extension).  At most `cap` rows are written;
+ * *n_chunks = the count.  Host only (planning; for tests and tools). */
+slf_status slf_lce_sharded_chunk_table(int64_t N, int64_t H, int64_t V_global, int world, int rank,
+                                       size_t budget_bytes, int64_t* out, int64_t cap, int64_t* n_chunks);
 
 /* The whole vocab-sharded step on this rank (schedule S, per row chunk c):
  *   stash GEMM + this shard's row statistics -> all-gather (16 B/row/rank, rank order)
  *   -> shard-order merge, loss rows, in-place G_P, grouped dX-partial (fp32) / dW (+)= launch
- *   -> all-reduce of the chunk's fp32 dX (comm stream, overlaps chunk c+1) -> bf16 dhidden rows;
+ *   -> all-reduce of the chunk's fp32 dX (comm stream, overlaps chunk c+1's stash GEMM) -> bf16
+ *   dhidden rows (the partial may live in dhidden's unwritten rows: slf_lce_sharded_chunk_table);
  *   after the chunks: one-hot dW correction (local targets) and the loss.
  *   hidden [N, H] bf16, targets [N] int32: identical on every rank            (read)
  *   weight_shard [V_local, H] bf16: this rank's rows (slf_shard_bounds)       (read)

@@ -27,7 +27,7 @@ EXPORTS = ["slf_lce_version", "slf_last_error_string", "slf_lce_workspace_bytes"
            "slf_debug_trace_read", "slf_debug_max_active_clusters", "slf_lce_fwd_bwd_ex", "slf_scale_bf16",
            "slf_lce_fwd_bwd_host", "slf_comm_get_unique_id", "slf_comm_init", "slf_comm_init_callbacks",
            "slf_comm_destroy", "slf_comm_rank", "slf_shard_bounds", "slf_lce_sharded_workspace_bytes",
-           "slf_lce_sharded_plan_describe", "slf_lce_fwd_bwd_sharded", "slf_comm_set_p2p", "slf_comm_status",
+           "slf_lce_sharded_plan_describe", "slf_lce_sharded_chunk_table", "slf_lce_fwd_bwd_sharded", "slf_comm_set_p2p", "slf_comm_status",
            "slf_lce_fwd_bwd_dp", "slf_target_csr_scratch_bytes", "slf_target_csr",
            "slf_rmsnorm_lce_workspace_bytes", "slf_rmsnorm_lce_plan_describe", "slf_rmsnorm_lce_fwd_bwd",
            "slf_scale_bf16_dev", "slf_rowstat_scale",
@@ -109,6 +109,7 @@ def _declare(lib):
         "slf_shard_bounds": (INT, [I64, INT, INT, ctypes.POINTER(I64), ctypes.POINTER(I64)]),
         "slf_lce_sharded_workspace_bytes": (SZ, [I64, I64, I64, INT, INT, SZ]),
         "slf_lce_sharded_plan_describe": (INT, [I64, I64, I64, INT, INT, SZ, ctypes.c_char_p, SZ]),
+        "slf_lce_sharded_chunk_table": (INT, [I64, I64, I64, INT, INT, SZ, P, I64, ctypes.POINTER(I64)]),
         "slf_lce_fwd_bwd_sharded": (INT, [P, P, P, I64, I64, I64, I32, INT, F32, P, P, P, P, SZ, SZ, P, P]),
         "slf_lce_fwd_bwd_dp": (INT, [P, P, P, I64, I64, I64, I32, INT, F32, P, P, P, P, SZ, INT, SZ, INT, P, P]),
         "slf_adam_last_error_string": (ctypes.c_char_p, []),

@@ -664,6 +664,10 @@ struct GroupArgs {
   // starts / ends the tile's accumulation, and its TMEM accumulator slot (the dX tiles
   // split into K segments interleaved with the dW tiles of the same vocabulary range)
   int il;
+  // early = 1: the operands are call inputs no kernel writes (the stash GEMM's hidden rows and W),
+  // so the TMA producer and the MMA issuer start while the previous grid drains (PDL); every other
+  // warp, the epilogue among them, waits for it before any global access
+  int early;
 };
 
 // One work item of a unit: a whole tile (il = 0), or a K segment of one (il = 1).
@@ -782,7 +786,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
   // PDL: let the next launch's CTAs start their prologue as soon as SMs free up, and wait for the
   // previous grid (whose outputs we read, and whose inputs we may overwrite) before any global access.
   griddep_launch_dependents();
-  griddep_wait();
+  if (!g.early || warp >= 2) griddep_wait();
 
   if (warp == 0) {
     if (lane == 0) {

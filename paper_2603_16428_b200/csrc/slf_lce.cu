@@ -237,6 +237,7 @@ struct ProbSpec {
   bool a_mn = false, b_mn = false;
   int a_split = NO_SPLIT, c_split = NO_SPLIT;
   bool a3d_force = false;  // ta is a 3-D MN-major map although M % 64 != 0 (over-read is harmless)
+  bool ro_operands = false;  // A and B are call inputs no kernel writes (GroupArgs::early)
 };
 
 int prof_kind_of(int epi) {
@@ -427,6 +428,8 @@ slf_status launch_group_cfg(DevInfo* dev, ProbSpec* ps, int n, cudaStream_t s, c
   g.sched = sched;
   g.sched_stride = sched_stride < 0 ? -sched_stride : sched_stride;  // negative: interleaved (seg) table
   g.il = sched && sched_stride < 0 ? 1 : 0;
+  static const bool early_off = getenv("SLF_EARLY_MAINLOOP") && atoi(getenv("SLF_EARLY_MAINLOOP")) == 0;
+  g.early = (!early_off && np == 1 && !sched && ps[0].ro_operands) ? 1 : 0;
   static const int dbg = getenv("SLF_DEBUG_EPI") ? atoi(getenv("SLF_DEBUG_EPI")) : 0;  // timing experiments only
   g.dbg = dbg & ~4;
   {  // SLF_DEBUG_TRACE=k: record the per-tile trace of the k-th group launch of this process
@@ -985,7 +988,13 @@ struct SChunk {
   const uint8_t* xrows = nullptr;  // the chunk's hidden rows when not X + r0 (fused RMSNorm: its y buffer)
   bool ref = false;       // per-row stash reference; false: the stash is rescaled in place
   uint8_t* xs = nullptr;  // with ref and dW: X'_chunk = bf16(f ⊙ X) [rows][H], the dW GEMM's B operand
+  // Vocab-sharded call only (shard_chunks): where the chunk's fp32 dX partial lives — a byte offset
+  // into dhidden (>= 0), PART_WS_TAIL (the workspace stash's tail) or PART_WS_REGION (a dedicated
+  // workspace region) — and the end (bytes into dhidden) of the rows X'^T may use.
+  int64_t part_off = -1;
+  size_t xt_lim = 0;
 };
+constexpr int64_t PART_WS_TAIL = -1, PART_WS_REGION = -2;
 
 SChunk s_plain_chunk(const Plan& p, int64_t N, int64_t ch) {
   const int64_t r0 = ch * p.C;
@@ -1042,6 +1051,7 @@ slf_status s_chunk_stats(Ctx& c, const SArgs& a, const SChunk& k, slf_shardstat*
   }
   ps.a = g;
   ps.epi = EPI_STASH;
+  ps.ro_operands = k.xrows == nullptr;  // X rows of the caller's hidden and W: the mainloop may start early
   SLF_TRY(launch_group(c.dev, &ps, 1, c.s));
   if (out) {  // shard statistics for the all-gather (vocab shards); one GPU merges in combine_transform
     const int tiles_v = (int)((a.V_l + BN - 1) / BN);
@@ -1506,36 +1516,134 @@ struct ShardPlan {
   Plan p;
   size_t b, off_dx, off_st, off_all, total;
   int64_t v0, V_l;
+  // The fp32 dX partial: with ws_part a dedicated [2C][H] workspace region (round 1
+  // layout); otherwise at the top of dhidden's unwritten rows, and for the last chunks (whose rows
+  // leave no room there) in the tail of the workspace stash, those chunks being r_tail rows.
+  bool ws_part = true;
+  int64_t r_tail = 0;
 };
 
-bool shard_layout(int64_t N, int64_t H, int64_t V_l, int g, size_t b, ShardPlan* sp) {
+// Stash row pitches of the largest / smallest shard (every rank cuts the same chunks from these).
+int64_t shard_ld_max(int64_t Vg, int g) { return (int64_t)align_up((size_t)((Vg + g - 1) / g), 8); }
+int64_t shard_ld_min(int64_t Vg, int g) { return (int64_t)align_up((size_t)(Vg / g), 8); }
+
+// Rows of a chunk whose stash and fp32 partial share the workspace stash of C rows on EVERY rank:
+// R * ld_max * 2 (rounded to 1 KB) + R * H * 4 <= C * ld_min * 2; a multiple of 8 (X'^T pitch).
+int64_t shard_tail_rows(int64_t C, int64_t H, int64_t ld_max, int64_t ld_min) {
+  const double cap = (double)C * ld_min * 2 - 1024;
+  int64_t R = (int64_t)(cap / ((double)ld_max * 2 + (double)H * 4)) / 8 * 8;
+  while (R > 0 && align_up((size_t)R * ld_max * 2, 1024) + (size_t)R * H * 4 > (size_t)C * ld_min * 2) R -= 8;
+  return std::max<int64_t>(R, 0);
+}
+
+bool shard_layout(int64_t N, int64_t H, int64_t V_l, int64_t Vg, int g, bool top, size_t b, ShardPlan* sp) {
   if (!plan_s(N, H, V_l, b, &sp->p)) return false;
   const int64_t C2 = 2 * sp->p.C;
+  const int64_t ldx = shard_ld_max(Vg, g), ldn = shard_ld_min(Vg, g);
+  // top: the partial leaves the workspace (shard_plan picks the layout with fewer chunks)
+  sp->ws_part = !top;
+  sp->r_tail = sp->ws_part ? 0 : shard_tail_rows(sp->p.C, H, ldx, ldn);
+  if (!sp->ws_part && sp->r_tail < 8) return false;
   sp->b = b;
   sp->off_dx = align_up(sp->p.total, 1024);
-  sp->off_st = align_up(sp->off_dx + (size_t)C2 * H * 4, 1024);
+  sp->off_st = align_up(sp->off_dx + (sp->ws_part ? (size_t)C2 * H * 4 : 0), 1024);
   sp->off_all = align_up(sp->off_st + (size_t)C2 * 16, 1024);
   sp->total = sp->off_all + (size_t)g * C2 * 16;
   return true;
 }
 
-// The chunks every rank cuts (identical on all ranks: the extension is computed with the largest
-// shard's stash row pitch).
+// The chunks every rank cuts (identical on all ranks: every size below is computed from the largest
+// shard's stash row pitch ld_max) and where each chunk's fp32 dX partial P lives.
+// With a dhidden (dX) and !ws_part, chunk c's partial goes to the top of dhidden, [D - rows*H*4, D)
+// with D = N*H*2, while it fits above the chunk's own rows, its extended stash and its X'^T (X'^T
+// must not overlap the partial its group writes); the previous chunk's partial is still in flight
+// (its all-reduce / P2P reads overlap this chunk's stash GEMM), so this chunk's extended stash also
+// stays below that one.  From the first chunk that does not fit on, chunks are r_tail rows (no
+// extension) and P sits in the workspace stash after the chunk's rows (the next chunk's stash GEMM
+// writes only the first r_tail rows, so it never touches the partial in flight).  X'^T (written by
+// the chunk's combine, after the previous chunk's partial was reduced and read) only has to stay
+// below the chunk's own partial.
 std::vector<SChunk> shard_chunks(const ShardPlan& sp, int64_t N, int64_t H, int64_t Vg, int g, bool extend,
                                  uint8_t* dX) {
   Plan pe = sp.p;
-  pe.ld_stash = (int64_t)align_up((size_t)((Vg + g - 1) / g), 8);
-  return s_chunks(pe, N, H, extend, dX);
+  pe.ld_stash = shard_ld_max(Vg, g);
+  if (!extend || sp.ws_part) {
+    std::vector<SChunk> v = s_chunks(pe, N, H, extend, dX);
+    for (SChunk& k : v) {
+      k.part_off = PART_WS_REGION;
+      k.xt_lim = (size_t)N * H * 2;
+    }
+    return v;
+  }
+  static const bool no_ext = getenv("SLF_S_NO_EXT") != nullptr;
+  static const int64_t ext_gran = getenv("SLF_S_EXT_GRAN") ? atoi(getenv("SLF_S_EXT_GRAN")) : 256;
+  const int64_t C = pe.C, ld = pe.ld_stash;
+  const size_t D = (size_t)N * H * 2;
+  std::vector<SChunk> chunks;
+  size_t prev_q = 0;  // bytes at dhidden's top held by the previous chunk's partial
+  bool tail = false;
+  int64_t tail_rows = 0;
+  for (int64_t r0 = 0, ci = 0; r0 < N; ++ci) {
+    SChunk k{ci, r0, 0, 0, nullptr, nullptr, 0};
+    const int64_t base = std::min(C, N - r0);
+    if (!tail) {
+      int64_t e = 0;
+      if (!no_ext && base == C) {
+        const int64_t free_rows = N - r0 - C;
+        e = free_rows > 0 ? std::min<int64_t>((free_rows * H) / (ld + H), C) / ext_gran * ext_gran : 0;
+      }
+      bool ok = false;
+      for (; e >= 0; e -= ext_gran) {
+        const int64_t rows = base + e;
+        const size_t end = (size_t)(r0 + rows) * H * 2;  // the chunk's own rows end here
+        if (end + (size_t)rows * H * 4 > D) continue;
+        // the extended stash is written while the previous partial is in flight and read while
+        // this chunk's partial is written
+        if (e > 0 && end + (size_t)e * ld * 2 > D - std::max(prev_q, (size_t)rows * H * 4)) continue;
+        ok = true;
+        k.rows = rows;
+        k.ext = e;
+        break;
+      }
+      if (!ok) {  // a shorter chunk (no extension) whose partial still fits above its rows
+        const int64_t r = (N - r0) / 3 / 256 * 256;
+        if (r > sp.r_tail) {
+          ok = true;
+          k.rows = r;
+          k.ext = 0;
+        }
+      }
+      if (ok) {
+        k.part_off = (int64_t)(D - (size_t)k.rows * H * 4);
+        k.xt_lim = (size_t)k.part_off;  // X'^T is written after the previous partial was consumed
+        if (k.ext) k.ext_base = dX ? dX + (size_t)(r0 + k.rows) * H * 2 : nullptr;
+        prev_q = (size_t)k.rows * H * 4;
+      } else {
+        tail = true;
+        const int64_t M = N - r0, n = (M + sp.r_tail - 1) / sp.r_tail;
+        tail_rows = std::min<int64_t>(sp.r_tail, ((M + n - 1) / n + 7) / 8 * 8);  // even split
+      }
+    }
+    if (tail) {
+      k.rows = std::min(tail_rows, N - r0);
+      k.part_off = PART_WS_TAIL;
+      k.xt_lim = D;
+    }
+    chunks.push_back(k);
+    r0 += k.rows;
+  }
+  return chunks;
 }
 
 // The largest planner budget whose layout fits `total` with a row chunk of at most c_cap (0: any).
-bool shard_fit(int64_t N, int64_t H, int64_t V_l, int g, size_t total, int64_t c_cap, ShardPlan* sp) {
+bool shard_fit(int64_t N, int64_t H, int64_t V_l, int64_t Vg, int g, bool top, size_t total, int64_t c_cap,
+               ShardPlan* sp) {
   auto ok = [&](size_t b) {
-    return shard_layout(N, H, V_l, g, b, sp) && sp->total <= total && (c_cap == 0 || sp->p.C <= c_cap);
+    return shard_layout(N, H, V_l, Vg, g, top, b, sp) && sp->total <= total && (c_cap == 0 || sp->p.C <= c_cap);
   };
   // bisection (the layout grows with the budget; 0 would mean the default): below the smallest
   // feasible planner budget the predicate counts as "go larger", so it is monotone
-  auto below_or_ok = [&](size_t b) { return !shard_layout(N, H, V_l, g, b, sp) || ok(b); };
+  auto below_or_ok = [&](size_t b) { return !shard_layout(N, H, V_l, Vg, g, top, b, sp) || ok(b); };
   size_t lo = 1, hi = total;
   while (lo < hi) {
     const size_t mid = lo + (hi - lo + 1) / 2;
@@ -1555,12 +1663,28 @@ bool shard_plan(int64_t N, int64_t H, int64_t Vg, int g, int k, size_t budget, S
   int64_t v0, vl;
   shard_bounds(Vg, g, k, &v0, &vl);
   const size_t total = budget ? budget : default_budget(N, Vg);
-  ShardPlan big, sp;
-  if (!shard_fit(N, H, (Vg + g - 1) / g, g, total, 0, &big)) return false;
-  if (!shard_fit(N, H, vl, g, total, big.p.C, &sp) || sp.p.C != big.p.C) return false;
-  sp.v0 = v0;
-  sp.V_l = vl;
-  *out = sp;
+  // Both placements of the fp32 dX partial (shard_layout); the one cutting fewer row chunks wins
+  // (ties: dhidden's top rows, the smaller workspace).  Everything here is the same on every rank.
+  ShardPlan best;
+  size_t best_n = 0;
+  static const char* force = getenv("SLF_SHARD_PART");  // "top" / "region": one placement only (tests)
+  for (const bool top : {true, false}) {
+    if (force && strcmp(force, top ? "region" : "top") == 0) continue;
+    ShardPlan big, sp;
+    if (!shard_fit(N, H, (Vg + g - 1) / g, Vg, g, top, total, 0, &big)) continue;
+    if (!shard_fit(N, H, vl, Vg, g, top, total, big.p.C, &sp) || sp.p.C != big.p.C) continue;
+    ShardPlan small;  // the same decision on every rank: the smallest shard must fit this C too
+    if (!shard_fit(N, H, Vg / g, Vg, g, top, total, big.p.C, &small) || small.p.C != big.p.C) continue;
+    sp.v0 = v0;
+    sp.V_l = vl;
+    const size_t n = shard_chunks(sp, N, H, Vg, g, true, nullptr).size();
+    if (best_n == 0 || n < best_n) {
+      best = sp;
+      best_n = n;
+    }
+  }
+  if (best_n == 0) return false;
+  *out = best;
   return true;
 }
 
@@ -1820,7 +1944,14 @@ slf_status phase_sharded(Ctx& c, const ShardPlan& sp, slf_comm cm, const void* X
   const Plan& p = c.plan;
   const int g = cm->world;
   const SArgs a{X, W, t, N, H, sp.V_l, sp.v0, Vg, ign};
-  float* dxp = reinterpret_cast<float*>(c.ws + sp.off_dx);  // this chunk's fp32 dX partial
+  // where a chunk's fp32 dX partial lives (shard_chunks): the workspace region (ws_part), the tail
+  // of the workspace stash after r_tail rows, or dhidden's top rows
+  const size_t tail_off = p.off_stash + align_up((size_t)sp.r_tail * shard_ld_max(Vg, g) * 2, 1024);
+  auto part_of = [&](const SChunk& k) -> float* {
+    if (k.part_off == PART_WS_REGION) return reinterpret_cast<float*>(c.ws + sp.off_dx);
+    if (k.part_off == PART_WS_TAIL) return reinterpret_cast<float*>(c.ws + tail_off);
+    return reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(dX) + k.part_off);
+  };
   slf_shardstat* st = reinterpret_cast<slf_shardstat*>(c.ws + sp.off_st);
   slf_shardstat* st_all = reinterpret_cast<slf_shardstat*>(c.ws + sp.off_all);
   const slf_rowstat* rs = reinterpret_cast<const slf_rowstat*>(c.ws + p.off_rowstat);
@@ -1832,8 +1963,8 @@ slf_status phase_sharded(Ctx& c, const ShardPlan& sp, slf_comm cm, const void* X
   // partials then differs between ranks.
   uint8_t* part_peer[P2P_MAX_RANKS] = {};
   uint8_t* dx_peer[P2P_MAX_RANKS] = {};
-  if (p2p_dx) {
-    SLF_TRY(p2p_map(cm, c.ws + sp.off_dx, c.s, part_peer));
+  if (p2p_dx) {  // the same maps on every rank (ws_part is a property of the problem)
+    SLF_TRY(p2p_map(cm, c.ws + (sp.ws_part ? sp.off_dx : tail_off), c.s, part_peer));
     SLF_TRY(p2p_map(cm, dX, c.s, dx_peer));
   }
   SLF_TRY(s_begin(c, a, dW != nullptr));
@@ -1850,7 +1981,7 @@ slf_status phase_sharded(Ctx& c, const ShardPlan& sp, slf_comm cm, const void* X
     for (auto& k : chunks) {
       const size_t lo = align_up((size_t)(k.r0 + k.rows) * H * 2 + (size_t)k.ext * ld_max * 2, 1024);
       const int64_t ld = (k.rows + 7) / 8 * 8;
-      if (lo + (size_t)H * ld * 2 <= (size_t)N * H * 2) {
+      if (lo + (size_t)H * ld * 2 <= k.xt_lim) {
         k.ref = any_ref = true;
         if (dW) {
           k.xt = reinterpret_cast<uint8_t*>(dX) + lo;
@@ -1887,7 +2018,7 @@ slf_status phase_sharded(Ctx& c, const ShardPlan& sp, slf_comm cm, const void* X
         rep.index = std::max<int64_t>(rep.index, 1);
         ProbSpec ps[2];
         int n = 0;
-        SLF_TRY(s_build_bwd(c, a, rep, dX ? dxp : nullptr, 1, dW, ps, &n));
+        SLF_TRY(s_build_bwd(c, a, rep, dX ? part_of(chunks[i]) : nullptr, 1, dW, ps, &n));
         found = arena.add(ps, n, usable_sms(c.dev) / cta_group());
         keys.push_back({key, found});
       }
@@ -1903,18 +2034,24 @@ slf_status phase_sharded(Ctx& c, const ShardPlan& sp, slf_comm cm, const void* X
   auto finish = [&]() -> slf_status {
     const SChunk& k = chunks[pending];
     SLF_TRY(comm_join(cm, 0, c.s));
-    SLF_TRY(dx_finalize_rows(c, dxp, rs + k.r0, reinterpret_cast<uint8_t*>(dX) + (size_t)k.r0 * H * 2, k.rows, H));
+    SLF_TRY(dx_finalize_rows(c, part_of(k), rs + k.r0, reinterpret_cast<uint8_t*>(dX) + (size_t)k.r0 * H * 2, k.rows, H));
     pending = -1;
     return SLF_OK;
   };
   for (size_t i = 0; i < chunks.size(); ++i) {
     const SChunk& k = chunks[i];
-    SLF_TRY(s_chunk_stats(c, a, k, st));
-    const slf_shardstat* gathered = st_all;
-    if (cm->p2p && (cm->p2p_mode & 1))
+    // World size 1: no statistics to exchange — the merge reads the stash GEMM's tile partials
+    // directly, as in the fused call (no shard-statistics pass, no all-gather).  The dX partial
+    // and its all-reduce stay (the transport's path).
+    const bool solo = g == 1;
+    SLF_TRY(s_chunk_stats(c, a, k, solo ? nullptr : st));
+    const slf_shardstat* gathered = solo ? nullptr : st_all;
+    if (solo) {
+    } else if (cm->p2p && (cm->p2p_mode & 1)) {
       SLF_TRY(p2p_allgather_stats(cm, st, k.rows, c.s, &gathered));
-    else
+    } else {
       SLF_TRY(comm_allgather(cm, st, st_all, (size_t)k.rows * 16, c.s));
+    }
     // the previous chunk's all-reduce is complete and its rows are written before this chunk's
     // group rewrites the partial
     if (pending >= 0) SLF_TRY(finish());
@@ -1922,13 +2059,14 @@ slf_status phase_sharded(Ctx& c, const ShardPlan& sp, slf_comm cm, const void* X
     // chunk i-1 have all signalled)
     if (p2p_dx && i >= 1) SLF_TRY(p2p_wait(cm, (int)P2P_DX_DONE_OFF, dx_ep[i - 1], c.s));
     const int tb = tab[i];
-    SLF_TRY(s_chunk_bwd(c, a, k, gathered, g, reduction, scale, loss_rows, dX ? dxp : nullptr, 1, dW,
+    float* dxp = dX ? part_of(k) : nullptr;
+    SLF_TRY(s_chunk_bwd(c, a, k, gathered, g, reduction, scale, loss_rows, dxp, 1, dW,
                         tb >= 0 ? arena.dev(c, tb) : nullptr, tb >= 0 ? arena.tables[tb].second : 0));
     if (p2p_dx) {  // reduce-scatter + all-gather + bf16 finalize of this chunk, one kernel on the comm stream
       dx_ep[i] = ++cm->dx_epoch;
       DxArgs xa{};
       for (int r = 0; r < g; ++r) {
-        xa.part.p[r] = part_peer[r];
+        xa.part.p[r] = k.part_off >= 0 ? dx_peer[r] + k.part_off : part_peer[r];
         xa.dx.p[r] = dx_peer[r] + (size_t)k.r0 * H * 2;
         xa.flags.p[r] = cm->p2p_peer[r];
       }
@@ -2451,12 +2589,34 @@ slf_status slf_lce_sharded_plan_describe(int64_t N, int64_t H, int64_t V_global,
   if (!out || cap == 0) return fail(SLF_ERR_ARG, "null output buffer");
   ShardPlan sp;
   if (!shard_plan(N, H, V_global, world, rank, budget_bytes, &sp)) return fail(SLF_ERR_WORKSPACE, "no plan fits");
-  const size_t ext_chunks = shard_chunks(sp, N, H, V_global, world, true, nullptr).size();
+  const std::vector<SChunk> ch = shard_chunks(sp, N, H, V_global, world, true, nullptr);
+  const size_t ext_chunks = ch.size();
+  size_t n_top = 0, n_tail = 0;
+  for (const SChunk& k : ch) {
+    n_top += k.part_off >= 0;
+    n_tail += k.part_off == PART_WS_TAIL;
+  }
   snprintf(out, cap,
            "schedule=S sharded world=%d rank=%d vocab_start=%lld V_local=%lld row_chunk=%lld n_chunks=%lld "
-           "chunks_with_dhidden=%zu planner_budget=%zu stash_bytes=%zu workspace=%zu",
+           "chunks_with_dhidden=%zu dx_partial=%s tail_rows=%lld top_chunks=%zu tail_chunks=%zu planner_budget=%zu stash_bytes=%zu workspace=%zu",
            world, rank, (long long)sp.v0, (long long)sp.V_l, (long long)sp.p.C, (long long)sp.p.nCh, ext_chunks,
-           sp.b, (size_t)sp.p.C * sp.p.ld_stash * 2, sp.total);
+           sp.ws_part ? "workspace" : "dhidden_top", (long long)sp.r_tail, n_top, n_tail, sp.b, (size_t)sp.p.C * sp.p.ld_stash * 2,
+           sp.total);
+  return SLF_OK;
+}
+
+slf_status slf_lce_sharded_chunk_table(int64_t N, int64_t H, int64_t V_global, int world, int rank,
+                                       size_t budget_bytes, int64_t* out, int64_t cap, int64_t* n_chunks) {
+  if (!n_chunks || (cap > 0 && !out)) return fail(SLF_ERR_ARG, "null output");
+  ShardPlan sp;
+  if (!shard_plan(N, H, V_global, world, rank, budget_bytes, &sp)) return fail(SLF_ERR_WORKSPACE, "no plan fits");
+  const std::vector<SChunk> ch = shard_chunks(sp, N, H, V_global, world, true, nullptr);
+  *n_chunks = (int64_t)ch.size();
+  for (int64_t i = 0; i < std::min<int64_t>(cap, (int64_t)ch.size()); ++i) {
+    const SChunk& k = ch[i];
+    const int64_t row[6] = {k.r0, k.rows, k.ext, k.part_off, (int64_t)k.xt_lim, shard_ld_max(V_global, world)};
+    memcpy(out + 6 * i, row, sizeof(row));
+  }
   return SLF_OK;
 }
 

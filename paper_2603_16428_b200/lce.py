@@ -535,6 +535,19 @@ def sharded_plan_describe(N: int, H: int, V_global: int, world: int, rank: int, 
     return buf.value.decode()
 
 
+def sharded_chunk_table(N: int, H: int, V_global: int, world: int, rank: int, budget_bytes: int = 0):
+    """The sharded call's row chunks (slf_lce_sharded_chunk_table): a list of dicts with r0, rows,
+    ext, part_off (bytes into dhidden; -1 workspace stash tail, -2 workspace region), xt_lim, ld."""
+    n = ctypes.c_int64(0)
+    check(lib().slf_lce_sharded_chunk_table(N, H, V_global, world, rank, budget_bytes, None, 0, ctypes.byref(n)),
+          "slf_lce_sharded_chunk_table")
+    buf = (ctypes.c_int64 * (6 * max(1, n.value)))()
+    check(lib().slf_lce_sharded_chunk_table(N, H, V_global, world, rank, budget_bytes, buf, n.value, ctypes.byref(n)),
+          "slf_lce_sharded_chunk_table")
+    keys = ("r0", "rows", "ext", "part_off", "xt_lim", "ld")
+    return [dict(zip(keys, buf[6 * i:6 * i + 6])) for i in range(n.value)]
+
+
 def lce_fwd_bwd_sharded(hidden, weight_shard, targets, V_global: int, comm: Comm, ignore_index: int = -100,
                         reduction: str = "mean", scale: float = 1.0, budget_bytes: int = 0, workspace=None,
                         out=None, need_dhidden: bool = True, need_dweight: bool = True, check_p2p: bool = True):

@@ -240,3 +240,50 @@ def test_rmsnorm_lce_planner(L, cfg):
     assert 0 < capped <= budget
     desc = lce.rmsnorm_lce_plan_describe(N, H, V, budget)
     assert desc.startswith("schedule=S rmsnorm_fused") and f"workspace={capped}" in desc
+
+
+@pytest.mark.parametrize("N,H,V,g,budget", [(16384, 4096, 128256, 1, 0), (16384, 4096, 128256, 2, 0),
+                                            (16384, 4096, 128256, 8, 0), (65536, 8192, 128256, 4, 0),
+                                            (65536, 12288, 32768, 8, 0), (32768, 3584, 152064, 1, 0),
+                                            (4096, 512, 3000, 2, 3 << 20), (4096, 256, 3001, 3, 3 << 20),
+                                            (900, 256, 5000, 2, 3 << 20), (8192, 512, 30001, 3, 13303808)])
+def test_sharded_partial_placement_invariants(L, N, H, V, g, budget):
+    """The vocab-sharded call's chunk table: identical on every rank; the chunks tile
+    [0, N); a chunk whose fp32 dX partial sits at dhidden's top has it disjoint from the chunk's own
+    rows and extended stash, the extended stash is also clear of the previous chunk's partial (in
+    flight during this chunk's stash GEMM), X'^T stays below the partial; chunks after the first
+    workspace-tail chunk are all tail chunks of at most tail_rows rows, whose stash and partial fit
+    the smallest shard's workspace stash."""
+    from paper_2603_16428_b200 import lce
+    tabs = [lce.sharded_chunk_table(N, H, V, g, r, budget) for r in range(g)]
+    assert all(t == tabs[0] for t in tabs)
+    desc = lce.sharded_plan_describe(N, H, V, g, 0, budget)
+    C = int(desc.split("row_chunk=")[1].split()[0])
+    r_tail = int(desc.split("tail_rows=")[1].split()[0])
+    assert len(tabs[0]) == int(desc.split("chunks_with_dhidden=")[1].split()[0])
+    D = N * H * 2
+    r0, prev_top, seen_tail = 0, None, False
+    for k in tabs[0]:
+        assert k["r0"] == r0 and k["rows"] > 0
+        r0 += k["rows"]
+        rows_end = (k["r0"] + k["rows"]) * H * 2
+        ext_end = rows_end + k["ext"] * k["ld"] * 2
+        if k["part_off"] >= 0:
+            assert not seen_tail
+            assert k["part_off"] + k["rows"] * H * 4 == D
+            assert rows_end <= k["part_off"] and ext_end <= k["part_off"] and k["xt_lim"] <= k["part_off"]
+            if k["ext"] and prev_top is not None:
+                assert ext_end <= prev_top
+            prev_top = k["part_off"]
+        elif k["part_off"] == -1:
+            seen_tail = True
+            assert k["ext"] == 0 and k["rows"] <= r_tail
+            prev_top = None
+        else:
+            assert k["part_off"] == -2 and "dx_partial=workspace" in desc
+        assert k["rows"] <= 2 * C
+    assert r0 == N
+    if "dx_partial=dhidden_top" in desc:
+        ld_max = tabs[0][0]["ld"]
+        ld_min = -(-(V // g) // 8) * 8
+        assert -(-(r_tail * ld_max * 2) // 1024) * 1024 + r_tail * H * 4 <= C * ld_min * 2

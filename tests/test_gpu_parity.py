@@ -672,13 +672,16 @@ def test_native_sharded_extended_chunks(slf, tmp_path, g, V, red):
     cut the same chunks): gloo callback transport, then the P2P statistics + dX exchanges — loss,
     dhidden and dW bit-identical between the two for g=2 (two partials), against the oracle."""
     N, H, budget = 2000, 512, 3 << 20
-    descs = [slf.sharded_plan_describe(N, H, V, g, r, budget) for r in range(g)]
+    args = ("--N", str(N), "--H", str(H), "--V", str(V))
+    # the dX partial in its dedicated workspace region (DESIGN.md §9b; the dhidden-top placement has
+    # its own test below), so the chunks are the workspace stash's, extended
+    env = {"SLF_SHARD_PART": "region"}
+    base = _run_native_ranks(tmp_path / "cb", g, red, budget, args, env_extra=env)
+    px = _run_native_ranks(tmp_path / "p2p", g, red, budget, (*args, "--p2p", "3", "--calls", "2"), env_extra=env)
+    descs = [str(r["plan"]) for r in base]
     nch = {int(d.split("chunks_with_dhidden=")[1].split()[0]) for d in descs}
     plain = int(descs[0].split("n_chunks=")[1].split()[0])
-    assert len(nch) == 1 and nch.pop() < plain, descs
-    args = ("--N", str(N), "--H", str(H), "--V", str(V))
-    base = _run_native_ranks(tmp_path / "cb", g, red, budget, args)
-    px = _run_native_ranks(tmp_path / "p2p", g, red, budget, (*args, "--p2p", "3", "--calls", "2"))
+    assert len(nch) == 1 and nch.pop() < plain and "dx_partial=workspace" in descs[0], descs
     inp = synth.make_inputs(N, H, V, seed=21, alpha=4.0, dist="zipf")
     Xo, Wo, to = oracle_inputs(inp)
     ref = oracle.lce(Xo, Wo, to, reduction=red)
@@ -814,6 +817,37 @@ def test_native_dp_callbacks(slf, tmp_path, g, red):
     assert rel_max_err(dX, ref["dX"]) <= GRAD_TOL
     assert rel_max_err(dW, ref["dW"]) <= GRAD_TOL
     assert np.all(np.concatenate([r["dX"] for r in res])[inp.t == -100] == 0)
+
+
+@pytest.mark.parametrize("N,H,V,g", [(4096, 512, 3000, 2), (4096, 256, 3001, 3)])
+def test_native_sharded_partial_placement(slf, tmp_path, N, H, V, g):
+    """Where the fp32 dX partial lives: the top of dhidden's unwritten rows (the
+    last chunks' partials in the workspace stash's tail) against the dedicated workspace region,
+    each forced with SLF_SHARD_PART; gloo transport, then the P2P statistics + dX exchanges (peers
+    read each chunk's partial at its placement); every rank identical; against the oracle."""
+    budget = 3 << 20
+    inp = synth.make_inputs(N, H, V, seed=21, alpha=4.0, dist="zipf")
+    Xo, Wo, to = oracle_inputs(inp)
+    ref = oracle.lce(Xo, Wo, to, reduction="mean")
+    tobf = lambda a: a.astype(np.int16).view(np.uint16).astype(np.uint32) << 16  # noqa: E731
+    args = ("--N", str(N), "--H", str(H), "--V", str(V))
+    for mode, word in (("top", "dhidden_top"), ("region", "workspace")):
+        for tag, extra in (("cb", ()), ("p2p", ("--p2p", "3", "--calls", "2"))):
+            res = _run_native_ranks(tmp_path / f"{mode}_{tag}", g, "mean", budget, (*args, *extra),
+                                    env_extra={"SLF_SHARD_PART": mode})
+            plan = str(res[0]["plan"])
+            assert f"dx_partial={word}" in plan, plan
+            if mode == "top":  # chunks of both kinds
+                assert int(plan.split("top_chunks=")[1].split()[0]) >= 2, plan
+                assert int(plan.split("tail_chunks=")[1].split()[0]) >= 1, plan
+            for r in res:
+                assert int(r["timeouts"]) == 0
+                assert np.array_equal(r["loss"], res[0]["loss"]) and np.array_equal(r["dX"], res[0]["dX"])
+            assert_loss_close(float(res[0]["loss"].reshape(-1)[0]), ref["loss"], "mean")
+            assert rel_max_err(tobf(res[0]["dX"]).view(np.float32).astype(np.float64), ref["dX"]) <= GRAD_TOL
+            dW = np.concatenate([tobf(r["dW"]).view(np.float32).astype(np.float64) for r in res])
+            assert rel_max_err(dW, ref["dW"]) <= GRAD_TOL
+            assert np.all(res[0]["dX"][inp.t == -100] == 0)
 
 
 @pytest.mark.parametrize("N,H,V", [(1, 8, 3), (257, 16, 130), (600, 72, 1000)])
