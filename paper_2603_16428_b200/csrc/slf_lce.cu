@@ -1051,7 +1051,13 @@ slf_status s_chunk_stats(Ctx& c, const SArgs& a, const SChunk& k, slf_shardstat*
   }
   ps.a = g;
   ps.epi = EPI_STASH;
-  ps.ro_operands = k.xrows == nullptr;  // X rows of the caller's hidden and W: the mainloop may start early
+  // The mainloop may start before the previous grid completes (GroupArgs::early) when its operands
+  // are the caller's hidden rows and W, which nothing in the call writes — and only from the second
+  // chunk on: a kernel of ours just before the call (e.g. rmsnorm_fwd producing the hidden rows)
+  // triggers its dependents early, so the first GEMM of a call must wait; a later chunk's stash GEMM
+  // launches only once the previous group launch is fully resident, i.e. after every earlier grid
+  // completed.  Host-input calls: not while chunks wait for their rows' copies (chunks 0-2).
+  ps.ro_operands = k.xrows == nullptr && k.index >= 1 && !(c.chunk_ready && k.index <= 2);
   SLF_TRY(launch_group(c.dev, &ps, 1, c.s));
   if (out) {  // shard statistics for the all-gather (vocab shards); one GPU merges in combine_transform
     const int tiles_v = (int)((a.V_l + BN - 1) / BN);
