@@ -850,6 +850,69 @@ def test_native_sharded_partial_placement(slf, tmp_path, N, H, V, g):
             assert np.all(res[0]["dX"][inp.t == -100] == 0)
 
 
+def _chunk_kinds(slf, N, H, V, g, budget):
+    """Kinds of the sharded call's row chunks (slf_lce_sharded_chunk_table): 'ext' (partial at
+    dhidden's top, extended stash), 'top', 'short' (top, fewer rows than C), 'tail' (partial in
+    the workspace stash tail), 'region'."""
+    C = int(slf.sharded_plan_describe(N, H, V, g, 0, budget).split("row_chunk=")[1].split()[0])
+    kinds = set()
+    for k in slf.sharded_chunk_table(N, H, V, g, 0, budget):
+        if k["part_off"] >= 0:
+            kinds.add("ext" if k["ext"] else ("short" if k["rows"] < C else "top"))
+        else:
+            kinds.add("tail" if k["part_off"] == -1 else "region")
+    return kinds
+
+
+@pytest.mark.parametrize("N,H,V,budget", [(5000, 512, 2000, 4 << 20), (6000, 256, 1000, 2 << 20)])
+@pytest.mark.parametrize("red", ["mean", "none"])
+@pytest.mark.parametrize("mode", [0, 3])
+def test_native_sharded_all_chunk_kinds_world1(slf, N, H, V, budget, red, mode):
+    """The native sharded call (NCCL, world 1; mode 3: P2P statistics + dX exchanges) at shapes whose
+    chunk table has every kind of chunk — extended with the partial at dhidden's top, plain top,
+    shortened top, and workspace-tail chunks — against the oracle."""
+    assert {"ext", "short", "tail"} <= _chunk_kinds(slf, N, H, V, 1, budget)
+    inp = synth.make_inputs(N, H, V, seed=37, alpha=4.0, dist="zipf")
+    X, W, t = to_dev(inp, torch)
+    comm = slf.Comm.nccl(slf.comm_unique_id(), 0, 1, torch.cuda.current_device())
+    try:
+        if mode:
+            comm.set_p2p(mode)
+        loss, dX, dW = slf.lce_fwd_bwd_sharded(X, W, t, V, comm, reduction=red, budget_bytes=budget)
+        torch.cuda.synchronize()
+        assert comm.p2p_timeouts() == 0
+    finally:
+        comm.close()
+    Xo, Wo, to = oracle_inputs(inp)
+    ref = oracle.lce(Xo, Wo, to, reduction=red)
+    assert_loss_close(loss.detach().cpu().numpy() if red == "none" else float(loss), ref["loss"], red)
+    assert rel_max_err(bf16_to_np64(dX), ref["dX"]) <= GRAD_TOL
+    assert rel_max_err(bf16_to_np64(dW), ref["dW"]) <= GRAD_TOL
+    assert np.all(dX.view(torch.int16).cpu().numpy()[inp.t == -100] == 0)
+
+
+def test_native_sharded_all_chunk_kinds_g2(slf, tmp_path):
+    """g = 2 ranks (processes on one GPU) at a shape whose chunk table mixes extended top,
+    plain top and workspace-tail chunks: gloo transport and P2P exchanges, every rank identical,
+    against the oracle."""
+    N, H, V, budget = 6000, 256, 1000, 2 << 20
+    assert {"ext", "top", "tail"} <= _chunk_kinds(slf, N, H, V, 2, budget)
+    inp = synth.make_inputs(N, H, V, seed=21, alpha=4.0, dist="zipf")
+    Xo, Wo, to = oracle_inputs(inp)
+    ref = oracle.lce(Xo, Wo, to, reduction="mean")
+    tobf = lambda a: a.astype(np.int16).view(np.uint16).astype(np.uint32) << 16  # noqa: E731
+    args = ("--N", str(N), "--H", str(H), "--V", str(V))
+    for tag, extra in (("cb", ()), ("p2p", ("--p2p", "3", "--calls", "2"))):
+        res = _run_native_ranks(tmp_path / tag, 2, "mean", budget, (*args, *extra))
+        for r in res:
+            assert int(r["timeouts"]) == 0
+            assert np.array_equal(r["loss"], res[0]["loss"]) and np.array_equal(r["dX"], res[0]["dX"])
+        assert_loss_close(float(res[0]["loss"].reshape(-1)[0]), ref["loss"], "mean")
+        assert rel_max_err(tobf(res[0]["dX"]).view(np.float32).astype(np.float64), ref["dX"]) <= GRAD_TOL
+        dW = np.concatenate([tobf(r["dW"]).view(np.float32).astype(np.float64) for r in res])
+        assert rel_max_err(dW, ref["dW"]) <= GRAD_TOL
+
+
 @pytest.mark.parametrize("N,H,V", [(1, 8, 3), (257, 16, 130), (600, 72, 1000)])
 @pytest.mark.parametrize("mode", [0, 3])
 def test_native_sharded_edges_world1(slf, N, H, V, mode):
