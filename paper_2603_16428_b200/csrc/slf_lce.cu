@@ -429,7 +429,6 @@ slf_status launch_group_cfg(DevInfo* dev, ProbSpec* ps, int n, cudaStream_t s, c
   g.sched_stride = sched_stride < 0 ? -sched_stride : sched_stride;  // negative: interleaved (seg) table
   g.il = sched && sched_stride < 0 ? 1 : 0;
   static const bool early_off = getenv("SLF_EARLY_MAINLOOP") && atoi(getenv("SLF_EARLY_MAINLOOP")) == 0;
-  g.early = (!early_off && np == 1 && !sched && ps[0].ro_operands) ? 1 : 0;
   static const int dbg = getenv("SLF_DEBUG_EPI") ? atoi(getenv("SLF_DEBUG_EPI")) : 0;  // timing experiments only
   g.dbg = dbg & ~4;
   {  // SLF_DEBUG_TRACE=k: record the per-tile trace of the k-th group launch of this process
@@ -438,6 +437,11 @@ slf_status launch_group_cfg(DevInfo* dev, ProbSpec* ps, int n, cudaStream_t s, c
     if (launch_no++ == trace_at) g.dbg |= 4;
   }
   const int units = sched ? usable_sms(dev) / CG : std::min(total, usable_sms(dev) / CG);
+  // Early mainloop (stash GEMM of chunk >= 1, s_chunk_stats): it can only launch once the previous
+  // group launch is fully resident, which cannot happen while the call's first stash GEMM still
+  // waits for the kernels before the call as long as this grid plus a full group grid exceed the
+  // SMs (not so with a tiny grid next to many SMs left to a communicator).
+  g.early = (!early_off && np == 1 && !sched && ps[0].ro_operands && units * CG + usable_sms(dev) > dev->sms) ? 1 : 0;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((unsigned)(units * CG));
   cfg.blockDim = dim3(GEMM_THREADS);
