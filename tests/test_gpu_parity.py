@@ -891,19 +891,19 @@ def test_native_sharded_all_chunk_kinds_world1(slf, N, H, V, budget, red, mode):
     assert np.all(dX.view(torch.int16).cpu().numpy()[inp.t == -100] == 0)
 
 
-def test_native_sharded_all_chunk_kinds_g2(slf, tmp_path):
-    """g = 2 ranks (processes on one GPU) at a shape whose chunk table mixes extended top,
-    plain top and workspace-tail chunks: gloo transport and P2P exchanges, every rank identical,
-    against the oracle."""
-    N, H, V, budget = 6000, 256, 1000, 2 << 20
-    assert {"ext", "top", "tail"} <= _chunk_kinds(slf, N, H, V, 2, budget)
+@pytest.mark.parametrize("g,N,H,V,budget", [(2, 6000, 256, 1000, 2 << 20), (4, 6000, 512, 4001, 4 << 20)])
+def test_native_sharded_all_chunk_kinds_multirank(slf, tmp_path, g, N, H, V, budget):
+    """g = 2 / 4 ranks (processes on one GPU; V = 4001 at g = 4: uneven shards) at shapes whose
+    chunk table mixes extended top, plain top and workspace-tail chunks: gloo transport and P2P
+    exchanges, every rank identical, against the oracle."""
+    assert {"ext", "top", "tail"} <= _chunk_kinds(slf, N, H, V, g, budget)
     inp = synth.make_inputs(N, H, V, seed=21, alpha=4.0, dist="zipf")
     Xo, Wo, to = oracle_inputs(inp)
     ref = oracle.lce(Xo, Wo, to, reduction="mean")
     tobf = lambda a: a.astype(np.int16).view(np.uint16).astype(np.uint32) << 16  # noqa: E731
     args = ("--N", str(N), "--H", str(H), "--V", str(V))
     for tag, extra in (("cb", ()), ("p2p", ("--p2p", "3", "--calls", "2"))):
-        res = _run_native_ranks(tmp_path / tag, 2, "mean", budget, (*args, *extra))
+        res = _run_native_ranks(tmp_path / tag, g, "mean", budget, (*args, *extra))
         for r in res:
             assert int(r["timeouts"]) == 0
             assert np.array_equal(r["loss"], res[0]["loss"]) and np.array_equal(r["dX"], res[0]["dX"])
