@@ -894,9 +894,10 @@ def test_native_sharded_all_chunk_kinds_world1(slf, N, H, V, budget, red, mode):
 @pytest.mark.parametrize("g,N,H,V,budget", [(2, 6000, 256, 1000, 2 << 20), (4, 6000, 512, 4001, 4 << 20)])
 def test_native_sharded_all_chunk_kinds_multirank(slf, tmp_path, g, N, H, V, budget):
     """g = 2 / 4 ranks (processes on one GPU; V = 4001 at g = 4: uneven shards) at shapes whose
-    chunk table mixes extended top, plain top and workspace-tail chunks: gloo transport and P2P
+    chunk table mixes extended top, plain or shortened top, and workspace-tail chunks: gloo transport and P2P
     exchanges, every rank identical, against the oracle."""
-    assert {"ext", "top", "tail"} <= _chunk_kinds(slf, N, H, V, g, budget)
+    kinds = _chunk_kinds(slf, N, H, V, g, budget)
+    assert {"ext", "tail"} <= kinds and kinds & {"top", "short"}, kinds
     inp = synth.make_inputs(N, H, V, seed=21, alpha=4.0, dist="zipf")
     Xo, Wo, to = oracle_inputs(inp)
     ref = oracle.lce(Xo, Wo, to, reduction="mean")
