@@ -62,7 +62,8 @@ class LMHeadTrainer:
         return b
 
     def step(self, x: torch.Tensor, targets: torch.Tensor, events=None):
-        """One step on the batch (x, targets): returns (loss [1] fp32, dx, dg) as device tensors.  The
+        """One step on the batch (x, targets): returns (loss [1] fp32, dx, dg) as device tensors —
+        the trainer's own buffers, rewritten by the next step() (clone them to keep them).  The
         dW of this step is being applied to W when it returns; the next step (or finish()) waits.
         `events` (optional pair of CUDA events) are recorded around the fused call (timing)."""
         b = self._buffers(x.shape[0])
