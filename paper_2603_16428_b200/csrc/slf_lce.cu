@@ -1158,6 +1158,9 @@ slf_status s_chunk_bwd(Ctx& c, const SArgs& a, const SChunk& k, const slf_shards
   const int64_t r0 = k.r0, rows = k.rows;
   const int tiles_v = (int)((a.V_l + BN - 1) / BN);
   static const bool skip_ct = getenv("SLF_DEBUG_EPI") && (atoi(getenv("SLF_DEBUG_EPI")) & 512);  // timing only
+  // SLF_DEBUG_CT2=1 (timing only): the combine launch is issued twice (same outputs) — its exposed
+  // cost per chunk is the step-time difference
+  static const int ct_reps = getenv("SLF_DEBUG_CT2") && atoi(getenv("SLF_DEBUG_CT2")) == 1 ? 2 : 1;
   if (k.ref && !skip_ct) {  // per-row stash reference: factors and X'_chunk, the stash stays as is
     ProfScope ps(SLF_PROF_COMBINE_TRANSFORM, c.s, 0.0, (double)rows * (tiles_v * 8.0 + a.H * 4.0 + 40.0));
     cudaLaunchConfig_t cfg = {};
@@ -1171,6 +1174,7 @@ slf_status s_chunk_bwd(Ctx& c, const SArgs& a, const SChunk& k, const slf_shards
     cfg.attrs = attr;
     cfg.numAttrs = 1;
     const uint8_t* xr = k.xrows ? k.xrows : reinterpret_cast<const uint8_t*>(a.X) + (size_t)r0 * a.H * 2;
+    for (int rep = 0; rep < (rms ? 1 : ct_reps); ++rep)
     SLF_CUDA(cudaLaunchKernelEx(
         &cfg, combine_scale_kernel, reinterpret_cast<const float2*>(c.ws + p.off_part), tiles_v, (int)rows,
         reinterpret_cast<const float*>(c.ws + p.off_zt) + r0, a.t + r0, a.V_l, p.ld_stash, a.ign, reduction, scale, 1.0f,
