@@ -18,10 +18,15 @@ struct WsHeader {
   unsigned int done;
   unsigned long long pad[6];
 };
-constexpr size_t WS_HEADER_BYTES = 64 * 1024;  // header (256 B) + block partial sums (double)
-// Blocks of 256 rows whose fp64 loss partials fit the header after its first 256 bytes (8160 blocks:
-// N <= 2,088,960 rows per statistics-combine call).
-constexpr int MAX_LOSS_BLOCKS = (int)((WS_HEADER_BYTES - 256) / 8);
+constexpr size_t WS_HEADER_BYTES = 64 * 1024;  // header (256 B) + block partial sums (double) + sync area
+// The header's last 8 KB: per-chunk synchronisation words of the in-kernel combine (schedule S,
+// DESIGN.md §6): [chunk] {arrivals, fallback flag}, zeroed at the start of every call.
+constexpr size_t WS_SYNC_BYTES = 8 * 1024;
+constexpr size_t WS_SYNC_OFF = WS_HEADER_BYTES - WS_SYNC_BYTES;
+constexpr int WS_SYNC_SLOTS = (int)(WS_SYNC_BYTES / 8);
+// Blocks of 256 rows whose fp64 loss partials fit the header between its first 256 bytes and the
+// sync area (7136 blocks: N <= 1,826,816 rows per statistics-combine call).
+constexpr int MAX_LOSS_BLOCKS = (int)((WS_SYNC_OFF - 256) / 8);
 
 // One block of 1024 threads: 16-byte vector loads of the targets.
 __global__ void __launch_bounds__(1024) prep_targets_kernel(const int32_t* __restrict__ t, int64_t N,

@@ -23,6 +23,7 @@
 #include <cstdint>
 
 #include "ptx.cuh"
+#include "combine_dev.cuh"
 #include "../../include/slf_lce.h"
 
 namespace slf {
@@ -85,11 +86,13 @@ struct GemmArgs {
   // own max); EPI_DXS multiplies the row's accumulator by fac[r].  Null: per-tile max / factor 1.
   const float* mref;
   const float* fac;
+  // EPI_STASH of a chunk whose combine runs inside the group launch (CombineJob): *fb_flag := 1 when
+  // a row of the tile may need the combine's in-place rescale (its dX tiles then wait for it)
+  unsigned* fb_flag;
+  const WsHeader* fb_hdr;
+  int fb_red;
+  float fb_scale, fb_gscale;
 };
-
-// A tile whose max exceeds the row reference by more than this keeps its own max in the stash
-// (exp(70) = 2.5e30: far from the bf16 / fp32 overflow at exp(88.7)).
-constexpr float STASH_REF_SLACK = 70.f;
 
 __device__ __forceinline__ void tile_coords(int tile, const GemmArgs& a, int& m_blk, int& n_blk) {
   // Grouped raster: walk group_m row tiles down before stepping to the next column tile, so one
@@ -542,6 +545,20 @@ __device__ __forceinline__ void epilogue_stash_tma(const GemmArgs& a, const CUte
   if (a.mref && row_ok) {
     const float M = a.mref[r];
     if (!(mx - M > STASH_REF_SLACK)) cmul = ex2((mx - M) * LOG2E);
+    if (a.fb_flag) {
+      // In-kernel combine (CombineJob): the group's dX tiles read this stash before the combine ran,
+      // which is only right if no row needs its in-place rescale.  A row may need it when a tile
+      // kept its own max (mx - M > SLACK) or when f = cg exp(M - lse) can leave [1e-30, 1e30]:
+      // M - lse <= M - z_t = STASH_REF_SHIFT (40) bounds it above; lse <= max_t m_t + ln V bounds it
+      // below, so f >= 1e-30 (with a factor e of margin) while mx - M <= ln|cg| + 68 - ln V.
+      float lim = STASH_REF_SLACK;
+      const float cg = fabsf(coef_of(a.fb_red, a.fb_scale, a.fb_hdr->n_valid) * a.fb_gscale);
+      if (cg != 0.f) {
+        if (!(cg * 2.36e17f <= 1e29f)) lim = -INFINITY;
+        else lim = fminf(lim, __logf(cg) + 68.f - __logf((float)a.N));
+      }
+      if (!(mx - M <= lim)) atomicOr(a.fb_flag, 1u);
+    }
   }
   // Per 64-column chunk: two 32-column TMEM loads -> exp -> bf16 pairs -> one staging buffer ->
   // one TMA store, chunk-pipelined as the dW epilogue: one bulk group per chunk, buffers by a running
@@ -668,6 +685,12 @@ struct GroupArgs {
   // so the TMA producer and the MMA issuer start while the previous grid drains (PDL); every other
   // warp, the epilogue among them, waits for it before any global access
   int early;
+  // cj_on = 1: the chunk's per-row combine runs here: the epilogue warps of every CTA
+  // combine their share of rows first and arrive on cj.counter; the producer waits for all arrivals
+  // before the first dW tile (X'^T) — and before anything when the stash flagged a rescale — and the
+  // epilogues before their first tile (RowStat, row factors)
+  int cj_on;
+  CombineJob cj;
 };
 
 // One work item of a unit: a whole tile (il = 0), or a K segment of one (il = 1).
@@ -795,11 +818,20 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
       uint32_t stage = 0, phase = 0;
       unsigned long long u_ew = 0;
       const bool tu = (g.dbg & 4) && unit < TRACE_UNITS && rank == 0;
+      // in-kernel combine: the stash flagged a possible in-place rescale -> wait before any load;
+      // else only the dW tiles (B = X'^T, written by the combine) wait
+      bool cj_wait = g.cj_on != 0;
+      const bool cj_all = cj_wait && ld_relaxed_u32(g.cj.fb_flag) != 0;
       TileIter it(g, unit, units);
       for (Item item = it.next_item(); item.tile >= 0; item = it.next_item()) {
         const int tile = item.tile;
         const int pi = prob_of(g, tile);
         const Prob& P = g.p[pi];
+        if (cj_wait && (cj_all || P.epi == EPI_DW)) {
+          spin_until_geq(g.cj.counter, gridDim.x);
+          fence_proxy_async_global();  // the combine's generic stores before these TMA reads
+          cj_wait = false;
+        }
         const CUtensorMap* tA = &tm.m[MAPS_PER_PROB * pi];
         const CUtensorMap* tB = &tm.m[MAPS_PER_PROB * pi + 1];
         const CUtensorMap* tA2 = &tm.m[MAPS_PER_PROB * pi + 3];
@@ -976,6 +1008,17 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
   } else if (warp >= 4) {
     // ===== epilogue: thread = TMEM lane = output row =====
     const uint32_t ew = warp - 4;
+    if (g.cj_on) {  // the chunk's combine, rows spread over every CTA of the launch
+      const int tid = (int)(ew * 32 + lane);
+      combine_rows_dev(g.cj, (int)blockIdx.x, (int)gridDim.x, tid, 1, reinterpret_cast<float*>(stg));
+      __threadfence();
+      named_bar_sync(1, 128);
+      if (tid == 0) {
+        atomicAdd(g.cj.counter, 1u);
+        spin_until_geq(g.cj.counter, gridDim.x);  // RowStat / row factors of every row
+      }
+      named_bar_sync(1, 128);
+    }
     uint32_t local = 0;
     uint32_t sphase = 0;  // parity bits of the two staging barriers
     uint32_t sq = 0;      // staging-buffer sequence of the chunk-pipelined dW epilogue

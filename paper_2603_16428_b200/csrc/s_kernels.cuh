@@ -13,14 +13,11 @@
 
 #include "../../include/slf_lce.h"
 #include "aux_kernels.cuh"
+#include "combine_dev.cuh"
 #include "ptx.cuh"
 #include "rmsnorm.cuh"
 
 namespace slf {
-
-__device__ __forceinline__ float coef_of(int reduction, float scale, unsigned long long n_valid) {
-  return (reduction == SLF_MEAN) ? (n_valid ? scale / (float)n_valid : 0.f) : scale;
-}
 
 // This shard's per-row ShardStat {m, s, z_t, hit} of a chunk: 8 rows per block of 256 threads, 32
 // lanes per row; lane p merges tiles p, p+32, ... of the [tile][row] partials online (for a fixed

@@ -391,7 +391,7 @@ struct ReserveSms {
 
 template <int CG, int NB>
 slf_status launch_group_cfg(DevInfo* dev, ProbSpec* ps, int n, cudaStream_t s, const int* sched, int sched_stride,
-                            int prof_kind) {
+                            int prof_kind, const CombineJob* cj = nullptr) {
   using C = Cfg<CG, NB>;
   auto kfn = lce_group_kernel<CG, NB>;
   {
@@ -428,6 +428,10 @@ slf_status launch_group_cfg(DevInfo* dev, ProbSpec* ps, int n, cudaStream_t s, c
   g.sched = sched;
   g.sched_stride = sched_stride < 0 ? -sched_stride : sched_stride;  // negative: interleaved (seg) table
   g.il = sched && sched_stride < 0 ? 1 : 0;
+  if (cj) {  // every CTA of the launch arrives once; the grid is one persistent CTA per usable SM
+    g.cj_on = 1;
+    g.cj = *cj;
+  }
   static const bool early_off = getenv("SLF_EARLY_MAINLOOP") && atoi(getenv("SLF_EARLY_MAINLOOP")) == 0;
   static const int dbg = getenv("SLF_DEBUG_EPI") ? atoi(getenv("SLF_DEBUG_EPI")) : 0;  // timing experiments only
   g.dbg = dbg & ~4;
@@ -479,16 +483,16 @@ int dw_acc_mode() {
 // buffers (5-stage ring); every other launch takes the 6-stage ring (SLF_STAGING=2|4 forces one,
 // timing experiments only).
 slf_status launch_group(DevInfo* dev, ProbSpec* ps, int n, cudaStream_t s, const int* sched = nullptr,
-                        int sched_stride = 0, int prof_kind = -1) {
+                        int sched_stride = 0, int prof_kind = -1, const CombineJob* cj = nullptr) {
   bool dw = false;
   for (int p = 0; p < n; ++p) dw = dw || (ps[p].epi == EPI_DW && ps[p].a.mode == 1);
   static const int force = getenv("SLF_STAGING") ? atoi(getenv("SLF_STAGING")) : 0;
   const bool four = force ? force == 4 : dw;
   if (cta_group() == 2)
-    return four ? launch_group_cfg<2, 4>(dev, ps, n, s, sched, sched_stride, prof_kind)
-                : launch_group_cfg<2, 2>(dev, ps, n, s, sched, sched_stride, prof_kind);
-  return four ? launch_group_cfg<1, 4>(dev, ps, n, s, sched, sched_stride, prof_kind)
-              : launch_group_cfg<1, 2>(dev, ps, n, s, sched, sched_stride, prof_kind);
+    return four ? launch_group_cfg<2, 4>(dev, ps, n, s, sched, sched_stride, prof_kind, cj)
+                : launch_group_cfg<2, 2>(dev, ps, n, s, sched, sched_stride, prof_kind, cj);
+  return four ? launch_group_cfg<1, 4>(dev, ps, n, s, sched, sched_stride, prof_kind, cj)
+              : launch_group_cfg<1, 2>(dev, ps, n, s, sched, sched_stride, prof_kind, cj);
 }
 
 template <int EPI, bool A_MN, bool B_MN>
@@ -651,6 +655,8 @@ struct Ctx {
   // tile tables) are queued — copies share the H2D engine in FIFO order
   std::function<slf_status()> enqueue_inputs;
   std::function<slf_status()> after_prep;  // e.g. the data-parallel all-reduce of n_valid
+  int cj_red = SLF_MEAN;  // reduction / scale of the call, for the stash epilogue's rescale bound
+  float cj_scale = 1.f;
 };
 
 WsHeader* hdr_of(uint8_t* ws) { return reinterpret_cast<WsHeader*>(ws); }
@@ -968,6 +974,7 @@ slf_status build_csr(cudaStream_t st, const int32_t* t, int64_t N, int32_t ign, 
 
 slf_status s_begin(Ctx& c, const SArgs& a, bool need_dw) {
   const Plan& p = c.plan;
+  SLF_CUDA(cudaMemsetAsync(c.ws + WS_SYNC_OFF, 0, WS_SYNC_BYTES, c.s));  // in-kernel combine sync words
   SLF_TRY(launch_prep(c, a.t, a.N, a.ign, a.Vg));
   if (need_dw) {
     // scratch: the tile-partials + stash region, idle until the first chunk's stash GEMM; span
@@ -997,6 +1004,7 @@ struct SChunk {
   // workspace region) — and the end (bytes into dhidden) of the rows X'^T may use.
   int64_t part_off = -1;
   size_t xt_lim = 0;
+  bool cj = false;  // the chunk's combine runs inside its group launch (CombineJob)
 };
 constexpr int64_t PART_WS_TAIL = -1, PART_WS_REGION = -2;
 
@@ -1052,6 +1060,13 @@ slf_status s_chunk_stats(Ctx& c, const SArgs& a, const SChunk& k, slf_shardstat*
   if (k.ext) {
     SLF_TRY(tmap_kmajor(&ps.tc2, k.ext_base, a.V_l, k.ext, p.ld_stash, BM));
     ps.c_split = (int)main_rows;
+  }
+  if (k.cj) {  // the group launch's dX tiles may start before the combine: flag possible rescales
+    g.fb_flag = reinterpret_cast<unsigned*>(c.ws + WS_SYNC_OFF) + 2 * k.index + 1;
+    g.fb_hdr = hdr_of(c.ws);
+    g.fb_red = c.cj_red;
+    g.fb_scale = c.cj_scale;
+    g.fb_gscale = 1.0f;
   }
   ps.a = g;
   ps.epi = EPI_STASH;
@@ -1161,7 +1176,40 @@ slf_status s_chunk_bwd(Ctx& c, const SArgs& a, const SChunk& k, const slf_shards
   // SLF_DEBUG_CT2=1 (timing only): the combine launch is issued twice (same outputs) — its exposed
   // cost per chunk is the step-time difference
   static const int ct_reps = getenv("SLF_DEBUG_CT2") && atoi(getenv("SLF_DEBUG_CT2")) == 1 ? 2 : 1;
-  if (k.ref && !skip_ct) {  // per-row stash reference: factors and X'_chunk, the stash stays as is
+  // In-kernel combine (k.cj): the group launch's epilogue warps do the work of combine_scale_kernel
+  // below, and its dX tiles start on the stash without waiting for it
+  CombineJob cj{};
+  const bool in_kernel = k.cj && !skip_ct && !rms && !st && g == 1 && (dXc || dW);
+  if (in_kernel) {
+    cj.partials = reinterpret_cast<const float2*>(c.ws + p.off_part);
+    cj.zt = reinterpret_cast<const float*>(c.ws + p.off_zt) + r0;
+    cj.t = a.t + r0;
+    cj.mref = reinterpret_cast<const float*>(c.ws + p.off_mref) + r0;
+    cj.hdr = hdr_of(c.ws);
+    cj.loss_rows = loss_rows_all + r0;
+    cj.rowstat = reinterpret_cast<slf_rowstat*>(c.ws + p.off_rowstat) + r0;
+    cj.fac = reinterpret_cast<float*>(c.ws + p.off_fac) + r0;
+    cj.stash = reinterpret_cast<uint16_t*>(c.ws + p.off_stash);
+    cj.stash2 = reinterpret_cast<uint16_t*>(k.ext_base);
+    cj.xrows = reinterpret_cast<const uint16_t*>(k.xrows ? k.xrows
+                                                         : reinterpret_cast<const uint8_t*>(a.X) + (size_t)r0 * a.H * 2);
+    cj.xs = reinterpret_cast<uint16_t*>(k.xt);
+    cj.V_l = a.V_l;
+    cj.ld_stash = p.ld_stash;
+    cj.H = a.H;
+    cj.ld_xst = k.xt ? k.ld_xt : 0;
+    cj.tiles = tiles_v;
+    cj.rows = (int)rows;
+    cj.split = (int)(rows - k.ext);
+    cj.reduction = reduction;
+    cj.ign = a.ign;
+    cj.scale = scale;
+    cj.grad_scale = 1.0f;
+    cj.counter = reinterpret_cast<unsigned*>(c.ws + WS_SYNC_OFF) + 2 * k.index;
+    cj.fb_flag = cj.counter + 1;
+  }
+  if (in_kernel) {
+  } else if (k.ref && !skip_ct) {  // per-row stash reference: factors and X'_chunk, the stash stays as is
     ProfScope ps(SLF_PROF_COMBINE_TRANSFORM, c.s, 0.0, (double)rows * (tiles_v * 8.0 + a.H * 4.0 + 40.0));
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3((unsigned)((rows + CS_ROWS - 1) / CS_ROWS + (rms ? rms_blocks_of(*rms) : 0)));
@@ -1214,7 +1262,8 @@ slf_status s_chunk_bwd(Ctx& c, const SArgs& a, const SChunk& k, const slf_shards
     sched = arena.dev(c, t);
     sched_stride = arena.tables[t].second;
   }
-  return launch_group(c.dev, ps, n, c.s, sched, sched_stride, n == 2 ? SLF_PROF_GEMM_GROUP : -1);
+  return launch_group(c.dev, ps, n, c.s, sched, sched_stride, n == 2 ? SLF_PROF_GEMM_GROUP : -1,
+                      in_kernel ? &cj : nullptr);
 }
 
 slf_status s_end(Ctx& c, const SArgs& a, int reduction, float scale, float* loss_out, void* dW,
@@ -1423,6 +1472,13 @@ slf_status phase_s(Ctx& c, const void* X, const void* W, const int32_t* t, int64
       }
     }
   }
+  // In-kernel combine (SLF_INKERNEL_COMBINE=0: the separate combine launch): chunks
+  // with the per-row reference whose X' is X'^T (or no dW), no RMSNorm jobs.
+  static const bool cj_off = getenv("SLF_INKERNEL_COMBINE") && atoi(getenv("SLF_INKERNEL_COMBINE")) == 0;
+  c.cj_red = reduction;
+  c.cj_scale = scale;
+  if (!rf && !cj_off && (V + BN - 1) / BN <= 7000)
+    for (auto& k : chunks) k.cj = k.ref && (!dW || k.xt) && k.index < WS_SYNC_SLOTS;
   // M_i = x_i . W[t_i] + shift: for every row at once when the inputs are resident; chunk by chunk,
   // after the chunk's rows arrived, in the host-input call
   auto launch_mref = [&](int64_t r0, int64_t rows) -> slf_status {
