@@ -176,7 +176,8 @@ __device__ __noinline__ void combine_rows_dev(const CombineJob& cj, int first, i
     // X'^T[h][i0 .. i0 + 4): 8 consecutive columns per thread, four 16-byte row loads, a register
     // transpose, eight 8-byte column stores (f = 1 for rescaled rows: an exact copy)
     const int nr = min(CJ_ROWS, rows - i0);
-    if (nr == CJ_ROWS && (cj.H % 8) == 0) {
+    if (!cj.xs) {  // no dW GEMM: no X'
+    } else if (nr == CJ_ROWS && (cj.H % 8) == 0) {
       for (int64_t h0 = (int64_t)tid * 8; h0 < cj.H; h0 += CJ_THREADS * 8) {
         float v[CJ_ROWS][8];
 #pragma unroll
