@@ -1044,3 +1044,40 @@ np.savez(sys.argv[2], l=l.cpu().numpy(), dX=dX.view(torch.int16).cpu().numpy(), 
         out[mode] = np.load(f)
     for k in ("l", "dX", "dW"):
         assert np.array_equal(out["0"][k], out["1"][k]), k
+
+
+@pytest.mark.parametrize("case", ["multichunk", "fallback", "dx_only", "none"])
+def test_inkernel_combine_bit_identical(slf, tmp_path, case):
+    """The per-row combine run inside the group launch (default) against the separate
+    combine launch (SLF_INKERNEL_COMBINE=0): the same arithmetic in the same order, so loss, dX and dW
+    are the same bits — multi-chunk with extended chunks, rows that need the in-place rescale (the
+    stash flags them and the dX tiles wait for the combine), a dX-only call, reduction 'none'."""
+    import os
+    import subprocess
+    import sys
+    code = r"""
+import sys, numpy as np, torch
+sys.path.insert(0, sys.argv[1]); sys.path.insert(0, sys.argv[1] + '/tests')
+import synth, paper_2603_16428_b200 as slf
+from gpu_util import to_dev
+case = sys.argv[3]
+alpha = 60.0 if case == 'fallback' else 4.0
+N, H, V = (1000, 256, 5000) if case == 'fallback' else (3000, 512, 6000)
+inp = synth.make_inputs(N, H, V, seed=36, alpha=alpha, dist='zipf')
+X, W, t = to_dev(inp, torch)
+l, dX, dW = slf.lce_fwd_bwd(X, W, t, budget_bytes=4 << 20, schedule='S', reduction='none' if case == 'none' else 'mean',
+                            need_dweight=case != 'dx_only')
+torch.cuda.synchronize()
+np.savez(sys.argv[2], l=l.cpu().numpy(), dX=dX.view(torch.int16).cpu().numpy(),
+         dW=(dW.view(torch.int16).cpu().numpy() if dW is not None else np.zeros(1)))
+"""
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    out = {}
+    for mode in ("0", "1"):
+        f = str(tmp_path / f"cj{mode}.npz")
+        env = dict(os.environ, SLF_INKERNEL_COMBINE=mode)
+        subprocess.run([sys.executable, "-c", code, root, f, case], check=True, env=env, timeout=300)
+        out[mode] = np.load(f)
+    for k in ("l", "dX", "dW"):
+        assert np.array_equal(out["0"][k], out["1"][k]), k
+    assert "n_chunks=1 " not in slf.plan_describe(3000, 512, 6000, "S", 4 << 20)
