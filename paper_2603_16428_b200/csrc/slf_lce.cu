@@ -2060,6 +2060,14 @@ slf_status phase_sharded(Ctx& c, const ShardPlan& sp, slf_comm cm, const void* X
       }
     }
   }
+  // World size 1 (no statistics exchange): the combine runs inside the group launch as in the fused
+  // call
+  if (g == 1 && !(getenv("SLF_INKERNEL_COMBINE") && atoi(getenv("SLF_INKERNEL_COMBINE")) == 0) &&
+      (sp.V_l + BN - 1) / BN <= 7000) {
+    c.cj_red = reduction;
+    c.cj_scale = scale;
+    for (auto& k : chunks) k.cj = k.ref && (!dW || k.xt) && k.index < WS_SYNC_SLOTS;
+  }
   if (any_ref) {
     float* mref = reinterpret_cast<float*>(c.ws + p.off_mref);
     {
