@@ -1318,6 +1318,21 @@ float* s_loss_rows(Ctx& c, int reduction, float* loss_out) {
 std::vector<SChunk> s_chunks(const Plan& p, int64_t N, int64_t H, bool extend, uint8_t* dX) {
   static const bool no_ext = getenv("SLF_S_NO_EXT") != nullptr;
   static const int64_t ext_gran = getenv("SLF_S_EXT_GRAN") ? atoi(getenv("SLF_S_EXT_GRAN")) : 256;
+  static const bool no_pref = getenv("SLF_S_REF_EXT") && atoi(getenv("SLF_S_REF_EXT")) == 0;
+  // X'^T [H][rows rounded to 8] fits in dhidden's rows after the chunk and its extended stash: the
+  // chunk can take the per-row stash reference (phase_s) instead of the in-place rescale
+  auto xt_fits = [&](int64_t r0, int64_t rows, int64_t e) {
+    const size_t lo = align_up((size_t)(r0 + rows) * H * 2 + (size_t)e * p.ld_stash * 2, 1024);
+    return lo + (size_t)H * ((rows + 7) / 8 * 8) * 2 <= (size_t)N * H * 2;
+  };
+  // pref: a chunk whose extension would leave no room for X'^T takes the largest extension that
+  // does (its rows move to the chunks after it) — kept when a simple cost model says it is cheaper:
+  // an extra chunk costs its launch tails (~60 us) plus a W read pass and a dW read-modify-write
+  // (8 V H bytes, mostly hidden under the MMAs: counted at 50 TB/s); a chunk on the in-place rescale
+  // costs a fully exposed pass over its stash (4 rows V bytes at 5 TB/s) plus its combine launch.
+  // Llama-8B: 19 chunks either way, 1 instead of 3 rescaled; Llama-70B: 16 instead of 15 chunks,
+  // 2 instead of 13 rescaled.
+  auto build = [&](bool pref) {
   std::vector<SChunk> chunks;
   for (int64_t r0 = 0, ci = 0; r0 < N; ++ci) {
     SChunk k{ci, r0, std::min(p.C, N - r0), 0, nullptr, nullptr, 0};
@@ -1325,6 +1340,8 @@ std::vector<SChunk> s_chunks(const Plan& p, int64_t N, int64_t H, bool extend, u
       const int64_t free_rows = N - r0 - p.C;
       int64_t e = free_rows > 0 ? (free_rows * H) / (p.ld_stash + H) : 0;
       e = std::min<int64_t>(e, p.C) / ext_gran * ext_gran;
+      if (pref && e > 0 && xt_fits(r0, p.C, 0) && !xt_fits(r0, p.C + e, e))
+        while (e > 0 && !xt_fits(r0, p.C + e, e)) e -= ext_gran;
       if (e > 0) {
         k.ext = e;
         k.rows = p.C + e;
@@ -1348,6 +1365,18 @@ std::vector<SChunk> s_chunks(const Plan& p, int64_t N, int64_t H, bool extend, u
     r0 += k.rows;
   }
   return chunks;
+  };
+  std::vector<SChunk> greedy = build(false);
+  if (!extend || no_ext || no_pref) return greedy;
+  std::vector<SChunk> pref = build(true);
+  auto cost = [&](const std::vector<SChunk>& v) {
+    const double Vd = (double)p.ld_stash, Hd = (double)H;
+    double t = (double)v.size() * (60e-6 + 8.0 * Vd * Hd / 50e12);
+    for (const SChunk& k : v)
+      if (!xt_fits(k.r0, k.rows, k.ext)) t += 4.0 * (double)k.rows * Vd / 5e12 + 20e-6;
+    return t;
+  };
+  return cost(pref) < cost(greedy) ? pref : greedy;
 }
 
 // The fused single-GPU call under schedule S (g = 1: a chunk's statistics are its own).  When dX

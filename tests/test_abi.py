@@ -64,7 +64,10 @@ def test_extended_chunk_plan(L):
     """Extended chunks: the fused call with dhidden runs fewer chunks than the plain
     plan, each a multiple of 256 rows, and the extension never outgrows the free dhidden rows."""
     from paper_2603_16428_b200 import lce
-    expect = {(16384, 4096, 128256): (768, 22, 19), (65536, 12288, 32768): (3072, 22, 12)}
+    # Mistral-Large: 13, not the greedy 12 — the last extended chunks give up extension rows so that
+    # X'^T fits (per-row stash reference instead of the in-place rescale), by the planner's cost
+    # model (DESIGN.md §5b; test_ref_preferring_extension below)
+    expect = {(16384, 4096, 128256): (768, 22, 19), (65536, 12288, 32768): (3072, 22, 13)}
     for (N, H, V), (C, n, fused) in expect.items():
         kv = dict(x.split("=") for x in lce.plan_describe(N, H, V, schedule="S").split())
         assert (int(kv["row_chunk"]), int(kv["n_chunks"]), int(kv["fused_chunks_with_dhidden"])) == (C, n, fused)
@@ -287,3 +290,44 @@ def test_sharded_partial_placement_invariants(L, N, H, V, g, budget):
         ld_max = tabs[0][0]["ld"]
         ld_min = -(-(V // g) // 8) * 8
         assert -(-(r_tail * ld_max * 2) // 1024) * 1024 + r_tail * H * 4 <= C * ld_min * 2
+
+
+def test_ref_preferring_extension(L):
+    """The fused call's chunk plan: a chunk whose extended stash would leave no
+    room in dhidden for X'^T gives up extension rows when the planner's cost model prefers it.
+    Restated here (greedy vs preferring build, cost = chunks x (60 us + 8 V H / 50 TB/s) + rescaled
+    chunks x (4 rows V / 5 TB/s + 20 us)) and checked against the library's chunk counts; the
+    preference turns 3 / 4 / 13 / 4 rescaled chunks into 1 / 1 / 2 / 2 at the four heads."""
+    from paper_2603_16428_b200 import lce
+
+    def al(x, a=1024):
+        return (x + a - 1) // a * a
+
+    def build(N, H, ld, C, pref):
+        def fits(r0, rows, e):
+            return al((r0 + rows) * H * 2 + e * ld * 2) + H * ((rows + 7) // 8 * 8) * 2 <= N * H * 2
+        out, r0 = [], 0
+        while r0 < N:
+            rows, e = min(C, N - r0), 0
+            if rows == C:
+                fr = N - r0 - C
+                e = min((fr * H) // (ld + H) if fr > 0 else 0, C) // 256 * 256
+                if pref and e > 0 and fits(r0, C, 0) and not fits(r0, C + e, e):
+                    while e > 0 and not fits(r0, C + e, e):
+                        e -= 256
+            out.append((rows + e, fits(r0, rows + e, e)))
+            r0 += rows + e
+        return out
+
+    def cost(v, V, H):
+        return len(v) * (60e-6 + 8.0 * V * H / 50e12) + sum(4.0 * r * V / 5e12 + 20e-6 for r, ok in v if not ok)
+
+    for (N, H, V), want_classic in {(16384, 4096, 128256): 1, (32768, 3584, 152064): 1,
+                                    (65536, 8192, 128256): 2, (65536, 12288, 32768): 2}.items():
+        kv = dict(x.split("=") for x in lce.plan_describe(N, H, V, schedule="S").split())
+        C, ld = int(kv["row_chunk"]), (V + 7) // 8 * 8
+        g, p = build(N, H, ld, C, False), build(N, H, ld, C, True)
+        chosen = p if cost(p, ld, H) < cost(g, ld, H) else g
+        assert int(kv["fused_chunks_with_dhidden"]) == len(chosen)
+        assert sum(not ok for _, ok in chosen) == want_classic
+        assert sum(not ok for _, ok in g) > want_classic
