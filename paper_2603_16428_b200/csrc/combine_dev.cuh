@@ -61,14 +61,15 @@ __device__ __forceinline__ unsigned ld_relaxed_u32(const unsigned* p) {
 __device__ __forceinline__ void fence_proxy_async_global() {
   asm volatile("fence.proxy.async.global;" ::: "memory");
 }
-// Wait until *p >= target.  Every CTA of the launch is resident (one per SM, persistent) and
-// arrives after a bounded amount of work, so this ends; a trap after ~4 s turns a logic error into
-// a launch failure instead of a hung GPU.
+// Wait until *p >= target.  Every CTA of the launch becomes resident (one per SM, persistent; the
+// kernels before it finish on their own) and arrives after a bounded amount of work, so this ends;
+// a trap after ~30 s (e.g. SMs held that long by other work on the device) turns a stall into a
+// launch failure instead of a hung GPU.
 __device__ __forceinline__ void spin_until_geq(const unsigned* p, unsigned target) {
   unsigned long long n = 0;
   while (ld_acquire_u32(p) < target) {
     __nanosleep(128);
-    if (++n > (1ull << 25)) __trap();
+    if (++n > (1ull << 28)) __trap();
   }
 }
 
