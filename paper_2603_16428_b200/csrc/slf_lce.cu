@@ -1620,28 +1620,39 @@ struct ShardPlan {
   // leave no room there) in the tail of the workspace stash, those chunks being r_tail rows.
   bool ws_part = true;
   int64_t r_tail = 0;
+  bool xt_tail = false;  // tail chunks hold X'^T after their partial (per-row stash reference)
 };
 
 // Stash row pitches of the largest / smallest shard (every rank cuts the same chunks from these).
 int64_t shard_ld_max(int64_t Vg, int g) { return (int64_t)align_up((size_t)((Vg + g - 1) / g), 8); }
 int64_t shard_ld_min(int64_t Vg, int g) { return (int64_t)align_up((size_t)(Vg / g), 8); }
 
-// Rows of a chunk whose stash and fp32 partial share the workspace stash of C rows on EVERY rank:
-// R * ld_max * 2 (rounded to 1 KB) + R * H * 4 <= C * ld_min * 2; a multiple of 8 (X'^T pitch).
-int64_t shard_tail_rows(int64_t C, int64_t H, int64_t ld_max, int64_t ld_min) {
-  const double cap = (double)C * ld_min * 2 - 1024;
-  int64_t R = (int64_t)(cap / ((double)ld_max * 2 + (double)H * 4)) / 8 * 8;
-  while (R > 0 && align_up((size_t)R * ld_max * 2, 1024) + (size_t)R * H * 4 > (size_t)C * ld_min * 2) R -= 8;
+// Rows of a chunk whose stash, fp32 partial and X'^T share the workspace stash of C rows on EVERY
+// rank: R * ld_max * 2 (rounded to 1 KB) + R * H * 4 (rounded) + H * R * 2 <= C * ld_min * 2; a
+// multiple of 8 (X'^T pitch).
+// Also X'^T [H][R] after the partial (the per-row stash reference, for tail chunks).
+size_t shard_tail_bytes(int64_t R, int64_t H, int64_t ld_max, bool xt) {
+  const size_t sp = align_up((size_t)R * ld_max * 2, 1024) + (size_t)R * H * 4;
+  return xt ? align_up(sp, 1024) + (size_t)H * R * 2 : sp;
+}
+int64_t shard_tail_rows(int64_t C, int64_t H, int64_t ld_max, int64_t ld_min, bool xt) {
+  const double cap = (double)C * ld_min * 2 - 2048;
+  int64_t R = (int64_t)(cap / ((double)ld_max * 2 + (double)H * (xt ? 6 : 4))) / 8 * 8;
+  while (R > 0 && shard_tail_bytes(R, H, ld_max, xt) > (size_t)C * ld_min * 2) R -= 8;
   return std::max<int64_t>(R, 0);
 }
 
-bool shard_layout(int64_t N, int64_t H, int64_t V_l, int64_t Vg, int g, bool top, size_t b, ShardPlan* sp) {
+// mode 0: the partial in a workspace region; 1: at dhidden's top (tail chunks: workspace stash
+// tail); 2: as 1, with room for the tail chunks' X'^T too
+bool shard_layout(int64_t N, int64_t H, int64_t V_l, int64_t Vg, int g, int mode, size_t b, ShardPlan* sp) {
+  const bool top = mode != 0;
   if (!plan_s(N, H, V_l, b, &sp->p)) return false;
   const int64_t C2 = 2 * sp->p.C;
   const int64_t ldx = shard_ld_max(Vg, g), ldn = shard_ld_min(Vg, g);
   // top: the partial leaves the workspace (shard_plan picks the layout with fewer chunks)
   sp->ws_part = !top;
-  sp->r_tail = sp->ws_part ? 0 : shard_tail_rows(sp->p.C, H, ldx, ldn);
+  sp->xt_tail = mode == 2;
+  sp->r_tail = sp->ws_part ? 0 : shard_tail_rows(sp->p.C, H, ldx, ldn, sp->xt_tail);
   if (!sp->ws_part && sp->r_tail < 8) return false;
   sp->b = b;
   sp->off_dx = align_up(sp->p.total, 1024);
@@ -1735,14 +1746,14 @@ std::vector<SChunk> shard_chunks(const ShardPlan& sp, int64_t N, int64_t H, int6
 }
 
 // The largest planner budget whose layout fits `total` with a row chunk of at most c_cap (0: any).
-bool shard_fit(int64_t N, int64_t H, int64_t V_l, int64_t Vg, int g, bool top, size_t total, int64_t c_cap,
+bool shard_fit(int64_t N, int64_t H, int64_t V_l, int64_t Vg, int g, int mode, size_t total, int64_t c_cap,
                ShardPlan* sp) {
   auto ok = [&](size_t b) {
-    return shard_layout(N, H, V_l, Vg, g, top, b, sp) && sp->total <= total && (c_cap == 0 || sp->p.C <= c_cap);
+    return shard_layout(N, H, V_l, Vg, g, mode, b, sp) && sp->total <= total && (c_cap == 0 || sp->p.C <= c_cap);
   };
   // bisection (the layout grows with the budget; 0 would mean the default): below the smallest
   // feasible planner budget the predicate counts as "go larger", so it is monotone
-  auto below_or_ok = [&](size_t b) { return !shard_layout(N, H, V_l, Vg, g, top, b, sp) || ok(b); };
+  auto below_or_ok = [&](size_t b) { return !shard_layout(N, H, V_l, Vg, g, mode, b, sp) || ok(b); };
   size_t lo = 1, hi = total;
   while (lo < hi) {
     const size_t mid = lo + (hi - lo + 1) / 2;
@@ -1762,24 +1773,34 @@ bool shard_plan(int64_t N, int64_t H, int64_t Vg, int g, int k, size_t budget, S
   int64_t v0, vl;
   shard_bounds(Vg, g, k, &v0, &vl);
   const size_t total = budget ? budget : default_budget(N, Vg);
-  // Both placements of the fp32 dX partial (shard_layout); the one cutting fewer row chunks wins
-  // (ties: dhidden's top rows, the smaller workspace).  Everything here is the same on every rank.
+  // The placements of the fp32 dX partial (shard_layout modes 2, 1, 0); the one cutting fewer row
+  // chunks wins, then the one leaving fewer chunks on the in-place rescale (ties: the earlier mode).
+  // Everything here is the same on every rank.
   ShardPlan best;
   size_t best_n = 0;
+  int best_cl = 0;
   static const char* force = getenv("SLF_SHARD_PART");  // "top" / "region": one placement only (tests)
-  for (const bool top : {true, false}) {
-    if (force && strcmp(force, top ? "region" : "top") == 0) continue;
+  const int64_t ldx = shard_ld_max(Vg, g);
+  for (const int mode : {2, 1, 0}) {
+    if (force && strcmp(force, mode ? "region" : "top") == 0) continue;
     ShardPlan big, sp;
-    if (!shard_fit(N, H, (Vg + g - 1) / g, Vg, g, top, total, 0, &big)) continue;
-    if (!shard_fit(N, H, vl, Vg, g, top, total, big.p.C, &sp) || sp.p.C != big.p.C) continue;
+    if (!shard_fit(N, H, (Vg + g - 1) / g, Vg, g, mode, total, 0, &big)) continue;
+    if (!shard_fit(N, H, vl, Vg, g, mode, total, big.p.C, &sp) || sp.p.C != big.p.C) continue;
     ShardPlan small;  // the same decision on every rank: the smallest shard must fit this C too
-    if (!shard_fit(N, H, Vg / g, Vg, g, top, total, big.p.C, &small) || small.p.C != big.p.C) continue;
+    if (!shard_fit(N, H, Vg / g, Vg, g, mode, total, big.p.C, &small) || small.p.C != big.p.C) continue;
     sp.v0 = v0;
     sp.V_l = vl;
-    const size_t n = shard_chunks(sp, N, H, Vg, g, true, nullptr).size();
-    if (best_n == 0 || n < best_n) {
+    const std::vector<SChunk> ch = shard_chunks(sp, N, H, Vg, g, true, nullptr);
+    int cl = 0;  // chunks without room for X'^T (phase_sharded's rule)
+    for (const SChunk& k : ch) {
+      if (k.part_off == PART_WS_TAIL && sp.xt_tail) continue;
+      const size_t lo = align_up((size_t)(k.r0 + k.rows) * H * 2 + (size_t)k.ext * ldx * 2, 1024);
+      cl += lo + (size_t)H * ((k.rows + 7) / 8 * 8) * 2 > k.xt_lim;
+    }
+    if (best_n == 0 || ch.size() < best_n || (ch.size() == best_n && cl < best_cl)) {
       best = sp;
-      best_n = n;
+      best_n = ch.size();
+      best_cl = cl;
     }
   }
   if (best_n == 0) return false;
@@ -2077,9 +2098,19 @@ slf_status phase_sharded(Ctx& c, const ShardPlan& sp, slf_comm cm, const void* X
   static const bool classic = getenv("SLF_S_CLASSIC") != nullptr;
   bool any_ref = false;
   if (!classic && dX) {
+    // tail chunks: X'^T in the workspace stash's tail, after the partial (shard_tail_bytes)
+    const size_t xt_tail = align_up(tail_off + (size_t)sp.r_tail * H * 4, 1024);
     for (auto& k : chunks) {
-      const size_t lo = align_up((size_t)(k.r0 + k.rows) * H * 2 + (size_t)k.ext * ld_max * 2, 1024);
       const int64_t ld = (k.rows + 7) / 8 * 8;
+      if (k.part_off == PART_WS_TAIL && sp.xt_tail) {
+        k.ref = any_ref = true;
+        if (dW) {
+          k.xt = c.ws + xt_tail;
+          k.ld_xt = ld;
+        }
+        continue;
+      }
+      const size_t lo = align_up((size_t)(k.r0 + k.rows) * H * 2 + (size_t)k.ext * ld_max * 2, 1024);
       if (lo + (size_t)H * ld * 2 <= k.xt_lim) {
         k.ref = any_ref = true;
         if (dW) {
@@ -2705,9 +2736,10 @@ slf_status slf_lce_sharded_plan_describe(int64_t N, int64_t H, int64_t V_global,
   }
   snprintf(out, cap,
            "schedule=S sharded world=%d rank=%d vocab_start=%lld V_local=%lld row_chunk=%lld n_chunks=%lld "
-           "chunks_with_dhidden=%zu dx_partial=%s tail_rows=%lld top_chunks=%zu tail_chunks=%zu planner_budget=%zu stash_bytes=%zu workspace=%zu",
+           "chunks_with_dhidden=%zu dx_partial=%s tail_rows=%lld xt_tail=%d top_chunks=%zu tail_chunks=%zu planner_budget=%zu "
+           "stash_bytes=%zu workspace=%zu",
            world, rank, (long long)sp.v0, (long long)sp.V_l, (long long)sp.p.C, (long long)sp.p.nCh, ext_chunks,
-           sp.ws_part ? "workspace" : "dhidden_top", (long long)sp.r_tail, n_top, n_tail, sp.b, (size_t)sp.p.C * sp.p.ld_stash * 2,
+           sp.ws_part ? "workspace" : "dhidden_top", (long long)sp.r_tail, sp.xt_tail ? 1 : 0, n_top, n_tail, sp.b, (size_t)sp.p.C * sp.p.ld_stash * 2,
            sp.total);
   return SLF_OK;
 }

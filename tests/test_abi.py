@@ -289,7 +289,11 @@ def test_sharded_partial_placement_invariants(L, N, H, V, g, budget):
     if "dx_partial=dhidden_top" in desc:
         ld_max = tabs[0][0]["ld"]
         ld_min = -(-(V // g) // 8) * 8
-        assert -(-(r_tail * ld_max * 2) // 1024) * 1024 + r_tail * H * 4 <= C * ld_min * 2
+        al = lambda x: -(-x // 1024) * 1024  # noqa: E731
+        # stash rows and fp32 partial (+ X'^T when the plan reserves it) of a tail chunk in the
+        # smallest shard's workspace stash
+        xt = H * r_tail * 2 if "xt_tail=1" in desc else 0
+        assert al(al(r_tail * ld_max * 2) + r_tail * H * 4) + xt <= C * ld_min * 2
 
 
 def test_ref_preferring_extension(L):

@@ -1,0 +1,13 @@
+mkdir -p gpurun_out/r2aq
+export PYTHONUNBUFFERED=1
+O=gpurun_out/r2aq
+timeout 1800 python -m pytest tests/test_gpu_parity.py -m gpu -q -k "sharded or shard or dp_" > $O/tests.log 2>&1; echo tests $?; tail -3 $O/tests.log
+for i in 1 2; do
+timeout 600 python bench.py --module --steps 20 --warmup 5 --no-cpu-baseline --no-e2e > $O/module_$i.json 2>/dev/null; echo module $?
+timeout 600 python bench.py --steps 20 --warmup 5 --no-cpu-baseline --no-e2e > $O/fused_$i.json 2>/dev/null; echo fused $?
+done
+python - <<'PY'
+import json,glob
+for f in sorted(glob.glob('gpurun_out/r2aq/*.json')):
+    d=json.load(open(f)); print(f, round(d['ms_per_step'],3), round(d['step_ms']['median'],3), d['clocks']['sm_mhz'])
+PY
