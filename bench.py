@@ -601,7 +601,7 @@ def main():
                      # clock64 / globaltimer counters instead)
                      **({"clock_mhz_peak_run": peaks["sustained_mhz"], "clock_mhz_this_run": ck["sm_mhz"]}
                         if peaks.get("sustained_mhz") and ck.get("sm_mhz") else {}),
-                     "ncu": "profiles/ncu_r02g.md (tensor pipe active % per kernel, DRAM bytes)"},
+                     "ncu": "profiles/ncu_r02h.md (tensor pipe active % per kernel, DRAM bytes)"},
         "kernels": kernels,
         "comm": ({"allgather_ms_per_step": kinds.get("comm_allgather", {}).get("ms", 0.0) / args.steps,
                   "allreduce_ms_per_step": kinds.get("comm_allreduce", {}).get("ms", 0.0) / args.steps,
