@@ -1730,8 +1730,15 @@ std::vector<SChunk> shard_chunks(const ShardPlan& sp, int64_t N, int64_t H, int6
         prev_q = (size_t)k.rows * H * 4;
       } else {
         tail = true;
-        const int64_t M = N - r0, n = (M + sp.r_tail - 1) / sp.r_tail;
-        tail_rows = std::min<int64_t>(sp.r_tail, ((M + n - 1) / n + 7) / 8 * 8);  // even split
+        // whole 256-row tiles where the tail allows them (a 696-row chunk computes 768 rows'
+        // worth of stash and dX tiles), else an even split
+        const int64_t M = N - r0, R256 = sp.r_tail / 256 * 256;
+        if (R256 >= 256) {
+          tail_rows = R256;
+        } else {
+          const int64_t n = (M + sp.r_tail - 1) / sp.r_tail;
+          tail_rows = std::min<int64_t>(sp.r_tail, ((M + n - 1) / n + 7) / 8 * 8);
+        }
       }
     }
     if (tail) {
