@@ -891,9 +891,9 @@ def test_native_sharded_all_chunk_kinds_world1(slf, N, H, V, budget, red, mode):
     assert np.all(dX.view(torch.int16).cpu().numpy()[inp.t == -100] == 0)
 
 
-@pytest.mark.parametrize("g,N,H,V,budget", [(2, 6000, 256, 1000, 2 << 20), (4, 6000, 512, 4001, 4 << 20)])
+@pytest.mark.parametrize("g,N,H,V,budget", [(2, 3000, 512, 4001, 2 << 20), (4, 3000, 512, 4001, 1 << 20)])
 def test_native_sharded_all_chunk_kinds_multirank(slf, tmp_path, g, N, H, V, budget):
-    """g = 2 / 4 ranks (processes on one GPU; V = 4001 at g = 4: uneven shards) at shapes whose
+    """g = 2 / 4 ranks (processes on one GPU; V = 4001: uneven shards) at shapes whose
     chunk table mixes extended top, plain or shortened top, and workspace-tail chunks: gloo transport and P2P
     exchanges, every rank identical, against the oracle."""
     kinds = _chunk_kinds(slf, N, H, V, g, budget)
