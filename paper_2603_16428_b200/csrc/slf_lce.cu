@@ -1687,8 +1687,19 @@ std::vector<SChunk> shard_chunks(const ShardPlan& sp, int64_t N, int64_t H, int6
   }
   static const bool no_ext = getenv("SLF_S_NO_EXT") != nullptr;
   static const int64_t ext_gran = getenv("SLF_S_EXT_GRAN") ? atoi(getenv("SLF_S_EXT_GRAN")) : 256;
+  static const bool no_pref = getenv("SLF_S_REF_EXT") && atoi(getenv("SLF_S_REF_EXT")) == 0;
   const int64_t C = pe.C, ld = pe.ld_stash;
   const size_t D = (size_t)N * H * 2;
+  // X'^T [H][rows rounded to 8] fits between the chunk's extended stash and its partial
+  // (phase_sharded's per-row-reference rule for a top chunk)
+  auto xt_ok = [&](int64_t r0, int64_t rows, int64_t e) {
+    const size_t lo = align_up((size_t)(r0 + rows) * H * 2 + (size_t)e * ld * 2, 1024);
+    return lo + (size_t)H * ((rows + 7) / 8 * 8) * 2 <= D - (size_t)rows * H * 4;
+  };
+  // pref: as s_chunks — a top chunk takes the largest extension (or, without one, the longest
+  // shorter length) that leaves room for X'^T when one does; the plan is kept if the cost model
+  // prefers it
+  auto build = [&](bool pref) {
   std::vector<SChunk> chunks;
   size_t prev_q = 0;  // bytes at dhidden's top held by the previous chunk's partial
   bool tail = false;
@@ -1697,23 +1708,30 @@ std::vector<SChunk> shard_chunks(const ShardPlan& sp, int64_t N, int64_t H, int6
     SChunk k{ci, r0, 0, 0, nullptr, nullptr, 0};
     const int64_t base = std::min(C, N - r0);
     if (!tail) {
-      int64_t e = 0;
+      int64_t e0 = 0;
       if (!no_ext && base == C) {
         const int64_t free_rows = N - r0 - C;
-        e = free_rows > 0 ? std::min<int64_t>((free_rows * H) / (ld + H), C) / ext_gran * ext_gran : 0;
+        e0 = free_rows > 0 ? std::min<int64_t>((free_rows * H) / (ld + H), C) / ext_gran * ext_gran : 0;
       }
       bool ok = false;
-      for (; e >= 0; e -= ext_gran) {
-        const int64_t rows = base + e;
-        const size_t end = (size_t)(r0 + rows) * H * 2;  // the chunk's own rows end here
-        if (end + (size_t)rows * H * 4 > D) continue;
-        // the extended stash is written while the previous partial is in flight and read while
-        // this chunk's partial is written
-        if (e > 0 && end + (size_t)e * ld * 2 > D - std::max(prev_q, (size_t)rows * H * 4)) continue;
-        ok = true;
-        k.rows = rows;
-        k.ext = e;
-        break;
+      for (int pass = pref ? 0 : 1; pass < 2 && !ok; ++pass) {  // pass 0: only extensions with room for X'^T
+        for (int64_t e = e0; e >= 0; e -= ext_gran) {
+          const int64_t rows = base + e;
+          const size_t end = (size_t)(r0 + rows) * H * 2;  // the chunk's own rows end here
+          if (end + (size_t)rows * H * 4 > D) continue;
+          // the extended stash is written while the previous partial is in flight and read while
+          // this chunk's partial is written
+          if (e > 0 && end + (size_t)e * ld * 2 > D - std::max(prev_q, (size_t)rows * H * 4)) continue;
+          if (pass == 0 && !xt_ok(r0, rows, e)) continue;
+          ok = true;
+          k.rows = rows;
+          k.ext = e;
+          break;
+        }
+      }
+      if (pref && ok && k.ext == 0 && !xt_ok(r0, k.rows, 0)) {  // a shorter chunk with room for X'^T
+        const int64_t r = (N - r0) / 4 / 256 * 256;
+        if (r >= 256 && r > sp.r_tail && xt_ok(r0, r, 0)) k.rows = r;
       }
       if (!ok) {  // a shorter chunk (no extension) whose partial still fits above its rows
         const int64_t r = (N - r0) / 3 / 256 * 256;
@@ -1750,6 +1768,19 @@ std::vector<SChunk> shard_chunks(const ShardPlan& sp, int64_t N, int64_t H, int6
     r0 += k.rows;
   }
   return chunks;
+  };
+  std::vector<SChunk> greedy = build(false);
+  if (no_pref) return greedy;
+  std::vector<SChunk> pref = build(true);
+  auto cost = [&](const std::vector<SChunk>& v) {  // the model of s_chunks
+    double t = (double)v.size() * (60e-6 + 8.0 * (double)ld * (double)H / 50e12);
+    for (const SChunk& k : v) {
+      const bool ref = k.part_off == PART_WS_TAIL ? sp.xt_tail : xt_ok(k.r0, k.rows, k.ext);
+      if (!ref) t += 4.0 * (double)k.rows * (double)ld / 5e12 + 20e-6;
+    }
+    return t;
+  };
+  return cost(pref) < cost(greedy) ? pref : greedy;
 }
 
 // The largest planner budget whose layout fits `total` with a row chunk of at most c_cap (0: any).
