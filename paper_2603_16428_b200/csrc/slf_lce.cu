@@ -2356,12 +2356,18 @@ slf_status slf_lce_plan_describe(int64_t N, int64_t H, int64_t V_local, int sche
   Plan p;
   if (!plan_any(N, H, V_local, schedule, budget_bytes, true, &p)) return fail(SLF_ERR_WORKSPACE, "no plan fits");
   if (p.sched == SLF_SCHED_S) {
-    const int64_t fused = (int64_t)s_chunks(p, N, H, true, nullptr).size();
+    const std::vector<SChunk> ch = s_chunks(p, N, H, true, nullptr);
+    const int64_t fused = (int64_t)ch.size();
+    int64_t rescaled = 0;  // chunks without room for X'^T: the in-place rescale, a combine launch of their own
+    for (const SChunk& k : ch) {
+      const size_t lo = align_up((size_t)(k.r0 + k.rows) * H * 2 + (size_t)k.ext * p.ld_stash * 2, 1024);
+      rescaled += lo + (size_t)H * ((k.rows + 7) / 8 * 8) * 2 > (size_t)N * H * 2;
+    }
     snprintf(out, cap,
-             "schedule=S row_chunk=%lld n_chunks=%lld fused_chunks_with_dhidden=%lld stash_bytes=%zu workspace=%zu "
-             "launches=%lld",
-             (long long)p.C, (long long)p.nCh, (long long)fused, (size_t)p.C * p.ld_stash * 2, p.total,
-             (long long)(8 + fused * 3));
+             "schedule=S row_chunk=%lld n_chunks=%lld fused_chunks_with_dhidden=%lld rescaled_chunks=%lld "
+             "stash_bytes=%zu workspace=%zu launches=%lld",
+             (long long)p.C, (long long)p.nCh, (long long)fused, (long long)rescaled, (size_t)p.C * p.ld_stash * 2,
+             p.total, (long long)(8 + fused * 2 + rescaled));
   } else {
     snprintf(out, cap,
              "schedule=R row_block=%lld n_row_blocks=%lld vocab_chunk=%lld n_vocab_chunks=%lld workspace=%zu "

@@ -333,5 +333,5 @@ def test_ref_preferring_extension(L):
         g, p = build(N, H, ld, C, False), build(N, H, ld, C, True)
         chosen = p if cost(p, ld, H) < cost(g, ld, H) else g
         assert int(kv["fused_chunks_with_dhidden"]) == len(chosen)
-        assert sum(not ok for _, ok in chosen) == want_classic
+        assert sum(not ok for _, ok in chosen) == want_classic == int(kv["rescaled_chunks"])
         assert sum(not ok for _, ok in g) > want_classic
